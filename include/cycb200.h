@@ -1,0 +1,198 @@
+/*
+ * cycb200.h -- C-ABI of the B200-native cyclic-ACF estimator (libcycb200.so).
+ *
+ * Drop-in boundary for the reference estimator `cycstat::CyclicCorrelator`
+ * (/root/reference/proj/include/cycstat/estimator.hpp:77-148).  Plain pointers
+ * and sizes only; no CUDA or torch types cross this boundary.  The C++
+ * wrapper include/cycstat_b200.hpp restores the reference's class names,
+ * exceptions and std::vector signatures on top of it.
+ *
+ * Every entry point replaces one reference interface (file:line cited) and
+ * keeps its argument meaning and error behaviour:
+ *   - configuration errors collect EVERY violation   (proj/src/types.cpp:30-63)
+ *   - a chunk with a non-finite sample is rejected whole, state unchanged,
+ *     and the message names the absolute index      (proj/src/estimator.cpp:41-52)
+ *   - frames are emitted per win_len consumed samples once buffer_need are
+ *     pending; the tail is never flushed             (proj/src/estimator.cpp:59-82)
+ *
+ * Values are the reference's quantity
+ *   R(a, m) = (1/N) sum_{n<N} x[k0+n+m] y^(*)[k0+n] e^{-j2pi a (k0+n)}
+ * computed on the GPU from complex64 samples (float32 arithmetic with fp64
+ * reductions; parity tolerance: relative L2 <= 1e-4 per table and per-value
+ * |dR| <= 1e-5 * mean power, BASELINE.json north_star).
+ *
+ * Thread safety: a handle is single-owner (estimator.hpp:95-96); distinct
+ * handles are independent.
+ */
+#ifndef CYCB200_H
+#define CYCB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CYC_ABI_VERSION 1
+
+/* Status codes.  Map 1:1 onto the reference exception types
+ * (proj/include/cycstat/errors.hpp:10-49). */
+typedef enum {
+    CYC_OK = 0,
+    CYC_ERR_CONFIG = 1,   /* ConfigError  (violation list in the message)      */
+    CYC_ERR_USAGE = 2,    /* UsageError   (mismatched chunks, bad arguments)   */
+    CYC_ERR_DATA = 3,     /* DataError    (non-finite sample; absolute index)  */
+    CYC_ERR_CUDA = 4,     /* device / driver failure (no CPU fallback exists)  */
+    CYC_ERR_INTERNAL = 5  /* std::logic_error equivalent                       */
+} cyc_status;
+
+/* Estimator mode (proj/include/cycstat/types.hpp:22-25) plus the
+ * exponential-forgetting estimator the reference lacks. */
+typedef enum {
+    CYC_MODE_SET = 0,       /* alpha list x lags; alpha-major, lags ascending    */
+    CYC_MODE_FULL = 1,      /* lag list x all N DFT bins; lag-major, natural bins */
+    CYC_MODE_RECURSIVE = 2  /* R_n = lam R_{n-1} + (1-lam) q_n e^{-j2pi a n}      */
+} cyc_mode;
+
+/* Which cyclic functions to compute.  The reference computes one per
+ * estimator (EstimatorConfig::conj, types.hpp:57-59); one pass here can
+ * produce both from the same four real correlations. */
+typedef enum {
+    CYC_FLAG_CONV = 1, /* conj == false: x * conj(y) (cyclic ACF)               */
+    CYC_FLAG_CONJ = 2, /* conj == true : x * y       (conjugate cyclic ACF)     */
+    CYC_FLAG_BOTH = 3
+} cyc_flags;
+
+typedef enum { CYC_AVG_COHERENT = 0, CYC_AVG_MAGNITUDE = 1 } cyc_avg_mode;
+
+typedef struct { float re, im; } cyc_cf32;
+typedef struct { double re, im; } cyc_cf64;
+
+/* EstimatorConfig (types.hpp:55-63) + extensions.  Initialise with
+ * cyc_config_init() and override fields. */
+typedef struct cyc_config {
+    int mode;              /* cyc_mode                                                */
+    int conj;              /* reference conj flag; used when flags == 0               */
+    int flags;             /* 0 => (conj ? CONJ : CONV); else cyc_flags bitmask       */
+    int win_len;           /* N; RECURSIVE: emission interval (samples)               */
+    const double* alphas;  /* SET / RECURSIVE: cycle frequencies, cycles/sample       */
+    size_t num_alphas;
+    int lag_symmetric;     /* 1: LagSpec::Symmetric(max_lag); 0: explicit list        */
+    int max_lag;
+    const int* lags;       /* explicit, strictly increasing                           */
+    size_t num_lags;
+    double lambda;         /* RECURSIVE forgetting factor, 0 < lambda < 1             */
+    int emit_frames;       /* 1: per-frame values go to the sink (reference push());  */
+                           /* 0: frames are only counted and folded into the running */
+                           /*    coherent average (cyc_average) -- the block mode     */
+    int channels;          /* >= 1 independent synchronized streams per handle        */
+    int device;            /* CUDA device ordinal                                     */
+} cyc_config;
+
+typedef struct cyc_est cyc_est;
+
+/* One emitted frame (CyclicFrame, types.hpp:97-104).  `values` is valid only
+ * during the sink call; layout as cyc_layout(). */
+typedef struct {
+    uint64_t frame_index;
+    uint64_t start_abs;     /* m_minus + frame_index * win_len                    */
+    int flag;               /* CYC_FLAG_CONV or CYC_FLAG_CONJ                     */
+    int channel;
+    size_t len;             /* layout_len                                         */
+    const cyc_cf64* values;
+} cyc_frame_view;
+
+/* Return 0 to continue; nonzero stops delivery (the push still commits). */
+typedef int (*cyc_frame_sink)(void* user, const cyc_frame_view* frame);
+
+/* Layout description (types.hpp:68-94). */
+typedef struct {
+    int kind;        /* 0 = SetLayout (alpha-major, lags ascending), 1 = FullLayout (lag-major) */
+    int num_alphas;  /* Set / Recursive                                           */
+    int max_lag;     /* Set: symmetric M (rows hold 2M+1 lags)                    */
+    int num_lags;    /* lags per alpha row (Set/Recursive) or lag rows (Full)     */
+    int win_len;     /* Full: bins per lag row                                    */
+    size_t len;      /* layout_len                                                */
+} cyc_layout_info;
+
+void cyc_config_init(cyc_config* cfg);
+
+/* validate_config (proj/src/types.cpp:30-63): returns the number of
+ * violations and writes them, '\n'-separated, into buf. */
+int cyc_validate(const cyc_config* cfg, char* buf, size_t buflen);
+
+/* CyclicCorrelator(const EstimatorConfig&) (proj/src/estimator.cpp:15-37).
+ * On CYC_ERR_CONFIG the message is "invalid config: [v1] [v2] ..."
+ * (errors.hpp:17-30). */
+int cyc_create(const cyc_config* cfg, cyc_est** out, char* err, size_t errlen);
+void cyc_destroy(cyc_est* est);
+
+/* CyclicCorrelator::push (proj/src/estimator.cpp:39-84).
+ * x, y: channels * n samples, channel-major.  y == NULL means y = x (the
+ * auto-correlation every BASELINE config uses; one stream is read).
+ * Caller memory is not retained after return.  Pinned (page-locked) host
+ * memory is DMA'd directly; pageable memory is staged. */
+int cyc_push(cyc_est* est, const cyc_cf32* x, const cyc_cf32* y, size_t n,
+             cyc_frame_sink sink, void* user);
+/* Same, from the reference's complex<double> samples (converted to float32;
+ * exact for data that came from cf32, proj/src/io.cpp:90-103). */
+int cyc_push_f64(cyc_est* est, const cyc_cf64* x, const cyc_cf64* y, size_t n,
+                 cyc_frame_sink sink, void* user);
+/* Same, from samples already resident in device memory (GPU pipelines). */
+int cyc_push_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size_t n,
+                    cyc_frame_sink sink, void* user);
+
+/* average_frames(frames emitted so far, mode) (proj/src/estimator.cpp:86-105)
+ * for one (flag, channel), without materialising the frames: the coherent
+ * mean equals one block sum over [m_minus, m_minus + F*N) / (F*N).
+ * MAGNITUDE needs emit_frames == 1.  out: layout_len values.
+ * CYC_ERR_USAGE when no frame was emitted yet. */
+int cyc_average(cyc_est* est, int avg_mode, int flag, int channel, cyc_cf64* out);
+
+/* Accessors (estimator.hpp:109-115). */
+size_t cyc_buffer_need(const cyc_est* est);
+uint64_t cyc_consumed(const cyc_est* est);
+uint64_t cyc_frames_emitted(const cyc_est* est);
+int cyc_layout(const cyc_est* est, cyc_layout_info* out);
+int cyc_num_flags(const cyc_est* est);
+/* Message of the last failed call on this handle ("" if none). */
+const char* cyc_last_error(const cyc_est* est);
+/* For CYC_ERR_DATA: absolute index of the offending sample, else -1. */
+int64_t cyc_data_error_index(const cyc_est* est);
+
+/* Block until all device work of this handle is complete. */
+int cyc_synchronize(cyc_est* est);
+/* The handle's compute stream (cudaStream_t as void*), for event timing. */
+void* cyc_stream(cyc_est* est);
+/* Kernel launches issued by this handle so far (instrumentation). */
+uint64_t cyc_kernel_launches(const cyc_est* est);
+/* Internal algorithm chosen for this handle: "fold-dft", "fold-fft",
+ * "direct", written into buf. */
+int cyc_algorithm(const cyc_est* est, char* buf, size_t buflen);
+
+/* Page-locked host buffers for zero-copy-staging pushes. */
+void* cyc_host_alloc(size_t bytes);
+void cyc_host_free(void* p);
+
+/* Library version / build info. */
+int cyc_abi_version(void);
+const char* cyc_build_info(void);
+
+/* Kernel-level API (estimator.hpp:20-75), used by tests and the bench:
+ * one-shot windows anchored at absolute index k0, computed on the device.
+ * compute_set_window (kernels.cpp:116-123): xw has |yw| + 2*max_lag samples,
+ * out: num_alphas * (2*max_lag+1).  compute_full_window (kernels.cpp:125-135):
+ * xw has |yw| + m_plus + m_minus samples, out: num_lags * |yw|. */
+int cyc_compute_set_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw,
+                           size_t yw_len, const double* alphas, size_t num_alphas,
+                           int max_lag, int conj, uint64_t k0, cyc_cf64* out,
+                           char* err, size_t errlen);
+int cyc_compute_full_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw,
+                            size_t yw_len, const int* lags, size_t num_lags, int conj,
+                            uint64_t k0, cyc_cf64* out, char* err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CYCB200_H */

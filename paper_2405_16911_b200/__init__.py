@@ -1,0 +1,517 @@
+"""B200-native cyclic-ACF estimator -- Python mirror of the reference interface.
+
+The product is ``libcycb200.so`` (CUDA kernels for sm_100a behind the C-ABI in
+``include/cycb200.h``).  This module binds it with ctypes and restates the
+reference's public names so callers and parity tests read like the
+reference's own (``/root/reference/proj/include/cycstat``):
+
+    Mode, LagSpec, EstimatorConfig, validate_config      types.hpp:22-66
+    SetLayout, FullLayout, layout_len, flat_index,
+    full_bin_to_alpha                                     types.hpp:68-94
+    CyclicFrame                                           types.hpp:97-104
+    CyclicCorrelator(cfg).push(x, y) -> [CyclicFrame]     estimator.hpp:97-137
+    AverageMode, average_frames                           estimator.hpp:143-148
+    compute_set_window, compute_full_window               estimator.hpp:59-68
+    UsageError, ConfigError, DataError                    errors.hpp:13-42
+
+There is no CPU fallback: importing works without a GPU, but every compute
+call goes through the CUDA library and fails loudly if it is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcycb200.so")
+
+__all__ = [
+    "Mode", "Flags", "AverageMode", "LagSpec", "EstimatorConfig", "SetLayout", "FullLayout",
+    "CyclicFrame", "CyclicCorrelator", "validate_config", "layout_len", "flat_index",
+    "full_bin_to_alpha", "average_frames", "compute_set_window", "compute_full_window",
+    "UsageError", "ConfigError", "DataError", "CudaError", "LogicError", "lib", "host_alloc",
+]
+
+
+# ---------------------------------------------------------------------------
+# errors (proj/include/cycstat/errors.hpp)
+# ---------------------------------------------------------------------------
+class UsageError(RuntimeError):
+    """errors.hpp:13-15"""
+
+
+class ConfigError(UsageError):
+    """errors.hpp:17-30: carries every violation."""
+
+    def __init__(self, violations: Sequence[str], message: Optional[str] = None):
+        self.violations = list(violations)
+        super().__init__(message or ("invalid config:" + "".join(f" [{v}]" for v in self.violations)))
+
+
+class DataError(RuntimeError):
+    """errors.hpp:40-42: non-finite input; `index` is the absolute sample index."""
+
+    def __init__(self, message: str, index: int = -1):
+        super().__init__(message)
+        self.index = index
+
+
+class CudaError(RuntimeError):
+    """Device failure -- there is no CPU fallback."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error: kernel contract violations (kernels.cpp:16-17, 29-30, 119-120)."""
+
+
+# ---------------------------------------------------------------------------
+# C-ABI binding
+# ---------------------------------------------------------------------------
+class _Config(C.Structure):
+    _fields_ = [
+        ("mode", C.c_int), ("conj", C.c_int), ("flags", C.c_int), ("win_len", C.c_int),
+        ("alphas", C.POINTER(C.c_double)), ("num_alphas", C.c_size_t),
+        ("lag_symmetric", C.c_int), ("max_lag", C.c_int),
+        ("lags", C.POINTER(C.c_int)), ("num_lags", C.c_size_t),
+        ("lam", C.c_double), ("emit_frames", C.c_int), ("channels", C.c_int), ("device", C.c_int),
+    ]
+
+
+class _FrameView(C.Structure):
+    _fields_ = [
+        ("frame_index", C.c_uint64), ("start_abs", C.c_uint64), ("flag", C.c_int),
+        ("channel", C.c_int), ("len", C.c_size_t), ("values", C.POINTER(C.c_double)),
+    ]
+
+
+class _LayoutInfo(C.Structure):
+    _fields_ = [("kind", C.c_int), ("num_alphas", C.c_int), ("max_lag", C.c_int),
+                ("num_lags", C.c_int), ("win_len", C.c_int), ("len", C.c_size_t)]
+
+
+_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(_FrameView))
+_lib: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    """Load libcycb200.so (built in-tree by paper_2405_16911_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2405_16911_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, sz = C.c_void_p, C.c_size_t
+    L.cyc_config_init.argtypes = [C.POINTER(_Config)]
+    L.cyc_validate.argtypes = [C.POINTER(_Config), C.c_char_p, sz]
+    L.cyc_create.argtypes = [C.POINTER(_Config), C.POINTER(vp), C.c_char_p, sz]
+    L.cyc_destroy.argtypes = [vp]
+    for f in ("cyc_push", "cyc_push_f64", "cyc_push_device"):
+        getattr(L, f).argtypes = [vp, vp, vp, sz, _SINK, vp]
+    L.cyc_average.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
+    L.cyc_buffer_need.argtypes = [vp]
+    L.cyc_buffer_need.restype = sz
+    L.cyc_consumed.argtypes = [vp]
+    L.cyc_consumed.restype = C.c_uint64
+    L.cyc_frames_emitted.argtypes = [vp]
+    L.cyc_frames_emitted.restype = C.c_uint64
+    L.cyc_layout.argtypes = [vp, C.POINTER(_LayoutInfo)]
+    L.cyc_num_flags.argtypes = [vp]
+    L.cyc_last_error.argtypes = [vp]
+    L.cyc_last_error.restype = C.c_char_p
+    L.cyc_data_error_index.argtypes = [vp]
+    L.cyc_data_error_index.restype = C.c_int64
+    L.cyc_synchronize.argtypes = [vp]
+    L.cyc_stream.argtypes = [vp]
+    L.cyc_stream.restype = vp
+    L.cyc_kernel_launches.argtypes = [vp]
+    L.cyc_kernel_launches.restype = C.c_uint64
+    L.cyc_algorithm.argtypes = [vp, C.c_char_p, sz]
+    L.cyc_host_alloc.argtypes = [sz]
+    L.cyc_host_alloc.restype = vp
+    L.cyc_host_free.argtypes = [vp]
+    L.cyc_build_info.restype = C.c_char_p
+    L.cyc_compute_set_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_int, C.c_uint64, vp,
+                                         C.c_char_p, sz]
+    L.cyc_compute_full_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_uint64, vp, C.c_char_p, sz]
+    _lib = L
+    return L
+
+
+def host_alloc(shape, dtype=np.complex64) -> np.ndarray:
+    """Page-locked numpy array (freed with the array) for zero-staging pushes."""
+    L = lib()
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    ptr = L.cyc_host_alloc(max(nbytes, 1))
+    if not ptr:
+        raise CudaError("cudaMallocHost failed")
+    buf = (C.c_char * max(nbytes, 1)).from_address(ptr)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+    class _Owner:
+        def __del__(self_inner):
+            try:
+                L.cyc_host_free(ptr)
+            except Exception:
+                pass
+
+    arr_owner = _Owner()
+    arr = arr.view(_Pinned)
+    arr._owner = arr_owner
+    return arr
+
+
+class _Pinned(np.ndarray):
+    _owner = None
+
+    def __array_finalize__(self, obj):
+        if obj is not None:
+            self._owner = getattr(obj, "_owner", None)
+
+
+# ---------------------------------------------------------------------------
+# types (proj/include/cycstat/types.hpp)
+# ---------------------------------------------------------------------------
+class Mode(enum.IntEnum):
+    Set = 0
+    Full = 1
+    Recursive = 2  # extension: exponential forgetting
+
+
+class Flags(enum.IntFlag):
+    CONV = 1
+    CONJ = 2
+    BOTH = 3
+
+
+class AverageMode(enum.IntEnum):
+    Coherent = 0
+    Magnitude = 1
+
+
+@dataclass
+class LagSpec:
+    """types.hpp:29-53"""
+    symmetric: bool = True
+    max_lag: int = 0
+    lags: list = field(default_factory=list)
+
+    @staticmethod
+    def Symmetric(m: int) -> "LagSpec":
+        return LagSpec(True, int(m), [])
+
+    @staticmethod
+    def Explicit(lags: Sequence[int]) -> "LagSpec":
+        return LagSpec(False, 0, [int(v) for v in lags])
+
+    def m_plus(self) -> int:
+        return self.max_lag if self.symmetric else max([0] + [l for l in self.lags])
+
+    def m_minus(self) -> int:
+        return self.max_lag if self.symmetric else max([0] + [-l for l in self.lags])
+
+    def values(self) -> list:
+        return list(range(-self.max_lag, self.max_lag + 1)) if self.symmetric else list(self.lags)
+
+
+@dataclass
+class EstimatorConfig:
+    """types.hpp:55-63 plus the B200 extensions (flags, recursive, block mode, channels)."""
+    mode: Mode = Mode.Set
+    conj: bool = False
+    win_len: int = 0
+    alphas: list = field(default_factory=list)
+    lag_spec: LagSpec = field(default_factory=LagSpec)
+    flags: int = 0            # 0 => from conj; Flags.BOTH computes both tables in one pass
+    lam: float = 0.0          # Recursive forgetting factor
+    emit_frames: bool = True  # False: block mode (count + fold; read with average())
+    channels: int = 1
+    device: int = 0
+
+    def _c(self):
+        c = _Config()
+        lib().cyc_config_init(C.byref(c))
+        al = np.ascontiguousarray(self.alphas, dtype=np.float64)
+        lg = np.ascontiguousarray(self.lag_spec.lags, dtype=np.int32)
+        c.mode, c.conj, c.flags, c.win_len = int(self.mode), int(bool(self.conj)), int(self.flags), int(self.win_len)
+        c.alphas = al.ctypes.data_as(C.POINTER(C.c_double)) if al.size else None
+        c.num_alphas = al.size
+        c.lag_symmetric = int(self.lag_spec.symmetric)
+        c.max_lag = int(self.lag_spec.max_lag)
+        c.lags = lg.ctypes.data_as(C.POINTER(C.c_int)) if lg.size else None
+        c.num_lags = lg.size
+        c.lam = float(self.lam)
+        c.emit_frames = int(bool(self.emit_frames))
+        c.channels = int(self.channels)
+        c.device = int(self.device)
+        return c, (al, lg)
+
+
+def validate_config(cfg: EstimatorConfig) -> list:
+    """types.cpp:30-63: every violated invariant; empty means ok."""
+    c, keep = cfg._c()
+    buf = C.create_string_buffer(8192)
+    n = lib().cyc_validate(C.byref(c), buf, 8192)
+    return [s for s in buf.value.decode().split("\n") if s][:n]
+
+
+@dataclass(frozen=True)
+class SetLayout:
+    num_alphas: int
+    max_lag: int
+
+
+@dataclass(frozen=True)
+class FullLayout:
+    num_lags: int
+    win_len: int
+
+
+@dataclass(frozen=True)
+class LagListLayout:
+    """Recursive mode: alpha-major over an explicit lag list."""
+    num_alphas: int
+    num_lags: int
+
+
+def layout_len(layout) -> int:
+    if isinstance(layout, SetLayout):
+        return layout.num_alphas * (2 * layout.max_lag + 1)
+    if isinstance(layout, FullLayout):
+        return layout.num_lags * layout.win_len
+    return layout.num_alphas * layout.num_lags
+
+
+def flat_index(layout, major: int, minor: int) -> int:
+    """types.cpp:81-98"""
+    if isinstance(layout, SetLayout):
+        if not 0 <= major < layout.num_alphas:
+            raise IndexError("cycle-frequency index out of range")
+        if not -layout.max_lag <= minor <= layout.max_lag:
+            raise IndexError("lag out of range")
+        return major * (2 * layout.max_lag + 1) + minor + layout.max_lag
+    if isinstance(layout, FullLayout):
+        if not 0 <= major < layout.num_lags:
+            raise IndexError("lag index out of range")
+        if not 0 <= minor < layout.win_len:
+            raise IndexError("DFT bin out of range")
+        return major * layout.win_len + minor
+    return major * layout.num_lags + minor
+
+
+def full_bin_to_alpha(k: int, n: int) -> float:
+    """types.cpp:100-104"""
+    if n <= 0 or k < 0 or k >= n:
+        raise IndexError("DFT bin out of range")
+    a = k / n
+    return a if 2 * k < n else a - 1.0
+
+
+@dataclass
+class CyclicFrame:
+    """types.hpp:97-104 (+ flag/channel for the multi-table extensions)."""
+    frame_index: int
+    start_abs: int
+    layout: object
+    values: np.ndarray
+    flag: int = 1
+    channel: int = 0
+
+
+def _raise(code: int, msg: str, index: int = -1):
+    if code == 1:
+        body = msg[len("invalid config:"):] if msg.startswith("invalid config:") else msg
+        viol = [v.strip().strip("[]") for v in body.split("] [")] if body.strip() else []
+        raise ConfigError(viol, msg)
+    if code == 2:
+        raise UsageError(msg)
+    if code == 3:
+        raise DataError(msg, index)
+    if code == 4:
+        raise CudaError(msg)
+    raise LogicError(msg)
+
+
+def _as_c64(a) -> np.ndarray:
+    a = np.asarray(a)
+    if a.dtype != np.complex64:
+        a = a.astype(np.complex64)
+    return np.ascontiguousarray(a)
+
+
+# ---------------------------------------------------------------------------
+# the estimator (estimator.hpp:97-137)
+# ---------------------------------------------------------------------------
+class CyclicCorrelator:
+    """Streaming cyclic (conjugate) cross-correlation estimator on the GPU.
+
+    Same contract as the reference: push() appends a chunk pair and returns
+    every frame that became computable; a non-finite sample rejects the whole
+    chunk (DataError naming its absolute index) and leaves the state
+    unchanged; the frame sequence is independent of chunk boundaries.
+    """
+
+    def __init__(self, cfg: EstimatorConfig):
+        self._cfg = cfg
+        L = lib()
+        c, keep = cfg._c()
+        h = C.c_void_p()
+        err = C.create_string_buffer(8192)
+        rc = L.cyc_create(C.byref(c), C.byref(h), err, 8192)
+        if rc:
+            _raise(rc, err.value.decode())
+        self._h = h
+        self._L = L
+        li = _LayoutInfo()
+        L.cyc_layout(h, C.byref(li))
+        self._li = li
+        if cfg.mode == Mode.Full:
+            self._layout = FullLayout(li.num_lags, li.win_len)
+        elif cfg.mode == Mode.Set:
+            self._layout = SetLayout(li.num_alphas, li.max_lag)
+        else:
+            self._layout = LagListLayout(li.num_alphas, li.num_lags)
+        self._frames: list = []
+        self._sink = _SINK(self._on_frame)
+
+    # -- reference accessors (estimator.hpp:109-115)
+    def config(self) -> EstimatorConfig:
+        return self._cfg
+
+    def layout(self):
+        return self._layout
+
+    def buffer_need(self) -> int:
+        return int(self._L.cyc_buffer_need(self._h))
+
+    def consumed(self) -> int:
+        return int(self._L.cyc_consumed(self._h))
+
+    def frames_emitted(self) -> int:
+        return int(self._L.cyc_frames_emitted(self._h))
+
+    # -- instrumentation
+    def kernel_launches(self) -> int:
+        return int(self._L.cyc_kernel_launches(self._h))
+
+    def algorithm(self) -> str:
+        b = C.create_string_buffer(256)
+        self._L.cyc_algorithm(self._h, b, 256)
+        return b.value.decode()
+
+    def stream(self) -> int:
+        return int(self._L.cyc_stream(self._h) or 0)
+
+    def synchronize(self):
+        self._check(self._L.cyc_synchronize(self._h))
+
+    def _on_frame(self, user, view):
+        v = view.contents
+        vals = np.ctypeslib.as_array(v.values, shape=(2 * v.len,)).view(np.complex128).copy()
+        self._frames.append(CyclicFrame(int(v.frame_index), int(v.start_abs), self._layout, vals,
+                                        int(v.flag), int(v.channel)))
+        return 0
+
+    def _check(self, rc: int):
+        if rc:
+            _raise(rc, self._L.cyc_last_error(self._h).decode(), int(self._L.cyc_data_error_index(self._h)))
+
+    def push(self, x, y=None) -> list:
+        """estimator.hpp:102-107.  x, y: complex arrays of one chunk (shape
+        (n,) or (channels, n)); y=None (or y is x) is the auto-correlation."""
+        same = y is None or y is x
+        cx = np.asarray(x)
+        if cx.dtype == np.complex128:
+            fn = self._L.cyc_push_f64
+            xa = np.ascontiguousarray(cx)
+            ya = None if same else np.ascontiguousarray(np.asarray(y, dtype=np.complex128))
+        else:
+            fn = self._L.cyc_push
+            xa = _as_c64(cx)
+            ya = None if same else _as_c64(y)
+        if ya is not None and ya.shape != xa.shape:
+            raise UsageError("x and y chunks must have equal length")
+        n = xa.shape[-1] if xa.ndim else 0
+        if xa.ndim == 2 and xa.shape[0] != self._cfg.channels:
+            raise UsageError("chunk rows must equal the channel count")
+        self._frames = []
+        rc = fn(self._h, xa.ctypes.data, ya.ctypes.data if ya is not None else None, n, self._sink, None)
+        self._check(rc)
+        out, self._frames = self._frames, []
+        return out
+
+    def push_device(self, x_ptr: int, n: int, y_ptr: Optional[int] = None) -> list:
+        """Push samples already resident in device memory (complex64)."""
+        self._frames = []
+        self._check(self._L.cyc_push_device(self._h, x_ptr, y_ptr, n, self._sink, None))
+        out, self._frames = self._frames, []
+        return out
+
+    def average(self, mode: AverageMode = AverageMode.Coherent, flag: Optional[int] = None,
+                channel: int = 0) -> np.ndarray:
+        """average_frames over every frame emitted so far (estimator.cpp:86-105)."""
+        out = np.zeros(layout_len(self._layout), dtype=np.complex128)
+        self._check(self._L.cyc_average(self._h, int(mode), int(flag or 0), int(channel), out.ctypes.data))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cyc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def average_frames(frames: Sequence[CyclicFrame], mode: AverageMode = AverageMode.Coherent) -> np.ndarray:
+    """estimator.cpp:86-105 over materialised frames (host-side, as the reference)."""
+    if not frames:
+        raise UsageError("cannot average an empty frame list")
+    lay = frames[0].layout
+    for f in frames:
+        if f.layout != lay or len(f.values) != len(frames[0].values):
+            raise UsageError("cannot average frames with mixed layouts")
+    acc = np.zeros(len(frames[0].values), dtype=np.complex128)
+    for f in frames:
+        acc += f.values if mode == AverageMode.Coherent else np.abs(f.values)
+    return acc / len(frames)
+
+
+def compute_set_window(xw, yw, alphas, max_lag: int, conj: bool, k0: int) -> np.ndarray:
+    """kernels.cpp:116-123 on the device."""
+    L = lib()
+    xa = np.ascontiguousarray(xw, dtype=np.complex128)
+    ya = np.ascontiguousarray(yw, dtype=np.complex128)
+    al = np.ascontiguousarray(alphas, dtype=np.float64)
+    out = np.zeros(len(al) * (2 * max_lag + 1), dtype=np.complex128)
+    err = C.create_string_buffer(1024)
+    rc = L.cyc_compute_set_window(xa.ctypes.data, len(xa), ya.ctypes.data, len(ya), al.ctypes.data, len(al),
+                                  int(max_lag), int(bool(conj)), int(k0), out.ctypes.data, err, 1024)
+    if rc:
+        _raise(rc, err.value.decode())
+    return out
+
+
+def compute_full_window(xw, yw, lags, conj: bool, k0: int) -> np.ndarray:
+    """kernels.cpp:125-135 on the device."""
+    L = lib()
+    xa = np.ascontiguousarray(xw, dtype=np.complex128)
+    ya = np.ascontiguousarray(yw, dtype=np.complex128)
+    lg = np.ascontiguousarray(lags, dtype=np.int32)
+    out = np.zeros(len(lg) * len(ya), dtype=np.complex128)
+    err = C.create_string_buffer(1024)
+    rc = L.cyc_compute_full_window(xa.ctypes.data, len(xa), ya.ctypes.data, len(ya), lg.ctypes.data, len(lg),
+                                   int(bool(conj)), int(k0), out.ctypes.data, err, 1024)
+    if rc:
+        _raise(rc, err.value.decode())
+    return out

@@ -1,0 +1,131 @@
+// direct.cu -- per-(alpha, tau) contraction for cycle frequencies that are not
+// on a usable rational grid (e.g. alpha = 0.1234507, proj/tests/test_estimator.cpp:107-124).
+//
+//   R(alpha, tau) = scale * sum_n x[n+tau] y^(*)[n] e^{-j2pi alpha n}
+//
+// The rotator is exact-index: the phase of sample n is alpha_fx * n (mod 2^64)
+// with alpha_fx = round(alpha * 2^64), i.e. an exact wrap-around fixed-point
+// turn count, instead of the reference's renormalised lead-phasor recurrence
+// (proj/src/estimator.cpp:70-73) or std::polar of a large argument
+// (proj/src/kernels.cpp:19-24).  The phasor is folded into y once per sample
+// and shared by every lag:  x conj(y e^{+j th}) and x (y e^{-j th}).
+#include "kernels.cuh"
+
+namespace cyc {
+namespace {
+
+constexpr int DT = 256;     // threads
+constexpr int TILE = 512;   // samples per smem tile
+constexpr int MAXL = 4;     // lags per thread (T <= 1024)
+
+__global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span) {
+    extern __shared__ float2 sm[];
+    float2* xs = sm;                  // TILE + span
+    float2* yc = xs + TILE + span;    // y * e^{+j th}
+    float2* yj = yc + TILE;           // y * e^{-j th}
+    const int split = blockIdx.x % L.splits;
+    const int a = (blockIdx.x / L.splits) % L.A;
+    const int si = blockIdx.x / (L.splits * L.A);
+    const DirectSeg seg = L.segs[si];
+    const uint64_t afx = L.alpha_fx[a];
+    const int64_t cnt = seg.n_end - seg.n_start;
+    const int64_t b0 = seg.n_start + cnt * split / L.splits;
+    const int64_t b1 = seg.n_start + cnt * (split + 1) / L.splits;
+
+    float2 accv[MAXL], accj[MAXL];
+    int loff[MAXL];
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k) {
+        accv[k] = make_float2(0.f, 0.f);
+        accj[k] = make_float2(0.f, 0.f);
+        const int t = threadIdx.x + k * DT;
+        loff[k] = t < L.T ? L.lags[t] - L.lag_lo : -1;
+    }
+    for (int64_t n0 = b0; n0 < b1; n0 += TILE) {
+        const int len = (int)min((int64_t)TILE, b1 - n0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < len + span; i += DT) {
+            const int64_t n = n0 + L.lag_lo + i;
+            xs[i] = (n >= seg.x_lo && n < seg.x_hi) ? seg.x[(uint64_t)n & seg.mask] : make_float2(0.f, 0.f);
+        }
+        for (int i = threadIdx.x; i < len; i += DT) {
+            const int64_t n = n0 + i;
+            float2 y = seg.y[(uint64_t)n & seg.mask];
+            if (seg.w_log2 != 0.f) {
+                const float w = seg.w_scale * exp2f((float)(seg.w_ref - n) * seg.w_log2);
+                y.x *= w;
+                y.y *= w;
+            }
+            const uint64_t ph = afx * (uint64_t)n;                    // exact turns * 2^64 (mod 1 turn)
+            const float u = (float)(int)(ph >> 32) * 4.656612873077393e-10f;  // 2 * turns in [-1, 1)
+            float sn, cs;
+            sincospif(u, &sn, &cs);
+            yc[i] = make_float2(y.x * cs - y.y * sn, y.x * sn + y.y * cs);
+            yj[i] = make_float2(y.x * cs + y.y * sn, y.y * cs - y.x * sn);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MAXL; ++k) {
+            if (loff[k] < 0) continue;
+            float2 av = accv[k], aj = accj[k];
+            const float2* xp = xs + loff[k];
+            for (int i = 0; i < len; ++i) {
+                const float2 xv = xp[i], c = yc[i], j = yj[i];
+                av.x += xv.x * c.x + xv.y * c.y;   // x * conj(c)
+                av.y += xv.y * c.x - xv.x * c.y;
+                aj.x += xv.x * j.x - xv.y * j.y;   // x * j
+                aj.y += xv.x * j.y + xv.y * j.x;
+            }
+            accv[k] = av;
+            accj[k] = aj;
+        }
+    }
+    float2* part = reinterpret_cast<float2*>(L.partials);
+    const size_t base = (((size_t)si * L.A + a) * L.splits + split) * 2;
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k) {
+        const int t = threadIdx.x + k * DT;
+        if (t >= L.T) continue;
+        part[(base + 0) * L.T + t] = accv[k];
+        part[(base + 1) * L.T + t] = accj[k];
+    }
+}
+
+__global__ void direct_reduce_kernel(DirectLaunch L) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int a = blockIdx.y;
+    const int si = blockIdx.z;
+    if (t >= L.T) return;
+    const float2* part = reinterpret_cast<const float2*>(L.partials);
+    const DirectSeg seg = L.segs[si];
+    int fi = 0;
+    for (int f = 0; f < 2; ++f) {
+        if (!(L.flags & (1 << f))) continue;
+        double re = 0.0, im = 0.0;
+        for (int s = 0; s < L.splits; ++s) {
+            const float2 v = part[((((size_t)si * L.A + a) * L.splits + s) * 2 + f) * L.T + t];
+            re += v.x;
+            im += v.y;
+        }
+        double2* out = L.out + (size_t)seg.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride;
+        out[(size_t)a * L.stride_a + (size_t)t * L.stride_t] = make_double2(re * L.scale, im * L.scale);
+        ++fi;
+    }
+}
+
+}  // namespace
+
+void launch_direct(const DirectLaunch& L, cudaStream_t st) {
+    if (L.n_segs == 0) return;
+    const int span = L.lag_hi - L.lag_lo;
+    const size_t smem = (size_t)(TILE + span + 2 * TILE) * sizeof(float2);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    direct_kernel<<<L.n_segs * L.A * L.splits, DT, smem, st>>>(L, span);
+    direct_reduce_kernel<<<dim3((L.T + 127) / 128, L.A, L.n_segs), 128, 0, st>>>(L);
+}
+
+}  // namespace cyc

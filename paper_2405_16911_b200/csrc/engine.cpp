@@ -1,0 +1,1166 @@
+// engine.cpp -- streaming cyclic-ACF engine (host side).  See engine.h.
+#include "engine.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+namespace cyc {
+
+namespace {
+
+constexpr int64_t PMAX = 1 << 16;          // largest rational alpha grid folded
+constexpr size_t MAX_TILES = 2048;          // fold tiles per launch (partials: 128 KiB each)
+constexpr size_t FRAME_SLOT_BUDGET = 256ull << 20;  // bytes of per-frame scratch per batch
+constexpr int SMS = 148;
+
+int64_t floor_div(int64_t a, int64_t b) {
+    int64_t q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+    return q;
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+    while (b) {
+        int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a < 0 ? -a : a;
+}
+
+int64_t next_pow2(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Smallest denominator q <= qmax with |alpha - p/q| <= 2^-50 (continued fractions).
+bool rational_of(double alpha, int64_t qmax, int64_t& p_out, int64_t& q_out) {
+    long double x = alpha;
+    int64_t h0 = 0, h1 = 1, k0 = 1, k1 = 0;  // convergents h/k
+    long double r = x;
+    for (int it = 0; it < 64; ++it) {
+        const long double a = floorl(r);
+        if (fabsl(a) > 9.0e18L) break;
+        const int64_t ai = (int64_t)a;
+        const int64_t h2 = ai * h1 + h0, k2 = ai * k1 + k0;
+        if (k2 > qmax || k2 <= 0) break;
+        h0 = h1;
+        h1 = h2;
+        k0 = k1;
+        k1 = k2;
+        if (fabsl(x - (long double)h1 / (long double)k1) <= ldexpl(1.0L, -50)) {
+            p_out = h1;
+            q_out = k1;
+            return true;
+        }
+        const long double frac = r - a;
+        if (frac == 0.0L) break;
+        r = 1.0L / frac;
+    }
+    return false;
+}
+
+bool find_grid(const std::vector<double>& alphas, int64_t& P, std::vector<int64_t>& k) {
+    P = 1;
+    for (double a : alphas) {
+        int64_t p, q;
+        if (!rational_of(a, PMAX, p, q)) return false;
+        const int64_t l = P / gcd64(P, q) * q;
+        if (l > PMAX) return false;
+        P = l;
+    }
+    k.resize(alphas.size());
+    for (size_t i = 0; i < alphas.size(); ++i) k[i] = llroundl((long double)alphas[i] * P);
+    return true;
+}
+
+uint64_t alpha_fixed(double a) {
+    // round(alpha * 2^64) in two's complement; alpha in [-1/2, 1/2)
+    const long double v = ldexpl((long double)a, 64);
+    return (uint64_t)(int64_t)llroundl(v);
+}
+
+inline bool finite_f32(float v) { return std::isfinite(v); }
+
+struct Bad {
+    uint64_t key = ~0ull;  // 2*i (x) or 2*i+1 (y)
+    int channel = 0;
+};
+
+// First non-finite sample in reference scan order (x before y per index,
+// proj/src/estimator.cpp:43-52); for f64 input also samples outside the
+// float32 range (the device computes in float32).
+template <typename T>
+Bad scan_bad(const T* x, const T* y, size_t n, int channels) {
+    auto bad_val = [](double v) { return !std::isfinite(v) || std::fabs(v) > (double)FLT_MAX; };
+    auto scan_range = [&](size_t i0, size_t i1, Bad& out) {
+        for (int c = 0; c < channels; ++c) {
+            const T* xc = x + (size_t)c * n;
+            const T* yc = y ? y + (size_t)c * n : nullptr;
+            for (size_t i = i0; i < i1; ++i) {
+                if (2ull * i >= out.key) break;
+                uint64_t k = ~0ull;
+                if (bad_val(xc[i].re) || bad_val(xc[i].im))
+                    k = 2ull * i;
+                else if (yc && (bad_val(yc[i].re) || bad_val(yc[i].im)))
+                    k = 2ull * i + 1;
+                if (k < out.key) {
+                    out.key = k;
+                    out.channel = c;
+                    break;
+                }
+            }
+        }
+    };
+    Bad best;
+    const size_t total = n * (size_t)channels;
+    unsigned nt = std::thread::hardware_concurrency();
+    if (nt == 0) nt = 1;
+    nt = std::min<unsigned>(nt, 16);
+    if (total < (1u << 20) || nt == 1) {
+        scan_range(0, n, best);
+        return best;
+    }
+    std::vector<Bad> part(nt);
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        const size_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
+        th.emplace_back([&, i0, i1, t] { scan_range(i0, i1, part[t]); });
+    }
+    for (auto& t : th) t.join();
+    for (auto& b : part)
+        if (b.key < best.key) best = b;
+    return best;
+}
+
+// Parallel copy / conversion into pinned staging ([channel][len] layout).
+template <typename T>
+void stage_copy(float2* dst, const T* src, size_t src_pitch, size_t off, size_t len, int channels) {
+    auto work = [&](int c0, int c1, size_t i0, size_t i1) {
+        for (int c = c0; c < c1; ++c) {
+            const T* s = src + (size_t)c * src_pitch + off;
+            float2* d = dst + (size_t)c * len;
+            if constexpr (sizeof(T) == sizeof(float2)) {
+                std::memcpy(d + i0, s + i0, (i1 - i0) * sizeof(float2));
+            } else {
+                for (size_t i = i0; i < i1; ++i) d[i] = make_float2((float)s[i].re, (float)s[i].im);
+            }
+        }
+    };
+    const size_t total = len * (size_t)channels;
+    unsigned nt = std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 8);
+    if (total < (1u << 19) || nt == 1) {
+        work(0, channels, 0, len);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        const size_t i0 = len * t / nt, i1 = len * (t + 1) / nt;
+        th.emplace_back([&, i0, i1] { work(0, channels, i0, i1); });
+    }
+    for (auto& t : th) t.join();
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    const cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// configuration
+// ---------------------------------------------------------------------------
+
+Cfg from_c(const cyc_config* c) {
+    Cfg g;
+    g.mode = c->mode;
+    g.flags = c->flags ? c->flags : (c->conj ? CYC_FLAG_CONJ : CYC_FLAG_CONV);
+    g.win_len = c->win_len;
+    if (c->alphas && c->num_alphas) g.alphas.assign(c->alphas, c->alphas + c->num_alphas);
+    g.lag_symmetric = c->lag_symmetric != 0;
+    g.max_lag = c->max_lag;
+    if (c->lags && c->num_lags) g.lags.assign(c->lags, c->lags + c->num_lags);
+    g.lambda = c->lambda;
+    g.emit_frames = c->emit_frames != 0;
+    g.channels = c->channels;
+    g.device = c->device;
+    return g;
+}
+
+// proj/src/types.cpp:30-63, same messages and order; extension rules appended.
+std::vector<std::string> validate(const Cfg& c) {
+    std::vector<std::string> bad;
+    if (c.win_len < 2) bad.push_back("win_len must be at least 2");
+    if (c.mode == CYC_MODE_SET) {
+        if (c.alphas.empty()) bad.push_back("Set mode needs at least one cycle frequency");
+        if (!c.lag_symmetric)
+            bad.push_back("Set mode requires a symmetric lag range");
+        else if (c.max_lag < 0)
+            bad.push_back("max_lag must be non-negative");
+    } else if (c.mode == CYC_MODE_FULL) {
+        if (c.lag_symmetric)
+            bad.push_back("Full mode requires an explicit lag list");
+        else if (c.lags.empty())
+            bad.push_back("Full mode needs at least one lag");
+    } else if (c.mode == CYC_MODE_RECURSIVE) {
+        if (c.alphas.empty()) bad.push_back("Recursive mode needs at least one cycle frequency");
+        if (c.lag_symmetric && c.max_lag < 0)
+            bad.push_back("max_lag must be non-negative");
+        else if (!c.lag_symmetric && c.lags.empty())
+            bad.push_back("Recursive mode needs at least one lag");
+        if (!(c.lambda > 0.0 && c.lambda < 1.0)) bad.push_back("forgetting factor must lie in (0, 1)");
+    } else {
+        bad.push_back("unknown estimator mode");
+    }
+    if (!c.lag_symmetric) {
+        for (size_t i = 1; i < c.lags.size(); ++i)
+            if (c.lags[i] <= c.lags[i - 1]) {
+                bad.push_back("explicit lags must be strictly increasing");
+                break;
+            }
+    }
+    for (double a : c.alphas)
+        if (!(a >= -0.5 && a < 0.5)) {
+            bad.push_back("cycle frequencies must lie in [-1/2, 1/2)");
+            break;
+        }
+    int mp = 0, mm = 0;
+    if (c.lag_symmetric) {
+        mp = mm = c.max_lag;
+    } else {
+        for (int l : c.lags) {
+            mp = std::max(mp, l);
+            mm = std::max(mm, -l);
+        }
+    }
+    const int span = std::max(mp, mm);
+    if (c.mode != CYC_MODE_RECURSIVE && c.win_len >= 2 && c.win_len <= 2 * span)
+        bad.push_back("win_len must exceed twice the largest |lag|");
+    if (c.flags < 1 || c.flags > 3) bad.push_back("flags must select the conventional and/or conjugate function");
+    if (c.channels < 1) bad.push_back("channels must be at least 1");
+    return bad;
+}
+
+// ---------------------------------------------------------------------------
+// lifetime
+// ---------------------------------------------------------------------------
+
+Status Engine::cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return Status::ok();
+    Status s;
+    s.code = CYC_ERR_CUDA;
+    s.msg = std::string(what) + ": " + cudaGetErrorString(e);
+    return s;
+}
+
+#define CK(expr)                                          \
+    do {                                                  \
+        Status _s = cuda_check((expr), #expr);            \
+        if (_s.code) return _s;                           \
+    } while (0)
+
+#define TRY(expr)                \
+    do {                         \
+        Status _s = (expr);      \
+        if (_s.code) return _s;  \
+    } while (0)
+
+Status Engine::create(const Cfg& cfg, Engine** out) {
+    auto v = validate(cfg);
+    if (!v.empty()) {
+        Status s;
+        s.code = CYC_ERR_CONFIG;
+        s.msg = "invalid config:";
+        for (auto& e : v) s.msg += " [" + e + "]";
+        return s;
+    }
+    Engine* e = new Engine();
+    Status s = e->init(cfg);
+    if (s.code) {
+        delete e;
+        return s;
+    }
+    *out = e;
+    return s;
+}
+
+Status Engine::create_unchecked(const Cfg& cfg, Engine** out) {
+    Engine* e = new Engine();
+    Status s = e->init(cfg);
+    if (s.code) {
+        delete e;
+        return s;
+    }
+    *out = e;
+    return s;
+}
+
+Status Engine::init(const Cfg& cfg) {
+    c_ = cfg;
+    CK(cudaSetDevice(c_.device));
+    nflags_ = (c_.flags == 3) ? 2 : 1;
+    // lags (types.cpp:9-28)
+    if (c_.lag_symmetric) {
+        for (int m = -c_.max_lag; m <= c_.max_lag; ++m) lags_req_.push_back(m);
+        m_plus_ = m_minus_ = c_.max_lag;
+    } else {
+        lags_req_ = c_.lags;
+        for (int l : lags_req_) {
+            m_plus_ = std::max(m_plus_, l);
+            m_minus_ = std::max(m_minus_, -l);
+        }
+    }
+    T_ = (int)lags_req_.size();
+    lag_lo_ = lags_req_.front();
+    lag_hi_ = lags_req_.back();
+    N_ = c_.win_len;
+    need_ = (size_t)N_ + m_plus_ + m_minus_;  // estimator.cpp:20
+    // layout (types.hpp:68-94)
+    std::vector<int64_t> k;
+    if (c_.mode == CYC_MODE_FULL) {
+        A_ = (int)N_;
+        layout_len_ = (size_t)T_ * N_;
+        stride_t_ = N_;
+        stride_a_ = 1;
+        P_ = N_;
+        k.resize(A_);
+        std::iota(k.begin(), k.end(), 0);
+        use_fold_ = true;
+    } else {
+        A_ = (int)c_.alphas.size();
+        layout_len_ = (size_t)A_ * T_;
+        stride_a_ = T_;
+        stride_t_ = 1;
+        use_fold_ = find_grid(c_.alphas, P_, k);
+    }
+    // fold geometry
+    const int span = lag_hi_ - lag_lo_ + 1;
+    lw_ = span <= 16 ? 2 : (span <= 32 ? 4 : 8);
+    TB_ = fold_tb(lw_);
+    RB_ = fold_rb(lw_);
+    n_lb_ = (span + TB_ - 1) / TB_;
+    t_pad_ = n_lb_ * TB_;
+    if (use_fold_) {
+        const int64_t l = P_ / gcd64(P_, RB_) * RB_;
+        if (P_ % RB_ == 0)
+            Pf_ = P_;
+        else if (l <= 16384)
+            Pf_ = l;
+        else
+            Pf_ = P_;
+        n_rb_ = (int)((Pf_ + RB_ - 1) / RB_);
+        if ((double)t_pad_ * Pf_ * 32.0 > 2.0e9) use_fold_ = false;  // accumulator too large
+    }
+    if (use_fold_) {
+        bins_.resize(A_);
+        for (int a = 0; a < A_; ++a) bins_[a] = (int)((((k[a] % P_) + P_) % P_) * (Pf_ / P_));
+        int lg = 0;
+        while ((int64_t(1) << lg) < Pf_) ++lg;
+        use_fft_ = is_pow2(Pf_) && Pf_ <= 8192 && A_ > 2 * lg;
+    } else {
+        if (T_ > 1024) {
+            Status s;
+            s.code = CYC_ERR_CONFIG;
+            s.msg = "invalid config: [more than 1024 lags with cycle frequencies off a rational grid]";
+            return s;
+        }
+        afx_.resize(A_);
+        for (int a = 0; a < A_; ++a) afx_[a] = alpha_fixed(c_.alphas[a]);
+    }
+
+    CK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+    // ring: pieces of Q samples per channel, four pieces per ring
+    int64_t qmin = std::max<int64_t>(next_pow2((int64_t)need_ + N_), 1 << 12);
+    int64_t qdef = std::max<int64_t>((1 << 21) / next_pow2(c_.channels), 1 << 12);
+    Q_ = std::max(qmin, qdef);
+    TRY(ensure_ring(4 * Q_));
+
+    const size_t lay_all = (size_t)c_.channels * nflags_ * layout_len_;
+    if (c_.mode != CYC_MODE_RECURSIVE) {
+        if (!c_.emit_frames) {
+            if (use_fold_) {
+                const size_t b = (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double);
+                CK(cudaMalloc(&S_main_, b));
+                CK(cudaMemsetAsync(S_main_, 0, b, cs_));
+            } else {
+                CK(cudaMalloc(&dsum_main_, lay_all * sizeof(double2)));
+                CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
+            }
+        } else {
+            CK(cudaMalloc(&coh_, lay_all * sizeof(double2)));
+            CK(cudaMalloc(&mag_, lay_all * sizeof(double)));
+            CK(cudaMemsetAsync(coh_, 0, lay_all * sizeof(double2), cs_));
+            CK(cudaMemsetAsync(mag_, 0, lay_all * sizeof(double), cs_));
+        }
+    } else {
+        rec_R_.assign(lay_all * 2, 0.0);
+        host_coh_.assign(lay_all * 2, 0.0);
+        host_mag_.assign(lay_all, 0.0);
+    }
+    CK(cudaMalloc(&avg_dev_, (size_t)nflags_ * layout_len_ * sizeof(double2)));
+    if (use_fold_) {
+        std::vector<double2> tw(Pf_);
+        for (int64_t j = 0; j < Pf_; ++j) {
+            const long double th = -2.0L * 3.14159265358979323846264338327950288L * (long double)j / (long double)Pf_;
+            tw[j] = make_double2((double)cosl(th), (double)sinl(th));
+        }
+        CK(cudaMalloc(&tw_, Pf_ * sizeof(double2)));
+        CK(cudaMemcpy(tw_, tw.data(), Pf_ * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&bins_dev_, A_ * sizeof(int)));
+        CK(cudaMemcpy(bins_dev_, bins_.data(), A_ * sizeof(int), cudaMemcpyHostToDevice));
+    } else {
+        CK(cudaMalloc(&afx_dev_, A_ * sizeof(uint64_t)));
+        CK(cudaMemcpy(afx_dev_, afx_.data(), A_ * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc(&lags_dev_, T_ * sizeof(int)));
+    CK(cudaMemcpy(lags_dev_, lags_req_.data(), T_ * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&key_dev_, sizeof(unsigned long long)));
+    CK(cudaMallocHost(&key_host_, sizeof(unsigned long long)));
+    TRY(ensure_meta(4u << 20));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&stage_ev_[i], cudaEventDisableTiming));
+    CK(cudaStreamSynchronize(cs_));
+    return Status::ok();
+}
+
+Engine::~Engine() {
+    if (cs_) cudaStreamSynchronize(cs_);
+    if (xs_) cudaStreamSynchronize(xs_);
+    cudaFree(ring_x_);
+    cudaFree(ring_y_);
+    cudaFree(S_main_);
+    cudaFree(dsum_main_);
+    cudaFree(S_frames_);
+    cudaFree(frames_dev_);
+    cudaFreeHost(frames_host_);
+    cudaFree(coh_);
+    cudaFree(mag_);
+    cudaFree(avg_dev_);
+    cudaFree(partials_);
+    cudaFree(tw_);
+    cudaFree(bins_dev_);
+    cudaFree(lags_dev_);
+    cudaFree(afx_dev_);
+    cudaFree(key_dev_);
+    cudaFreeHost(key_host_);
+    cudaFree(dev_tmp_);
+    cudaFreeHost(meta_host_);
+    cudaFree(meta_dev_);
+    for (int i = 0; i < META_SLOTS; ++i)
+        if (meta_ev_[i]) cudaEventDestroy(meta_ev_[i]);
+    for (int i = 0; i < 2; ++i) {
+        cudaFreeHost(stage_[i]);
+        cudaFreeHost(stage_y_[i]);
+        if (stage_ev_[i]) cudaEventDestroy(stage_ev_[i]);
+    }
+    for (auto& m : reads_) ev_pool_.push_back(m.ev);
+    for (auto e : ev_pool_) cudaEventDestroy(e);
+    if (cs_) cudaStreamDestroy(cs_);
+    if (xs_) cudaStreamDestroy(xs_);
+}
+
+Status Engine::ensure_ring(int64_t cap_min) {
+    if (ring_x_) return Status::ok();  // sized once at create
+    const int64_t cap = next_pow2(cap_min);
+    float2* nx = nullptr;
+    CK(cudaMalloc(&nx, (size_t)c_.channels * cap * sizeof(float2)));
+    CK(cudaMemsetAsync(nx, 0, (size_t)c_.channels * cap * sizeof(float2), cs_));
+    ring_x_ = nx;
+    cap_ = cap;
+    mask_ = (uint64_t)cap - 1;
+    return Status::ok();
+}
+
+Status Engine::ensure_partials(size_t bytes) {
+    if (partials_bytes_ >= bytes) return Status::ok();
+    if (partials_) {
+        CK(cudaStreamSynchronize(cs_));
+        cudaFree(partials_);
+    }
+    partials_bytes_ = std::max(bytes, partials_bytes_ * 2);
+    CK(cudaMalloc(&partials_, partials_bytes_));
+    return Status::ok();
+}
+
+Status Engine::ensure_frames(size_t slots) {
+    const size_t per = (size_t)nflags_ * layout_len_;
+    if (frames_slots_ < slots) {
+        if (frames_dev_) {
+            CK(cudaStreamSynchronize(cs_));
+            cudaFree(frames_dev_);
+            cudaFreeHost(frames_host_);
+        }
+        frames_slots_ = slots;
+        CK(cudaMalloc(&frames_dev_, frames_slots_ * per * sizeof(double2)));
+        CK(cudaMallocHost(&frames_host_, frames_slots_ * per * sizeof(double2)));
+    }
+    if (use_fold_ && S_frames_slots_ < slots) {
+        if (S_frames_) {
+            CK(cudaStreamSynchronize(cs_));
+            cudaFree(S_frames_);
+        }
+        S_frames_slots_ = slots;
+        CK(cudaMalloc(&S_frames_, S_frames_slots_ * (size_t)t_pad_ * Pf_ * 4 * sizeof(double)));
+    }
+    return Status::ok();
+}
+
+Status Engine::ensure_meta(size_t bytes) {
+    if (meta_slot_bytes_ >= bytes) return Status::ok();
+    if (meta_host_) {
+        CK(cudaStreamSynchronize(cs_));
+        cudaFreeHost(meta_host_);
+        cudaFree(meta_dev_);
+    }
+    meta_slot_bytes_ = std::max(bytes, meta_slot_bytes_ * 2);
+    CK(cudaMallocHost(&meta_host_, META_SLOTS * meta_slot_bytes_));
+    CK(cudaMalloc(&meta_dev_, META_SLOTS * meta_slot_bytes_));
+    for (int i = 0; i < META_SLOTS; ++i) {
+        if (!meta_ev_[i]) CK(cudaEventCreateWithFlags(&meta_ev_[i], cudaEventDisableTiming));
+        meta_ev_live_[i] = false;
+    }
+    meta_used_ = 0;
+    meta_slot_ = 0;
+    return Status::ok();
+}
+
+void* Engine::upload(const void* src, size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes > meta_slot_bytes_) {
+        ensure_meta(bytes);
+    }
+    if (meta_used_ + bytes > meta_slot_bytes_) {
+        cudaEventRecord(meta_ev_[meta_slot_], cs_);
+        meta_ev_live_[meta_slot_] = true;
+        meta_slot_ = (meta_slot_ + 1) % META_SLOTS;
+        if (meta_ev_live_[meta_slot_]) cudaEventSynchronize(meta_ev_[meta_slot_]);
+        meta_used_ = 0;
+    }
+    const size_t off = (size_t)meta_slot_ * meta_slot_bytes_ + meta_used_;
+    std::memcpy(meta_host_ + off, src, bytes);
+    cudaMemcpyAsync(meta_dev_ + off, meta_host_ + off, bytes, cudaMemcpyHostToDevice, cs_);
+    meta_used_ += bytes;
+    return meta_dev_ + off;
+}
+
+cudaEvent_t Engine::get_event() {
+    if (!ev_pool_.empty()) {
+        cudaEvent_t e = ev_pool_.back();
+        ev_pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+}
+
+void Engine::mark_read(int64_t lo) {
+    cudaEvent_t e = get_event();
+    cudaEventRecord(e, cs_);
+    reads_.push_back({e, lo});
+}
+
+// Before the copy stream overwrites ring positions up to abs_end, wait for every
+// compute launch that read the samples those positions held (abs - cap).
+void Engine::wait_ring_free(int64_t abs_end) {
+    const int64_t old_end = abs_end - cap_;
+    int found = -1;
+    for (int i = 0; i < (int)reads_.size(); ++i)
+        if (reads_[i].lo < old_end) found = i;
+    if (found < 0) return;
+    cudaStreamWaitEvent(xs_, reads_[found].ev, 0);
+    for (int i = 0; i <= found; ++i) {
+        ev_pool_.push_back(reads_.front().ev);
+        reads_.pop_front();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// compute primitives
+// ---------------------------------------------------------------------------
+
+Status Engine::fold(const std::vector<FoldSeg>& segs, double* S) {
+    struct G {
+        int seg, rb, lb;
+        int64_t p0, p1;
+    };
+    std::vector<G> groups;
+    int64_t work = 0;
+    for (int s = 0; s < (int)segs.size(); ++s) {
+        if (segs[s].n_end <= segs[s].n_start) continue;
+        const int64_t p0 = floor_div(segs[s].n_start, Pf_);
+        const int64_t p1 = floor_div(segs[s].n_end - 1, Pf_) + 1;
+        for (int rb = 0; rb < n_rb_; ++rb)
+            for (int lb = 0; lb < n_lb_; ++lb) {
+                groups.push_back({s, rb, lb, p0, p1});
+                work += p1 - p0;
+            }
+    }
+    if (groups.empty()) return Status::ok();
+    // split long groups so the grid covers the SMs (>= 2 waves of 1 CTA/SM)
+    const int64_t target = std::max<int64_t>(2 * SMS, (int64_t)groups.size());
+    const int64_t per_tile = std::max<int64_t>(4, (work + target - 1) / target);
+    size_t g0 = 0;
+    while (g0 < groups.size()) {
+        std::vector<FoldTile> tiles;
+        std::vector<FoldGroup> fg;
+        size_t g = g0;
+        for (; g < groups.size(); ++g) {
+            const G& gr = groups[g];
+            const int64_t np = gr.p1 - gr.p0;
+            const int sp = (int)std::max<int64_t>(1, std::min<int64_t>((np + per_tile - 1) / per_tile, 4096));
+            if (!tiles.empty() && tiles.size() + sp > MAX_TILES) break;
+            FoldGroup G2{gr.seg, gr.rb, gr.lb, (int)tiles.size(), 0, 0};
+            for (int i = 0; i < sp; ++i) {
+                const int64_t a = gr.p0 + np * i / sp, b = gr.p0 + np * (i + 1) / sp;
+                if (b > a) tiles.push_back({gr.seg, gr.rb, gr.lb, (int)fg.size(), a, b});
+            }
+            G2.t1 = (int)tiles.size();
+            fg.push_back(G2);
+        }
+        TRY(ensure_partials(tiles.size() * (size_t)TB_ * RB_ * sizeof(float4)));
+        FoldLaunch L{};
+        L.segs = (const FoldSeg*)upload(segs.data(), segs.size() * sizeof(FoldSeg));
+        L.tiles = (const FoldTile*)upload(tiles.data(), tiles.size() * sizeof(FoldTile));
+        L.groups = (const FoldGroup*)upload(fg.data(), fg.size() * sizeof(FoldGroup));
+        L.n_tiles = (int)tiles.size();
+        L.n_groups = (int)fg.size();
+        L.Pf = (int)Pf_;
+        L.lag_lo = lag_lo_;
+        L.t_pad = t_pad_;
+        L.lw = lw_;
+        L.partials = partials_;
+        L.S = S;
+        launch_fold(L, cs_);
+        launches_ += 2;
+        g0 = g;
+    }
+    return cuda_check(cudaGetLastError(), "fold launch");
+}
+
+Status Engine::finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
+                        double2* out) {
+    std::vector<FinalRow> rows;
+    rows.reserve((size_t)nslots * T_);
+    for (int s = 0; s < nslots; ++s)
+        for (int t = 0; t < T_; ++t) rows.push_back({s, lags_req_[t] - lag_lo_, t, s});
+    FinalizeLaunch L{};
+    L.S = S;
+    L.t_pad = t_pad_;
+    L.Pf = (int)Pf_;
+    L.rows = (const FinalRow*)upload(rows.data(), rows.size() * sizeof(FinalRow));
+    L.n_rows = (int)rows.size();
+    L.flags = c_.flags;
+    L.bins = bins_dev_;
+    L.A = A_;
+    L.tw = tw_;
+    L.scale_default = scale;
+    L.row_scale = slot_scale ? (const double*)upload(slot_scale->data(), slot_scale->size() * sizeof(double)) : nullptr;
+    L.out = out;
+    L.out_block_stride = (int64_t)nflags_ * layout_len_;
+    L.out_flag_stride = (int64_t)layout_len_;
+    L.stride_a = stride_a_;
+    L.stride_t = stride_t_;
+    L.use_fft = use_fft_ ? 1 : 0;
+    launch_finalize(L, cs_);
+    launches_ += 1;
+    return cuda_check(cudaGetLastError(), "finalize launch");
+}
+
+Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2* out) {
+    if (segs.empty()) return Status::ok();
+    int64_t maxcnt = 0;
+    for (auto& s : segs) maxcnt = std::max(maxcnt, s.n_end - s.n_start);
+    int splits = (int)std::min<int64_t>(256, std::max<int64_t>(1, maxcnt / 8192));
+    while (splits > 1 && (int64_t)segs.size() * A_ * splits > 64 * SMS) splits /= 2;
+    const size_t pbytes = segs.size() * (size_t)A_ * splits * 2 * T_ * sizeof(float2);
+    TRY(ensure_partials(pbytes));
+    DirectLaunch L{};
+    L.segs = (const DirectSeg*)upload(segs.data(), segs.size() * sizeof(DirectSeg));
+    L.n_segs = (int)segs.size();
+    L.alpha_fx = afx_dev_;
+    L.A = A_;
+    L.lags = lags_dev_;
+    L.T = T_;
+    L.lag_lo = lag_lo_;
+    L.lag_hi = lag_hi_;
+    L.splits = splits;
+    L.flags = c_.flags;
+    L.partials = partials_;
+    L.out = out;
+    L.out_block_stride = (int64_t)nflags_ * layout_len_;
+    L.out_flag_stride = (int64_t)layout_len_;
+    L.stride_a = stride_a_;
+    L.stride_t = stride_t_;
+    L.scale = scale;
+    launch_direct(L, cs_);
+    launches_ += 2;
+    return cuda_check(cudaGetLastError(), "direct launch");
+}
+
+// Tables of the windows [k0, k0+N) for each (k0, channel) -> frames_dev_.
+Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector<int>& chans, bool recursive,
+                              const float2* xbo, const float2* ybo, uint64_t mask_o) {
+    const size_t slots = k0s.size();
+    TRY(ensure_frames(slots));
+    const uint64_t mask = xbo ? mask_o : mask_;
+    const float lam_log2 = recursive ? (float)std::log2(c_.lambda) : 0.f;
+    const float w_scale = recursive ? (float)(1.0 - c_.lambda) : 1.f;
+    const double scale = recursive ? 1.0 : 1.0 / (double)N_;
+    if (use_fold_) {
+        std::vector<FoldSeg> segs(slots);
+        for (size_t s = 0; s < slots; ++s) {
+            const int ch = chans[s];
+            FoldSeg& g = segs[s];
+            g.x = xbo ? xbo : ring_x_ + (size_t)ch * cap_;
+            g.y = ybo ? ybo : ((cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_);
+            g.n_start = k0s[s];
+            g.n_end = k0s[s] + N_;
+            g.x_lo = k0s[s] + lag_lo_;
+            g.x_hi = k0s[s] + N_ + lag_hi_;
+            g.mask = mask;
+            g.w_ref = k0s[s] + N_ - 1;
+            g.w_log2 = lam_log2;
+            g.w_scale = w_scale;
+            g.slot = (int)s;
+        }
+        CK(cudaMemsetAsync(S_frames_, 0, slots * (size_t)t_pad_ * Pf_ * 4 * sizeof(double), cs_));
+        TRY(fold(segs, S_frames_));
+        TRY(finalize(S_frames_, (int)slots, scale, nullptr, frames_dev_));
+    } else {
+        std::vector<DirectSeg> segs(slots);
+        for (size_t s = 0; s < slots; ++s) {
+            const int ch = chans[s];
+            DirectSeg& g = segs[s];
+            g.x = xbo ? xbo : ring_x_ + (size_t)ch * cap_;
+            g.y = ybo ? ybo : ((cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_);
+            g.n_start = k0s[s];
+            g.n_end = k0s[s] + N_;
+            g.x_lo = k0s[s] + lag_lo_;
+            g.x_hi = k0s[s] + N_ + lag_hi_;
+            g.mask = mask;
+            g.w_ref = k0s[s] + N_ - 1;
+            g.w_log2 = lam_log2;
+            g.w_scale = w_scale;
+            g.out_block = (int)s;
+        }
+        TRY(direct(segs, scale, frames_dev_));
+    }
+    return Status::ok();
+}
+
+Status Engine::deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const std::vector<int>& chans,
+                       cyc_frame_sink sink, void* user, bool& stop) {
+    const size_t per = (size_t)nflags_ * layout_len_;
+    for (size_t s = 0; s < n_slots && !stop; ++s) {
+        for (int fi = 0; fi < nflags_; ++fi) {
+            cyc_frame_view v;
+            v.frame_index = fidx[s];
+            v.start_abs = (uint64_t)m_minus_ + fidx[s] * (uint64_t)N_;
+            v.flag = (c_.flags == 3) ? (fi == 0 ? CYC_FLAG_CONV : CYC_FLAG_CONJ) : c_.flags;
+            v.channel = chans[s];
+            v.len = layout_len_;
+            v.values = reinterpret_cast<const cyc_cf64*>(frames_host_ + s * per + (size_t)fi * layout_len_);
+            if (sink && sink(user, &v) != 0) {
+                stop = true;
+                break;
+            }
+        }
+    }
+    return Status::ok();
+}
+
+// Emit every frame that became computable (estimator.cpp:59-82).
+Status Engine::emit_new_frames(cyc_frame_sink sink, void* user) {
+    const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
+    if (avail <= frames_) return Status::ok();
+    const uint64_t f0 = frames_, f1 = avail;
+    const int C = c_.channels;
+    const int64_t lo_read = (int64_t)m_minus_ + (int64_t)f0 * N_ + lag_lo_;
+
+    if (c_.mode == CYC_MODE_RECURSIVE || c_.emit_frames) {
+        const size_t per_slot = (size_t)nflags_ * layout_len_ * 16 * 2 + (use_fold_ ? (size_t)t_pad_ * Pf_ * 32 : 0);
+        const uint64_t batch = std::max<uint64_t>(1, FRAME_SLOT_BUDGET / (per_slot * C));
+        bool stop = false;
+        const size_t per = (size_t)nflags_ * layout_len_;
+        for (uint64_t fb = f0; fb < f1; fb += batch) {
+            const uint64_t fe = std::min(f1, fb + batch);
+            std::vector<int64_t> k0s;
+            std::vector<int> chans;
+            std::vector<uint64_t> fidx;
+            for (uint64_t f = fb; f < fe; ++f)
+                for (int ch = 0; ch < C; ++ch) {
+                    k0s.push_back((int64_t)m_minus_ + (int64_t)f * N_);
+                    chans.push_back(ch);
+                    fidx.push_back(f);
+                }
+            TRY(compute_frames(k0s, chans, c_.mode == CYC_MODE_RECURSIVE));
+            const size_t slots = k0s.size();
+            if (c_.mode != CYC_MODE_RECURSIVE) {
+                // running average_frames sums; slots are [frame][channel] blocks
+                launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
+                launches_ += 1;
+            }
+            CK(cudaMemcpyAsync(frames_host_, frames_dev_, slots * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
+            CK(cudaStreamSynchronize(cs_));
+            if (c_.mode == CYC_MODE_RECURSIVE) {
+                // R_f = lam^N R_{f-1} + (weighted window sum)
+                const double decay = std::pow(c_.lambda, (double)N_);
+                for (size_t s = 0; s < slots; ++s) {
+                    const int ch = chans[s];
+                    double* R = rec_R_.data() + (size_t)ch * per * 2;
+                    double* hc = host_coh_.data() + (size_t)ch * per * 2;
+                    double* hm = host_mag_.data() + (size_t)ch * per;
+                    double2* v = frames_host_ + s * per;
+                    for (size_t i = 0; i < per; ++i) {
+                        R[2 * i] = decay * R[2 * i] + v[i].x;
+                        R[2 * i + 1] = decay * R[2 * i + 1] + v[i].y;
+                        v[i] = make_double2(R[2 * i], R[2 * i + 1]);
+                        hc[2 * i] += v[i].x;
+                        hc[2 * i + 1] += v[i].y;
+                        hm[i] += std::hypot(v[i].x, v[i].y);
+                    }
+                }
+            }
+            if (c_.emit_frames && !stop) TRY(deliver(slots, fidx, chans, sink, user, stop));
+        }
+    } else if (use_fold_) {
+        std::vector<FoldSeg> segs(C);
+        for (int ch = 0; ch < C; ++ch) {
+            FoldSeg& g = segs[ch];
+            g.x = ring_x_ + (size_t)ch * cap_;
+            g.y = (cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_;
+            g.n_start = (int64_t)m_minus_ + (int64_t)f0 * N_;
+            g.n_end = (int64_t)m_minus_ + (int64_t)f1 * N_;
+            g.x_lo = g.n_start + lag_lo_;
+            g.x_hi = g.n_end + lag_hi_;
+            g.mask = mask_;
+            g.w_log2 = 0.f;
+            g.w_scale = 1.f;
+            g.slot = ch;
+        }
+        TRY(fold(segs, S_main_));
+    } else {
+        std::vector<DirectSeg> segs(C);
+        for (int ch = 0; ch < C; ++ch) {
+            DirectSeg& g = segs[ch];
+            g.x = ring_x_ + (size_t)ch * cap_;
+            g.y = (cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_;
+            g.n_start = (int64_t)m_minus_ + (int64_t)f0 * N_;
+            g.n_end = (int64_t)m_minus_ + (int64_t)f1 * N_;
+            g.x_lo = g.n_start + lag_lo_;
+            g.x_hi = g.n_end + lag_hi_;
+            g.mask = mask_;
+            g.w_log2 = 0.f;
+            g.w_scale = 1.f;
+            g.out_block = ch;
+        }
+        // unnormalised block sums into scratch frames_dev_, then accumulate
+        TRY(ensure_frames(C));
+        TRY(direct(segs, 1.0, frames_dev_));
+        launch_add_f64((double*)dsum_main_, (const double*)frames_dev_, (int64_t)C * nflags_ * layout_len_ * 2, cs_);
+        launches_ += 1;
+    }
+    frames_ = f1;
+    mark_read(lo_read);
+    return Status::ok();
+}
+
+// ---------------------------------------------------------------------------
+// push (estimator.cpp:39-84)
+// ---------------------------------------------------------------------------
+
+Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_frame_sink sink, void* user) {
+    CK(cudaSetDevice(c_.device));
+    if (n == 0) return Status::ok();
+    if (!xv) {
+        Status s;
+        s.code = CYC_ERR_USAGE;
+        s.msg = "x and y chunks must have equal length";
+        return s;
+    }
+    const int C = c_.channels;
+    // 1. whole-chunk validation before any state change (estimator.cpp:43-52)
+    Bad bad;
+    if (kind == IN_HOST_F32) {
+        bad = scan_bad((const cyc_cf32*)xv, (const cyc_cf32*)yv, n, C);
+    } else if (kind == IN_HOST_F64) {
+        bad = scan_bad((const cyc_cf64*)xv, (const cyc_cf64*)yv, n, C);
+    } else {
+        *key_host_ = ~0ull;
+        CK(cudaMemcpyAsync(key_dev_, key_host_, sizeof(unsigned long long), cudaMemcpyHostToDevice, cs_));
+        for (int ch = 0; ch < C; ++ch) {
+            // per channel, keys are per-sample; channel resolution done below
+            launch_finite_check((const float2*)xv + (size_t)ch * n, yv ? (const float2*)yv + (size_t)ch * n : nullptr,
+                                (int64_t)n, key_dev_, cs_);
+            launches_ += 1;
+        }
+        CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs_));
+        CK(cudaStreamSynchronize(cs_));
+        bad.key = *key_host_;
+    }
+    if (bad.key != ~0ull) {
+        const uint64_t i = bad.key >> 1;
+        Status s;
+        s.code = CYC_ERR_DATA;
+        s.index = (int64_t)(consumed_ + i);
+        bool range = false;
+        if (kind == IN_HOST_F64) {
+            const cyc_cf64* p = (const cyc_cf64*)((bad.key & 1) ? yv : xv) + (size_t)bad.channel * n + i;
+            range = std::isfinite(p->re) && std::isfinite(p->im);
+        }
+        s.msg = std::string(range ? "sample outside the float32 range" : "non-finite sample") + " at absolute index " +
+                std::to_string(consumed_ + i) + " in " + ((bad.key & 1) ? "y" : "x") + " stream";
+        if (C > 1) s.msg += " of channel " + std::to_string(bad.channel);
+        return s;
+    }
+    // cross-correlation: materialise a y ring (copy x history on first use)
+    if (yv && !cross_) {
+        CK(cudaMalloc(&ring_y_, (size_t)C * cap_ * sizeof(float2)));
+        CK(cudaStreamSynchronize(xs_));
+        CK(cudaMemcpyAsync(ring_y_, ring_x_, (size_t)C * cap_ * sizeof(float2), cudaMemcpyDeviceToDevice, cs_));
+        cross_ = true;
+    }
+    const bool pinned = kind == IN_HOST_F32 && is_pinned(xv) && (!yv || is_pinned(yv));
+    if (kind != IN_DEVICE_F32 && !pinned && stage_len_ < (size_t)Q_) {
+        for (int i = 0; i < 2; ++i) {
+            if (stage_[i]) {
+                cudaEventSynchronize(stage_ev_[i]);
+                cudaFreeHost(stage_[i]);
+                cudaFreeHost(stage_y_[i]);
+                stage_y_[i] = nullptr;
+            }
+            CK(cudaMallocHost(&stage_[i], (size_t)C * Q_ * sizeof(float2)));
+            stage_ev_live_[i] = false;
+        }
+        stage_len_ = (size_t)Q_;
+    }
+    if (cross_ && kind != IN_DEVICE_F32 && !pinned && !stage_y_[0]) {
+        for (int i = 0; i < 2; ++i) CK(cudaMallocHost(&stage_y_[i], (size_t)C * Q_ * sizeof(float2)));
+    }
+
+    cudaEvent_t copy_ev = get_event();
+    int stage_k = 0;
+    for (size_t off = 0; off < n; off += (size_t)Q_) {
+        const size_t len = std::min((size_t)Q_, n - off);
+        const int64_t abs0 = (int64_t)consumed_;
+        wait_ring_free(abs0 + (int64_t)len);
+        // source rows for x and y: [channel][len] with a row pitch
+        const float2* sx = nullptr;
+        const float2* sy = nullptr;
+        size_t pitch = 0;
+        if (kind == IN_DEVICE_F32) {
+            for (int ch = 0; ch < C; ++ch) {
+                launch_ring_write(ring_x_ + (size_t)ch * cap_, mask_, abs0, (const float2*)xv + (size_t)ch * n + off,
+                                  (int64_t)len, xs_);
+                launches_ += 1;
+                if (cross_) {
+                    const float2* ysrc = (const float2*)(yv ? yv : xv) + (size_t)ch * n + off;
+                    launch_ring_write(ring_y_ + (size_t)ch * cap_, mask_, abs0, ysrc, (int64_t)len, xs_);
+                    launches_ += 1;
+                }
+            }
+        } else {
+            if (pinned) {
+                sx = (const float2*)xv + off;
+                sy = yv ? (const float2*)yv + off : (cross_ ? sx : nullptr);
+                pitch = n;
+            } else {
+                if (stage_ev_live_[stage_k]) CK(cudaEventSynchronize(stage_ev_[stage_k]));
+                if (kind == IN_HOST_F32) {
+                    stage_copy(stage_[stage_k], (const cyc_cf32*)xv, n, off, len, C);
+                    if (cross_)
+                        stage_copy(stage_y_[stage_k], (const cyc_cf32*)(yv ? yv : xv), n, off, len, C);
+                } else {
+                    stage_copy(stage_[stage_k], (const cyc_cf64*)xv, n, off, len, C);
+                    if (cross_)
+                        stage_copy(stage_y_[stage_k], (const cyc_cf64*)(yv ? yv : xv), n, off, len, C);
+                }
+                sx = stage_[stage_k];
+                sy = cross_ ? stage_y_[stage_k] : nullptr;
+                pitch = len;
+            }
+            // 2D DMA: C rows of len samples into the rings, split at the wrap
+            const size_t pos = (size_t)((uint64_t)abs0 & mask_);
+            const size_t first = std::min(len, (size_t)cap_ - pos);
+            auto dma = [&](float2* ring, const float2* src) -> Status {
+                CK(cudaMemcpy2DAsync(ring + pos, cap_ * sizeof(float2), src, pitch * sizeof(float2),
+                                     first * sizeof(float2), C, cudaMemcpyHostToDevice, xs_));
+                if (first < len)
+                    CK(cudaMemcpy2DAsync(ring, cap_ * sizeof(float2), src + first, pitch * sizeof(float2),
+                                         (len - first) * sizeof(float2), C, cudaMemcpyHostToDevice, xs_));
+                return Status::ok();
+            };
+            TRY(dma(ring_x_, sx));
+            if (cross_) TRY(dma(ring_y_, sy));
+            if (!pinned) {
+                CK(cudaEventRecord(stage_ev_[stage_k], xs_));
+                stage_ev_live_[stage_k] = true;
+                stage_k ^= 1;
+            }
+        }
+        CK(cudaEventRecord(copy_ev, xs_));
+        CK(cudaStreamWaitEvent(cs_, copy_ev, 0));
+        consumed_ += len;
+        TRY(emit_new_frames(sink, user));
+    }
+    ev_pool_.push_back(copy_ev);
+    // caller memory may not be retained after return
+    if (pinned || kind == IN_DEVICE_F32) CK(cudaStreamSynchronize(xs_));
+    return cuda_check(cudaGetLastError(), "push");
+}
+
+// ---------------------------------------------------------------------------
+// averages (estimator.cpp:86-105)
+// ---------------------------------------------------------------------------
+
+Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
+    CK(cudaSetDevice(c_.device));
+    Status u;
+    u.code = CYC_ERR_USAGE;
+    if (frames_ == 0) {
+        u.msg = "cannot average an empty frame list";
+        return u;
+    }
+    if (channel < 0 || channel >= c_.channels) {
+        u.msg = "channel out of range";
+        return u;
+    }
+    if (flag == 0) flag = c_.flags == 3 ? CYC_FLAG_CONV : c_.flags;
+    if (!(flag & c_.flags) || (flag != CYC_FLAG_CONV && flag != CYC_FLAG_CONJ)) {
+        u.msg = "flag not computed by this estimator";
+        return u;
+    }
+    const int fi = (c_.flags == 3 && flag == CYC_FLAG_CONJ) ? 1 : 0;
+    const size_t per = (size_t)nflags_ * layout_len_;
+    const double invF = 1.0 / (double)frames_;
+    if (c_.mode == CYC_MODE_RECURSIVE) {
+        const double* hc = host_coh_.data() + ((size_t)channel * per + (size_t)fi * layout_len_) * 2;
+        const double* hm = host_mag_.data() + (size_t)channel * per + (size_t)fi * layout_len_;
+        for (size_t i = 0; i < layout_len_; ++i) {
+            if (avg_mode == CYC_AVG_MAGNITUDE) {
+                out[i].re = hm[i] * invF;
+                out[i].im = 0.0;
+            } else {
+                out[i].re = hc[2 * i] * invF;
+                out[i].im = hc[2 * i + 1] * invF;
+            }
+        }
+        return Status::ok();
+    }
+    std::vector<double2> tmp(layout_len_);
+    if (c_.emit_frames) {
+        const size_t off = (size_t)channel * per + (size_t)fi * layout_len_;
+        if (avg_mode == CYC_AVG_MAGNITUDE) {
+            std::vector<double> m(layout_len_);
+            CK(cudaMemcpyAsync(m.data(), mag_ + off, layout_len_ * sizeof(double), cudaMemcpyDeviceToHost, cs_));
+            CK(cudaStreamSynchronize(cs_));
+            for (size_t i = 0; i < layout_len_; ++i) {
+                out[i].re = m[i] * invF;
+                out[i].im = 0.0;
+            }
+            return Status::ok();
+        }
+        CK(cudaMemcpyAsync(tmp.data(), coh_ + off, layout_len_ * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
+        CK(cudaStreamSynchronize(cs_));
+        for (size_t i = 0; i < layout_len_; ++i) {
+            out[i].re = tmp[i].x * invF;
+            out[i].im = tmp[i].y * invF;
+        }
+        return Status::ok();
+    }
+    if (avg_mode == CYC_AVG_MAGNITUDE) {
+        u.msg = "magnitude averaging needs per-frame values (emit_frames = 1)";
+        return u;
+    }
+    const double scale = invF / (double)N_;
+    if (use_fold_) {
+        const double* S = S_main_ + (size_t)channel * t_pad_ * Pf_ * 4;
+        TRY(finalize(S, 1, scale, nullptr, avg_dev_));
+        CK(cudaMemcpyAsync(tmp.data(), avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
+                           cudaMemcpyDeviceToHost, cs_));
+        CK(cudaStreamSynchronize(cs_));
+        for (size_t i = 0; i < layout_len_; ++i) {
+            out[i].re = tmp[i].x;
+            out[i].im = tmp[i].y;
+        }
+        return Status::ok();
+    }
+    CK(cudaMemcpyAsync(tmp.data(), dsum_main_ + (size_t)channel * per + (size_t)fi * layout_len_,
+                       layout_len_ * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
+    CK(cudaStreamSynchronize(cs_));
+    for (size_t i = 0; i < layout_len_; ++i) {
+        out[i].re = tmp[i].x * scale;
+        out[i].im = tmp[i].y * scale;
+    }
+    return Status::ok();
+}
+
+// One-shot window anchored at k0 (kernels.cpp:116-135): xw[0] is absolute
+// sample k0 - m_minus, yw[0] is absolute k0.
+Status Engine::compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw, size_t yw_len, uint64_t k0,
+                              cyc_cf64* out) {
+    CK(cudaSetDevice(c_.device));
+    // linear scratch: x window then y window, addressed with explicit offsets
+    const size_t tot = xw_len + yw_len;
+    if (dev_tmp_len_ < tot) {
+        cudaFree(dev_tmp_);
+        CK(cudaMalloc(&dev_tmp_, tot * sizeof(float2)));
+        dev_tmp_len_ = tot;
+    }
+    std::vector<float2> h(tot);
+    for (size_t i = 0; i < xw_len; ++i) h[i] = make_float2((float)xw[i].re, (float)xw[i].im);
+    for (size_t i = 0; i < yw_len; ++i) h[xw_len + i] = make_float2((float)yw[i].re, (float)yw[i].im);
+    CK(cudaMemcpyAsync(dev_tmp_, h.data(), tot * sizeof(float2), cudaMemcpyHostToDevice, cs_));
+    // absolute n maps to dev_tmp_[n - (k0 - m_minus)] for x and dev_tmp_[xw_len + n - k0] for y
+    const float2* xb = dev_tmp_ - ((int64_t)k0 - m_minus_);
+    const float2* yb = dev_tmp_ + xw_len - (int64_t)k0;
+    TRY(compute_frames({(int64_t)k0}, {0}, false, xb, yb, ~0ull));
+    const size_t per = (size_t)nflags_ * layout_len_;
+    std::vector<double2> r(per);
+    CK(cudaMemcpyAsync(r.data(), frames_dev_, per * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
+    CK(cudaStreamSynchronize(cs_));
+    for (size_t i = 0; i < layout_len_; ++i) {
+        out[i].re = r[i].x;
+        out[i].im = r[i].y;
+    }
+    return Status::ok();
+}
+
+Status Engine::synchronize() {
+    CK(cudaSetDevice(c_.device));
+    CK(cudaStreamSynchronize(xs_));
+    CK(cudaStreamSynchronize(cs_));
+    return Status::ok();
+}
+
+void Engine::layout(cyc_layout_info* li) const {
+    li->kind = c_.mode == CYC_MODE_FULL ? 1 : 0;
+    li->num_alphas = c_.mode == CYC_MODE_FULL ? 0 : A_;
+    li->max_lag = c_.lag_symmetric ? c_.max_lag : 0;
+    li->num_lags = T_;
+    li->win_len = (int)N_;
+    li->len = layout_len_;
+}
+
+std::string Engine::algorithm() const {
+    if (!use_fold_) return "direct";
+    return std::string(use_fft_ ? "fold-fft" : "fold-dft") + " P=" + std::to_string(P_) + " Pf=" +
+           std::to_string(Pf_) + " lw=" + std::to_string(lw_);
+}
+
+}  // namespace cyc

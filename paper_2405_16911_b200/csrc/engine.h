@@ -1,0 +1,197 @@
+// engine.h -- host-side streaming engine (C++), the implementation behind the
+// C-ABI in include/cycb200.h.
+//
+// Mirrors cycstat::CyclicCorrelator (proj/include/cycstat/estimator.hpp:97-137):
+// the same config contract, buffer_need, frame emission rule, absolute-phase
+// anchor and error semantics.  What changes is where the work runs:
+//   * ingest: samples go into power-of-two device rings indexed by absolute
+//     sample number (no O(buffer) front erase, proj/src/estimator.cpp:78-79);
+//     host chunks are DMA'd in pieces on a copy stream that overlaps the
+//     compute stream, through pinned staging when the caller's memory is
+//     pageable;
+//   * compute: fold + finalize (alphas on a rational grid) or the direct
+//     fixed-point-phase contraction (kernels.cuh);
+//   * block mode (emit_frames == 0): frames are only counted and folded into
+//     a running fp64 accumulator, so the coherent average_frames() of any
+//     number of frames costs one fold pass over the samples.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/cycb200.h"
+#include "kernels.cuh"
+
+namespace cyc {
+
+struct Status {
+    int code = CYC_OK;
+    std::string msg;
+    int64_t index = -1;
+    static Status ok() { return {}; }
+};
+
+// Normalised configuration (EstimatorConfig, proj/include/cycstat/types.hpp:55-63).
+struct Cfg {
+    int mode = CYC_MODE_SET;
+    int flags = CYC_FLAG_CONV;
+    int win_len = 0;
+    std::vector<double> alphas;
+    bool lag_symmetric = true;
+    int max_lag = 0;
+    std::vector<int> lags;  // explicit list as given
+    double lambda = 0.0;
+    bool emit_frames = true;
+    int channels = 1;
+    int device = 0;
+};
+
+// validate_config (proj/src/types.cpp:30-63) + rules of the extensions.
+std::vector<std::string> validate(const Cfg& c);
+Cfg from_c(const cyc_config* c);
+
+class Engine {
+public:
+    static Status create(const Cfg& cfg, Engine** out);
+    // For one-shot kernel-level windows (kernels.cpp:116-135), whose contract
+    // is only the window geometry, not the streaming span rule.
+    static Status create_unchecked(const Cfg& cfg, Engine** out);
+    ~Engine();
+
+    Status push(const void* x, const void* y, size_t n, int kind, cyc_frame_sink sink, void* user);
+    Status average(int avg_mode, int flag, int channel, cyc_cf64* out);
+    Status compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw, size_t yw_len,
+                          uint64_t k0, cyc_cf64* out);
+    Status synchronize();
+
+    size_t buffer_need() const { return need_; }
+    uint64_t consumed() const { return consumed_; }
+    uint64_t frames_emitted() const { return frames_; }
+    void layout(cyc_layout_info* li) const;
+    int num_flags() const { return nflags_; }
+    cudaStream_t stream() const { return cs_; }
+    uint64_t launches() const { return launches_; }
+    std::string algorithm() const;
+
+    std::string last_error;
+    int64_t last_error_index = -1;
+
+    enum { IN_HOST_F32 = 0, IN_HOST_F64 = 1, IN_DEVICE_F32 = 2 };
+
+private:
+    Engine() = default;
+    Status init(const Cfg& cfg);
+    Status cuda_check(cudaError_t e, const char* what);
+    Status ensure_ring(int64_t cap_min);
+    Status ensure_partials(size_t bytes);
+    Status ensure_frames(size_t slots);
+    Status ensure_meta(size_t bytes);
+    // Upload metadata through the pinned arena; returns device pointer.
+    void* upload(const void* src, size_t bytes);
+
+    // Fold `segs` (one per slot) into S (slots x t_pad x Pf x 4 fp64).
+    Status fold(const std::vector<FoldSeg>& segs, double* S);
+    // Finalize slots [0, nslots) of S into out tables (out_block = slot) with per-slot scale.
+    Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
+                    double2* out);
+    // Direct contraction of segs into out tables (out_block = seg.out_block).
+    Status direct(const std::vector<DirectSeg>& segs, double scale, double2* out);
+
+    // Per-frame tables for the given (k0, channel) windows -> frames_dev_ (fp64).
+    // Recursive weighting when `recursive`.
+    Status compute_frames(const std::vector<int64_t>& k0s, const std::vector<int>& chans, bool recursive,
+                          const float2* xbase_override = nullptr, const float2* ybase_override = nullptr,
+                          uint64_t mask_override = 0);
+    Status emit_new_frames(cyc_frame_sink sink, void* user);
+    Status deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const std::vector<int>& chans,
+                   cyc_frame_sink sink, void* user, bool& stop);
+
+    // ---- configuration ----
+    Cfg c_;
+    int nflags_ = 1;
+    std::vector<int> lags_req_;  // output lags ascending
+    int T_ = 0;
+    int lag_lo_ = 0, lag_hi_ = 0;
+    int m_plus_ = 0, m_minus_ = 0;
+    size_t need_ = 0;
+    int64_t N_ = 0;  // hop (win_len or emission interval)
+    int A_ = 0;      // output alphas (Full: N bins)
+    size_t layout_len_ = 0;
+    int64_t stride_a_ = 0, stride_t_ = 0;
+
+    bool use_fold_ = true;
+    int64_t P_ = 1, Pf_ = 1;
+    std::vector<int> bins_;
+    int lw_ = 8, TB_ = 64, RB_ = 128, n_rb_ = 1, n_lb_ = 1, t_pad_ = 64;
+    bool use_fft_ = false;
+    std::vector<uint64_t> afx_;
+
+    // ---- device resources ----
+    cudaStream_t cs_ = nullptr, xs_ = nullptr;
+    float2* ring_x_ = nullptr;
+    float2* ring_y_ = nullptr;  // null => auto-correlation (y = x)
+    bool cross_ = false;
+    int64_t cap_ = 0, Q_ = 0;
+    uint64_t mask_ = 0;
+    double* S_main_ = nullptr;        // block fold accumulators [channels][t_pad][Pf][4]
+    double2* dsum_main_ = nullptr;    // block direct sums [channels][nflags][layout]
+    double* S_frames_ = nullptr;      // per-frame folds
+    size_t S_frames_slots_ = 0;
+    double2* frames_dev_ = nullptr;   // per-frame tables [slot][nflags][layout]
+    size_t frames_slots_ = 0;
+    double2* frames_host_ = nullptr;  // pinned
+    double2* coh_ = nullptr;          // running coherent sums [channels][nflags][layout]
+    double* mag_ = nullptr;           // running magnitude sums
+    double2* avg_dev_ = nullptr;      // average scratch
+    float* partials_ = nullptr;
+    size_t partials_bytes_ = 0;
+    double2* tw_ = nullptr;
+    int* bins_dev_ = nullptr;
+    int* lags_dev_ = nullptr;
+    uint64_t* afx_dev_ = nullptr;
+    unsigned long long* key_dev_ = nullptr;
+    unsigned long long* key_host_ = nullptr;
+    float2* dev_tmp_ = nullptr;       // compute_window scratch
+    size_t dev_tmp_len_ = 0;
+
+    // pinned metadata arena (ring of slots guarded by events)
+    static constexpr int META_SLOTS = 4;
+    char* meta_host_ = nullptr;
+    char* meta_dev_ = nullptr;
+    size_t meta_slot_bytes_ = 0;
+    size_t meta_used_ = 0;
+    int meta_slot_ = 0;
+    cudaEvent_t meta_ev_[META_SLOTS] = {};
+    bool meta_ev_live_[META_SLOTS] = {};
+
+    // pinned staging for pageable host input
+    float2* stage_[2] = {nullptr, nullptr};
+    float2* stage_y_[2] = {nullptr, nullptr};
+    cudaEvent_t stage_ev_[2] = {};
+    bool stage_ev_live_[2] = {};
+    size_t stage_len_ = 0;
+
+    // ring overwrite protection: (event, lowest absolute x index read)
+    struct ReadMark {
+        cudaEvent_t ev;
+        int64_t lo;
+    };
+    std::deque<ReadMark> reads_;
+    std::vector<cudaEvent_t> ev_pool_;
+    cudaEvent_t get_event();
+    void mark_read(int64_t lo);
+    void wait_ring_free(int64_t abs_end);
+
+    // ---- streaming state (estimator.hpp:117-136) ----
+    uint64_t consumed_ = 0;
+    uint64_t frames_ = 0;
+    uint64_t launches_ = 0;
+    // recursive mode: running R per (channel, flag) on host, fp64
+    std::vector<double> rec_R_;
+    std::vector<double> host_coh_, host_mag_;  // recursive-mode averages
+};
+
+}  // namespace cyc

@@ -1,0 +1,124 @@
+// finalize.cu -- residue folds S_tau[r] -> cyclic ACF tables R(alpha, tau).
+//
+//   R(alpha_a, tau) = scale * sum_{r < Pf} q_tau[r] * W^{bin_a * r},  W = e^{-j2pi/Pf}
+//
+// with q built from the four real correlations of fold.cu per flag, and
+// bin_a = k_a * (Pf / P) (mod Pf) exact integers, so the phase is anchored to
+// absolute sample 0 exactly (the reference's exact-integer bin lead,
+// proj/src/kernels.cpp:103-114, generalised to every alpha on the grid).
+//
+// Two paths, both fp64:
+//   * radix-2 DIT FFT in shared memory (Pf a power of two <= 8192): replaces
+//     the reference's per-lag Fft::forward (proj/src/fft.cpp:44-87);
+//   * direct DFT with an exact (bin*r mod Pf) twiddle index, for small alpha
+//     sets or non-power-of-two periods (proj/src/fft.cpp:89-100 analogue).
+#include "kernels.cuh"
+
+namespace cyc {
+namespace {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+__device__ __forceinline__ double2 combine(const double* s, int flag_bit) {
+    // s = (c0, c1, c2, c3) = (sum xr*yr, sum xi*yr, sum xr*yi, sum xi*yi)
+    return flag_bit == 0 ? make_double2(s[0] + s[3], s[1] - s[2])   // x * conj(y)
+                         : make_double2(s[0] - s[3], s[1] + s[2]);  // x * y
+}
+
+// grid: (n_rows, n_flag_tables); one CTA per (row, flag).
+__global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
+    extern __shared__ double2 buf[];
+    const FinalRow row = L.rows[blockIdx.x];
+    const int fi = blockIdx.y;  // index among requested flags
+    const int flag_bit = (L.flags == 2) ? 1 : fi;
+    const int Pf = L.Pf;
+    const double* Srow = L.S + ((size_t)row.slot * L.t_pad + row.t_span) * (size_t)Pf * 4;
+    for (int r = threadIdx.x; r < Pf; r += blockDim.x) {
+        const int rev = (int)(__brev((unsigned)r) >> (32 - log2Pf));
+        buf[rev] = combine(Srow + (size_t)r * 4, flag_bit);
+    }
+    __syncthreads();
+    for (int len = 2; len <= Pf; len <<= 1) {
+        const int half = len >> 1;
+        const int tstep = Pf / len;
+        for (int j = threadIdx.x; j < (Pf >> 1); j += blockDim.x) {
+            const int grp = j / half, pos = j - grp * half;
+            const int i0 = grp * len + pos, i1 = i0 + half;
+            const double2 w = L.tw[pos * tstep];
+            const double2 u = buf[i0];
+            const double2 v = cmul(buf[i1], w);
+            buf[i0] = make_double2(u.x + v.x, u.y + v.y);
+            buf[i1] = make_double2(u.x - v.x, u.y - v.y);
+        }
+        __syncthreads();
+    }
+    const double sc = L.row_scale ? L.row_scale[row.out_block] : L.scale_default;
+    double2* out = L.out + (size_t)row.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride +
+                   (size_t)row.t_out * L.stride_t;
+    for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
+        const double2 v = buf[L.bins[a]];
+        out[(size_t)a * L.stride_a] = make_double2(v.x * sc, v.y * sc);
+    }
+}
+
+// Direct DFT: grid (n_rows, n_flag_tables, ceil(A / 256)); thread per alpha.
+constexpr int DFT_CHUNK = 2048;
+__global__ void __launch_bounds__(256) finalize_dft_kernel(FinalizeLaunch L) {
+    __shared__ double2 q[DFT_CHUNK];
+    const FinalRow row = L.rows[blockIdx.x];
+    const int fi = blockIdx.y;
+    const int flag_bit = (L.flags == 2) ? 1 : fi;
+    const int Pf = L.Pf;
+    const int a = blockIdx.z * blockDim.x + threadIdx.x;
+    const bool active = a < L.A;
+    const int64_t bin = active ? L.bins[a] : 0;
+    const double* Srow = L.S + ((size_t)row.slot * L.t_pad + row.t_span) * (size_t)Pf * 4;
+    double re = 0.0, im = 0.0;
+    for (int r0 = 0; r0 < Pf; r0 += DFT_CHUNK) {
+        const int n = min(DFT_CHUNK, Pf - r0);
+        __syncthreads();
+        for (int r = threadIdx.x; r < n; r += blockDim.x) q[r] = combine(Srow + (size_t)(r0 + r) * 4, flag_bit);
+        __syncthreads();
+        if (active) {
+            int64_t idx = (bin * r0) % Pf;
+            for (int r = 0; r < n; ++r) {
+                const double2 w = L.tw[idx];
+                const double2 v = q[r];
+                re += v.x * w.x - v.y * w.y;
+                im += v.x * w.y + v.y * w.x;
+                idx += bin;
+                if (idx >= Pf) idx -= Pf;
+            }
+        }
+    }
+    if (!active) return;
+    const double sc = L.row_scale ? L.row_scale[row.out_block] : L.scale_default;
+    double2* out = L.out + (size_t)row.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride +
+                   (size_t)row.t_out * L.stride_t;
+    out[(size_t)a * L.stride_a] = make_double2(re * sc, im * sc);
+}
+
+}  // namespace
+
+void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
+    if (L.n_rows == 0) return;
+    const int nflag = L.flags == 3 ? 2 : 1;
+    if (L.use_fft) {
+        int lg = 0;
+        while ((1 << lg) < L.Pf) ++lg;
+        const size_t smem = (size_t)L.Pf * sizeof(double2);
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 8192 * (int)sizeof(double2));
+            attr_set = true;
+        }
+        finalize_fft_kernel<<<dim3(L.n_rows, nflag), 512, smem, st>>>(L, lg);
+    } else {
+        finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + 255) / 256), 256, 0, st>>>(L);
+    }
+}
+
+}  // namespace cyc

@@ -1,0 +1,142 @@
+// kernels.cuh -- device-side data structures and launchers for the sm_100a
+// cyclic-ACF kernels.  Host code (engine.cpp) only sees the launch_* functions.
+//
+// Algorithm map:
+//   fold      exact reassociation of sum_n q_tau[n] e^{-j2pi k n/P} into
+//             S_tau[r] = sum_{n = r mod Pf} q_tau[n]  (4 real correlations per
+//             (tau, r) give both the conventional and the conjugate ACF);
+//             replaces the per-alpha inner loop of set_window_values
+//             (proj/src/kernels.cpp:46-55) and the lag product of
+//             full_window_values (proj/src/kernels.cpp:85-87).
+//   finalize  S -> R(alpha, tau): radix-2 fp64 FFT over residues (replaces
+//             Fft::forward, proj/src/fft.cpp:44-87) or a direct DFT with exact
+//             (k r mod Pf) twiddles for small alpha sets / non-pow2 periods.
+//   direct    alphas not on a rational grid: per-(alpha, tau) contraction with
+//             a 64-bit fixed-point phase (exact wrap) instead of the reference's
+//             drifting lead-phasor recurrence (proj/src/estimator.cpp:70-73).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cyc {
+
+// One contiguous y-index range [n_start, n_end) of one stream whose fold goes
+// into accumulator slot `slot`.  Samples live in power-of-two device rings
+// indexed by absolute sample number (ring[n & mask]).
+struct FoldSeg {
+    const float2* x;     // x ring base
+    const float2* y;     // y ring base (== x for auto-correlation)
+    int64_t n_start;     // first y index (absolute)
+    int64_t n_end;       // one past the last y index
+    int64_t x_lo, x_hi;  // absolute x range present in the ring
+    uint64_t mask;       // ring mask (~0 for a linear device buffer)
+    int64_t w_ref;       // recursive weighting: w(n) = w_scale * 2^{(w_ref - n) * w_log2}
+    float w_log2;        // 0 => unweighted
+    float w_scale;
+    int slot;
+    int pad;
+};
+
+// A CTA's unit of work: one (segment, residue block, lag block) over the
+// absolute fold-period range [p0, p1).  `group` indexes (seg, rb, lb).
+struct FoldTile {
+    int seg, rb, lb, group;
+    int64_t p0, p1;
+};
+
+// (seg, rb, lb) -> contiguous tile range, for the deterministic fp64 reduce.
+struct FoldGroup {
+    int seg, rb, lb;
+    int t0, t1;
+    int pad;
+};
+
+struct FoldLaunch {
+    const FoldSeg* segs;
+    const FoldTile* tiles;
+    const FoldGroup* groups;
+    int n_tiles, n_groups;
+    int Pf;              // fold period (residues)
+    int lag_lo;          // lowest lag of the computed span
+    int t_pad;           // padded lag span (multiple of the lag block)
+    int lw;              // lag lanes per warp: 2, 4 or 8  (TB = 8*lw, RB = 1024/lw)
+    float* partials;     // [n_tiles][TB][RB] float4
+    double* S;           // [slots][t_pad][Pf][4] fp64 accumulators
+};
+
+void launch_fold(const FoldLaunch& L, cudaStream_t st);   // fold + fp64 reduce
+
+inline int fold_tb(int lw) { return 8 * lw; }
+inline int fold_rb(int lw) { return 1024 / lw; }
+
+// Finalize: S rows -> output tables.
+struct FinalRow {
+    int slot;       // accumulator slot
+    int t_span;     // row in S (lag - lag_lo)
+    int t_out;      // output lag index
+    int out_block;  // output table index (slot-major, see engine)
+};
+
+struct FinalizeLaunch {
+    const double* S;          // [slots][t_pad][Pf][4]
+    int t_pad, Pf;
+    const FinalRow* rows;
+    int n_rows;
+    int flags;                // bit0 conv, bit1 conj
+    const int* bins;          // [A] DFT bin (mod Pf) per output alpha
+    int A;
+    const double2* tw;        // e^{-j2pi j / Pf}, j < Pf
+    double scale_default;     // multiply (1/count)
+    const double* row_scale;  // optional per-out_block scale (nullptr => scale_default)
+    double2* out;             // [out_block][flag_index][...] with strides below
+    int64_t out_block_stride; // elements per out_block (all flags)
+    int64_t out_flag_stride;  // elements per flag table
+    int64_t stride_a, stride_t;
+    int use_fft;              // 1: radix-2 FFT (Pf pow2 <= 8192); 0: direct DFT
+};
+
+void launch_finalize(const FinalizeLaunch& L, cudaStream_t st);
+
+// Direct contraction for arbitrary alphas.
+struct DirectSeg {
+    const float2* x;
+    const float2* y;
+    int64_t n_start, n_end;
+    int64_t x_lo, x_hi;
+    uint64_t mask;
+    int64_t w_ref;       // recursive weighting (as FoldSeg)
+    float w_log2, w_scale;
+    int out_block;
+    int pad;
+};
+
+struct DirectLaunch {
+    const DirectSeg* segs;
+    int n_segs;
+    const uint64_t* alpha_fx;   // [A] round(alpha * 2^64)
+    int A;
+    const int* lags;            // [T] requested lags (ascending)
+    int T;
+    int lag_lo, lag_hi;
+    int splits;                 // sample splits per (seg, alpha)
+    int flags;
+    float* partials;            // [n_segs][A][splits][2 flags][T] float2
+    double2* out;               // [out_block][flag_index][...]
+    int64_t out_block_stride, out_flag_stride, stride_a, stride_t;
+    double scale;
+};
+
+void launch_direct(const DirectLaunch& L, cudaStream_t st);
+
+// Utilities.
+void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st);
+void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len,
+                         double2* coh, double* mag, cudaStream_t st);
+// First non-finite sample (key = 2*i for x, 2*i+1 for y) -> atomicMin(*key).
+void launch_finite_check(const float2* x, const float2* y, int64_t n,
+                         unsigned long long* key, cudaStream_t st);
+// Ring write from a device source with wrap: ring[(abs0 + i) & mask] = src[i].
+void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src,
+                       int64_t n, cudaStream_t st);
+
+}  // namespace cyc

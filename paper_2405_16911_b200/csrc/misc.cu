@@ -1,0 +1,74 @@
+// misc.cu -- small device utilities of the streaming engine.
+#include "kernels.cuh"
+
+namespace cyc {
+namespace {
+
+__global__ void add_f64_kernel(double* dst, const double* src, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+
+// average_frames (proj/src/estimator.cpp:86-105): running coherent and
+// magnitude sums in frame order (deterministic per element).
+__global__ void accum_frames_kernel(const double2* frames, int64_t n_frames, int64_t len, double2* coh,
+                                    double* mag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        double2 c = coh[i];
+        double m = mag[i];
+        for (int64_t f = 0; f < n_frames; ++f) {
+            const double2 v = frames[f * len + i];
+            c.x += v.x;
+            c.y += v.y;
+            m += hypot(v.x, v.y);
+        }
+        coh[i] = c;
+        mag[i] = m;
+    }
+}
+
+// Whole-chunk finite scan (proj/src/estimator.cpp:43-52): the smallest key
+// 2*i (x) / 2*i+1 (y) names the first offending sample in the reference's
+// scan order (x before y at each index).
+__global__ void finite_check_kernel(const float2* x, const float2* y, int64_t n, unsigned long long* key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 a = x[i];
+        unsigned long long k = ~0ull;
+        if (!isfinite(a.x) || !isfinite(a.y)) {
+            k = 2ull * (unsigned long long)i;
+        } else if (y) {
+            const float2 b = y[i];
+            if (!isfinite(b.x) || !isfinite(b.y)) k = 2ull * (unsigned long long)i + 1ull;
+        }
+        if (k != ~0ull) atomicMin(key, k);
+    }
+}
+
+__global__ void ring_write_kernel(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ring[(uint64_t)(abs0 + i) & mask] = src[i];
+}
+
+int grid_for(int64_t n, int threads) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g > 148 * 16) g = 148 * 16;
+    return g < 1 ? 1 : (int)g;
+}
+
+}  // namespace
+
+void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st) {
+    if (n > 0) add_f64_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, src, n);
+}
+void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len, double2* coh, double* mag,
+                         cudaStream_t st) {
+    if (n_frames > 0 && len > 0) accum_frames_kernel<<<grid_for(len, 256), 256, 0, st>>>(frames, n_frames, len, coh, mag);
+}
+void launch_finite_check(const float2* x, const float2* y, int64_t n, unsigned long long* key, cudaStream_t st) {
+    if (n > 0) finite_check_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, key);
+}
+void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n, cudaStream_t st) {
+    if (n > 0) ring_write_kernel<<<grid_for(n, 256), 256, 0, st>>>(ring, mask, abs0, src, n);
+}
+
+}  // namespace cyc

@@ -1,0 +1,363 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Every case replays a pin of the reference's own tests
+(proj/tests/test_estimator.cpp, test_reference.cpp, acceptance_main.cpp) with
+the north-star tolerance (relative L2 <= 1e-4 per table, |dR| <= 1e-5 * mean
+power per value) in place of the reference's fp64 1e-12.
+"""
+import numpy as np
+import pytest
+
+from conftest import assert_parity, mean_power, rand_c
+
+pytestmark = pytest.mark.gpu
+
+
+def set_cfg(cyc, n, m, alphas, conj=False, **kw):
+    return cyc.EstimatorConfig(mode=cyc.Mode.Set, conj=conj, win_len=n, alphas=list(alphas),
+                               lag_spec=cyc.LagSpec.Symmetric(m), **kw)
+
+
+def full_cfg(cyc, n, lags, conj=False, **kw):
+    return cyc.EstimatorConfig(mode=cyc.Mode.Full, conj=conj, win_len=n,
+                               lag_spec=cyc.LagSpec.Explicit(lags), **kw)
+
+
+def frames_array(frames):
+    return np.array([f.values for f in frames])
+
+
+# test_estimator.cpp:211-229 -- Set windows vs the reference, x != y, both flags
+@pytest.mark.parametrize("conj", [False, True])
+def test_set_frames_match_oracle(cyc, oracle, conj):
+    x = rand_c(400, 1234)
+    y = rand_c(400, 4321)
+    alphas = [3 / 64, 0.0, -0.21]
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 64, 3, alphas, conj))
+    frames = est.push(x, y)
+    want = oracle.stream(0, conj, 64, x.astype(complex), y.astype(complex), alphas=alphas, max_lag=3)
+    assert len(frames) == len(want) >= 5
+    for f, fr in enumerate(frames):
+        assert fr.frame_index == f and fr.start_abs == 3 + 64 * f
+    assert_parity(frames_array(frames), want, mean_power(x) ** 0.5 * mean_power(y) ** 0.5, what="set")
+
+
+# test_estimator.cpp:242-272 -- Full mode bins, lags {-3, 0, 5}
+@pytest.mark.parametrize("conj", [False, True])
+def test_full_frames_match_oracle(cyc, oracle, conj):
+    x = rand_c(300, 777)
+    y = rand_c(300, 888)
+    est = cyc.CyclicCorrelator(full_cfg(cyc, 64, [-3, 0, 5], conj))
+    frames = est.push(x, y)
+    want = oracle.stream(1, conj, 64, x.astype(complex), y.astype(complex), lags=[-3, 0, 5])
+    assert len(frames) == len(want) >= 3
+    assert_parity(frames_array(frames), want, 2.0, what="full")
+
+
+def test_full_frames_match_reference(cyc, ref):
+    x = rand_c(1 << 12, 5)
+    for conj in (False, True):
+        est = cyc.CyclicCorrelator(full_cfg(cyc, 256, [-2, 0, 3], conj))
+        frames = est.push(x)
+        want, st = ref.stream(1, conj, 256, x.astype(complex), x.astype(complex), lags=[-2, 0, 3], chunk=100)
+        assert [f.start_abs for f in frames] == list(st)
+        assert_parity(frames_array(frames), want, mean_power(x), what="full vs reference")
+
+
+# test_estimator.cpp:81-105 -- tone identities
+def test_tone_identities(cyc):
+    f0 = 0.125
+    n = np.arange(256)
+    x = np.exp(2j * np.pi * f0 * n).astype(np.complex64)
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 64, 2, [0.0]))
+    frames = est.push(x, x)
+    assert frames
+    lay = cyc.SetLayout(1, 2)
+    for fr in frames:
+        for m in range(-2, 3):
+            want = np.exp(2j * np.pi * f0 * m)
+            assert abs(fr.values[cyc.flat_index(lay, 0, m)] - want) <= 1e-5
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 64, 2, [0.25], conj=True))
+    for fr in est.push(x, x):
+        assert abs(fr.values[cyc.flat_index(lay, 0, 1)] - np.exp(2j * np.pi * f0)) <= 1e-5
+
+
+# test_estimator.cpp:107-124 -- absolute anchoring at an off-grid alpha (direct path)
+def test_absolute_anchoring_direct_path(cyc):
+    alpha = 0.1234507
+    f0 = alpha / 2
+    n = np.arange(300 * 64 + 8)
+    x = np.exp(1j * (2 * np.pi * np.fmod(f0 * n, 1.0) + 0.3)).astype(np.complex64)
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 64, 2, [alpha], conj=True))
+    assert est.algorithm() == "direct"
+    frames = est.push(x, x)
+    assert len(frames) == 300
+    first = frames[0].values
+    for fr in frames:
+        assert np.max(np.abs(fr.values - first)) <= 2e-5
+    coh = est.average(cyc.AverageMode.Coherent)
+    assert abs(abs(coh[2]) - 1.0) <= 2e-5
+
+
+# test_estimator.cpp:126-140 -- mismatched chunks and NaN rejection, state unchanged
+def test_push_rejects_bad_chunks(cyc):
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 8, 1, [0.0]))
+    good = rand_c(4, 1)
+    with pytest.raises(cyc.UsageError):
+        est.push(good, rand_c(3, 2))
+    poisoned = rand_c(4, 3)
+    poisoned[2] = np.nan
+    assert est.push(good, good) == []
+    with pytest.raises(cyc.DataError, match="index 6") as ei:
+        est.push(poisoned, poisoned)
+    assert ei.value.index == 6
+    assert est.consumed() == 4
+    x = rand_c(32, 4)
+    assert est.push(x, x)
+
+
+def test_nan_in_y_names_y_stream(cyc):
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 8, 1, [0.0]))
+    x = rand_c(16, 1)
+    y = rand_c(16, 2)
+    y[5] = np.inf
+    with pytest.raises(cyc.DataError, match="index 5 in y stream"):
+        est.push(x, y)
+    assert est.consumed() == 0 and est.frames_emitted() == 0
+
+
+# test_estimator.cpp:142-182 -- chunking invariance
+def test_chunking_invariance(cyc):
+    x = rand_c(1 << 13, 99)
+    y = rand_c(1 << 13, 100)
+
+    def run(cuts):
+        est = cyc.CyclicCorrelator(set_cfg(cyc, 512, 5, [0.125, -0.3]))
+        out, pos = [], 0
+        for c in cuts:
+            out += est.push(x[pos:pos + c], y[pos:pos + c])
+            pos += c
+        assert pos == len(x)
+        return out
+
+    whole = run([len(x)])
+    assert len(whole) == 15
+    rng = np.random.default_rng(7)
+    parts = [[1] * 700 + [len(x) - 700], [1, 7, 64, 1000, len(x) - 1072]]
+    for _ in range(2):
+        cuts, left = [], len(x)
+        while left:
+            t = min(left, int(rng.integers(1, 701)))
+            cuts.append(t)
+            left -= t
+        parts.append(cuts)
+    for cuts in parts:
+        got = run(cuts)
+        assert len(got) == len(whole)
+        for a, b in zip(whole, got):
+            assert a.frame_index == b.frame_index and a.start_abs == b.start_abs
+            assert np.max(np.abs(a.values - b.values)) <= 1e-12
+
+
+# test_estimator.cpp:184-209 -- frame bookkeeping and the emission rule
+def test_frame_bookkeeping(cyc):
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 16, 3, [0.1]))
+    need = est.buffer_need()
+    assert need == 22
+    x = rand_c(200, 55)
+    fed = emitted = 0
+    rng = np.random.default_rng(3)
+    while fed < len(x):
+        take = min(len(x) - fed, int(rng.integers(0, 37)))
+        frames = est.push(x[fed:fed + take], x[fed:fed + take])
+        fed += take
+        for fr in frames:
+            assert fr.frame_index == emitted and fr.start_abs == 3 + emitted * 16
+            emitted += 1
+        assert est.frames_emitted() == ((fed - need) // 16 + 1 if fed >= need else 0)
+        assert est.consumed() == fed
+    assert est.frames_emitted() == 12
+
+
+# test_estimator.cpp:60-68
+def test_buffer_need(cyc):
+    assert cyc.CyclicCorrelator(set_cfg(cyc, 8, 2, [0.125])).buffer_need() == 12
+    assert cyc.CyclicCorrelator(full_cfg(cyc, 16, [-3, 5])).buffer_need() == 24
+    assert cyc.CyclicCorrelator(full_cfg(cyc, 8, [0])).buffer_need() == 8
+    assert cyc.CyclicCorrelator(full_cfg(cyc, 16, [-2, -1])).buffer_need() == 18
+
+
+# test_estimator.cpp:231-240 -- Full-mode all-ones window
+def test_full_window_all_ones(cyc):
+    out = cyc.compute_full_window(np.ones(33), np.ones(32), [0, 1], False, 0)
+    lay = cyc.FullLayout(2, 32)
+    for l in range(2):
+        assert abs(out[cyc.flat_index(lay, l, 0)] - 1) <= 1e-6
+        for k in range(1, 32):
+            assert abs(out[cyc.flat_index(lay, l, k)]) <= 1e-6
+
+
+# test_reference.cpp:54-67 -- frozen golden values through the device window kernel
+def test_frozen_values_via_set_window(cyc):
+    x = np.array([1, 1j, -1 + 0.5j, 2 - 1j, 1 + 1j, -1j, 0.5, -1 - 1j])
+    # a: cyclic_xcorr_direct(x, x, 0.25, m=1, conj=false, k0=1, N=4)
+    v = cyc.compute_set_window(x[0:6], x[1:5], [0.25], 1, False, 1)
+    assert abs(v[2] - (-0.12499999999999993 - 0.12500000000000011j)) <= 1e-6
+    v = cyc.compute_set_window(x[0:6], x[1:5], [0.25], 1, True, 1)
+    assert abs(v[2] - (0.12499999999999999 + 0.12500000000000006j)) <= 1e-6
+    # c: alpha 0.11, m=-1, k0=2  -> window xw = x[1:7], yw = x[2:6]
+    v = cyc.compute_set_window(x[1:7], x[2:6], [0.11], 1, False, 2)
+    assert abs(v[0] - (-0.26908075755090433 + 0.66834328861739112j)) <= 1e-6
+
+
+# test_reference.cpp:92-115 -- compute_set_window == direct sum
+def test_set_window_vs_direct(cyc, oracle):
+    x = rand_c(200, 2718).astype(complex)
+    y = rand_c(200, 2719).astype(complex)
+    alphas = [0.0, 0.125, -0.37, 0.11]
+    M, k0 = 4, 37
+    for conj in (False, True):
+        vals = cyc.compute_set_window(x[k0 - M:k0 + 64 + M], y[k0:k0 + 64], alphas, M, conj, k0)
+        lay = cyc.SetLayout(4, M)
+        for a, al in enumerate(alphas):
+            for m in range(-M, M + 1):
+                want = oracle.direct(x, y, al, m, conj, k0, 64)
+                assert abs(vals[cyc.flat_index(lay, a, m)] - want) <= 1e-5
+
+
+# Block mode (emit_frames = 0): coherent average == reference average_frames
+@pytest.mark.parametrize("conj", [False, True])
+def test_block_average_full_mode(cyc, oracle, conj):
+    x = rand_c(1 << 16, 11)
+    N, lags = 256, list(range(8))
+    est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, conj, emit_frames=False))
+    assert est.push(x) == []
+    F = est.frames_emitted()
+    assert F == (len(x) - N - 7) // N + 1
+    got = est.average()
+    cv, cj = oracle.block_fold(x, x, np.arange(N), N, lags, 0, F * N)
+    want = (cj if conj else cv).T.reshape(-1)
+    assert_parity(got, want, mean_power(x), what="block full")
+
+
+def test_block_average_both_flags_chunked(cyc, oracle):
+    x = rand_c(100_000, 12)
+    N, lags = 1024, list(range(64))
+    cfg = full_cfg(cyc, N, lags, flags=cyc.Flags.BOTH, emit_frames=False)
+    est = cyc.CyclicCorrelator(cfg)
+    for c in np.array_split(np.arange(len(x)), 7):
+        est.push(x[c[0]:c[-1] + 1])
+    F = est.frames_emitted()
+    cv, cj = oracle.block_fold(x, x, np.arange(N), N, lags, 0, F * N)
+    assert_parity(est.average(flag=cyc.Flags.CONV), cv.T.reshape(-1), mean_power(x), what="conv")
+    assert_parity(est.average(flag=cyc.Flags.CONJ), cj.T.reshape(-1), mean_power(x), what="conj")
+
+
+def test_block_average_matches_reference_block(cyc, ref):
+    x = rand_c(1 << 15, 21)
+    N, lags = 512, list(range(16))
+    for conj in (False, True):
+        est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, conj, emit_frames=False))
+        est.push(x)
+        want, F = ref.block_average(1, conj, N, x, x, lags=lags)
+        assert F == est.frames_emitted()
+        assert_parity(est.average(), want, mean_power(x), what="vs reference")
+
+
+def test_set_block_average_grid_alphas(cyc, oracle):
+    """Set-mode block average at the C1 conjugate grid alpha = 0.1 + k/16 (P = 80)."""
+    x = rand_c(40_000, 31)
+    alphas = [0.1 + k / 16 for k in range(-2, 3)]
+    M, N = 15, 4096
+    for conj in (False, True):
+        est = cyc.CyclicCorrelator(set_cfg(cyc, N, M, alphas, conj, emit_frames=False))
+        assert est.algorithm().startswith("fold")
+        est.push(x)
+        F = est.frames_emitted()
+        want = oracle.block_direct(x.astype(complex), x.astype(complex), alphas, list(range(-M, M + 1)), conj,
+                                   M, F * N)
+        assert_parity(est.average(), want.reshape(-1), mean_power(x), what="set block")
+
+
+def test_direct_block_average(cyc, oracle):
+    x = rand_c(20_000, 41)
+    alphas = [0.1234507, -0.3333333]
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 1000, 4, alphas, False, emit_frames=False))
+    assert est.algorithm() == "direct"
+    est.push(x)
+    F = est.frames_emitted()
+    want = oracle.block_direct(x.astype(complex), x.astype(complex), alphas, list(range(-4, 5)), False, 4, F * 1000)
+    assert_parity(est.average(), want.reshape(-1), mean_power(x), what="direct block")
+
+
+def test_magnitude_average(cyc):
+    x = rand_c(64, 31)
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 16, 1, [0.25]))
+    frames = est.push(x, x)
+    assert len(frames) >= 2
+    mag = est.average(cyc.AverageMode.Magnitude)
+    want = cyc.average_frames(frames, cyc.AverageMode.Magnitude)
+    assert np.max(np.abs(mag - want)) <= 1e-12
+    coh = est.average(cyc.AverageMode.Coherent)
+    assert np.max(np.abs(coh - cyc.average_frames(frames))) <= 1e-12
+
+
+def test_recursive_matches_oracle(cyc, oracle):
+    x = rand_c(5000, 51)
+    alphas = [m / 64 for m in range(-4, 4)]
+    lags = [0, 1, 2, 3]
+    lam, E = 1 - 2 ** -6, 512
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Recursive, win_len=E, alphas=alphas,
+                              lag_spec=cyc.LagSpec.Explicit(lags), lam=lam)
+    est = cyc.CyclicCorrelator(cfg)
+    frames = []
+    for c in np.array_split(np.arange(len(x)), 5):
+        frames += est.push(x[c[0]:c[-1] + 1])
+    want = oracle.recursive(x.astype(complex), x.astype(complex), alphas, lags, False, lam, E)
+    assert len(frames) == len(want)
+    got = np.array([f.values for f in frames]).reshape(want.shape)
+    assert_parity(got, want, mean_power(x), what="recursive")
+
+
+def test_multichannel_block(cyc, oracle):
+    C_, L = 4, 30_000
+    xs = np.stack([rand_c(L, 100 + c) for c in range(C_)])
+    N, lags = 256, list(range(32))
+    est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, flags=cyc.Flags.BOTH, emit_frames=False, channels=C_))
+    est.push(xs)
+    F = est.frames_emitted()
+    for c in range(C_):
+        cv, cj = oracle.block_fold(xs[c], xs[c], np.arange(N), N, lags, 0, F * N)
+        assert_parity(est.average(flag=cyc.Flags.CONV, channel=c), cv.T.reshape(-1), mean_power(xs[c]))
+        assert_parity(est.average(flag=cyc.Flags.CONJ, channel=c), cj.T.reshape(-1), mean_power(xs[c]))
+
+
+def test_pinned_and_f64_inputs_agree(cyc):
+    x = rand_c(50_000, 61)
+    N, lags = 1024, list(range(16))
+    outs = []
+    for kind in ("pageable", "pinned", "f64"):
+        est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, emit_frames=False))
+        if kind == "pinned":
+            px = cyc.host_alloc(x.shape)
+            px[:] = x
+            est.push(px)
+        elif kind == "f64":
+            est.push(x.astype(np.complex128))
+        else:
+            est.push(x)
+        outs.append(est.average())
+    assert np.max(np.abs(outs[0] - outs[1])) <= 1e-12
+    assert np.max(np.abs(outs[0] - outs[2])) <= 1e-12
+
+
+def test_device_push(cyc):
+    import torch
+    x = rand_c(70_000, 71)
+    N, lags = 1024, list(range(64))
+    a = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, emit_frames=False))
+    a.push(x)
+    b = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, emit_frames=False))
+    dx = torch.from_numpy(x).cuda()
+    b.push_device(dx.data_ptr(), len(x))
+    assert np.max(np.abs(a.average() - b.average())) <= 1e-12
