@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 cyclic-ACF hot path (BASELINE.json metric, configs[1]).
+
+Workload (config 2, "dense uniform grid"): 2^24 complex64 samples of QPSK,
+RRC rolloff 0.35, 4 samples/symbol, f_c = 0.1, SNR 5 dB (seeded synthetic);
+1024 cycle frequencies k/1024 in [-1/2, 1/2) x lags 0..63, conventional AND
+conjugate, one block average over the whole record.  The reference computes
+this as Full mode N = 1024, lags 0..63, pushes + average_frames(Coherent)
+(proj/tools/main.cpp:212-214, proj/src/estimator.cpp:86-105); F = 16383
+frames cover L_eff = 16,776,192 samples.
+
+One step = reset the estimator, push the record, read both (alpha, tau)
+tables.  Two measurements per run:
+  value  -- input already resident in HBM (cyc_push_device), CUDA events on
+            the estimator's stream;
+  e2e    -- input in pinned HOST memory through the reference-facing C-ABI
+            call (cyc_push), H2D DMA and the D2H of both tables inside the
+            timed region.
+metric = direct-sum-equivalent (alpha, tau) updates/s = A*T*L_eff*flags / t
+(SURVEY §8d); the executed algorithm is the exact residue fold (4 FP32 FMAs
+per (lag, sample) for both flags) + fp64 FFT, so the roofline line reports
+the fold kernel's executed FP32 rate against the device's FFMA peak.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cyclic-ACF (alpha,tau) updates/s"
+UNIT = "updates/s"
+N_WIN, LAGS, A, FLAGS = 1024, 64, 1024, 2
+L_REC = 1 << 24
+
+
+def l_eff(L: int) -> int:
+    need = N_WIN + LAGS - 1
+    F = (L - need) // N_WIN + 1
+    return F * N_WIN
+
+
+def updates(L: int) -> int:
+    return A * LAGS * l_eff(L) * FLAGS
+
+
+def config_block(n_gpus: int):
+    return {"workload": "C2 dense grid: QPSK-RRC(0.35) 4 sps f_c=0.1 5 dB, 2^24 cf32 samples/GPU; "
+                        "1024 alphas k/1024 x tau 0..63, conv+conj, one block average",
+            "samples_per_gpu": L_REC, "alphas": A, "lags": LAGS, "flags": ["conv", "conj"],
+            "win_len": N_WIN, "l_eff": l_eff(L_REC), "parallelism": f"independent records x{n_gpus}",
+            "l2": "input 134 MB > 126 MB L2 (no reuse across steps)",
+            "algorithm": "exact residue fold (FFMA2) + fp64 radix-2 FFT"}
+
+
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def allreduce_max(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "fold_ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    except Exception:
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(L_sample_frames: int, threads: int, x: np.ndarray):
+    """The reference library (oracle/_ref, else the C restatement) on the host cores."""
+    os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    from oracle.oracle import Oracle, RefLib, have_ref
+    lags = list(range(LAGS))
+    n = (L_sample_frames - 1) * N_WIN + N_WIN + LAGS - 1
+    xs = np.ascontiguousarray(x[:n])
+    if have_ref():
+        r = RefLib()
+        t0 = time.perf_counter()
+        F = 0
+        for conj in (0, 1):
+            _, F = r.block_average(1, conj, N_WIN, xs, xs, lags=lags)
+        dt = time.perf_counter() - t0
+        kind = "reference"
+    else:
+        o = Oracle()
+        t0 = time.perf_counter()
+        o.block_fold(xs, xs, np.arange(N_WIN), N_WIN, lags, 0, L_sample_frames * N_WIN)
+        dt = time.perf_counter() - t0
+        F = L_sample_frames
+        kind = "port"
+    ups = A * LAGS * F * N_WIN * FLAGS
+    return {"value": ups / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"Full N=1024 lags 0..63, conv+conj, {F} frames ({F * N_WIN} samples) of the C2 record, "
+                      f"N-sized pushes + running coherent sum, OMP_NUM_THREADS={threads}, "
+                      f"OMP_WAIT_POLICY={os.environ.get('OMP_WAIT_POLICY')}",
+            "seconds": dt, "msamples_per_s": F * N_WIN / dt / 1e6}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU path on this box's host cores."""
+    if rank != 0:
+        return
+    from paper_2405_16911_b200 import siggen
+    x = siggen.c2_record(seed=2, n=L_REC)
+    threads = os.cpu_count() or 1
+    frames = int(os.environ.get("CYC_REF_FRAMES", "1024"))
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_baseline(64, threads, x)
+    vals = []
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(frames, threads, x))
+    v = statistics.median([c["value"] for c in vals])
+    cb = dict(vals[-1])
+    cb["value"] = v
+    ms = 1e3 * updates(L_REC) / v  # time the full record would take at this rate
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args.gpus), "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2405_16911_b200 as cyc
+    from paper_2405_16911_b200 import siggen
+
+    dev = local
+    torch.cuda.set_device(dev)
+    x = siggen.c2_record(seed=2 + rank, n=L_REC)
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=N_WIN, lag_spec=cyc.LagSpec.Explicit(range(LAGS)),
+                              flags=cyc.Flags.BOTH, emit_frames=False, device=dev)
+    est = cyc.CyclicCorrelator(cfg)
+    stream = torch.cuda.ExternalStream(est.stream(), device=dev)
+    dx = torch.from_numpy(x.view(np.float32)).to(f"cuda:{dev}")
+    ptr = dx.data_ptr()
+
+    def step_device():
+        est.reset()
+        est.push_device(ptr, L_REC)
+        a = est.average(flag=cyc.Flags.CONV)
+        b = est.average(flag=cyc.Flags.CONJ)
+        return a, b
+
+    px = cyc.host_alloc(x.shape)
+    px[:] = x
+
+    def step_e2e():
+        est.reset()
+        est.push(px)
+        a = est.average(flag=cyc.Flags.CONV)
+        b = est.average(flag=cyc.Flags.CONJ)
+        return a, b
+
+    def timed(fn, k):
+        barrier(ws)
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier(ws)
+        return e0.elapsed_time(e1) / k
+
+    # warm-up (untimed)
+    for _ in range(max(args.warmup, 0)):
+        step_device()
+        step_e2e()
+    # device-resident (value)
+    est.profile(True)
+    n0, ms0, fl0 = est.profile_read()
+    launches0 = est.kernel_launches()
+    clk = Clocks(dev)
+    ms_dev = timed(step_device, args.steps)
+    clocks = clk.stop()
+    n1, ms1, fl1 = est.profile_read()
+    launches = est.kernel_launches() - launches0
+    est.profile(False)
+    # e2e through the host C-ABI call
+    ms_e2e = timed(step_e2e, args.steps)
+
+    ms_dev_max = allreduce_max(ms_dev, ws)
+    ms_e2e_max = allreduce_max(ms_e2e, ws)
+    fold_ms = (ms1 - ms0) / max(1, n1 - n0)
+    fold_flops = (fl1 - fl0) / max(1, n1 - n0)
+    fold_tflops = fold_flops / (fold_ms * 1e-3) / 1e12 if fold_ms > 0 else 0.0
+    peak = cyc.measure_fp32_peak(dev)
+    traffic, tsrc = traffic_from_profiles()
+    if rank != 0:
+        return
+    ups = updates(L_REC) * ws
+    line = {
+        "metric": METRIC, "value": ups / (ms_dev_max * 1e-3), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 reductions)", "data": "synthetic",
+        "config": config_block(ws),
+        "msamples_per_s": L_REC * ws / (ms_dev_max * 1e-3) / 1e6,
+        "e2e": {"value": ups / (ms_e2e_max * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e_max,
+                "h2d_bytes_per_step": L_REC * 8, "d2h_bytes_per_step": 2 * A * LAGS * 16,
+                "msamples_per_s": L_REC * ws / (ms_e2e_max * 1e-3) / 1e6,
+                "path": "cyc_push(pinned host cf32) + cyc_average x2 (D2H)"},
+        "roofline": {"bound": "fp32", "kernel": "fold_kernel", "achieved": fold_tflops, "peak": peak,
+                     "unit": "TFLOP/s", "frac": fold_tflops / peak if peak else None,
+                     "traffic": traffic, "traffic_source": tsrc,
+                     "algorithmic_flops_per_launch": fold_flops, "ms_per_launch": fold_ms,
+                     "launches_per_step": (n1 - n0) / args.steps,
+                     "fold_share_of_step": (ms1 - ms0) / args.steps / ms_dev_max,
+                     "peak_source": "measured live: FFMA microbenchmark in libcycb200 "
+                                    "(MEASURED_PEAKS.json carries no FP32 figure)",
+                     "algorithmic_unit": "8 FP32 flops per (requested lag, folded sample): 4 FMAs give "
+                                         "both flags"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(int(os.environ.get("CYC_CPU_FRAMES", "512")), os.cpu_count() or 1, x)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_init()
+    try:
+        if args.impl == "reference":
+            run_reference(args, ws, rank)
+        else:
+            run_ours(args, ws, rank, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

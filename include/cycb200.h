@@ -163,6 +163,16 @@ int64_t cyc_data_error_index(const cyc_est* est);
 
 /* Block until all device work of this handle is complete. */
 int cyc_synchronize(cyc_est* est);
+/* Fresh stream state with the same config and allocations: equivalent to
+ * destroying and re-creating the estimator (a new CyclicCorrelator(cfg)). */
+int cyc_reset(cyc_est* est);
+/* Fold-kernel timing with CUDA events on the handle's compute stream:
+ * launches, total kernel milliseconds and algorithmic FP32 flops
+ * (8 per requested lag per folded sample, both flags). */
+int cyc_profile_enable(cyc_est* est, int on);
+int cyc_profile_read(cyc_est* est, uint64_t* launches, double* ms, double* flops);
+/* FP32 FFMA throughput of `device`, TFLOP/s (roofline denominator). */
+double cyc_measure_fp32_peak(int device);
 /* The handle's compute stream (cudaStream_t as void*), for event timing. */
 void* cyc_stream(cyc_est* est);
 /* Kernel launches issued by this handle so far (instrumentation). */

@@ -139,6 +139,11 @@ def lib() -> C.CDLL:
     L.cyc_build_info.restype = C.c_char_p
     L.cyc_compute_set_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_int, C.c_uint64, vp,
                                          C.c_char_p, sz]
+    L.cyc_reset.argtypes = [vp]
+    L.cyc_profile_enable.argtypes = [vp, C.c_int]
+    L.cyc_profile_read.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.cyc_measure_fp32_peak.argtypes = [C.c_int]
+    L.cyc_measure_fp32_peak.restype = C.c_double
     L.cyc_compute_full_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_uint64, vp, C.c_char_p, sz]
     _lib = L
     return L
@@ -412,6 +417,19 @@ class CyclicCorrelator:
     def synchronize(self):
         self._check(self._L.cyc_synchronize(self._h))
 
+    def reset(self):
+        """Fresh stream state (same as constructing a new estimator with this config)."""
+        self._check(self._L.cyc_reset(self._h))
+
+    def profile(self, on: bool = True):
+        self._L.cyc_profile_enable(self._h, int(on))
+
+    def profile_read(self):
+        """(fold launches, fold kernel ms, algorithmic fold flops) so far."""
+        n, ms, fl = C.c_uint64(), C.c_double(), C.c_double()
+        self._check(self._L.cyc_profile_read(self._h, C.byref(n), C.byref(ms), C.byref(fl)))
+        return int(n.value), float(ms.value), float(fl.value)
+
     def _on_frame(self, user, view):
         v = view.contents
         vals = np.ctypeslib.as_array(v.values, shape=(2 * v.len,)).view(np.complex128).copy()
@@ -471,6 +489,11 @@ class CyclicCorrelator:
             self.close()
         except Exception:
             pass
+
+
+def measure_fp32_peak(device: int = 0) -> float:
+    """FP32 FFMA TFLOP/s of the device (fold-kernel roofline denominator)."""
+    return float(lib().cyc_measure_fp32_peak(int(device)))
 
 
 def average_frames(frames: Sequence[CyclicFrame], mode: AverageMode = AverageMode.Coherent) -> np.ndarray:

@@ -217,3 +217,29 @@ int cyc_compute_full_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* y
 }
 
 }  // extern "C"
+
+namespace cyc {
+double measure_fp32_peak_tflops(int device);
+}
+
+extern "C" {
+
+int cyc_reset(cyc_est* est) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->reset());
+}
+
+int cyc_profile_enable(cyc_est* est, int on) {
+    if (!est) return CYC_ERR_USAGE;
+    est->e->set_profiling(on != 0);
+    return CYC_OK;
+}
+
+int cyc_profile_read(cyc_est* est, uint64_t* launches, double* ms, double* flops) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->profile_read(launches, ms, flops));
+}
+
+double cyc_measure_fp32_peak(int device) { return cyc::measure_fp32_peak_tflops(device); }
+
+}  // extern "C"

@@ -348,7 +348,8 @@ Status Engine::init(const Cfg& cfg) {
         use_fold_ = find_grid(c_.alphas, P_, k);
     }
     // fold geometry
-    const int span = lag_hi_ - lag_lo_ + 1;
+    f_lo_ = lag_lo_ - (((lag_lo_ % 2) + 2) % 2);  // even fold origin: 16-byte pair staging
+    const int span = lag_hi_ - f_lo_ + 1;
     lw_ = span <= 16 ? 2 : (span <= 32 ? 4 : 8);
     TB_ = fold_tb(lw_);
     RB_ = fold_rb(lw_);
@@ -618,6 +619,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs, double* S) {
     while (g0 < groups.size()) {
         std::vector<FoldTile> tiles;
         std::vector<FoldGroup> fg;
+        double launch_flops = 0.0;  // algorithmic: 4 FMA per (requested lag, sample), both flags
         size_t g = g0;
         for (; g < groups.size(); ++g) {
             const G& gr = groups[g];
@@ -631,21 +633,32 @@ Status Engine::fold(const std::vector<FoldSeg>& segs, double* S) {
             }
             G2.t1 = (int)tiles.size();
             fg.push_back(G2);
+            const FoldSeg& sg = segs[gr.seg];
+            launch_flops += 8.0 * T_ * (double)(sg.n_end - sg.n_start) / ((double)n_rb_ * n_lb_);
         }
         TRY(ensure_partials(tiles.size() * (size_t)TB_ * RB_ * sizeof(float4)));
         FoldLaunch L{};
-        L.segs = (const FoldSeg*)upload(segs.data(), segs.size() * sizeof(FoldSeg));
+        std::vector<FoldSeg> sg(segs);
+        for (auto& g : sg)
+            g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
+        L.segs = (const FoldSeg*)upload(sg.data(), sg.size() * sizeof(FoldSeg));
         L.tiles = (const FoldTile*)upload(tiles.data(), tiles.size() * sizeof(FoldTile));
         L.groups = (const FoldGroup*)upload(fg.data(), fg.size() * sizeof(FoldGroup));
         L.n_tiles = (int)tiles.size();
         L.n_groups = (int)fg.size();
         L.Pf = (int)Pf_;
-        L.lag_lo = lag_lo_;
+        L.lag_lo = f_lo_;
         L.t_pad = t_pad_;
         L.lw = lw_;
         L.partials = partials_;
         L.S = S;
-        launch_fold(L, cs_);
+        if (prof_) {
+            ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
+            launch_fold(L, cs_, r.a, r.b);
+            prof_pending_.push_back(r);
+        } else {
+            launch_fold(L, cs_);
+        }
         launches_ += 2;
         g0 = g;
     }
@@ -657,7 +670,7 @@ Status Engine::finalize(const double* S, int nslots, double scale, const std::ve
     std::vector<FinalRow> rows;
     rows.reserve((size_t)nslots * T_);
     for (int s = 0; s < nslots; ++s)
-        for (int t = 0; t < T_; ++t) rows.push_back({s, lags_req_[t] - lag_lo_, t, s});
+        for (int t = 0; t < T_; ++t) rows.push_back({s, lags_req_[t] - f_lo_, t, s});
     FinalizeLaunch L{};
     L.S = S;
     L.t_pad = t_pad_;
@@ -935,6 +948,8 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         CK(cudaMemcpyAsync(ring_y_, ring_x_, (size_t)C * cap_ * sizeof(float2), cudaMemcpyDeviceToDevice, cs_));
         cross_ = true;
     }
+    if (kind == IN_DEVICE_F32 && !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_)
+        return push_device_zero_copy((const float2*)xv, (const float2*)yv, n);
     const bool pinned = kind == IN_HOST_F32 && is_pinned(xv) && (!yv || is_pinned(yv));
     if (kind != IN_DEVICE_F32 && !pinned && stage_len_ < (size_t)Q_) {
         for (int i = 0; i < 2; ++i) {
@@ -1024,6 +1039,74 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     return cuda_check(cudaGetLastError(), "push");
 }
 
+// Device-resident block-mode push: frames whose x window lies inside the new
+// chunk are folded straight from the caller's device buffer; only the head
+// (frames straddling the previous chunk) and the tail (history for the next
+// chunk) are copied into the rings.
+Status Engine::push_device_zero_copy(const float2* x, const float2* y, size_t n) {
+    const int C = c_.channels;
+    const int64_t c0 = (int64_t)consumed_, c1 = c0 + (int64_t)n;
+    const int64_t keep = std::min<int64_t>((int64_t)n, (int64_t)need_ + N_);
+    wait_ring_free(c1);
+    for (int ch = 0; ch < C; ++ch) {
+        const float2* xs = x + (size_t)ch * n;
+        const float2* ys = (y ? y : x) + (size_t)ch * n;
+        launch_ring_write(ring_x_ + (size_t)ch * cap_, mask_, c0, xs, keep, xs_);
+        launch_ring_write(ring_x_ + (size_t)ch * cap_, mask_, c1 - keep, xs + (n - keep), keep, xs_);
+        launches_ += 2;
+        if (cross_) {
+            launch_ring_write(ring_y_ + (size_t)ch * cap_, mask_, c0, ys, keep, xs_);
+            launch_ring_write(ring_y_ + (size_t)ch * cap_, mask_, c1 - keep, ys + (n - keep), keep, xs_);
+            launches_ += 2;
+        }
+    }
+    cudaEvent_t ev = get_event();
+    CK(cudaEventRecord(ev, xs_));
+    CK(cudaStreamWaitEvent(cs_, ev, 0));
+    ev_pool_.push_back(ev);
+    consumed_ = (uint64_t)c1;
+    const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
+    if (avail > frames_) {
+        const int64_t s = (int64_t)m_minus_ + (int64_t)frames_ * N_;
+        const int64_t e = (int64_t)m_minus_ + (int64_t)avail * N_;
+        const int64_t split = std::max(c0, c0 - (int64_t)lag_lo_);
+        std::vector<FoldSeg> ring_segs, user_segs;
+        for (int ch = 0; ch < C; ++ch) {
+            FoldSeg g{};
+            g.w_log2 = 0.f;
+            g.w_scale = 1.f;
+            g.slot = ch;
+            if (s < std::min(e, split)) {
+                g.x = ring_x_ + (size_t)ch * cap_;
+                g.y = (cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_;
+                g.n_start = s;
+                g.n_end = std::min(e, split);
+                g.x_lo = g.n_start + lag_lo_;
+                g.x_hi = g.n_end + lag_hi_;
+                g.mask = mask_;
+                ring_segs.push_back(g);
+            }
+            if (std::max(s, split) < e) {
+                g.x = x + (size_t)ch * n - c0;
+                g.y = (y ? y : x) + (size_t)ch * n - c0;
+                g.n_start = std::max(s, split);
+                g.n_end = e;
+                g.x_lo = c0;
+                g.x_hi = c1;
+                g.mask = ~0ull;
+                user_segs.push_back(g);
+            }
+        }
+        TRY(fold(ring_segs, S_main_));
+        TRY(fold(user_segs, S_main_));
+        mark_read(s + lag_lo_);
+        frames_ = avail;
+    }
+    // the caller's device buffer may not be retained after return
+    CK(cudaStreamSynchronize(cs_));
+    return cuda_check(cudaGetLastError(), "push_device");
+}
+
 // ---------------------------------------------------------------------------
 // averages (estimator.cpp:86-105)
 // ---------------------------------------------------------------------------
@@ -1090,7 +1173,12 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
     const double scale = invF / (double)N_;
     if (use_fold_) {
         const double* S = S_main_ + (size_t)channel * t_pad_ * Pf_ * 4;
-        TRY(finalize(S, 1, scale, nullptr, avg_dev_));
+        // both flag tables come out of one finalize; reuse it until new frames arrive
+        if (!(avg_cache_frames_ == frames_ && avg_cache_channel_ == channel)) {
+            TRY(finalize(S, 1, scale, nullptr, avg_dev_));
+            avg_cache_frames_ = frames_;
+            avg_cache_channel_ = channel;
+        }
         CK(cudaMemcpyAsync(tmp.data(), avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
                            cudaMemcpyDeviceToHost, cs_));
         CK(cudaStreamSynchronize(cs_));
@@ -1138,6 +1226,52 @@ Status Engine::compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64*
         out[i].re = r[i].x;
         out[i].im = r[i].y;
     }
+    return Status::ok();
+}
+
+cudaEvent_t Engine::get_event_timed() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+Status Engine::profile_read(uint64_t* launches, double* ms, double* flops) {
+    CK(cudaStreamSynchronize(cs_));
+    for (auto& r : prof_pending_) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, r.a, r.b));
+        prof_ms_ += t;
+        prof_flops_ += r.flops;
+        ++prof_launches_;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    prof_pending_.clear();
+    if (launches) *launches = prof_launches_;
+    if (ms) *ms = prof_ms_;
+    if (flops) *flops = prof_flops_;
+    return Status::ok();
+}
+
+Status Engine::reset() {
+    CK(cudaSetDevice(c_.device));
+    CK(cudaStreamSynchronize(xs_));
+    CK(cudaStreamSynchronize(cs_));
+    const size_t lay_all = (size_t)c_.channels * nflags_ * layout_len_;
+    if (S_main_) CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
+    if (dsum_main_) CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
+    if (coh_) CK(cudaMemsetAsync(coh_, 0, lay_all * sizeof(double2), cs_));
+    if (mag_) CK(cudaMemsetAsync(mag_, 0, lay_all * sizeof(double), cs_));
+    std::fill(rec_R_.begin(), rec_R_.end(), 0.0);
+    std::fill(host_coh_.begin(), host_coh_.end(), 0.0);
+    std::fill(host_mag_.begin(), host_mag_.end(), 0.0);
+    for (auto& m : reads_) ev_pool_.push_back(m.ev);
+    reads_.clear();
+    consumed_ = 0;
+    frames_ = 0;
+    avg_cache_frames_ = ~0ull;
+    avg_cache_channel_ = -1;
+    CK(cudaStreamSynchronize(cs_));
     return Status::ok();
 }
 

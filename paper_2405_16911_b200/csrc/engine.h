@@ -66,6 +66,11 @@ public:
     Status compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw, size_t yw_len,
                           uint64_t k0, cyc_cf64* out);
     Status synchronize();
+    // Fresh stream state, same config and allocations (== a new CyclicCorrelator(cfg)).
+    Status reset();
+    // Fold-kernel timing with CUDA events on the compute stream.
+    void set_profiling(bool on) { prof_ = on; }
+    Status profile_read(uint64_t* launches, double* ms, double* flops);
 
     size_t buffer_need() const { return need_; }
     uint64_t consumed() const { return consumed_; }
@@ -115,6 +120,7 @@ private:
     std::vector<int> lags_req_;  // output lags ascending
     int T_ = 0;
     int lag_lo_ = 0, lag_hi_ = 0;
+    int f_lo_ = 0;  // fold lag origin (lag_lo_ rounded down to even)
     int m_plus_ = 0, m_minus_ = 0;
     size_t need_ = 0;
     int64_t N_ = 0;  // hop (win_len or emission interval)
@@ -182,8 +188,26 @@ private:
     std::deque<ReadMark> reads_;
     std::vector<cudaEvent_t> ev_pool_;
     cudaEvent_t get_event();
+    cudaEvent_t get_event_timed();
     void mark_read(int64_t lo);
     void wait_ring_free(int64_t abs_end);
+
+    // ---- profiling ----
+    struct ProfRec {
+        cudaEvent_t a, b;
+        double flops;
+    };
+    bool prof_ = false;
+    std::vector<ProfRec> prof_pending_;
+    uint64_t prof_launches_ = 0;
+    double prof_ms_ = 0.0, prof_flops_ = 0.0;
+
+    // device-resident push without a ring copy of the bulk
+    Status push_device_zero_copy(const float2* x, const float2* y, size_t n);
+
+    // finalize cache of the block average (frames count, channel)
+    uint64_t avg_cache_frames_ = ~0ull;
+    int avg_cache_channel_ = -1;
 
     // ---- streaming state (estimator.hpp:117-136) ----
     uint64_t consumed_ = 0;

@@ -1,6 +1,6 @@
 // fold.cu -- the hot kernel: lag products folded over residues n mod Pf.
 //
-// For every requested lag tau and residue r it accumulates the four real
+// For every computed lag tau and residue r it accumulates the four real
 // correlations
 //     c0 = sum xr*yr,  c1 = sum xi*yr,  c2 = sum xr*yi,  c3 = sum xi*yi
 // over n = r (mod Pf), x = x[n+tau], y = y[n].  Both cyclic functions follow:
@@ -12,14 +12,17 @@
 // finalize DFT (exact reassociation: every alpha is k/P and Pf is a multiple
 // of P).
 //
-// CTA = 8 warps.  A thread owns R=4 consecutive residues x U=8 consecutive
-// lags (128 fp32 accumulators, issued as packed FFMA2).  Sample windows are
-// staged per fold period by cp.async into shared memory in a "phase-split by
-// 4" layout E[s & 3][s >> 2] so the sliding register windows of neighbouring
-// lanes hit consecutive 8-byte words (conflict-free), and y reads are
-// broadcast across the lag lanes of a warp.  Per period a thread issues 15
-// LDS.64 for 64 FFMA2 (128 FMAs).  Partial sums leave the CTA in fp32 and are
-// reduced in fp64 in a fixed order (deterministic; SURVEY §7 "Hard parts").
+// CTA = 8 warps, 1 CTA/SM (~215 registers).  A thread owns R=4 consecutive
+// residues x U=8 consecutive lags = 128 fp32 accumulators, updated with packed
+// FFMA2 (y broadcast as the scalar operand).  Sample windows are staged per
+// fold period by 16-byte cp.async into a "pair, phase-split by 2" layout
+//     X[b][c] = (x[4c+2b], x[4c+2b+1])        (float4)
+// so a thread's sliding window x[4k .. 4k+11] is 6 LDS.128 at consecutive
+// addresses across lanes (conflict-free), and its 4 y samples are 2 LDS.128
+// broadcast across the lag lanes.  Per period a thread issues 8 LDS.128 for
+// 64 FFMA2 (128 FMAs); the next period's registers are loaded while the
+// current one is multiplied.  Partial sums leave the CTA in fp32 and are
+// reduced in fp64 in a fixed order (deterministic).
 #include "kernels.cuh"
 
 namespace cyc {
@@ -29,25 +32,31 @@ constexpr int NW = 8;
 constexpr int NT = NW * 32;
 constexpr int R = 4;
 constexpr int U = 8;
-constexpr int XV = R + U - 1;
 constexpr int NSTAGE = 3;
 
-constexpr int pad4mod16(int c) { return c + ((4 - c % 16) + 16) % 16; }
+constexpr int pad4mod8(int c) { return c + ((4 - c % 8) + 8) % 8; }
 
 template <int LW>
 struct Geo {
-    static constexpr int RL = 32 / LW;       // residue lanes per warp
-    static constexpr int TB = 8 * LW;        // lags per CTA
-    static constexpr int RB = NW * RL * R;   // residues per CTA (= 1024 / LW)
-    static constexpr int XW = RB + TB;       // x samples staged per period
-    static constexpr int XCP = pad4mod16(XW / 4);
-    static constexpr int YCP = pad4mod16(RB / 4);
-    static constexpr int PER = 4 * XCP + 4 * YCP;  // float2 per period
-    static constexpr int PS = LW == 2 ? 4 : 8;     // periods per pipeline stage
+    static constexpr int RL = 32 / LW;           // residue lanes per warp
+    static constexpr int TB = 8 * LW;            // lags per CTA
+    static constexpr int RB = NW * RL * R;       // residues per CTA (= 1024 / LW)
+    static constexpr int XW = RB + TB;           // x samples staged per period
+    static constexpr int XC = pad4mod8(XW / 4);  // float4 per X row
+    static constexpr int YC = pad4mod8(RB / 4);  // float4 per Y row
+    static constexpr int PER = 2 * XC + 2 * YC;  // float4 per period
+    static constexpr int NX = XW / 2;            // x pairs per period
+    static constexpr int NY = RB / 2;            // y pairs per period
+    static constexpr int EPP = NX + NY;          // staged pairs per period
+    static constexpr int PS = LW == 8 ? 16 : (LW == 4 ? 8 : 4);  // periods per stage
     static constexpr int STAGE = PS * PER;
-    static constexpr int SMEM = NSTAGE * STAGE * 8;
+    static constexpr int SMEM = NSTAGE * STAGE * 16;
+    static constexpr int EPT = (PS * EPP + NT - 1) / NT;  // staged pairs per thread per stage
 };
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, int bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
 }
@@ -60,7 +69,7 @@ union F2U {
     unsigned long long u;
 };
 
-// acc += a * (b, b)  -- packed fp32x2 FMA (SASS FFMA2)
+// acc += a * (b, b)  -- packed fp32x2 FMA (SASS FFMA2 with a scalar operand)
 __device__ __forceinline__ void ffma2_bcast(float2& acc, float2 a, float b) {
     F2U A, B, C;
     A.f = a;
@@ -70,53 +79,146 @@ __device__ __forceinline__ void ffma2_bcast(float2& acc, float2 a, float b) {
     acc = C.f;
 }
 
+struct Regs {
+    float4 x[6];  // x[4k .. 4k+11] as pairs
+    float4 y[2];  // y[4rho .. 4rho+3] as pairs
+};
+
+template <int LW>
+__device__ __forceinline__ void load_period(Regs& r, const float4* per, int kap, int rho) {
+    using G = Geo<LW>;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) r.x[j] = per[(j & 1) * G::XC + kap + (j >> 1)];
+    r.y[0] = per[2 * G::XC + rho];
+    r.y[1] = per[2 * G::XC + G::YC + rho];
+}
+
+__device__ __forceinline__ void mac_period(float2 (&lo)[R][U], float2 (&hi)[R][U], const Regs& r) {
+    float2 xv[12];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        xv[2 * j] = make_float2(r.x[j].x, r.x[j].y);
+        xv[2 * j + 1] = make_float2(r.x[j].z, r.x[j].w);
+    }
+    const float yr[4] = {r.y[0].x, r.y[0].z, r.y[1].x, r.y[1].z};
+    const float yi[4] = {r.y[0].y, r.y[0].w, r.y[1].y, r.y[1].w};
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ffma2_bcast(lo[a][u], xv[a + u], yr[a]);
+            ffma2_bcast(hi[a][u], xv[a + u], yi[a]);
+        }
+}
+
+// recursive mode: y[n] *= w_scale * 2^{(w_ref - n) * w_log2}
+__device__ __forceinline__ void weight_period(Regs& r, const FoldSeg& seg, int64_t nb) {
+    float w[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) w[a] = seg.w_scale * exp2f((float)(seg.w_ref - (nb + a)) * seg.w_log2);
+    r.y[0].x *= w[0];
+    r.y[0].y *= w[0];
+    r.y[0].z *= w[1];
+    r.y[0].w *= w[1];
+    r.y[1].x *= w[2];
+    r.y[1].y *= w[2];
+    r.y[1].z *= w[3];
+    r.y[1].w *= w[3];
+}
+
 template <int LW>
 __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
     using G = Geo<LW>;
-    extern __shared__ __align__(16) float2 smem[];
+    extern __shared__ __align__(16) float4 smem4[];
     const FoldTile tile = L.tiles[blockIdx.x];
     const FoldSeg seg = L.segs[tile.seg];
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int rho = warp * G::RL + (lane % G::RL);  // residue group: residues 4*rho .. 4*rho+3
-    const int lam = lane / G::RL;                   // lag group: lags 8*lam .. 8*lam+7
+    const int rho = warp * G::RL + (lane % G::RL);  // residues 4*rho .. 4*rho+3
+    const int lam = lane / G::RL;                   // lags 8*lam .. 8*lam+7
+    const int kap = rho + 2 * lam;                  // x window starts at 4*kap
 
     const int64_t Pf = L.Pf;
     const int64_t res0 = (int64_t)tile.rb * G::RB;
     const int64_t xoff = res0 + L.lag_lo + (int64_t)tile.lb * G::TB;
-    const int64_t nper = tile.p1 - tile.p0;
-    const int nstages = (int)((nper + G::PS - 1) / G::PS);
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const int nper = (int)(tile.p1 - tile.p0);
+    const int nstages = (nper + G::PS - 1) / G::PS;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem4);
     const uint64_t mask = seg.mask;
+    const bool vec = seg.vec != 0;
+
+    // Fixed per-thread staging assignment (pair e of period q for idx = tid + k*NT),
+    // packed into one word: [0,13) float4 offset in the stage, [13,24) sample
+    // offset in the period window, bit 24 = x (else y), bit 31 = idle.
+    uint32_t st_pack[G::EPT];
+#pragma unroll
+    for (int k = 0; k < G::EPT; ++k) {
+        const int idx = tid + k * NT;
+        const int q = idx / G::EPP;
+        const int e = idx - q * G::EPP;
+        const bool isx = e < G::NX;
+        const int ee = isx ? e : e - G::NX;
+        const int b = ee & 1, c = ee >> 1;
+        const uint32_t dst = (uint32_t)(q * G::PER + (isx ? b * G::XC + c : 2 * G::XC + b * G::YC + c));
+        const uint32_t rel = (uint32_t)(4 * c + 2 * b);
+        st_pack[k] = idx < G::PS * G::EPP ? (dst | (rel << 13) | (isx ? 1u << 24 : 0u)) : 0x80000000u;
+    }
+    static_assert(G::STAGE < (1 << 13) && G::XW < (1 << 11), "staging pack overflow");
 
     auto load_stage = [&](int s) {
         const int64_t pbeg = tile.p0 + (int64_t)s * G::PS;
-        const uint32_t dst0 = sbase + (uint32_t)((s % NSTAGE) * G::STAGE) * 8u;
-        constexpr int EPP = G::XW + G::RB;  // elements per period
-        for (int e = tid; e < G::PS * EPP; e += NT) {
-            const int q = e / EPP;
-            const int sidx = e - q * EPP;
-            const int64_t p = pbeg + q;
-            uint32_t dst = dst0 + (uint32_t)(q * G::PER) * 8u;
-            const float2* src = seg.x;
-            int bytes = 0;
-            if (sidx < G::XW) {
-                const int64_t n = p * Pf + xoff + sidx;
-                dst += (uint32_t)((sidx & 3) * G::XCP + (sidx >> 2)) * 8u;
-                if (p < tile.p1 && n >= seg.x_lo && n < seg.x_hi) {
-                    src = seg.x + ((uint64_t)n & mask);
-                    bytes = 8;
-                }
-            } else {
-                const int sy = sidx - G::XW;
-                const int64_t n = p * Pf + res0 + sy;
-                dst += (uint32_t)(4 * G::XCP + (sy & 3) * G::YCP + (sy >> 2)) * 8u;
-                if (p < tile.p1 && n >= seg.n_start && n < seg.n_end && res0 + sy < Pf) {
-                    src = seg.y + ((uint64_t)n & mask);
-                    bytes = 8;
-                }
+        const uint32_t dst0 = sbase + (uint32_t)((s % NSTAGE) * G::STAGE) * 16u;
+        const int64_t pend = pbeg + G::PS;
+        // stage-uniform fast path: every window of the stage inside the valid ranges
+        const bool fast = vec && pend <= tile.p1 && pbeg * Pf + xoff >= seg.x_lo &&
+                          (pend - 1) * Pf + xoff + G::XW <= seg.x_hi && pbeg * Pf + res0 >= seg.n_start &&
+                          (pend - 1) * Pf + res0 + G::RB <= seg.n_end && res0 + G::RB <= Pf;
+        if (fast) {
+#pragma unroll
+            for (int k = 0; k < G::EPT; ++k) {
+                const uint32_t w = st_pack[k];
+                if (w & 0x80000000u) continue;
+                const uint32_t off = w & 0x1fffu;
+                const int q = (int)(off / G::PER);
+                const bool isx = (w >> 24) & 1u;
+                const int64_t n = (pbeg + q) * Pf + (isx ? xoff : res0) + (int64_t)((w >> 13) & 0x7ffu);
+                cp_async16(dst0 + off * 16u, (isx ? seg.x : seg.y) + ((uint64_t)n & mask), 16);
             }
-            cp_async8(dst, src, bytes);
+            return;
+        }
+#pragma unroll 1
+        for (int k = 0; k < G::EPT; ++k) {
+            const uint32_t w = st_pack[k];
+            if (w & 0x80000000u) continue;
+            const uint32_t off = w & 0x1fffu;
+            const int q = (int)(off / G::PER);
+            const bool isx = (w >> 24) & 1u;
+            const int rel = (int)((w >> 13) & 0x7ffu);
+            const int64_t p = pbeg + q;
+            const uint32_t dst = dst0 + off * 16u;
+            int64_t n, lo, hi;
+            const float2* base;
+            if (isx) {
+                n = p * Pf + xoff + rel;
+                lo = seg.x_lo;
+                hi = seg.x_hi;
+                base = seg.x;
+            } else {
+                n = p * Pf + res0 + rel;
+                lo = seg.n_start;
+                hi = (res0 + rel < Pf) ? seg.n_end : lo;  // masked residue-block tail
+                base = seg.y;
+            }
+            if (p >= tile.p1) hi = lo;
+            const bool v0 = n >= lo && n < hi;
+            const bool v1 = n + 1 >= lo && n + 1 < hi;
+            if (vec && v0 == v1) {
+                cp_async16(dst, v0 ? (const void*)(base + ((uint64_t)n & mask)) : (const void*)base, v0 ? 16 : 0);
+            } else {
+                cp_async8(dst, v0 ? (const void*)(base + ((uint64_t)n & mask)) : (const void*)base, v0 ? 8 : 0);
+                cp_async8(dst + 8, v1 ? (const void*)(base + ((uint64_t)(n + 1) & mask)) : (const void*)base,
+                          v1 ? 8 : 0);
+            }
         }
     };
 
@@ -136,40 +238,29 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
     }
 
     const bool weighted = seg.w_log2 != 0.f;
+    Regs ra, rb;
     for (int s = 0; s < nstages; ++s) {
         cp_async_wait<NSTAGE - 2>();
         __syncthreads();
         if (s + NSTAGE - 1 < nstages) load_stage(s + NSTAGE - 1);
         cp_async_commit();
 
-        const float2* st = smem + (s % NSTAGE) * G::STAGE;
+        const float4* st = smem4 + (s % NSTAGE) * G::STAGE;
         const int64_t pbeg = tile.p0 + (int64_t)s * G::PS;
-        const int nq = (int)min((int64_t)G::PS, tile.p1 - pbeg);
-        for (int q = 0; q < nq; ++q) {
-            const float2* Ex = st + q * G::PER;
-            const float2* Ey = Ex + 4 * G::XCP;
-            float2 xv[XV];
-#pragma unroll
-            for (int i = 0; i < XV; ++i) xv[i] = Ex[(i & 3) * G::XCP + rho + 2 * lam + (i >> 2)];
-            float2 yv[R];
-#pragma unroll
-            for (int a = 0; a < R; ++a) yv[a] = Ey[a * G::YCP + rho];
-            if (weighted) {
-                const int64_t nb = (pbeg + q) * Pf + res0 + 4 * rho;
-#pragma unroll
-                for (int a = 0; a < R; ++a) {
-                    const float w = seg.w_scale * exp2f((float)(seg.w_ref - (nb + a)) * seg.w_log2);
-                    yv[a].x *= w;
-                    yv[a].y *= w;
-                }
-            }
-#pragma unroll
-            for (int a = 0; a < R; ++a)
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    ffma2_bcast(lo[a][u], xv[a + u], yv[a].x);
-                    ffma2_bcast(hi[a][u], xv[a + u], yv[a].y);
-                }
+        const int nq = min(G::PS, nper - s * G::PS);
+        load_period<LW>(ra, st, kap, rho);
+        int q = 0;
+        for (; q + 1 < nq; q += 2) {
+            load_period<LW>(rb, st + (q + 1) * G::PER, kap, rho);
+            if (weighted) weight_period(ra, seg, (pbeg + q) * Pf + res0 + 4 * rho);
+            mac_period(lo, hi, ra);
+            if (q + 2 < nq) load_period<LW>(ra, st + (q + 2) * G::PER, kap, rho);
+            if (weighted) weight_period(rb, seg, (pbeg + q + 1) * Pf + res0 + 4 * rho);
+            mac_period(lo, hi, rb);
+        }
+        if (q < nq) {
+            if (weighted) weight_period(ra, seg, (pbeg + q) * Pf + res0 + 4 * rho);
+            mac_period(lo, hi, ra);
         }
     }
     cp_async_wait<0>();
@@ -211,26 +302,28 @@ __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
 }
 
 template <int LW>
-void run_fold(const FoldLaunch& L, cudaStream_t st) {
+void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
     using G = Geo<LW>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(fold_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         attr_set = true;
     }
+    if (ev0) cudaEventRecord(ev0, st);
     fold_kernel<LW><<<L.n_tiles, NT, G::SMEM, st>>>(L);
+    if (ev1) cudaEventRecord(ev1, st);
     dim3 rg((G::TB * G::RB + 255) / 256, L.n_groups);
     fold_reduce_kernel<<<rg, 256, 0, st>>>(L, G::TB, G::RB);
 }
 
 }  // namespace
 
-void launch_fold(const FoldLaunch& L, cudaStream_t st) {
+void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
     if (L.n_tiles == 0) return;
     switch (L.lw) {
-        case 2: run_fold<2>(L, st); break;
-        case 4: run_fold<4>(L, st); break;
-        default: run_fold<8>(L, st); break;
+        case 2: run_fold<2>(L, st, ev0, ev1); break;
+        case 4: run_fold<4>(L, st, ev0, ev1); break;
+        default: run_fold<8>(L, st, ev0, ev1); break;
     }
 }
 

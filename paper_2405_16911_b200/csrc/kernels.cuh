@@ -34,7 +34,7 @@ struct FoldSeg {
     float w_log2;        // 0 => unweighted
     float w_scale;
     int slot;
-    int pad;
+    int vec;             // 1: x/y bases 16-byte aligned and window starts even (16-B cp.async)
 };
 
 // A CTA's unit of work: one (segment, residue block, lag block) over the
@@ -64,7 +64,8 @@ struct FoldLaunch {
     double* S;           // [slots][t_pad][Pf][4] fp64 accumulators
 };
 
-void launch_fold(const FoldLaunch& L, cudaStream_t st);   // fold + fp64 reduce
+// fold + fp64 reduce; optional events bracket the fold kernel alone (profiling)
+void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 inline int fold_tb(int lw) { return 8 * lw; }
 inline int fold_rb(int lw) { return 1024 / lw; }

@@ -72,3 +72,53 @@ void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* 
 }
 
 }  // namespace cyc
+
+// ---------------------------------------------------------------------------
+// FP32 FFMA peak microbenchmark: the roofline denominator for the fold kernel
+// (MEASURED_PEAKS.json only carries HBM and bf16 tensor peaks).  16
+// independent FMA chains per thread, 4 CTAs x 256 threads per SM.
+// ---------------------------------------------------------------------------
+namespace cyc {
+namespace {
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, float a, float b, int iters) {
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = fmaf(acc[i], a, b);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+
+double measure_fp32_peak_tflops(int device) {
+    cudaSetDevice(device);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int grid = sms * 4, block = 256, iters = 20000;
+    float* out = nullptr;
+    if (cudaMalloc(&out, (size_t)grid * block * sizeof(float)) != cudaSuccess) return 0.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(e0);
+        ffma_peak_kernel<<<grid, block>>>(out, 1.0001f, 0.999f, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 2.0 * 16 * iters * (double)grid * block;
+    return flops / (best * 1e-3) / 1e12;
+}
+}  // namespace cyc
