@@ -66,44 +66,52 @@ def config_block(n_gpus: int):
 
 # ---------------------------------------------------------------------------
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    clocks line).  NVML is polled every ~2 ms from a thread (nvidia-smi's 100 ms
+    floor cannot resolve a region of a few ms)."""
+
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+        0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
 
     def __init__(self, index: int):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
+        self.samples, self.reasons, self.smax = [], set(), None
+        self._stop = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.nv = None
+            self.err = str(e)
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.002)
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.seek(0)
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().strip().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        os.unlink(self.f.name)
-        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable"}
+        self._stop.set()
+        self.t.join()
+        sm = self.samples
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": "NVML poll ~2 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -187,7 +195,7 @@ def run_reference(args, ws, rank):
     from paper_2405_16911_b200 import siggen
     x = siggen.c2_record(seed=2, n=L_REC)
     threads = os.cpu_count() or 1
-    frames = int(os.environ.get("CYC_REF_FRAMES", "1024"))
+    frames = int(os.environ.get("CYC_REF_FRAMES", "4096"))  # ~1/4 of the record per step
     for _ in range(args.warmup if args.warmup < 1 else 1):
         cpu_baseline(64, threads, x)
     vals = []
@@ -221,12 +229,14 @@ def run_ours(args, ws, rank, local):
     dx = torch.from_numpy(x.view(np.float32)).to(f"cuda:{dev}")
     ptr = dx.data_ptr()
 
+    out_conv = np.zeros(A * LAGS, dtype=np.complex128)
+    out_conj = np.zeros(A * LAGS, dtype=np.complex128)
+
     def step_device():
         est.reset()
         est.push_device(ptr, L_REC)
-        a = est.average(flag=cyc.Flags.CONV)
-        b = est.average(flag=cyc.Flags.CONJ)
-        return a, b
+        est.average(flag=cyc.Flags.CONV, out=out_conv)
+        est.average(flag=cyc.Flags.CONJ, out=out_conj)
 
     px = cyc.host_alloc(x.shape)
     px[:] = x
@@ -234,9 +244,8 @@ def run_ours(args, ws, rank, local):
     def step_e2e():
         est.reset()
         est.push(px)
-        a = est.average(flag=cyc.Flags.CONV)
-        b = est.average(flag=cyc.Flags.CONJ)
-        return a, b
+        est.average(flag=cyc.Flags.CONV, out=out_conv)
+        est.average(flag=cyc.Flags.CONJ, out=out_conj)
 
     def timed(fn, k):
         barrier(ws)
@@ -302,7 +311,8 @@ def run_ours(args, ws, rank, local):
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(int(os.environ.get("CYC_CPU_FRAMES", "512")), os.cpu_count() or 1, x)
+        # the whole C2 record (16383 frames; ~10-15 s on 16 host cores)
+        line["cpu_baseline"] = cpu_baseline(int(os.environ.get("CYC_CPU_FRAMES", "16383")), os.cpu_count() or 1, x)
     print(json.dumps(line), flush=True)
 
 

@@ -473,9 +473,14 @@ class CyclicCorrelator:
         return out
 
     def average(self, mode: AverageMode = AverageMode.Coherent, flag: Optional[int] = None,
-                channel: int = 0) -> np.ndarray:
-        """average_frames over every frame emitted so far (estimator.cpp:86-105)."""
-        out = np.zeros(layout_len(self._layout), dtype=np.complex128)
+                channel: int = 0, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """average_frames over every frame emitted so far (estimator.cpp:86-105).
+        `out` (complex128, layout_len) may be passed to reuse a buffer."""
+        n = layout_len(self._layout)
+        if out is None:
+            out = np.empty(n, dtype=np.complex128)
+        elif out.dtype != np.complex128 or out.size != n or not out.flags.c_contiguous:
+            raise UsageError("out must be a contiguous complex128 array of layout_len values")
         self._check(self._L.cyc_average(self._h, int(mode), int(flag or 0), int(channel), out.ctypes.data))
         return out
 

@@ -414,6 +414,7 @@ Status Engine::init(const Cfg& cfg) {
         host_mag_.assign(lay_all, 0.0);
     }
     CK(cudaMalloc(&avg_dev_, (size_t)nflags_ * layout_len_ * sizeof(double2)));
+    CK(cudaMallocHost(&avg_host_, layout_len_ * sizeof(double2)));
     if (use_fold_) {
         std::vector<double2> tw(Pf_);
         for (int64_t j = 0; j < Pf_; ++j) {
@@ -451,6 +452,7 @@ Engine::~Engine() {
     cudaFree(coh_);
     cudaFree(mag_);
     cudaFree(avg_dev_);
+    cudaFreeHost(avg_host_);
     cudaFree(partials_);
     cudaFree(tw_);
     cudaFree(bins_dev_);
@@ -459,6 +461,8 @@ Engine::~Engine() {
     cudaFree(key_dev_);
     cudaFreeHost(key_host_);
     cudaFree(dev_tmp_);
+    cudaFree(S_pend_);
+    cudaFree(hist_bak_);
     cudaFreeHost(meta_host_);
     cudaFree(meta_dev_);
     for (int i = 0; i < META_SLOTS; ++i)
@@ -798,7 +802,7 @@ Status Engine::deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const 
 }
 
 // Emit every frame that became computable (estimator.cpp:59-82).
-Status Engine::emit_new_frames(cyc_frame_sink sink, void* user) {
+Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target) {
     const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
     if (avail <= frames_) return Status::ok();
     const uint64_t f0 = frames_, f1 = avail;
@@ -866,7 +870,7 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user) {
             g.w_scale = 1.f;
             g.slot = ch;
         }
-        TRY(fold(segs, S_main_));
+        TRY(fold(segs, S_target ? S_target : S_main_));
     } else {
         std::vector<DirectSeg> segs(C);
         for (int ch = 0; ch < C; ++ch) {
@@ -907,39 +911,35 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         return s;
     }
     const int C = c_.channels;
-    // 1. whole-chunk validation before any state change (estimator.cpp:43-52)
-    Bad bad;
-    if (kind == IN_HOST_F32) {
-        bad = scan_bad((const cyc_cf32*)xv, (const cyc_cf32*)yv, n, C);
-    } else if (kind == IN_HOST_F64) {
-        bad = scan_bad((const cyc_cf64*)xv, (const cyc_cf64*)yv, n, C);
-    } else {
-        *key_host_ = ~0ull;
-        CK(cudaMemcpyAsync(key_dev_, key_host_, sizeof(unsigned long long), cudaMemcpyHostToDevice, cs_));
-        for (int ch = 0; ch < C; ++ch) {
-            // per channel, keys are per-sample; channel resolution done below
-            launch_finite_check((const float2*)xv + (size_t)ch * n, yv ? (const float2*)yv + (size_t)ch * n : nullptr,
-                                (int64_t)n, key_dev_, cs_);
-            launches_ += 1;
+    const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
+    const bool pinned = kind == IN_HOST_F32 && is_pinned(xv) && (!yv || is_pinned(yv));
+    // Block-mode pushes from pinned or device memory validate on the GPU while
+    // they are folded into a pending accumulator; the push commits only if the
+    // whole chunk was finite, otherwise the state is rolled back
+    // (estimator.cpp:43-52 semantics: reject whole, state unchanged).
+    const bool speculative = block_fold && (pinned || kind == IN_DEVICE_F32);
+    if (!speculative) {
+        // whole-chunk validation before any state change (estimator.cpp:43-52)
+        Bad bad;
+        if (kind == IN_HOST_F32) {
+            bad = scan_bad((const cyc_cf32*)xv, (const cyc_cf32*)yv, n, C);
+        } else if (kind == IN_HOST_F64) {
+            bad = scan_bad((const cyc_cf64*)xv, (const cyc_cf64*)yv, n, C);
+        } else {
+            CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
+            for (int ch = 0; ch < C; ++ch) {
+                launch_finite_check((const float2*)xv + (size_t)ch * n, yv ? (const float2*)yv + (size_t)ch * n : nullptr,
+                                    (int64_t)n, 0, C, ch, key_dev_, cs_);
+                launches_ += 1;
+            }
+            CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs_));
+            CK(cudaStreamSynchronize(cs_));
+            if (*key_host_ != ~0ull) {
+                bad.key = *key_host_ / C;
+                bad.channel = (int)(*key_host_ % C);
+            }
         }
-        CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs_));
-        CK(cudaStreamSynchronize(cs_));
-        bad.key = *key_host_;
-    }
-    if (bad.key != ~0ull) {
-        const uint64_t i = bad.key >> 1;
-        Status s;
-        s.code = CYC_ERR_DATA;
-        s.index = (int64_t)(consumed_ + i);
-        bool range = false;
-        if (kind == IN_HOST_F64) {
-            const cyc_cf64* p = (const cyc_cf64*)((bad.key & 1) ? yv : xv) + (size_t)bad.channel * n + i;
-            range = std::isfinite(p->re) && std::isfinite(p->im);
-        }
-        s.msg = std::string(range ? "sample outside the float32 range" : "non-finite sample") + " at absolute index " +
-                std::to_string(consumed_ + i) + " in " + ((bad.key & 1) ? "y" : "x") + " stream";
-        if (C > 1) s.msg += " of channel " + std::to_string(bad.channel);
-        return s;
+        if (bad.key != ~0ull) return data_error(bad.key, bad.channel, kind, xv, yv, n);
     }
     // cross-correlation: materialise a y ring (copy x history on first use)
     if (yv && !cross_) {
@@ -948,102 +948,211 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         CK(cudaMemcpyAsync(ring_y_, ring_x_, (size_t)C * cap_ * sizeof(float2), cudaMemcpyDeviceToDevice, cs_));
         cross_ = true;
     }
-    if (kind == IN_DEVICE_F32 && !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_)
-        return push_device_zero_copy((const float2*)xv, (const float2*)yv, n);
-    const bool pinned = kind == IN_HOST_F32 && is_pinned(xv) && (!yv || is_pinned(yv));
-    if (kind != IN_DEVICE_F32 && !pinned && stage_len_ < (size_t)Q_) {
-        for (int i = 0; i < 2; ++i) {
-            if (stage_[i]) {
-                cudaEventSynchronize(stage_ev_[i]);
-                cudaFreeHost(stage_[i]);
-                cudaFreeHost(stage_y_[i]);
-                stage_y_[i] = nullptr;
-            }
-            CK(cudaMallocHost(&stage_[i], (size_t)C * Q_ * sizeof(float2)));
-            stage_ev_live_[i] = false;
-        }
-        stage_len_ = (size_t)Q_;
-    }
+    if (speculative) return push_speculative(xv, yv, n, kind);
+    if (kind != IN_DEVICE_F32 && !pinned && stage_len_ < (size_t)Q_) TRY(ensure_staging());
     if (cross_ && kind != IN_DEVICE_F32 && !pinned && !stage_y_[0]) {
         for (int i = 0; i < 2; ++i) CK(cudaMallocHost(&stage_y_[i], (size_t)C * Q_ * sizeof(float2)));
     }
-
-    cudaEvent_t copy_ev = get_event();
-    int stage_k = 0;
     for (size_t off = 0; off < n; off += (size_t)Q_) {
         const size_t len = std::min((size_t)Q_, n - off);
-        const int64_t abs0 = (int64_t)consumed_;
-        wait_ring_free(abs0 + (int64_t)len);
-        // source rows for x and y: [channel][len] with a row pitch
-        const float2* sx = nullptr;
-        const float2* sy = nullptr;
-        size_t pitch = 0;
-        if (kind == IN_DEVICE_F32) {
-            for (int ch = 0; ch < C; ++ch) {
-                launch_ring_write(ring_x_ + (size_t)ch * cap_, mask_, abs0, (const float2*)xv + (size_t)ch * n + off,
-                                  (int64_t)len, xs_);
-                launches_ += 1;
-                if (cross_) {
-                    const float2* ysrc = (const float2*)(yv ? yv : xv) + (size_t)ch * n + off;
-                    launch_ring_write(ring_y_ + (size_t)ch * cap_, mask_, abs0, ysrc, (int64_t)len, xs_);
-                    launches_ += 1;
-                }
-            }
-        } else {
-            if (pinned) {
-                sx = (const float2*)xv + off;
-                sy = yv ? (const float2*)yv + off : (cross_ ? sx : nullptr);
-                pitch = n;
-            } else {
-                if (stage_ev_live_[stage_k]) CK(cudaEventSynchronize(stage_ev_[stage_k]));
-                if (kind == IN_HOST_F32) {
-                    stage_copy(stage_[stage_k], (const cyc_cf32*)xv, n, off, len, C);
-                    if (cross_)
-                        stage_copy(stage_y_[stage_k], (const cyc_cf32*)(yv ? yv : xv), n, off, len, C);
-                } else {
-                    stage_copy(stage_[stage_k], (const cyc_cf64*)xv, n, off, len, C);
-                    if (cross_)
-                        stage_copy(stage_y_[stage_k], (const cyc_cf64*)(yv ? yv : xv), n, off, len, C);
-                }
-                sx = stage_[stage_k];
-                sy = cross_ ? stage_y_[stage_k] : nullptr;
-                pitch = len;
-            }
-            // 2D DMA: C rows of len samples into the rings, split at the wrap
-            const size_t pos = (size_t)((uint64_t)abs0 & mask_);
-            const size_t first = std::min(len, (size_t)cap_ - pos);
-            auto dma = [&](float2* ring, const float2* src) -> Status {
-                CK(cudaMemcpy2DAsync(ring + pos, cap_ * sizeof(float2), src, pitch * sizeof(float2),
-                                     first * sizeof(float2), C, cudaMemcpyHostToDevice, xs_));
-                if (first < len)
-                    CK(cudaMemcpy2DAsync(ring, cap_ * sizeof(float2), src + first, pitch * sizeof(float2),
-                                         (len - first) * sizeof(float2), C, cudaMemcpyHostToDevice, xs_));
-                return Status::ok();
-            };
-            TRY(dma(ring_x_, sx));
-            if (cross_) TRY(dma(ring_y_, sy));
-            if (!pinned) {
-                CK(cudaEventRecord(stage_ev_[stage_k], xs_));
-                stage_ev_live_[stage_k] = true;
-                stage_k ^= 1;
-            }
-        }
-        CK(cudaEventRecord(copy_ev, xs_));
-        CK(cudaStreamWaitEvent(cs_, copy_ev, 0));
+        TRY(ingest_piece(xv, yv, n, off, len, kind, pinned));
         consumed_ += len;
-        TRY(emit_new_frames(sink, user));
+        TRY(emit_new_frames(sink, user, S_main_));
     }
-    ev_pool_.push_back(copy_ev);
     // caller memory may not be retained after return
     if (pinned || kind == IN_DEVICE_F32) CK(cudaStreamSynchronize(xs_));
     return cuda_check(cudaGetLastError(), "push");
 }
 
-// Device-resident block-mode push: frames whose x window lies inside the new
+Status Engine::data_error(uint64_t key, int channel, int kind, const void* xv, const void* yv, size_t n) {
+    const uint64_t i = key >> 1;
+    Status s;
+    s.code = CYC_ERR_DATA;
+    s.index = (int64_t)(consumed_ + i);
+    bool range = false;
+    if (kind == IN_HOST_F64) {
+        const cyc_cf64* p = (const cyc_cf64*)((key & 1) ? yv : xv) + (size_t)channel * n + i;
+        range = std::isfinite(p->re) && std::isfinite(p->im);
+    }
+    s.msg = std::string(range ? "sample outside the float32 range" : "non-finite sample") + " at absolute index " +
+            std::to_string(consumed_ + i) + " in " + ((key & 1) ? "y" : "x") + " stream";
+    if (c_.channels > 1) s.msg += " of channel " + std::to_string(channel);
+    return s;
+}
+
+Status Engine::ensure_staging() {
+    const int C = c_.channels;
+    for (int i = 0; i < 2; ++i) {
+        if (stage_[i]) {
+            cudaEventSynchronize(stage_ev_[i]);
+            cudaFreeHost(stage_[i]);
+            cudaFreeHost(stage_y_[i]);
+            stage_y_[i] = nullptr;
+        }
+        CK(cudaMallocHost(&stage_[i], (size_t)C * Q_ * sizeof(float2)));
+        stage_ev_live_[i] = false;
+    }
+    stage_len_ = (size_t)Q_;
+    return Status::ok();
+}
+
+// Copy samples [off, off+len) of every channel into the rings at absolute
+// consumed_ + [0, len), on the copy stream; the compute stream waits for it.
+Status Engine::ingest_piece(const void* xv, const void* yv, size_t n, size_t off, size_t len, int kind, bool pinned) {
+    const int C = c_.channels;
+    const int64_t abs0 = (int64_t)consumed_;
+    wait_ring_free(abs0 + (int64_t)len);
+    if (kind == IN_DEVICE_F32) {
+        for (int ch = 0; ch < C; ++ch) {
+            launch_ring_write(ring_x_ + (size_t)ch * cap_, mask_, abs0, (const float2*)xv + (size_t)ch * n + off,
+                              (int64_t)len, xs_);
+            launches_ += 1;
+            if (cross_) {
+                const float2* ysrc = (const float2*)(yv ? yv : xv) + (size_t)ch * n + off;
+                launch_ring_write(ring_y_ + (size_t)ch * cap_, mask_, abs0, ysrc, (int64_t)len, xs_);
+                launches_ += 1;
+            }
+        }
+    } else {
+        const float2* sx = nullptr;
+        const float2* sy = nullptr;
+        size_t pitch = 0;
+        if (pinned) {
+            sx = (const float2*)xv + off;
+            sy = yv ? (const float2*)yv + off : (cross_ ? sx : nullptr);
+            pitch = n;
+        } else {
+            if (stage_ev_live_[stage_k_]) CK(cudaEventSynchronize(stage_ev_[stage_k_]));
+            if (kind == IN_HOST_F32) {
+                stage_copy(stage_[stage_k_], (const cyc_cf32*)xv, n, off, len, C);
+                if (cross_) stage_copy(stage_y_[stage_k_], (const cyc_cf32*)(yv ? yv : xv), n, off, len, C);
+            } else {
+                stage_copy(stage_[stage_k_], (const cyc_cf64*)xv, n, off, len, C);
+                if (cross_) stage_copy(stage_y_[stage_k_], (const cyc_cf64*)(yv ? yv : xv), n, off, len, C);
+            }
+            sx = stage_[stage_k_];
+            sy = cross_ ? stage_y_[stage_k_] : nullptr;
+            pitch = len;
+        }
+        // 2D DMA: C rows of len samples into the rings, split at the wrap
+        const size_t pos = (size_t)((uint64_t)abs0 & mask_);
+        const size_t first = std::min(len, (size_t)cap_ - pos);
+        auto dma = [&](float2* ring, const float2* src) -> Status {
+            CK(cudaMemcpy2DAsync(ring + pos, cap_ * sizeof(float2), src, pitch * sizeof(float2), first * sizeof(float2), C,
+                                 cudaMemcpyHostToDevice, xs_));
+            if (first < len)
+                CK(cudaMemcpy2DAsync(ring, cap_ * sizeof(float2), src + first, pitch * sizeof(float2),
+                                     (len - first) * sizeof(float2), C, cudaMemcpyHostToDevice, xs_));
+            return Status::ok();
+        };
+        TRY(dma(ring_x_, sx));
+        if (cross_) TRY(dma(ring_y_, sy));
+        if (!pinned) {
+            CK(cudaEventRecord(stage_ev_[stage_k_], xs_));
+            stage_ev_live_[stage_k_] = true;
+            stage_k_ ^= 1;
+        }
+    }
+    cudaEvent_t ev = get_event();
+    CK(cudaEventRecord(ev, xs_));
+    CK(cudaStreamWaitEvent(cs_, ev, 0));
+    ev_pool_.push_back(ev);
+    return Status::ok();
+}
+
+// Ring positions [a, b) (absolute) of every channel <-> the history backup.
+Status Engine::history_copy(int64_t a, int64_t b, bool save) {
+    const int C = c_.channels;
+    const int64_t len = b - a;
+    if (len <= 0) return Status::ok();
+    const size_t rows = cross_ ? 2 : 1;
+    const size_t need = rows * (size_t)C * (size_t)len;
+    if (hist_cap_ < need) {
+        CK(cudaStreamSynchronize(cs_));
+        cudaFree(hist_bak_);
+        CK(cudaMalloc(&hist_bak_, need * sizeof(float2)));
+        hist_cap_ = need;
+    }
+    const size_t pos = (size_t)((uint64_t)a & mask_);
+    const size_t first = std::min((size_t)len, (size_t)cap_ - pos);
+    for (size_t r = 0; r < rows; ++r) {
+        float2* ring = r ? ring_y_ : ring_x_;
+        float2* bak = hist_bak_ + r * (size_t)C * len;
+        const size_t rp = cap_ * sizeof(float2), bp = (size_t)len * sizeof(float2);
+        if (save) {
+            CK(cudaMemcpy2DAsync(bak, bp, ring + pos, rp, first * sizeof(float2), C, cudaMemcpyDeviceToDevice, cs_));
+            if (first < (size_t)len)
+                CK(cudaMemcpy2DAsync(bak + first, bp, ring, rp, (len - first) * sizeof(float2), C,
+                                     cudaMemcpyDeviceToDevice, cs_));
+        } else {
+            CK(cudaMemcpy2DAsync(ring + pos, rp, bak, bp, first * sizeof(float2), C, cudaMemcpyDeviceToDevice, cs_));
+            if (first < (size_t)len)
+                CK(cudaMemcpy2DAsync(ring, rp, bak + first, bp, (len - first) * sizeof(float2), C,
+                                     cudaMemcpyDeviceToDevice, cs_));
+        }
+    }
+    return Status::ok();
+}
+
+Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int kind) {
+    const int C = c_.channels;
+    const uint64_t c0 = consumed_, f0 = frames_;
+    // the samples the next frames still need: [f0*N, c0) (< buffer_need long)
+    const int64_t hb = std::min<int64_t>((int64_t)f0 * N_, (int64_t)c0);
+    TRY(history_copy(hb, (int64_t)c0, true));
+    if (!S_pend_) CK(cudaMalloc(&S_pend_, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double)));
+    CK(cudaMemsetAsync(S_pend_, 0, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
+    CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
+    if (kind == IN_DEVICE_F32) {
+        for (int ch = 0; ch < C; ++ch) {
+            launch_finite_check((const float2*)xv + (size_t)ch * n, yv ? (const float2*)yv + (size_t)ch * n : nullptr,
+                                (int64_t)n, 0, C, ch, key_dev_, cs_);
+            launches_ += 1;
+        }
+        TRY(fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_pend_));
+    } else {
+        for (size_t off = 0; off < n; off += (size_t)Q_) {
+            const size_t len = std::min((size_t)Q_, n - off);
+            const int64_t abs0 = (int64_t)consumed_;
+            TRY(ingest_piece(xv, yv, n, off, len, kind, true));
+            // GPU finite scan of the piece as it sits in the ring (wrap split)
+            const size_t pos = (size_t)((uint64_t)abs0 & mask_);
+            const size_t first = std::min(len, (size_t)cap_ - pos);
+            for (int ch = 0; ch < C; ++ch) {
+                const float2* rx = ring_x_ + (size_t)ch * cap_;
+                const float2* ry = cross_ ? ring_y_ + (size_t)ch * cap_ : nullptr;
+                launch_finite_check(rx + pos, ry ? ry + pos : nullptr, (int64_t)first, (int64_t)off, C, ch, key_dev_, cs_);
+                if (first < len)
+                    launch_finite_check(rx, ry, (int64_t)(len - first), (int64_t)(off + first), C, ch, key_dev_, cs_);
+                launches_ += first < len ? 2 : 1;
+            }
+            mark_read(abs0);
+            consumed_ += len;
+            TRY(emit_new_frames(nullptr, nullptr, S_pend_));
+        }
+    }
+    CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs_));
+    CK(cudaStreamSynchronize(xs_));
+    CK(cudaStreamSynchronize(cs_));
+    const uint64_t key = *key_host_;
+    if (key == ~0ull) {
+        launch_add_f64(S_main_, S_pend_, (int64_t)C * t_pad_ * Pf_ * 4, cs_);
+        launches_ += 1;
+        return cuda_check(cudaGetLastError(), "push");
+    }
+    // roll back: counters, history samples; the pending fold is discarded
+    consumed_ = c0;
+    frames_ = f0;
+    TRY(history_copy(hb, (int64_t)c0, false));
+    CK(cudaStreamSynchronize(cs_));
+    return data_error(key / C, (int)(key % C), kind, xv, yv, n);
+}
+
+// Device-resident block-mode chunk: frames whose x window lies inside the new
 // chunk are folded straight from the caller's device buffer; only the head
 // (frames straddling the previous chunk) and the tail (history for the next
 // chunk) are copied into the rings.
-Status Engine::push_device_zero_copy(const float2* x, const float2* y, size_t n) {
+Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, double* S) {
     const int C = c_.channels;
     const int64_t c0 = (int64_t)consumed_, c1 = c0 + (int64_t)n;
     const int64_t keep = std::min<int64_t>((int64_t)n, (int64_t)need_ + N_);
@@ -1097,13 +1206,11 @@ Status Engine::push_device_zero_copy(const float2* x, const float2* y, size_t n)
                 user_segs.push_back(g);
             }
         }
-        TRY(fold(ring_segs, S_main_));
-        TRY(fold(user_segs, S_main_));
+        TRY(fold(ring_segs, S));
+        TRY(fold(user_segs, S));
         mark_read(s + lag_lo_);
         frames_ = avail;
     }
-    // the caller's device buffer may not be retained after return
-    CK(cudaStreamSynchronize(cs_));
     return cuda_check(cudaGetLastError(), "push_device");
 }
 
@@ -1145,12 +1252,12 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
         }
         return Status::ok();
     }
-    std::vector<double2> tmp(layout_len_);
+    double2* tmp = avg_host_;  // pinned: the D2H of a table is a DMA, not a staged copy
     if (c_.emit_frames) {
         const size_t off = (size_t)channel * per + (size_t)fi * layout_len_;
         if (avg_mode == CYC_AVG_MAGNITUDE) {
-            std::vector<double> m(layout_len_);
-            CK(cudaMemcpyAsync(m.data(), mag_ + off, layout_len_ * sizeof(double), cudaMemcpyDeviceToHost, cs_));
+            double* m = reinterpret_cast<double*>(avg_host_);
+            CK(cudaMemcpyAsync(m, mag_ + off, layout_len_ * sizeof(double), cudaMemcpyDeviceToHost, cs_));
             CK(cudaStreamSynchronize(cs_));
             for (size_t i = 0; i < layout_len_; ++i) {
                 out[i].re = m[i] * invF;
@@ -1158,7 +1265,7 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
             }
             return Status::ok();
         }
-        CK(cudaMemcpyAsync(tmp.data(), coh_ + off, layout_len_ * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
+        CK(cudaMemcpyAsync(tmp,coh_ + off, layout_len_ * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
         CK(cudaStreamSynchronize(cs_));
         for (size_t i = 0; i < layout_len_; ++i) {
             out[i].re = tmp[i].x * invF;
@@ -1179,7 +1286,7 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
             avg_cache_frames_ = frames_;
             avg_cache_channel_ = channel;
         }
-        CK(cudaMemcpyAsync(tmp.data(), avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
+        CK(cudaMemcpyAsync(tmp,avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
                            cudaMemcpyDeviceToHost, cs_));
         CK(cudaStreamSynchronize(cs_));
         for (size_t i = 0; i < layout_len_; ++i) {
@@ -1188,7 +1295,7 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
         }
         return Status::ok();
     }
-    CK(cudaMemcpyAsync(tmp.data(), dsum_main_ + (size_t)channel * per + (size_t)fi * layout_len_,
+    CK(cudaMemcpyAsync(tmp,dsum_main_ + (size_t)channel * per + (size_t)fi * layout_len_,
                        layout_len_ * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
     CK(cudaStreamSynchronize(cs_));
     for (size_t i = 0; i < layout_len_; ++i) {
@@ -1207,6 +1314,8 @@ Status Engine::compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64*
     const size_t tot = xw_len + yw_len;
     if (dev_tmp_len_ < tot) {
         cudaFree(dev_tmp_);
+    cudaFree(S_pend_);
+    cudaFree(hist_bak_);
         CK(cudaMalloc(&dev_tmp_, tot * sizeof(float2)));
         dev_tmp_len_ = tot;
     }

@@ -110,7 +110,13 @@ private:
     Status compute_frames(const std::vector<int64_t>& k0s, const std::vector<int>& chans, bool recursive,
                           const float2* xbase_override = nullptr, const float2* ybase_override = nullptr,
                           uint64_t mask_override = 0);
-    Status emit_new_frames(cyc_frame_sink sink, void* user);
+    Status emit_new_frames(cyc_frame_sink sink, void* user, double* S_target);
+    Status data_error(uint64_t key, int channel, int kind, const void* xv, const void* yv, size_t n);
+    Status ensure_staging();
+    Status ingest_piece(const void* xv, const void* yv, size_t n, size_t off, size_t len, int kind, bool pinned);
+    Status history_copy(int64_t a, int64_t b, bool save);
+    Status push_speculative(const void* xv, const void* yv, size_t n, int kind);
+    Status fold_device_chunk(const float2* x, const float2* y, size_t n, double* S);
     Status deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const std::vector<int>& chans,
                    cyc_frame_sink sink, void* user, bool& stop);
 
@@ -152,6 +158,7 @@ private:
     double2* coh_ = nullptr;          // running coherent sums [channels][nflags][layout]
     double* mag_ = nullptr;           // running magnitude sums
     double2* avg_dev_ = nullptr;      // average scratch
+    double2* avg_host_ = nullptr;     // pinned average readback
     float* partials_ = nullptr;
     size_t partials_bytes_ = 0;
     double2* tw_ = nullptr;
@@ -202,8 +209,11 @@ private:
     uint64_t prof_launches_ = 0;
     double prof_ms_ = 0.0, prof_flops_ = 0.0;
 
-    // device-resident push without a ring copy of the bulk
-    Status push_device_zero_copy(const float2* x, const float2* y, size_t n);
+    // speculative block pushes: pending fold + history backup for roll-back
+    double* S_pend_ = nullptr;
+    float2* hist_bak_ = nullptr;
+    size_t hist_cap_ = 0;
+    int stage_k_ = 0;
 
     // finalize cache of the block average (frames count, channel)
     uint64_t avg_cache_frames_ = ~0ull;

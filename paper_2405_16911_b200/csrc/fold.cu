@@ -32,7 +32,7 @@ constexpr int NW = 8;
 constexpr int NT = NW * 32;
 constexpr int R = 4;
 constexpr int U = 8;
-constexpr int NSTAGE = 3;
+constexpr int NSTAGE = 2;
 
 constexpr int pad4mod8(int c) { return c + ((4 - c % 8) + 8) % 8; }
 
@@ -48,7 +48,7 @@ struct Geo {
     static constexpr int NX = XW / 2;            // x pairs per period
     static constexpr int NY = RB / 2;            // y pairs per period
     static constexpr int EPP = NX + NY;          // staged pairs per period
-    static constexpr int PS = LW == 8 ? 16 : (LW == 4 ? 8 : 4);  // periods per stage
+    static constexpr int PS = LW == 8 ? 32 : (LW == 4 ? 16 : 8);  // periods per stage
     static constexpr int STAGE = PS * PER;
     static constexpr int SMEM = NSTAGE * STAGE * 16;
     static constexpr int EPT = (PS * EPP + NT - 1) / NT;  // staged pairs per thread per stage
@@ -147,23 +147,11 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
     const uint64_t mask = seg.mask;
     const bool vec = seg.vec != 0;
 
-    // Fixed per-thread staging assignment (pair e of period q for idx = tid + k*NT),
-    // packed into one word: [0,13) float4 offset in the stage, [13,24) sample
-    // offset in the period window, bit 24 = x (else y), bit 31 = idle.
-    uint32_t st_pack[G::EPT];
-#pragma unroll
-    for (int k = 0; k < G::EPT; ++k) {
-        const int idx = tid + k * NT;
-        const int q = idx / G::EPP;
-        const int e = idx - q * G::EPP;
-        const bool isx = e < G::NX;
-        const int ee = isx ? e : e - G::NX;
-        const int b = ee & 1, c = ee >> 1;
-        const uint32_t dst = (uint32_t)(q * G::PER + (isx ? b * G::XC + c : 2 * G::XC + b * G::YC + c));
-        const uint32_t rel = (uint32_t)(4 * c + 2 * b);
-        st_pack[k] = idx < G::PS * G::EPP ? (dst | (rel << 13) | (isx ? 1u << 24 : 0u)) : 0x80000000u;
-    }
-    static_assert(G::STAGE < (1 << 13) && G::XW < (1 << 11), "staging pack overflow");
+    // Staging assignment: stage element idx = tid + k*NT is pair e of period q;
+    // (q, e) advance incrementally so no per-element table lives in registers.
+    const int q_first = tid / G::EPP;
+    const int e_first = tid - q_first * G::EPP;
+    constexpr int DQ = NT / G::EPP, DE = NT % G::EPP;
 
     auto load_stage = [&](int s) {
         const int64_t pbeg = tile.p0 + (int64_t)s * G::PS;
@@ -173,51 +161,65 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
         const bool fast = vec && pend <= tile.p1 && pbeg * Pf + xoff >= seg.x_lo &&
                           (pend - 1) * Pf + xoff + G::XW <= seg.x_hi && pbeg * Pf + res0 >= seg.n_start &&
                           (pend - 1) * Pf + res0 + G::RB <= seg.n_end && res0 + G::RB <= Pf;
+        int q = q_first, e = e_first;
         if (fast) {
-#pragma unroll
+#pragma unroll 2
             for (int k = 0; k < G::EPT; ++k) {
-                const uint32_t w = st_pack[k];
-                if (w & 0x80000000u) continue;
-                const uint32_t off = w & 0x1fffu;
-                const int q = (int)(off / G::PER);
-                const bool isx = (w >> 24) & 1u;
-                const int64_t n = (pbeg + q) * Pf + (isx ? xoff : res0) + (int64_t)((w >> 13) & 0x7ffu);
-                cp_async16(dst0 + off * 16u, (isx ? seg.x : seg.y) + ((uint64_t)n & mask), 16);
+                if (q < G::PS) {
+                    const bool isx = e < G::NX;
+                    const int ee = isx ? e : e - G::NX;
+                    const int b = ee & 1, c = ee >> 1;
+                    const int off = q * G::PER + (isx ? b * G::XC + c : 2 * G::XC + b * G::YC + c);
+                    const int64_t n = (pbeg + q) * Pf + (isx ? xoff : res0) + (4 * c + 2 * b);
+                    cp_async16(dst0 + (uint32_t)off * 16u, (isx ? seg.x : seg.y) + ((uint64_t)n & mask), 16);
+                }
+                q += DQ;
+                e += DE;
+                if (e >= G::EPP) {
+                    e -= G::EPP;
+                    ++q;
+                }
             }
             return;
         }
 #pragma unroll 1
         for (int k = 0; k < G::EPT; ++k) {
-            const uint32_t w = st_pack[k];
-            if (w & 0x80000000u) continue;
-            const uint32_t off = w & 0x1fffu;
-            const int q = (int)(off / G::PER);
-            const bool isx = (w >> 24) & 1u;
-            const int rel = (int)((w >> 13) & 0x7ffu);
-            const int64_t p = pbeg + q;
-            const uint32_t dst = dst0 + off * 16u;
-            int64_t n, lo, hi;
-            const float2* base;
-            if (isx) {
-                n = p * Pf + xoff + rel;
-                lo = seg.x_lo;
-                hi = seg.x_hi;
-                base = seg.x;
-            } else {
-                n = p * Pf + res0 + rel;
-                lo = seg.n_start;
-                hi = (res0 + rel < Pf) ? seg.n_end : lo;  // masked residue-block tail
-                base = seg.y;
+            if (q < G::PS) {
+                const bool isx = e < G::NX;
+                const int ee = isx ? e : e - G::NX;
+                const int b = ee & 1, c = ee >> 1;
+                const int rel = 4 * c + 2 * b;
+                const uint32_t dst = dst0 + (uint32_t)(q * G::PER + (isx ? b * G::XC + c : 2 * G::XC + b * G::YC + c)) * 16u;
+                const int64_t p = pbeg + q;
+                int64_t n, lo, hi;
+                const float2* base;
+                if (isx) {
+                    n = p * Pf + xoff + rel;
+                    lo = seg.x_lo;
+                    hi = seg.x_hi;
+                    base = seg.x;
+                } else {
+                    n = p * Pf + res0 + rel;
+                    lo = seg.n_start;
+                    hi = (res0 + rel < Pf) ? seg.n_end : lo;  // masked residue-block tail
+                    base = seg.y;
+                }
+                if (p >= tile.p1) hi = lo;
+                const bool v0 = n >= lo && n < hi;
+                const bool v1 = n + 1 >= lo && n + 1 < hi;
+                if (vec && v0 == v1) {
+                    cp_async16(dst, v0 ? (const void*)(base + ((uint64_t)n & mask)) : (const void*)base, v0 ? 16 : 0);
+                } else {
+                    cp_async8(dst, v0 ? (const void*)(base + ((uint64_t)n & mask)) : (const void*)base, v0 ? 8 : 0);
+                    cp_async8(dst + 8, v1 ? (const void*)(base + ((uint64_t)(n + 1) & mask)) : (const void*)base,
+                              v1 ? 8 : 0);
+                }
             }
-            if (p >= tile.p1) hi = lo;
-            const bool v0 = n >= lo && n < hi;
-            const bool v1 = n + 1 >= lo && n + 1 < hi;
-            if (vec && v0 == v1) {
-                cp_async16(dst, v0 ? (const void*)(base + ((uint64_t)n & mask)) : (const void*)base, v0 ? 16 : 0);
-            } else {
-                cp_async8(dst, v0 ? (const void*)(base + ((uint64_t)n & mask)) : (const void*)base, v0 ? 8 : 0);
-                cp_async8(dst + 8, v1 ? (const void*)(base + ((uint64_t)(n + 1) & mask)) : (const void*)base,
-                          v1 ? 8 : 0);
+            q += DQ;
+            e += DE;
+            if (e >= G::EPP) {
+                e -= G::EPP;
+                ++q;
             }
         }
     };

@@ -133,8 +133,9 @@ void launch_direct(const DirectLaunch& L, cudaStream_t st);
 void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st);
 void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len,
                          double2* coh, double* mag, cudaStream_t st);
-// First non-finite sample (key = 2*i for x, 2*i+1 for y) -> atomicMin(*key).
-void launch_finite_check(const float2* x, const float2* y, int64_t n,
+// First non-finite sample -> atomicMin(*key);
+// key = (2*(base+i) + is_y) * channels + ch  -- smallest = reference scan order.
+void launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
                          unsigned long long* key, cudaStream_t st);
 // Ring write from a device source with wrap: ring[(abs0 + i) & mask] = src[i].
 void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src,

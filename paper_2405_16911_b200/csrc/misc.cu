@@ -30,15 +30,17 @@ __global__ void accum_frames_kernel(const double2* frames, int64_t n_frames, int
 // Whole-chunk finite scan (proj/src/estimator.cpp:43-52): the smallest key
 // 2*i (x) / 2*i+1 (y) names the first offending sample in the reference's
 // scan order (x before y at each index).
-__global__ void finite_check_kernel(const float2* x, const float2* y, int64_t n, unsigned long long* key) {
+__global__ void finite_check_kernel(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
+                                    unsigned long long* key) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float2 a = x[i];
         unsigned long long k = ~0ull;
+        const unsigned long long idx = (unsigned long long)(base + i);
         if (!isfinite(a.x) || !isfinite(a.y)) {
-            k = 2ull * (unsigned long long)i;
+            k = (2ull * idx) * (unsigned long long)channels + (unsigned long long)ch;
         } else if (y) {
             const float2 b = y[i];
-            if (!isfinite(b.x) || !isfinite(b.y)) k = 2ull * (unsigned long long)i + 1ull;
+            if (!isfinite(b.x) || !isfinite(b.y)) k = (2ull * idx + 1ull) * (unsigned long long)channels + (unsigned long long)ch;
         }
         if (k != ~0ull) atomicMin(key, k);
     }
@@ -64,8 +66,9 @@ void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len, d
                          cudaStream_t st) {
     if (n_frames > 0 && len > 0) accum_frames_kernel<<<grid_for(len, 256), 256, 0, st>>>(frames, n_frames, len, coh, mag);
 }
-void launch_finite_check(const float2* x, const float2* y, int64_t n, unsigned long long* key, cudaStream_t st) {
-    if (n > 0) finite_check_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, key);
+void launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
+                         unsigned long long* key, cudaStream_t st) {
+    if (n > 0) finite_check_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, base, channels, ch, key);
 }
 void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n, cudaStream_t st) {
     if (n > 0) ring_write_kernel<<<grid_for(n, 256), 256, 0, st>>>(ring, mask, abs0, src, n);

@@ -361,3 +361,52 @@ def test_device_push(cyc):
     dx = torch.from_numpy(x).cuda()
     b.push_device(dx.data_ptr(), len(x))
     assert np.max(np.abs(a.average() - b.average())) <= 1e-12
+
+
+# Speculative block pushes (pinned host / device input): the GPU finite scan
+# runs while the chunk is folded into a pending accumulator; a bad chunk must
+# leave the estimator exactly as it was (estimator.cpp:43-52).
+@pytest.mark.parametrize("kind", ["pinned", "device"])
+def test_speculative_push_rollback(cyc, kind):
+    import torch
+    N, lags = 1024, list(range(64))
+    x = rand_c(3 << 20, 81)
+    bad = rand_c(5 << 20, 82)
+    bad[(3 << 20) + 12345] = np.nan + 1j
+    cfg = full_cfg(cyc, N, lags, flags=cyc.Flags.BOTH, emit_frames=False)
+    ref_est, est = cyc.CyclicCorrelator(cfg), cyc.CyclicCorrelator(cfg)
+
+    def push(e, a):
+        if kind == "pinned":
+            p = cyc.host_alloc(a.shape)
+            p[:] = a
+            return e.push(p)
+        d = torch.from_numpy(a.view(np.float32)).cuda()
+        return e.push_device(d.data_ptr(), len(a))
+
+    push(ref_est, x[: 1 << 20])
+    push(est, x[: 1 << 20])
+    c0, f0 = est.consumed(), est.frames_emitted()
+    with pytest.raises(cyc.DataError, match=f"index {c0 + (3 << 20) + 12345} in x stream"):
+        push(est, bad)
+    assert est.consumed() == c0 and est.frames_emitted() == f0
+    push(ref_est, x[1 << 20:])
+    push(est, x[1 << 20:])
+    for fl in (cyc.Flags.CONV, cyc.Flags.CONJ):
+        assert np.max(np.abs(est.average(flag=fl) - ref_est.average(flag=fl))) <= 1e-12
+
+
+def test_c2_scale_block_average_vs_oracle(cyc, oracle):
+    """Config 2 geometry at 2^22 samples (the oracle's fold finishes in seconds)."""
+    from paper_2405_16911_b200 import siggen
+    x = siggen.c2_record(seed=2, n=1 << 22)
+    N, lags = 1024, list(range(64))
+    est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, flags=cyc.Flags.BOTH, emit_frames=False))
+    p = cyc.host_alloc(x.shape)
+    p[:] = x
+    est.push(p)
+    F = est.frames_emitted()
+    cv, cj = oracle.block_fold(x, x, np.arange(N), N, lags, 0, F * N)
+    mp = mean_power(x)
+    assert_parity(est.average(flag=cyc.Flags.CONV), cv.T.reshape(-1), mp, what="C2 conv")
+    assert_parity(est.average(flag=cyc.Flags.CONJ), cj.T.reshape(-1), mp, what="C2 conj")
