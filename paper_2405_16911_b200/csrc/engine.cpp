@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cfloat>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -167,6 +170,19 @@ void stage_copy(float2* dst, const T* src, size_t src_pitch, size_t off, size_t 
         th.emplace_back([&, i0, i1] { work(0, channels, i0, i1); });
     }
     for (auto& t : th) t.join();
+}
+
+// CYC_TRACE=1: host timestamps (ms since the last trace(nullptr)) on stderr.
+void trace(const char* what) {
+    static const bool on = std::getenv("CYC_TRACE") != nullptr;
+    static std::chrono::steady_clock::time_point t0;
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    if (!what) {
+        t0 = now;
+        return;
+    }
+    std::fprintf(stderr, "[cyc] %8.3f ms  %s\n", std::chrono::duration<double, std::milli>(now - t0).count(), what);
 }
 
 bool is_pinned(const void* p) {
@@ -389,6 +405,7 @@ Status Engine::init(const Cfg& cfg) {
     int64_t qmin = std::max<int64_t>(next_pow2((int64_t)need_ + N_), 1 << 12);
     int64_t qdef = std::max<int64_t>((1 << 21) / next_pow2(c_.channels), 1 << 12);
     Q_ = std::max(qmin, qdef);
+    if (const char* qs = std::getenv("CYC_PIECE")) Q_ = std::max(qmin, next_pow2(std::atoll(qs)));  // tuning knob
     TRY(ensure_ring(4 * Q_));
 
     const size_t lay_all = (size_t)c_.channels * nflags_ * layout_len_;
@@ -464,7 +481,6 @@ Engine::~Engine() {
     cudaFree(S_pend_);
     cudaFree(hist_bak_);
     cudaFreeHost(meta_host_);
-    cudaFree(meta_dev_);
     for (int i = 0; i < META_SLOTS; ++i)
         if (meta_ev_[i]) cudaEventDestroy(meta_ev_[i]);
     for (int i = 0; i < 2; ++i) {
@@ -479,7 +495,7 @@ Engine::~Engine() {
 }
 
 Status Engine::ensure_ring(int64_t cap_min) {
-    if (ring_x_) return Status::ok();  // sized once at create
+    if (ring_x_) return Status::ok();  // sized once at create; grow_ring() enlarges
     const int64_t cap = next_pow2(cap_min);
     float2* nx = nullptr;
     CK(cudaMalloc(&nx, (size_t)c_.channels * cap * sizeof(float2)));
@@ -487,6 +503,39 @@ Status Engine::ensure_ring(int64_t cap_min) {
     ring_x_ = nx;
     cap_ = cap;
     mask_ = (uint64_t)cap - 1;
+    return Status::ok();
+}
+
+// Enlarge the rings to >= cap_min samples per channel, re-placing the live
+// history [frames*N, consumed) at its new positions (absolute n -> n & mask).
+Status Engine::grow_ring(int64_t cap_min) {
+    if (cap_ >= cap_min) return Status::ok();
+    const int C = c_.channels;
+    const int64_t cap = next_pow2(cap_min);
+    const uint64_t mask = (uint64_t)cap - 1;
+    CK(cudaStreamSynchronize(xs_));
+    CK(cudaStreamSynchronize(cs_));
+    const int64_t hi = (int64_t)consumed_;
+    const int64_t lo = std::max<int64_t>(0, std::min<int64_t>((int64_t)frames_ * N_, hi) - (int64_t)need_);
+    for (int r = 0; r < (cross_ ? 2 : 1); ++r) {
+        float2*& ring = r ? ring_y_ : ring_x_;
+        float2* nr = nullptr;
+        CK(cudaMalloc(&nr, (size_t)C * cap * sizeof(float2)));
+        for (int64_t n = lo; n < hi;) {
+            const int64_t po = (int64_t)((uint64_t)n & mask_), pn = (int64_t)((uint64_t)n & mask);
+            const int64_t run = std::min({hi - n, cap_ - po, cap - pn});
+            CK(cudaMemcpy2DAsync(nr + pn, cap * sizeof(float2), ring + po, cap_ * sizeof(float2), run * sizeof(float2),
+                                 C, cudaMemcpyDeviceToDevice, cs_));
+            n += run;
+        }
+        CK(cudaStreamSynchronize(cs_));
+        cudaFree(ring);
+        ring = nr;
+    }
+    for (auto& m : reads_) ev_pool_.push_back(m.ev);
+    reads_.clear();
+    cap_ = cap;
+    mask_ = mask;
     return Status::ok();
 }
 
@@ -524,16 +573,20 @@ Status Engine::ensure_frames(size_t slots) {
     return Status::ok();
 }
 
+// Launch metadata (segments, tiles, rows) lives in mapped page-locked host
+// memory that the kernels read directly over PCIe: no H2D copy is queued on
+// the copy engines, so it never waits behind the bulk sample DMAs.
 Status Engine::ensure_meta(size_t bytes) {
     if (meta_slot_bytes_ >= bytes) return Status::ok();
     if (meta_host_) {
         CK(cudaStreamSynchronize(cs_));
         cudaFreeHost(meta_host_);
-        cudaFree(meta_dev_);
     }
     meta_slot_bytes_ = std::max(bytes, meta_slot_bytes_ * 2);
-    CK(cudaMallocHost(&meta_host_, META_SLOTS * meta_slot_bytes_));
-    CK(cudaMalloc(&meta_dev_, META_SLOTS * meta_slot_bytes_));
+    CK(cudaHostAlloc(&meta_host_, META_SLOTS * meta_slot_bytes_, cudaHostAllocMapped | cudaHostAllocPortable));
+    void* d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, meta_host_, 0));
+    meta_dev_ = static_cast<char*>(d);
     for (int i = 0; i < META_SLOTS; ++i) {
         if (!meta_ev_[i]) CK(cudaEventCreateWithFlags(&meta_ev_[i], cudaEventDisableTiming));
         meta_ev_live_[i] = false;
@@ -544,11 +597,11 @@ Status Engine::ensure_meta(size_t bytes) {
 }
 
 void* Engine::upload(const void* src, size_t bytes) {
-    bytes = (bytes + 255) & ~size_t(255);
-    if (bytes > meta_slot_bytes_) {
-        ensure_meta(bytes);
-    }
-    if (meta_used_ + bytes > meta_slot_bytes_) {
+    const size_t span = (bytes + 255) & ~size_t(255);
+    if (span > meta_slot_bytes_) ensure_meta(span);
+    if (meta_used_ + span > meta_slot_bytes_) {
+        // the slot being left is guarded by an event; the next slot is reused
+        // only after the kernels that read it have completed
         cudaEventRecord(meta_ev_[meta_slot_], cs_);
         meta_ev_live_[meta_slot_] = true;
         meta_slot_ = (meta_slot_ + 1) % META_SLOTS;
@@ -557,8 +610,7 @@ void* Engine::upload(const void* src, size_t bytes) {
     }
     const size_t off = (size_t)meta_slot_ * meta_slot_bytes_ + meta_used_;
     std::memcpy(meta_host_ + off, src, bytes);
-    cudaMemcpyAsync(meta_dev_ + off, meta_host_ + off, bytes, cudaMemcpyHostToDevice, cs_);
-    meta_used_ += bytes;
+    meta_used_ += span;
     return meta_dev_ + off;
 }
 
@@ -1038,6 +1090,12 @@ Status Engine::ingest_piece(const void* xv, const void* yv, size_t n, size_t off
         const size_t pos = (size_t)((uint64_t)abs0 & mask_);
         const size_t first = std::min(len, (size_t)cap_ - pos);
         auto dma = [&](float2* ring, const float2* src) -> Status {
+            if (C == 1) {  // plain 1D DMA for a single channel
+                CK(cudaMemcpyAsync(ring + pos, src, first * sizeof(float2), cudaMemcpyHostToDevice, xs_));
+                if (first < len)
+                    CK(cudaMemcpyAsync(ring, src + first, (len - first) * sizeof(float2), cudaMemcpyHostToDevice, xs_));
+                return Status::ok();
+            }
             CK(cudaMemcpy2DAsync(ring + pos, cap_ * sizeof(float2), src, pitch * sizeof(float2), first * sizeof(float2), C,
                                  cudaMemcpyHostToDevice, xs_));
             if (first < len)
@@ -1099,6 +1157,14 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
     const uint64_t c0 = consumed_, f0 = frames_;
     // the samples the next frames still need: [f0*N, c0) (< buffer_need long)
     const int64_t hb = std::min<int64_t>((int64_t)f0 * N_, (int64_t)c0);
+    trace(nullptr);
+    // Host chunks: let the whole chunk plus its history sit in the ring so the
+    // copy stream never waits on compute inside the push (budget: 4 GiB).
+    if (kind != IN_DEVICE_F32) {
+        const int64_t want = next_pow2((int64_t)c0 + (int64_t)n - hb + Q_);
+        if (want > cap_ && (double)want * C * (cross_ ? 2 : 1) * sizeof(float2) <= 4.0 * (1ull << 30))
+            TRY(grow_ring(want));
+    }
     TRY(history_copy(hb, (int64_t)c0, true));
     if (!S_pend_) CK(cudaMalloc(&S_pend_, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double)));
     CK(cudaMemsetAsync(S_pend_, 0, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
@@ -1111,9 +1177,18 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
         }
         TRY(fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_pend_));
     } else {
+        static const bool tr = std::getenv("CYC_TRACE") != nullptr;
+        cudaEvent_t ta = nullptr, tb = nullptr, tc = nullptr;
+        if (tr) {
+            cudaEventCreate(&ta);
+            cudaEventCreate(&tb);
+            cudaEventCreate(&tc);
+            cudaEventRecord(ta, xs_);
+        }
         for (size_t off = 0; off < n; off += (size_t)Q_) {
             const size_t len = std::min((size_t)Q_, n - off);
             const int64_t abs0 = (int64_t)consumed_;
+            if (tr && off == (size_t)Q_) cudaEventRecord(tc, xs_);
             TRY(ingest_piece(xv, yv, n, off, len, kind, true));
             // GPU finite scan of the piece as it sits in the ring (wrap split)
             const size_t pos = (size_t)((uint64_t)abs0 & mask_);
@@ -1128,12 +1203,28 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
             }
             mark_read(abs0);
             consumed_ += len;
-            TRY(emit_new_frames(nullptr, nullptr, S_pend_));
+            // Fold in few, shrinking batches (after 1/2, 3/4 and all of the chunk):
+            // each fold launch writes ~38 MB of partials that contend with the
+            // DMA, and the batch folded after the last DMA is the exposed tail.
+            const size_t done = off + len;
+            if (done == n || (done >= n / 2 && off < n / 2) || (done >= (3 * n) / 4 && off < (3 * n) / 4))
+                TRY(emit_new_frames(nullptr, nullptr, S_pend_));
+            trace("piece enqueued");
+        }
+        if (tr) {
+            cudaEventRecord(tb, xs_);
+            cudaEventSynchronize(tb);
+            float ms = 0.f, ms1 = 0.f;
+            cudaEventElapsedTime(&ms, ta, tb);
+            cudaEventElapsedTime(&ms1, ta, tc);
+            std::fprintf(stderr, "[cyc] copy-stream span %.3f ms (first piece %.3f ms)\n", ms, ms1);
         }
     }
     CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs_));
     CK(cudaStreamSynchronize(xs_));
+    trace("copies done");
     CK(cudaStreamSynchronize(cs_));
+    trace("compute done");
     const uint64_t key = *key_host_;
     if (key == ~0ull) {
         launch_add_f64(S_main_, S_pend_, (int64_t)C * t_pad_ * Pf_ * 4, cs_);
@@ -1219,6 +1310,7 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
 // ---------------------------------------------------------------------------
 
 Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
+    trace(nullptr);
     CK(cudaSetDevice(c_.device));
     Status u;
     u.code = CYC_ERR_USAGE;
@@ -1286,13 +1378,13 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
             avg_cache_frames_ = frames_;
             avg_cache_channel_ = channel;
         }
-        CK(cudaMemcpyAsync(tmp,avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
+        trace("avg finalize enqueued");
+        CK(cudaMemcpyAsync(tmp, avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
                            cudaMemcpyDeviceToHost, cs_));
         CK(cudaStreamSynchronize(cs_));
-        for (size_t i = 0; i < layout_len_; ++i) {
-            out[i].re = tmp[i].x;
-            out[i].im = tmp[i].y;
-        }
+        trace("avg d2h done");
+        std::memcpy(out, tmp, layout_len_ * sizeof(double2));
+        trace("avg copied");
         return Status::ok();
     }
     CK(cudaMemcpyAsync(tmp,dsum_main_ + (size_t)channel * per + (size_t)fi * layout_len_,

@@ -91,6 +91,7 @@ private:
     Status init(const Cfg& cfg);
     Status cuda_check(cudaError_t e, const char* what);
     Status ensure_ring(int64_t cap_min);
+    Status grow_ring(int64_t cap_min);
     Status ensure_partials(size_t bytes);
     Status ensure_frames(size_t slots);
     Status ensure_meta(size_t bytes);
