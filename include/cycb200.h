@@ -180,6 +180,9 @@ uint64_t cyc_kernel_launches(const cyc_est* est);
 /* Internal algorithm chosen for this handle: "fold-dft", "fold-fft",
  * "direct", written into buf. */
 int cyc_algorithm(const cyc_est* est, char* buf, size_t buflen);
+/* The same plan for a config without creating a handle (host-only, no
+ * device): rational alpha grid P, fold period Pf, lag-lane width. */
+int cyc_plan(const cyc_config* cfg, char* buf, size_t buflen);
 
 /* Page-locked host buffers for zero-copy-staging pushes. */
 void* cyc_host_alloc(size_t bytes);

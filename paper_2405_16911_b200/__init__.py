@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
     L.cyc_build_info.restype = C.c_char_p
     L.cyc_compute_set_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_int, C.c_uint64, vp,
                                          C.c_char_p, sz]
+    L.cyc_plan.argtypes = [C.POINTER(_Config), C.c_char_p, sz]
     L.cyc_reset.argtypes = [vp]
     L.cyc_profile_enable.argtypes = [vp, C.c_int]
     L.cyc_profile_read.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -257,6 +258,16 @@ class EstimatorConfig:
         c.channels = int(self.channels)
         c.device = int(self.device)
         return c, (al, lg)
+
+
+def plan(cfg: EstimatorConfig) -> str:
+    """Algorithm the engine picks for cfg (host-only; no device needed)."""
+    c, keep = cfg._c()
+    buf = C.create_string_buffer(1024)
+    rc = lib().cyc_plan(C.byref(c), buf, 1024)
+    if rc:
+        _raise(rc, buf.value.decode())
+    return buf.value.decode()
 
 
 def validate_config(cfg: EstimatorConfig) -> list:

@@ -243,3 +243,17 @@ int cyc_profile_read(cyc_est* est, uint64_t* launches, double* ms, double* flops
 double cyc_measure_fp32_peak(int device) { return cyc::measure_fp32_peak_tflops(device); }
 
 }  // extern "C"
+
+extern "C" int cyc_plan(const cyc_config* cfg, char* buf, size_t buflen) {
+    if (!cfg) return CYC_ERR_USAGE;
+    const cyc::Cfg g = cyc::from_c(cfg);
+    const auto v = cyc::validate(g);
+    if (!v.empty()) {
+        std::string s = "invalid config:";
+        for (auto& e : v) s += " [" + e + "]";
+        write_err(buf, buflen, s);
+        return CYC_ERR_CONFIG;
+    }
+    write_err(buf, buflen, cyc::Engine::plan_string(g));
+    return CYC_OK;
+}

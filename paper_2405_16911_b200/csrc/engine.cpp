@@ -325,9 +325,10 @@ Status Engine::create_unchecked(const Cfg& cfg, Engine** out) {
     return s;
 }
 
-Status Engine::init(const Cfg& cfg) {
+// Host-only planning: lag geometry, layout, rational alpha grid and the fold /
+// finalize / direct algorithm choice.  No CUDA calls (testable on a CPU box).
+Status Engine::plan(const Cfg& cfg) {
     c_ = cfg;
-    CK(cudaSetDevice(c_.device));
     nflags_ = (c_.flags == 3) ? 2 : 1;
     // lags (types.cpp:9-28)
     if (c_.lag_symmetric) {
@@ -398,7 +399,18 @@ Status Engine::init(const Cfg& cfg) {
         afx_.resize(A_);
         for (int a = 0; a < A_; ++a) afx_[a] = alpha_fixed(c_.alphas[a]);
     }
+    return Status::ok();
+}
 
+std::string Engine::plan_string(const Cfg& cfg) {
+    Engine e;
+    Status s = e.plan(cfg);
+    return s.code ? s.msg : e.algorithm();
+}
+
+Status Engine::init(const Cfg& cfg) {
+    TRY(plan(cfg));
+    CK(cudaSetDevice(c_.device));
     CK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
     // ring: pieces of Q samples per channel, four pieces per ring

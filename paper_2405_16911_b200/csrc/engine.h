@@ -59,6 +59,8 @@ public:
     // For one-shot kernel-level windows (kernels.cpp:116-135), whose contract
     // is only the window geometry, not the streaming span rule.
     static Status create_unchecked(const Cfg& cfg, Engine** out);
+    // Algorithm the engine would pick for cfg (no device needed).
+    static std::string plan_string(const Cfg& cfg);
     ~Engine();
 
     Status push(const void* x, const void* y, size_t n, int kind, cyc_frame_sink sink, void* user);
@@ -88,6 +90,7 @@ public:
 
 private:
     Engine() = default;
+    Status plan(const Cfg& cfg);
     Status init(const Cfg& cfg);
     Status cuda_check(cudaError_t e, const char* what);
     Status ensure_ring(int64_t cap_min);
