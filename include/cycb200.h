@@ -88,6 +88,9 @@ typedef struct cyc_config {
                            /*    coherent average (cyc_average) -- the block mode     */
     int channels;          /* >= 1 independent synchronized streams per handle        */
     int device;            /* CUDA device ordinal                                     */
+    int64_t origin;        /* absolute index of the first pushed sample (default 0):  */
+                           /* phases and start_abs are anchored to absolute sample 0, */
+                           /* so a stream may be resumed or time-sharded exactly      */
 } cyc_config;
 
 typedef struct cyc_est cyc_est;
@@ -160,6 +163,14 @@ int cyc_num_flags(const cyc_est* est);
 const char* cyc_last_error(const cyc_est* est);
 /* For CYC_ERR_DATA: absolute index of the offending sample, else -1. */
 int64_t cyc_data_error_index(const cyc_est* est);
+
+/* Block-mode fold state: device pointer to the fp64 residue-fold accumulators
+ * (count doubles) and the number of frames folded into them.  Time shards of
+ * one record (each created with origin = its first frame * win_len) sum these
+ * buffers in place (e.g. ncclAllReduce) and set the total frame count; the
+ * coherent average is then exactly the whole record's. */
+int cyc_fold_state(cyc_est* est, void** dev_ptr, size_t* count, uint64_t* frames);
+int cyc_fold_set_frames(cyc_est* est, uint64_t frames);
 
 /* Block until all device work of this handle is complete. */
 int cyc_synchronize(cyc_est* est);

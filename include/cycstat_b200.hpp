@@ -93,6 +93,7 @@ struct EstimatorConfig {
     bool emit_frames = true;  // false: block mode (count + fold; read average())
     int channels = 1;
     int device = 0;
+    std::int64_t origin = 0;  // absolute index of the first pushed sample
 };
 
 namespace detail {
@@ -113,6 +114,7 @@ inline cyc_config to_c(const EstimatorConfig& c) {
     r.emit_frames = c.emit_frames ? 1 : 0;
     r.channels = c.channels;
     r.device = c.device;
+    r.origin = c.origin;
     return r;
 }
 inline std::vector<std::string> split_lines(const std::string& s) {

@@ -79,6 +79,7 @@ class _Config(C.Structure):
         ("lag_symmetric", C.c_int), ("max_lag", C.c_int),
         ("lags", C.POINTER(C.c_int)), ("num_lags", C.c_size_t),
         ("lam", C.c_double), ("emit_frames", C.c_int), ("channels", C.c_int), ("device", C.c_int),
+        ("origin", C.c_int64),
     ]
 
 
@@ -140,6 +141,8 @@ def lib() -> C.CDLL:
     L.cyc_compute_set_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_int, C.c_uint64, vp,
                                          C.c_char_p, sz]
     L.cyc_plan.argtypes = [C.POINTER(_Config), C.c_char_p, sz]
+    L.cyc_fold_state.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), C.POINTER(C.c_uint64)]
+    L.cyc_fold_set_frames.argtypes = [vp, C.c_uint64]
     L.cyc_reset.argtypes = [vp]
     L.cyc_profile_enable.argtypes = [vp, C.c_int]
     L.cyc_profile_read.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -240,6 +243,7 @@ class EstimatorConfig:
     emit_frames: bool = True  # False: block mode (count + fold; read with average())
     channels: int = 1
     device: int = 0
+    origin: int = 0           # absolute index of the first pushed sample (resume / time shards)
 
     def _c(self):
         c = _Config()
@@ -257,6 +261,7 @@ class EstimatorConfig:
         c.emit_frames = int(bool(self.emit_frames))
         c.channels = int(self.channels)
         c.device = int(self.device)
+        c.origin = int(self.origin)
         return c, (al, lg)
 
 
@@ -427,6 +432,15 @@ class CyclicCorrelator:
 
     def synchronize(self):
         self._check(self._L.cyc_synchronize(self._h))
+
+    def fold_state(self):
+        """(device pointer, fp64 count, frames) of the block-mode fold accumulators."""
+        p, n, f = C.c_void_p(), C.c_size_t(), C.c_uint64()
+        self._check(self._L.cyc_fold_state(self._h, C.byref(p), C.byref(n), C.byref(f)))
+        return int(p.value), int(n.value), int(f.value)
+
+    def fold_set_frames(self, frames: int):
+        self._check(self._L.cyc_fold_set_frames(self._h, int(frames)))
 
     def reset(self):
         """Fresh stream state (same as constructing a new estimator with this config)."""

@@ -257,3 +257,13 @@ extern "C" int cyc_plan(const cyc_config* cfg, char* buf, size_t buflen) {
     write_err(buf, buflen, cyc::Engine::plan_string(g));
     return CYC_OK;
 }
+
+extern "C" int cyc_fold_state(cyc_est* est, void** dev_ptr, size_t* count, uint64_t* frames) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->fold_state(dev_ptr, count, frames));
+}
+
+extern "C" int cyc_fold_set_frames(cyc_est* est, uint64_t frames) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->set_frames(frames));
+}

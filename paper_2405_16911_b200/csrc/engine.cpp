@@ -214,6 +214,7 @@ Cfg from_c(const cyc_config* c) {
     g.emit_frames = c->emit_frames != 0;
     g.channels = c->channels;
     g.device = c->device;
+    g.origin = c->origin;
     return g;
 }
 
@@ -345,6 +346,7 @@ Status Engine::plan(const Cfg& cfg) {
     lag_lo_ = lags_req_.front();
     lag_hi_ = lags_req_.back();
     N_ = c_.win_len;
+    origin_ = c_.origin;
     need_ = (size_t)N_ + m_plus_ + m_minus_;  // estimator.cpp:20
     // layout (types.hpp:68-94)
     std::vector<int64_t> k;
@@ -527,8 +529,8 @@ Status Engine::grow_ring(int64_t cap_min) {
     const uint64_t mask = (uint64_t)cap - 1;
     CK(cudaStreamSynchronize(xs_));
     CK(cudaStreamSynchronize(cs_));
-    const int64_t hi = (int64_t)consumed_;
-    const int64_t lo = std::max<int64_t>(0, std::min<int64_t>((int64_t)frames_ * N_, hi) - (int64_t)need_);
+    const int64_t hi = origin_ + (int64_t)consumed_;
+    const int64_t lo = std::max<int64_t>(origin_, std::min<int64_t>(origin_ + (int64_t)frames_ * N_, hi) - (int64_t)need_);
     for (int r = 0; r < (cross_ ? 2 : 1); ++r) {
         float2*& ring = r ? ring_y_ : ring_x_;
         float2* nr = nullptr;
@@ -851,7 +853,7 @@ Status Engine::deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const 
         for (int fi = 0; fi < nflags_; ++fi) {
             cyc_frame_view v;
             v.frame_index = fidx[s];
-            v.start_abs = (uint64_t)m_minus_ + fidx[s] * (uint64_t)N_;
+            v.start_abs = (uint64_t)(origin_ + m_minus_) + fidx[s] * (uint64_t)N_;
             v.flag = (c_.flags == 3) ? (fi == 0 ? CYC_FLAG_CONV : CYC_FLAG_CONJ) : c_.flags;
             v.channel = chans[s];
             v.len = layout_len_;
@@ -871,7 +873,7 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
     if (avail <= frames_) return Status::ok();
     const uint64_t f0 = frames_, f1 = avail;
     const int C = c_.channels;
-    const int64_t lo_read = (int64_t)m_minus_ + (int64_t)f0 * N_ + lag_lo_;
+    const int64_t lo_read = origin_ + (int64_t)m_minus_ + (int64_t)f0 * N_ + lag_lo_;
 
     if (c_.mode == CYC_MODE_RECURSIVE || c_.emit_frames) {
         const size_t per_slot = (size_t)nflags_ * layout_len_ * 16 * 2 + (use_fold_ ? (size_t)t_pad_ * Pf_ * 32 : 0);
@@ -885,7 +887,7 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             std::vector<uint64_t> fidx;
             for (uint64_t f = fb; f < fe; ++f)
                 for (int ch = 0; ch < C; ++ch) {
-                    k0s.push_back((int64_t)m_minus_ + (int64_t)f * N_);
+                    k0s.push_back(origin_ + (int64_t)m_minus_ + (int64_t)f * N_);
                     chans.push_back(ch);
                     fidx.push_back(f);
                 }
@@ -925,8 +927,8 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             FoldSeg& g = segs[ch];
             g.x = ring_x_ + (size_t)ch * cap_;
             g.y = (cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_;
-            g.n_start = (int64_t)m_minus_ + (int64_t)f0 * N_;
-            g.n_end = (int64_t)m_minus_ + (int64_t)f1 * N_;
+            g.n_start = origin_ + (int64_t)m_minus_ + (int64_t)f0 * N_;
+            g.n_end = origin_ + (int64_t)m_minus_ + (int64_t)f1 * N_;
             g.x_lo = g.n_start + lag_lo_;
             g.x_hi = g.n_end + lag_hi_;
             g.mask = mask_;
@@ -941,8 +943,8 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             DirectSeg& g = segs[ch];
             g.x = ring_x_ + (size_t)ch * cap_;
             g.y = (cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_;
-            g.n_start = (int64_t)m_minus_ + (int64_t)f0 * N_;
-            g.n_end = (int64_t)m_minus_ + (int64_t)f1 * N_;
+            g.n_start = origin_ + (int64_t)m_minus_ + (int64_t)f0 * N_;
+            g.n_end = origin_ + (int64_t)m_minus_ + (int64_t)f1 * N_;
             g.x_lo = g.n_start + lag_lo_;
             g.x_hi = g.n_end + lag_hi_;
             g.mask = mask_;
@@ -1064,7 +1066,7 @@ Status Engine::ensure_staging() {
 // consumed_ + [0, len), on the copy stream; the compute stream waits for it.
 Status Engine::ingest_piece(const void* xv, const void* yv, size_t n, size_t off, size_t len, int kind, bool pinned) {
     const int C = c_.channels;
-    const int64_t abs0 = (int64_t)consumed_;
+    const int64_t abs0 = origin_ + (int64_t)consumed_;
     wait_ring_free(abs0 + (int64_t)len);
     if (kind == IN_DEVICE_F32) {
         for (int ch = 0; ch < C; ++ch) {
@@ -1167,17 +1169,18 @@ Status Engine::history_copy(int64_t a, int64_t b, bool save) {
 Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int kind) {
     const int C = c_.channels;
     const uint64_t c0 = consumed_, f0 = frames_;
-    // the samples the next frames still need: [f0*N, c0) (< buffer_need long)
-    const int64_t hb = std::min<int64_t>((int64_t)f0 * N_, (int64_t)c0);
+    // the samples the next frames still need: absolute [origin + f0*N, origin + c0)
+    const int64_t hb = origin_ + std::min<int64_t>((int64_t)f0 * N_, (int64_t)c0);
+    const int64_t hc = origin_ + (int64_t)c0;
     trace(nullptr);
     // Host chunks: let the whole chunk plus its history sit in the ring so the
     // copy stream never waits on compute inside the push (budget: 4 GiB).
     if (kind != IN_DEVICE_F32) {
-        const int64_t want = next_pow2((int64_t)c0 + (int64_t)n - hb + Q_);
+        const int64_t want = next_pow2(hc + (int64_t)n - hb + Q_);
         if (want > cap_ && (double)want * C * (cross_ ? 2 : 1) * sizeof(float2) <= 4.0 * (1ull << 30))
             TRY(grow_ring(want));
     }
-    TRY(history_copy(hb, (int64_t)c0, true));
+    TRY(history_copy(hb, hc, true));
     if (!S_pend_) CK(cudaMalloc(&S_pend_, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double)));
     CK(cudaMemsetAsync(S_pend_, 0, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
     CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
@@ -1199,7 +1202,7 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
         }
         for (size_t off = 0; off < n; off += (size_t)Q_) {
             const size_t len = std::min((size_t)Q_, n - off);
-            const int64_t abs0 = (int64_t)consumed_;
+            const int64_t abs0 = origin_ + (int64_t)consumed_;
             if (tr && off == (size_t)Q_) cudaEventRecord(tc, xs_);
             TRY(ingest_piece(xv, yv, n, off, len, kind, true));
             // GPU finite scan of the piece as it sits in the ring (wrap split)
@@ -1246,7 +1249,7 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
     // roll back: counters, history samples; the pending fold is discarded
     consumed_ = c0;
     frames_ = f0;
-    TRY(history_copy(hb, (int64_t)c0, false));
+    TRY(history_copy(hb, hc, false));
     CK(cudaStreamSynchronize(cs_));
     return data_error(key / C, (int)(key % C), kind, xv, yv, n);
 }
@@ -1257,7 +1260,7 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
 // chunk) are copied into the rings.
 Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, double* S) {
     const int C = c_.channels;
-    const int64_t c0 = (int64_t)consumed_, c1 = c0 + (int64_t)n;
+    const int64_t c0 = origin_ + (int64_t)consumed_, c1 = c0 + (int64_t)n;  // absolute
     const int64_t keep = std::min<int64_t>((int64_t)n, (int64_t)need_ + N_);
     wait_ring_free(c1);
     for (int ch = 0; ch < C; ++ch) {
@@ -1276,11 +1279,11 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     CK(cudaEventRecord(ev, xs_));
     CK(cudaStreamWaitEvent(cs_, ev, 0));
     ev_pool_.push_back(ev);
-    consumed_ = (uint64_t)c1;
+    consumed_ = (uint64_t)(c1 - origin_);
     const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
     if (avail > frames_) {
-        const int64_t s = (int64_t)m_minus_ + (int64_t)frames_ * N_;
-        const int64_t e = (int64_t)m_minus_ + (int64_t)avail * N_;
+        const int64_t s = origin_ + (int64_t)m_minus_ + (int64_t)frames_ * N_;
+        const int64_t e = origin_ + (int64_t)m_minus_ + (int64_t)avail * N_;
         const int64_t split = std::max(c0, c0 - (int64_t)lag_lo_);
         std::vector<FoldSeg> ring_segs, user_segs;
         for (int ch = 0; ch < C; ++ch) {
@@ -1463,6 +1466,26 @@ Status Engine::profile_read(uint64_t* launches, double* ms, double* flops) {
     if (launches) *launches = prof_launches_;
     if (ms) *ms = prof_ms_;
     if (flops) *flops = prof_flops_;
+    return Status::ok();
+}
+
+Status Engine::fold_state(void** dev_ptr, size_t* count, uint64_t* frames) {
+    if (!S_main_) {
+        Status u;
+        u.code = CYC_ERR_USAGE;
+        u.msg = "fold state exists only in block mode (emit_frames = 0) with a rational alpha grid";
+        return u;
+    }
+    CK(cudaStreamSynchronize(cs_));
+    if (dev_ptr) *dev_ptr = S_main_;
+    if (count) *count = (size_t)c_.channels * t_pad_ * Pf_ * 4;
+    if (frames) *frames = frames_;
+    return Status::ok();
+}
+
+Status Engine::set_frames(uint64_t frames) {
+    frames_ = frames;
+    avg_cache_frames_ = ~0ull;
     return Status::ok();
 }
 

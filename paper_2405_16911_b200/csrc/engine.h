@@ -47,6 +47,7 @@ struct Cfg {
     bool emit_frames = true;
     int channels = 1;
     int device = 0;
+    int64_t origin = 0;  // absolute index of the first pushed sample
 };
 
 // validate_config (proj/src/types.cpp:30-63) + rules of the extensions.
@@ -70,6 +71,9 @@ public:
     Status synchronize();
     // Fresh stream state, same config and allocations (== a new CyclicCorrelator(cfg)).
     Status reset();
+    // Block-mode fold state (time-sharded multi-GPU, checkpoint/resume).
+    Status fold_state(void** dev_ptr, size_t* count, uint64_t* frames);
+    Status set_frames(uint64_t frames);
     // Fold-kernel timing with CUDA events on the compute stream.
     void set_profiling(bool on) { prof_ = on; }
     Status profile_read(uint64_t* launches, double* ms, double* flops);
@@ -134,6 +138,7 @@ private:
     int m_plus_ = 0, m_minus_ = 0;
     size_t need_ = 0;
     int64_t N_ = 0;  // hop (win_len or emission interval)
+    int64_t origin_ = 0;  // absolute index of local sample 0 (phase anchor offset)
     int A_ = 0;      // output alphas (Full: N bins)
     size_t layout_len_ = 0;
     int64_t stride_a_ = 0, stride_t_ = 0;
