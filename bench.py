@@ -343,6 +343,217 @@ def run_ours(args, ws, rank, local):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# The other BASELINE.json configurations (single GPU; `--config c1|c3|c4|c5`).
+# C2 above is the headline workload the driver runs.
+# ---------------------------------------------------------------------------
+C1_CONV = [k / 8 for k in range(-2, 3)]
+C1_CONJ = [0.1 + k / 16 for k in range(-2, 3)]
+C3_ALPHAS = [m / 1024 for m in range(-128, 128)]
+
+
+def cfg_spec(name):
+    """(description, units of work, reference geometry) per config."""
+    if name == "c1":
+        F = (2 ** 20 - 4096 - 30) // 4096 + 1
+        return dict(workload="C1 GMSK BT0.3 8sps f_c=0.05 10 dB, 2^20 samples in 4096-sample pushes; Set N=4096 "
+                             "Symmetric(15); conv alpha=k/8, conj alpha=0.1+k/16 (k=-2..2); per-frame + coherent avg",
+                    updates=5 * 31 * F * 4096 * 2, samples=2 ** 20, F=F)
+    if name == "c3":
+        E = 65536
+        F = (2 ** 28 - E - 31) // E + 1
+        return dict(workload="C3 GMSK BT0.3 8sps f_c=0.02 0 dB, 2^28 samples in 8192-sample work() calls; recursive "
+                             "lambda=1-2^-12, 256 alpha=m/1024 x tau 0..31, conv, emit every 2^16",
+                    updates=256 * 32 * F * E, samples=2 ** 28, F=F)
+    if name == "c4":
+        F = (2 ** 22 - 256 - 31) // 256 + 1
+        return dict(workload="C4 64 channels x 2^22 (BPSK/QPSK-RRC, GMSK, noise; per-channel draws); Full N=256 "
+                             "lags 0..31, conv+conj, 128 alphas in [-1/4,1/4) counted, block average per channel",
+                    updates=64 * 2 * 128 * 32 * F * 256, samples=64 * 2 ** 22, F=F)
+    if name == "c5":
+        F = (2 ** 26 - 8192 - 255) // 8192 + 1
+        return dict(workload="C5 BPSK-RRC(0.35,5sps,0.07)+GMSK(BT0.3,8sps,-0.11)@-6dB, AWGN 3 dB, 2^26 samples; "
+                             "8192 alphas k/8192 x tau 0..255, conv+conj, block average",
+                    updates=8192 * 256 * F * 8192 * 2, samples=2 ** 26, F=F)
+    raise ValueError(name)
+
+
+def cfg_cpu_baseline(name, x, threads):
+    """Reference library on the host cores, bounded sample of the config's workload."""
+    os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    from oracle.oracle import RefLib
+    r = RefLib()
+    t0 = time.perf_counter()
+    if name == "c1":
+        xs = x.astype(np.complex128)
+        F = 0
+        for conj, al in ((0, C1_CONV), (1, C1_CONJ)):
+            fr, _ = r.stream(0, conj, 4096, xs, xs, alphas=al, max_lag=15, chunk=4096)
+            F = len(fr)
+        ups, smp = 5 * 31 * F * 4096 * 2, f"whole record, both estimators ({F} frames each), 4096-sample pushes"
+    elif name == "c3":
+        n = 2048 * 1024 + 31
+        xs = np.ascontiguousarray(x[:n])
+        _, F = r.block_average(1, 0, 1024, xs, xs, lags=list(range(32)))
+        ups, smp = 256 * 32 * F * 1024, (f"block-mode stand-in (no recursive mode in the reference): Full N=1024 "
+                                         f"lags 0..31, {F} frames, 256 of 1024 bins counted")
+    elif name == "c4":
+        F, nch = 0, 2
+        for c in range(nch):
+            xs = np.ascontiguousarray(x[c])
+            for conj in (0, 1):
+                _, F = r.block_average(1, conj, 256, xs, xs, lags=list(range(32)))
+        ups, smp = nch * 2 * 128 * 32 * F * 256, f"{nch} of 64 channels, whole channel ({F} frames), conv+conj"
+    else:
+        nf = 48
+        xs = np.ascontiguousarray(x[:nf * 8192 + 255])
+        for conj in (0, 1):
+            _, F = r.block_average(1, conj, 8192, xs, xs, lags=list(range(256)))
+        ups, smp = 8192 * 256 * F * 8192 * 2, f"{F} of 8191 frames, conv+conj"
+    dt = time.perf_counter() - t0
+    return {"value": ups / dt, "unit": UNIT, "cores": threads, "kind": "reference", "seconds": dt,
+            "sample": smp + f"; OMP_NUM_THREADS={threads}"}
+
+
+def run_config(args, ws, rank, local):
+    import torch
+    import paper_2405_16911_b200 as cyc
+    from paper_2405_16911_b200 import siggen
+
+    name = args.config
+    spec = cfg_spec(name)
+    dev = local
+    torch.cuda.set_device(dev)
+    if name == "c1":
+        x = siggen.c1_record(n=2 ** 20)
+    elif name == "c3":
+        x = siggen.c3_record(n=2 ** 28)
+    elif name == "c4":
+        x = np.stack([siggen.c4_channel(c, n=2 ** 22) for c in range(64)])
+    else:
+        x = siggen.c5_record(n=2 ** 26)
+    if args.impl == "reference":
+        if rank == 0:
+            vals = [cfg_cpu_baseline(name, x, os.cpu_count() or 1) for _ in range(max(1, args.steps))]
+            cb = dict(vals[-1])
+            cb["value"] = statistics.median(v["value"] for v in vals)
+            print(json.dumps({"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+                              "n_gpus": ws, "steps": args.steps, "warmup": 0, "higher_is_better": True,
+                              "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                              "config": {"workload": spec["workload"]}, "cpu_baseline": cb,
+                              "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                      "d2h_bytes_per_step": 0}}), flush=True)
+        return
+
+    ests = []
+    if name == "c1":
+        for conj, al in ((False, C1_CONV), (True, C1_CONJ)):
+            ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
+                mode=cyc.Mode.Set, conj=conj, win_len=4096, alphas=al, lag_spec=cyc.LagSpec.Symmetric(15),
+                device=dev)))
+    elif name == "c3":
+        ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
+            mode=cyc.Mode.Recursive, win_len=65536, alphas=C3_ALPHAS, lag_spec=cyc.LagSpec.Explicit(range(32)),
+            lam=1 - 2 ** -12, device=dev)))
+    elif name == "c4":
+        ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
+            mode=cyc.Mode.Full, win_len=256, lag_spec=cyc.LagSpec.Explicit(range(32)), flags=cyc.Flags.BOTH,
+            emit_frames=False, channels=64, device=dev)))
+    else:
+        ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
+            mode=cyc.Mode.Full, win_len=8192, lag_spec=cyc.LagSpec.Explicit(range(256)), flags=cyc.Flags.BOTH,
+            emit_frames=False, device=dev)))
+    est = ests[0]
+    stream = torch.cuda.ExternalStream(est.stream(), device=dev)
+    lay = cyc.layout_len(est.layout())
+    outs = [np.zeros(lay, dtype=np.complex128) for _ in range(2)]
+    n = x.shape[-1]
+
+    if name in ("c1", "c3"):
+        chunk = 4096 if name == "c1" else 8192
+        px = cyc.host_alloc(x.shape)
+        px[:] = x
+
+        def step_e2e():
+            nfr = 0
+            for e in ests:
+                e.reset()
+            for off in range(0, n, chunk):
+                for e in ests:
+                    nfr += len(e.push(px[off:off + chunk]))
+            for e in ests:
+                e.average(out=outs[0])
+            return nfr
+        step_dev = None
+    else:
+        dx = torch.from_numpy(x.view(np.float32)).to(f"cuda:{dev}")
+        px = cyc.host_alloc(x.shape)
+        px[:] = x
+
+        out_all = np.zeros((est.config().channels, 2, lay), dtype=np.complex128)
+
+        def finish():
+            est.average_all(out=out_all)  # every (channel, flag) table: one finalize + one D2H
+
+        def step_dev():
+            est.reset()
+            est.push_device(dx.data_ptr(), n)
+            finish()
+
+        def step_e2e():
+            est.reset()
+            est.push(px)
+            finish()
+
+    def timed(fn, k):
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / k
+
+    for _ in range(max(args.warmup, 1)):
+        (step_dev or step_e2e)()
+        if step_dev:
+            step_e2e()
+    est.profile(True)
+    n0, ms0, fl0 = est.profile_read()
+    l0 = sum(e.kernel_launches() for e in ests)
+    clk = Clocks(dev)
+    ms_dev = timed(step_dev, args.steps) if step_dev else None
+    ms_e2e = timed(step_e2e, args.steps) if not step_dev else None
+    clocks = clk.stop()
+    n1, ms1, fl1 = est.profile_read()
+    launches = sum(e.kernel_launches() for e in ests) - l0
+    if step_dev:
+        ms_e2e = timed(step_e2e, args.steps)
+    fold_ms = (ms1 - ms0) / max(1, n1 - n0)
+    fold_tf = (fl1 - fl0) / max(1, n1 - n0) / (fold_ms * 1e-3) / 1e12 if fold_ms > 0 else 0.0
+    peak = cyc.measure_fp32_peak(dev)
+    ms_val = ms_dev if ms_dev is not None else ms_e2e
+    line = {"metric": METRIC, "value": spec["updates"] / (ms_val * 1e-3), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_val, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 reductions)", "data": "synthetic",
+            "config": {"workload": spec["workload"], "algorithm": est.algorithm(),
+                       "value_path": "device-resident input" if step_dev else
+                       "host pushes of the stated chunk size (the workload is the streaming call pattern)"},
+            "msamples_per_s": spec["samples"] / (ms_val * 1e-3) / 1e6,
+            "e2e": {"value": spec["updates"] / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
+                    "h2d_bytes_per_step": int(x.size) * 8,
+                    "d2h_bytes_per_step": int(lay * 16 * (2 * est.config().channels if step_dev else len(ests)))},
+            "roofline": {"bound": "fp32", "kernel": "fold_kernel", "achieved": fold_tf, "peak": peak,
+                         "unit": "TFLOP/s", "frac": fold_tf / peak if peak else None, "traffic": None,
+                         "ms_per_launch": fold_ms, "launches_per_step": (n1 - n0) / args.steps},
+            "gpu_launches": launches, "clocks": clocks}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cfg_cpu_baseline(name, x, os.cpu_count() or 1)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -352,10 +563,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = one C2 record per GPU; strong = one record time-sharded + NCCL fold reduce")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE.json configuration (c2 = the headline workload)")
     args = ap.parse_args()
     ws, rank, local = dist_init()
     try:
-        if args.impl == "reference":
+        if args.config != "c2":
+            run_config(args, ws, rank, local)
+        elif args.impl == "reference":
             run_reference(args, ws, rank)
         else:
             run_ours(args, ws, rank, local)

@@ -152,6 +152,9 @@ int cyc_push_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size
  * MAGNITUDE needs emit_frames == 1.  out: layout_len values.
  * CYC_ERR_USAGE when no frame was emitted yet. */
 int cyc_average(cyc_est* est, int avg_mode, int flag, int channel, cyc_cf64* out);
+/* Every (channel, flag) table in one call: out = channels * num_flags *
+ * layout_len values, [channel][flag][layout] (flag order: CONV, CONJ). */
+int cyc_average_all(cyc_est* est, int avg_mode, cyc_cf64* out);
 
 /* Accessors (estimator.hpp:109-115). */
 size_t cyc_buffer_need(const cyc_est* est);

@@ -143,6 +143,7 @@ def lib() -> C.CDLL:
     L.cyc_plan.argtypes = [C.POINTER(_Config), C.c_char_p, sz]
     L.cyc_fold_state.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), C.POINTER(C.c_uint64)]
     L.cyc_fold_set_frames.argtypes = [vp, C.c_uint64]
+    L.cyc_average_all.argtypes = [vp, C.c_int, vp]
     L.cyc_reset.argtypes = [vp]
     L.cyc_profile_enable.argtypes = [vp, C.c_int]
     L.cyc_profile_read.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -507,6 +508,17 @@ class CyclicCorrelator:
         elif out.dtype != np.complex128 or out.size != n or not out.flags.c_contiguous:
             raise UsageError("out must be a contiguous complex128 array of layout_len values")
         self._check(self._L.cyc_average(self._h, int(mode), int(flag or 0), int(channel), out.ctypes.data))
+        return out
+
+    def average_all(self, mode: AverageMode = AverageMode.Coherent, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """All (channel, flag) tables: array [channels, flags, layout_len]."""
+        nf = int(self._L.cyc_num_flags(self._h))
+        shape = (self._cfg.channels, nf, layout_len(self._layout))
+        if out is None:
+            out = np.empty(shape, dtype=np.complex128)
+        elif out.shape != shape or out.dtype != np.complex128 or not out.flags.c_contiguous:
+            raise UsageError(f"out must be a contiguous complex128 array of shape {shape}")
+        self._check(self._L.cyc_average_all(self._h, int(mode), out.ctypes.data))
         return out
 
     def close(self):

@@ -267,3 +267,8 @@ extern "C" int cyc_fold_set_frames(cyc_est* est, uint64_t frames) {
     if (!est) return CYC_ERR_USAGE;
     return finish(est, est->e->set_frames(frames));
 }
+
+extern "C" int cyc_average_all(cyc_est* est, int avg_mode, cyc_cf64* out) {
+    if (!est || !out) return CYC_ERR_USAGE;
+    return finish(est, est->e->average_all(avg_mode, out));
+}

@@ -483,6 +483,7 @@ Engine::~Engine() {
     cudaFree(coh_);
     cudaFree(mag_);
     cudaFree(avg_dev_);
+    cudaFree(avg_all_dev_);
     cudaFreeHost(avg_host_);
     cudaFree(partials_);
     cudaFree(tw_);
@@ -1323,6 +1324,33 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
 // ---------------------------------------------------------------------------
 // averages (estimator.cpp:86-105)
 // ---------------------------------------------------------------------------
+
+// Every (channel, flag) table at once, [channel][flag][layout] -- one finalize
+// launch and one D2H for multi-channel block mode.
+Status Engine::average_all(int avg_mode, cyc_cf64* out) {
+    CK(cudaSetDevice(c_.device));
+    const int C = c_.channels;
+    const size_t per = (size_t)nflags_ * layout_len_;
+    const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
+    if (!block_fold || avg_mode != CYC_AVG_COHERENT || frames_ == 0) {
+        for (int ch = 0; ch < C; ++ch)
+            for (int fi = 0; fi < nflags_; ++fi) {
+                const int flag = nflags_ == 2 ? (fi ? CYC_FLAG_CONJ : CYC_FLAG_CONV) : c_.flags;
+                TRY(average(avg_mode, flag, ch, out + (size_t)ch * per + (size_t)fi * layout_len_));
+            }
+        return Status::ok();
+    }
+    if (avg_all_len_ < (size_t)C * per) {
+        CK(cudaStreamSynchronize(cs_));
+        cudaFree(avg_all_dev_);
+        CK(cudaMalloc(&avg_all_dev_, (size_t)C * per * sizeof(double2)));
+        avg_all_len_ = (size_t)C * per;
+    }
+    TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, avg_all_dev_));
+    CK(cudaMemcpyAsync(out, avg_all_dev_, (size_t)C * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
+    CK(cudaStreamSynchronize(cs_));
+    return Status::ok();
+}
 
 Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
     trace(nullptr);

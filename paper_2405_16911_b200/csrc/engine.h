@@ -66,6 +66,7 @@ public:
 
     Status push(const void* x, const void* y, size_t n, int kind, cyc_frame_sink sink, void* user);
     Status average(int avg_mode, int flag, int channel, cyc_cf64* out);
+    Status average_all(int avg_mode, cyc_cf64* out);
     Status compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw, size_t yw_len,
                           uint64_t k0, cyc_cf64* out);
     Status synchronize();
@@ -168,6 +169,8 @@ private:
     double* mag_ = nullptr;           // running magnitude sums
     double2* avg_dev_ = nullptr;      // average scratch
     double2* avg_host_ = nullptr;     // pinned average readback
+    double2* avg_all_dev_ = nullptr;  // all channels' tables (average_all)
+    size_t avg_all_len_ = 0;
     float* partials_ = nullptr;
     size_t partials_bytes_ = 0;
     double2* tw_ = nullptr;

@@ -410,3 +410,67 @@ def test_c2_scale_block_average_vs_oracle(cyc, oracle):
     mp = mean_power(x)
     assert_parity(est.average(flag=cyc.Flags.CONV), cv.T.reshape(-1), mp, what="C2 conv")
     assert_parity(est.average(flag=cyc.Flags.CONJ), cj.T.reshape(-1), mp, what="C2 conj")
+
+
+def test_average_all_matches_per_channel(cyc):
+    C_, L = 3, 20_000
+    xs = np.stack([rand_c(L, 200 + c) for c in range(C_)])
+    est = cyc.CyclicCorrelator(full_cfg(cyc, 256, list(range(8)), flags=cyc.Flags.BOTH, emit_frames=False, channels=C_))
+    est.push(xs)
+    allt = est.average_all()
+    assert allt.shape == (C_, 2, 8 * 256)
+    for c in range(C_):
+        assert np.max(np.abs(allt[c, 0] - est.average(flag=cyc.Flags.CONV, channel=c))) <= 1e-15
+        assert np.max(np.abs(allt[c, 1] - est.average(flag=cyc.Flags.CONJ, channel=c))) <= 1e-15
+
+
+# BASELINE configs at reduced sizes (full sizes run in bench.py --config cN)
+def test_c5_geometry_vs_oracle(cyc, oracle):
+    """Config 5: 8192-bin grid x lags 0..255, both flags (2^20 samples; oracle on 24 bins)."""
+    from paper_2405_16911_b200 import siggen
+    x = siggen.c5_record(n=1 << 20)
+    est = cyc.CyclicCorrelator(full_cfg(cyc, 8192, list(range(256)), flags=cyc.Flags.BOTH, emit_frames=False))
+    est.push(x)
+    F = est.frames_emitted()
+    bins = np.array([0, 1, 2, 7, 100, 1147, 1148, 2000, 2294, 4095, 4096, 5000, 6000, 7000, 7045, 8191,
+                     3, 8190, 1802, 6389, 12, 33, 4444, 8000])
+    cv, cj = oracle.block_fold(x, x, bins, 8192, list(range(256)), 0, F * 8192)
+    mp = mean_power(x)
+    got = est.average_all()  # [1, 2, 256 * 8192]
+    for fi, want in ((0, cv), (1, cj)):
+        g = got[0, fi].reshape(256, 8192)[:, bins]
+        assert_parity(g, want.T, mp, what=f"C5 flag {fi}")
+
+
+def test_c3_geometry_vs_oracle(cyc, oracle):
+    """Config 3: recursive lambda = 1 - 2^-12, 256 alphas m/1024 x lags 0..31, emit every 2^16
+    (2^18 samples in 8192-sample calls; oracle on 6 alphas)."""
+    from paper_2405_16911_b200 import siggen
+    x = siggen.gmsk(1 << 18, 0.3, 8, 0.02, 3).astype(np.complex64)
+    alphas = [m / 1024 for m in range(-128, 128)]
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Recursive, win_len=1 << 16, alphas=alphas,
+                              lag_spec=cyc.LagSpec.Explicit(range(32)), lam=1 - 2 ** -12)
+    est = cyc.CyclicCorrelator(cfg)
+    frames = []
+    for off in range(0, len(x), 8192):
+        frames += est.push(x[off:off + 8192])
+    assert len(frames) == (len(x) - (1 << 16) - 31) // (1 << 16) + 1
+    pick = [0, 5, 100, 128, 200, 255]
+    want = oracle.recursive(x.astype(complex), x.astype(complex), [alphas[i] for i in pick], list(range(32)), 0,
+                            1 - 2 ** -12, 1 << 16)
+    got = np.array([f.values.reshape(256, 32)[pick] for f in frames])
+    assert_parity(got, want, mean_power(x), what="C3")
+
+
+def test_c1_geometry_vs_oracle(cyc, oracle):
+    """Config 1: Set N=4096, Symmetric(15), conj alphas 0.1 + k/16 (P = 80), 4096-sample pushes."""
+    from paper_2405_16911_b200 import siggen
+    x = siggen.c1_record(n=1 << 16)
+    for conj, al in ((False, [k / 8 for k in range(-2, 3)]), (True, [0.1 + k / 16 for k in range(-2, 3)])):
+        est = cyc.CyclicCorrelator(set_cfg(cyc, 4096, 15, al, conj))
+        frames = []
+        for off in range(0, len(x), 4096):
+            frames += est.push(x[off:off + 4096])
+        want = oracle.stream(0, conj, 4096, x.astype(complex), x.astype(complex), alphas=al, max_lag=15)
+        assert len(frames) == len(want)
+        assert_parity(frames_array(frames), want, mean_power(x), what=f"C1 conj={conj}")
