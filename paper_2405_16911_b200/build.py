@@ -64,5 +64,20 @@ def build(force: bool = False) -> str:
     return LIB
 
 
+def build_tools(force: bool = False) -> str:
+    """tools/stream_bench: the C++ streaming driver bench.py uses for C1/C3."""
+    lib = build(force)
+    src = os.path.join(ROOT, "tools", "stream_bench.cpp")
+    exe = os.path.join(ROOT, "tools", "stream_bench")
+    if force or not os.path.exists(exe) or os.path.getmtime(exe) < max(os.path.getmtime(src), os.path.getmtime(lib)):
+        cmd = [NVCC, "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-x", "c++", src, "-o", exe,
+               f"-L{HERE}", "-lcycb200", "-Xlinker", f"-rpath,{HERE}"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"stream_bench build failed:\n{r.stdout}\n{r.stderr}")
+    return exe
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv))
+    print(build_tools())

@@ -101,10 +101,28 @@ struct Bad {
 // First non-finite sample in reference scan order (x before y per index,
 // proj/src/estimator.cpp:43-52); for f64 input also samples outside the
 // float32 range (the device computes in float32).
+// Branch-free screen of [i0, i1): true if any component may be non-finite
+// (float32: exponent all ones; float64: non-finite or beyond the float32
+// range).  Vectorises; only flagged blocks are rescanned exactly.
+inline bool screen(const cyc_cf32* p, size_t i0, size_t i1) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(p + i0);
+    const size_t m = 2 * (i1 - i0);
+    uint32_t acc = 0;
+    for (size_t i = 0; i < m; ++i) acc |= (uint32_t)((w[i] & 0x7f800000u) == 0x7f800000u);
+    return acc != 0;
+}
+inline bool screen(const cyc_cf64* p, size_t i0, size_t i1) {
+    const double* d = reinterpret_cast<const double*>(p + i0);
+    const size_t m = 2 * (i1 - i0);
+    int acc = 0;
+    for (size_t i = 0; i < m; ++i) acc |= !(std::fabs(d[i]) <= (double)FLT_MAX);  // NaN compares false
+    return acc != 0;
+}
+
 template <typename T>
 Bad scan_bad(const T* x, const T* y, size_t n, int channels) {
     auto bad_val = [](double v) { return !std::isfinite(v) || std::fabs(v) > (double)FLT_MAX; };
-    auto scan_range = [&](size_t i0, size_t i1, Bad& out) {
+    auto scan_exact = [&](size_t i0, size_t i1, Bad& out) {
         for (int c = 0; c < channels; ++c) {
             const T* xc = x + (size_t)c * n;
             const T* yc = y ? y + (size_t)c * n : nullptr;
@@ -120,6 +138,20 @@ Bad scan_bad(const T* x, const T* y, size_t n, int channels) {
                     out.channel = c;
                     break;
                 }
+            }
+        }
+    };
+    auto scan_range = [&](size_t i0, size_t i1, Bad& out) {
+        constexpr size_t BLK = 2048;
+        for (size_t b0 = i0; b0 < i1; b0 += BLK) {
+            const size_t b1 = std::min(i1, b0 + BLK);
+            bool flag = false;
+            for (int c = 0; c < channels && !flag; ++c) {
+                flag = screen(x + (size_t)c * n, b0, b1) || (y && screen(y + (size_t)c * n, b0, b1));
+            }
+            if (flag) {
+                scan_exact(b0, b1, out);
+                if (out.key != ~0ull) return;  // blocks are visited in order
             }
         }
     };
@@ -471,8 +503,24 @@ Status Engine::init(const Cfg& cfg) {
 }
 
 Engine::~Engine() {
+    if (std::getenv("CYC_PROFILE") && hprof_calls_)
+        std::fprintf(stderr, "[cyc] %llu pushes, host us/push: validate %.2f ingest %.2f emit %.2f (emit total %.1f ms)\n",
+                     (unsigned long long)hprof_calls_, hprof_us_[1] / hprof_calls_, hprof_us_[2] / hprof_calls_,
+                     hprof_us_[3] / hprof_calls_, hprof_us_[3] / 1e3);
+    if (std::getenv("CYC_PROFILE") && hprof_us_[7] > 0)
+        std::fprintf(stderr, "[cyc] %.0f frame-graph replays, GPU us/replay %.2f\n", hprof_us_[7],
+                     hprof_us_[6] / hprof_us_[7]);
     if (cs_) cudaStreamSynchronize(cs_);
     if (xs_) cudaStreamSynchronize(xs_);
+    for (auto& g : graphs_) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        cudaFreeHost(g.meta_host);
+        cudaFree(g.meta_dev);
+        cudaFree(g.S);
+        cudaFree(g.partials);
+        cudaFree(g.tables_dev);
+        cudaFreeHost(g.tables_host);
+    }
     cudaFree(ring_x_);
     cudaFree(ring_y_);
     cudaFree(S_main_);
@@ -665,7 +713,7 @@ void Engine::wait_ring_free(int64_t abs_end) {
 // compute primitives
 // ---------------------------------------------------------------------------
 
-Status Engine::fold(const std::vector<FoldSeg>& segs, double* S) {
+Status Engine::fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite) {
     struct G {
         int seg, rb, lb;
         int64_t p0, p1;
@@ -723,6 +771,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs, double* S) {
         L.lw = lw_;
         L.partials = partials_;
         L.S = S;
+        L.overwrite = overwrite ? 1 : 0;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
             launch_fold(L, cs_, r.a, r.b);
@@ -822,8 +871,8 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
             g.w_scale = w_scale;
             g.slot = (int)s;
         }
-        CK(cudaMemsetAsync(S_frames_, 0, slots * (size_t)t_pad_ * Pf_ * 4 * sizeof(double), cs_));
-        TRY(fold(segs, S_frames_));
+        // every (slot, lag, residue) of S_frames_ is stored by exactly one group: no memset
+        TRY(fold(segs, S_frames_, true));
         TRY(finalize(S_frames_, (int)slots, scale, nullptr, frames_dev_));
     } else {
         std::vector<DirectSeg> segs(slots);
@@ -847,8 +896,162 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
     return Status::ok();
 }
 
+bool Engine::graph_eligible(size_t slots) const {
+    static const bool off = std::getenv("CYC_NO_GRAPH") != nullptr;
+    return !off && use_fold_ && slots <= 16 && (N_ + Pf_ - 1) / Pf_ + 1 <= 4096;
+}
+
+void Engine::fill_frame_segs(FoldSeg* segs, const std::vector<int64_t>& k0s, const std::vector<int>& chans,
+                             bool recursive) const {
+    const float lam_log2 = recursive ? (float)std::log2(c_.lambda) : 0.f;
+    const float w_scale = recursive ? (float)(1.0 - c_.lambda) : 1.f;
+    for (size_t s = 0; s < k0s.size(); ++s) {
+        const int ch = chans[s];
+        FoldSeg g{};
+        g.x = ring_x_ + (size_t)ch * cap_;
+        g.y = (cross_ ? ring_y_ : ring_x_) + (size_t)ch * cap_;
+        g.n_start = k0s[s];
+        g.n_end = k0s[s] + N_;
+        g.x_lo = k0s[s] + lag_lo_;
+        g.x_hi = k0s[s] + N_ + lag_hi_;
+        g.mask = mask_;
+        g.w_ref = k0s[s] + N_ - 1;
+        g.w_log2 = lam_log2;
+        g.w_scale = w_scale;
+        g.slot = (int)s;
+        g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
+        segs[s] = g;
+    }
+}
+
+// One graph per frame-batch shape: fold (one tile per (slot, residue block,
+// lag block)) -> fp64 reduce (store) -> finalize -> running sums -> D2H.  The
+// per-frame descriptors live in mapped host memory and are rewritten before
+// each replay (the previous replay has been synchronised).
+Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vector<int>& chans, bool recursive,
+                               double2** tables) {
+    const size_t slots = k0s.size();
+    const size_t per = (size_t)nflags_ * layout_len_;
+    FrameGraph* g = nullptr;
+    for (auto& fg : graphs_)
+        if (fg.slots == slots) g = &fg;
+    if (!g) {
+        FrameGraph n;
+        n.slots = slots;
+        const int n_groups = (int)slots * n_rb_ * n_lb_;
+        // split each frame's periods over a few tiles so a frame is not one CTA's work
+        const int64_t maxper = (N_ + Pf_ - 1) / Pf_ + 1;
+        n.split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (maxper + 7) / 8));
+        n.n_tiles = n_groups * n.split;
+        const size_t rows_n = slots * (size_t)T_;
+        const size_t b_segs = slots * sizeof(FoldSeg), b_tiles = n.n_tiles * sizeof(FoldTile),
+                     b_groups = n_groups * sizeof(FoldGroup), b_rows = rows_n * sizeof(FinalRow);
+        // descriptors: pinned host copy rewritten per replay + device copy the
+        // kernels read (one captured H2D node; device loads, not PCIe reads)
+        n.meta_bytes = b_segs + b_tiles + b_groups + b_rows;
+        CK(cudaMallocHost(&n.meta_host, n.meta_bytes));
+        CK(cudaMalloc(&n.meta_dev, n.meta_bytes));
+        char* md = n.meta_dev;
+        n.segs = reinterpret_cast<FoldSeg*>(n.meta_host);
+        n.tiles = reinterpret_cast<FoldTile*>(n.meta_host + b_segs);
+        FoldGroup* groups = reinterpret_cast<FoldGroup*>(n.meta_host + b_segs + b_tiles);
+        FinalRow* rows = reinterpret_cast<FinalRow*>(n.meta_host + b_segs + b_tiles + b_groups);
+        int t = 0, gi = 0;
+        for (size_t s = 0; s < slots; ++s)
+            for (int rb = 0; rb < n_rb_; ++rb)
+                for (int lb = 0; lb < n_lb_; ++lb, ++gi) {
+                    groups[gi] = FoldGroup{(int)s, rb, lb, t, t + n.split, 0};
+                    for (int k = 0; k < n.split; ++k, ++t) n.tiles[t] = FoldTile{(int)s, rb, lb, gi, 0, 0};
+                }
+        size_t r = 0;
+        for (size_t s = 0; s < slots; ++s)
+            for (int tt = 0; tt < T_; ++tt) rows[r++] = FinalRow{(int)s, lags_req_[tt] - f_lo_, tt, (int)s};
+        CK(cudaMalloc(&n.S, slots * (size_t)t_pad_ * Pf_ * 4 * sizeof(double)));
+        CK(cudaMalloc(&n.partials, (size_t)n.n_tiles * TB_ * RB_ * sizeof(float4)));
+        CK(cudaMalloc(&n.tables_dev, slots * per * sizeof(double2)));
+        CK(cudaMallocHost(&n.tables_host, slots * per * sizeof(double2)));
+        fill_frame_segs(n.segs, k0s, chans, recursive);
+
+        FoldLaunch L{};
+        L.segs = reinterpret_cast<const FoldSeg*>(md);
+        L.tiles = reinterpret_cast<const FoldTile*>(md + b_segs);
+        L.groups = reinterpret_cast<const FoldGroup*>(md + b_segs + b_tiles);
+        L.n_tiles = n.n_tiles;
+        L.n_groups = n_groups;
+        L.Pf = (int)Pf_;
+        L.lag_lo = f_lo_;
+        L.t_pad = t_pad_;
+        L.lw = lw_;
+        L.partials = n.partials;
+        L.S = n.S;
+        L.overwrite = 1;
+        FinalizeLaunch Fz{};
+        Fz.S = n.S;
+        Fz.t_pad = t_pad_;
+        Fz.Pf = (int)Pf_;
+        Fz.rows = reinterpret_cast<const FinalRow*>(md + b_segs + b_tiles + b_groups);
+        Fz.n_rows = (int)rows_n;
+        Fz.flags = c_.flags;
+        Fz.bins = bins_dev_;
+        Fz.A = A_;
+        Fz.tw = tw_;
+        Fz.scale_default = recursive ? 1.0 : 1.0 / (double)N_;
+        Fz.out = n.tables_dev;
+        Fz.out_block_stride = (int64_t)per;
+        Fz.out_flag_stride = (int64_t)layout_len_;
+        Fz.stride_a = stride_a_;
+        Fz.stride_t = stride_t_;
+        Fz.use_fft = use_fft_ ? 1 : 0;
+        prepare_fold_kernels();  // attributes are set outside the capture
+        prepare_finalize_kernels();
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal));
+        cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_);
+        launch_fold(L, cs_);
+        launch_finalize(Fz, cs_);
+        if (!recursive)
+            launch_accum_frames(n.tables_dev, (int64_t)(slots / c_.channels), (int64_t)c_.channels * (int64_t)per,
+                                coh_, mag_, cs_);
+        cudaMemcpyAsync(n.tables_host, n.tables_dev, slots * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_);
+        CK(cudaStreamEndCapture(cs_, &graph));
+        CK(cudaGraphInstantiate(&n.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        graphs_.push_back(n);
+        g = &graphs_.back();
+    }
+    fill_frame_segs(g->segs, k0s, chans, recursive);
+    for (int t = 0; t < g->n_tiles; t += g->split) {
+        const FoldSeg& s = g->segs[g->tiles[t].seg];
+        const int64_t p0 = floor_div(s.n_start, Pf_), np = floor_div(s.n_end - 1, Pf_) + 1 - p0;
+        for (int k = 0; k < g->split; ++k) {  // an empty range (p0 == p1) folds nothing
+            g->tiles[t + k].p0 = p0 + np * k / g->split;
+            g->tiles[t + k].p1 = p0 + np * (k + 1) / g->split;
+        }
+    }
+    static const bool prof = std::getenv("CYC_PROFILE") != nullptr;
+    if (prof) {
+        if (!gev_[0]) {
+            cudaEventCreate(&gev_[0]);
+            cudaEventCreate(&gev_[1]);
+        }
+        cudaEventRecord(gev_[0], cs_);
+    }
+    CK(cudaGraphLaunch(g->exec, cs_));
+    if (prof) {
+        cudaEventRecord(gev_[1], cs_);
+        cudaEventSynchronize(gev_[1]);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, gev_[0], gev_[1]);
+        hprof_us_[6] += ms * 1e3;
+        hprof_us_[7] += 1;
+    }
+    launches_ += recursive ? 3 : 4;
+    *tables = g->tables_host;
+    return Status::ok();
+}
+
 Status Engine::deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const std::vector<int>& chans,
-                       cyc_frame_sink sink, void* user, bool& stop) {
+                       cyc_frame_sink sink, void* user, bool& stop, const double2* tables) {
     const size_t per = (size_t)nflags_ * layout_len_;
     for (size_t s = 0; s < n_slots && !stop; ++s) {
         for (int fi = 0; fi < nflags_; ++fi) {
@@ -858,7 +1061,7 @@ Status Engine::deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const 
             v.flag = (c_.flags == 3) ? (fi == 0 ? CYC_FLAG_CONV : CYC_FLAG_CONJ) : c_.flags;
             v.channel = chans[s];
             v.len = layout_len_;
-            v.values = reinterpret_cast<const cyc_cf64*>(frames_host_ + s * per + (size_t)fi * layout_len_);
+            v.values = reinterpret_cast<const cyc_cf64*>(tables + s * per + (size_t)fi * layout_len_);
             if (sink && sink(user, &v) != 0) {
                 stop = true;
                 break;
@@ -892,14 +1095,23 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                     chans.push_back(ch);
                     fidx.push_back(f);
                 }
-            TRY(compute_frames(k0s, chans, c_.mode == CYC_MODE_RECURSIVE));
             const size_t slots = k0s.size();
-            if (c_.mode != CYC_MODE_RECURSIVE) {
-                // running average_frames sums; slots are [frame][channel] blocks
-                launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
-                launches_ += 1;
+            double2* tables = frames_host_;
+            if (graph_eligible(slots)) {
+                // small frame batches: one CUDA-graph replay (fold, reduce, finalize,
+                // accumulate, D2H) instead of five launches and a memcpy
+                TRY(run_frame_graph(k0s, chans, c_.mode == CYC_MODE_RECURSIVE, &tables));
+            } else {
+                TRY(compute_frames(k0s, chans, c_.mode == CYC_MODE_RECURSIVE));
+                tables = frames_host_;
+                if (c_.mode != CYC_MODE_RECURSIVE) {
+                    // running average_frames sums; slots are [frame][channel] blocks
+                    launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
+                    launches_ += 1;
+                }
+                CK(cudaMemcpyAsync(frames_host_, frames_dev_, slots * per * sizeof(double2), cudaMemcpyDeviceToHost,
+                                   cs_));
             }
-            CK(cudaMemcpyAsync(frames_host_, frames_dev_, slots * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
             CK(cudaStreamSynchronize(cs_));
             if (c_.mode == CYC_MODE_RECURSIVE) {
                 // R_f = lam^N R_{f-1} + (weighted window sum)
@@ -909,18 +1121,18 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                     double* R = rec_R_.data() + (size_t)ch * per * 2;
                     double* hc = host_coh_.data() + (size_t)ch * per * 2;
                     double* hm = host_mag_.data() + (size_t)ch * per;
-                    double2* v = frames_host_ + s * per;
+                    double2* v = tables + s * per;
                     for (size_t i = 0; i < per; ++i) {
                         R[2 * i] = decay * R[2 * i] + v[i].x;
                         R[2 * i + 1] = decay * R[2 * i + 1] + v[i].y;
                         v[i] = make_double2(R[2 * i], R[2 * i + 1]);
                         hc[2 * i] += v[i].x;
                         hc[2 * i + 1] += v[i].y;
-                        hm[i] += std::hypot(v[i].x, v[i].y);
+                        hm[i] += std::sqrt(v[i].x * v[i].x + v[i].y * v[i].y);  // |R|, no overflow risk here
                     }
                 }
             }
-            if (c_.emit_frames && !stop) TRY(deliver(slots, fidx, chans, sink, user, stop));
+            if (c_.emit_frames && !stop) TRY(deliver(slots, fidx, chans, sink, user, stop, tables));
         }
     } else if (use_fold_) {
         std::vector<FoldSeg> segs(C);
@@ -968,7 +1180,19 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
 // push (estimator.cpp:39-84)
 // ---------------------------------------------------------------------------
 
+// CYC_PROFILE=1: accumulated host time per push phase, printed at destruction
+// (0: entry->validation, 1: validation, 2: ingest, 3: emit/deliver).
+void Engine::hprof(int phase) {
+    static const bool on = std::getenv("CYC_PROFILE") != nullptr;
+    if (!on) return;
+    const double now = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (phase > 0 && phase < 8) hprof_us_[phase] += now - hprof_t_;
+    hprof_t_ = now;
+}
+
 Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_frame_sink sink, void* user) {
+    hprof(-1);
+    ++hprof_calls_;
     CK(cudaSetDevice(c_.device));
     if (n == 0) return Status::ok();
     if (!xv) {
@@ -979,7 +1203,11 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     }
     const int C = c_.channels;
     const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
-    const bool pinned = kind == IN_HOST_F32 && is_pinned(xv) && (!yv || is_pinned(yv));
+    // Small chunks (< 1 MiB) are copied into our pinned staging even when the
+    // caller's memory is pinned: a host memcpy is cheaper than the stream sync
+    // that reading caller memory in place would need before returning.
+    const bool small = n * (size_t)C * sizeof(float2) < (1u << 20);
+    const bool pinned = kind == IN_HOST_F32 && !small && is_pinned(xv) && (!yv || is_pinned(yv));
     // Block-mode pushes from pinned or device memory validate on the GPU while
     // they are folded into a pending accumulator; the push commits only if the
     // whole chunk was finite, otherwise the state is rolled back
@@ -1007,6 +1235,7 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
             }
         }
         if (bad.key != ~0ull) return data_error(bad.key, bad.channel, kind, xv, yv, n);
+        hprof(1);
     }
     // cross-correlation: materialise a y ring (copy x history on first use)
     if (yv && !cross_) {
@@ -1022,9 +1251,12 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     }
     for (size_t off = 0; off < n; off += (size_t)Q_) {
         const size_t len = std::min((size_t)Q_, n - off);
+        hprof(0);
         TRY(ingest_piece(xv, yv, n, off, len, kind, pinned));
+        hprof(2);
         consumed_ += len;
         TRY(emit_new_frames(sink, user, S_main_));
+        hprof(3);
     }
     // caller memory may not be retained after return
     if (pinned || kind == IN_DEVICE_F32) CK(cudaStreamSynchronize(xs_));

@@ -107,7 +107,7 @@ private:
     void* upload(const void* src, size_t bytes);
 
     // Fold `segs` (one per slot) into S (slots x t_pad x Pf x 4 fp64).
-    Status fold(const std::vector<FoldSeg>& segs, double* S);
+    Status fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite = false);
     // Finalize slots [0, nslots) of S into out tables (out_block = slot) with per-slot scale.
     Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
                     double2* out);
@@ -127,7 +127,35 @@ private:
     Status push_speculative(const void* xv, const void* yv, size_t n, int kind);
     Status fold_device_chunk(const float2* x, const float2* y, size_t n, double* S);
     Status deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const std::vector<int>& chans,
-                   cyc_frame_sink sink, void* user, bool& stop);
+                   cyc_frame_sink sink, void* user, bool& stop, const double2* tables);
+
+    // CUDA-graph replay of the per-frame pipeline for small frame batches
+    struct FrameGraph {
+        size_t slots = 0;
+        cudaGraphExec_t exec = nullptr;
+        char* meta_host = nullptr;  // pinned: segs | tiles | groups | rows
+        char* meta_dev = nullptr;   // device copy (captured H2D node)
+        size_t meta_bytes = 0;
+        FoldSeg* segs = nullptr;
+        FoldTile* tiles = nullptr;
+        int n_tiles = 0;
+        int split = 1;  // tiles per (slot, residue block, lag block)
+        double* S = nullptr;
+        float* partials = nullptr;
+        double2* tables_dev = nullptr;
+        double2* tables_host = nullptr;  // pinned
+    };
+    std::vector<FrameGraph> graphs_;
+    void hprof(int phase);
+    double hprof_us_[8] = {};
+    double hprof_t_ = 0.0;
+    uint64_t hprof_calls_ = 0;
+    cudaEvent_t gev_[2] = {};
+    bool graph_eligible(size_t slots) const;
+    Status run_frame_graph(const std::vector<int64_t>& k0s, const std::vector<int>& chans, bool recursive,
+                           double2** tables);
+    void fill_frame_segs(FoldSeg* segs, const std::vector<int64_t>& k0s, const std::vector<int>& chans,
+                         bool recursive) const;
 
     // ---- configuration ----
     Cfg c_;

@@ -63,41 +63,61 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
     }
 }
 
-// Direct DFT: grid (n_rows, n_flag_tables, ceil(A / 256)); thread per alpha.
-constexpr int DFT_CHUNK = 2048;
-__global__ void __launch_bounds__(256) finalize_dft_kernel(FinalizeLaunch L) {
-    __shared__ double2 q[DFT_CHUNK];
+// Direct DFT: grid (n_rows, n_flag_tables, ceil(A / DFT_AB)); a CTA computes
+// DFT_AB alphas of one row with its 256 threads striding over the residues
+// (twiddle index advanced exactly mod Pf), then a fixed-order block reduction.
+constexpr int DFT_T = 256;
+constexpr int DFT_AB = 8;
+__global__ void __launch_bounds__(DFT_T) finalize_dft_kernel(FinalizeLaunch L) {
+    __shared__ double2 red[DFT_T / 32][DFT_AB];
     const FinalRow row = L.rows[blockIdx.x];
     const int fi = blockIdx.y;
     const int flag_bit = (L.flags == 2) ? 1 : fi;
     const int Pf = L.Pf;
-    const int a = blockIdx.z * blockDim.x + threadIdx.x;
-    const bool active = a < L.A;
-    const int64_t bin = active ? L.bins[a] : 0;
+    const int a0 = blockIdx.z * DFT_AB;
+    const int na = min(DFT_AB, L.A - a0);
     const double* Srow = L.S + ((size_t)row.slot * L.t_pad + row.t_span) * (size_t)Pf * 4;
-    double re = 0.0, im = 0.0;
-    for (int r0 = 0; r0 < Pf; r0 += DFT_CHUNK) {
-        const int n = min(DFT_CHUNK, Pf - r0);
-        __syncthreads();
-        for (int r = threadIdx.x; r < n; r += blockDim.x) q[r] = combine(Srow + (size_t)(r0 + r) * 4, flag_bit);
-        __syncthreads();
-        if (active) {
-            int64_t idx = (bin * r0) % Pf;
-            for (int r = 0; r < n; ++r) {
-                const double2 w = L.tw[idx];
-                const double2 v = q[r];
-                re += v.x * w.x - v.y * w.y;
-                im += v.x * w.y + v.y * w.x;
-                idx += bin;
-                if (idx >= Pf) idx -= Pf;
-            }
+    int idx[DFT_AB], step[DFT_AB];
+    double re[DFT_AB], im[DFT_AB];
+#pragma unroll
+    for (int k = 0; k < DFT_AB; ++k) {
+        const int64_t bin = k < na ? L.bins[a0 + k] : 0;
+        idx[k] = (int)((bin * threadIdx.x) % Pf);
+        step[k] = (int)((bin * DFT_T) % Pf);
+        re[k] = im[k] = 0.0;
+    }
+    for (int r = threadIdx.x; r < Pf; r += DFT_T) {
+        const double2 v = combine(Srow + (size_t)r * 4, flag_bit);
+#pragma unroll
+        for (int k = 0; k < DFT_AB; ++k) {
+            const double2 w = L.tw[idx[k]];
+            re[k] += v.x * w.x - v.y * w.y;
+            im[k] += v.x * w.y + v.y * w.x;
+            idx[k] += step[k];
+            if (idx[k] >= Pf) idx[k] -= Pf;
         }
     }
-    if (!active) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < DFT_AB; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            re[k] += __shfl_down_sync(0xffffffffu, re[k], o);
+            im[k] += __shfl_down_sync(0xffffffffu, im[k], o);
+        }
+        if (lane == 0) red[warp][k] = make_double2(re[k], im[k]);
+    }
+    __syncthreads();
+    if (threadIdx.x >= na) return;
+    const int k = threadIdx.x;
+    double sr = 0.0, si = 0.0;
+    for (int w = 0; w < DFT_T / 32; ++w) {
+        sr += red[w][k].x;
+        si += red[w][k].y;
+    }
     const double sc = L.row_scale ? L.row_scale[row.out_block] : L.scale_default;
     double2* out = L.out + (size_t)row.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride +
                    (size_t)row.t_out * L.stride_t;
-    out[(size_t)a * L.stride_a] = make_double2(re * sc, im * sc);
+    out[(size_t)(a0 + k) * L.stride_a] = make_double2(sr * sc, si * sc);
 }
 
 }  // namespace
@@ -117,8 +137,17 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
         }
         finalize_fft_kernel<<<dim3(L.n_rows, nflag), 512, smem, st>>>(L, lg);
     } else {
-        finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + 255) / 256), 256, 0, st>>>(L);
+        finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
     }
 }
 
+}  // namespace cyc
+
+namespace cyc {
+void prepare_finalize_kernels() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * (int)sizeof(double2));
+    done = true;
+}
 }  // namespace cyc

@@ -297,10 +297,17 @@ __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
     }
     const int slot = L.segs[g.seg].slot;
     double* d = L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4;
-    d[0] += s0;
-    d[1] += s1;
-    d[2] += s2;
-    d[3] += s3;
+    if (L.overwrite) {
+        d[0] = s0;
+        d[1] = s1;
+        d[2] = s2;
+        d[3] = s3;
+    } else {
+        d[0] += s0;
+        d[1] += s1;
+        d[2] += s2;
+        d[3] += s3;
+    }
 }
 
 template <int LW>
@@ -329,4 +336,16 @@ void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEven
     }
 }
 
+}  // namespace cyc
+
+namespace cyc {
+// Set the dynamic-shared-memory attributes outside any stream capture.
+void prepare_fold_kernels() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(fold_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<4>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<8>::SMEM);
+    done = true;
+}
 }  // namespace cyc

@@ -62,10 +62,14 @@ struct FoldLaunch {
     int lw;              // lag lanes per warp: 2, 4 or 8  (TB = 8*lw, RB = 1024/lw)
     float* partials;     // [n_tiles][TB][RB] float4
     double* S;           // [slots][t_pad][Pf][4] fp64 accumulators
+    int overwrite;       // 1: reduce stores (fresh per-frame slots, no memset); 0: accumulates
 };
 
 // fold + fp64 reduce; optional events bracket the fold kernel alone (profiling)
 void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+
+void prepare_fold_kernels();      // set smem attributes (call outside stream capture)
+void prepare_finalize_kernels();
 
 inline int fold_tb(int lw) { return 8 * lw; }
 inline int fold_rb(int lw) { return 1024 / lw; }
