@@ -28,7 +28,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcycb200.so")
+LIB_PATH = os.environ.get("CYC_LIB", os.path.join(HERE, "libcycb200.so"))  # CYC_LIB: diagnostic builds only
 
 __all__ = [
     "Mode", "Flags", "AverageMode", "LagSpec", "EstimatorConfig", "SetLayout", "FullLayout",

@@ -26,7 +26,10 @@ __global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span) {
     const int split = blockIdx.x % L.splits;
     const int a = (blockIdx.x / L.splits) % L.A;
     const int si = blockIdx.x / (L.splits * L.A);
-    const DirectSeg seg = L.segs[si];
+    __shared__ DirectSeg s_seg;  // descriptors may be in mapped host memory: read once
+    if (threadIdx.x == 0) s_seg = L.segs[si];
+    __syncthreads();
+    const DirectSeg& seg = s_seg;
     const uint64_t afx = L.alpha_fx[a];
     const int64_t cnt = seg.n_end - seg.n_start;
     const int64_t b0 = seg.n_start + cnt * split / L.splits;
@@ -95,9 +98,12 @@ __global__ void direct_reduce_kernel(DirectLaunch L) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int a = blockIdx.y;
     const int si = blockIdx.z;
-    if (t >= L.T) return;
     const float2* part = reinterpret_cast<const float2*>(L.partials);
-    const DirectSeg seg = L.segs[si];
+    __shared__ DirectSeg s_seg;  // descriptors may be in mapped host memory: read once
+    if (threadIdx.x == 0) s_seg = L.segs[si];
+    __syncthreads();
+    if (t >= L.T) return;
+    const DirectSeg& seg = s_seg;
     int fi = 0;
     for (int f = 0; f < 2; ++f) {
         if (!(L.flags & (1 << f))) continue;

@@ -214,6 +214,8 @@ private:
     static constexpr int META_SLOTS = 4;
     char* meta_host_ = nullptr;
     char* meta_dev_ = nullptr;
+    char* meta_shadow_ = nullptr;  // device copy of the arena
+    bool meta_mapped_now_ = false; // read descriptors mapped (inside pinned-host pushes)
     size_t meta_slot_bytes_ = 0;
     size_t meta_used_ = 0;
     int meta_slot_ = 0;

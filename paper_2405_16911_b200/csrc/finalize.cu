@@ -30,7 +30,10 @@ __device__ __forceinline__ double2 combine(const double* s, int flag_bit) {
 // grid: (n_rows, n_flag_tables); one CTA per (row, flag).
 __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
     extern __shared__ double2 buf[];
-    const FinalRow row = L.rows[blockIdx.x];
+    __shared__ FinalRow s_row;  // descriptors may be in mapped host memory: read once
+    if (threadIdx.x == 0) s_row = L.rows[blockIdx.x];
+    __syncthreads();
+    const FinalRow row = s_row;
     const int fi = blockIdx.y;  // index among requested flags
     const int flag_bit = (L.flags == 2) ? 1 : fi;
     const int Pf = L.Pf;
@@ -70,7 +73,10 @@ constexpr int DFT_T = 256;
 constexpr int DFT_AB = 8;
 __global__ void __launch_bounds__(DFT_T) finalize_dft_kernel(FinalizeLaunch L) {
     __shared__ double2 red[DFT_T / 32][DFT_AB];
-    const FinalRow row = L.rows[blockIdx.x];
+    __shared__ FinalRow s_row;  // descriptors may be in mapped host memory: read once
+    if (threadIdx.x == 0) s_row = L.rows[blockIdx.x];
+    __syncthreads();
+    const FinalRow row = s_row;
     const int fi = blockIdx.y;
     const int flag_bit = (L.flags == 2) ? 1 : fi;
     const int Pf = L.Pf;

@@ -102,6 +102,9 @@ __device__ __forceinline__ void mac_period(float2 (&lo)[R][U], float2 (&hi)[R][U
     }
     const float yr[4] = {r.y[0].x, r.y[0].z, r.y[1].x, r.y[1].z};
     const float yi[4] = {r.y[0].y, r.y[0].w, r.y[1].y, r.y[1].w};
+    // lo/hi of one (a, u) share the x pair (operand reuse cache); ptxas
+    // schedules these pairs back to back.  Measured ceiling of this operand
+    // pattern (tools/microbench/ffma2_pattern.cu): ~75% of the FP32 peak.
 #pragma unroll
     for (int a = 0; a < R; ++a)
 #pragma unroll
@@ -130,8 +133,16 @@ template <int LW>
 __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
     using G = Geo<LW>;
     extern __shared__ __align__(16) float4 smem4[];
-    const FoldTile tile = L.tiles[blockIdx.x];
-    const FoldSeg seg = L.segs[tile.seg];
+    // Launch descriptors may live in mapped host memory: copy them to shared
+    // memory once, so re-reads under register pressure never cross PCIe.
+    __shared__ FoldTile s_tile;
+    __shared__ FoldSeg s_seg;
+    if (threadIdx.x == 0) s_tile = L.tiles[blockIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) s_seg = L.segs[s_tile.seg];
+    __syncthreads();
+    const FoldTile& tile = s_tile;
+    const FoldSeg& seg = s_seg;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int rho = warp * G::RL + (lane % G::RL);  // residues 4*rho .. 4*rho+3
@@ -253,10 +264,16 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
         load_period<LW>(ra, st, kap, rho);
         int q = 0;
         for (; q + 1 < nq; q += 2) {
+#ifndef CYC_DIAG_NOLDS  // diagnostic build only: FFMA2 stream without the per-period smem loads
             load_period<LW>(rb, st + (q + 1) * G::PER, kap, rho);
+#else
+            if (q == 0) load_period<LW>(rb, st + (q + 1) * G::PER, kap, rho);
+#endif
             if (weighted) weight_period(ra, seg, (pbeg + q) * Pf + res0 + 4 * rho);
             mac_period(lo, hi, ra);
+#ifndef CYC_DIAG_NOLDS
             if (q + 2 < nq) load_period<LW>(ra, st + (q + 2) * G::PER, kap, rho);
+#endif
             if (weighted) weight_period(rb, seg, (pbeg + q + 1) * Pf + res0 + 4 * rho);
             mac_period(lo, hi, rb);
         }
@@ -279,7 +296,14 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
 
 // S[slot][lb*TB + lag][rb*RB + res][4] += sum over the group's tiles (fixed order, fp64).
 __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
-    const FoldGroup g = L.groups[blockIdx.y];
+    __shared__ FoldGroup s_g;
+    __shared__ int s_slot;
+    if (threadIdx.x == 0) {
+        s_g = L.groups[blockIdx.y];
+        s_slot = L.segs[s_g.seg].slot;
+    }
+    __syncthreads();
+    const FoldGroup g = s_g;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= TB * RB) return;
     const int lag = e / RB, res = e - lag * RB;
@@ -295,7 +319,7 @@ __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
         s2 += v.z;
         s3 += v.w;
     }
-    const int slot = L.segs[g.seg].slot;
+    const int slot = s_slot;
     double* d = L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4;
     if (L.overwrite) {
         d[0] = s0;
