@@ -44,7 +44,8 @@ typedef enum {
     CYC_ERR_USAGE = 2,    /* UsageError   (mismatched chunks, bad arguments)   */
     CYC_ERR_DATA = 3,     /* DataError    (non-finite sample; absolute index)  */
     CYC_ERR_CUDA = 4,     /* device / driver failure (no CPU fallback exists)  */
-    CYC_ERR_INTERNAL = 5  /* std::logic_error equivalent                       */
+    CYC_ERR_INTERNAL = 5, /* std::logic_error equivalent                       */
+    CYC_ERR_IO = 6        /* IoError / FormatError (errors.hpp:32-38)          */
 } cyc_status;
 
 /* Estimator mode (proj/include/cycstat/types.hpp:22-25) plus the
@@ -145,6 +146,22 @@ int cyc_push_f64(cyc_est* est, const cyc_cf64* x, const cyc_cf64* y, size_t n,
 /* Same, from samples already resident in device memory (GPU pipelines). */
 int cyc_push_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size_t n,
                     cyc_frame_sink sink, void* user);
+
+/* read_cf32 + push (proj/src/io.cpp:90-103, proj/tools/main.cpp:212-214):
+ * the cf32 file (interleaved little-endian float32 I/Q) is pushed as ONE
+ * chunk -- validated whole, then streamed from the page cache into the device
+ * rings without an fp64 copy.  CYC_ERR_IO for open/read failures and a length
+ * that is not a multiple of 8 bytes (FormatError). */
+int cyc_push_cf32_file(cyc_est* est, const char* path, cyc_frame_sink sink, void* user);
+
+/* estimate_cfo_ccf (proj/src/impair.cpp:45-115): conjugate Full-mode lag-0
+ * scan over num_frames windows of N samples, magnitude average (on the
+ * device), peak within +-N/8 bins of expected_beta, median test, log-parabola
+ * refinement; *eps_out = wrapped(beta_peak - expected_beta) / 2.
+ * CYC_ERR_USAGE for the reference's argument errors, CYC_ERR_DATA with
+ * "no feature detected ..." for its NoFeatureError. */
+int cyc_estimate_cfo_ccf(const cyc_cf32* x, size_t n, double expected_beta, int N, int num_frames,
+                         int device, double* eps_out, char* err, size_t errlen);
 
 /* average_frames(frames emitted so far, mode) (proj/src/estimator.cpp:86-105)
  * for one (flag, channel), without materialising the frames: the coherent

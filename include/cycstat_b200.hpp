@@ -48,6 +48,12 @@ struct DataError : std::runtime_error {
     std::int64_t index = -1;
     DataError(const std::string& m, std::int64_t i) : std::runtime_error(m), index(i) {}
 };
+struct NoFeatureError : DataError {  // errors.hpp:44-46
+    explicit NoFeatureError(const std::string& m) : DataError(m, -1) {}
+};
+struct IoError : std::runtime_error {  // errors.hpp:32-34
+    explicit IoError(const std::string& m) : std::runtime_error(m) {}
+};
 struct DeviceError : std::runtime_error {  // no CPU fallback exists
     explicit DeviceError(const std::string& m) : std::runtime_error(m) {}
 };
@@ -200,6 +206,7 @@ namespace detail {
     if (code == CYC_ERR_USAGE) throw UsageError(msg);
     if (code == CYC_ERR_DATA) throw DataError(msg, index);
     if (code == CYC_ERR_CUDA) throw DeviceError(msg);
+    if (code == CYC_ERR_IO) throw IoError(msg);
     throw std::logic_error(msg);
 }
 }  // namespace detail
@@ -239,6 +246,11 @@ public:
         return run([&](cyc_frame_sink s, void* u) {
             return cyc_push(h_, reinterpret_cast<const cyc_cf32*>(x), reinterpret_cast<const cyc_cf32*>(y), n, s, u);
         });
+    }
+
+    // read_cf32 (io.cpp:90-103) + push of the whole file, y auto
+    std::vector<CyclicFrame> push_file(const std::string& path) {
+        return run([&](cyc_frame_sink s, void* u) { return cyc_push_cf32_file(h_, path.c_str(), s, u); });
     }
 
     // average_frames over every frame emitted so far, without materialising them
@@ -322,6 +334,19 @@ inline std::vector<cx> compute_full_window(const std::vector<cx>& xw, const std:
                                            err.data(), err.size());
     if (rc) detail::raise(rc, err.c_str());
     return out;
+}
+
+// impair.cpp:45-115 on the device
+inline double estimate_cfo_ccf(const std::vector<cx>& x, double expected_beta, int N, int num_frames,
+                               int device = 0) {
+    std::vector<std::complex<float>> xf(x.begin(), x.end());
+    double eps = 0.0;
+    std::string err(1024, '\0');
+    const int rc = cyc_estimate_cfo_ccf(reinterpret_cast<const cyc_cf32*>(xf.data()), xf.size(), expected_beta, N,
+                                        num_frames, device, &eps, err.data(), err.size());
+    if (rc == CYC_ERR_DATA && std::string(err.c_str()).rfind("no feature", 0) == 0) throw NoFeatureError(err.c_str());
+    if (rc) detail::raise(rc, err.c_str());
+    return eps;
 }
 
 }  // namespace cycstat_b200

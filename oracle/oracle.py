@@ -162,7 +162,25 @@ class RefLib:
         L.ref_awgn.argtypes = [C.c_size_t, C.c_double, C.c_uint64, _dp]
         L.ref_apply_cfo.argtypes = [_dp, C.c_size_t, C.c_double, C.c_double]
         L.ref_add_noise_snr.argtypes = [_dp, C.c_size_t, C.c_double, C.c_uint64]
+        L.ref_cpm.argtypes = [C.c_size_t, C.c_double, C.c_double, C.c_int, C.c_uint64, _dp]
+        L.ref_estimate_cfo_ccf.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, _dp]
         self.lib = L
+
+    def cpm(self, n, h=0.5, bt=0.25, sps=8, seed=0):
+        out = np.zeros(2 * n)
+        self._err(self.lib.ref_cpm(n, h, bt, sps, seed, _p(out, _dp)))
+        return out.view(np.complex128)
+
+    def estimate_cfo_ccf(self, x, beta, N, frames):
+        """eps, or raises LookupError for NoFeatureError / ValueError for UsageError."""
+        xd = _cd(x)
+        eps = C.c_double()
+        rc = self.lib.ref_estimate_cfo_ccf(_p(xd, _dp), len(x), beta, N, frames, C.byref(eps))
+        if rc == 4:
+            raise LookupError(self.lib.ref_last_error().decode())
+        if rc:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return eps.value
 
     def _err(self, rc):
         if rc:

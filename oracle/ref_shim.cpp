@@ -192,6 +192,31 @@ int ref_gmsk(std::size_t len, double bt, int sps, std::uint64_t seed, double* ou
     } catch (const std::exception& e) { return fail(e, 1); }
 }
 
+// CPM record with modulation index h (proj/tests/test_impair.cpp gmsk_record).
+int ref_cpm(std::size_t len, double h, double bt, int sps, std::uint64_t seed, double* out) {
+    try {
+        CpmParams p;
+        p.h = h;
+        p.bt = bt;
+        p.sps = sps;
+        const auto syms = random_symbols(p.alphabet_size, (len + sps - 1) / sps, seed);
+        auto x = cpm_modulate(p, syms);
+        x.resize(len);
+        store(x, out);
+        return 0;
+    } catch (const std::exception& e) { return fail(e, 1); }
+}
+
+// estimate_cfo_ccf (proj/src/impair.cpp:45-115); 4 = NoFeatureError.
+int ref_estimate_cfo_ccf(const double* x, std::size_t len, double beta, int N, int frames, double* eps) {
+    try {
+        *eps = estimate_cfo_ccf(load(x, len), beta, N, frames);
+        return 0;
+    } catch (const NoFeatureError& e) { return fail(e, 4); }
+    catch (const UsageError& e) { return fail(e, 1); }
+    catch (const std::exception& e) { return fail(e, 5); }
+}
+
 int ref_tone(double f0, double phi0, std::size_t len, double* out) {
     store(tone(f0, phi0, len), out);
     return 0;

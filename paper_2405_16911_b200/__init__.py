@@ -61,6 +61,14 @@ class DataError(RuntimeError):
         self.index = index
 
 
+class NoFeatureError(DataError):
+    """errors.hpp:44-46: estimate_cfo_ccf found no conjugate feature."""
+
+
+class IoError(RuntimeError):
+    """errors.hpp:32-34 (FormatError, errors.hpp:36-38, is reported the same way)."""
+
+
 class CudaError(RuntimeError):
     """Device failure -- there is no CPU fallback."""
 
@@ -144,6 +152,9 @@ def lib() -> C.CDLL:
     L.cyc_fold_state.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), C.POINTER(C.c_uint64)]
     L.cyc_fold_set_frames.argtypes = [vp, C.c_uint64]
     L.cyc_average_all.argtypes = [vp, C.c_int, vp]
+    L.cyc_push_cf32_file.argtypes = [vp, C.c_char_p, _SINK, vp]
+    L.cyc_estimate_cfo_ccf.argtypes = [vp, sz, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                       C.c_char_p, sz]
     L.cyc_reset.argtypes = [vp]
     L.cyc_profile_enable.argtypes = [vp, C.c_int]
     L.cyc_profile_read.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -358,6 +369,8 @@ def _raise(code: int, msg: str, index: int = -1):
         raise DataError(msg, index)
     if code == 4:
         raise CudaError(msg)
+    if code == 6:
+        raise IoError(msg)
     raise LogicError(msg)
 
 
@@ -491,6 +504,13 @@ class CyclicCorrelator:
         out, self._frames = self._frames, []
         return out
 
+    def push_file(self, path: str) -> list:
+        """read_cf32 + push (io.cpp:90-103): the whole cf32 file as one chunk."""
+        self._frames = []
+        self._check(self._L.cyc_push_cf32_file(self._h, os.fsencode(path), self._sink, None))
+        out, self._frames = self._frames, []
+        return out
+
     def push_device(self, x_ptr: int, n: int, y_ptr: Optional[int] = None) -> list:
         """Push samples already resident in device memory (complex64)."""
         self._frames = []
@@ -531,6 +551,33 @@ class CyclicCorrelator:
             self.close()
         except Exception:
             pass
+
+
+def estimate_cfo_ccf(x, expected_beta: float, N: int, num_frames: int, device: int = 0) -> float:
+    """impair.cpp:45-115 on the device: CFO from the conjugate lag-0 scan."""
+    xa = _as_c64(x)
+    eps = C.c_double()
+    err = C.create_string_buffer(1024)
+    rc = lib().cyc_estimate_cfo_ccf(xa.ctypes.data, xa.size, float(expected_beta), int(N), int(num_frames),
+                                    int(device), C.byref(eps), err, 1024)
+    msg = err.value.decode()
+    if rc == 3 and msg.startswith("no feature"):
+        raise NoFeatureError(msg)
+    if rc:
+        _raise(rc, msg)
+    return eps.value
+
+
+def write_cf32(path: str, samples) -> int:
+    """io.cpp:74-88: interleaved little-endian float32 I/Q; non-finite rejected."""
+    a = np.asarray(samples)
+    bad = ~np.isfinite(a)
+    if bad.any():
+        raise DataError(f"non-finite sample at index {int(np.flatnonzero(bad)[0])}", int(np.flatnonzero(bad)[0]))
+    b = np.ascontiguousarray(a, dtype=np.complex64).astype("<c8").tobytes()
+    with open(path, "wb") as f:
+        f.write(b)
+    return len(b)
 
 
 def measure_fp32_peak(device: int = 0) -> float:

@@ -8,9 +8,6 @@
 
 #include "engine.h"
 
-struct cyc_est {
-    cyc::Engine* e;
-};
 
 namespace {
 

@@ -1111,6 +1111,14 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                 }
             const size_t slots = k0s.size();
             double2* tables = frames_host_;
+            if (!sink && c_.mode != CYC_MODE_RECURSIVE) {
+                // nobody receives the frames: keep only the running average_frames
+                // sums on the device (no frame D2H, no synchronisation)
+                TRY(compute_frames(k0s, chans, false));
+                launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
+                launches_ += 1;
+                continue;
+            }
             if (graph_eligible(slots)) {
                 // small frame batches: one CUDA-graph replay (fold, reduce, finalize,
                 // accumulate, D2H) instead of five launches and a memcpy
@@ -1231,7 +1239,9 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     if (!speculative) {
         // whole-chunk validation before any state change (estimator.cpp:43-52)
         Bad bad;
-        if (kind == IN_HOST_F32) {
+        if (kind == IN_HOST_F32 && prevalidated_) {
+            prevalidated_ = false;  // the caller (push_file) scanned this chunk already
+        } else if (kind == IN_HOST_F32) {
             bad = scan_bad((const cyc_cf32*)xv, (const cyc_cf32*)yv, n, C);
         } else if (kind == IN_HOST_F64) {
             bad = scan_bad((const cyc_cf64*)xv, (const cyc_cf64*)yv, n, C);
@@ -1792,6 +1802,15 @@ Status Engine::synchronize() {
     CK(cudaSetDevice(c_.device));
     CK(cudaStreamSynchronize(xs_));
     CK(cudaStreamSynchronize(cs_));
+    return Status::ok();
+}
+
+// The whole-chunk finite scan on its own (push_file validates the mapped file
+// before pushing it, then marks the push prevalidated).
+Status Engine::validate_host_f32(const void* x, const void* y, size_t n) {
+    const Bad bad = scan_bad((const cyc_cf32*)x, (const cyc_cf32*)y, n, c_.channels);
+    if (bad.key != ~0ull) return data_error(bad.key, bad.channel, IN_HOST_F32, x, y, n);
+    prevalidated_ = true;
     return Status::ok();
 }
 

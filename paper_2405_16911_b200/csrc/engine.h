@@ -70,6 +70,8 @@ public:
     Status compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw, size_t yw_len,
                           uint64_t k0, cyc_cf64* out);
     Status synchronize();
+    // Finite scan of a host cf32 chunk; on success the next push of it skips its scan.
+    Status validate_host_f32(const void* x, const void* y, size_t n);
     // Fresh stream state, same config and allocations (== a new CyclicCorrelator(cfg)).
     Status reset();
     // Block-mode fold state (time-sharded multi-GPU, checkpoint/resume).
@@ -216,6 +218,7 @@ private:
     char* meta_dev_ = nullptr;
     char* meta_shadow_ = nullptr;  // device copy of the arena
     bool meta_mapped_now_ = false; // read descriptors mapped (inside pinned-host pushes)
+    bool prevalidated_ = false;    // next host-f32 push was scanned by validate_host_f32
     size_t meta_slot_bytes_ = 0;
     size_t meta_used_ = 0;
     int meta_slot_ = 0;
@@ -271,3 +274,8 @@ private:
 };
 
 }  // namespace cyc
+
+// The opaque C-ABI handle.
+struct cyc_est {
+    cyc::Engine* e;
+};

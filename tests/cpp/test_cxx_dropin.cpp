@@ -136,6 +136,49 @@ int main() {
         for (std::size_t i = 0; i < avg.size(); ++i) worst = std::max(worst, std::abs(avg[i] - b[i]));
         CHECK(worst <= 2e-5);
     }
+    // cf32 file push (io.cpp:74-103) == pushing the same samples as an array
+    {
+        const auto x = random_stream(4096, 21);
+        std::vector<std::complex<float>> xf(x.begin(), x.end());
+        const char* path = "/tmp/cyc_cxx_dropin.cf32";
+        FILE* f = std::fopen(path, "wb");
+        std::fwrite(xf.data(), sizeof(xf[0]), xf.size(), f);
+        std::fclose(f);
+        CyclicCorrelator a(set_cfg(256, 3, {0.0, 0.125}));
+        CyclicCorrelator b(set_cfg(256, 3, {0.0, 0.125}));
+        const auto fa = a.push_file(path);
+        const auto fb = b.push(x, x);
+        CHECK(fa.size() == 15 && fb.size() == 15);  // the 16th waits for m lookahead samples
+        double worst = 0;
+        for (std::size_t i = 0; i < fa.size() && i < fb.size(); ++i)
+            for (std::size_t j = 0; j < fa[i].values.size(); ++j)
+                worst = std::max(worst, std::abs(fa[i].values[j] - fb[i].values[j]));
+        CHECK(worst <= 1e-6);
+        f = std::fopen(path, "ab");
+        std::fputc(0, f);
+        std::fclose(f);
+        try {
+            a.push_file(path);
+            CHECK(false);
+        } catch (const IoError& e) {
+            CHECK(std::string(e.what()).find("truncated") != std::string::npos);
+        }
+        std::remove(path);
+    }
+    // estimate_cfo_ccf argument guards and the no-feature path (test_impair.cpp:160-172)
+    {
+        const auto noise = random_stream(16 * 1024 + 8, 9);
+        try {
+            estimate_cfo_ccf(noise, 0.0625, 1024, 0);
+            CHECK(false);
+        } catch (const UsageError&) {
+        }
+        try {
+            estimate_cfo_ccf(noise, 0.0625, 1024, 16);
+            CHECK(false);
+        } catch (const NoFeatureError&) {
+        }
+    }
     std::printf("%s: %d failure(s)\n", g_fail ? "FAIL" : "PASS", g_fail);
     return g_fail;
 }
