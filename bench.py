@@ -11,8 +11,9 @@ frames cover L_eff = 16,776,192 samples.
 
 One step = reset the estimator, push the record, read both (alpha, tau)
 tables.  Two measurements per run:
-  value  -- input already resident in HBM (cyc_push_device), CUDA events on
-            the estimator's stream;
+  value  -- input already resident in HBM (cyc_push_device), both result
+            tables finalized into HBM (cyc_average_all to device memory),
+            CUDA events on the estimator's stream;
   e2e    -- input in pinned HOST memory through the reference-facing C-ABI
             call (cyc_push), H2D DMA and the D2H of both tables inside the
             timed region.
@@ -240,8 +241,10 @@ def run_ours(args, ws, rank, local):
     n_local = len(x)
     F_total = l_eff(L_REC) // N_WIN
 
-    out_conv = np.zeros(A * LAGS, dtype=np.complex128)
-    out_conj = np.zeros(A * LAGS, dtype=np.complex128)
+    # the step's result: both flag tables, [1 channel][conv, conj][A * LAGS] --
+    # in HBM for `value`, DMA'd into pinned host memory for `e2e`
+    out_dev = torch.empty((1, 2, A * LAGS), dtype=torch.complex128, device=f"cuda:{dev}")
+    out_host = cyc.host_alloc((1, 2, A * LAGS), dtype=np.complex128)
 
     def exchange():
         """Time shards: NCCL all-reduce (sum) of the fp64 fold accumulators."""
@@ -256,8 +259,7 @@ def run_ours(args, ws, rank, local):
         est.reset()
         est.push_device(ptr, n_local)
         exchange()
-        est.average(flag=cyc.Flags.CONV, out=out_conv)
-        est.average(flag=cyc.Flags.CONJ, out=out_conj)
+        est.average_all(out=out_dev)
 
     px = cyc.host_alloc(x.shape)
     px[:] = x
@@ -266,8 +268,7 @@ def run_ours(args, ws, rank, local):
         est.reset()
         est.push(px)
         exchange()
-        est.average(flag=cyc.Flags.CONV, out=out_conv)
-        est.average(flag=cyc.Flags.CONJ, out=out_conj)
+        est.average_all(out=out_host)
 
     def timed(fn, k):
         barrier(ws)
@@ -323,7 +324,7 @@ def run_ours(args, ws, rank, local):
         "e2e": {"value": ups / (ms_e2e_max * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e_max,
                 "h2d_bytes_per_step": n_local * 8, "d2h_bytes_per_step": 2 * A * LAGS * 16,
                 "msamples_per_s": L_REC * records / (ms_e2e_max * 1e-3) / 1e6,
-                "path": "cyc_push(pinned host cf32) + cyc_average x2 (D2H)"},
+                "path": "cyc_push(pinned host cf32) + cyc_average_all (both tables, one D2H into pinned host)"},
         "roofline": {"bound": "fp32", "kernel": "fold_kernel", "achieved": fold_tflops, "peak": peak,
                      "unit": "TFLOP/s", "frac": fold_tflops / peak if peak else None,
                      "traffic": traffic, "traffic_source": tsrc,
@@ -492,20 +493,19 @@ def run_config(args, ws, rank, local):
         px = cyc.host_alloc(x.shape)
         px[:] = x
 
-        out_all = np.zeros((est.config().channels, 2, lay), dtype=np.complex128)
+        shape = (est.config().channels, 2, lay)
+        out_dev = torch.empty(shape, dtype=torch.complex128, device=f"cuda:{dev}")
+        out_host = cyc.host_alloc(shape, dtype=np.complex128)
 
-        def finish():
-            est.average_all(out=out_all)  # every (channel, flag) table: one finalize + one D2H
-
-        def step_dev():
+        def step_dev():  # result tables stay in HBM
             est.reset()
             est.push_device(dx.data_ptr(), n)
-            finish()
+            est.average_all(out=out_dev)
 
-        def step_e2e():
+        def step_e2e():  # every (channel, flag) table: one finalize + one D2H into pinned host
             est.reset()
             est.push(px)
-            finish()
+            est.average_all(out=out_host)
 
     def timed(fn, k):
         torch.cuda.synchronize(dev)

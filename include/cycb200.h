@@ -170,7 +170,13 @@ int cyc_estimate_cfo_ccf(const cyc_cf32* x, size_t n, double expected_beta, int 
  * CYC_ERR_USAGE when no frame was emitted yet. */
 int cyc_average(cyc_est* est, int avg_mode, int flag, int channel, cyc_cf64* out);
 /* Every (channel, flag) table in one call: out = channels * num_flags *
- * layout_len values, [channel][flag][layout] (flag order: CONV, CONJ). */
+ * layout_len values, [channel][flag][layout] (flag order: CONV, CONJ).
+ * For cyc_average and cyc_average_all, `out` may be pageable host memory,
+ * pinned host memory (the table is DMA'd straight into it) or -- for a
+ * block-mode coherent average -- device memory (the table never leaves HBM;
+ * the copy is then stream-ordered on cyc_stream(est) and the call returns
+ * without waiting: synchronize that stream, or call cyc_synchronize, before
+ * reading it from another stream). */
 int cyc_average_all(cyc_est* est, int avg_mode, cyc_cf64* out);
 
 /* Accessors (estimator.hpp:109-115). */

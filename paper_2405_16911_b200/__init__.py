@@ -523,6 +523,12 @@ class CyclicCorrelator:
         """average_frames over every frame emitted so far (estimator.cpp:86-105).
         `out` (complex128, layout_len) may be passed to reuse a buffer."""
         n = layout_len(self._layout)
+        cai = getattr(out, "__cuda_array_interface__", None)
+        if cai is not None:  # device memory (block-mode coherent averages only)
+            if int(np.prod(cai["shape"])) != n or cai["typestr"] != "<c16" or cai.get("strides") is not None:
+                raise UsageError("device out must be a contiguous complex128 array of layout_len values")
+            self._check(self._L.cyc_average(self._h, int(mode), int(flag or 0), int(channel), int(cai["data"][0])))
+            return out
         if out is None:
             out = np.empty(n, dtype=np.complex128)
         elif out.dtype != np.complex128 or out.size != n or not out.flags.c_contiguous:
@@ -530,10 +536,20 @@ class CyclicCorrelator:
         self._check(self._L.cyc_average(self._h, int(mode), int(flag or 0), int(channel), out.ctypes.data))
         return out
 
-    def average_all(self, mode: AverageMode = AverageMode.Coherent, out: Optional[np.ndarray] = None) -> np.ndarray:
-        """All (channel, flag) tables: array [channels, flags, layout_len]."""
+    def average_all(self, mode: AverageMode = AverageMode.Coherent, out: Optional[np.ndarray] = None):
+        """All (channel, flag) tables: array [channels, flags, layout_len].
+        `out` may also be a device array (`__cuda_array_interface__`, e.g. a
+        torch complex128 CUDA tensor) for a block-mode coherent average; that
+        copy is stream-ordered on `stream()` -- call `synchronize()` before
+        reading it from another stream."""
         nf = int(self._L.cyc_num_flags(self._h))
         shape = (self._cfg.channels, nf, layout_len(self._layout))
+        cai = getattr(out, "__cuda_array_interface__", None)
+        if cai is not None:
+            if tuple(cai["shape"]) != shape or cai["typestr"] not in ("<c16",) or cai.get("strides") not in (None,):
+                raise UsageError(f"device out must be a contiguous complex128 array of shape {shape}")
+            self._check(self._L.cyc_average_all(self._h, int(mode), int(cai["data"][0])))
+            return out
         if out is None:
             out = np.empty(shape, dtype=np.complex128)
         elif out.shape != shape or out.dtype != np.complex128 or not out.flags.c_contiguous:

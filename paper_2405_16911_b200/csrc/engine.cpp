@@ -217,6 +217,25 @@ void trace(const char* what) {
     std::fprintf(stderr, "[cyc] %8.3f ms  %s\n", std::chrono::duration<double, std::milli>(now - t0).count(), what);
 }
 
+// Pinned host or device memory (a DMA can land there directly).
+bool dma_target(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_device(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice;
+}
+
 bool is_pinned(const void* p) {
     cudaPointerAttributes a;
     const cudaError_t e = cudaPointerGetAttributes(&a, p);
@@ -774,9 +793,17 @@ Status Engine::fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite)
         std::vector<FoldSeg> sg(segs);
         for (auto& g : sg)
             g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
-        L.segs = (const FoldSeg*)upload(sg.data(), sg.size() * sizeof(FoldSeg));
-        L.tiles = (const FoldTile*)upload(tiles.data(), tiles.size() * sizeof(FoldTile));
-        L.groups = (const FoldGroup*)upload(fg.data(), fg.size() * sizeof(FoldGroup));
+        // one descriptor blob per launch: a single small H2D copy, not three
+        const size_t o_t = (sg.size() * sizeof(FoldSeg) + 15) & ~size_t(15);
+        const size_t o_g = o_t + ((tiles.size() * sizeof(FoldTile) + 15) & ~size_t(15));
+        blob_.resize(o_g + fg.size() * sizeof(FoldGroup));
+        std::memcpy(blob_.data(), sg.data(), sg.size() * sizeof(FoldSeg));
+        std::memcpy(blob_.data() + o_t, tiles.data(), tiles.size() * sizeof(FoldTile));
+        std::memcpy(blob_.data() + o_g, fg.data(), fg.size() * sizeof(FoldGroup));
+        const char* dblob = (const char*)upload(blob_.data(), blob_.size());
+        L.segs = (const FoldSeg*)dblob;
+        L.tiles = (const FoldTile*)(dblob + o_t);
+        L.groups = (const FoldGroup*)(dblob + o_g);
         L.n_tiles = (int)tiles.size();
         L.n_groups = (int)fg.size();
         L.Pf = (int)Pf_;
@@ -786,6 +813,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite)
         L.partials = partials_;
         L.S = S;
         L.overwrite = overwrite ? 1 : 0;
+        L.gate = fold_gate_;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
             launch_fold(L, cs_, r.a, r.b);
@@ -1248,9 +1276,9 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         } else {
             CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
             for (int ch = 0; ch < C; ++ch) {
-                launch_finite_check((const float2*)xv + (size_t)ch * n, yv ? (const float2*)yv + (size_t)ch * n : nullptr,
-                                    (int64_t)n, 0, C, ch, key_dev_, cs_);
-                launches_ += 1;
+                launches_ += launch_finite_check((const float2*)xv + (size_t)ch * n,
+                                                 yv ? (const float2*)yv + (size_t)ch * n : nullptr, (int64_t)n, 0, C,
+                                                 ch, key_dev_, cs_);
             }
             CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs_));
             CK(cudaStreamSynchronize(cs_));
@@ -1439,17 +1467,24 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
             TRY(grow_ring(want));
     }
     TRY(history_copy(hb, hc, true));
-    if (!S_pend_) CK(cudaMalloc(&S_pend_, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double)));
-    CK(cudaMemsetAsync(S_pend_, 0, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
     CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
-    if (kind == IN_DEVICE_F32) {
+    const bool gated = kind == IN_DEVICE_F32;
+    if (gated) {
+        // The whole chunk is scanned before any fold is enqueued (same stream),
+        // so the fold's reduce can commit straight into S_main behind the
+        // scan's verdict: no pending accumulator, no commit pass.
         for (int ch = 0; ch < C; ++ch) {
-            launch_finite_check((const float2*)xv + (size_t)ch * n, yv ? (const float2*)yv + (size_t)ch * n : nullptr,
-                                (int64_t)n, 0, C, ch, key_dev_, cs_);
-            launches_ += 1;
+            launches_ += launch_finite_check((const float2*)xv + (size_t)ch * n,
+                                             yv ? (const float2*)yv + (size_t)ch * n : nullptr, (int64_t)n, 0, C, ch,
+                                             key_dev_, cs_);
         }
-        TRY(fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_pend_));
+        fold_gate_ = key_dev_;
+        const Status st = fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_main_);
+        fold_gate_ = nullptr;
+        TRY(st);
     } else {
+        if (!S_pend_) CK(cudaMalloc(&S_pend_, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double)));
+        CK(cudaMemsetAsync(S_pend_, 0, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
         static const bool tr = std::getenv("CYC_TRACE") != nullptr;
         cudaEvent_t ta = nullptr, tb = nullptr, tc = nullptr;
         if (tr) {
@@ -1470,10 +1505,11 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
             for (int ch = 0; ch < C; ++ch) {
                 const float2* rx = ring_x_ + (size_t)ch * cap_;
                 const float2* ry = cross_ ? ring_y_ + (size_t)ch * cap_ : nullptr;
-                launch_finite_check(rx + pos, ry ? ry + pos : nullptr, (int64_t)first, (int64_t)off, C, ch, key_dev_, cs_);
+                launches_ += launch_finite_check(rx + pos, ry ? ry + pos : nullptr, (int64_t)first, (int64_t)off, C,
+                                                 ch, key_dev_, cs_);
                 if (first < len)
-                    launch_finite_check(rx, ry, (int64_t)(len - first), (int64_t)(off + first), C, ch, key_dev_, cs_);
-                launches_ += first < len ? 2 : 1;
+                    launches_ += launch_finite_check(rx, ry, (int64_t)(len - first), (int64_t)(off + first), C, ch,
+                                                     key_dev_, cs_);
             }
             mark_read(abs0);
             consumed_ += len;
@@ -1502,8 +1538,10 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
     trace("compute done");
     const uint64_t key = *key_host_;
     if (key == ~0ull) {
-        launch_add_f64(S_main_, S_pend_, (int64_t)C * t_pad_ * Pf_ * 4, cs_);
-        launches_ += 1;
+        if (!gated) {
+            launch_add_f64(S_main_, S_pend_, (int64_t)C * t_pad_ * Pf_ * 4, cs_);
+            launches_ += 1;
+        }
         return cuda_check(cudaGetLastError(), "push");
     }
     // roll back: counters, history samples; the pending fold is discarded
@@ -1606,8 +1644,8 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
         avg_all_len_ = (size_t)C * per;
     }
     TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, avg_all_dev_));
-    CK(cudaMemcpyAsync(out, avg_all_dev_, (size_t)C * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_));
-    CK(cudaStreamSynchronize(cs_));
+    CK(cudaMemcpyAsync(out, avg_all_dev_, (size_t)C * per * sizeof(double2), cudaMemcpyDefault, cs_));
+    if (!is_device(out)) CK(cudaStreamSynchronize(cs_));  // device out: stream-ordered on cyc_stream
     return Status::ok();
 }
 
@@ -1627,6 +1665,11 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
     if (flag == 0) flag = c_.flags == 3 ? CYC_FLAG_CONV : c_.flags;
     if (!(flag & c_.flags) || (flag != CYC_FLAG_CONV && flag != CYC_FLAG_CONJ)) {
         u.msg = "flag not computed by this estimator";
+        return u;
+    }
+    if (is_device(out) && !(use_fold_ && !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE &&
+                            avg_mode == CYC_AVG_COHERENT)) {
+        u.msg = "device-memory output needs a block-mode (emit_frames = 0) coherent average";
         return u;
     }
     const int fi = (c_.flags == 3 && flag == CYC_FLAG_CONJ) ? 1 : 0;
@@ -1681,6 +1724,12 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
             avg_cache_channel_ = channel;
         }
         trace("avg finalize enqueued");
+        if (dma_target(out)) {  // pinned host or device memory: one copy, no bounce
+            CK(cudaMemcpyAsync(out, avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
+                               cudaMemcpyDefault, cs_));
+            if (!is_device(out)) CK(cudaStreamSynchronize(cs_));  // device out: stream-ordered
+            return Status::ok();
+        }
         CK(cudaMemcpyAsync(tmp, avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
                            cudaMemcpyDeviceToHost, cs_));
         CK(cudaStreamSynchronize(cs_));

@@ -256,6 +256,8 @@ private:
 
     // speculative block pushes: pending fold + history backup for roll-back
     double* S_pend_ = nullptr;
+    std::vector<char> blob_;  // host staging of one launch's descriptors
+    const unsigned long long* fold_gate_ = nullptr;  // set while a device chunk folds straight into S_main
     float2* hist_bak_ = nullptr;
     size_t hist_cap_ = 0;
     int stage_k_ = 0;

@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
 
 // S[slot][lb*TB + lag][rb*RB + res][4] += sum over the group's tiles (fixed order, fp64).
 __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
+    if (L.gate && *L.gate != ~0ull) return;
     __shared__ FoldGroup s_g;
     __shared__ int s_slot;
     if (threadIdx.x == 0) {
@@ -310,10 +311,26 @@ __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
     const int64_t rg = (int64_t)g.rb * RB + res;
     const int tg = g.lb * TB + lag;
     if (rg >= L.Pf || tg >= L.t_pad) return;
-    const float4* part = reinterpret_cast<const float4*>(L.partials);
+    const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
+    const size_t stride = (size_t)TB * RB;
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-    for (int t = g.t0; t < g.t1; ++t) {
-        const float4 v = part[(size_t)t * TB * RB + e];
+    // 8 independent loads in flight per thread (the partials were just written
+    // and sit in L2); the fp64 sum keeps the fixed tile order.
+    int t = g.t0;
+    for (; t + 8 <= g.t1; t += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(part + (size_t)(t + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            s0 += v[u].x;
+            s1 += v[u].y;
+            s2 += v[u].z;
+            s3 += v[u].w;
+        }
+    }
+    for (; t < g.t1; ++t) {
+        const float4 v = __ldcs(part + (size_t)t * stride);
         s0 += v.x;
         s1 += v.y;
         s2 += v.z;

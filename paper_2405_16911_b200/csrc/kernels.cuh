@@ -63,6 +63,9 @@ struct FoldLaunch {
     float* partials;     // [n_tiles][TB][RB] float4
     double* S;           // [slots][t_pad][Pf][4] fp64 accumulators
     int overwrite;       // 1: reduce stores (fresh per-frame slots, no memset); 0: accumulates
+    // non-null: the reduce commits only if *gate == ~0 (the chunk's finite scan,
+    // stream-ordered before the fold, found nothing) -- a rejected chunk leaves S untouched
+    const unsigned long long* gate;
 };
 
 // fold + fp64 reduce; optional events bracket the fold kernel alone (profiling)
@@ -139,8 +142,9 @@ void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len,
                          double2* coh, double* mag, cudaStream_t st);
 // First non-finite sample -> atomicMin(*key);
 // key = (2*(base+i) + is_y) * channels + ch  -- smallest = reference scan order.
-void launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
-                         unsigned long long* key, cudaStream_t st);
+// returns the number of kernels launched
+int launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
+                        unsigned long long* key, cudaStream_t st);
 // Ring write from a device source with wrap: ring[(abs0 + i) & mask] = src[i].
 void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src,
                        int64_t n, cudaStream_t st);

@@ -396,6 +396,34 @@ def test_speculative_push_rollback(cyc, kind):
         assert np.max(np.abs(est.average(flag=fl) - ref_est.average(flag=fl))) <= 1e-12
 
 
+@pytest.mark.parametrize("n", [(1 << 16) + 1, 1 << 16, 1000, 3])
+def test_device_scan_names_first_bad_sample(cyc, n):
+    """The device finite scan (vectorised + scalar tail) reports exactly the
+    reference's first offender: lowest index, x before y at the same index."""
+    import torch
+    rng = np.random.default_rng(n)
+    cases = [[0], [n - 1], [n // 2, n // 2 + 1], [n - 2, n - 1]] + [sorted(rng.choice(n, 3, replace=False))
+                                                                      for _ in range(3)]
+    for pos in cases:
+        pos = [int(p) for p in pos if 0 <= p < n]
+        for stream in ("x", "y", "both"):
+            x, y = rand_c(n, 5), rand_c(n, 6)
+            for p in pos:
+                if stream in ("x", "both"):
+                    x[p] = np.inf
+                if stream in ("y", "both"):
+                    y[p] = np.nan
+            est = cyc.CyclicCorrelator(full_cfg(cyc, 2, [0], flags=cyc.Flags.BOTH, emit_frames=False))
+            dx = torch.from_numpy(x).cuda()
+            dy = torch.from_numpy(y).cuda()
+            with pytest.raises(cyc.DataError) as ei:
+                est.push_device(dx.data_ptr(), n, dy.data_ptr())
+            first = min(pos)
+            assert ei.value.index == first, (n, pos, stream)
+            assert f"in {'y' if stream == 'y' else 'x'} stream" in str(ei.value)
+            assert est.consumed() == 0
+
+
 def test_c2_scale_block_average_vs_oracle(cyc, oracle):
     """Config 2 geometry at 2^22 samples (the oracle's fold finishes in seconds)."""
     from paper_2405_16911_b200 import siggen
@@ -422,6 +450,29 @@ def test_average_all_matches_per_channel(cyc):
     for c in range(C_):
         assert np.max(np.abs(allt[c, 0] - est.average(flag=cyc.Flags.CONV, channel=c))) <= 1e-15
         assert np.max(np.abs(allt[c, 1] - est.average(flag=cyc.Flags.CONJ, channel=c))) <= 1e-15
+    # the same tables DMA'd into pinned host memory and into device memory
+    pinned = cyc.host_alloc(allt.shape, dtype=np.complex128)
+    assert est.average_all(out=pinned) is pinned
+    assert np.array_equal(np.asarray(pinned), allt)
+    import torch
+    dev = torch.empty(allt.shape, dtype=torch.complex128, device="cuda")
+    est.average_all(out=dev)  # stream-ordered on the estimator's stream
+    est.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), allt)
+    one = cyc.host_alloc(8 * 256, dtype=np.complex128)
+    est.average(flag=cyc.Flags.CONJ, channel=2, out=one)
+    assert np.array_equal(np.asarray(one), allt[2, 1])
+
+
+def test_device_output_needs_block_mode(cyc):
+    """Per-frame estimators scale on the host, so a device `out` is refused."""
+    import torch
+    x = rand_c(4096, 201)
+    est = cyc.CyclicCorrelator(full_cfg(cyc, 256, [0, 1]))
+    est.push(x)
+    dev = torch.empty(2 * 256, dtype=torch.complex128, device="cuda")
+    with pytest.raises(cyc.UsageError, match="device-memory output"):
+        est.average(out=dev)
 
 
 # BASELINE configs at reduced sizes (full sizes run in bench.py --config cN)
