@@ -419,6 +419,17 @@ Status Engine::plan(const Cfg& cfg) {
     }
     // fold geometry
     f_lo_ = lag_lo_ - (((lag_lo_ % 2) + 2) % 2);  // even fold origin: 16-byte pair staging
+    {
+        // a multiple-of-4 origin lets self stages read y from the staged x
+        // window (fold.cu); take it when it costs no extra lag block
+        const int f4 = lag_lo_ - (((lag_lo_ % 4) + 4) % 4);
+        auto blocks = [&](int lo) {
+            const int sp = lag_hi_ - lo + 1;
+            const int lw = sp <= 16 ? 2 : (sp <= 32 ? 4 : 8);
+            return std::make_pair(lw, (sp + fold_tb(lw) - 1) / fold_tb(lw));
+        };
+        if (blocks(f4) == blocks(f_lo_)) f_lo_ = f4;
+    }
     const int span = lag_hi_ - f_lo_ + 1;
     lw_ = span <= 16 ? 2 : (span <= 32 ? 4 : 8);
     TB_ = fold_tb(lw_);
@@ -793,17 +804,28 @@ Status Engine::fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite)
         std::vector<FoldSeg> sg(segs);
         for (auto& g : sg)
             g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
-        // one descriptor blob per launch: a single small H2D copy, not three
-        const size_t o_t = (sg.size() * sizeof(FoldSeg) + 15) & ~size_t(15);
-        const size_t o_g = o_t + ((tiles.size() * sizeof(FoldTile) + 15) & ~size_t(15));
-        blob_.resize(o_g + fg.size() * sizeof(FoldGroup));
-        std::memcpy(blob_.data(), sg.data(), sg.size() * sizeof(FoldSeg));
-        std::memcpy(blob_.data() + o_t, tiles.data(), tiles.size() * sizeof(FoldTile));
-        std::memcpy(blob_.data() + o_g, fg.data(), fg.size() * sizeof(FoldGroup));
-        const char* dblob = (const char*)upload(blob_.data(), blob_.size());
-        L.segs = (const FoldSeg*)dblob;
-        L.tiles = (const FoldTile*)(dblob + o_t);
-        L.groups = (const FoldGroup*)(dblob + o_g);
+        static const bool no_inline = std::getenv("CYC_NO_INLINE") != nullptr;  // A/B knob
+        const bool inl = !no_inline && sg.size() <= (size_t)FI_SEGS && tiles.size() <= (size_t)FI_TILES &&
+                         fg.size() <= (size_t)FI_GROUPS;
+        if (inl) {
+            // descriptors ride in the kernel parameter block
+            if (!inline_) inline_.reset(new FoldInline);
+            std::memcpy(inline_->segs, sg.data(), sg.size() * sizeof(FoldSeg));
+            std::memcpy(inline_->tiles, tiles.data(), tiles.size() * sizeof(FoldTile));
+            std::memcpy(inline_->groups, fg.data(), fg.size() * sizeof(FoldGroup));
+        } else {
+            // one descriptor blob per launch: a single small H2D copy, not three
+            const size_t o_t = (sg.size() * sizeof(FoldSeg) + 15) & ~size_t(15);
+            const size_t o_g = o_t + ((tiles.size() * sizeof(FoldTile) + 15) & ~size_t(15));
+            blob_.resize(o_g + fg.size() * sizeof(FoldGroup));
+            std::memcpy(blob_.data(), sg.data(), sg.size() * sizeof(FoldSeg));
+            std::memcpy(blob_.data() + o_t, tiles.data(), tiles.size() * sizeof(FoldTile));
+            std::memcpy(blob_.data() + o_g, fg.data(), fg.size() * sizeof(FoldGroup));
+            const char* dblob = (const char*)upload(blob_.data(), blob_.size());
+            L.segs = (const FoldSeg*)dblob;
+            L.tiles = (const FoldTile*)(dblob + o_t);
+            L.groups = (const FoldGroup*)(dblob + o_g);
+        }
         L.n_tiles = (int)tiles.size();
         L.n_groups = (int)fg.size();
         L.Pf = (int)Pf_;
@@ -814,12 +836,13 @@ Status Engine::fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite)
         L.S = S;
         L.overwrite = overwrite ? 1 : 0;
         L.gate = fold_gate_;
+        const FoldInline* di = inl ? inline_.get() : nullptr;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
-            launch_fold(L, cs_, r.a, r.b);
+            launch_fold(L, cs_, r.a, r.b, di);
             prof_pending_.push_back(r);
         } else {
-            launch_fold(L, cs_);
+            launch_fold(L, cs_, nullptr, nullptr, di);
         }
         launches_ += 2;
         g0 = g;
@@ -1493,7 +1516,8 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
             cudaEventCreate(&tc);
             cudaEventRecord(ta, xs_);
         }
-        meta_mapped_now_ = true;  // descriptor copies would queue behind the bulk DMA
+        static const bool nomap = std::getenv("CYC_META_NOMAP") != nullptr;  // experiment knob
+        meta_mapped_now_ = !nomap;  // descriptor copies would queue behind the bulk DMA
         for (size_t off = 0; off < n; off += (size_t)Q_) {
             const size_t len = std::min((size_t)Q_, n - off);
             const int64_t abs0 = origin_ + (int64_t)consumed_;

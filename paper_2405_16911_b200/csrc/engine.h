@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <deque>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/cycb200.h"
@@ -256,7 +257,8 @@ private:
 
     // speculative block pushes: pending fold + history backup for roll-back
     double* S_pend_ = nullptr;
-    std::vector<char> blob_;  // host staging of one launch's descriptors
+    std::vector<char> blob_;              // host staging of one launch's descriptors
+    std::unique_ptr<FoldInline> inline_;  // by-value descriptors of the next fold launch
     const unsigned long long* fold_gate_ = nullptr;  // set while a device chunk folds straight into S_main
     float2* hist_bak_ = nullptr;
     size_t hist_cap_ = 0;

@@ -23,6 +23,8 @@
 // 64 FFMA2 (128 FMAs); the next period's registers are loaded while the
 // current one is multiplied.  Partial sums leave the CTA in fp32 and are
 // reduced in fp64 in a fixed order (deterministic).
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace cyc {
@@ -84,13 +86,16 @@ struct Regs {
     float4 y[2];  // y[4rho .. 4rho+3] as pairs
 };
 
+// y pairs come from the Y rows, or -- in a self stage -- from the X rows
+// (x == y and the y window lies inside the staged x window): yb0/yb1 are the
+// float4 row offsets of (y[4rho], y[4rho+1]) and (y[4rho+2], y[4rho+3]).
 template <int LW>
-__device__ __forceinline__ void load_period(Regs& r, const float4* per, int kap, int rho) {
+__device__ __forceinline__ void load_period(Regs& r, const float4* per, int kap, int rho, int yb0, int yb1) {
     using G = Geo<LW>;
 #pragma unroll
     for (int j = 0; j < 6; ++j) r.x[j] = per[(j & 1) * G::XC + kap + (j >> 1)];
-    r.y[0] = per[2 * G::XC + rho];
-    r.y[1] = per[2 * G::XC + G::YC + rho];
+    r.y[0] = per[yb0 + rho];
+    r.y[1] = per[yb1 + rho];
 }
 
 __device__ __forceinline__ void mac_period(float2 (&lo)[R][U], float2 (&hi)[R][U], const Regs& r) {
@@ -129,17 +134,56 @@ __device__ __forceinline__ void weight_period(Regs& r, const FoldSeg& seg, int64
     r.y[1].w *= w[3];
 }
 
-template <int LW>
-__global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
+// One stage's periods.  The next period's registers load while the current
+// one multiplies; the loads are unconditional (the last re-reads period nq-1)
+// so the loop body is one basic block and ptxas can spread the LDS between
+// the FFMA2s.  W: recursive-mode weights (compile-time, no branch in the body).
+template <int LW, bool W>
+__device__ __forceinline__ void compute_stage(float2 (&lo)[R][U], float2 (&hi)[R][U], const float4* st, int nq,
+                                              int kap, int rho, int yb0, int yb1, const FoldSeg& seg, int64_t n0,
+                                              int64_t Pf) {
+    using G = Geo<LW>;
+    Regs ra, rb;
+    load_period<LW>(ra, st, kap, rho, yb0, yb1);
+    int q = 0;
+    for (; q + 1 < nq; q += 2) {
+        load_period<LW>(rb, st + (q + 1) * G::PER, kap, rho, yb0, yb1);
+        if (W) weight_period(ra, seg, n0 + q * Pf);
+        mac_period(lo, hi, ra);
+        load_period<LW>(ra, st + min(q + 2, nq - 1) * G::PER, kap, rho, yb0, yb1);
+        if (W) weight_period(rb, seg, n0 + (q + 1) * Pf);
+        mac_period(lo, hi, rb);
+    }
+    if (q < nq) {
+        if (W) weight_period(ra, seg, n0 + q * Pf);
+        mac_period(lo, hi, ra);
+    }
+}
+
+struct NoInline {};
+
+template <int LW, bool INL>
+__global__ void __launch_bounds__(NT, 1)
+    fold_kernel(FoldLaunch L, const __grid_constant__ std::conditional_t<INL, FoldInline, NoInline> D) {
     using G = Geo<LW>;
     extern __shared__ __align__(16) float4 smem4[];
-    // Launch descriptors may live in mapped host memory: copy them to shared
-    // memory once, so re-reads under register pressure never cross PCIe.
+    // Descriptors come from the parameter block or (pointer launches) from
+    // device / mapped memory: copy them to shared memory once.
     __shared__ FoldTile s_tile;
     __shared__ FoldSeg s_seg;
-    if (threadIdx.x == 0) s_tile = L.tiles[blockIdx.x];
+    if (threadIdx.x == 0) {
+        if constexpr (INL)
+            s_tile = D.tiles[blockIdx.x];
+        else
+            s_tile = L.tiles[blockIdx.x];
+    }
     __syncthreads();
-    if (threadIdx.x == 0) s_seg = L.segs[s_tile.seg];
+    if (threadIdx.x == 0) {
+        if constexpr (INL)
+            s_seg = D.segs[s_tile.seg];
+        else
+            s_seg = L.segs[s_tile.seg];
+    }
     __syncthreads();
     const FoldTile& tile = s_tile;
     const FoldSeg& seg = s_seg;
@@ -164,35 +208,59 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
     const int e_first = tid - q_first * G::EPP;
     constexpr int DQ = NT / G::EPP, DE = NT % G::EPP;
 
+    // x window offset from the residue: d = lag_lo + lb*TB.  Self stages read y
+    // from the X rows when x == y and [res, res+RB) sits inside the x window
+    // at a 4-sample boundary (every BASELINE config: lags start at 0 or -M).
+    const int64_t dwin = (int64_t)L.lag_lo + (int64_t)tile.lb * G::TB;
+    const bool self_ok = seg.x == seg.y && dwin <= 0 && -dwin <= G::TB && ((-dwin) & 3) == 0;
+    const int yshift = (int)(-dwin) / 4;
+
+    // stage-uniform fast path: every window of the stage inside the valid
+    // ranges and (ring input) no wrap inside the stage
+    auto stage_fast = [&](int s) -> bool {
+        const int64_t pbeg = tile.p0 + (int64_t)s * G::PS;
+        const int64_t pend = pbeg + G::PS;
+        if (!(vec && pend <= tile.p1 && pbeg * Pf + xoff >= seg.x_lo && (pend - 1) * Pf + xoff + G::XW <= seg.x_hi &&
+              pbeg * Pf + res0 >= seg.n_start && (pend - 1) * Pf + res0 + G::RB <= seg.n_end && res0 + G::RB <= Pf))
+            return false;
+        if (mask == ~0ull) return true;
+        const uint64_t span = (uint64_t)(G::PS - 1) * (uint64_t)Pf;
+        return ((uint64_t)(pbeg * Pf + xoff) & mask) + span + G::XW <= mask + 1 &&
+               ((uint64_t)(pbeg * Pf + res0) & mask) + span + G::RB <= mask + 1;
+    };
+
     auto load_stage = [&](int s) {
         const int64_t pbeg = tile.p0 + (int64_t)s * G::PS;
         const uint32_t dst0 = sbase + (uint32_t)((s % NSTAGE) * G::STAGE) * 16u;
-        const int64_t pend = pbeg + G::PS;
-        // stage-uniform fast path: every window of the stage inside the valid ranges
-        const bool fast = vec && pend <= tile.p1 && pbeg * Pf + xoff >= seg.x_lo &&
-                          (pend - 1) * Pf + xoff + G::XW <= seg.x_hi && pbeg * Pf + res0 >= seg.n_start &&
-                          (pend - 1) * Pf + res0 + G::RB <= seg.n_end && res0 + G::RB <= Pf;
-        int q = q_first, e = e_first;
-        if (fast) {
-#pragma unroll 2
-            for (int k = 0; k < G::EPT; ++k) {
-                if (q < G::PS) {
-                    const bool isx = e < G::NX;
-                    const int ee = isx ? e : e - G::NX;
-                    const int b = ee & 1, c = ee >> 1;
-                    const int off = q * G::PER + (isx ? b * G::XC + c : 2 * G::XC + b * G::YC + c);
-                    const int64_t n = (pbeg + q) * Pf + (isx ? xoff : res0) + (4 * c + 2 * b);
-                    cp_async16(dst0 + (uint32_t)off * 16u, (isx ? seg.x : seg.y) + ((uint64_t)n & mask), 16);
-                }
-                q += DQ;
-                e += DE;
-                if (e >= G::EPP) {
-                    e -= G::EPP;
-                    ++q;
+        if (stage_fast(s)) {
+            // column-fixed assignment: a thread owns one staged pair column
+            // (x or y, phase b, float4 c) and walks the stage's periods, so an
+            // element costs one cp.async plus two pointer increments
+            const int cols = self_ok ? G::NX : G::EPP;
+            const bool wide = cols > NT;
+            const int qs = wide ? 1 : NT / cols;
+            int col = wide ? tid : tid % cols;
+            const int q0 = wide ? 0 : tid / cols;
+            if (q0 >= qs) return;
+            for (; col < cols; col += wide ? NT : cols) {
+                const bool isx = col < G::NX;
+                const int ee = isx ? col : col - G::NX;
+                const int b = ee & 1, c = ee >> 1;
+                uint32_t dst = dst0 + (uint32_t)(q0 * G::PER + (isx ? b * G::XC + c : 2 * G::XC + b * G::YC + c)) * 16u;
+                const int64_t n = (pbeg + q0) * Pf + (isx ? xoff : res0) + (4 * c + 2 * b);
+                const float2* src = (isx ? seg.x : seg.y) + ((uint64_t)n & mask);
+                const uint32_t dstep = (uint32_t)(qs * G::PER) * 16u;
+                const int64_t sstep = (int64_t)qs * Pf;
+#pragma unroll 4
+                for (int q = q0; q < G::PS; q += qs) {
+                    cp_async16(dst, src, 16);
+                    dst += dstep;
+                    src += sstep;
                 }
             }
             return;
         }
+        int q = q_first, e = e_first;
 #pragma unroll 1
         for (int k = 0; k < G::EPT; ++k) {
             if (q < G::PS) {
@@ -251,7 +319,6 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
     }
 
     const bool weighted = seg.w_log2 != 0.f;
-    Regs ra, rb;
     for (int s = 0; s < nstages; ++s) {
         cp_async_wait<NSTAGE - 2>();
         __syncthreads();
@@ -261,26 +328,13 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
         const float4* st = smem4 + (s % NSTAGE) * G::STAGE;
         const int64_t pbeg = tile.p0 + (int64_t)s * G::PS;
         const int nq = min(G::PS, nper - s * G::PS);
-        load_period<LW>(ra, st, kap, rho);
-        int q = 0;
-        for (; q + 1 < nq; q += 2) {
-#ifndef CYC_DIAG_NOLDS  // diagnostic build only: FFMA2 stream without the per-period smem loads
-            load_period<LW>(rb, st + (q + 1) * G::PER, kap, rho);
-#else
-            if (q == 0) load_period<LW>(rb, st + (q + 1) * G::PER, kap, rho);
-#endif
-            if (weighted) weight_period(ra, seg, (pbeg + q) * Pf + res0 + 4 * rho);
-            mac_period(lo, hi, ra);
-#ifndef CYC_DIAG_NOLDS
-            if (q + 2 < nq) load_period<LW>(ra, st + (q + 2) * G::PER, kap, rho);
-#endif
-            if (weighted) weight_period(rb, seg, (pbeg + q + 1) * Pf + res0 + 4 * rho);
-            mac_period(lo, hi, rb);
-        }
-        if (q < nq) {
-            if (weighted) weight_period(ra, seg, (pbeg + q) * Pf + res0 + 4 * rho);
-            mac_period(lo, hi, ra);
-        }
+        const bool self_st = self_ok && stage_fast(s);
+        const int yb0 = self_st ? yshift : 2 * G::XC;
+        const int yb1 = self_st ? G::XC + yshift : 2 * G::XC + G::YC;
+        if (weighted)
+            compute_stage<LW, true>(lo, hi, st, nq, kap, rho, yb0, yb1, seg, pbeg * Pf + res0 + 4 * rho, Pf);
+        else
+            compute_stage<LW, false>(lo, hi, st, nq, kap, rho, yb0, yb1, seg, 0, Pf);
     }
     cp_async_wait<0>();
 
@@ -295,13 +349,20 @@ __global__ void __launch_bounds__(NT, 1) fold_kernel(FoldLaunch L) {
 }
 
 // S[slot][lb*TB + lag][rb*RB + res][4] += sum over the group's tiles (fixed order, fp64).
-__global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
+template <bool INL>
+__global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB,
+                                   const __grid_constant__ std::conditional_t<INL, FoldInline, NoInline> D) {
     if (L.gate && *L.gate != ~0ull) return;
     __shared__ FoldGroup s_g;
     __shared__ int s_slot;
     if (threadIdx.x == 0) {
-        s_g = L.groups[blockIdx.y];
-        s_slot = L.segs[s_g.seg].slot;
+        if constexpr (INL) {
+            s_g = D.groups[blockIdx.y];
+            s_slot = D.segs[s_g.seg].slot;
+        } else {
+            s_g = L.groups[blockIdx.y];
+            s_slot = L.segs[s_g.seg].slot;
+        }
     }
     __syncthreads();
     const FoldGroup g = s_g;
@@ -352,28 +413,30 @@ __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB) {
 }
 
 template <int LW>
-void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, const FoldInline* inl) {
     using G = Geo<LW>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(fold_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        attr_set = true;
-    }
     if (ev0) cudaEventRecord(ev0, st);
-    fold_kernel<LW><<<L.n_tiles, NT, G::SMEM, st>>>(L);
-    if (ev1) cudaEventRecord(ev1, st);
     dim3 rg((G::TB * G::RB + 255) / 256, L.n_groups);
-    fold_reduce_kernel<<<rg, 256, 0, st>>>(L, G::TB, G::RB);
+    if (inl) {
+        fold_kernel<LW, true><<<L.n_tiles, NT, G::SMEM, st>>>(L, *inl);
+        if (ev1) cudaEventRecord(ev1, st);
+        fold_reduce_kernel<true><<<rg, 256, 0, st>>>(L, G::TB, G::RB, *inl);
+    } else {
+        fold_kernel<LW, false><<<L.n_tiles, NT, G::SMEM, st>>>(L, NoInline{});
+        if (ev1) cudaEventRecord(ev1, st);
+        fold_reduce_kernel<false><<<rg, 256, 0, st>>>(L, G::TB, G::RB, NoInline{});
+    }
 }
 
 }  // namespace
 
-void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, const FoldInline* inl) {
     if (L.n_tiles == 0) return;
+    prepare_fold_kernels();
     switch (L.lw) {
-        case 2: run_fold<2>(L, st, ev0, ev1); break;
-        case 4: run_fold<4>(L, st, ev0, ev1); break;
-        default: run_fold<8>(L, st, ev0, ev1); break;
+        case 2: run_fold<2>(L, st, ev0, ev1, inl); break;
+        case 4: run_fold<4>(L, st, ev0, ev1, inl); break;
+        default: run_fold<8>(L, st, ev0, ev1, inl); break;
     }
 }
 
@@ -384,9 +447,12 @@ namespace cyc {
 void prepare_fold_kernels() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(fold_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
-    cudaFuncSetAttribute(fold_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<4>::SMEM);
-    cudaFuncSetAttribute(fold_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<8>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<4>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<8>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<4>::SMEM);
+    cudaFuncSetAttribute(fold_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<8>::SMEM);
     done = true;
 }
 }  // namespace cyc

@@ -68,8 +68,20 @@ struct FoldLaunch {
     const unsigned long long* gate;
 };
 
-// fold + fp64 reduce; optional events bracket the fold kernel alone (profiling)
-void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+// Launch descriptors carried in the kernel parameter block (<= 32 KB since
+// CUDA 12.1): no H2D descriptor copy queued behind bulk DMA, no PCIe reads of
+// mapped host memory.  Launches that do not fit use the pointers in FoldLaunch.
+constexpr int FI_SEGS = 64, FI_TILES = 296, FI_GROUPS = 128;
+struct FoldInline {
+    FoldSeg segs[FI_SEGS];
+    FoldTile tiles[FI_TILES];
+    FoldGroup groups[FI_GROUPS];
+};
+
+// fold + fp64 reduce; optional events bracket the fold kernel alone (profiling).
+// inl != nullptr: descriptors by value (L.segs/tiles/groups are ignored).
+void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr,
+                 const FoldInline* inl = nullptr);
 
 void prepare_fold_kernels();      // set smem attributes (call outside stream capture)
 void prepare_finalize_kernels();
