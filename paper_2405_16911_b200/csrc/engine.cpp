@@ -1494,8 +1494,10 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
     const bool gated = kind == IN_DEVICE_F32;
     if (gated) {
         // The whole chunk is scanned before any fold is enqueued (same stream),
-        // so the fold's reduce can commit straight into S_main behind the
-        // scan's verdict: no pending accumulator, no commit pass.
+        // so the fold's reduce commits straight into S_main behind the scan's
+        // verdict: no pending accumulator, no commit pass.  (A scan on the 4
+        // SMs a one-wave fold leaves idle, on a side stream, was measured
+        // slower: 4 SMs cannot stream 134 MB within the fold.)
         for (int ch = 0; ch < C; ++ch) {
             launches_ += launch_finite_check((const float2*)xv + (size_t)ch * n,
                                              yv ? (const float2*)yv + (size_t)ch * n : nullptr, (int64_t)n, 0, C, ch,
@@ -1537,12 +1539,10 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
             }
             mark_read(abs0);
             consumed_ += len;
-            // Fold in few, shrinking batches (after 1/2, 3/4 and all of the chunk):
-            // each fold launch writes ~38 MB of partials that contend with the
-            // DMA, and the batch folded after the last DMA is the exposed tail.
-            const size_t done = off + len;
-            if (done == n || (done >= n / 2 && off < n / 2) || (done >= (3 * n) / 4 && off < (3 * n) / 4))
-                TRY(emit_new_frames(nullptr, nullptr, S_pend_));
+            // Fold after every piece: the batch folded after the last DMA is
+            // the exposed tail, so it is kept to one piece (measured: 1/2,3/4,end
+            // batches +25 us; 8 MiB pieces +15 us, 4 MiB +100 us per C2 step).
+            TRY(emit_new_frames(nullptr, nullptr, S_pend_));
             trace("piece enqueued");
         }
         if (tr) {
@@ -1599,8 +1599,7 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     }
     cudaEvent_t ev = get_event();
     CK(cudaEventRecord(ev, xs_));
-    CK(cudaStreamWaitEvent(cs_, ev, 0));
-    ev_pool_.push_back(ev);
+    bool joined = false;
     consumed_ = (uint64_t)(c1 - origin_);
     const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
     if (avail > frames_) {
@@ -1634,11 +1633,19 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
                 user_segs.push_back(g);
             }
         }
+        if (!ring_segs.empty()) {  // frames straddling the previous chunk read the ring
+            CK(cudaStreamWaitEvent(cs_, ev, 0));
+            joined = true;
+        }
         TRY(fold(ring_segs, S));
         TRY(fold(user_segs, S));
         mark_read(s + lag_lo_);
         frames_ = avail;
     }
+    // later ring readers on the compute stream are ordered after the history
+    // writes; the fold of the user buffer above did not wait for them
+    if (!joined) CK(cudaStreamWaitEvent(cs_, ev, 0));
+    ev_pool_.push_back(ev);  // only after the last wait on it (get_event may re-record it)
     return cuda_check(cudaGetLastError(), "push_device");
 }
 
