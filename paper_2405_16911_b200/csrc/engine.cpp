@@ -27,6 +27,8 @@ int64_t floor_div(int64_t a, int64_t b) {
     return q;
 }
 
+int64_t ceil_div(int64_t a, int64_t b) { return -floor_div(-a, b); }
+
 int64_t gcd64(int64_t a, int64_t b) {
     while (b) {
         int64_t t = a % b;
@@ -475,6 +477,11 @@ std::string Engine::plan_string(const Cfg& cfg) {
 Status Engine::init(const Cfg& cfg) {
     TRY(plan(cfg));
     CK(cudaSetDevice(c_.device));
+    {
+        int major = 0;
+        CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c_.device));
+        tc_capable_ = major == 10;  // tcgen05 (the library is built for sm_100a only)
+    }
     CK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
     // ring: pieces of Q samples per channel, four pieces per ring
@@ -755,11 +762,113 @@ void Engine::wait_ring_free(int64_t abs_end) {
 // compute primitives
 // ---------------------------------------------------------------------------
 
-Status Engine::fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite) {
+// Tensor-core fold of the interior periods of `segs` (every 64-residue x
+// 64-lag window of the period valid); the head/tail periods that are not go
+// back to the FP32 kernel through `rest`.  Block-mode accumulation only.
+Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<FoldSeg>& rest) {
     struct G {
         int seg, rb, lb;
         int64_t p0, p1;
     };
+    const int nrb = (int)(Pf_ / 64), nlb = t_pad_ / 64;
+    std::vector<G> groups;
+    std::vector<FoldSeg> tsegs;
+    int64_t work = 0;
+    for (const FoldSeg& g : segs) {
+        if (g.n_end <= g.n_start) continue;
+        // period p is interior when y [pPf, (p+1)Pf) and every x window
+        // [pPf + r0 + d, +128) lie inside the segment's valid ranges
+        const int64_t pa = std::max(ceil_div(g.n_start, Pf_), ceil_div(g.x_lo - f_lo_, Pf_));
+        const int64_t pb = std::min(floor_div(g.n_end, Pf_), floor_div(g.x_hi - Pf_ - f_lo_ - 64 * nlb, Pf_) + 1);
+        const bool ok = g.vec && g.w_log2 == 0.f && pb - pa >= 16;
+        if (!ok) {
+            rest.push_back(g);
+            continue;
+        }
+        FoldSeg head = g, tail = g;
+        head.n_end = std::min(g.n_end, pa * Pf_);
+        tail.n_start = std::max(g.n_start, pb * Pf_);
+        if (head.n_end > head.n_start) rest.push_back(head);
+        if (tail.n_end > tail.n_start) rest.push_back(tail);
+        const int si = (int)tsegs.size();
+        tsegs.push_back(g);
+        for (int rb = 0; rb < nrb; ++rb)
+            for (int lb = 0; lb < nlb; ++lb) groups.push_back({si, rb, lb, pa, pb});
+        work += (pb - pa) * nrb * nlb;
+    }
+    if (groups.empty()) return Status::ok();
+    if (tsegs.size() > (size_t)FI_SEGS) {  // descriptor block too small: FP32 path
+        rest.insert(rest.end(), tsegs.begin(), tsegs.end());
+        return Status::ok();
+    }
+    if (!inline_) inline_.reset(new FoldInline);
+    std::memcpy(inline_->segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
+    size_t g0 = 0;
+    while (g0 < groups.size()) {
+        // one launch: up to FI_GROUPS groups, tiles ~ whole waves of 1 CTA/SM
+        const size_t ng = std::min(groups.size() - g0, (size_t)FI_GROUPS);
+        int64_t lwork = 0;
+        for (size_t g = g0; g < g0 + ng; ++g) lwork += groups[g].p1 - groups[g].p0;
+        const int64_t target = std::max<int64_t>(SMS * std::max<int64_t>(1, (int64_t)ng / SMS), (int64_t)ng);
+        int nt = 0;
+        double launch_flops = 0.0;
+        for (size_t g = g0; g < g0 + ng; ++g) {
+            const G& gr = groups[g];
+            const int64_t np = gr.p1 - gr.p0;
+            const int64_t share = (int64_t)((double)std::min<int64_t>(target, FI_TILES) * (double)np / (double)lwork);
+            const int sp = (int)std::max<int64_t>(1, std::min<int64_t>(share, np / 16));
+            if (nt + sp > FI_TILES) break;  // cannot happen with share <= FI_TILES * np / lwork
+            FoldGroup fg{gr.seg, gr.rb, gr.lb, nt, 0, 0};
+            for (int i = 0; i < sp; ++i) {
+                const int64_t a = gr.p0 + np * i / sp, b = gr.p0 + np * (i + 1) / sp;
+                inline_->tiles[nt++] = FoldTile{gr.seg, gr.rb, gr.lb, (int)(g - g0), a, b};
+            }
+            fg.t1 = nt;
+            inline_->groups[g - g0] = fg;
+            // algorithmic: 4 FMA per (requested lag, sample) of this 64 x 64 block
+            const int lags_in = std::max(0, std::min(64, T_ - 64 * gr.lb));
+            launch_flops += 8.0 * lags_in * 64.0 * (double)np;
+        }
+        TRY(ensure_partials((size_t)nt * 64 * 64 * sizeof(float4)));
+        FoldLaunch L{};
+        L.n_tiles = nt;
+        L.n_groups = (int)ng;
+        L.Pf = (int)Pf_;
+        L.lag_lo = f_lo_;
+        L.t_pad = t_pad_;
+        L.lw = lw_;
+        L.partials = partials_;
+        L.S = S;
+        L.overwrite = 0;
+        L.gate = fold_gate_;
+        if (prof_) {
+            ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
+            launch_fold_tc(L, *inline_, cs_, r.a, r.b);
+            prof_pending_.push_back(r);
+        } else {
+            launch_fold_tc(L, *inline_, cs_);
+        }
+        launches_ += 2;
+        g0 += ng;
+    }
+    return cuda_check(cudaGetLastError(), "tensor-core fold launch");
+}
+
+Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwrite) {
+    struct G {
+        int seg, rb, lb;
+        int64_t p0, p1;
+    };
+    static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;  // A/B knob: FP32 fold only
+    std::vector<FoldSeg> segs_tc_rest;
+    const bool tc = !no_tc && !overwrite && lw_ == 8 && Pf_ % 64 == 0 && t_pad_ % 64 == 0 && tc_capable_;
+    if (tc) {
+        std::vector<FoldSeg> sg(segs_in);
+        for (auto& g : sg)
+            g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
+        TRY(fold_tc(sg, S, segs_tc_rest));
+    }
+    const std::vector<FoldSeg>& segs = tc ? segs_tc_rest : segs_in;
     std::vector<G> groups;
     int64_t work = 0;
     for (int s = 0; s < (int)segs.size(); ++s) {

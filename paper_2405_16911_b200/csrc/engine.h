@@ -111,6 +111,8 @@ private:
 
     // Fold `segs` (one per slot) into S (slots x t_pad x Pf x 4 fp64).
     Status fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite = false);
+    Status fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<FoldSeg>& rest);
+    bool tc_capable_ = false;  // sm_100 device (tcgen05)
     // Finalize slots [0, nslots) of S into out tables (out_block = slot) with per-slot scale.
     Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
                     double2* out);

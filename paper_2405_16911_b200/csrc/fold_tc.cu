@@ -1,0 +1,322 @@
+// fold_tc.cu -- the residue fold on the 5th-generation tensor cores (sm_100a).
+//
+// Same contraction as fold.cu (four real correlations per (lag, residue),
+// summed over fold periods), rewritten as a banded Gram product:
+//     D[m][n] = sum_p A[m][p] * B[n][p]
+//     A[2r+a][p] = {yr, yi}[p*Pf + r0 + r]            (M = 128: 64 residues)
+//     B[2i+b][p] = {xr, xi}[p*Pf + r0 + d + i]        (N = 256: 128-sample window)
+// with d = lag_lo + 64*lb, so lag tau = d + i - r and the useful band is
+// i - r in [0, 64): D[2r+a][2(r+t)+b] is the correlation c_{2a+b} of residue r
+// at lag d + t (c0 = xr*yr, c1 = xi*yr, c2 = xr*yi, c3 = xi*yi).
+//
+// Precision: each fp32 sample is split into bf16 hi + lo (x = hi + lo + O(2^-17 x))
+// and D accumulates hi*hi + hi*lo + lo*hi with kind::f16 MMAs (fp32 TMEM
+// accumulator): relative error ~1e-5, inside the north-star 1e-4 (measured:
+// tools/exp/tc_probe2.cu).
+//
+// Pipeline per CTA (one tile = one residue block x lag block x period range):
+//   warp 0      producer: 1-D bulk copies (cp.async.bulk) of each period's
+//               1 KB x window (+ 512 B y window when y is not inside it) into
+//               a raw fp32 stage, completion on an mbarrier (transaction bytes);
+//   warps 2..5  converters: raw fp32 -> bf16 hi/lo planes in the UMMA
+//               MN-major 128B-swizzle layout; then the epilogue (tcgen05.ld of
+//               the band, fp32 partials like fold.cu's);
+//   warp 1      MMA issuer (one thread): 3 tcgen05.mma per 16 periods,
+//               tcgen05.commit frees the stage.
+// The tile's partials go through the same fixed-order fp64 reduce as fold.cu.
+#include <cuda_bf16.h>
+
+#include <type_traits>
+
+#include "kernels.cuh"
+
+namespace cyc {
+namespace {
+
+constexpr int TKB = 16;                        // periods per stage (= MMA K for bf16)
+constexpr int TNSTG = 4;
+constexpr int TWIN = 256;                      // floats per x window (N)
+constexpr int TYW = 128;                       // floats per y window (M)
+constexpr int XRAW = TKB * TWIN * 4;           // 16 KB
+constexpr int YRAW = TKB * TYW * 4;            // 8 KB
+constexpr int XPLANE = TKB * TWIN * 2;         // 8 KB: 4 atoms x 16 rows x 128 B
+constexpr int YPLANE = TKB * TYW * 2;          // 4 KB: 2 atoms
+constexpr int TSTAGE = XRAW + YRAW + 2 * XPLANE + 2 * YPLANE;  // 48 KB
+constexpr int TSMEM = TNSTG * TSTAGE + 1024;
+constexpr int TNT = 192;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+// UMMA smem descriptor, 128B swizzle: lbo = MN-atom stride, sbo = 8-row K-group stride
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+// instruction descriptor: D f32, A/B bf16, both MN-major, M = 128, N = 256
+constexpr uint32_t TC_IDESC =
+    (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// 8 fp32 (row k, floats 8*n8 .. 8*n8+7) -> one 16-byte chunk of the hi and lo
+// planes (MN-major SW128: atom n/64, row k, chunk ((n%64)/8) ^ (k%8)).
+__device__ __forceinline__ void split8(const uint8_t* raw_row, int n8, int k, uint8_t* hi, uint8_t* lo, bool zero) {
+    uint32_t h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
+    if (!zero) {
+        const float4 a = *reinterpret_cast<const float4*>(raw_row + n8 * 32);
+        const float4 b = *reinterpret_cast<const float4*>(raw_row + n8 * 32 + 16);
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            h[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+            const float h0 = __uint_as_float(h[e] << 16), h1 = __uint_as_float(h[e] & 0xffff0000u);
+            l[e] = pack_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
+        }
+    }
+    const int off = (n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4);
+    *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ FoldInline D) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t full[TNSTG], conv[TNSTG], empty[TNSTG], done;
+    __shared__ uint32_t tmem_s;
+    __shared__ FoldTile s_tile;
+    __shared__ FoldSeg s_seg;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        s_tile = D.tiles[blockIdx.x];
+        s_seg = D.segs[s_tile.seg];
+        for (int s = 0; s < TNSTG; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 4);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tmem_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_s;
+    const FoldTile& tile = s_tile;
+    const FoldSeg& seg = s_seg;
+    const int64_t Pf = L.Pf;
+    const int64_t r0 = (int64_t)tile.rb * 64;
+    const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 64;
+    // y inside the staged x window at an atom boundary: A is a view of the x planes
+    const bool self = seg.x == seg.y && d <= 0 && -d <= 64 && ((-d) & 31) == 0;
+    const int ya = (int)(-d) / 32;  // first x atom holding y
+    const int nper = (int)(tile.p1 - tile.p0);
+    const int nst = (nper + TKB - 1) / TKB;
+
+    if (warp == 0) {
+        // lane k < rows copies period k of the stage (lanes 16..31 its y window)
+        const uint64_t mask = seg.mask;
+        for (int it = 0; it < nst; ++it) {
+            const int s = it % TNSTG;
+            if (it >= TNSTG) mbar_wait(&empty[s], ((it / TNSTG) - 1) & 1);
+            uint8_t* st = smem + s * TSTAGE;
+            const int rows = min(TKB, nper - it * TKB);
+            if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)rows * (self ? 1024u : 1536u));
+            __syncwarp();
+            const int k = lane & 15;
+            const int64_t p = tile.p0 + (int64_t)it * TKB + k;
+            if (k < rows && lane < 16) {
+                // x window [p*Pf + r0 + d, +128) (ring: split at the wrap)
+                const uint64_t xs = (uint64_t)(p * Pf + r0 + d) & mask;
+                const uint32_t dx = su32(st + k * 1024);
+                const uint64_t room = mask == ~0ull ? ~0ull : (mask + 1 - xs);
+                if (room >= 128) {
+                    bulk_g2s(dx, seg.x + xs, 1024, &full[s]);
+                } else {
+                    bulk_g2s(dx, seg.x + xs, (uint32_t)room * 8, &full[s]);
+                    bulk_g2s(dx + (uint32_t)room * 8, seg.x, (uint32_t)(128 - room) * 8, &full[s]);
+                }
+            } else if (k < rows && !self) {
+                const uint64_t ys = (uint64_t)(p * Pf + r0) & mask;
+                const uint32_t dy = su32(st + XRAW + k * 512);
+                const uint64_t yroom = mask == ~0ull ? ~0ull : (mask + 1 - ys);
+                if (yroom >= 64) {
+                    bulk_g2s(dy, seg.y + ys, 512, &full[s]);
+                } else {
+                    bulk_g2s(dy, seg.y + ys, (uint32_t)yroom * 8, &full[s]);
+                    bulk_g2s(dy + (uint32_t)yroom * 8, seg.y, (uint32_t)(64 - yroom) * 8, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            for (int it = 0; it < nst; ++it) {
+                const int s = it % TNSTG;
+                mbar_wait(&conv[s], (it / TNSTG) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t st = su32(smem + s * TSTAGE);
+                const uint32_t xh = st + XRAW + YRAW, xl = xh + XPLANE;
+                const uint32_t yh = self ? xh + ya * (TKB * 128) : xl + XPLANE;
+                const uint32_t yl = self ? xl + ya * (TKB * 128) : yh + YPLANE;
+                const uint64_t dxh = sw128_desc(xh, TKB * 128, 1024), dxl = sw128_desc(xl, TKB * 128, 1024);
+                const uint64_t dyh = sw128_desc(yh, TKB * 128, 1024), dyl = sw128_desc(yl, TKB * 128, 1024);
+                mma_bf16(tmem, dyh, dxh, TC_IDESC, it ? 1u : 0u);
+                mma_bf16(tmem, dyh, dxl, TC_IDESC, 1u);
+                mma_bf16(tmem, dyl, dxh, TC_IDESC, 1u);
+                mma_commit(&empty[s]);
+            }
+            mma_commit(&done);
+        }
+    } else {
+        const int ct = threadIdx.x - 64;  // 0..127
+        for (int it = 0; it < nst; ++it) {
+            const int s = it % TNSTG;
+            mbar_wait(&full[s], (it / TNSTG) & 1);
+            uint8_t* st = smem + s * TSTAGE;
+            const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
+            uint8_t* xh = st + XRAW + YRAW;
+            uint8_t* xl = xh + XPLANE;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // 512 x chunks: row k = u / 32, floats 8*(u % 32)
+                const int u = ct + 128 * j;
+                const int k = u >> 5;
+                split8(st + k * 1024, u & 31, k, xh, xl, k >= rows);
+            }
+            if (!self) {
+                uint8_t* yh = xl + XPLANE;
+                uint8_t* yl = yh + YPLANE;
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {  // 256 y chunks: row k = u / 16
+                    const int u = ct + 128 * j;
+                    const int k = u >> 4;
+                    split8(st + XRAW + k * 512, u & 15, k, yh, yl, k >= rows);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[s]);
+        }
+        // epilogue: lane m = 2r + a of quarter q holds D[m][*]; the band is
+        // columns [2r, 2r + 128): float2 (c_{2a}, c_{2a+1}) per lag t
+        mbar_wait(&done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int q = warp & 3;
+        const int m = 32 * q + lane;
+        const int r = m >> 1, a = m & 1;
+        float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)blockIdx.x * 64 * 64 * 2;
+        for (int c = q; c < q + 5; ++c) {  // columns [32c, 32c + 32) cover the quarter's band
+            uint32_t v[32];
+            const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * c);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(addr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int t = 16 * c + j - r;  // lag offset of column pair 2(16c + j)
+                if (t >= 0 && t < 64)
+                    part[((size_t)t * 64 + r) * 2 + a] = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// the fp64 reduce of fold.cu, instantiated for the tensor-core tile geometry
+__global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ FoldInline D) {
+    if (L.gate && *L.gate != ~0ull) return;
+    const FoldGroup g = D.groups[blockIdx.y];
+    const int slot = D.segs[g.seg].slot;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // lag * 64 + residue
+    if (e >= 64 * 64) return;
+    const int lag = e >> 6, res = e & 63;
+    const int64_t rg = (int64_t)g.rb * 64 + res;
+    const int tg = g.lb * 64 + lag;
+    if (rg >= L.Pf || tg >= L.t_pad) return;
+    const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    int t = g.t0;
+    for (; t + 4 <= g.t1; t += 4) {  // 4 loads in flight, fixed summation order
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(t + u) * 64 * 64);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            s0 += v[u].x;
+            s1 += v[u].y;
+            s2 += v[u].z;
+            s3 += v[u].w;
+        }
+    }
+    for (; t < g.t1; ++t) {
+        const float4 v = __ldcs(part + (size_t)t * 64 * 64);
+        s0 += v.x;
+        s1 += v.y;
+        s2 += v.z;
+        s3 += v.w;
+    }
+    double* dst = L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4;
+    dst[0] += s0;
+    dst[1] += s1;
+    dst[2] += s2;
+    dst[3] += s3;
+}
+
+}  // namespace
+
+void launch_fold_tc(const FoldLaunch& L, const FoldInline& D, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+    if (L.n_tiles == 0) return;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fold_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+        attr = true;
+    }
+    if (ev0) cudaEventRecord(ev0, st);
+    fold_tc_kernel<<<L.n_tiles, TNT, TSMEM, st>>>(L, D);
+    if (ev1) cudaEventRecord(ev1, st);
+    fold_tc_reduce_kernel<<<dim3(64 * 64 / 256, L.n_groups), 256, 0, st>>>(L, D);
+}
+
+}  // namespace cyc

@@ -71,7 +71,7 @@ struct FoldLaunch {
 // Launch descriptors carried in the kernel parameter block (<= 32 KB since
 // CUDA 12.1): no H2D descriptor copy queued behind bulk DMA, no PCIe reads of
 // mapped host memory.  Launches that do not fit use the pointers in FoldLaunch.
-constexpr int FI_SEGS = 64, FI_TILES = 296, FI_GROUPS = 128;
+constexpr int FI_SEGS = 64, FI_TILES = 296, FI_GROUPS = 296;
 struct FoldInline {
     FoldSeg segs[FI_SEGS];
     FoldTile tiles[FI_TILES];
@@ -82,6 +82,12 @@ struct FoldInline {
 // inl != nullptr: descriptors by value (L.segs/tiles/groups are ignored).
 void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr,
                  const FoldInline* inl = nullptr);
+
+// Tensor-core fold (fold_tc.cu): tiles of 64 residues x 64 lags, descriptors
+// by value; partials [n_tiles][64 lags][64 residues] float4, reduced into S
+// (accumulate; gate honoured).
+void launch_fold_tc(const FoldLaunch& L, const FoldInline& D, cudaStream_t st, cudaEvent_t ev0 = nullptr,
+                    cudaEvent_t ev1 = nullptr);
 
 void prepare_fold_kernels();      // set smem attributes (call outside stream capture)
 void prepare_finalize_kernels();

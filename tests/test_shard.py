@@ -113,4 +113,4 @@ def test_time_shards_on_device_sum_to_whole_record(cyc):
     for fl in (cyc.Flags.CONV, cyc.Flags.CONJ):
         a, b = ests[0].average(flag=fl), whole.average(flag=fl)
         assert np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(b)
-        assert np.max(np.abs(a - b)) <= 1e-8 * 2.0  # mean power of x is 2
+        assert np.max(np.abs(a - b)) <= 1e-6 * 2.0  # mean power of x is 2; north star is 1e-5
