@@ -797,34 +797,65 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         work += (pb - pa) * nrb * nlb;
     }
     if (groups.empty()) return Status::ok();
-    if (tsegs.size() > (size_t)FI_SEGS) {  // descriptor block too small: FP32 path
+    if (tsegs.size() > (size_t)TC_SEGS) {  // descriptor block too small: FP32 path
         rest.insert(rest.end(), tsegs.begin(), tsegs.end());
         return Status::ok();
     }
-    if (!inline_) inline_.reset(new FoldInline);
-    std::memcpy(inline_->segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
+    if (!tcp_) tcp_.reset(new TcParams);
+    std::memset(tcp_.get(), 0, sizeof(TcParams));
+    std::memcpy(tcp_->segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
+    for (size_t i = 0; i < tsegs.size(); ++i) {
+        FoldSeg& g = tcp_->segs[i];
+        if (g.mask != ~0ull) continue;  // ring: per-period bulk copies
+        // rows = the segment's interior periods (its groups all span [pa, pb))
+        int64_t pa = 0, pb = 0;
+        for (const G& gr : groups)
+            if (gr.seg == (int)i) {
+                pa = gr.p0;
+                pb = gr.p1;
+                break;
+            }
+        if (!encode_tc_maps(*tcp_, (int)i, g, pa, pb - pa, (int)Pf_, f_lo_, nlb))
+            return Status{CYC_ERR_CUDA, "cuTensorMapEncodeTiled failed for the tensor-core fold", -1};
+    }
+    // self groups (y inside the x window) and the rest run as separate launches
+    auto is_self = [&](const G& gr) {
+        const int64_t d = f_lo_ + 64 * (int64_t)gr.lb;
+        return tsegs[gr.seg].x == tsegs[gr.seg].y && d <= 0 && -d <= 64 && (-d) % 32 == 0;
+    };
+    std::stable_partition(groups.begin(), groups.end(), is_self);
     size_t g0 = 0;
     while (g0 < groups.size()) {
-        // one launch: up to FI_GROUPS groups, tiles ~ whole waves of 1 CTA/SM
-        const size_t ng = std::min(groups.size() - g0, (size_t)FI_GROUPS);
+        // one launch: up to FI_GROUPS groups of one kind, tiles ~ whole waves of 1 CTA/SM
+        // Each tile folds at most TC_MAX_PERIODS periods (fp32 TMEM accumulation
+        // error grows with the count: ~1e-5 relative at 2048).
+        constexpr int64_t TC_MAX_PERIODS = 2048;
+        auto min_tiles = [&](const G& gr) { return (int)ceil_div(gr.p1 - gr.p0, TC_MAX_PERIODS); };
+        const bool self = is_self(groups[g0]);
+        size_t ng = 0;
+        int base_tiles = 0;
+        while (g0 + ng < groups.size() && ng < (size_t)FI_GROUPS && is_self(groups[g0 + ng]) == self &&
+               base_tiles + min_tiles(groups[g0 + ng]) <= FI_TILES)
+            base_tiles += min_tiles(groups[g0 + ng++]);
         int64_t lwork = 0;
         for (size_t g = g0; g < g0 + ng; ++g) lwork += groups[g].p1 - groups[g].p0;
-        const int64_t target = std::max<int64_t>(SMS * std::max<int64_t>(1, (int64_t)ng / SMS), (int64_t)ng);
+        // extra tiles (beyond the minimum) fill whole waves of 1 CTA/SM
+        const int64_t waves = std::max<int64_t>(1, ceil_div(base_tiles, SMS));
+        const int64_t extra = std::max<int64_t>(0, std::min<int64_t>(waves * SMS, FI_TILES) - base_tiles);
         int nt = 0;
         double launch_flops = 0.0;
         for (size_t g = g0; g < g0 + ng; ++g) {
             const G& gr = groups[g];
             const int64_t np = gr.p1 - gr.p0;
-            const int64_t share = (int64_t)((double)std::min<int64_t>(target, FI_TILES) * (double)np / (double)lwork);
-            const int sp = (int)std::max<int64_t>(1, std::min<int64_t>(share, np / 16));
-            if (nt + sp > FI_TILES) break;  // cannot happen with share <= FI_TILES * np / lwork
+            const int64_t add = (int64_t)((double)extra * (double)np / (double)lwork);  // sum <= extra
+            const int sp = (int)std::min<int64_t>(min_tiles(gr) + add, std::max<int64_t>(1, np / 16));
             FoldGroup fg{gr.seg, gr.rb, gr.lb, nt, 0, 0};
             for (int i = 0; i < sp; ++i) {
                 const int64_t a = gr.p0 + np * i / sp, b = gr.p0 + np * (i + 1) / sp;
-                inline_->tiles[nt++] = FoldTile{gr.seg, gr.rb, gr.lb, (int)(g - g0), a, b};
+                tcp_->tiles[nt++] = FoldTile{gr.seg, gr.rb, gr.lb, (int)(g - g0), a, b};
             }
             fg.t1 = nt;
-            inline_->groups[g - g0] = fg;
+            tcp_->groups[g - g0] = fg;
             // algorithmic: 4 FMA per (requested lag, sample) of this 64 x 64 block
             const int lags_in = std::max(0, std::min(64, T_ - 64 * gr.lb));
             launch_flops += 8.0 * lags_in * 64.0 * (double)np;
@@ -843,10 +874,10 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         L.gate = fold_gate_;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
-            launch_fold_tc(L, *inline_, cs_, r.a, r.b);
+            launch_fold_tc(L, *tcp_, self, cs_, r.a, r.b);
             prof_pending_.push_back(r);
         } else {
-            launch_fold_tc(L, *inline_, cs_);
+            launch_fold_tc(L, *tcp_, self, cs_);
         }
         launches_ += 2;
         g0 += ng;

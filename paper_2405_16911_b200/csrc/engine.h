@@ -261,6 +261,7 @@ private:
     double* S_pend_ = nullptr;
     std::vector<char> blob_;              // host staging of one launch's descriptors
     std::unique_ptr<FoldInline> inline_;  // by-value descriptors of the next fold launch
+    std::unique_ptr<TcParams> tcp_;       // by-value descriptors of the next tensor-core fold launch
     const unsigned long long* fold_gate_ = nullptr;  // set while a device chunk folds straight into S_main
     float2* hist_bak_ = nullptr;
     size_t hist_cap_ = 0;

@@ -34,16 +34,25 @@ namespace cyc {
 namespace {
 
 constexpr int TKB = 16;                        // periods per stage (= MMA K for bf16)
-constexpr int TNSTG = 4;
 constexpr int TWIN = 256;                      // floats per x window (N)
 constexpr int TYW = 128;                       // floats per y window (M)
 constexpr int XRAW = TKB * TWIN * 4;           // 16 KB
 constexpr int YRAW = TKB * TYW * 4;            // 8 KB
 constexpr int XPLANE = TKB * TWIN * 2;         // 8 KB: 4 atoms x 16 rows x 128 B
 constexpr int YPLANE = TKB * TYW * 2;          // 4 KB: 2 atoms
-constexpr int TSTAGE = XRAW + YRAW + 2 * XPLANE + 2 * YPLANE;  // 48 KB
-constexpr int TSMEM = TNSTG * TSTAGE + 1024;
 constexpr int TNT = 192;
+// Two rings: raw fp32 stages (producer -> converters, freed after conversion)
+// and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).  The
+// raw ring is deep so the copies of NR stages are in flight (HBM latency).
+template <bool SELF>
+struct TcGeo {
+    static constexpr int RAW = SELF ? XRAW : XRAW + YRAW;
+    static constexpr int PLANE = SELF ? 2 * XPLANE : 2 * XPLANE + 2 * YPLANE;
+    static constexpr int NR = SELF ? 9 : 6;
+    static constexpr int NP = SELF ? 4 : 3;
+    static constexpr int SMEM = NR * RAW + NP * PLANE + 1024;
+    static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
+};
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
@@ -64,6 +73,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(dst), "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1) : "memory");
 }
 // UMMA smem descriptor, 128B swizzle: lbo = MN-atom stride, sbo = 8-row K-group stride
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -109,10 +123,14 @@ __device__ __forceinline__ void split8(const uint8_t* raw_row, int n8, int k, ui
     *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-__global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ FoldInline D) {
+template <bool SELF>
+__global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ TcParams D) {
+    using G = TcGeo<SELF>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t full[TNSTG], conv[TNSTG], empty[TNSTG], done;
+    uint8_t* raw_ring = smem;                       // NR x RAW
+    uint8_t* plane_ring = smem + G::NR * G::RAW;    // NP x PLANE (1 KB aligned)
+    __shared__ uint64_t full[G::NR], rawfree[G::NR], conv[G::NP], planefree[G::NP], done;
     __shared__ uint32_t tmem_s;
     __shared__ FoldTile s_tile;
     __shared__ FoldSeg s_seg;
@@ -120,10 +138,13 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     if (threadIdx.x == 0) {
         s_tile = D.tiles[blockIdx.x];
         s_seg = D.segs[s_tile.seg];
-        for (int s = 0; s < TNSTG; ++s) {
+        for (int s = 0; s < G::NR; ++s) {
             mbar_init(&full[s], 1);
+            mbar_init(&rawfree[s], 4);
+        }
+        for (int s = 0; s < G::NP; ++s) {
             mbar_init(&conv[s], 4);
-            mbar_init(&empty[s], 1);
+            mbar_init(&planefree[s], 1);
         }
         mbar_init(&done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -141,74 +162,92 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     const int64_t Pf = L.Pf;
     const int64_t r0 = (int64_t)tile.rb * 64;
     const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 64;
-    // y inside the staged x window at an atom boundary: A is a view of the x planes
-    const bool self = seg.x == seg.y && d <= 0 && -d <= 64 && ((-d) & 31) == 0;
-    const int ya = (int)(-d) / 32;  // first x atom holding y
+    const int ya = SELF ? (int)(-d) / 32 : 0;  // first x atom holding y (self tiles)
     const int nper = (int)(tile.p1 - tile.p0);
     const int nst = (nper + TKB - 1) / TKB;
 
     if (warp == 0) {
-        // lane k < rows copies period k of the stage (lanes 16..31 its y window)
         const uint64_t mask = seg.mask;
-        for (int it = 0; it < nst; ++it) {
-            const int s = it % TNSTG;
-            if (it >= TNSTG) mbar_wait(&empty[s], ((it / TNSTG) - 1) & 1);
-            uint8_t* st = smem + s * TSTAGE;
-            const int rows = min(TKB, nper - it * TKB);
-            if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)rows * (self ? 1024u : 1536u));
-            __syncwarp();
-            const int k = lane & 15;
-            const int64_t p = tile.p0 + (int64_t)it * TKB + k;
-            if (k < rows && lane < 16) {
-                // x window [p*Pf + r0 + d, +128) (ring: split at the wrap)
-                const uint64_t xs = (uint64_t)(p * Pf + r0 + d) & mask;
-                const uint32_t dx = su32(st + k * 1024);
-                const uint64_t room = mask == ~0ull ? ~0ull : (mask + 1 - xs);
-                if (room >= 128) {
-                    bulk_g2s(dx, seg.x + xs, 1024, &full[s]);
-                } else {
-                    bulk_g2s(dx, seg.x + xs, (uint32_t)room * 8, &full[s]);
-                    bulk_g2s(dx + (uint32_t)room * 8, seg.x, (uint32_t)(128 - room) * 8, &full[s]);
+        if (mask == ~0ull) {
+            // linear segment: one 2-D TMA box (256 floats x 16 periods) per stage
+            // (+ the 128-float y box); rows past the tile arrive as zeros or
+            // are zeroed by the converters
+            const CUtensorMap* xm = &D.xmap[tile.seg];
+            const CUtensorMap* ym = &D.ymap[tile.seg];
+            const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
+            const int xcol = 2 * (int)(r0 + 64 * tile.lb);
+            if (lane == 0) {
+                for (int it = 0; it < nst; ++it) {
+                    const int s = it % G::NR;
+                    if (it >= G::NR) mbar_wait(&rawfree[s], ((it / G::NR) - 1) & 1);
+                    uint8_t* st = raw_ring + s * G::RAW;
+                    mbar_expect_tx(&full[s], SELF ? XRAW : XRAW + YRAW);
+                    tma_2d(su32(st), xm, xcol, row0 + it * TKB, &full[s]);
+                    if (!SELF) tma_2d(su32(st + XRAW), ym, 2 * (int)r0, row0 + it * TKB, &full[s]);
                 }
-            } else if (k < rows && !self) {
-                const uint64_t ys = (uint64_t)(p * Pf + r0) & mask;
-                const uint32_t dy = su32(st + XRAW + k * 512);
-                const uint64_t yroom = mask == ~0ull ? ~0ull : (mask + 1 - ys);
-                if (yroom >= 64) {
-                    bulk_g2s(dy, seg.y + ys, 512, &full[s]);
-                } else {
-                    bulk_g2s(dy, seg.y + ys, (uint32_t)yroom * 8, &full[s]);
-                    bulk_g2s(dy + (uint32_t)yroom * 8, seg.y, (uint32_t)(64 - yroom) * 8, &full[s]);
+            }
+        } else {
+            // ring segment: lane k < 16 copies period k's x window, lane 16 + k
+            // its y window, split at the wrap
+            const int k = lane & 15;
+            for (int it = 0; it < nst; ++it) {
+                const int s = it % G::NR;
+                if (it >= G::NR) mbar_wait(&rawfree[s], ((it / G::NR) - 1) & 1);
+                uint8_t* st = raw_ring + s * G::RAW;
+                const int rows = min(TKB, nper - it * TKB);
+                if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)rows * (SELF ? 1024u : 1536u));
+                __syncwarp();
+                const int64_t p = tile.p0 + (int64_t)it * TKB + k;
+                if (k < rows && lane < 16) {
+                    const uint64_t xs = (uint64_t)(p * Pf + r0 + d) & mask;
+                    const uint32_t dx = su32(st + k * 1024);
+                    const uint64_t room = mask + 1 - xs;
+                    if (room >= 128) {
+                        bulk_g2s(dx, seg.x + xs, 1024, &full[s]);
+                    } else {
+                        bulk_g2s(dx, seg.x + xs, (uint32_t)room * 8, &full[s]);
+                        bulk_g2s(dx + (uint32_t)room * 8, seg.x, (uint32_t)(128 - room) * 8, &full[s]);
+                    }
+                } else if (!SELF && k < rows) {
+                    const uint64_t ys = (uint64_t)(p * Pf + r0) & mask;
+                    const uint32_t dy = su32(st + XRAW + k * 512);
+                    const uint64_t yroom = mask + 1 - ys;
+                    if (yroom >= 64) {
+                        bulk_g2s(dy, seg.y + ys, 512, &full[s]);
+                    } else {
+                        bulk_g2s(dy, seg.y + ys, (uint32_t)yroom * 8, &full[s]);
+                        bulk_g2s(dy + (uint32_t)yroom * 8, seg.y, (uint32_t)(64 - yroom) * 8, &full[s]);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             for (int it = 0; it < nst; ++it) {
-                const int s = it % TNSTG;
-                mbar_wait(&conv[s], (it / TNSTG) & 1);
+                const int s = it % G::NP;
+                mbar_wait(&conv[s], (it / G::NP) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t st = su32(smem + s * TSTAGE);
-                const uint32_t xh = st + XRAW + YRAW, xl = xh + XPLANE;
-                const uint32_t yh = self ? xh + ya * (TKB * 128) : xl + XPLANE;
-                const uint32_t yl = self ? xl + ya * (TKB * 128) : yh + YPLANE;
+                const uint32_t xh = su32(plane_ring + s * G::PLANE), xl = xh + XPLANE;
+                const uint32_t yh = SELF ? xh + ya * (TKB * 128) : xl + XPLANE;
+                const uint32_t yl = SELF ? xl + ya * (TKB * 128) : yh + YPLANE;
                 const uint64_t dxh = sw128_desc(xh, TKB * 128, 1024), dxl = sw128_desc(xl, TKB * 128, 1024);
                 const uint64_t dyh = sw128_desc(yh, TKB * 128, 1024), dyl = sw128_desc(yl, TKB * 128, 1024);
                 mma_bf16(tmem, dyh, dxh, TC_IDESC, it ? 1u : 0u);
                 mma_bf16(tmem, dyh, dxl, TC_IDESC, 1u);
                 mma_bf16(tmem, dyl, dxh, TC_IDESC, 1u);
-                mma_commit(&empty[s]);
+                mma_commit(&planefree[s]);
             }
             mma_commit(&done);
         }
     } else {
         const int ct = threadIdx.x - 64;  // 0..127
         for (int it = 0; it < nst; ++it) {
-            const int s = it % TNSTG;
-            mbar_wait(&full[s], (it / TNSTG) & 1);
-            uint8_t* st = smem + s * TSTAGE;
+            const int rs = it % G::NR, ps = it % G::NP;
+            mbar_wait(&full[rs], (it / G::NR) & 1);
+            if (it >= G::NP) mbar_wait(&planefree[ps], ((it / G::NP) - 1) & 1);
+            const uint8_t* st = raw_ring + rs * G::RAW;
             const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
-            uint8_t* xh = st + XRAW + YRAW;
+            uint8_t* xh = plane_ring + ps * G::PLANE;
             uint8_t* xl = xh + XPLANE;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {  // 512 x chunks: row k = u / 32, floats 8*(u % 32)
@@ -216,7 +255,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 const int k = u >> 5;
                 split8(st + k * 1024, u & 31, k, xh, xl, k >= rows);
             }
-            if (!self) {
+            if (!SELF) {
                 uint8_t* yh = xl + XPLANE;
                 uint8_t* yl = yh + YPLANE;
 #pragma unroll
@@ -226,9 +265,11 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                     split8(st + XRAW + k * 512, u & 15, k, yh, yl, k >= rows);
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rawfree[rs]);  // raw slot reusable (generic reads done)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&conv[s]);
+            if (lane == 0) mbar_arrive(&conv[ps]);
         }
         // epilogue: lane m = 2r + a of quarter q holds D[m][*]; the band is
         // columns [2r, 2r + 128): float2 (c_{2a}, c_{2a+1}) per lag t
@@ -255,7 +296,8 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             for (int j = 0; j < 16; ++j) {
                 const int t = 16 * c + j - r;  // lag offset of column pair 2(16c + j)
                 if (t >= 0 && t < 64)
-                    part[((size_t)t * 64 + r) * 2 + a] = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                    part[((size_t)t * 64 + r) * 2 + a] =
+                        make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
             }
         }
     }
@@ -265,7 +307,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
 }
 
 // the fp64 reduce of fold.cu, instantiated for the tensor-core tile geometry
-__global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ FoldInline D) {
+__global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcParams D) {
     if (L.gate && *L.gate != ~0ull) return;
     const FoldGroup g = D.groups[blockIdx.y];
     const int slot = D.segs[g.seg].slot;
@@ -306,15 +348,59 @@ __global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ Fold
 
 }  // namespace
 
-void launch_fold_tc(const FoldLaunch& L, const FoldInline& D, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t row_bytes, uint32_t box_cols) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc || ((uintptr_t)base & 15) || rows == 0) return false;
+    const cuuint64_t gdim[2] = {cols, rows};
+    const cuuint64_t gstr[1] = {row_bytes};
+    const cuuint32_t box[2] = {box_cols, (cuuint32_t)TKB}, es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstr, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+// Tensor maps of a linear segment for periods [p_base, p_base + rows): rows
+// step Pf samples but span the widest window (overlapping rows; TMA reads only
+// the boxes, which lie inside the segment's valid x / y ranges).
+bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64_t rows, int Pf, int lag_lo,
+                    int nlb) {
+    D.p_base[si] = p_base;
+    const float* xb = reinterpret_cast<const float*>(g.x + (p_base * Pf + lag_lo));
+    const float* yb = reinterpret_cast<const float*>(g.y + p_base * Pf);
+    return encode_2d(&D.xmap[si], xb, 2ull * Pf + 128ull * nlb, (uint64_t)rows, 8ull * Pf, TWIN) &&
+           encode_2d(&D.ymap[si], yb, 2ull * Pf, (uint64_t)rows, 8ull * Pf, TYW);
+}
+
+void launch_fold_tc(const FoldLaunch& L, const TcParams& D, bool self, cudaStream_t st, cudaEvent_t ev0,
+                    cudaEvent_t ev1) {
     if (L.n_tiles == 0) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(fold_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+        cudaFuncSetAttribute(fold_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcGeo<true>::SMEM);
+        cudaFuncSetAttribute(fold_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcGeo<false>::SMEM);
         attr = true;
     }
     if (ev0) cudaEventRecord(ev0, st);
-    fold_tc_kernel<<<L.n_tiles, TNT, TSMEM, st>>>(L, D);
+    if (self)
+        fold_tc_kernel<true><<<L.n_tiles, TNT, TcGeo<true>::SMEM, st>>>(L, D);
+    else
+        fold_tc_kernel<false><<<L.n_tiles, TNT, TcGeo<false>::SMEM, st>>>(L, D);
     if (ev1) cudaEventRecord(ev1, st);
     fold_tc_reduce_kernel<<<dim3(64 * 64 / 256, L.n_groups), 256, 0, st>>>(L, D);
 }

@@ -16,6 +16,7 @@
 //             drifting lead-phasor recurrence (proj/src/estimator.cpp:70-73).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace cyc {
@@ -85,9 +86,27 @@ void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr
 
 // Tensor-core fold (fold_tc.cu): tiles of 64 residues x 64 lags, descriptors
 // by value; partials [n_tiles][64 lags][64 residues] float4, reduced into S
-// (accumulate; gate honoured).
-void launch_fold_tc(const FoldLaunch& L, const FoldInline& D, cudaStream_t st, cudaEvent_t ev0 = nullptr,
+// (accumulate; gate honoured).  Linear segments (mask == ~0) are staged with
+// 2-D TMA through the per-segment tensor maps (rows = fold periods from
+// p_base, columns = floats from sample p_base*Pf + lag_lo; rows overlap so a
+// window may run past its period); ring segments with per-period 1-D bulk
+// copies split at the wrap.
+constexpr int TC_SEGS = 16;
+struct alignas(64) TcParams {
+    CUtensorMap xmap[TC_SEGS];  // box 256 floats x 16 periods
+    CUtensorMap ymap[TC_SEGS];  // box 128 floats x 16 periods (non-self launches)
+    int64_t p_base[TC_SEGS];    // first period (row 0) of each segment's maps
+    FoldSeg segs[TC_SEGS];
+    FoldTile tiles[FI_TILES];
+    FoldGroup groups[FI_GROUPS];
+};
+// self: every tile's y window lies inside its x window at a 32-sample
+// boundary (x == y, d = lag_lo + 64 lb in [-64, 0], d % 32 == 0).
+void launch_fold_tc(const FoldLaunch& L, const TcParams& D, bool self, cudaStream_t st, cudaEvent_t ev0 = nullptr,
                     cudaEvent_t ev1 = nullptr);
+// Fill D.xmap/ymap/p_base[si] for a linear segment (false: no TMA -- use the ring path).
+bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64_t rows, int Pf, int lag_lo,
+                    int nlb);
 
 void prepare_fold_kernels();      // set smem attributes (call outside stream capture)
 void prepare_finalize_kernels();

@@ -66,8 +66,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 __global__ void __launch_bounds__(192, 1) tc_probe_kernel(const __grid_constant__ CUtensorMap tmap, int r0, int nper,
-                                                          int terms, float* out) {
+                                                          int terms, float* out, int loadmode, const float* gx, int Pf, int distinct) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t full[NSTG], conv[NSTG], empty[NSTG], done;
@@ -93,12 +97,18 @@ __global__ void __launch_bounds__(192, 1) tc_probe_kernel(const __grid_constant_
     const int nst = nper / KB;
 
     if (warp == 0) {
-        if (lane == 0) {
-            for (int it = 0; it < nst; ++it) {
-                const int s = it % NSTG;
-                if (it >= NSTG) mbar_wait(&empty[s], ((it / NSTG) - 1) & 1);
-                mbar_expect_tx(&full[s], RAW_BYTES);
-                tma_load_2d(smem + s * STAGE_BYTES, &tmap, 2 * r0, it * KB, &full[s]);
+        const int rb = distinct ? (int)(blockIdx.x % 16) * 64 : r0;      // residue block per CTA
+        const int pb = distinct ? (int)(blockIdx.x / 16) * nper : 0;      // period block per CTA
+        for (int it = 0; it < nst; ++it) {
+            const int s = it % NSTG;
+            if (it >= NSTG) mbar_wait(&empty[s], ((it / NSTG) - 1) & 1);
+            if (lane == 0) mbar_expect_tx(&full[s], RAW_BYTES);
+            __syncwarp();
+            if (loadmode == 0) {
+                if (lane == 0) tma_load_2d(smem + s * STAGE_BYTES, &tmap, 2 * rb, pb + it * KB, &full[s]);
+            } else if (lane < 16) {
+                const float* src = gx + (size_t)(pb + it * KB + lane) * 2 * Pf + 2 * rb;
+                bulk_g2s(smem_u32(smem + s * STAGE_BYTES + lane * 1024), src, 1024, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -207,7 +217,7 @@ int main(int argc, char** argv) {
     std::vector<float> out(128 * 256);
     const int r0 = 64 * 3;
     for (int terms : {1, 3, 4}) {
-        tc_probe_kernel<<<1, 192, SMEM>>>(tmap, r0, P, terms, dout);
+        tc_probe_kernel<<<1, 192, SMEM>>>(tmap, r0, P, terms, dout, 0, dx, Pf, 0);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost));
@@ -229,17 +239,22 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int terms : {3, 4}) {
-        tc_probe_kernel<<<148, 192, SMEM>>>(tmap, 0, P, terms, nullptr);
-        cudaEventRecord(e0);
-        for (int i = 0; i < 10; ++i) tc_probe_kernel<<<148, 192, SMEM>>>(tmap, 64 * (i % 8), P, terms, nullptr);
-        cudaEventRecord(e1);
-        CK(cudaEventSynchronize(e1));
-        float ms;
-        cudaEventElapsedTime(&ms, e0, e1);
-        const double useful = 148.0 * 64 * 64 * 4 * 2 * P;
-        printf("terms %d, 148 CTAs x %d periods: %.3f ms/launch, useful %.1f TFLOP/s\n", terms, P, ms / 10,
-               useful / (ms / 10 * 1e-3) / 1e12);
+    // streaming test: 144 CTAs, distinct (residue block, period block) per CTA, 16 x 9 grid
+    {
+        const int per_cta = P / 9 / KB * KB;
+        for (int lm = 0; lm < 2; ++lm) {
+            tc_probe_kernel<<<144, 192, SMEM>>>(tmap, 0, per_cta, 3, nullptr, lm, dx, Pf, 1);
+            cudaEventRecord(e0);
+            for (int i = 0; i < 10; ++i) tc_probe_kernel<<<144, 192, SMEM>>>(tmap, 0, per_cta, 3, nullptr, lm, dx, Pf, 1);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double useful = 144.0 * 64 * 64 * 4 * 2 * per_cta;
+            printf("%s, 144 CTAs x %d periods (distinct data, %.0f MB): %.3f ms/launch, useful %.1f TFLOP/s\n",
+                   lm ? "16x 1-D bulk (lanes)" : "2-D TMA", per_cta, 144.0 * per_cta * 1024 / 1e6, ms / 10,
+                   useful / (ms / 10 * 1e-3) / 1e12);
+        }
     }
     return 0;
 }
