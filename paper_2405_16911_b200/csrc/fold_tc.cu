@@ -103,13 +103,23 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
 // 8 fp32 (row k, floats 8*n8 .. 8*n8+7) -> one 16-byte chunk of the hi and lo
 // planes (MN-major SW128: atom n/64, row k, chunk ((n%64)/8) ^ (k%8)).
-__device__ __forceinline__ void split8(const uint8_t* raw_row, int n8, int k, uint8_t* hi, uint8_t* lo, bool zero) {
+// Shared-window addresses throughout (LDS/STS, not generic loads/stores).
+__device__ __forceinline__ void split8(uint32_t raw_row, int n8, int k, uint32_t hi, uint32_t lo, bool zero) {
     uint32_t h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
     if (!zero) {
-        const float4 a = *reinterpret_cast<const float4*>(raw_row + n8 * 32);
-        const float4 b = *reinterpret_cast<const float4*>(raw_row + n8 * 32 + 16);
+        const float4 a = lds128(raw_row + n8 * 32);
+        const float4 b = lds128(raw_row + n8 * 32 + 16);
         const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -118,9 +128,9 @@ __device__ __forceinline__ void split8(const uint8_t* raw_row, int n8, int k, ui
             l[e] = pack_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
         }
     }
-    const int off = (n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4);
-    *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    const uint32_t off = (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
+    sts128(hi + off, h[0], h[1], h[2], h[3]);
+    sts128(lo + off, l[0], l[1], l[2], l[3]);
 }
 
 template <bool SELF>
@@ -245,10 +255,10 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             const int rs = it % G::NR, ps = it % G::NP;
             mbar_wait(&full[rs], (it / G::NR) & 1);
             if (it >= G::NP) mbar_wait(&planefree[ps], ((it / G::NP) - 1) & 1);
-            const uint8_t* st = raw_ring + rs * G::RAW;
+            const uint32_t st = su32(raw_ring + rs * G::RAW);
             const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
-            uint8_t* xh = plane_ring + ps * G::PLANE;
-            uint8_t* xl = xh + XPLANE;
+            const uint32_t xh = su32(plane_ring + ps * G::PLANE);
+            const uint32_t xl = xh + XPLANE;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {  // 512 x chunks: row k = u / 32, floats 8*(u % 32)
                 const int u = ct + 128 * j;
@@ -256,8 +266,8 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 split8(st + k * 1024, u & 31, k, xh, xl, k >= rows);
             }
             if (!SELF) {
-                uint8_t* yh = xl + XPLANE;
-                uint8_t* yl = yh + YPLANE;
+                const uint32_t yh = xl + XPLANE;
+                const uint32_t yl = yh + YPLANE;
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {  // 256 y chunks: row k = u / 16
                     const int u = ct + 128 * j;
