@@ -40,7 +40,8 @@ constexpr int XRAW = TKB * TWIN * 4;           // 16 KB
 constexpr int YRAW = TKB * TYW * 4;            // 8 KB
 constexpr int XPLANE = TKB * TWIN * 2;         // 8 KB: 4 atoms x 16 rows x 128 B
 constexpr int YPLANE = TKB * TYW * 2;          // 4 KB: 2 atoms
-constexpr int TNT = 192;
+constexpr int TNT = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 converters/epilogue
+constexpr int TNC = 8;    // converter warps
 // Two rings: raw fp32 stages (producer -> converters, freed after conversion)
 // and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).  The
 // raw ring is deep so the copies of NR stages are in flight (HBM latency).
@@ -150,10 +151,10 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         s_seg = D.segs[s_tile.seg];
         for (int s = 0; s < G::NR; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&rawfree[s], 4);
+            mbar_init(&rawfree[s], TNC);
         }
         for (int s = 0; s < G::NP; ++s) {
-            mbar_init(&conv[s], 4);
+            mbar_init(&conv[s], TNC);
             mbar_init(&planefree[s], 1);
         }
         mbar_init(&done, 1);
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             mma_commit(&done);
         }
     } else {
-        const int ct = threadIdx.x - 64;  // 0..127
+        const int ct = threadIdx.x - 64;  // 0 .. 32*TNC-1
         for (int it = 0; it < nst; ++it) {
             const int rs = it % G::NR, ps = it % G::NP;
             mbar_wait(&full[rs], (it / G::NR) & 1);
@@ -260,8 +261,8 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             const uint32_t xh = su32(plane_ring + ps * G::PLANE);
             const uint32_t xl = xh + XPLANE;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {  // 512 x chunks: row k = u / 32, floats 8*(u % 32)
-                const int u = ct + 128 * j;
+            for (int j = 0; j < 512 / (32 * TNC); ++j) {  // 512 x chunks: row k = u / 32, floats 8*(u % 32)
+                const int u = ct + 32 * TNC * j;
                 const int k = u >> 5;
                 split8(st + k * 1024, u & 31, k, xh, xl, k >= rows);
             }
@@ -269,8 +270,8 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 const uint32_t yh = xl + XPLANE;
                 const uint32_t yl = yh + YPLANE;
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {  // 256 y chunks: row k = u / 16
-                    const int u = ct + 128 * j;
+                for (int j = 0; j < 256 / (32 * TNC); ++j) {  // 256 y chunks: row k = u / 16
+                    const int u = ct + 32 * TNC * j;
                     const int k = u >> 4;
                     split8(st + XRAW + k * 512, u & 15, k, yh, yl, k >= rows);
                 }
@@ -289,7 +290,10 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         const int m = 32 * q + lane;
         const int r = m >> 1, a = m & 1;
         float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)blockIdx.x * 64 * 64 * 2;
-        for (int c = q; c < q + 5; ++c) {  // columns [32c, 32c + 32) cover the quarter's band
+        // columns [32c, 32c + 32), c = q .. q+4, cover the quarter's band; the
+        // two warps of a quarter split them 3 + 2
+        const int c_lo = warp < 6 ? q : q + 3, c_hi = warp < 6 ? q + 3 : q + 5;
+        for (int c = c_lo; c < c_hi; ++c) {
             uint32_t v[32];
             const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * c);
             asm volatile(
