@@ -40,8 +40,8 @@ constexpr int XRAW = TKB * TWIN * 4;           // 16 KB
 constexpr int YRAW = TKB * TYW * 4;            // 8 KB
 constexpr int XPLANE = TKB * TWIN * 2;         // 8 KB: 4 atoms x 16 rows x 128 B
 constexpr int YPLANE = TKB * TYW * 2;          // 4 KB: 2 atoms
-constexpr int TNT = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 converters/epilogue
-constexpr int TNC = 8;    // converter warps
+constexpr int TNC = 8;              // converter / epilogue warps (warps 2 .. TNC+1)
+constexpr int TNT = 64 + 32 * TNC;  // + warp 0 producer, warp 1 MMA issuer
 // Two rings: raw fp32 stages (producer -> converters, freed after conversion)
 // and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).  The
 // raw ring is deep so the copies of NR stages are in flight (HBM latency).
@@ -113,14 +113,14 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 
-// 8 fp32 (row k, floats 8*n8 .. 8*n8+7) -> one 16-byte chunk of the hi and lo
-// planes (MN-major SW128: atom n/64, row k, chunk ((n%64)/8) ^ (k%8)).
-// Shared-window addresses throughout (LDS/STS, not generic loads/stores).
-__device__ __forceinline__ void split8(uint32_t raw_row, int n8, int k, uint32_t hi, uint32_t lo, bool zero) {
+// 8 fp32 of row k (two 16-byte raw chunks at ra, rb) -> one 16-byte chunk of
+// the hi and lo planes for floats 8*n8 .. 8*n8+7 (MN-major SW128: atom n/64,
+// row k, chunk ((n%64)/8) ^ (k%8)).  Shared-window addresses (LDS/STS).
+__device__ __forceinline__ void split8(uint32_t ra, uint32_t rb, int n8, int k, uint32_t hi, uint32_t lo, bool zero) {
     uint32_t h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
     if (!zero) {
-        const float4 a = lds128(raw_row + n8 * 32);
-        const float4 b = lds128(raw_row + n8 * 32 + 16);
+        const float4 a = lds128(ra);
+        const float4 b = lds128(rb);
         const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -132,6 +132,30 @@ __device__ __forceinline__ void split8(uint32_t raw_row, int n8, int k, uint32_t
     const uint32_t off = (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
     sts128(hi + off, h[0], h[1], h[2], h[3]);
     sts128(lo + off, l[0], l[1], l[2], l[3]);
+}
+
+// Unit u of a raw stage region (boxes of 32 floats x 16 rows): box a = u / 64;
+// within the box a warp takes one 8-row group and each quarter-warp the row
+// pair (k1, k1 ^ 5), 8-float groups m = 0..3 of both rows.  With the TMA 128B
+// swizzle (chunk c of row k at c ^ (k % 8)) the raw reads, (2m | 2m+1) ^ k,
+// and the plane writes, (4(a%2) + m) ^ k, of a quarter-warp then land on 8
+// distinct 16-byte bank groups: k1 ^ k2 = 5 has bits 0 and 2 set.
+// swz == false: rows are linear (1-D bulk copies, row pitch `pitch`).
+__device__ __forceinline__ void convert_unit(uint32_t raw, int u, bool swz, uint32_t pitch, uint32_t hi, uint32_t lo,
+                                             int rows) {
+    const int a = u >> 6, w = u & 63, l = w & 31, qd = l >> 3, pos = l & 7;
+    const int m = pos & 3;
+    const int k = 8 * (w >> 5) + ((pos >> 2) ? (qd ^ 5) : qd);
+    uint32_t ra, rb;
+    if (swz) {
+        const uint32_t row = raw + (uint32_t)(a * (TKB * 128) + k * 128);
+        ra = row + ((uint32_t)((2 * m) ^ (k & 7)) << 4);
+        rb = row + ((uint32_t)((2 * m + 1) ^ (k & 7)) << 4);
+    } else {
+        ra = raw + (uint32_t)k * pitch + (uint32_t)(a * 128 + m * 32);
+        rb = ra + 16;
+    }
+    split8(ra, rb, 4 * a + m, k, hi, lo, k >= rows);
 }
 
 template <bool SELF>
@@ -176,6 +200,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     const int ya = SELF ? (int)(-d) / 32 : 0;  // first x atom holding y (self tiles)
     const int nper = (int)(tile.p1 - tile.p0);
     const int nst = (nper + TKB - 1) / TKB;
+    const bool swz = seg.mask == ~0ull;  // TMA-staged (128B-swizzled boxes) vs bulk-copied rows
 
     if (warp == 0) {
         const uint64_t mask = seg.mask;
@@ -193,8 +218,14 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                     if (it >= G::NR) mbar_wait(&rawfree[s], ((it / G::NR) - 1) & 1);
                     uint8_t* st = raw_ring + s * G::RAW;
                     mbar_expect_tx(&full[s], SELF ? XRAW : XRAW + YRAW);
-                    tma_2d(su32(st), xm, xcol, row0 + it * TKB, &full[s]);
-                    if (!SELF) tma_2d(su32(st + XRAW), ym, 2 * (int)r0, row0 + it * TKB, &full[s]);
+#pragma unroll
+                    for (int a = 0; a < TWIN / 32; ++a)
+                        tma_2d(su32(st) + a * (TKB * 128), xm, xcol + 32 * a, row0 + it * TKB, &full[s]);
+                    if (!SELF)
+#pragma unroll
+                        for (int a = 0; a < TYW / 32; ++a)
+                            tma_2d(su32(st + XRAW) + a * (TKB * 128), ym, 2 * (int)r0 + 32 * a, row0 + it * TKB,
+                                   &full[s]);
                 }
             }
         } else {
@@ -261,20 +292,12 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             const uint32_t xh = su32(plane_ring + ps * G::PLANE);
             const uint32_t xl = xh + XPLANE;
 #pragma unroll
-            for (int j = 0; j < 512 / (32 * TNC); ++j) {  // 512 x chunks: row k = u / 32, floats 8*(u % 32)
-                const int u = ct + 32 * TNC * j;
-                const int k = u >> 5;
-                split8(st + k * 1024, u & 31, k, xh, xl, k >= rows);
-            }
+            for (int u = ct; u < 512; u += 32 * TNC) convert_unit(st, u, swz, 1024, xh, xl, rows);
             if (!SELF) {
                 const uint32_t yh = xl + XPLANE;
                 const uint32_t yl = yh + YPLANE;
 #pragma unroll
-                for (int j = 0; j < 256 / (32 * TNC); ++j) {  // 256 y chunks: row k = u / 16
-                    const int u = ct + 32 * TNC * j;
-                    const int k = u >> 4;
-                    split8(st + XRAW + k * 512, u & 15, k, yh, yl, k >= rows);
-                }
+                for (int u = ct; u < 256; u += 32 * TNC) convert_unit(st + XRAW, u, swz, 512, yh, yl, rows);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&rawfree[rs]);  // raw slot reusable (generic reads done)
@@ -291,9 +314,8 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         const int r = m >> 1, a = m & 1;
         float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)blockIdx.x * 64 * 64 * 2;
         // columns [32c, 32c + 32), c = q .. q+4, cover the quarter's band; the
-        // two warps of a quarter split them 3 + 2
-        const int c_lo = warp < 6 ? q : q + 3, c_hi = warp < 6 ? q + 3 : q + 5;
-        for (int c = c_lo; c < c_hi; ++c) {
+        // TNC/4 warps of a quarter take every (TNC/4)-th chunk
+        for (int c = q + (warp - 2) / 4; c < q + 5; c += TNC / 4) {
             uint32_t v[32];
             const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * c);
             asm volatile(
@@ -377,14 +399,14 @@ EncodeTiledFn encode_fn() {
     }();
     return fn;
 }
-bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t row_bytes, uint32_t box_cols) {
+bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t row_bytes) {
     EncodeTiledFn enc = encode_fn();
     if (!enc || ((uintptr_t)base & 15) || rows == 0) return false;
     const cuuint64_t gdim[2] = {cols, rows};
     const cuuint64_t gstr[1] = {row_bytes};
-    const cuuint32_t box[2] = {box_cols, (cuuint32_t)TKB}, es[2] = {1, 1};
+    const cuuint32_t box[2] = {32, (cuuint32_t)TKB}, es[2] = {1, 1};  // one 128-byte swizzle atom column
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstr, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace
@@ -397,8 +419,8 @@ bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64
     D.p_base[si] = p_base;
     const float* xb = reinterpret_cast<const float*>(g.x + (p_base * Pf + lag_lo));
     const float* yb = reinterpret_cast<const float*>(g.y + p_base * Pf);
-    return encode_2d(&D.xmap[si], xb, 2ull * Pf + 128ull * nlb, (uint64_t)rows, 8ull * Pf, TWIN) &&
-           encode_2d(&D.ymap[si], yb, 2ull * Pf, (uint64_t)rows, 8ull * Pf, TYW);
+    return encode_2d(&D.xmap[si], xb, 2ull * Pf + 128ull * nlb, (uint64_t)rows, 8ull * Pf) &&
+           encode_2d(&D.ymap[si], yb, 2ull * Pf, (uint64_t)rows, 8ull * Pf);
 }
 
 void launch_fold_tc(const FoldLaunch& L, const TcParams& D, bool self, cudaStream_t st, cudaEvent_t ev0,

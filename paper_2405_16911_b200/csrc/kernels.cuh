@@ -93,8 +93,8 @@ void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr
 // copies split at the wrap.
 constexpr int TC_SEGS = 16;
 struct alignas(64) TcParams {
-    CUtensorMap xmap[TC_SEGS];  // box 256 floats x 16 periods
-    CUtensorMap ymap[TC_SEGS];  // box 128 floats x 16 periods (non-self launches)
+    CUtensorMap xmap[TC_SEGS];  // box 32 floats x 16 periods, 128B swizzle (8 boxes per window)
+    CUtensorMap ymap[TC_SEGS];  // same boxes over y (non-self launches: 4 per window)
     int64_t p_base[TC_SEGS];    // first period (row 0) of each segment's maps
     FoldSeg segs[TC_SEGS];
     FoldTile tiles[FI_TILES];
