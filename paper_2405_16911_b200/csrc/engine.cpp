@@ -770,7 +770,7 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         int seg, rb, lb;
         int64_t p0, p1;
     };
-    const int nrb = (int)(Pf_ / 64), nlb = t_pad_ / 64;
+    const int nrb = (int)(Pf_ / 128), nlb = t_pad_ / 64;  // tiles: 128 residues x 64 lags
     std::vector<G> groups;
     std::vector<FoldSeg> tsegs;
     int64_t work = 0;
@@ -856,11 +856,11 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
             }
             fg.t1 = nt;
             tcp_->groups[g - g0] = fg;
-            // algorithmic: 4 FMA per (requested lag, sample) of this 64 x 64 block
+            // algorithmic: 4 FMA per (requested lag, sample) of this 128-residue x 64-lag block
             const int lags_in = std::max(0, std::min(64, T_ - 64 * gr.lb));
-            launch_flops += 8.0 * lags_in * 64.0 * (double)np;
+            launch_flops += 8.0 * lags_in * 128.0 * (double)np;
         }
-        TRY(ensure_partials((size_t)nt * 64 * 64 * sizeof(float4)));
+        TRY(ensure_partials((size_t)nt * 64 * 128 * sizeof(float4)));
         FoldLaunch L{};
         L.n_tiles = nt;
         L.n_groups = (int)ng;
@@ -872,6 +872,7 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         L.S = S;
         L.overwrite = 0;
         L.gate = fold_gate_;
+        L.dbg = std::getenv("CYC_TC_DBG") ? std::atoi(std::getenv("CYC_TC_DBG")) : 0;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
             launch_fold_tc(L, *tcp_, self, cs_, r.a, r.b);
@@ -892,7 +893,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
     };
     static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;  // A/B knob: FP32 fold only
     std::vector<FoldSeg> segs_tc_rest;
-    const bool tc = !no_tc && !overwrite && lw_ == 8 && Pf_ % 64 == 0 && t_pad_ % 64 == 0 && tc_capable_;
+    const bool tc = !no_tc && !overwrite && lw_ == 8 && Pf_ % 128 == 0 && t_pad_ % 64 == 0 && tc_capable_;
     if (tc) {
         std::vector<FoldSeg> sg(segs_in);
         for (auto& g : sg)

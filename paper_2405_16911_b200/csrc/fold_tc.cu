@@ -8,6 +8,9 @@
 // with d = lag_lo + 64*lb, so lag tau = d + i - r and the useful band is
 // i - r in [0, 64): D[2r+a][2(r+t)+b] is the correlation c_{2a+b} of residue r
 // at lag d + t (c0 = xr*yr, c1 = xi*yr, c2 = xr*yi, c3 = xi*yi).
+// A CTA covers 128 residues with two such products (TMEM columns 0..255 and
+// 256..511) over one staged 192-sample window, so each x sample is read 1.5x
+// (not 2x) from L2 -- the staging bandwidth is this kernel's floor.
 //
 // Precision: each fp32 sample is split into bf16 hi + lo (x = hi + lo + O(2^-17 x))
 // and D accumulates hi*hi + hi*lo + lo*hi with kind::f16 MMAs (fp32 TMEM
@@ -33,24 +36,25 @@
 namespace cyc {
 namespace {
 
-constexpr int TKB = 16;                        // periods per stage (= MMA K for bf16)
-constexpr int TWIN = 256;                      // floats per x window (N)
-constexpr int TYW = 128;                       // floats per y window (M)
-constexpr int XRAW = TKB * TWIN * 4;           // 16 KB
-constexpr int YRAW = TKB * TYW * 4;            // 8 KB
-constexpr int XPLANE = TKB * TWIN * 2;         // 8 KB: 4 atoms x 16 rows x 128 B
-constexpr int YPLANE = TKB * TYW * 2;          // 4 KB: 2 atoms
-constexpr int TNC = 8;              // converter / epilogue warps (warps 2 .. TNC+1)
-constexpr int TNT = 64 + 32 * TNC;  // + warp 0 producer, warp 1 MMA issuer
+constexpr int TKB = 16;                 // periods per stage (= MMA K for bf16)
+constexpr int TRB = 128;                // residues per CTA (two 64-residue halves)
+constexpr int XF = 2 * (TRB + 64);      // floats per x window: 192 samples
+constexpr int YF = 2 * TRB;             // floats per y window: 128 samples
+constexpr int XRAW = TKB * XF * 4;      // 24 KB (12 TMA boxes of 32 floats x 16 rows)
+constexpr int YRAW = TKB * YF * 4;      // 16 KB
+constexpr int ATOM = TKB * 128;         // one MN atom column of a plane: 64 bf16 x 16 rows
+constexpr int XPLANE = TKB * XF * 2;    // 12 KB: 6 atoms
+constexpr int YPLANE = TKB * YF * 2;    // 8 KB: 4 atoms
+constexpr int TNC = 8;                  // converter / epilogue warps (warps 2 .. TNC+1)
+constexpr int TNT = 64 + 32 * TNC;      // + warp 0 producer, warp 1 MMA issuer
 // Two rings: raw fp32 stages (producer -> converters, freed after conversion)
-// and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).  The
-// raw ring is deep so the copies of NR stages are in flight (HBM latency).
+// and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).
 template <bool SELF>
 struct TcGeo {
     static constexpr int RAW = SELF ? XRAW : XRAW + YRAW;
     static constexpr int PLANE = SELF ? 2 * XPLANE : 2 * XPLANE + 2 * YPLANE;
-    static constexpr int NR = SELF ? 9 : 6;
-    static constexpr int NP = SELF ? 4 : 3;
+    static constexpr int NR = SELF ? 5 : 3;
+    static constexpr int NP = SELF ? 4 : 2;
     static constexpr int SMEM = NR * RAW + NP * PLANE + 1024;
     static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
 };
@@ -184,8 +188,8 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         mbar_init(&done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tmem_s)));
+    if (warp == 1) {  // two 128 x 256 fp32 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_s)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     const FoldTile& tile = s_tile;
     const FoldSeg& seg = s_seg;
     const int64_t Pf = L.Pf;
-    const int64_t r0 = (int64_t)tile.rb * 64;
+    const int64_t r0 = (int64_t)tile.rb * TRB;
     const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 64;
     const int ya = SELF ? (int)(-d) / 32 : 0;  // first x atom holding y (self tiles)
     const int nper = (int)(tile.p1 - tile.p0);
@@ -205,9 +209,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     if (warp == 0) {
         const uint64_t mask = seg.mask;
         if (mask == ~0ull) {
-            // linear segment: one 2-D TMA box (256 floats x 16 periods) per stage
-            // (+ the 128-float y box); rows past the tile arrive as zeros or
-            // are zeroed by the converters
+            // linear segment: 2-D TMA boxes (32 floats x 16 periods) per stage
             const CUtensorMap* xm = &D.xmap[tile.seg];
             const CUtensorMap* ym = &D.ymap[tile.seg];
             const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
@@ -216,16 +218,14 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 for (int it = 0; it < nst; ++it) {
                     const int s = it % G::NR;
                     if (it >= G::NR) mbar_wait(&rawfree[s], ((it / G::NR) - 1) & 1);
-                    uint8_t* st = raw_ring + s * G::RAW;
-                    mbar_expect_tx(&full[s], SELF ? XRAW : XRAW + YRAW);
+                    const uint32_t st = su32(raw_ring + s * G::RAW);
+                    mbar_expect_tx(&full[s], G::RAW);
 #pragma unroll
-                    for (int a = 0; a < TWIN / 32; ++a)
-                        tma_2d(su32(st) + a * (TKB * 128), xm, xcol + 32 * a, row0 + it * TKB, &full[s]);
+                    for (int a = 0; a < XF / 32; ++a) tma_2d(st + a * ATOM, xm, xcol + 32 * a, row0 + it * TKB, &full[s]);
                     if (!SELF)
 #pragma unroll
-                        for (int a = 0; a < TYW / 32; ++a)
-                            tma_2d(su32(st + XRAW) + a * (TKB * 128), ym, 2 * (int)r0 + 32 * a, row0 + it * TKB,
-                                   &full[s]);
+                        for (int a = 0; a < YF / 32; ++a)
+                            tma_2d(st + XRAW + a * ATOM, ym, 2 * (int)r0 + 32 * a, row0 + it * TKB, &full[s]);
                 }
             }
         } else {
@@ -237,28 +237,28 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 if (it >= G::NR) mbar_wait(&rawfree[s], ((it / G::NR) - 1) & 1);
                 uint8_t* st = raw_ring + s * G::RAW;
                 const int rows = min(TKB, nper - it * TKB);
-                if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)rows * (SELF ? 1024u : 1536u));
+                if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)rows * (SELF ? XF * 4 : (XF + YF) * 4));
                 __syncwarp();
                 const int64_t p = tile.p0 + (int64_t)it * TKB + k;
                 if (k < rows && lane < 16) {
                     const uint64_t xs = (uint64_t)(p * Pf + r0 + d) & mask;
-                    const uint32_t dx = su32(st + k * 1024);
+                    const uint32_t dx = su32(st + k * (XF * 4));
                     const uint64_t room = mask + 1 - xs;
-                    if (room >= 128) {
-                        bulk_g2s(dx, seg.x + xs, 1024, &full[s]);
+                    if (room >= XF / 2) {
+                        bulk_g2s(dx, seg.x + xs, XF * 4, &full[s]);
                     } else {
                         bulk_g2s(dx, seg.x + xs, (uint32_t)room * 8, &full[s]);
-                        bulk_g2s(dx + (uint32_t)room * 8, seg.x, (uint32_t)(128 - room) * 8, &full[s]);
+                        bulk_g2s(dx + (uint32_t)room * 8, seg.x, (uint32_t)(XF / 2 - room) * 8, &full[s]);
                     }
                 } else if (!SELF && k < rows) {
                     const uint64_t ys = (uint64_t)(p * Pf + r0) & mask;
-                    const uint32_t dy = su32(st + XRAW + k * 512);
+                    const uint32_t dy = su32(st + XRAW + k * (YF * 4));
                     const uint64_t yroom = mask + 1 - ys;
-                    if (yroom >= 64) {
-                        bulk_g2s(dy, seg.y + ys, 512, &full[s]);
+                    if (yroom >= YF / 2) {
+                        bulk_g2s(dy, seg.y + ys, YF * 4, &full[s]);
                     } else {
                         bulk_g2s(dy, seg.y + ys, (uint32_t)yroom * 8, &full[s]);
-                        bulk_g2s(dy + (uint32_t)yroom * 8, seg.y, (uint32_t)(64 - yroom) * 8, &full[s]);
+                        bulk_g2s(dy + (uint32_t)yroom * 8, seg.y, (uint32_t)(YF / 2 - yroom) * 8, &full[s]);
                     }
                 }
             }
@@ -270,13 +270,21 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 mbar_wait(&conv[s], (it / G::NP) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t xh = su32(plane_ring + s * G::PLANE), xl = xh + XPLANE;
-                const uint32_t yh = SELF ? xh + ya * (TKB * 128) : xl + XPLANE;
-                const uint32_t yl = SELF ? xl + ya * (TKB * 128) : yh + YPLANE;
-                const uint64_t dxh = sw128_desc(xh, TKB * 128, 1024), dxl = sw128_desc(xl, TKB * 128, 1024);
-                const uint64_t dyh = sw128_desc(yh, TKB * 128, 1024), dyl = sw128_desc(yl, TKB * 128, 1024);
-                mma_bf16(tmem, dyh, dxh, TC_IDESC, it ? 1u : 0u);
-                mma_bf16(tmem, dyh, dxl, TC_IDESC, 1u);
-                mma_bf16(tmem, dyl, dxh, TC_IDESC, 1u);
+                const uint32_t yh0 = SELF ? xh + ya * ATOM : xl + XPLANE;
+                const uint32_t yl0 = SELF ? xl + ya * ATOM : yh0 + YPLANE;
+                if (L.dbg != 2 && L.dbg != 3) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {  // residues 64h..64h+63: y atoms 2h.., x atoms 2h..2h+3
+                        const uint64_t dxh = sw128_desc(xh + 2 * h * ATOM, ATOM, 1024);
+                        const uint64_t dxl = sw128_desc(xl + 2 * h * ATOM, ATOM, 1024);
+                        const uint64_t dyh = sw128_desc(yh0 + 2 * h * ATOM, ATOM, 1024);
+                        const uint64_t dyl = sw128_desc(yl0 + 2 * h * ATOM, ATOM, 1024);
+                        const uint32_t dt = tmem + 256 * h;
+                        mma_bf16(dt, dyh, dxh, TC_IDESC, it ? 1u : 0u);
+                        mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
+                        mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
+                    }
+                }
                 mma_commit(&planefree[s]);
             }
             mma_commit(&done);
@@ -291,13 +299,16 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
             const uint32_t xh = su32(plane_ring + ps * G::PLANE);
             const uint32_t xl = xh + XPLANE;
+            if (L.dbg != 1 && L.dbg != 3) {
 #pragma unroll
-            for (int u = ct; u < 512; u += 32 * TNC) convert_unit(st, u, swz, 1024, xh, xl, rows);
-            if (!SELF) {
-                const uint32_t yh = xl + XPLANE;
-                const uint32_t yl = yh + YPLANE;
+                for (int u = ct; u < (XF / 32) * 64; u += 32 * TNC) convert_unit(st, u, swz, XF * 4, xh, xl, rows);
+                if (!SELF) {
+                    const uint32_t yh = xl + XPLANE;
+                    const uint32_t yl = yh + YPLANE;
 #pragma unroll
-                for (int u = ct; u < 256; u += 32 * TNC) convert_unit(st + XRAW, u, swz, 512, yh, yl, rows);
+                    for (int u = ct; u < (YF / 32) * 64; u += 32 * TNC)
+                        convert_unit(st + XRAW, u, swz, YF * 4, yh, yl, rows);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&rawfree[rs]);  // raw slot reusable (generic reads done)
@@ -305,19 +316,18 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[ps]);
         }
-        // epilogue: lane m = 2r + a of quarter q holds D[m][*]; the band is
-        // columns [2r, 2r + 128): float2 (c_{2a}, c_{2a+1}) per lag t
+        // epilogue: warps 2-5 read accumulator 0 (residues 0-63), warps 6-9
+        // accumulator 1 (64-127).  Lane m = 2r + a of quarter q holds D[m][*];
+        // the band is columns [2r, 2r + 128): float2 (c_{2a}, c_{2a+1}) per lag t
         mbar_wait(&done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const int q = warp & 3;
+        const int q = warp & 3, h = (warp - 2) >> 2;
         const int m = 32 * q + lane;
         const int r = m >> 1, a = m & 1;
-        float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)blockIdx.x * 64 * 64 * 2;
-        // columns [32c, 32c + 32), c = q .. q+4, cover the quarter's band; the
-        // TNC/4 warps of a quarter take every (TNC/4)-th chunk
-        for (int c = q + (warp - 2) / 4; c < q + 5; c += TNC / 4) {
+        float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)blockIdx.x * 64 * TRB * 2;
+        for (int c = q; c < q + 5; ++c) {  // columns [32c, 32c + 32) cover the quarter's band
             uint32_t v[32];
-            const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * c);
+            const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h + 32 * c);
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -332,25 +342,25 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             for (int j = 0; j < 16; ++j) {
                 const int t = 16 * c + j - r;  // lag offset of column pair 2(16c + j)
                 if (t >= 0 && t < 64)
-                    part[((size_t)t * 64 + r) * 2 + a] =
+                    part[((size_t)t * TRB + 64 * h + r) * 2 + a] =
                         make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// the fp64 reduce of fold.cu, instantiated for the tensor-core tile geometry
+// the fp64 reduce of fold.cu for the tensor-core tile geometry (64 lags x 128 residues)
 __global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcParams D) {
     if (L.gate && *L.gate != ~0ull) return;
     const FoldGroup g = D.groups[blockIdx.y];
     const int slot = D.segs[g.seg].slot;
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // lag * 64 + residue
-    if (e >= 64 * 64) return;
-    const int lag = e >> 6, res = e & 63;
-    const int64_t rg = (int64_t)g.rb * 64 + res;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // lag * TRB + residue
+    if (e >= 64 * TRB) return;
+    const int lag = e / TRB, res = e % TRB;
+    const int64_t rg = (int64_t)g.rb * TRB + res;
     const int tg = g.lb * 64 + lag;
     if (rg >= L.Pf || tg >= L.t_pad) return;
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
@@ -359,7 +369,7 @@ __global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcPa
     for (; t + 4 <= g.t1; t += 4) {  // 4 loads in flight, fixed summation order
         float4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(t + u) * 64 * 64);
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(t + u) * 64 * TRB);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             s0 += v[u].x;
@@ -369,7 +379,7 @@ __global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcPa
         }
     }
     for (; t < g.t1; ++t) {
-        const float4 v = __ldcs(part + (size_t)t * 64 * 64);
+        const float4 v = __ldcs(part + (size_t)t * 64 * TRB);
         s0 += v.x;
         s1 += v.y;
         s2 += v.z;
@@ -419,6 +429,7 @@ bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64
     D.p_base[si] = p_base;
     const float* xb = reinterpret_cast<const float*>(g.x + (p_base * Pf + lag_lo));
     const float* yb = reinterpret_cast<const float*>(g.y + p_base * Pf);
+    // widest x window: residues Pf-128.. at lag block nlb-1 -> floats up to 2 Pf + 128 nlb
     return encode_2d(&D.xmap[si], xb, 2ull * Pf + 128ull * nlb, (uint64_t)rows, 8ull * Pf) &&
            encode_2d(&D.ymap[si], yb, 2ull * Pf, (uint64_t)rows, 8ull * Pf);
 }
@@ -438,7 +449,7 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, bool self, cudaStrea
     else
         fold_tc_kernel<false><<<L.n_tiles, TNT, TcGeo<false>::SMEM, st>>>(L, D);
     if (ev1) cudaEventRecord(ev1, st);
-    fold_tc_reduce_kernel<<<dim3(64 * 64 / 256, L.n_groups), 256, 0, st>>>(L, D);
+    fold_tc_reduce_kernel<<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, D);
 }
 
 }  // namespace cyc

@@ -67,6 +67,7 @@ struct FoldLaunch {
     // non-null: the reduce commits only if *gate == ~0 (the chunk's finite scan,
     // stream-ordered before the fold, found nothing) -- a rejected chunk leaves S untouched
     const unsigned long long* gate;
+    int dbg;  // experiments only (tensor-core fold: 1 = skip conversion, 2 = skip MMAs)
 };
 
 // Launch descriptors carried in the kernel parameter block (<= 32 KB since
@@ -84,8 +85,8 @@ struct FoldInline {
 void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr,
                  const FoldInline* inl = nullptr);
 
-// Tensor-core fold (fold_tc.cu): tiles of 64 residues x 64 lags, descriptors
-// by value; partials [n_tiles][64 lags][64 residues] float4, reduced into S
+// Tensor-core fold (fold_tc.cu): tiles of 128 residues x 64 lags, descriptors
+// by value; partials [n_tiles][64 lags][128 residues] float4, reduced into S
 // (accumulate; gate honoured).  Linear segments (mask == ~0) are staged with
 // 2-D TMA through the per-segment tensor maps (rows = fold periods from
 // p_base, columns = floats from sample p_base*Pf + lag_lo; rows overlap so a
