@@ -815,6 +815,7 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
                 pb = gr.p1;
                 break;
             }
+        trace("tc plan");
         if (!encode_tc_maps(*tcp_, (int)i, g, pa, pb - pa, (int)Pf_, f_lo_, nlb))
             return Status{CYC_ERR_CUDA, "cuTensorMapEncodeTiled failed for the tensor-core fold", -1};
     }
@@ -875,10 +876,12 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         L.dbg = std::getenv("CYC_TC_DBG") ? std::atoi(std::getenv("CYC_TC_DBG")) : 0;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
-            launch_fold_tc(L, *tcp_, self, cs_, r.a, r.b);
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b);
             prof_pending_.push_back(r);
         } else {
-            launch_fold_tc(L, *tcp_, self, cs_);
+            trace("tc maps encoded");
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_);
+            trace("tc launched");
         }
         launches_ += 2;
         g0 += ng;
@@ -1644,9 +1647,11 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
                                              yv ? (const float2*)yv + (size_t)ch * n : nullptr, (int64_t)n, 0, C, ch,
                                              key_dev_, cs_);
         }
+        trace("scan enqueued");
         fold_gate_ = key_dev_;
         const Status st = fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_main_);
         fold_gate_ = nullptr;
+        trace("fold enqueued");
         TRY(st);
     } else {
         if (!S_pend_) CK(cudaMalloc(&S_pend_, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double)));
@@ -1999,8 +2004,17 @@ Status Engine::set_frames(uint64_t frames) {
 
 Status Engine::reset() {
     CK(cudaSetDevice(c_.device));
-    CK(cudaStreamSynchronize(xs_));
-    CK(cudaStreamSynchronize(cs_));
+    // Order both streams after everything already enqueued on either (ring
+    // readers / writers of the old stream) without blocking the host.
+    {
+        cudaEvent_t a = get_event(), b = get_event();
+        CK(cudaEventRecord(a, cs_));
+        CK(cudaEventRecord(b, xs_));
+        CK(cudaStreamWaitEvent(xs_, a, 0));
+        CK(cudaStreamWaitEvent(cs_, b, 0));
+        ev_pool_.push_back(a);
+        ev_pool_.push_back(b);
+    }
     const size_t lay_all = (size_t)c_.channels * nflags_ * layout_len_;
     if (S_main_) CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
     if (dsum_main_) CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
@@ -2015,7 +2029,6 @@ Status Engine::reset() {
     frames_ = 0;
     avg_cache_frames_ = ~0ull;
     avg_cache_channel_ = -1;
-    CK(cudaStreamSynchronize(cs_));
     return Status::ok();
 }
 

@@ -29,6 +29,7 @@
 // The tile's partials go through the same fixed-order fp64 reduce as fold.cu.
 #include <cuda_bf16.h>
 
+#include <cstring>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -162,8 +163,8 @@ __device__ __forceinline__ void convert_unit(uint32_t raw, int u, bool swz, uint
     split8(ra, rb, 4 * a + m, k, hi, lo, k >= rows);
 }
 
-template <bool SELF>
-__global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ TcParams D) {
+template <bool SELF, class DESC>
+__global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
     using G = TcGeo<SELF>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -352,11 +353,18 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+template <int MG>
+struct TcRed {
+    FoldGroup groups[MG];
+    int slot[MG];  // accumulator slot of each group's segment
+};
+
 // the fp64 reduce of fold.cu for the tensor-core tile geometry (64 lags x 128 residues)
-__global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcParams D) {
+template <int MG>
+__global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcRed<MG> R) {
     if (L.gate && *L.gate != ~0ull) return;
-    const FoldGroup g = D.groups[blockIdx.y];
-    const int slot = D.segs[g.seg].slot;
+    const FoldGroup g = R.groups[blockIdx.y];
+    const int slot = R.slot[blockIdx.y];
     const int e = blockIdx.x * blockDim.x + threadIdx.x;  // lag * TRB + residue
     if (e >= 64 * TRB) return;
     const int lag = e / TRB, res = e % TRB;
@@ -434,22 +442,57 @@ bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64
            encode_2d(&D.ymap[si], yb, 2ull * Pf, (uint64_t)rows, 8ull * Pf);
 }
 
-void launch_fold_tc(const FoldLaunch& L, const TcParams& D, bool self, cudaStream_t st, cudaEvent_t ev0,
-                    cudaEvent_t ev1) {
-    if (L.n_tiles == 0) return;
+namespace {
+using TcSmall = TcDesc<160, 16, 2>;  // one or two segments, one wave of tiles
+
+template <class DESC, int MG>
+void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self, cudaStream_t st, cudaEvent_t ev0,
+               cudaEvent_t ev1) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(fold_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcGeo<true>::SMEM);
-        cudaFuncSetAttribute(fold_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcGeo<false>::SMEM);
+        cudaFuncSetAttribute(fold_tc_kernel<true, DESC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             TcGeo<true>::SMEM);
+        cudaFuncSetAttribute(fold_tc_kernel<false, DESC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             TcGeo<false>::SMEM);
         attr = true;
     }
     if (ev0) cudaEventRecord(ev0, st);
     if (self)
-        fold_tc_kernel<true><<<L.n_tiles, TNT, TcGeo<true>::SMEM, st>>>(L, D);
+        fold_tc_kernel<true, DESC><<<L.n_tiles, TNT, TcGeo<true>::SMEM, st>>>(L, D);
     else
-        fold_tc_kernel<false><<<L.n_tiles, TNT, TcGeo<false>::SMEM, st>>>(L, D);
+        fold_tc_kernel<false, DESC><<<L.n_tiles, TNT, TcGeo<false>::SMEM, st>>>(L, D);
     if (ev1) cudaEventRecord(ev1, st);
-    fold_tc_reduce_kernel<<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, D);
+    fold_tc_reduce_kernel<MG><<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+}
+
+template <int MG>
+void fill_red(TcRed<MG>& R, const TcParams& D, int ng) {
+    for (int g = 0; g < ng; ++g) {
+        R.groups[g] = D.groups[g];
+        R.slot[g] = D.segs[D.groups[g].seg].slot;
+    }
+}
+}  // namespace
+
+void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool self, cudaStream_t st, cudaEvent_t ev0,
+                    cudaEvent_t ev1) {
+    if (L.n_tiles == 0) return;
+    if (L.n_tiles <= 160 && L.n_groups <= 16 && n_segs <= 2) {
+        thread_local TcSmall S;  // host staging (the launch copies it)
+        thread_local TcRed<16> R;
+        std::memcpy(S.xmap, D.xmap, n_segs * sizeof(CUtensorMap));
+        std::memcpy(S.ymap, D.ymap, n_segs * sizeof(CUtensorMap));
+        std::memcpy(S.p_base, D.p_base, n_segs * sizeof(int64_t));
+        std::memcpy(S.segs, D.segs, n_segs * sizeof(FoldSeg));
+        std::memcpy(S.tiles, D.tiles, L.n_tiles * sizeof(FoldTile));
+        std::memcpy(S.groups, D.groups, L.n_groups * sizeof(FoldGroup));
+        fill_red(R, D, L.n_groups);
+        launch_tc(L, S, R, self, st, ev0, ev1);
+    } else {
+        thread_local TcRed<FI_GROUPS> R;
+        fill_red(R, D, L.n_groups);
+        launch_tc(L, D, R, self, st, ev0, ev1);
+    }
 }
 
 }  // namespace cyc

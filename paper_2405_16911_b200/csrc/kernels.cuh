@@ -92,19 +92,25 @@ void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr
 // p_base, columns = floats from sample p_base*Pf + lag_lo; rows overlap so a
 // window may run past its period); ring segments with per-period 1-D bulk
 // copies split at the wrap.
+// Kernel parameters are copied into every launch at their declared size, and
+// a large block costs host time (measured: ~36 us for two 22 KB launches), so
+// the device descriptor comes in capacity classes; TcParams is the host-side
+// master that launch_fold_tc packs into the smallest class that fits.
 constexpr int TC_SEGS = 16;
-struct alignas(64) TcParams {
-    CUtensorMap xmap[TC_SEGS];  // box 32 floats x 16 periods, 128B swizzle (8 boxes per window)
-    CUtensorMap ymap[TC_SEGS];  // same boxes over y (non-self launches: 4 per window)
-    int64_t p_base[TC_SEGS];    // first period (row 0) of each segment's maps
-    FoldSeg segs[TC_SEGS];
-    FoldTile tiles[FI_TILES];
-    FoldGroup groups[FI_GROUPS];
+template <int MT, int MG, int MS>
+struct alignas(64) TcDesc {
+    CUtensorMap xmap[MS];  // box 32 floats x 16 periods, 128B swizzle (12 boxes per window)
+    CUtensorMap ymap[MS];  // same boxes over y (non-self launches: 8 per window)
+    int64_t p_base[MS];    // first period (row 0) of each segment's maps
+    FoldSeg segs[MS];
+    FoldTile tiles[MT];
+    FoldGroup groups[MG];
 };
+using TcParams = TcDesc<FI_TILES, FI_GROUPS, TC_SEGS>;
 // self: every tile's y window lies inside its x window at a 32-sample
 // boundary (x == y, d = lag_lo + 64 lb in [-64, 0], d % 32 == 0).
-void launch_fold_tc(const FoldLaunch& L, const TcParams& D, bool self, cudaStream_t st, cudaEvent_t ev0 = nullptr,
-                    cudaEvent_t ev1 = nullptr);
+void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool self, cudaStream_t st,
+                    cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 // Fill D.xmap/ymap/p_base[si] for a linear segment (false: no TMA -- use the ring path).
 bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64_t rows, int Pf, int lag_lo,
                     int nlb);
