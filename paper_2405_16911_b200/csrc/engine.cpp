@@ -484,6 +484,7 @@ Status Engine::init(const Cfg& cfg) {
     }
     CK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&vs_, cudaStreamNonBlocking));
     // ring: pieces of Q samples per channel, four pieces per ring
     int64_t qmin = std::max<int64_t>(next_pow2((int64_t)need_ + N_), 1 << 12);
     int64_t qdef = std::max<int64_t>((1 << 21) / next_pow2(c_.channels), 1 << 12);
@@ -593,6 +594,7 @@ Engine::~Engine() {
     for (auto e : ev_pool_) cudaEventDestroy(e);
     if (cs_) cudaStreamDestroy(cs_);
     if (xs_) cudaStreamDestroy(xs_);
+    if (vs_) cudaStreamDestroy(vs_);
 }
 
 Status Engine::ensure_ring(int64_t cap_min) {
@@ -876,11 +878,11 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         L.dbg = std::getenv("CYC_TC_DBG") ? std::atoi(std::getenv("CYC_TC_DBG")) : 0;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
-            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b);
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b, reduce_wait_ev_);
             prof_pending_.push_back(r);
         } else {
             trace("tc maps encoded");
-            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_);
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, nullptr, nullptr, reduce_wait_ev_);
             trace("tc launched");
         }
         launches_ += 2;
@@ -983,10 +985,10 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
         const FoldInline* di = inl ? inline_.get() : nullptr;
         if (prof_) {
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
-            launch_fold(L, cs_, r.a, r.b, di);
+            launch_fold(L, cs_, r.a, r.b, di, reduce_wait_ev_);
             prof_pending_.push_back(r);
         } else {
-            launch_fold(L, cs_, nullptr, nullptr, di);
+            launch_fold(L, cs_, nullptr, nullptr, di, reduce_wait_ev_);
         }
         launches_ += 2;
         g0 = g;
@@ -1637,20 +1639,28 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
     CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
     const bool gated = kind == IN_DEVICE_F32;
     if (gated) {
-        // The whole chunk is scanned before any fold is enqueued (same stream),
-        // so the fold's reduce commits straight into S_main behind the scan's
-        // verdict: no pending accumulator, no commit pass.  (A scan on the 4
-        // SMs a one-wave fold leaves idle, on a side stream, was measured
-        // slower: 4 SMs cannot stream 134 MB within the fold.)
+        // The fold's reduces commit straight into S_main behind the scan's
+        // verdict (no pending accumulator, no commit pass).  The scan runs on a
+        // side stream, co-resident with the fold kernels (HBM-bound beside an
+        // L2/tensor-bound fold); only the reduces wait for it.
+        cudaEvent_t ev_k = get_event(), ev_c = get_event();
+        CK(cudaEventRecord(ev_k, cs_));
+        CK(cudaStreamWaitEvent(vs_, ev_k, 0));
         for (int ch = 0; ch < C; ++ch) {
             launches_ += launch_finite_check((const float2*)xv + (size_t)ch * n,
                                              yv ? (const float2*)yv + (size_t)ch * n : nullptr, (int64_t)n, 0, C, ch,
-                                             key_dev_, cs_);
+                                             key_dev_, vs_);
         }
+        CK(cudaEventRecord(ev_c, vs_));
         trace("scan enqueued");
         fold_gate_ = key_dev_;
+        reduce_wait_ev_ = ev_c;
         const Status st = fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_main_);
         fold_gate_ = nullptr;
+        reduce_wait_ev_ = nullptr;
+        CK(cudaStreamWaitEvent(cs_, ev_c, 0));  // the key read below (and pushes that fold nothing)
+        ev_pool_.push_back(ev_k);
+        ev_pool_.push_back(ev_c);
         trace("fold enqueued");
         TRY(st);
     } else {

@@ -186,6 +186,8 @@ private:
 
     // ---- device resources ----
     cudaStream_t cs_ = nullptr, xs_ = nullptr;
+    cudaStream_t vs_ = nullptr;             // side stream: a device chunk's finite scan beside its fold
+    cudaEvent_t reduce_wait_ev_ = nullptr;  // fold reduces wait for it (the side scan)
     float2* ring_x_ = nullptr;
     float2* ring_y_ = nullptr;  // null => auto-correlation (y = x)
     bool cross_ = false;

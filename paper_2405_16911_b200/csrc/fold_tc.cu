@@ -447,7 +447,7 @@ using TcSmall = TcDesc<160, 16, 2>;  // one or two segments, one wave of tiles
 
 template <class DESC, int MG>
 void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self, cudaStream_t st, cudaEvent_t ev0,
-               cudaEvent_t ev1) {
+               cudaEvent_t ev1, cudaEvent_t before_reduce) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fold_tc_kernel<true, DESC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -462,6 +462,7 @@ void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self
     else
         fold_tc_kernel<false, DESC><<<L.n_tiles, TNT, TcGeo<false>::SMEM, st>>>(L, D);
     if (ev1) cudaEventRecord(ev1, st);
+    if (before_reduce) cudaStreamWaitEvent(st, before_reduce, 0);
     fold_tc_reduce_kernel<MG><<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
 }
 
@@ -475,7 +476,7 @@ void fill_red(TcRed<MG>& R, const TcParams& D, int ng) {
 }  // namespace
 
 void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool self, cudaStream_t st, cudaEvent_t ev0,
-                    cudaEvent_t ev1) {
+                    cudaEvent_t ev1, cudaEvent_t before_reduce) {
     if (L.n_tiles == 0) return;
     if (L.n_tiles <= 160 && L.n_groups <= 16 && n_segs <= 2) {
         thread_local TcSmall S;  // host staging (the launch copies it)
@@ -487,11 +488,11 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool sel
         std::memcpy(S.tiles, D.tiles, L.n_tiles * sizeof(FoldTile));
         std::memcpy(S.groups, D.groups, L.n_groups * sizeof(FoldGroup));
         fill_red(R, D, L.n_groups);
-        launch_tc(L, S, R, self, st, ev0, ev1);
+        launch_tc(L, S, R, self, st, ev0, ev1, before_reduce);
     } else {
         thread_local TcRed<FI_GROUPS> R;
         fill_red(R, D, L.n_groups);
-        launch_tc(L, D, R, self, st, ev0, ev1);
+        launch_tc(L, D, R, self, st, ev0, ev1, before_reduce);
     }
 }
 

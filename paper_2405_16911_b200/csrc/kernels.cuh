@@ -83,7 +83,7 @@ struct FoldInline {
 // fold + fp64 reduce; optional events bracket the fold kernel alone (profiling).
 // inl != nullptr: descriptors by value (L.segs/tiles/groups are ignored).
 void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr,
-                 const FoldInline* inl = nullptr);
+                 const FoldInline* inl = nullptr, cudaEvent_t before_reduce = nullptr);
 
 // Tensor-core fold (fold_tc.cu): tiles of 128 residues x 64 lags, descriptors
 // by value; partials [n_tiles][64 lags][128 residues] float4, reduced into S
@@ -109,8 +109,9 @@ struct alignas(64) TcDesc {
 using TcParams = TcDesc<FI_TILES, FI_GROUPS, TC_SEGS>;
 // self: every tile's y window lies inside its x window at a 32-sample
 // boundary (x == y, d = lag_lo + 64 lb in [-64, 0], d % 32 == 0).
+// before_reduce: the reduce (not the fold) waits for this event (a gate scan on another stream).
 void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool self, cudaStream_t st,
-                    cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+                    cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr, cudaEvent_t before_reduce = nullptr);
 // Fill D.xmap/ymap/p_base[si] for a linear segment (false: no TMA -- use the ring path).
 bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64_t rows, int Pf, int lag_lo,
                     int nlb);
