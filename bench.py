@@ -18,9 +18,11 @@ tables.  Two measurements per run:
             call (cyc_push), H2D DMA and the D2H of both tables inside the
             timed region.
 metric = direct-sum-equivalent (alpha, tau) updates/s = A*T*L_eff*flags / t
-(SURVEY §8d); the executed algorithm is the exact residue fold (4 FP32 FMAs
-per (lag, sample) for both flags) + fp64 FFT, so the roofline line reports
-the fold kernel's executed FP32 rate against the device's FFMA peak.
+(SURVEY §8d); the executed algorithm is the exact residue fold + fp64 FFT.
+The fold runs on the tensor cores (tcgen05, bf16x3 split of the fp32 samples,
+banded Gram product; FP32 FFMA2 kernel for partial periods), so the roofline
+line reports the fold's algorithmic rate (8 flops per lag x sample) against the
+measured bf16 tensor peak, with the executed MMA rate beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
@@ -62,7 +64,7 @@ def config_block(n_gpus: int):
             "samples_per_gpu": L_REC, "alphas": A, "lags": LAGS, "flags": ["conv", "conj"],
             "win_len": N_WIN, "l_eff": l_eff(L_REC), "parallelism": f"independent records x{n_gpus}",
             "l2": "input 134 MB > 126 MB L2 (no reuse across steps)",
-            "algorithm": "exact residue fold (FFMA2) + fp64 radix-2 FFT"}
+            "algorithm": "exact residue fold on tcgen05 (bf16x3 banded Gram product; FFMA2 for partial periods) + fp64 radix-2 FFT"}
 
 
 # ---------------------------------------------------------------------------
@@ -147,14 +149,62 @@ def barrier(ws: int):
         dist.barrier()
 
 
-def traffic_from_profiles():
-    p = os.path.join(ROOT, "profiles", "fold_ncu_summary.json")
+DTYPE = "cf32 in; fold: bf16x3 split on tcgen05 (~fp32 products), fp32 TMEM accumulation; fp64 reductions/FFT"
+
+
+def traffic_from_profiles(tensor: bool):
+    name = "foldtc_ncu_summary.json" if tensor else "fold_ncu_summary.json"
+    p = os.path.join(ROOT, "profiles", name)
     try:
         with open(p) as f:
             d = json.load(f)
         return d.get("dram_bytes_per_launch"), d.get("source")
     except Exception:
         return None, None
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int) -> dict:
+    """The dominant kernel (the fold) from CUDA-event profiles on its stream.
+    achieved = ALGORITHMIC flops (8 per requested lag x folded sample: 4 FMAs
+    give both flags) / launch duration.  Tensor-core folds also report the
+    executed MMA rate (bf16x3 split x banded 128x256 product = ~6x algorithmic)."""
+    n = max(1, p1["launches"] - p0["launches"])
+    ms = (p1["ms"] - p0["ms"]) / n
+    alg = (p1["flops"] - p0["flops"]) / n
+    exe = (p1["exec_flops"] - p0["exec_flops"]) / n
+    tc = p1["tensor_launches"] - p0["tensor_launches"]
+    rate = alg / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    import paper_2405_16911_b200 as cyc
+    fp32 = cyc.measure_fp32_peak(dev)
+    traffic, tsrc = traffic_from_profiles(tc > 0)
+    common = {"unit": "TFLOP/s", "traffic": traffic, "traffic_source": tsrc, "algorithmic_flops_per_launch": alg,
+              "ms_per_launch": ms, "launches_per_step": (p1["launches"] - p0["launches"]) / steps,
+              "fold_share_of_step": (p1["ms"] - p0["ms"]) / steps / ms_step,
+              "algorithmic_unit": "8 flops per (requested lag, folded sample): 4 FMAs give both flags"}
+    if tc > 0:
+        mp = measured_peaks()
+        peak = mp["bf16_tflops"] if mp and mp.get("bf16_tflops") else 1590.0
+        ex_rate = exe / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+        return {"bound": "tensor", "kernel": "fold_tc_kernel (tcgen05 bf16x3 banded Gram product)",
+                "achieved": rate, "peak": peak, "frac": rate / peak, **common,
+                "executed_tflops": ex_rate, "executed_frac": ex_rate / peak,
+                "executed_per_algorithmic": exe / alg if alg else None,
+                "fp32_ffma_peak_tflops": fp32, "algorithmic_vs_fp32_peak": rate / fp32 if fp32 else None,
+                "tensor_launches_share": tc / n,
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 burst, this pool)" if mp
+                                else "fallback 1.59 PFLOP/s (B200_PROFILING.md)")}
+    return {"bound": "fp32", "kernel": "fold_kernel (FFMA2 residue fold)", "achieved": rate, "peak": fp32,
+            "frac": rate / fp32 if fp32 else None, **common,
+            "peak_source": "measured live: FFMA microbenchmark in libcycb200 (MEASURED_PEAKS.json carries no "
+                           "FP32 figure)"}
 
 
 # ---------------------------------------------------------------------------
@@ -289,12 +339,12 @@ def run_ours(args, ws, rank, local):
         step_e2e()
     # device-resident (value)
     est.profile(True)
-    n0, ms0, fl0 = est.profile_read()
+    prof0 = est.profile_read_ex()
     launches0 = est.kernel_launches()
     clk = Clocks(dev)
     ms_dev = timed(step_device, args.steps)
     clocks = clk.stop()
-    n1, ms1, fl1 = est.profile_read()
+    prof1 = est.profile_read_ex()
     launches = est.kernel_launches() - launches0
     est.profile(False)
     # e2e through the host C-ABI call
@@ -302,11 +352,7 @@ def run_ours(args, ws, rank, local):
 
     ms_dev_max = allreduce_max(ms_dev, ws)
     ms_e2e_max = allreduce_max(ms_e2e, ws)
-    fold_ms = (ms1 - ms0) / max(1, n1 - n0)
-    fold_flops = (fl1 - fl0) / max(1, n1 - n0)
-    fold_tflops = fold_flops / (fold_ms * 1e-3) / 1e12 if fold_ms > 0 else 0.0
-    peak = cyc.measure_fp32_peak(dev)
-    traffic, tsrc = traffic_from_profiles()
+    roof = roofline_block(prof0, prof1, args.steps, ms_dev_max, dev)
     if rank != 0:
         return
     records = 1 if strong else ws
@@ -317,7 +363,7 @@ def run_ours(args, ws, rank, local):
     line = {
         "metric": METRIC, "value": ups / (ms_dev_max * 1e-3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev_max, "higher_is_better": True,
-        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32 (fp64 reductions)",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic",
         "config": cfgb,
         "msamples_per_s": L_REC * records / (ms_dev_max * 1e-3) / 1e6,
@@ -325,16 +371,7 @@ def run_ours(args, ws, rank, local):
                 "h2d_bytes_per_step": n_local * 8, "d2h_bytes_per_step": 2 * A * LAGS * 16,
                 "msamples_per_s": L_REC * records / (ms_e2e_max * 1e-3) / 1e6,
                 "path": "cyc_push(pinned host cf32) + cyc_average_all (both tables, one D2H into pinned host)"},
-        "roofline": {"bound": "fp32", "kernel": "fold_kernel", "achieved": fold_tflops, "peak": peak,
-                     "unit": "TFLOP/s", "frac": fold_tflops / peak if peak else None,
-                     "traffic": traffic, "traffic_source": tsrc,
-                     "algorithmic_flops_per_launch": fold_flops, "ms_per_launch": fold_ms,
-                     "launches_per_step": (n1 - n0) / args.steps,
-                     "fold_share_of_step": (ms1 - ms0) / args.steps / ms_dev_max,
-                     "peak_source": "measured live: FFMA microbenchmark in libcycb200 "
-                                    "(MEASURED_PEAKS.json carries no FP32 figure)",
-                     "algorithmic_unit": "8 FP32 flops per (requested lag, folded sample): 4 FMAs give "
-                                         "both flags"},
+        "roofline": roof,
         "gpu_launches": launches,
         "clocks": clocks,
     }
@@ -539,23 +576,21 @@ def run_config(args, ws, rank, local):
         if step_dev:
             step_e2e()
     est.profile(True)
-    n0, ms0, fl0 = est.profile_read()
+    prof0 = est.profile_read_ex()
     l0 = sum(e.kernel_launches() for e in ests)
     clk = Clocks(dev)
     ms_dev = timed(step_dev, args.steps) if step_dev else None
     ms_e2e = timed(step_e2e, args.steps) if not step_dev else None
     clocks = clk.stop()
-    n1, ms1, fl1 = est.profile_read()
+    prof1 = est.profile_read_ex()
     launches = sum(e.kernel_launches() for e in ests) - l0
     if step_dev:
         ms_e2e = timed(step_e2e, args.steps)
-    fold_ms = (ms1 - ms0) / max(1, n1 - n0)
-    fold_tf = (fl1 - fl0) / max(1, n1 - n0) / (fold_ms * 1e-3) / 1e12 if fold_ms > 0 else 0.0
-    peak = cyc.measure_fp32_peak(dev)
     ms_val = ms_dev if ms_dev is not None else ms_e2e
+    roof = roofline_block(prof0, prof1, args.steps, ms_val, dev)
     line = {"metric": METRIC, "value": spec["updates"] / (ms_val * 1e-3), "unit": UNIT, "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_val, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 reductions)", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
             "config": {"workload": spec["workload"], "algorithm": est.algorithm(),
                        "value_path": "device-resident input" if step_dev else
                        "host pushes of the stated chunk size (the workload is the streaming call pattern)"},
@@ -563,9 +598,7 @@ def run_config(args, ws, rank, local):
             "e2e": {"value": spec["updates"] / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": int(x.size) * 8,
                     "d2h_bytes_per_step": int(lay * 16 * (2 * est.config().channels if step_dev else len(ests)))},
-            "roofline": {"bound": "fp32", "kernel": "fold_kernel", "achieved": fold_tf, "peak": peak,
-                         "unit": "TFLOP/s", "frac": fold_tf / peak if peak else None, "traffic": None,
-                         "ms_per_launch": fold_ms, "launches_per_step": (n1 - n0) / args.steps},
+            "roofline": roof,
             "gpu_launches": launches, "clocks": clocks}
     if cxx is not None:
         # headline for the small-call configs: the C++ caller through the C-ABI

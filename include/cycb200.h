@@ -208,6 +208,11 @@ int cyc_reset(cyc_est* est);
  * (8 per requested lag per folded sample, both flags). */
 int cyc_profile_enable(cyc_est* est, int on);
 int cyc_profile_read(cyc_est* est, uint64_t* launches, double* ms, double* flops);
+/* Same, plus the executed flops (tensor-core launches: the MMA flops of the
+ * bf16x3 banded product; FP32 launches: = algorithmic) and how many of the
+ * launches ran on the tensor cores. */
+int cyc_profile_read_ex(cyc_est* est, uint64_t* launches, double* ms, double* flops, double* exec_flops,
+                        uint64_t* tensor_launches);
 /* FP32 FFMA throughput of `device`, TFLOP/s (roofline denominator). */
 double cyc_measure_fp32_peak(int device);
 /* The handle's compute stream (cudaStream_t as void*), for event timing. */

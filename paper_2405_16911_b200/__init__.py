@@ -158,6 +158,8 @@ def lib() -> C.CDLL:
     L.cyc_reset.argtypes = [vp]
     L.cyc_profile_enable.argtypes = [vp, C.c_int]
     L.cyc_profile_read.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.cyc_profile_read_ex.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
     L.cyc_measure_fp32_peak.argtypes = [C.c_int]
     L.cyc_measure_fp32_peak.restype = C.c_double
     L.cyc_compute_full_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_uint64, vp, C.c_char_p, sz]
@@ -468,6 +470,14 @@ class CyclicCorrelator:
         n, ms, fl = C.c_uint64(), C.c_double(), C.c_double()
         self._check(self._L.cyc_profile_read(self._h, C.byref(n), C.byref(ms), C.byref(fl)))
         return int(n.value), float(ms.value), float(fl.value)
+
+    def profile_read_ex(self) -> dict:
+        """profile_read plus executed flops and the tensor-core launch count."""
+        n, ms, fl, ex, tc = C.c_uint64(), C.c_double(), C.c_double(), C.c_double(), C.c_uint64()
+        self._check(self._L.cyc_profile_read_ex(self._h, C.byref(n), C.byref(ms), C.byref(fl), C.byref(ex),
+                                                C.byref(tc)))
+        return {"launches": int(n.value), "ms": float(ms.value), "flops": float(fl.value),
+                "exec_flops": float(ex.value), "tensor_launches": int(tc.value)}
 
     def _on_frame(self, user, view):
         v = view.contents

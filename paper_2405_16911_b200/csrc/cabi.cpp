@@ -237,6 +237,12 @@ int cyc_profile_read(cyc_est* est, uint64_t* launches, double* ms, double* flops
     return finish(est, est->e->profile_read(launches, ms, flops));
 }
 
+int cyc_profile_read_ex(cyc_est* est, uint64_t* launches, double* ms, double* flops, double* exec_flops,
+                        uint64_t* tensor_launches) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->profile_read(launches, ms, flops, exec_flops, tensor_launches));
+}
+
 double cyc_measure_fp32_peak(int device) { return cyc::measure_fp32_peak_tflops(device); }
 
 }  // extern "C"

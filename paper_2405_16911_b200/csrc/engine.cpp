@@ -877,7 +877,11 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         L.gate = fold_gate_;
         L.dbg = std::getenv("CYC_TC_DBG") ? std::atoi(std::getenv("CYC_TC_DBG")) : 0;
         if (prof_) {
-            ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
+            // executed: 2 accumulators x 3 MMAs (M=128, N=256, K=16) per 16-period stage
+            double exec = 0.0;
+            for (int t = 0; t < nt; ++t)
+                exec += (double)ceil_div(tcp_->tiles[t].p1 - tcp_->tiles[t].p0, 16) * 6.0 * 2.0 * 128 * 256 * 16;
+            ProfRec r{get_event_timed(), get_event_timed(), launch_flops, exec, true};
             launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b, reduce_wait_ev_);
             prof_pending_.push_back(r);
         } else {
@@ -984,7 +988,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
         L.gate = fold_gate_;
         const FoldInline* di = inl ? inline_.get() : nullptr;
         if (prof_) {
-            ProfRec r{get_event_timed(), get_event_timed(), launch_flops};
+            ProfRec r{get_event_timed(), get_event_timed(), launch_flops, launch_flops, false};
             launch_fold(L, cs_, r.a, r.b, di, reduce_wait_ev_);
             prof_pending_.push_back(r);
         } else {
@@ -1974,13 +1978,16 @@ cudaEvent_t Engine::get_event_timed() {
     return e;
 }
 
-Status Engine::profile_read(uint64_t* launches, double* ms, double* flops) {
+Status Engine::profile_read(uint64_t* launches, double* ms, double* flops, double* exec_flops,
+                            uint64_t* tensor_launches) {
     CK(cudaStreamSynchronize(cs_));
     for (auto& r : prof_pending_) {
         float t = 0.f;
         CK(cudaEventElapsedTime(&t, r.a, r.b));
         prof_ms_ += t;
         prof_flops_ += r.flops;
+        prof_exec_flops_ += r.exec_flops;
+        prof_tc_launches_ += r.tensor ? 1 : 0;
         ++prof_launches_;
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -1989,6 +1996,8 @@ Status Engine::profile_read(uint64_t* launches, double* ms, double* flops) {
     if (launches) *launches = prof_launches_;
     if (ms) *ms = prof_ms_;
     if (flops) *flops = prof_flops_;
+    if (exec_flops) *exec_flops = prof_exec_flops_;
+    if (tensor_launches) *tensor_launches = prof_tc_launches_;
     return Status::ok();
 }
 

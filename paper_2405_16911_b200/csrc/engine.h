@@ -80,7 +80,8 @@ public:
     Status set_frames(uint64_t frames);
     // Fold-kernel timing with CUDA events on the compute stream.
     void set_profiling(bool on) { prof_ = on; }
-    Status profile_read(uint64_t* launches, double* ms, double* flops);
+    Status profile_read(uint64_t* launches, double* ms, double* flops, double* exec_flops = nullptr,
+                        uint64_t* tensor_launches = nullptr);
 
     size_t buffer_need() const { return need_; }
     uint64_t consumed() const { return consumed_; }
@@ -252,12 +253,14 @@ private:
     // ---- profiling ----
     struct ProfRec {
         cudaEvent_t a, b;
-        double flops;
+        double flops;       // algorithmic: 8 per (requested lag, folded sample)
+        double exec_flops;  // executed: tensor-core MMA flops (bf16x3 banded product), else = flops
+        bool tensor;
     };
     bool prof_ = false;
     std::vector<ProfRec> prof_pending_;
-    uint64_t prof_launches_ = 0;
-    double prof_ms_ = 0.0, prof_flops_ = 0.0;
+    uint64_t prof_launches_ = 0, prof_tc_launches_ = 0;
+    double prof_ms_ = 0.0, prof_flops_ = 0.0, prof_exec_flops_ = 0.0;
 
     // speculative block pushes: pending fold + history backup for roll-back
     double* S_pend_ = nullptr;
