@@ -772,7 +772,8 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         int seg, rb, lb;
         int64_t p0, p1;
     };
-    const int nrb = (int)(Pf_ / 128), nlb = t_pad_ / 64;  // tiles: 128 residues x 64 lags
+    // tiles: 128 residues x 64 lags (t_pad < 64: the block's extra lags are computed and dropped)
+    const int nrb = (int)(Pf_ / 128), nlb = (t_pad_ + 63) / 64;
     std::vector<G> groups;
     std::vector<FoldSeg> tsegs;
     int64_t work = 0;
@@ -799,10 +800,25 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         work += (pb - pa) * nrb * nlb;
     }
     if (groups.empty()) return Status::ok();
-    if (tsegs.size() > (size_t)TC_SEGS) {  // descriptor block too small: FP32 path
-        rest.insert(rest.end(), tsegs.begin(), tsegs.end());
-        return Status::ok();
+    (void)work;
+    // launches take at most TC_SEGS segments (tensor maps per segment): batch them
+    for (size_t b0 = 0; b0 < tsegs.size(); b0 += TC_SEGS) {
+        const size_t b1 = std::min(tsegs.size(), b0 + (size_t)TC_SEGS);
+        std::vector<FoldSeg> bsegs(tsegs.begin() + b0, tsegs.begin() + b1);
+        std::vector<TcGroupPlan> bgroups;
+        for (const G& gr : groups)
+            if (gr.seg >= (int)b0 && gr.seg < (int)b1)
+                bgroups.push_back({gr.seg - (int)b0, gr.rb, gr.lb, gr.p0, gr.p1});
+        TRY(fold_tc_batch(bsegs, bgroups, S, nlb));
     }
+    return Status::ok();
+}
+
+Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S,
+                             int nlb) {
+    using G = TcGroupPlan;
+    static const bool dry = std::getenv("CYC_TC_DRYRUN") != nullptr;  // diagnostics: plan, do not launch
+    if (dry) return Status::ok();
     if (!tcp_) tcp_.reset(new TcParams);
     std::memset(tcp_.get(), 0, sizeof(TcParams));
     std::memcpy(tcp_->segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
@@ -902,13 +918,17 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
     };
     static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;  // A/B knob: FP32 fold only
     std::vector<FoldSeg> segs_tc_rest;
-    const bool tc = !no_tc && !overwrite && lw_ == 8 && Pf_ % 128 == 0 && t_pad_ % 64 == 0 && tc_capable_;
+    // tensor cores from 32 lags up (a 64-lag tile block; below that the FP32
+    // kernel's finer lag blocks win)
+    const bool tc = !no_tc && !overwrite && t_pad_ >= 32 && Pf_ % 128 == 0 && tc_capable_;
     if (tc) {
         std::vector<FoldSeg> sg(segs_in);
         for (auto& g : sg)
             g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
         TRY(fold_tc(sg, S, segs_tc_rest));
     }
+    static const bool skip_rest = std::getenv("CYC_TC_SKIP_REST") != nullptr;  // diagnostics
+    if (tc && skip_rest) segs_tc_rest.clear();
     const std::vector<FoldSeg>& segs = tc ? segs_tc_rest : segs_in;
     std::vector<G> groups;
     int64_t work = 0;
@@ -923,6 +943,16 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
             }
     }
     if (groups.empty()) return Status::ok();
+    // Segments sharing an accumulator slot (the head and tail periods left by the
+    // tensor-core fold) must reduce in ONE group: two groups of one launch
+    // updating the same S cells would race.  Order by (slot, rb, lb) and merge.
+    std::stable_sort(groups.begin(), groups.end(), [&](const G& a, const G& b) {
+        const int sa = segs[a.seg].slot, sb = segs[b.seg].slot;
+        return sa != sb ? sa < sb : (a.rb != b.rb ? a.rb < b.rb : a.lb < b.lb);
+    });
+    auto same_key = [&](const G& a, const G& b) {
+        return segs[a.seg].slot == segs[b.seg].slot && a.rb == b.rb && a.lb == b.lb;
+    };
     // split long groups into whole waves of 1 CTA/SM: each group gets a share of
     // `target` tiles proportional to its periods (floor), so no partial wave
     static const int waves = std::getenv("CYC_FOLD_WAVES") ? std::atoi(std::getenv("CYC_FOLD_WAVES")) : 1;
@@ -939,13 +969,13 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
             const int64_t share = (int64_t)((double)target * (double)np / (double)work);
             const int sp = (int)std::max<int64_t>(1, std::min<int64_t>({share, np / 4 + 1, 4096}));
             if (!tiles.empty() && tiles.size() + sp > MAX_TILES) break;
-            FoldGroup G2{gr.seg, gr.rb, gr.lb, (int)tiles.size(), 0, 0};
+            const bool merge = g > g0 && same_key(groups[g - 1], gr);
+            if (!merge) fg.push_back(FoldGroup{gr.seg, gr.rb, gr.lb, (int)tiles.size(), 0, 0});
             for (int i = 0; i < sp; ++i) {
                 const int64_t a = gr.p0 + np * i / sp, b = gr.p0 + np * (i + 1) / sp;
-                if (b > a) tiles.push_back({gr.seg, gr.rb, gr.lb, (int)fg.size(), a, b});
+                if (b > a) tiles.push_back({gr.seg, gr.rb, gr.lb, (int)fg.size() - 1, a, b});
             }
-            G2.t1 = (int)tiles.size();
-            fg.push_back(G2);
+            fg.back().t1 = (int)tiles.size();
             const FoldSeg& sg = segs[gr.seg];
             launch_flops += 8.0 * T_ * (double)(sg.n_end - sg.n_start) / ((double)n_rb_ * n_lb_);
         }

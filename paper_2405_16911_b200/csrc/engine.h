@@ -113,6 +113,11 @@ private:
     // Fold `segs` (one per slot) into S (slots x t_pad x Pf x 4 fp64).
     Status fold(const std::vector<FoldSeg>& segs, double* S, bool overwrite = false);
     Status fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<FoldSeg>& rest);
+    struct TcGroupPlan {
+        int seg, rb, lb;
+        int64_t p0, p1;
+    };
+    Status fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S, int nlb);
     bool tc_capable_ = false;  // sm_100 device (tcgen05)
     // Finalize slots [0, nslots) of S into out tables (out_block = slot) with per-slot scale.
     Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,

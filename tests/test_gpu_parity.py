@@ -377,11 +377,14 @@ def test_device_push_tensor_core_fold_vs_oracle(cyc, oracle):
     dx = torch.from_numpy(x).cuda()
     mp = mean_power(x)
     bins = np.array([0, 1, 3, 100, 511, 512, 700, 1023])
-    for lags in (list(range(64)), list(range(128))):
+    # negative lags: the x window starts before the residue block, and the
+    # partial head/tail periods fold on the FP32 kernel into the same slot
+    for lags in (list(range(64)), list(range(128)), list(range(-32, 32)), list(range(-16, 16)), list(range(32))):
         est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, flags=cyc.Flags.BOTH, emit_frames=False))
         est.push_device(dx.data_ptr(), len(x))
         F = est.frames_emitted()
-        cv, cj = oracle.block_fold(x, x, bins, N, lags, 0, F * N)
+        m_minus = max(0, -lags[0])
+        cv, cj = oracle.block_fold(x, x, bins, N, lags, m_minus, F * N)
         for fl, want in ((cyc.Flags.CONV, cv), (cyc.Flags.CONJ, cj)):
             got = est.average(flag=fl).reshape(len(lags), N)[:, bins]
             assert_parity(got, want.T, mp, what=f"tc fold {len(lags)} lags flag {fl}")
