@@ -783,7 +783,10 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         // [pPf + r0 + d, +128) lie inside the segment's valid ranges
         const int64_t pa = std::max(ceil_div(g.n_start, Pf_), ceil_div(g.x_lo - f_lo_, Pf_));
         const int64_t pb = std::min(floor_div(g.n_end, Pf_), floor_div(g.x_hi - Pf_ - f_lo_ - 64 * nlb, Pf_) + 1);
-        const bool ok = g.vec && g.w_log2 == 0.f && pb - pa >= 16;
+        // short ranges (e.g. a 64-channel record's per-piece share) keep the
+        // FP32 kernel: a tensor-core tile needs a long period range to amortise
+        // its pipeline fill and its 128 KB partials (measured on C4 e2e)
+        const bool ok = g.vec && g.w_log2 == 0.f && pb - pa >= 192;
         if (!ok) {
             rest.push_back(g);
             continue;
