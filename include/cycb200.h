@@ -154,6 +154,34 @@ int cyc_push_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size
  * that is not a multiple of 8 bytes (FormatError). */
 int cyc_push_cf32_file(cyc_est* est, const char* path, cyc_frame_sink sink, void* user);
 
+/* ---- CPM / GMSK generation and the Monte-Carlo oracle ----
+ * CpmParams (proj/include/cycstat/siggen.hpp:16-23). */
+enum { CYC_PULSE_GAUSSIAN = 0, CYC_PULSE_RECT = 1 };
+typedef struct cyc_cpm_params {
+    double h;          /* modulation index, > 0 */
+    int alphabet_size; /* even M >= 2 */
+    int pulse_len;     /* L, frequency-pulse span in symbols */
+    double bt;         /* bandwidth-symbol-time product (Gaussian pulse) */
+    int sps;           /* samples per symbol */
+    int pulse_kind;    /* CYC_PULSE_* */
+} cyc_cpm_params;
+/* Reference defaults: h 0.5, M 2, L 4, BT 0.25, 8 sps, Gaussian. */
+void cyc_cpm_params_init(cyc_cpm_params* p);
+/* random_symbols (proj/src/siggen.cpp:147-157): the same std::mt19937_64 draw. */
+int cyc_random_symbols(int alphabet_size, size_t count, uint64_t seed, int* out, char* err, size_t errlen);
+/* make_pulse (proj/src/siggen.cpp:30-110): f and its running sum g, len = L*sps. */
+int cyc_cpm_pulse(const cyc_cpm_params* p, double* f_out, double* g_out, size_t len, char* err, size_t errlen);
+/* cpm_modulate (proj/src/siggen.cpp:111-145) on the device: n_symbols*sps
+ * samples into `out` (device or host memory), cf32 (out_f64 = 0) or cf64.
+ * CYC_ERR_USAGE / CYC_ERR_DATA with the reference's messages. */
+int cyc_cpm_modulate(const cyc_cpm_params* p, const int* symbols, size_t n_symbols, int device, int out_f64,
+                     void* out, char* err, size_t errlen);
+/* gmsk_mc_oracle (proj/src/reference.cpp:34-96): mean |R| over every window
+ * of every trial, row-major |alphas| x |lags|; trial t uses seed + t. */
+int cyc_gmsk_mc_oracle(const cyc_cpm_params* p, const double* alphas, size_t n_alphas, const int* lags,
+                       size_t n_lags, int conj, int win_len, int trials, size_t record_len, uint64_t seed,
+                       int device, double* mean_magnitude, char* err, size_t errlen);
+
 /* estimate_cfo_ccf (proj/src/impair.cpp:45-115): conjugate Full-mode lag-0
  * scan over num_frames windows of N samples, magnitude average (on the
  * device), peak within +-N/8 bins of expected_beta, median test, log-parabola

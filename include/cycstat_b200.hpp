@@ -22,6 +22,7 @@
 #ifndef CYCSTAT_B200_HPP
 #define CYCSTAT_B200_HPP
 
+#include <algorithm>
 #include <complex>
 #include <cstdint>
 #include <numeric>
@@ -334,6 +335,89 @@ inline std::vector<cx> compute_full_window(const std::vector<cx>& xw, const std:
                                            err.data(), err.size());
     if (rc) detail::raise(rc, err.c_str());
     return out;
+}
+
+// ---- CPM / GMSK generation and the Monte-Carlo oracle (siggen.hpp, reference.hpp) ----
+enum class PulseKind { GaussianGmsk = CYC_PULSE_GAUSSIAN, Rectangular = CYC_PULSE_RECT };
+struct CpmParams {  // siggen.hpp:16-23
+    double h = 0.5;
+    int alphabet_size = 2;
+    int pulse_len = 4;
+    double bt = 0.25;
+    int sps = 8;
+    PulseKind pulse_kind = PulseKind::GaussianGmsk;
+};
+struct PulseTable {  // siggen.hpp:27-30
+    std::vector<double> f;
+    std::vector<double> g;
+};
+struct OracleTable {  // reference.hpp:15-28
+    std::vector<double> alphas;
+    std::vector<int> lags;
+    std::vector<double> mean_magnitude;
+    int trials = 0;
+    std::size_t record_len = 0;
+    std::uint64_t seed = 0;
+    double cell(std::size_t a, std::size_t l) const { return mean_magnitude[a * lags.size() + l]; }
+};
+namespace detail {
+inline cyc_cpm_params to_c(const CpmParams& p) {
+    cyc_cpm_params c;
+    c.h = p.h;
+    c.alphabet_size = p.alphabet_size;
+    c.pulse_len = p.pulse_len;
+    c.bt = p.bt;
+    c.sps = p.sps;
+    c.pulse_kind = static_cast<int>(p.pulse_kind);
+    return c;
+}
+}  // namespace detail
+inline std::vector<int> random_symbols(int alphabet_size, std::size_t count, std::uint64_t seed) {
+    std::vector<int> out(count);
+    std::string err(1024, '\0');
+    const int rc = cyc_random_symbols(alphabet_size, count, seed, out.data(), err.data(), err.size());
+    if (rc) detail::raise(rc, err.c_str());
+    return out;
+}
+inline PulseTable make_pulse(const CpmParams& params) {
+    const cyc_cpm_params c = detail::to_c(params);
+    const std::size_t n = params.pulse_len > 0 && params.sps > 0 ? (std::size_t)params.pulse_len * params.sps : 0;
+    PulseTable t;
+    t.f.resize(n);
+    t.g.resize(n);
+    std::string err(1024, '\0');
+    const int rc = cyc_cpm_pulse(&c, t.f.data(), t.g.data(), n, err.data(), err.size());
+    if (rc) detail::raise(rc, err.c_str());
+    return t;
+}
+// siggen.cpp:111-145 on the device (fp64 samples, as the reference returns)
+inline std::vector<cx> cpm_modulate(const CpmParams& params, const std::vector<int>& symbols, int device = 0) {
+    const cyc_cpm_params c = detail::to_c(params);
+    std::vector<cx> out(symbols.size() * (std::size_t)std::max(params.sps, 0));
+    std::string err(1024, '\0');
+    const int rc = cyc_cpm_modulate(&c, symbols.data(), symbols.size(), device, 1, out.data(), err.data(), err.size());
+    if (rc) detail::raise(rc, err.c_str());
+    return out;
+}
+// reference.cpp:34-96 on the device
+inline OracleTable gmsk_mc_oracle(const CpmParams& params, const std::vector<double>& alphas,
+                                  const std::vector<int>& lags, bool conj, int win_len, int trials,
+                                  std::size_t record_len, std::uint64_t seed, int device = 0) {
+    const cyc_cpm_params c = detail::to_c(params);
+    OracleTable t;
+    t.alphas = alphas;
+    t.lags = lags;
+    t.trials = trials;
+    t.record_len = record_len;
+    t.seed = seed;
+    t.mean_magnitude.assign(std::max<std::size_t>(alphas.size() * lags.size(), 1), 0.0);
+    std::string err(1024, '\0');
+    const int rc = cyc_gmsk_mc_oracle(&c, alphas.data(), alphas.size(), lags.data(), lags.size(), conj ? 1 : 0,
+                                      win_len, trials, record_len, seed, device, t.mean_magnitude.data(), err.data(),
+                                      err.size());
+    if (rc) detail::raise(rc, err.c_str());
+    t.mean_magnitude.resize(alphas.size() * lags.size());
+    return t;
 }
 
 // impair.cpp:45-115 on the device

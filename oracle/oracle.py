@@ -163,6 +163,12 @@ class RefLib:
         L.ref_apply_cfo.argtypes = [_dp, C.c_size_t, C.c_double, C.c_double]
         L.ref_add_noise_snr.argtypes = [_dp, C.c_size_t, C.c_double, C.c_uint64]
         L.ref_cpm.argtypes = [C.c_size_t, C.c_double, C.c_double, C.c_int, C.c_uint64, _dp]
+        _cpm = [C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int]
+        L.ref_random_symbols.argtypes = [C.c_int, C.c_size_t, C.c_uint64, C.POINTER(C.c_int)]
+        L.ref_pulse.argtypes = _cpm + [_dp, _dp]
+        L.ref_cpm_modulate.argtypes = _cpm + [C.POINTER(C.c_int), C.c_size_t, _dp]
+        L.ref_gmsk_mc_oracle.argtypes = _cpm + [_dp, C.c_size_t, C.POINTER(C.c_int), C.c_size_t, C.c_int, C.c_int,
+                                                C.c_int, C.c_size_t, C.c_uint64, _dp]
         L.ref_estimate_cfo_ccf.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, _dp]
         self.lib = L
 
@@ -170,6 +176,43 @@ class RefLib:
         out = np.zeros(2 * n)
         self._err(self.lib.ref_cpm(n, h, bt, sps, seed, _p(out, _dp)))
         return out.view(np.complex128)
+
+    @staticmethod
+    def _cpm_args(p):
+        return [float(p.get("h", 0.5)), int(p.get("alphabet_size", 2)), int(p.get("pulse_len", 4)),
+                float(p.get("bt", 0.25)), int(p.get("sps", 8)), int(p.get("pulse_kind", 0))]
+
+    def random_symbols(self, M, count, seed):
+        out = np.zeros(count, dtype=np.int32)
+        self._err(self.lib.ref_random_symbols(M, count, seed, out.ctypes.data_as(C.POINTER(C.c_int))))
+        return out
+
+    def pulse(self, **p):
+        a = self._cpm_args(p)
+        n = a[2] * a[4]
+        f, g = np.zeros(n), np.zeros(n)
+        self._err(self.lib.ref_pulse(*a, _p(f, _dp), _p(g, _dp)))
+        return f, g
+
+    def cpm_modulate(self, symbols, **p):
+        sym = np.ascontiguousarray(symbols, dtype=np.int32)
+        out = np.zeros(2 * len(sym) * int(p.get("sps", 8)))
+        rc = self.lib.ref_cpm_modulate(*self._cpm_args(p), sym.ctypes.data_as(C.POINTER(C.c_int)), len(sym),
+                                       _p(out, _dp))
+        if rc:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return out.view(np.complex128)
+
+    def gmsk_mc_oracle(self, alphas, lags, conj, win_len, trials, record_len, seed, **p):
+        al = np.ascontiguousarray(alphas, dtype=np.float64)
+        lg = np.ascontiguousarray(lags, dtype=np.int32)
+        out = np.zeros(len(al) * len(lg))
+        rc = self.lib.ref_gmsk_mc_oracle(*self._cpm_args(p), _p(al, _dp), len(al),
+                                         lg.ctypes.data_as(C.POINTER(C.c_int)), len(lg), int(conj), int(win_len),
+                                         int(trials), int(record_len), int(seed), _p(out, _dp))
+        if rc:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return out.reshape(len(al), len(lg))
 
     def estimate_cfo_ccf(self, x, beta, N, frames):
         """eps, or raises LookupError for NoFeatureError / ValueError for UsageError."""

@@ -217,6 +217,60 @@ int ref_estimate_cfo_ccf(const double* x, std::size_t len, double beta, int N, i
     catch (const std::exception& e) { return fail(e, 5); }
 }
 
+CpmParams make_cpm(double h, int M, int L, double bt, int sps, int kind) {
+    CpmParams p;
+    p.h = h;
+    p.alphabet_size = M;
+    p.pulse_len = L;
+    p.bt = bt;
+    p.sps = sps;
+    p.pulse_kind = kind == 0 ? PulseKind::GaussianGmsk : PulseKind::Rectangular;
+    return p;
+}
+
+// random_symbols / make_pulse / cpm_modulate / gmsk_mc_oracle with explicit
+// CpmParams (proj/src/siggen.cpp, proj/src/reference.cpp:34-96)
+int ref_random_symbols(int M, std::size_t count, std::uint64_t seed, int* out) {
+    try {
+        const auto s = random_symbols(M, count, seed);
+        std::copy(s.begin(), s.end(), out);
+        return 0;
+    } catch (const std::exception& e) { return fail(e, 1); }
+}
+
+int ref_pulse(double h, int M, int L, double bt, int sps, int kind, double* f, double* g) {
+    try {
+        const auto t = make_pulse(make_cpm(h, M, L, bt, sps, kind));
+        std::copy(t.f.begin(), t.f.end(), f);
+        std::copy(t.g.begin(), t.g.end(), g);
+        return 0;
+    } catch (const UsageError& e) { return fail(e, 1); }
+    catch (const std::exception& e) { return fail(e, 3); }
+}
+
+int ref_cpm_modulate(double h, int M, int L, double bt, int sps, int kind, const int* sym, std::size_t n,
+                     double* out) {
+    try {
+        const auto x = cpm_modulate(make_cpm(h, M, L, bt, sps, kind), std::vector<int>(sym, sym + n));
+        store(x, out);
+        return 0;
+    } catch (const UsageError& e) { return fail(e, 1); }
+    catch (const DataError& e) { return fail(e, 3); }
+    catch (const std::exception& e) { return fail(e, 5); }
+}
+
+int ref_gmsk_mc_oracle(double h, int M, int L, double bt, int sps, int kind, const double* alphas, std::size_t na,
+                       const int* lags, std::size_t nl, int conj, int win_len, int trials, std::size_t record_len,
+                       std::uint64_t seed, double* out) {
+    try {
+        const auto t = gmsk_mc_oracle(make_cpm(h, M, L, bt, sps, kind), std::vector<double>(alphas, alphas + na),
+                                      std::vector<int>(lags, lags + nl), conj != 0, win_len, trials, record_len, seed);
+        std::copy(t.mean_magnitude.begin(), t.mean_magnitude.end(), out);
+        return 0;
+    } catch (const UsageError& e) { return fail(e, 1); }
+    catch (const std::exception& e) { return fail(e, 5); }
+}
+
 int ref_tone(double f0, double phi0, std::size_t len, double* out) {
     store(tone(f0, phi0, len), out);
     return 0;

@@ -35,6 +35,8 @@ __all__ = [
     "CyclicFrame", "CyclicCorrelator", "validate_config", "layout_len", "flat_index",
     "full_bin_to_alpha", "average_frames", "compute_set_window", "compute_full_window",
     "UsageError", "ConfigError", "DataError", "CudaError", "LogicError", "lib", "host_alloc",
+    "NoFeatureError", "IoError", "estimate_cfo_ccf", "write_cf32", "PulseKind", "CpmParams", "OracleTable",
+    "random_symbols", "cpm_pulse", "cpm_modulate", "gmsk_mc_oracle",
 ]
 
 
@@ -103,6 +105,11 @@ class _LayoutInfo(C.Structure):
                 ("num_lags", C.c_int), ("win_len", C.c_int), ("len", C.c_size_t)]
 
 
+class _CpmParams(C.Structure):
+    _fields_ = [("h", C.c_double), ("alphabet_size", C.c_int), ("pulse_len", C.c_int), ("bt", C.c_double),
+                ("sps", C.c_int), ("pulse_kind", C.c_int)]
+
+
 _SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(_FrameView))
 _lib: Optional[C.CDLL] = None
 
@@ -156,6 +163,15 @@ def lib() -> C.CDLL:
     L.cyc_estimate_cfo_ccf.argtypes = [vp, sz, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
                                        C.c_char_p, sz]
     L.cyc_reset.argtypes = [vp]
+    L.cyc_cpm_params_init.argtypes = [C.POINTER(_CpmParams)]
+    L.cyc_random_symbols.argtypes = [C.c_int, sz, C.c_uint64, C.POINTER(C.c_int), C.c_char_p, sz]
+    L.cyc_cpm_pulse.argtypes = [C.POINTER(_CpmParams), C.POINTER(C.c_double), C.POINTER(C.c_double), sz,
+                                C.c_char_p, sz]
+    L.cyc_cpm_modulate.argtypes = [C.POINTER(_CpmParams), C.POINTER(C.c_int), sz, C.c_int, C.c_int, vp,
+                                   C.c_char_p, sz]
+    L.cyc_gmsk_mc_oracle.argtypes = [C.POINTER(_CpmParams), C.POINTER(C.c_double), sz, C.POINTER(C.c_int), sz,
+                                     C.c_int, C.c_int, C.c_int, sz, C.c_uint64, C.c_int, C.POINTER(C.c_double),
+                                     C.c_char_p, sz]
     L.cyc_profile_enable.argtypes = [vp, C.c_int]
     L.cyc_profile_read.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.cyc_profile_read_ex.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -577,6 +593,106 @@ class CyclicCorrelator:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# CPM / GMSK generation and the Monte-Carlo oracle (proj/include/cycstat/siggen.hpp,
+# reference.hpp) -- SURVEY §8 f4
+# ---------------------------------------------------------------------------
+class PulseKind(enum.IntEnum):
+    GaussianGmsk = 0
+    Rectangular = 1
+
+
+@dataclass
+class CpmParams:
+    """siggen.hpp:16-23 (defaults: h 0.5, M 2, L 4, BT 0.25, 8 sps, Gaussian)."""
+    h: float = 0.5
+    alphabet_size: int = 2
+    pulse_len: int = 4
+    bt: float = 0.25
+    sps: int = 8
+    pulse_kind: PulseKind = PulseKind.GaussianGmsk
+
+    def _c(self) -> _CpmParams:
+        return _CpmParams(float(self.h), int(self.alphabet_size), int(self.pulse_len), float(self.bt),
+                          int(self.sps), int(self.pulse_kind))
+
+
+@dataclass
+class OracleTable:
+    """reference.hpp:15-28: row-major |alphas| x |lags| mean magnitudes."""
+    alphas: list
+    lags: list
+    mean_magnitude: np.ndarray
+    trials: int
+    record_len: int
+    seed: int
+
+    def cell(self, alpha_idx: int, lag_idx: int) -> float:
+        return float(self.mean_magnitude[alpha_idx * len(self.lags) + lag_idx])
+
+
+def _err_buf():
+    return C.create_string_buffer(1024)
+
+
+def random_symbols(alphabet_size: int, count: int, seed: int) -> np.ndarray:
+    """siggen.cpp:147-157 (the same mt19937_64 draw)."""
+    out = np.zeros(count, dtype=np.int32)
+    err = _err_buf()
+    _raise_rc(lib().cyc_random_symbols(int(alphabet_size), count, int(seed) & (2**64 - 1),
+                                       out.ctypes.data_as(C.POINTER(C.c_int)), err, 1024), err)
+    return out
+
+
+def cpm_pulse(params: Optional[CpmParams] = None):
+    """make_pulse (siggen.cpp:103-109): (f, g), length pulse_len * sps."""
+    p = params or CpmParams()
+    n = int(p.pulse_len) * int(p.sps)
+    f, g = np.zeros(max(n, 0)), np.zeros(max(n, 0))
+    err = _err_buf()
+    _raise_rc(lib().cyc_cpm_pulse(C.byref(p._c()), f.ctypes.data_as(C.POINTER(C.c_double)),
+                                  g.ctypes.data_as(C.POINTER(C.c_double)), max(n, 0), err, 1024), err)
+    return f, g
+
+
+def cpm_modulate(params: Optional[CpmParams], symbols, device: int = 0, out=None, f64: bool = False):
+    """cpm_modulate (siggen.cpp:111-145) on the device.  Returns a host array
+    (complex64, or complex128 with f64=True); `out` may be a device array
+    (`__cuda_array_interface__`) that receives the samples instead."""
+    p = params or CpmParams()
+    sym = np.ascontiguousarray(symbols, dtype=np.int32)
+    n = sym.size * int(p.sps)
+    err = _err_buf()
+    if out is None:
+        out = np.empty(n, dtype=np.complex128 if f64 else np.complex64)
+        ptr = out.ctypes.data
+    else:
+        ptr = int(out.__cuda_array_interface__["data"][0])
+    _raise_rc(lib().cyc_cpm_modulate(C.byref(p._c()), sym.ctypes.data_as(C.POINTER(C.c_int)), sym.size,
+                                     int(device), int(bool(f64)), ptr, err, 1024), err)
+    return out
+
+
+def gmsk_mc_oracle(params: Optional[CpmParams], alphas, lags, conj: bool, win_len: int, trials: int,
+                   record_len: int, seed: int, device: int = 0) -> OracleTable:
+    """gmsk_mc_oracle (reference.cpp:34-96) on the device."""
+    p = params or CpmParams()
+    al = np.ascontiguousarray(list(alphas), dtype=np.float64)
+    lg = np.ascontiguousarray(list(lags), dtype=np.int32)
+    out = np.zeros(max(al.size * lg.size, 1))
+    err = _err_buf()
+    _raise_rc(lib().cyc_gmsk_mc_oracle(C.byref(p._c()), al.ctypes.data_as(C.POINTER(C.c_double)), al.size,
+                                       lg.ctypes.data_as(C.POINTER(C.c_int)), lg.size, int(bool(conj)),
+                                       int(win_len), int(trials), int(record_len), int(seed) & (2**64 - 1),
+                                       int(device), out.ctypes.data_as(C.POINTER(C.c_double)), err, 1024), err)
+    return OracleTable(list(al), list(lg), out[:al.size * lg.size], int(trials), int(record_len), int(seed))
+
+
+def _raise_rc(rc: int, err) -> None:
+    if rc:
+        _raise(rc, err.value.decode())
 
 
 def estimate_cfo_ccf(x, expected_beta: float, N: int, num_frames: int, device: int = 0) -> float:

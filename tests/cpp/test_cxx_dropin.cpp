@@ -179,6 +179,27 @@ int main() {
         } catch (const NoFeatureError&) {
         }
     }
+    // CPM generation and the Monte-Carlo oracle (test_reference.cpp:117-145)
+    {
+        CpmParams p;
+        const auto syms = random_symbols(p.alphabet_size, 256, 42);
+        const auto x = cpm_modulate(p, syms);
+        CHECK(x.size() == 256u * 8u);
+        double worst = 0;
+        for (const auto& v : x) worst = std::max(worst, std::abs(std::abs(v) - 1.0));
+        CHECK(worst <= 1e-12);  // constant envelope
+        CHECK(make_pulse(p).g.back() == 0.5);
+        const auto t = gmsk_mc_oracle(p, {0.125, 0.0}, {-4, -1, 0, 2}, false, 256, 3, 1100, 42);
+        CHECK(t.mean_magnitude.size() == 8);
+        const auto again = gmsk_mc_oracle(p, {0.125, 0.0}, {-4, -1, 0, 2}, false, 256, 3, 1100, 42);
+        CHECK(t.mean_magnitude == again.mean_magnitude);
+        CHECK(std::abs(t.cell(1, 2) - 1.0) <= 1e-6);  // |R(0, 0)| = mean power = 1
+        try {
+            gmsk_mc_oracle(p, {}, {0}, false, 256, 1, 1100, 1);
+            CHECK(false);
+        } catch (const UsageError&) {
+        }
+    }
     std::printf("%s: %d failure(s)\n", g_fail ? "FAIL" : "PASS", g_fail);
     return g_fail;
 }
