@@ -676,9 +676,9 @@ Status Engine::ensure_frames(size_t slots) {
     return Status::ok();
 }
 
-// Launch metadata (segments, tiles, rows) lives in mapped page-locked host
-// memory (also usable directly by kernels, CYC_META_MAPPED); by default each
-// upload is copied to a device shadow arena on the compute stream.
+// Launch metadata that does not ride in a kernel's parameter block (finalize
+// rows, direct segments, ...) is staged in mapped page-locked host memory;
+// each upload is copied to a device shadow arena on the compute stream.
 Status Engine::ensure_meta(size_t bytes) {
     if (meta_slot_bytes_ >= bytes) return Status::ok();
     if (meta_host_) {
@@ -716,13 +716,12 @@ void* Engine::upload(const void* src, size_t bytes) {
     const size_t off = (size_t)meta_slot_ * meta_slot_bytes_ + meta_used_;
     std::memcpy(meta_host_ + off, src, bytes);
     meta_used_ += span;
-    // Kernels read descriptors from a device copy: measured 15% faster folds
-    // than reading the mapped host arena directly (CYC_META_MAPPED=1 restores
-    // the mapped path for experiments).
-    // Exception: during a pinned-host push the copy engines are busy with the
-    // bulk DMA and a descriptor copy would queue behind it -- read mapped then.
-    static const bool mapped = std::getenv("CYC_META_MAPPED") != nullptr;
-    if (mapped || meta_mapped_now_) return meta_dev_ + off;
+    // Kernels read descriptors from a device copy (measured 15% faster folds
+    // than reading the mapped host arena) -- except during a pinned-host push,
+    // when the copy engines are busy with the bulk DMA and a descriptor copy
+    // would queue behind it: read mapped then.  (Fold launches carry their
+    // descriptors in the parameter block; this arena serves the rest.)
+    if (meta_mapped_now_) return meta_dev_ + off;
     if (!meta_shadow_) cudaMalloc(&meta_shadow_, META_SLOTS * meta_slot_bytes_);
     cudaMemcpyAsync(meta_shadow_ + off, meta_host_ + off, bytes, cudaMemcpyHostToDevice, cs_);
     return meta_shadow_ + off;
@@ -820,8 +819,6 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
 Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S,
                              int nlb) {
     using G = TcGroupPlan;
-    static const bool dry = std::getenv("CYC_TC_DRYRUN") != nullptr;  // diagnostics: plan, do not launch
-    if (dry) return Status::ok();
     if (!tcp_) tcp_.reset(new TcParams);
     std::memset(tcp_.get(), 0, sizeof(TcParams));
     std::memcpy(tcp_->segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
@@ -894,7 +891,6 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         L.S = S;
         L.overwrite = 0;
         L.gate = fold_gate_;
-        L.dbg = std::getenv("CYC_TC_DBG") ? std::atoi(std::getenv("CYC_TC_DBG")) : 0;
         if (prof_) {
             // executed: 2 accumulators x 3 MMAs (M=128, N=256, K=16) per 16-period stage
             double exec = 0.0;
@@ -930,8 +926,6 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
             g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
         TRY(fold_tc(sg, S, segs_tc_rest));
     }
-    static const bool skip_rest = std::getenv("CYC_TC_SKIP_REST") != nullptr;  // diagnostics
-    if (tc && skip_rest) segs_tc_rest.clear();
     const std::vector<FoldSeg>& segs = tc ? segs_tc_rest : segs_in;
     std::vector<G> groups;
     int64_t work = 0;
@@ -958,8 +952,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
     };
     // split long groups into whole waves of 1 CTA/SM: each group gets a share of
     // `target` tiles proportional to its periods (floor), so no partial wave
-    static const int waves = std::getenv("CYC_FOLD_WAVES") ? std::atoi(std::getenv("CYC_FOLD_WAVES")) : 1;
-    const int64_t target = std::max<int64_t>((int64_t)std::max(waves, 1) * SMS, (int64_t)groups.size());
+    const int64_t target = std::max<int64_t>(SMS, (int64_t)groups.size());
     size_t g0 = 0;
     while (g0 < groups.size()) {
         std::vector<FoldTile> tiles;
@@ -987,8 +980,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
         std::vector<FoldSeg> sg(segs);
         for (auto& g : sg)
             g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
-        static const bool no_inline = std::getenv("CYC_NO_INLINE") != nullptr;  // A/B knob
-        const bool inl = !no_inline && sg.size() <= (size_t)FI_SEGS && tiles.size() <= (size_t)FI_TILES &&
+        const bool inl = sg.size() <= (size_t)FI_SEGS && tiles.size() <= (size_t)FI_TILES &&
                          fg.size() <= (size_t)FI_GROUPS;
         if (inl) {
             // descriptors ride in the kernel parameter block
@@ -1711,8 +1703,7 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
             cudaEventCreate(&tc);
             cudaEventRecord(ta, xs_);
         }
-        static const bool nomap = std::getenv("CYC_META_NOMAP") != nullptr;  // experiment knob
-        meta_mapped_now_ = !nomap;  // descriptor copies would queue behind the bulk DMA
+        meta_mapped_now_ = true;  // descriptor copies would queue behind the bulk DMA
         for (size_t off = 0; off < n; off += (size_t)Q_) {
             const size_t len = std::min((size_t)Q_, n - off);
             const int64_t abs0 = origin_ + (int64_t)consumed_;

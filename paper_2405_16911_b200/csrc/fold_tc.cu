@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 const uint32_t xh = su32(plane_ring + s * G::PLANE), xl = xh + XPLANE;
                 const uint32_t yh0 = SELF ? xh + ya * ATOM : xl + XPLANE;
                 const uint32_t yl0 = SELF ? xl + ya * ATOM : yh0 + YPLANE;
-                if (L.dbg != 2 && L.dbg != 3) {
+                {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {  // residues 64h..64h+63: y atoms 2h.., x atoms 2h..2h+3
                         const uint64_t dxh = sw128_desc(xh + 2 * h * ATOM, ATOM, 1024);
@@ -300,16 +300,13 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
             const uint32_t xh = su32(plane_ring + ps * G::PLANE);
             const uint32_t xl = xh + XPLANE;
-            if (L.dbg != 1 && L.dbg != 3) {
 #pragma unroll
-                for (int u = ct; u < (XF / 32) * 64; u += 32 * TNC) convert_unit(st, u, swz, XF * 4, xh, xl, rows);
-                if (!SELF) {
-                    const uint32_t yh = xl + XPLANE;
-                    const uint32_t yl = yh + YPLANE;
+            for (int u = ct; u < (XF / 32) * 64; u += 32 * TNC) convert_unit(st, u, swz, XF * 4, xh, xl, rows);
+            if (!SELF) {
+                const uint32_t yh = xl + XPLANE;
+                const uint32_t yl = yh + YPLANE;
 #pragma unroll
-                    for (int u = ct; u < (YF / 32) * 64; u += 32 * TNC)
-                        convert_unit(st + XRAW, u, swz, YF * 4, yh, yl, rows);
-                }
+                for (int u = ct; u < (YF / 32) * 64; u += 32 * TNC) convert_unit(st + XRAW, u, swz, YF * 4, yh, yl, rows);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&rawfree[rs]);  // raw slot reusable (generic reads done)

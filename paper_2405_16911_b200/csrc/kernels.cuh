@@ -67,7 +67,6 @@ struct FoldLaunch {
     // non-null: the reduce commits only if *gate == ~0 (the chunk's finite scan,
     // stream-ordered before the fold, found nothing) -- a rejected chunk leaves S untouched
     const unsigned long long* gate;
-    int dbg;  // experiments only (tensor-core fold: 1 = skip conversion, 2 = skip MMAs)
 };
 
 // Launch descriptors carried in the kernel parameter block (<= 32 KB since
