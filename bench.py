@@ -256,10 +256,15 @@ def run_reference(args, ws, rank):
     cb = dict(vals[-1])
     cb["value"] = v
     ms = 1e3 * updates(L_REC) / v  # time the full record would take at this rate
+    cfgb = config_block(args.gpus)
+    cfgb["algorithm"] = ("reference cycstat (oracle/_ref, compiled from proj/src): full_window_values + radix-2 "
+                         "FFT per frame, fp64, OpenMP over lags")
+    cfgb["ms_per_step_basis"] = (f"the full C2 record at the measured rate; each timed step is a bounded "
+                                 f"{frames}-frame sample")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args.gpus), "cpu_baseline": cb,
+            "config": cfgb, "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
