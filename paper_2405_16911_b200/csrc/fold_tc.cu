@@ -46,7 +46,7 @@ constexpr int YRAW = TKB * YF * 4;      // 16 KB
 constexpr int ATOM = TKB * 128;         // one MN atom column of a plane: 64 bf16 x 16 rows
 constexpr int XPLANE = TKB * XF * 2;    // 12 KB: 6 atoms
 constexpr int YPLANE = TKB * YF * 2;    // 8 KB: 4 atoms
-constexpr int TNC = 8;                  // converter / epilogue warps (warps 2 .. TNC+1)
+constexpr int TNC = 12;                 // converter / epilogue warps (warps 2 .. TNC+1), a multiple of 4
 constexpr int TNT = 64 + 32 * TNC;      // + warp 0 producer, warp 1 MMA issuer
 // Two rings: raw fp32 stages (producer -> converters, freed after conversion)
 // and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).
@@ -319,11 +319,14 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         // the band is columns [2r, 2r + 128): float2 (c_{2a}, c_{2a+1}) per lag t
         mbar_wait(&done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int q = warp & 3;  // TMEM lane quarter this warp may read
         const int m = 32 * q + lane;
         const int r = m >> 1, a = m & 1;
         float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)blockIdx.x * 64 * TRB * 2;
-        for (int c = q; c < q + 5; ++c) {  // columns [32c, 32c + 32) cover the quarter's band
+        // a quarter's work: 2 accumulators x 5 column chunks [32c, 32c + 32),
+        // c = q .. q+4 (they cover the band), shared by the quarter's TNC/4 warps
+        for (int item = (warp - 2) >> 2; item < 10; item += TNC / 4) {
+            const int h = item / 5, c = q + item % 5;
             uint32_t v[32];
             const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h + 32 * c);
             asm volatile(
