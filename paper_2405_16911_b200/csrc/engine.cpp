@@ -1473,11 +1473,8 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
             bad = scan_bad((const cyc_cf64*)xv, (const cyc_cf64*)yv, n, C);
         } else {
             CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
-            for (int ch = 0; ch < C; ++ch) {
-                launches_ += launch_finite_check((const float2*)xv + (size_t)ch * n,
-                                                 yv ? (const float2*)yv + (size_t)ch * n : nullptr, (int64_t)n, 0, C,
-                                                 ch, key_dev_, cs_);
-            }
+            launches_ += launch_finite_check((const float2*)xv, (const float2*)yv, (int64_t)n, 0, C, 0, key_dev_, cs_,
+                                             C, (int64_t)n);
             CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs_));
             CK(cudaStreamSynchronize(cs_));
             if (*key_host_ != ~0ull) {
@@ -1675,11 +1672,8 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
         cudaEvent_t ev_k = get_event(), ev_c = get_event();
         CK(cudaEventRecord(ev_k, cs_));
         CK(cudaStreamWaitEvent(vs_, ev_k, 0));
-        for (int ch = 0; ch < C; ++ch) {
-            launches_ += launch_finite_check((const float2*)xv + (size_t)ch * n,
-                                             yv ? (const float2*)yv + (size_t)ch * n : nullptr, (int64_t)n, 0, C, ch,
-                                             key_dev_, vs_);
-        }
+        launches_ += launch_finite_check((const float2*)xv, (const float2*)yv, (int64_t)n, 0, C, 0, key_dev_, vs_, C,
+                                         (int64_t)n);
         CK(cudaEventRecord(ev_c, vs_));
         trace("scan enqueued");
         fold_gate_ = key_dev_;
@@ -1712,15 +1706,13 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
             // GPU finite scan of the piece as it sits in the ring (wrap split)
             const size_t pos = (size_t)((uint64_t)abs0 & mask_);
             const size_t first = std::min(len, (size_t)cap_ - pos);
-            for (int ch = 0; ch < C; ++ch) {
-                const float2* rx = ring_x_ + (size_t)ch * cap_;
-                const float2* ry = cross_ ? ring_y_ + (size_t)ch * cap_ : nullptr;
-                launches_ += launch_finite_check(rx + pos, ry ? ry + pos : nullptr, (int64_t)first, (int64_t)off, C,
-                                                 ch, key_dev_, cs_);
-                if (first < len)
-                    launches_ += launch_finite_check(rx, ry, (int64_t)(len - first), (int64_t)(off + first), C, ch,
-                                                     key_dev_, cs_);
-            }
+            // every channel's piece in one launch (rows cap_ apart), split at the wrap
+            const float2* ry = cross_ ? ring_y_ : nullptr;
+            launches_ += launch_finite_check(ring_x_ + pos, ry ? ry + pos : nullptr, (int64_t)first, (int64_t)off, C, 0,
+                                             key_dev_, cs_, C, cap_);
+            if (first < len)
+                launches_ += launch_finite_check(ring_x_, ry, (int64_t)(len - first), (int64_t)(off + first), C, 0,
+                                                 key_dev_, cs_, C, cap_);
             mark_read(abs0);
             consumed_ += len;
             // Fold after every piece: the batch folded after the last DMA is

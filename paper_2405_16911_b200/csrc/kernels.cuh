@@ -186,9 +186,10 @@ void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len,
                          double2* coh, double* mag, cudaStream_t st);
 // First non-finite sample -> atomicMin(*key);
 // key = (2*(base+i) + is_y) * channels + ch  -- smallest = reference scan order.
-// returns the number of kernels launched
+// returns the number of kernels launched; nch > 1 scans channels ch .. ch+nch-1
+// in one launch, channel rows `pitch` samples apart
 int launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
-                        unsigned long long* key, cudaStream_t st);
+                        unsigned long long* key, cudaStream_t st, int nch = 1, int64_t pitch = 0);
 // Ring write from a device source with wrap: ring[(abs0 + i) & mask] = src[i].
 void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src,
                        int64_t n, cudaStream_t st);

@@ -1,4 +1,6 @@
 // misc.cu -- small device utilities of the streaming engine.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace cyc {
@@ -30,8 +32,12 @@ __global__ void accum_frames_kernel(const double2* frames, int64_t n_frames, int
 // Whole-chunk finite scan (proj/src/estimator.cpp:43-52): the smallest key
 // 2*i (x) / 2*i+1 (y) names the first offending sample in the reference's
 // scan order (x before y at each index).
+// blockIdx.y selects channel ch + blockIdx.y, whose samples start pitch * blockIdx.y further
 __global__ void finite_check_kernel(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
-                                    unsigned long long* key) {
+                                    unsigned long long* key, int64_t pitch) {
+    x += pitch * blockIdx.y;
+    if (y) y += pitch * blockIdx.y;
+    ch += blockIdx.y;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float2 a = x[i];
         unsigned long long k = ~0ull;
@@ -57,7 +63,10 @@ __device__ __forceinline__ bool nonfinite4(const float4& v) {
 // sample so the key is exactly the scalar kernel's.
 __global__ void __launch_bounds__(256) finite_check_v4_kernel(const float4* x, const float4* y, int64_t pairs,
                                                               int64_t base, int channels, int ch,
-                                                              unsigned long long* key) {
+                                                              unsigned long long* key, int64_t pitch) {
+    x += (pitch / 2) * blockIdx.y;  // pitch in samples (even: 16-byte aligned rows)
+    if (y) y += (pitch / 2) * blockIdx.y;
+    ch += blockIdx.y;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     auto slow = [&](int64_t p) {
         unsigned long long k = ~0ull;
@@ -117,22 +126,23 @@ void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len, d
     if (n_frames > 0 && len > 0) accum_frames_kernel<<<grid_for(len, 256), 256, 0, st>>>(frames, n_frames, len, coh, mag);
 }
 int launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
-                        unsigned long long* key, cudaStream_t st) {
-    if (n <= 0) return 0;
-    const bool aligned = ((uintptr_t)x % 16 == 0) && (!y || (uintptr_t)y % 16 == 0);
+                        unsigned long long* key, cudaStream_t st, int nch, int64_t pitch) {
+    if (n <= 0 || nch <= 0) return 0;
+    const bool aligned = ((uintptr_t)x % 16 == 0) && (!y || (uintptr_t)y % 16 == 0) && (nch == 1 || pitch % 2 == 0);
     if (aligned && n >= 2 * 256) {
         const int64_t pairs = n / 2;
         int64_t g = (pairs + 4 * 256 - 1) / (4 * 256);
-        if (g > 148 * 8) g = 148 * 8;
-        finite_check_v4_kernel<<<(int)g, 256, 0, st>>>(reinterpret_cast<const float4*>(x),
-                                                        reinterpret_cast<const float4*>(y), pairs, base, channels, ch,
-                                                        key);
+        g = std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8 / nch));
+        finite_check_v4_kernel<<<dim3((unsigned)g, (unsigned)nch), 256, 0, st>>>(
+            reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(y), pairs, base, channels, ch, key,
+            pitch);
         if (n & 1)
-            finite_check_kernel<<<1, 32, 0, st>>>(x + n - 1, y ? y + n - 1 : nullptr, 1, base + n - 1, channels, ch,
-                                                  key);
+            finite_check_kernel<<<dim3(1, (unsigned)nch), 32, 0, st>>>(x + n - 1, y ? y + n - 1 : nullptr, 1,
+                                                                       base + n - 1, channels, ch, key, pitch);
         return (n & 1) ? 2 : 1;
     }
-    finite_check_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, base, channels, ch, key);
+    const int g = std::max(1, std::min(grid_for(n, 256), 148 * 16 / nch));
+    finite_check_kernel<<<dim3((unsigned)g, (unsigned)nch), 256, 0, st>>>(x, y, n, base, channels, ch, key, pitch);
     return 1;
 }
 void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n, cudaStream_t st) {

@@ -573,3 +573,33 @@ def test_multichannel_tensor_core_fold_batches(cyc):
         mp = mean_power(xs[c])
         for fi, fl in ((0, cyc.Flags.CONV), (1, cyc.Flags.CONJ)):
             assert np.max(np.abs(allt[c, fi] - one.average(flag=fl))) <= 1e-6 * mp, (c, fl)
+
+
+@pytest.mark.parametrize("kind", ["pinned", "device", "pageable"])
+def test_multichannel_first_bad_sample(cyc, kind):
+    """The finite scan covers every channel (one launch over all channel rows):
+    the error names the first offender in (index, x-before-y, channel) order
+    and leaves the estimator unchanged."""
+    import torch
+    C_, L = 5, 3 << 20
+    xs = np.stack([rand_c(L, 400 + c) for c in range(C_)])
+    xs[3, 2_000_123] = np.nan
+    xs[1, 2_500_000] = np.inf
+    cfg = full_cfg(cyc, 1024, list(range(32)), emit_frames=False, channels=C_)
+    est = cyc.CyclicCorrelator(cfg)
+    good = np.stack([rand_c(4096, 500 + c) for c in range(C_)])
+    est.push(good)
+    c0 = est.consumed()
+    if kind == "pinned":
+        p = cyc.host_alloc(xs.shape)
+        p[:] = xs
+        call = lambda: est.push(p)
+    elif kind == "device":
+        d = torch.from_numpy(xs).cuda()
+        call = lambda: est.push_device(d.data_ptr(), L)
+    else:
+        call = lambda: est.push(xs)
+    with pytest.raises(cyc.DataError, match=f"index {c0 + 2_000_123} in x stream of channel 3") as ei:
+        call()
+    assert ei.value.index == c0 + 2_000_123
+    assert est.consumed() == c0
