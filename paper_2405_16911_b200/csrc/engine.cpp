@@ -572,6 +572,7 @@ Engine::~Engine() {
     cudaFree(avg_all_dev_);
     cudaFreeHost(avg_host_);
     cudaFree(partials_);
+    for (auto& rc : rows_cache_) cudaFree(rc.second);
     cudaFree(tw_);
     cudaFree(bins_dev_);
     cudaFree(lags_dev_);
@@ -1027,16 +1028,29 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
 
 Status Engine::finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
                         double2* out) {
-    std::vector<FinalRow> rows;
-    rows.reserve((size_t)nslots * T_);
-    for (int s = 0; s < nslots; ++s)
-        for (int t = 0; t < T_; ++t) rows.push_back({s, lags_req_[t] - f_lo_, t, s});
+    // The row table depends on nslots only: build and upload it once per size
+    // (device memory kept for the estimator's lifetime), not per call.
+    const FinalRow* drows = nullptr;
+    for (const auto& rc : rows_cache_)
+        if (rc.first == nslots) drows = rc.second;
+    if (!drows) {
+        std::vector<FinalRow> rows;
+        rows.reserve((size_t)nslots * T_);
+        for (int s = 0; s < nslots; ++s)
+            for (int t = 0; t < T_; ++t) rows.push_back({s, lags_req_[t] - f_lo_, t, s});
+        FinalRow* d = nullptr;
+        CK(cudaMalloc(&d, rows.size() * sizeof(FinalRow)));
+        CK(cudaMemcpyAsync(d, rows.data(), rows.size() * sizeof(FinalRow), cudaMemcpyHostToDevice, cs_));
+        CK(cudaStreamSynchronize(cs_));  // `rows` is pageable and goes out of scope
+        rows_cache_.push_back({nslots, d});
+        drows = d;
+    }
     FinalizeLaunch L{};
     L.S = S;
     L.t_pad = t_pad_;
     L.Pf = (int)Pf_;
-    L.rows = (const FinalRow*)upload(rows.data(), rows.size() * sizeof(FinalRow));
-    L.n_rows = (int)rows.size();
+    L.rows = drows;
+    L.n_rows = nslots * T_;
     L.flags = c_.flags;
     L.bins = bins_dev_;
     L.A = A_;

@@ -270,6 +270,7 @@ private:
     // speculative block pushes: pending fold + history backup for roll-back
     double* S_pend_ = nullptr;
     std::vector<char> blob_;              // host staging of one launch's descriptors
+    std::vector<std::pair<int, FinalRow*>> rows_cache_;  // finalize row tables by slot count (device)
     std::unique_ptr<FoldInline> inline_;  // by-value descriptors of the next fold launch
     std::unique_ptr<TcParams> tcp_;       // by-value descriptors of the next tensor-core fold launch
     const unsigned long long* fold_gate_ = nullptr;  // set while a device chunk folds straight into S_main
