@@ -593,6 +593,11 @@ Engine::~Engine() {
     }
     for (auto& m : reads_) ev_pool_.push_back(m.ev);
     for (auto e : ev_pool_) cudaEventDestroy(e);
+    for (auto e : timed_pool_) cudaEventDestroy(e);
+    for (auto& r : prof_pending_) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
     if (cs_) cudaStreamDestroy(cs_);
     if (xs_) cudaStreamDestroy(xs_);
     if (vs_) cudaStreamDestroy(vs_);
@@ -821,7 +826,6 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
                              int nlb) {
     using G = TcGroupPlan;
     if (!tcp_) tcp_.reset(new TcParams);
-    std::memset(tcp_.get(), 0, sizeof(TcParams));
     std::memcpy(tcp_->segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
     for (size_t i = 0; i < tsegs.size(); ++i) {
         FoldSeg& g = tcp_->segs[i];
@@ -835,8 +839,17 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
                 break;
             }
         trace("tc plan");
+        // re-encode only when the segment's buffer or period range changed
+        MapCache& mc = map_cache_[i];
+        if (mc.valid && mc.x == g.x && mc.y == g.y && mc.p_base == pa && mc.rows == pb - pa) {
+            tcp_->xmap[i] = mc.xm;
+            tcp_->ymap[i] = mc.ym;
+            tcp_->p_base[i] = pa;
+            continue;
+        }
         if (!encode_tc_maps(*tcp_, (int)i, g, pa, pb - pa, (int)Pf_, f_lo_, nlb))
             return Status{CYC_ERR_CUDA, "cuTensorMapEncodeTiled failed for the tensor-core fold", -1};
+        mc = MapCache{g.x, g.y, pa, pb - pa, tcp_->xmap[i], tcp_->ymap[i], true};
     }
     // self groups (y inside the x window) and the rest run as separate launches
     auto is_self = [&](const G& gr) {
@@ -2002,7 +2015,14 @@ Status Engine::compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64*
     return Status::ok();
 }
 
+// Timing events come from a pool refilled by profile_read: creating events
+// inside the profiled step would add their cost to it.
 cudaEvent_t Engine::get_event_timed() {
+    if (!timed_pool_.empty()) {
+        cudaEvent_t e = timed_pool_.back();
+        timed_pool_.pop_back();
+        return e;
+    }
     cudaEvent_t e;
     cudaEventCreate(&e);
     return e;
@@ -2019,8 +2039,8 @@ Status Engine::profile_read(uint64_t* launches, double* ms, double* flops, doubl
         prof_exec_flops_ += r.exec_flops;
         prof_tc_launches_ += r.tensor ? 1 : 0;
         ++prof_launches_;
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
+        timed_pool_.push_back(r.a);
+        timed_pool_.push_back(r.b);
     }
     prof_pending_.clear();
     if (launches) *launches = prof_launches_;

@@ -264,6 +264,7 @@ private:
     };
     bool prof_ = false;
     std::vector<ProfRec> prof_pending_;
+    std::vector<cudaEvent_t> timed_pool_;
     uint64_t prof_launches_ = 0, prof_tc_launches_ = 0;
     double prof_ms_ = 0.0, prof_flops_ = 0.0, prof_exec_flops_ = 0.0;
 
@@ -273,6 +274,14 @@ private:
     std::vector<std::pair<int, FinalRow*>> rows_cache_;  // finalize row tables by slot count (device)
     std::unique_ptr<FoldInline> inline_;  // by-value descriptors of the next fold launch
     std::unique_ptr<TcParams> tcp_;       // by-value descriptors of the next tensor-core fold launch
+    struct MapCache {                     // last tensor maps encoded per segment index
+        const float2* x = nullptr;
+        const float2* y = nullptr;
+        int64_t p_base = 0, rows = 0;
+        CUtensorMap xm, ym;
+        bool valid = false;
+    };
+    MapCache map_cache_[TC_SEGS];
     const unsigned long long* fold_gate_ = nullptr;  // set while a device chunk folds straight into S_main
     float2* hist_bak_ = nullptr;
     size_t hist_cap_ = 0;
