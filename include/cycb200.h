@@ -143,7 +143,14 @@ int cyc_push(cyc_est* est, const cyc_cf32* x, const cyc_cf32* y, size_t n,
  * exact for data that came from cf32, proj/src/io.cpp:90-103). */
 int cyc_push_f64(cyc_est* est, const cyc_cf64* x, const cyc_cf64* y, size_t n,
                  cyc_frame_sink sink, void* user);
-/* Same, from samples already resident in device memory (GPU pipelines). */
+/* Same, from samples already resident in device memory (GPU pipelines).
+ * Stream order: the chunk is read after work already queued on the legacy
+ * default stream (e.g. the kernel that produced it), and work queued there
+ * after the call (e.g. refilling d_x) waits for every read of it.  The call
+ * returns once the chunk's finite check is known -- a rejected chunk returns
+ * CYC_ERR_DATA with the state unchanged, as for host chunks -- while the fold
+ * itself may still be running on cyc_stream(est).  Callers writing d_x from a
+ * non-blocking stream synchronize with cyc_stream(est) first. */
 int cyc_push_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size_t n,
                     cyc_frame_sink sink, void* user);
 
@@ -202,9 +209,10 @@ int cyc_average(cyc_est* est, int avg_mode, int flag, int channel, cyc_cf64* out
  * For cyc_average and cyc_average_all, `out` may be pageable host memory,
  * pinned host memory (the table is DMA'd straight into it) or -- for a
  * block-mode coherent average -- device memory (the table never leaves HBM;
- * the copy is then stream-ordered on cyc_stream(est) and the call returns
- * without waiting: synchronize that stream, or call cyc_synchronize, before
- * reading it from another stream). */
+ * it is then written stream-ordered on cyc_stream(est) and the call returns
+ * without waiting: work later queued on the legacy default stream is ordered
+ * after the write; from a non-blocking stream, synchronize cyc_stream(est) or
+ * call cyc_synchronize before reading it). */
 int cyc_average_all(cyc_est* est, int avg_mode, cyc_cf64* out);
 
 /* Accessors (estimator.hpp:109-115). */

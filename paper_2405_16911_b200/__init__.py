@@ -538,7 +538,9 @@ class CyclicCorrelator:
         return out
 
     def push_device(self, x_ptr: int, n: int, y_ptr: Optional[int] = None) -> list:
-        """Push samples already resident in device memory (complex64)."""
+        """Push samples already resident in device memory (complex64).  Read
+        after the caller's default-stream work; later default-stream work waits
+        for the fold; returns once the chunk's finite check is known."""
         self._frames = []
         self._check(self._L.cyc_push_device(self._h, x_ptr, y_ptr, n, self._sink, None))
         out, self._frames = self._frames, []
@@ -565,9 +567,10 @@ class CyclicCorrelator:
     def average_all(self, mode: AverageMode = AverageMode.Coherent, out: Optional[np.ndarray] = None):
         """All (channel, flag) tables: array [channels, flags, layout_len].
         `out` may also be a device array (`__cuda_array_interface__`, e.g. a
-        torch complex128 CUDA tensor) for a block-mode coherent average; that
-        copy is stream-ordered on `stream()` -- call `synchronize()` before
-        reading it from another stream."""
+        torch complex128 CUDA tensor) for a block-mode coherent average; the
+        table is written stream-ordered on `stream()`, and work later queued
+        on the default stream (torch's) waits for it -- from other streams,
+        call `synchronize()` first."""
         nf = int(self._L.cyc_num_flags(self._h))
         shape = (self._cfg.channels, nf, layout_len(self._layout))
         cai = getattr(out, "__cuda_array_interface__", None)

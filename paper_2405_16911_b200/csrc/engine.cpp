@@ -219,6 +219,11 @@ void trace(const char* what) {
     std::fprintf(stderr, "[cyc] %8.3f ms  %s\n", std::chrono::duration<double, std::milli>(now - t0).count(), what);
 }
 
+bool timeline_on() {
+    static const bool on = std::getenv("CYC_TIMELINE") != nullptr;
+    return on;
+}
+
 // Pinned host or device memory (a DMA can land there directly).
 bool dma_target(const void* p) {
     cudaPointerAttributes a;
@@ -484,7 +489,13 @@ Status Engine::init(const Cfg& cfg) {
     }
     CK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&vs_, cudaStreamNonBlocking));
+    if (std::getenv("CYC_SCAN_PRIO")) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        CK(cudaStreamCreateWithPriority(&vs_, cudaStreamNonBlocking, hi));
+    } else {
+        CK(cudaStreamCreateWithFlags(&vs_, cudaStreamNonBlocking));
+    }
     // ring: pieces of Q samples per channel, four pieces per ring
     int64_t qmin = std::max<int64_t>(next_pow2((int64_t)need_ + N_), 1 << 12);
     int64_t qdef = std::max<int64_t>((1 << 21) / next_pow2(c_.channels), 1 << 12);
@@ -534,6 +545,7 @@ Status Engine::init(const Cfg& cfg) {
     CK(cudaMemcpy(lags_dev_, lags_req_.data(), T_ * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&key_dev_, sizeof(unsigned long long)));
     CK(cudaMallocHost(&key_host_, sizeof(unsigned long long)));
+    CK(cudaEventCreateWithFlags(&verdict_ev_, cudaEventDisableTiming));
     TRY(ensure_meta(4u << 20));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&stage_ev_[i], cudaEventDisableTiming));
     CK(cudaStreamSynchronize(cs_));
@@ -545,6 +557,12 @@ Engine::~Engine() {
         std::fprintf(stderr, "[cyc] %llu pushes, host us/push: validate %.2f ingest %.2f emit %.2f (emit total %.1f ms)\n",
                      (unsigned long long)hprof_calls_, hprof_us_[1] / hprof_calls_, hprof_us_[2] / hprof_calls_,
                      hprof_us_[3] / hprof_calls_, hprof_us_[3] / 1e3);
+    if (timeline_on()) {
+        tl_resolve(true);
+        for (auto& a : tl_acc_)
+            std::fprintf(stderr, "[cyc] timeline %-18s %8.2f us (n=%d)\n", a.first.c_str(),
+                         a.second.first / std::max(1, a.second.second), a.second.second);
+    }
     if (std::getenv("CYC_PROFILE") && hprof_us_[7] > 0)
         std::fprintf(stderr, "[cyc] %.0f frame-graph replays, GPU us/replay %.2f\n", hprof_us_[7],
                      hprof_us_[6] / hprof_us_[7]);
@@ -572,6 +590,11 @@ Engine::~Engine() {
     cudaFree(avg_all_dev_);
     cudaFreeHost(avg_host_);
     cudaFree(partials_);
+    for (auto& tc : tile_cache_) {
+        cudaFree(tc.dev);
+        cudaFreeHost(tc.pin);
+        if (tc.ev) cudaEventDestroy(tc.ev);
+    }
     for (auto& rc : rows_cache_) cudaFree(rc.second);
     cudaFree(tw_);
     cudaFree(bins_dev_);
@@ -579,6 +602,8 @@ Engine::~Engine() {
     cudaFree(afx_dev_);
     cudaFree(key_dev_);
     cudaFreeHost(key_host_);
+    for (auto& g : push_graphs_) drop_push_graph(g);
+    if (verdict_ev_) cudaEventDestroy(verdict_ev_);
     cudaFree(dev_tmp_);
     cudaFree(S_pend_);
     cudaFree(hist_bak_);
@@ -745,6 +770,10 @@ cudaEvent_t Engine::get_event() {
 }
 
 void Engine::mark_read(int64_t lo) {
+    if (capturing_) {  // recorded after each replay of the graph being captured
+        cap_marks_.push_back(lo);
+        return;
+    }
     cudaEvent_t e = get_event();
     cudaEventRecord(e, cs_);
     reads_.push_back({e, lo});
@@ -772,6 +801,50 @@ void Engine::wait_ring_free(int64_t abs_end) {
 // Tensor-core fold of the interior periods of `segs` (every 64-residue x
 // 64-lag window of the period valid); the head/tail periods that are not go
 // back to the FP32 kernel through `rest`.  Block-mode accumulation only.
+// Interior periods [pa, pb) of a segment for the tensor-core fold, and
+// whether it takes the tensor-core path at all.
+bool Engine::tc_interior(const FoldSeg& g, int64_t& pa, int64_t& pb) const {
+    const int nlb = (t_pad_ + 63) / 64;
+    // period p is interior when y [pPf, (p+1)Pf) and every x window
+    // [pPf + r0 + d, +128) lie inside the segment's valid ranges
+    pa = std::max(ceil_div(g.n_start, Pf_), ceil_div(g.x_lo - f_lo_, Pf_));
+    pb = std::min(floor_div(g.n_end, Pf_), floor_div(g.x_hi - Pf_ - f_lo_ - 64 * nlb, Pf_) + 1);
+    // short ranges (e.g. a 64-channel record's per-piece share) keep the
+    // FP32 kernel: a tensor-core tile needs a long period range to amortise
+    // its pipeline fill and its 128 KB partials (measured on C4 e2e)
+    return g.n_end > g.n_start && g.vec && g.w_log2 == 0.f && pb - pa >= 192;
+}
+
+// A device chunk's folds qualify for the fused finite check when they are
+// exactly one tensor-core launch: every segment tensor-core eligible with the
+// same interior [pa, pb), one segment batch, one tile kind (self or not) for
+// every lag block, and the groups and minimum tiles within one launch.
+bool Engine::tc_check_plan(const std::vector<FoldSeg>& segs_in, int64_t& pa, int64_t& pb) const {
+    static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;
+    if (no_tc || t_pad_ < 32 || Pf_ % 128 != 0 || !tc_capable_ || segs_in.empty()) return false;
+    const int nrb = (int)(Pf_ / 128), nlb = (t_pad_ + 63) / 64;
+    if (segs_in.size() > (size_t)TC_SEGS || segs_in.size() * nrb * nlb > (size_t)FI_GROUPS) return false;
+    for (size_t i = 0; i < segs_in.size(); ++i) {
+        FoldSeg g = segs_in[i];
+        g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
+        int64_t a = 0, b = 0;
+        if (!tc_interior(g, a, b)) return false;
+        if (i == 0) {
+            pa = a;
+            pb = b;
+        } else if (a != pa || b != pb) {
+            return false;
+        }
+        for (int lb = 0; lb < nlb; ++lb) {
+            const int64_t d = f_lo_ + 64 * (int64_t)lb;
+            const bool self = g.x == g.y && d <= 0 && -d <= 64 && (-d) % 32 == 0;
+            const bool self0 = segs_in[0].x == segs_in[0].y && f_lo_ <= 0 && -f_lo_ <= 64 && (-f_lo_) % 32 == 0;
+            if (self != self0) return false;
+        }
+    }
+    return (int64_t)segs_in.size() * nrb * nlb * ceil_div(pb - pa, (int64_t)2048) <= FI_TILES;
+}
+
 Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<FoldSeg>& rest) {
     struct G {
         int seg, rb, lb;
@@ -784,14 +857,8 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
     int64_t work = 0;
     for (const FoldSeg& g : segs) {
         if (g.n_end <= g.n_start) continue;
-        // period p is interior when y [pPf, (p+1)Pf) and every x window
-        // [pPf + r0 + d, +128) lie inside the segment's valid ranges
-        const int64_t pa = std::max(ceil_div(g.n_start, Pf_), ceil_div(g.x_lo - f_lo_, Pf_));
-        const int64_t pb = std::min(floor_div(g.n_end, Pf_), floor_div(g.x_hi - Pf_ - f_lo_ - 64 * nlb, Pf_) + 1);
-        // short ranges (e.g. a 64-channel record's per-piece share) keep the
-        // FP32 kernel: a tensor-core tile needs a long period range to amortise
-        // its pipeline fill and its 128 KB partials (measured on C4 e2e)
-        const bool ok = g.vec && g.w_log2 == 0.f && pb - pa >= 192;
+        int64_t pa = 0, pb = 0;
+        const bool ok = tc_interior(g, pa, pb);
         if (!ok) {
             rest.push_back(g);
             continue;
@@ -820,6 +887,36 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         TRY(fold_tc_batch(bsegs, bgroups, S, nlb));
     }
     return Status::ok();
+}
+
+// Device copy of a tile table: a hit returns the cached copy; a miss uploads
+// it on the compute stream (not while a bulk host DMA is in flight, where a
+// small copy would queue behind it -- those launches keep inline parameters).
+const FoldTile* Engine::cached_tiles(const FoldTile* t, int nt) {
+    if (capturing_) return nullptr;  // a graph bakes its parameters in; cache slots get reused
+    for (auto& tc : tile_cache_)
+        if ((int)tc.host.size() == nt && std::memcmp(tc.host.data(), t, nt * sizeof(FoldTile)) == 0) return tc.dev;
+    if (meta_mapped_now_) return nullptr;
+    TileCache& tc = tile_cache_[tile_cache_next_];
+    tile_cache_next_ = (tile_cache_next_ + 1) % 4;
+    if (!tc.dev) {
+        if (cudaMalloc(&tc.dev, FI_TILES * sizeof(FoldTile)) != cudaSuccess ||
+            cudaMallocHost(&tc.pin, FI_TILES * sizeof(FoldTile)) != cudaSuccess ||
+            cudaEventCreateWithFlags(&tc.ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+    } else {
+        cudaEventSynchronize(tc.ev);  // the previous upload has left the staging buffer
+    }
+    std::memcpy(tc.pin, t, nt * sizeof(FoldTile));
+    if (cudaMemcpyAsync(tc.dev, tc.pin, nt * sizeof(FoldTile), cudaMemcpyHostToDevice, cs_) != cudaSuccess) {
+        tc.host.clear();
+        return nullptr;
+    }
+    cudaEventRecord(tc.ev, cs_);
+    tc.host.assign(t, t + nt);
+    return tc.dev;
 }
 
 Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S,
@@ -905,17 +1002,30 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         L.S = S;
         L.overwrite = 0;
         L.gate = fold_gate_;
+        L.chk_key = chk_key_;
+        L.chk_c0 = chk_c0_;
+        L.chk_channels = c_.channels;
+        if (chk_key_) ++chk_launches_;
+        const FoldTile* dt = (tsegs.size() <= 2 && ng <= 16) ? cached_tiles(tcp_->tiles, nt) : nullptr;
         if (prof_) {
             // executed: 2 accumulators x 3 MMAs (M=128, N=256, K=16) per 16-period stage
             double exec = 0.0;
             for (int t = 0; t < nt; ++t)
                 exec += (double)ceil_div(tcp_->tiles[t].p1 - tcp_->tiles[t].p0, 16) * 6.0 * 2.0 * 128 * 256 * 16;
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops, exec, true};
-            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b, reduce_wait_ev_);
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b, reduce_wait_ev_, dt, fold_done_ev_);
             prof_pending_.push_back(r);
         } else {
             trace("tc maps encoded");
-            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, nullptr, nullptr, reduce_wait_ev_);
+            cudaEvent_t a = nullptr, b = nullptr;
+            if (timeline_on()) {
+                tl("tc.start", cs_);
+                a = tl_steps_.back().back().ev;
+                cudaEventCreate(&b);
+                tl_steps_.back().push_back({"tc.fold.end", b});
+            }
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, a, b, reduce_wait_ev_, dt, fold_done_ev_);
+            tl("tc.reduce.end", cs_);
             trace("tc launched");
         }
         launches_ += 2;
@@ -1003,6 +1113,8 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
             std::memcpy(inline_->tiles, tiles.data(), tiles.size() * sizeof(FoldTile));
             std::memcpy(inline_->groups, fg.data(), fg.size() * sizeof(FoldGroup));
         } else {
+            // (a graph would replay the copy from a reused staging slot)
+            if (capturing_) return Status{CYC_ERR_CUDA, "fold descriptors too large for a captured push", -1};
             // one descriptor blob per launch: a single small H2D copy, not three
             const size_t o_t = (sg.size() * sizeof(FoldSeg) + 15) & ~size_t(15);
             const size_t o_g = o_t + ((tiles.size() * sizeof(FoldTile) + 15) & ~size_t(15));
@@ -1478,6 +1590,9 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         return s;
     }
     const int C = c_.channels;
+    // device chunks are read in stream order after the caller's work on the
+    // legacy default stream (e.g. the torch kernel that produced them)
+    if (kind == IN_DEVICE_F32) TRY(legacy_fence(true, true));
     const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
     // Small chunks (< 1 MiB) are copied into our pinned staging even when the
     // caller's memory is pinned: a host memcpy is cheaper than the stream sync
@@ -1674,6 +1789,151 @@ Status Engine::history_copy(int64_t a, int64_t b, bool save) {
     return Status::ok();
 }
 
+Status Engine::enqueue_gated(const void* xv, const void* yv, size_t n, int64_t hb, int64_t hc) {
+    TRY(history_copy(hb, hc, true));
+    CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
+    // fork the side (scan) and copy streams off the compute stream; the scan
+    // runs co-resident with the fold kernels and only the reduces wait for it
+    cudaEvent_t ev_k = get_event();
+    tl("push", cs_);
+    CK(cudaEventRecord(ev_k, cs_));
+    CK(cudaStreamWaitEvent(vs_, ev_k, 0));
+    CK(cudaStreamWaitEvent(xs_, ev_k, 0));
+    ev_pool_.push_back(ev_k);
+    fold_gate_ = key_dev_;
+    const Status st = fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_main_);
+    fold_gate_ = nullptr;
+    return st;
+}
+
+void Engine::drop_push_graph(PushGraph& g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    for (auto& p : g.prof_recs) {
+        cudaEventDestroy(p.a0);
+        cudaEventDestroy(p.b0);
+    }
+    g = PushGraph{};
+}
+
+Status Engine::push_gated(const void* xv, const void* yv, size_t n, int64_t hb, int64_t hc) {
+    static const bool off = std::getenv("CYC_NO_GRAPH") != nullptr;
+    const int64_t c1 = origin_ + (int64_t)consumed_ + (int64_t)n;
+    bool eligible = !off && !timeline_on() && hb == hc;
+    for (const auto& m : reads_)  // a ring-reuse wait would be an edge to work outside the graph
+        if (m.lo < c1 - cap_) eligible = false;
+    if (!eligible) return enqueue_gated(xv, yv, n, hb, hc);
+    PushGraph k;
+    k.x = xv;
+    k.y = yv;
+    k.n = n;
+    k.c0 = consumed_;
+    k.f0 = frames_;
+    k.origin = origin_;
+    k.cap = cap_;
+    k.rx = ring_x_;
+    k.ry = ring_y_;
+    k.S = S_main_;
+    k.partials = partials_;
+    k.cross = cross_;
+    k.prof = prof_;
+    PushGraph* e = nullptr;
+    for (auto& g : push_graphs_)
+        if (g.x == k.x && g.y == k.y && g.n == k.n && g.c0 == k.c0 && g.f0 == k.f0 && g.origin == k.origin &&
+            g.cap == k.cap && g.rx == k.rx && g.ry == k.ry && g.S == k.S && g.partials == k.partials &&
+            g.cross == k.cross && g.prof == k.prof)
+            e = &g;
+    if (!e) {  // first sighting: run directly (it also sizes every buffer the capture will bake in)
+        if (push_graphs_.size() >= 4) {
+            drop_push_graph(push_graphs_.front());
+            push_graphs_.erase(push_graphs_.begin());
+        }
+        push_graphs_.push_back(k);
+        push_graphs_.back().seen = 1;
+        return enqueue_gated(xv, yv, n, hb, hc);
+    }
+    if (e->failed) return enqueue_gated(xv, yv, n, hb, hc);
+    if (!e->exec) {
+        // second sighting: capture (nothing executes), then replay below
+        const uint64_t c0 = consumed_, f0 = frames_, l0 = launches_;
+        const size_t p0 = prof_pending_.size();
+        cap_marks_.clear();
+        capturing_ = true;
+        g_capture_events = true;
+        cudaGraph_t graph = nullptr;
+        Status st = cuda_check(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal), "push graph capture");
+        if (st.code == CYC_OK) {
+            st = enqueue_gated(xv, yv, n, hb, hc);
+            const cudaError_t ce = cudaStreamEndCapture(cs_, &graph);
+            if (st.code == CYC_OK && ce != cudaSuccess) st = cuda_check(ce, "push graph capture");
+        }
+        capturing_ = false;
+        g_capture_events = false;
+        e->c1 = consumed_;
+        e->f1 = frames_;
+        e->launches = launches_ - l0;
+        e->marks = cap_marks_;
+        consumed_ = c0;
+        frames_ = f0;
+        launches_ = l0;
+        std::vector<ProfRec> recs(prof_pending_.begin() + p0, prof_pending_.end());
+        prof_pending_.resize(p0);
+        cudaGraphExec_t exec = nullptr;
+        if (st.code == CYC_OK && graph && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) exec = nullptr;
+        // profiled launches: find the event-record nodes of their events
+        std::vector<cudaGraphNode_t> nodes;
+        if (exec) {
+            size_t cnt = 0;
+            cudaGraphGetNodes(graph, nullptr, &cnt);
+            nodes.resize(cnt);
+            cudaGraphGetNodes(graph, nodes.data(), &cnt);
+        }
+        auto node_of = [&](cudaEvent_t ev) -> cudaGraphNode_t {
+            for (auto nd : nodes) {
+                cudaGraphNodeType t;
+                cudaEvent_t x = nullptr;
+                if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeEventRecord &&
+                    cudaGraphEventRecordNodeGetEvent(nd, &x) == cudaSuccess && x == ev)
+                    return nd;
+            }
+            return nullptr;
+        };
+        bool ok = exec != nullptr;
+        for (const auto& r : recs) {
+            PushGraph::Prof p{node_of(r.a), node_of(r.b), r.a, r.b, r.flops, r.exec_flops, r.tensor};
+            if (!p.na || !p.nb) ok = false;
+            e->prof_recs.push_back(p);
+        }
+        if (!ok) {
+            cudaGetLastError();
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+            e->prof_recs.clear();
+            for (const auto& r : recs) {
+                timed_pool_.push_back(r.a);
+                timed_pool_.push_back(r.b);
+            }
+            e->failed = true;
+            return enqueue_gated(xv, yv, n, hb, hc);
+        }
+        e->graph = graph;
+        e->exec = exec;
+    }
+    // replay: fresh profiling events per launch, then the host-side effects
+    for (const auto& p : e->prof_recs) {
+        ProfRec r{get_event_timed(), get_event_timed(), p.flops, p.exec_flops, p.tensor};
+        CK(cudaGraphExecEventRecordNodeSetEvent(e->exec, p.na, r.a));
+        CK(cudaGraphExecEventRecordNodeSetEvent(e->exec, p.nb, r.b));
+        prof_pending_.push_back(r);
+    }
+    CK(cudaGraphLaunch(e->exec, cs_));
+    consumed_ = e->c1;
+    frames_ = e->f1;
+    launches_ += e->launches;
+    for (int64_t lo : e->marks) mark_read(lo);
+    return Status::ok();
+}
+
 Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int kind) {
     const int C = c_.channels;
     const uint64_t c0 = consumed_, f0 = frames_;
@@ -1688,32 +1948,34 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
         if (want > cap_ && (double)want * C * (cross_ ? 2 : 1) * sizeof(float2) <= 4.0 * (1ull << 30))
             TRY(grow_ring(want));
     }
-    TRY(history_copy(hb, hc, true));
-    CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
     const bool gated = kind == IN_DEVICE_F32;
     if (gated) {
         // The fold's reduces commit straight into S_main behind the scan's
-        // verdict (no pending accumulator, no commit pass).  The scan runs on a
-        // side stream, co-resident with the fold kernels (HBM-bound beside an
-        // L2/tensor-bound fold); only the reduces wait for it.
-        cudaEvent_t ev_k = get_event(), ev_c = get_event();
-        CK(cudaEventRecord(ev_k, cs_));
-        CK(cudaStreamWaitEvent(vs_, ev_k, 0));
-        launches_ += launch_finite_check((const float2*)xv, (const float2*)yv, (int64_t)n, 0, C, 0, key_dev_, vs_, C,
-                                         (int64_t)n);
-        CK(cudaEventRecord(ev_c, vs_));
-        trace("scan enqueued");
-        fold_gate_ = key_dev_;
-        reduce_wait_ev_ = ev_c;
-        const Status st = fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_main_);
-        fold_gate_ = nullptr;
-        reduce_wait_ev_ = nullptr;
-        CK(cudaStreamWaitEvent(cs_, ev_c, 0));  // the key read below (and pushes that fold nothing)
-        ev_pool_.push_back(ev_k);
-        ev_pool_.push_back(ev_c);
+        // verdict (no pending accumulator, no commit pass).
+        //
+        // The call returns once the scan's verdict is on the host; the fold
+        // may still be running.  The caller's buffer stays safe: the legacy
+        // default stream (torch's default stream, and every blocking stream)
+        // is made to wait for the fold, so work enqueued there after the call
+        // -- e.g. refilling d_x -- is ordered after it.
+        const Status st = push_gated(xv, yv, n, hb, hc);
+        tl("push.end", cs_);
+        TRY(legacy_fence(false));  // every reader of the caller's buffer is on cs_ now
         trace("fold enqueued");
         TRY(st);
-    } else {
+        CK(cudaEventSynchronize(verdict_ev_));  // the verdict (the fold keeps running)
+        trace("verdict");
+        const uint64_t key = *key_host_;
+        if (key == ~0ull) return cuda_check(cudaGetLastError(), "push");
+        consumed_ = c0;  // roll back; the gated reduces skipped themselves
+        frames_ = f0;
+        TRY(history_copy(hb, hc, false));
+        CK(cudaStreamSynchronize(cs_));
+        return data_error(key / C, (int)(key % C), kind, xv, yv, n);
+    }
+    TRY(history_copy(hb, hc, true));
+    CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
+    {
         if (!S_pend_) CK(cudaMalloc(&S_pend_, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double)));
         CK(cudaMemsetAsync(S_pend_, 0, (size_t)C * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
         static const bool tr = std::getenv("CYC_TRACE") != nullptr;
@@ -1765,10 +2027,8 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
     trace("compute done");
     const uint64_t key = *key_host_;
     if (key == ~0ull) {
-        if (!gated) {
-            launch_add_f64(S_main_, S_pend_, (int64_t)C * t_pad_ * Pf_ * 4, cs_);
-            launches_ += 1;
-        }
+        launch_add_f64(S_main_, S_pend_, (int64_t)C * t_pad_ * Pf_ * 4, cs_);
+        launches_ += 1;
         return cuda_check(cudaGetLastError(), "push");
     }
     // roll back: counters, history samples; the pending fold is discarded
@@ -1802,14 +2062,15 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     }
     cudaEvent_t ev = get_event();
     CK(cudaEventRecord(ev, xs_));
+    tl("ring.end", xs_);
     bool joined = false;
     consumed_ = (uint64_t)(c1 - origin_);
     const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
+    std::vector<FoldSeg> ring_segs, user_segs;
+    const int64_t s = origin_ + (int64_t)m_minus_ + (int64_t)frames_ * N_;
     if (avail > frames_) {
-        const int64_t s = origin_ + (int64_t)m_minus_ + (int64_t)frames_ * N_;
         const int64_t e = origin_ + (int64_t)m_minus_ + (int64_t)avail * N_;
         const int64_t split = std::max(c0, c0 - (int64_t)lag_lo_);
-        std::vector<FoldSeg> ring_segs, user_segs;
         for (int ch = 0; ch < C; ++ch) {
             FoldSeg g{};
             g.w_log2 = 0.f;
@@ -1836,19 +2097,75 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
                 user_segs.push_back(g);
             }
         }
+    }
+    // The chunk's finite scan (the fold's gate) on the side stream.  When the
+    // folds are one tensor-core launch, that launch checks the samples it
+    // stages (each sample of the covered range once) and the scan covers only
+    // the rest of the chunk: the record is read from HBM once, not twice.
+    static const bool no_fuse = std::getenv("CYC_NO_FUSED_CHECK") != nullptr;
+    int64_t pa = 0, pb = 0;
+    const bool fused = !no_fuse && ring_segs.empty() && !user_segs.empty() && tc_check_plan(user_segs, pa, pb);
+    cudaEvent_t ev_c = get_event(), ev_v = get_event(), ev_f = nullptr;
+    auto scan = [&](int64_t a, int64_t b) {  // absolute [a, b) of every channel
+        if (b <= a) return;
+        launches_ += launch_finite_check(x + (a - c0), y ? y + (a - c0) : nullptr, b - a, a - c0, C, 0, key_dev_, vs_,
+                                         C, (int64_t)n);
+    };
+    tl("scan.start", vs_);
+    if (fused) {
+        bool self = true;
+        for (const auto& g : user_segs) self = self && g.x == g.y;
+        const int64_t lo = pa * Pf_ + (self ? 0 : std::max(0, f_lo_));
+        const int64_t hi = pb * Pf_ + (self ? 0 : std::min(0, f_lo_));
+        scan(c0, std::min(lo, c1));
+        scan(std::max(hi, c0), c1);
+        ev_f = get_event();
+        chk_key_ = key_dev_;
+        chk_c0_ = c0;
+        fold_done_ev_ = ev_f;
+        chk_launches_ = 0;
+    } else {
+        scan(c0, c1);
+    }
+    CK(cudaEventRecord(ev_c, vs_));
+    tl("scan.end", vs_);
+    if (!fused) {  // the verdict is the scan's: back to the host before the fold ends
+        CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, vs_));
+        CK(record_event(verdict_ev_, vs_));
+    }
+    trace("scan enqueued");
+    reduce_wait_ev_ = ev_c;
+    Status st;
+    if (avail > frames_) {
         if (!ring_segs.empty()) {  // frames straddling the previous chunk read the ring
             CK(cudaStreamWaitEvent(cs_, ev, 0));
             joined = true;
         }
-        TRY(fold(ring_segs, S));
-        TRY(fold(user_segs, S));
+        st = fold(ring_segs, S);
+        if (st.code == CYC_OK) st = fold(user_segs, S);
+        if (st.code == CYC_OK && fused && chk_launches_ != 1)
+            st = Status{CYC_ERR_CUDA, "fused finite check: the fold was not one tensor-core launch", -1};
         mark_read(s + lag_lo_);
         frames_ = avail;
     }
+    chk_key_ = nullptr;
+    fold_done_ev_ = nullptr;
+    reduce_wait_ev_ = nullptr;
+    if (fused) {  // the verdict waits for the checking fold kernel (not its reduce)
+        CK(cudaStreamWaitEvent(vs_, ev_f, 0));
+        CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, vs_));
+        CK(record_event(verdict_ev_, vs_));
+    }
+    CK(cudaEventRecord(ev_v, vs_));
+    CK(cudaStreamWaitEvent(cs_, ev_v, 0));  // joins the side stream (and orders pushes that fold nothing)
     // later ring readers on the compute stream are ordered after the history
     // writes; the fold of the user buffer above did not wait for them
     if (!joined) CK(cudaStreamWaitEvent(cs_, ev, 0));
     ev_pool_.push_back(ev);  // only after the last wait on it (get_event may re-record it)
+    ev_pool_.push_back(ev_c);
+    ev_pool_.push_back(ev_v);
+    if (ev_f) ev_pool_.push_back(ev_f);
+    TRY(st);
     return cuda_check(cudaGetLastError(), "push_device");
 }
 
@@ -1871,6 +2188,13 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
             }
         return Status::ok();
     }
+    if (is_device(out)) {  // finalize straight into the caller's table
+        TRY(legacy_fence(true));
+        tl("avg", cs_);
+        TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, (double2*)out));
+        tl("avg.end", cs_);
+        return legacy_fence(false);
+    }
     if (avg_all_len_ < (size_t)C * per) {
         CK(cudaStreamSynchronize(cs_));
         cudaFree(avg_all_dev_);
@@ -1879,7 +2203,7 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
     }
     TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, avg_all_dev_));
     CK(cudaMemcpyAsync(out, avg_all_dev_, (size_t)C * per * sizeof(double2), cudaMemcpyDefault, cs_));
-    if (!is_device(out)) CK(cudaStreamSynchronize(cs_));  // device out: stream-ordered on cyc_stream
+    CK(cudaStreamSynchronize(cs_));
     return Status::ok();
 }
 
@@ -1959,9 +2283,12 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
         }
         trace("avg finalize enqueued");
         if (dma_target(out)) {  // pinned host or device memory: one copy, no bounce
+            const bool dev = is_device(out);
+            if (dev) TRY(legacy_fence(true));
             CK(cudaMemcpyAsync(out, avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
                                cudaMemcpyDefault, cs_));
-            if (!is_device(out)) CK(cudaStreamSynchronize(cs_));  // device out: stream-ordered
+            if (dev) return legacy_fence(false);
+            CK(cudaStreamSynchronize(cs_));
             return Status::ok();
         }
         CK(cudaMemcpyAsync(tmp, avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
@@ -2065,7 +2392,59 @@ Status Engine::fold_state(void** dev_ptr, size_t* count, uint64_t* frames) {
     return Status::ok();
 }
 
+void Engine::tl(const char* name, cudaStream_t s) {
+    if (!timeline_on()) return;
+    if (tl_steps_.empty()) tl_steps_.emplace_back();
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    tl_steps_.back().push_back({name, e});
+}
+
+void Engine::tl_resolve(bool wait) {
+    while (!tl_steps_.empty()) {
+        auto& m = tl_steps_.front();
+        bool ready = true;
+        for (auto& k : m) {
+            if (wait) cudaEventSynchronize(k.ev);
+            if (cudaEventQuery(k.ev) != cudaSuccess) ready = false;
+        }
+        if (!ready) return;
+        for (auto& k : m) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, m[0].ev, k.ev);
+            size_t i = 0;
+            while (i < tl_acc_.size() && tl_acc_[i].first != k.name) ++i;
+            if (i == tl_acc_.size()) tl_acc_.push_back({k.name, {0.0, 0}});
+            tl_acc_[i].second.first += ms * 1e3;
+            tl_acc_[i].second.second += 1;
+        }
+        for (auto& k : m) cudaEventDestroy(k.ev);
+        tl_steps_.pop_front();
+    }
+}
+
+// Stream order with the caller's legacy default stream (torch's default
+// stream; every blocking stream syncs with it): before = our compute stream
+// (and, with copy, the copy stream) waits for the caller's work enqueued so
+// far; otherwise the caller's later work waits for ours on the compute stream.
+Status Engine::legacy_fence(bool before, bool copy) {
+    cudaEvent_t ev = get_event();
+    CK(cudaEventRecord(ev, before ? cudaStreamLegacy : cs_));
+    if (before) {
+        CK(cudaStreamWaitEvent(cs_, ev, 0));
+        if (copy) CK(cudaStreamWaitEvent(xs_, ev, 0));
+    } else {
+        CK(cudaStreamWaitEvent(cudaStreamLegacy, ev, 0));
+    }
+    ev_pool_.push_back(ev);
+    return Status::ok();
+}
+
 Status Engine::set_frames(uint64_t frames) {
+    // the caller's in-place reduction of the fold state (fold_state) was
+    // enqueued on the legacy default stream or a stream it waits for
+    TRY(legacy_fence(true));
     frames_ = frames;
     avg_cache_frames_ = ~0ull;
     return Status::ok();
@@ -2073,6 +2452,11 @@ Status Engine::set_frames(uint64_t frames) {
 
 Status Engine::reset() {
     CK(cudaSetDevice(c_.device));
+    if (timeline_on()) {
+        tl_resolve(false);
+        tl_steps_.emplace_back();
+        tl("reset", cs_);
+    }
     // Order both streams after everything already enqueued on either (ring
     // readers / writers of the old stream) without blocking the host.
     {

@@ -135,7 +135,64 @@ private:
     Status ensure_staging();
     Status ingest_piece(const void* xv, const void* yv, size_t n, size_t off, size_t len, int kind, bool pinned);
     Status history_copy(int64_t a, int64_t b, bool save);
+    Status legacy_fence(bool before, bool copy = false);
+    // CYC_TIMELINE=1: timed events at named points of each step (reset to
+    // reset), mean offsets printed at destruction (diagnostics)
+    struct TlMark {
+        const char* name;
+        cudaEvent_t ev;
+    };
+    std::deque<std::vector<TlMark>> tl_steps_;
+    std::vector<std::pair<std::string, std::pair<double, int>>> tl_acc_;
+    void tl(const char* name, cudaStream_t s);
+    void tl_resolve(bool wait);
     Status push_speculative(const void* xv, const void* yv, size_t n, int kind);
+    // Device-resident block push: history save, key reset, the finite scan +
+    // verdict copy on vs_, the fold (reduces gated on the verdict) -- enqueued
+    // directly, or replayed as one CUDA graph when the same (buffer, length,
+    // stream position) repeats (the ~20 launches/copies/event edges cost ~70
+    // us of host time per push; one graph launch costs a few).
+    Status enqueue_gated(const void* xv, const void* yv, size_t n, int64_t hb, int64_t hc);
+    Status push_gated(const void* xv, const void* yv, size_t n, int64_t hb, int64_t hc);
+    struct PushGraph {
+        // key
+        const void* x = nullptr;
+        const void* y = nullptr;
+        size_t n = 0;
+        uint64_t c0 = 0, f0 = 0;
+        int64_t origin = 0, cap = 0;
+        const float2* rx = nullptr;
+        const float2* ry = nullptr;
+        const double* S = nullptr;
+        const float* partials = nullptr;
+        bool cross = false, prof = false;
+        // state
+        int seen = 0;
+        bool failed = false;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t c1 = 0, f1 = 0, launches = 0;
+        std::vector<int64_t> marks;  // mark_read positions, recorded after each replay
+        struct Prof {
+            cudaGraphNode_t na, nb;  // event-record nodes around a profiled fold launch
+            cudaEvent_t a0, b0;      // the events captured into them
+            double flops, exec_flops;
+            bool tensor;
+        };
+        std::vector<Prof> prof_recs;
+    };
+    std::vector<PushGraph> push_graphs_;
+    // fused finite check of the current gated push (see fold_device_chunk)
+    unsigned long long* chk_key_ = nullptr;
+    int64_t chk_c0_ = 0;
+    int chk_launches_ = 0;
+    cudaEvent_t fold_done_ev_ = nullptr;
+    bool tc_interior(const FoldSeg& g, int64_t& pa, int64_t& pb) const;
+    bool tc_check_plan(const std::vector<FoldSeg>& segs, int64_t& pa, int64_t& pb) const;
+    bool capturing_ = false;
+    std::vector<int64_t> cap_marks_;
+    cudaEvent_t verdict_ev_ = nullptr;  // the verdict copy of the last gated push landed
+    void drop_push_graph(PushGraph& g);
     Status fold_device_chunk(const float2* x, const float2* y, size_t n, double* S);
     Status deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const std::vector<int>& chans,
                    cyc_frame_sink sink, void* user, bool& stop, const double2* tables);
@@ -282,6 +339,17 @@ private:
         bool valid = false;
     };
     MapCache map_cache_[TC_SEGS];
+    // device copies of recent tensor-core tile tables: a repeated plan
+    // launches with the small TcDev parameter block
+    struct TileCache {
+        std::vector<FoldTile> host;
+        FoldTile* dev = nullptr;
+        FoldTile* pin = nullptr;
+        cudaEvent_t ev = nullptr;  // the upload from `pin` completed
+    };
+    TileCache tile_cache_[4];
+    int tile_cache_next_ = 0;
+    const FoldTile* cached_tiles(const FoldTile* t, int nt);
     const unsigned long long* fold_gate_ = nullptr;  // set while a device chunk folds straight into S_main
     float2* hist_bak_ = nullptr;
     size_t hist_cap_ = 0;

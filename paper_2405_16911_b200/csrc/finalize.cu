@@ -8,7 +8,8 @@
 // proj/src/kernels.cpp:103-114, generalised to every alpha on the grid).
 //
 // Two paths, both fp64:
-//   * radix-2 DIT FFT in shared memory (Pf a power of two <= 8192): replaces
+//   * radix-2 DIT FFT in shared memory (Pf a power of two <= 8192; levels
+//     fused in pairs, twiddles in shared memory): replaces
 //     the reference's per-lag Fft::forward (proj/src/fft.cpp:44-87);
 //   * direct DFT with an exact (bin*r mod Pf) twiddle index, for small alpha
 //     sets or non-power-of-two periods (proj/src/fft.cpp:89-100 analogue).
@@ -21,37 +22,66 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-__device__ __forceinline__ double2 combine(const double* s, int flag_bit) {
+__device__ __forceinline__ double2 combine(const double* s, int flag_bit) {  // s: 4 values
     // s = (c0, c1, c2, c3) = (sum xr*yr, sum xi*yr, sum xr*yi, sum xi*yi)
     return flag_bit == 0 ? make_double2(s[0] + s[3], s[1] - s[2])   // x * conj(y)
                          : make_double2(s[0] - s[3], s[1] + s[2]);  // x * y
 }
 
-// grid: (n_rows, n_flag_tables); one CTA per (row, flag).
+// grid: (n_rows, n_flag_tables); one CTA per (row, flag).  Radix-2 stages are
+// executed in pairs: each thread keeps the four points of two consecutive
+// butterfly levels in registers (exactly the radix-2 arithmetic, one barrier
+// per pair), with the Pf/2-entry twiddle table staged in shared memory.
 __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
-    extern __shared__ double2 buf[];
-    __shared__ FinalRow s_row;  // descriptors may be in mapped host memory: read once
+    extern __shared__ double2 buf[];  // Pf points, then Pf/2 twiddles
+    __shared__ FinalRow s_row;        // descriptors may be in mapped host memory: read once
+    const int Pf = L.Pf;
+    double2* tw = buf + Pf;
     if (threadIdx.x == 0) s_row = L.rows[blockIdx.x];
+    for (int k = threadIdx.x; k < (Pf >> 1); k += blockDim.x) tw[k] = __ldg(L.tw + k);
     __syncthreads();
     const FinalRow row = s_row;
     const int fi = blockIdx.y;  // index among requested flags
     const int flag_bit = (L.flags == 2) ? 1 : fi;
-    const int Pf = L.Pf;
     const double* Srow = L.S + ((size_t)row.slot * L.t_pad + row.t_span) * (size_t)Pf * 4;
     for (int r = threadIdx.x; r < Pf; r += blockDim.x) {
         const int rev = (int)(__brev((unsigned)r) >> (32 - log2Pf));
-        buf[rev] = combine(Srow + (size_t)r * 4, flag_bit);
+        const double2 v0 = __ldg(reinterpret_cast<const double2*>(Srow) + 2 * r);
+        const double2 v1 = __ldg(reinterpret_cast<const double2*>(Srow) + 2 * r + 1);
+        const double c[4] = {v0.x, v0.y, v1.x, v1.y};
+        buf[rev] = combine(c, flag_bit);
     }
     __syncthreads();
-    for (int len = 2; len <= Pf; len <<= 1) {
+    int len = 2;
+    for (; 2 * len <= Pf; len <<= 2) {  // levels len (half h) and 2 len, fused
+        const int h = len >> 1;
+        const int ts1 = Pf / len, ts2 = ts1 >> 1;
+        for (int j = threadIdx.x; j < (Pf >> 2); j += blockDim.x) {
+            const int grp = j / h, pos = j - grp * h;
+            const int i0 = grp * 2 * len + pos;
+            double2 a = buf[i0], b = buf[i0 + h], c = buf[i0 + 2 * h], d = buf[i0 + 3 * h];
+            const double2 w1 = tw[pos * ts1];
+            double2 v = cmul(b, w1);
+            b = make_double2(a.x - v.x, a.y - v.y);
+            a = make_double2(a.x + v.x, a.y + v.y);
+            v = cmul(d, w1);
+            d = make_double2(c.x - v.x, c.y - v.y);
+            c = make_double2(c.x + v.x, c.y + v.y);
+            v = cmul(c, tw[pos * ts2]);
+            buf[i0] = make_double2(a.x + v.x, a.y + v.y);
+            buf[i0 + 2 * h] = make_double2(a.x - v.x, a.y - v.y);
+            v = cmul(d, tw[(pos + h) * ts2]);
+            buf[i0 + h] = make_double2(b.x + v.x, b.y + v.y);
+            buf[i0 + 3 * h] = make_double2(b.x - v.x, b.y - v.y);
+        }
+        __syncthreads();
+    }
+    if (len <= Pf) {  // odd log2 Pf: the last radix-2 level
         const int half = len >> 1;
-        const int tstep = Pf / len;
         for (int j = threadIdx.x; j < (Pf >> 1); j += blockDim.x) {
-            const int grp = j / half, pos = j - grp * half;
-            const int i0 = grp * len + pos, i1 = i0 + half;
-            const double2 w = L.tw[pos * tstep];
+            const int i0 = j, i1 = j + half;  // a single group of size Pf
             const double2 u = buf[i0];
-            const double2 v = cmul(buf[i1], w);
+            const double2 v = cmul(buf[i1], tw[j]);
             buf[i0] = make_double2(u.x + v.x, u.y + v.y);
             buf[i1] = make_double2(u.x - v.x, u.y - v.y);
         }
@@ -134,14 +164,14 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
     if (L.use_fft) {
         int lg = 0;
         while ((1 << lg) < L.Pf) ++lg;
-        const size_t smem = (size_t)L.Pf * sizeof(double2);
+        const size_t smem = (size_t)L.Pf * 3 / 2 * sizeof(double2);
         static bool attr_set = false;
         if (!attr_set) {
             cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 8192 * (int)sizeof(double2));
+                                 12288 * (int)sizeof(double2));
             attr_set = true;
         }
-        finalize_fft_kernel<<<dim3(L.n_rows, nflag), 512, smem, st>>>(L, lg);
+        finalize_fft_kernel<<<dim3(L.n_rows, nflag), std::min(512, std::max(32, L.Pf / 4)), smem, st>>>(L, lg);
     } else {
         finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
     }
@@ -153,7 +183,7 @@ namespace cyc {
 void prepare_finalize_kernels() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * (int)sizeof(double2));
+    cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12288 * (int)sizeof(double2));
     done = true;
 }
 }  // namespace cyc

@@ -416,16 +416,16 @@ template <int LW>
 void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, const FoldInline* inl,
               cudaEvent_t before_reduce) {
     using G = Geo<LW>;
-    if (ev0) cudaEventRecord(ev0, st);
+    if (ev0) record_event(ev0, st);
     dim3 rg((G::TB * G::RB + 255) / 256, L.n_groups);
     if (inl) {
         fold_kernel<LW, true><<<L.n_tiles, NT, G::SMEM, st>>>(L, *inl);
-        if (ev1) cudaEventRecord(ev1, st);
+        if (ev1) record_event(ev1, st);
         if (before_reduce) cudaStreamWaitEvent(st, before_reduce, 0);
         fold_reduce_kernel<true><<<rg, 256, 0, st>>>(L, G::TB, G::RB, *inl);
     } else {
         fold_kernel<LW, false><<<L.n_tiles, NT, G::SMEM, st>>>(L, NoInline{});
-        if (ev1) cudaEventRecord(ev1, st);
+        if (ev1) record_event(ev1, st);
         if (before_reduce) cudaStreamWaitEvent(st, before_reduce, 0);
         fold_reduce_kernel<false><<<rg, 256, 0, st>>>(L, G::TB, G::RB, NoInline{});
     }

@@ -121,8 +121,14 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
 // 8 fp32 of row k (two 16-byte raw chunks at ra, rb) -> one 16-byte chunk of
 // the hi and lo planes for floats 8*n8 .. 8*n8+7 (MN-major SW128: atom n/64,
 // row k, chunk ((n%64)/8) ^ (k%8)).  Shared-window addresses (LDS/STS).
-__device__ __forceinline__ void split8(uint32_t ra, uint32_t rb, int n8, int k, uint32_t hi, uint32_t lo, bool zero) {
+// check: also flag a possibly non-finite input -- an inf or NaN makes its lo
+// part (x - hi) NaN, caught by one bf16x2 FMA with zero per pair (finite
+// values give +-0).  A flag is only a hint (so is the lo = -inf of a finite
+// value that rounds to a bf16 infinity): the caller re-checks the fp32 samples.
+__device__ __forceinline__ bool split8(uint32_t ra, uint32_t rb, int n8, int k, uint32_t hi, uint32_t lo, bool zero,
+                                      bool check) {
     uint32_t h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
+    uint32_t acc = 0;
     if (!zero) {
         const float4 a = lds128(ra);
         const float4 b = lds128(rb);
@@ -133,10 +139,15 @@ __device__ __forceinline__ void split8(uint32_t ra, uint32_t rb, int n8, int k, 
             const float h0 = __uint_as_float(h[e] << 16), h1 = __uint_as_float(h[e] & 0xffff0000u);
             l[e] = pack_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
         }
+        if (check) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) asm("fma.rn.bf16x2 %0, %1, %2, %0;" : "+r"(acc) : "r"(l[e]), "r"(0u));
+        }
     }
     const uint32_t off = (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
     sts128(hi + off, h[0], h[1], h[2], h[3]);
     sts128(lo + off, l[0], l[1], l[2], l[3]);
+    return (acc & 0x7fff7fffu) != 0u;
 }
 
 // Unit u of a raw stage region (boxes of 32 floats x 16 rows): box a = u / 64;
@@ -146,21 +157,47 @@ __device__ __forceinline__ void split8(uint32_t ra, uint32_t rb, int n8, int k, 
 // and the plane writes, (4(a%2) + m) ^ k, of a quarter-warp then land on 8
 // distinct 16-byte bank groups: k1 ^ k2 = 5 has bits 0 and 2 set.
 // swz == false: rows are linear (1-D bulk copies, row pitch `pitch`).
-__device__ __forceinline__ void convert_unit(uint32_t raw, int u, bool swz, uint32_t pitch, uint32_t hi, uint32_t lo,
-                                             int rows) {
-    const int a = u >> 6, w = u & 63, l = w & 31, qd = l >> 3, pos = l & 7;
-    const int m = pos & 3;
-    const int k = 8 * (w >> 5) + ((pos >> 2) ? (qd ^ 5) : qd);
-    uint32_t ra, rb;
+struct UnitPos {
+    uint32_t ra, rb;  // shared addresses of the unit's two 16-byte raw chunks
+    int a, m, k;      // box, 8-float group, row (period within the stage)
+};
+__device__ __forceinline__ UnitPos unit_pos(uint32_t raw, int u, bool swz, uint32_t pitch) {
+    UnitPos q;
+    const int w = u & 63, l = w & 31, qd = l >> 3, pos = l & 7;
+    q.a = u >> 6;
+    q.m = pos & 3;
+    q.k = 8 * (w >> 5) + ((pos >> 2) ? (qd ^ 5) : qd);
     if (swz) {
-        const uint32_t row = raw + (uint32_t)(a * (TKB * 128) + k * 128);
-        ra = row + ((uint32_t)((2 * m) ^ (k & 7)) << 4);
-        rb = row + ((uint32_t)((2 * m + 1) ^ (k & 7)) << 4);
+        const uint32_t row = raw + (uint32_t)(q.a * (TKB * 128) + q.k * 128);
+        q.ra = row + ((uint32_t)((2 * q.m) ^ (q.k & 7)) << 4);
+        q.rb = row + ((uint32_t)((2 * q.m + 1) ^ (q.k & 7)) << 4);
     } else {
-        ra = raw + (uint32_t)k * pitch + (uint32_t)(a * 128 + m * 32);
-        rb = ra + 16;
+        q.ra = raw + (uint32_t)q.k * pitch + (uint32_t)(q.a * 128 + q.m * 32);
+        q.rb = q.ra + 16;
     }
-    split8(ra, rb, 4 * a + m, k, hi, lo, k >= rows);
+    return q;
+}
+// returns the check hint (see split8)
+__device__ __forceinline__ bool convert_unit(uint32_t raw, int u, bool swz, uint32_t pitch, uint32_t hi, uint32_t lo,
+                                             int rows, bool check) {
+    const UnitPos q = unit_pos(raw, u, swz, pitch);
+    return split8(q.ra, q.rb, 4 * q.a + q.m, q.k, hi, lo, q.k >= rows, check);
+}
+// Exact re-check of a flagged unit: samples 16a + 4m + j of the window of
+// period p + k, which starts at absolute sample (p + k) Pf + win0; atomicMin
+// of the scan's key.
+__device__ __noinline__ void check_unit_slow(const FoldLaunch& L, uint32_t raw, int u, bool swz, uint32_t pitch,
+                                             int64_t p, int64_t win0, int is_y, int slot) {
+    const UnitPos q = unit_pos(raw, u, swz, pitch);
+    const float4 A = lds128(q.ra), B = lds128(q.rb);
+    const float v[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+    for (int j = 3; j >= 0; --j) {
+        if (isfinite(v[2 * j]) && isfinite(v[2 * j + 1])) continue;
+        const int64_t abs = (p + q.k) * L.Pf + win0 + 16 * q.a + 4 * q.m + j;
+        const unsigned long long idx = (unsigned long long)(abs - L.chk_c0);
+        atomicMin(L.chk_key, (2ull * idx + (unsigned long long)is_y) * (unsigned long long)L.chk_channels +
+                                 (unsigned long long)slot);
+    }
 }
 
 template <bool SELF, class DESC>
@@ -292,6 +329,12 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         }
     } else {
         const int ct = threadIdx.x - 64;  // 0 .. 32*TNC-1
+        // fused check (lb = 0 tiles): the 128 samples of each period that this
+        // tile's residues own -- x boxes [cb0, cb0 + 8) (self: the y part of
+        // the x window; else x samples [0, 128)), and the y window
+        const bool chk = L.chk_key != nullptr && tile.lb == 0;
+        const int cb0 = SELF ? (int)(-d) / 16 : 0;
+        const int chk_y = (seg.x != seg.y) ? 1 : 0;
         for (int it = 0; it < nst; ++it) {
             const int rs = it % G::NR, ps = it % G::NP;
             mbar_wait(&full[rs], (it / G::NR) & 1);
@@ -301,12 +344,19 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             const uint32_t xh = su32(plane_ring + ps * G::PLANE);
             const uint32_t xl = xh + XPLANE;
 #pragma unroll
-            for (int u = ct; u < (XF / 32) * 64; u += 32 * TNC) convert_unit(st, u, swz, XF * 4, xh, xl, rows);
+            for (int u = ct; u < (XF / 32) * 64; u += 32 * TNC) {
+                const int a = u >> 6;  // warp-uniform
+                if (convert_unit(st, u, swz, XF * 4, xh, xl, rows, chk && a >= cb0 && a < cb0 + 8))
+                    check_unit_slow(L, st, u, swz, XF * 4, tile.p0 + (int64_t)it * TKB, r0 + d, 0, seg.slot);
+            }
             if (!SELF) {
                 const uint32_t yh = xl + XPLANE;
                 const uint32_t yl = yh + YPLANE;
 #pragma unroll
-                for (int u = ct; u < (YF / 32) * 64; u += 32 * TNC) convert_unit(st + XRAW, u, swz, YF * 4, yh, yl, rows);
+                for (int u = ct; u < (YF / 32) * 64; u += 32 * TNC)
+                    if (convert_unit(st + XRAW, u, swz, YF * 4, yh, yl, rows, chk))
+                        check_unit_slow(L, st + XRAW, u, swz, YF * 4, tile.p0 + (int64_t)it * TKB, r0, chk_y,
+                                        seg.slot);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&rawfree[rs]);  // raw slot reusable (generic reads done)
@@ -359,25 +409,28 @@ struct TcRed {
     int slot[MG];  // accumulator slot of each group's segment
 };
 
-// the fp64 reduce of fold.cu for the tensor-core tile geometry (64 lags x 128 residues)
+// The fp64 reduce of fold.cu for the tensor-core tile geometry (64 lags x 128
+// residues).  Four lanes share an output: lane quarter q sums the group's tiles
+// t0+q, t0+q+4, ... in order, then the quarters combine as (q0+q1)+(q2+q3) --
+// a fixed order, so results are reproducible bit for bit.  A warp covers 8
+// outputs x 4 tiles per load (4 full 128-byte lines).
 template <int MG>
-__global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcRed<MG> R) {
+__global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcRed<MG> R) {
     if (L.gate && *L.gate != ~0ull) return;
     const FoldGroup g = R.groups[blockIdx.y];
     const int slot = R.slot[blockIdx.y];
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // lag * TRB + residue
-    if (e >= 64 * TRB) return;
+    const int lane = threadIdx.x & 31, q = lane >> 3;
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x - lane) / 4 + (lane & 7);  // lag * TRB + residue
     const int lag = e / TRB, res = e % TRB;
     const int64_t rg = (int64_t)g.rb * TRB + res;
     const int tg = g.lb * 64 + lag;
-    if (rg >= L.Pf || tg >= L.t_pad) return;
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-    int t = g.t0;
-    for (; t + 4 <= g.t1; t += 4) {  // 4 loads in flight, fixed summation order
+    int t = g.t0 + q;
+    for (; t + 12 < g.t1; t += 16) {  // 4 loads in flight, fixed summation order
         float4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(t + u) * 64 * TRB);
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(t + 4 * u) * 64 * TRB);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             s0 += v[u].x;
@@ -386,13 +439,21 @@ __global__ void fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcRe
             s3 += v[u].w;
         }
     }
-    for (; t < g.t1; ++t) {
+    for (; t < g.t1; t += 4) {
         const float4 v = __ldcs(part + (size_t)t * 64 * TRB);
         s0 += v.x;
         s1 += v.y;
         s2 += v.z;
         s3 += v.w;
     }
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1) {
+        s0 += __shfl_down_sync(0xffffffffu, s0, o);
+        s1 += __shfl_down_sync(0xffffffffu, s1, o);
+        s2 += __shfl_down_sync(0xffffffffu, s2, o);
+        s3 += __shfl_down_sync(0xffffffffu, s3, o);
+    }
+    if (q != 0 || e >= 64 * TRB || rg >= L.Pf || tg >= L.t_pad) return;
     double* dst = L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4;
     dst[0] += s0;
     dst[1] += s1;
@@ -447,7 +508,7 @@ using TcSmall = TcDesc<160, 16, 2>;  // one or two segments, one wave of tiles
 
 template <class DESC, int MG>
 void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self, cudaStream_t st, cudaEvent_t ev0,
-               cudaEvent_t ev1, cudaEvent_t before_reduce) {
+               cudaEvent_t ev1, cudaEvent_t before_reduce, cudaEvent_t fold_done) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fold_tc_kernel<true, DESC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -456,14 +517,15 @@ void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self
                              TcGeo<false>::SMEM);
         attr = true;
     }
-    if (ev0) cudaEventRecord(ev0, st);
+    if (ev0) record_event(ev0, st);
     if (self)
         fold_tc_kernel<true, DESC><<<L.n_tiles, TNT, TcGeo<true>::SMEM, st>>>(L, D);
     else
         fold_tc_kernel<false, DESC><<<L.n_tiles, TNT, TcGeo<false>::SMEM, st>>>(L, D);
-    if (ev1) cudaEventRecord(ev1, st);
+    if (ev1) record_event(ev1, st);
+    if (fold_done) cudaEventRecord(fold_done, st);
     if (before_reduce) cudaStreamWaitEvent(st, before_reduce, 0);
-    fold_tc_reduce_kernel<MG><<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+    fold_tc_reduce_kernel<MG><<<dim3(4 * 64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
 }
 
 template <int MG>
@@ -476,9 +538,19 @@ void fill_red(TcRed<MG>& R, const TcParams& D, int ng) {
 }  // namespace
 
 void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool self, cudaStream_t st, cudaEvent_t ev0,
-                    cudaEvent_t ev1, cudaEvent_t before_reduce) {
+                    cudaEvent_t ev1, cudaEvent_t before_reduce, const FoldTile* dev_tiles, cudaEvent_t fold_done) {
     if (L.n_tiles == 0) return;
-    if (L.n_tiles <= 160 && L.n_groups <= 16 && n_segs <= 2) {
+    if (dev_tiles && L.n_groups <= 16 && n_segs <= 2) {
+        thread_local TcDev S;
+        thread_local TcRed<16> R;
+        std::memcpy(S.xmap, D.xmap, n_segs * sizeof(CUtensorMap));
+        std::memcpy(S.ymap, D.ymap, n_segs * sizeof(CUtensorMap));
+        std::memcpy(S.p_base, D.p_base, n_segs * sizeof(int64_t));
+        std::memcpy(S.segs, D.segs, n_segs * sizeof(FoldSeg));
+        S.tiles = dev_tiles;
+        fill_red(R, D, L.n_groups);
+        launch_tc(L, S, R, self, st, ev0, ev1, before_reduce, fold_done);
+    } else if (L.n_tiles <= 160 && L.n_groups <= 16 && n_segs <= 2) {
         thread_local TcSmall S;  // host staging (the launch copies it)
         thread_local TcRed<16> R;
         std::memcpy(S.xmap, D.xmap, n_segs * sizeof(CUtensorMap));
@@ -488,11 +560,11 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool sel
         std::memcpy(S.tiles, D.tiles, L.n_tiles * sizeof(FoldTile));
         std::memcpy(S.groups, D.groups, L.n_groups * sizeof(FoldGroup));
         fill_red(R, D, L.n_groups);
-        launch_tc(L, S, R, self, st, ev0, ev1, before_reduce);
+        launch_tc(L, S, R, self, st, ev0, ev1, before_reduce, fold_done);
     } else {
         thread_local TcRed<FI_GROUPS> R;
         fill_red(R, D, L.n_groups);
-        launch_tc(L, D, R, self, st, ev0, ev1, before_reduce);
+        launch_tc(L, D, R, self, st, ev0, ev1, before_reduce, fold_done);
     }
 }
 

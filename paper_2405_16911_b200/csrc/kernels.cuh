@@ -67,6 +67,13 @@ struct FoldLaunch {
     // non-null: the reduce commits only if *gate == ~0 (the chunk's finite scan,
     // stream-ordered before the fold, found nothing) -- a rejected chunk leaves S untouched
     const unsigned long long* gate;
+    // Fused finite check (tensor-core fold of a gated device chunk): non-null:
+    // the lb = 0 tiles check every sample they stage for the reduce role (each
+    // sample of the covered range exactly once) and atomicMin the scan's key,
+    // ((2 * (abs - chk_c0) + is_y) * chk_channels + slot), into *chk_key.
+    unsigned long long* chk_key;
+    long long chk_c0;
+    int chk_channels;
 };
 
 // Launch descriptors carried in the kernel parameter block (<= 32 KB since
@@ -106,14 +113,34 @@ struct alignas(64) TcDesc {
     FoldGroup groups[MG];
 };
 using TcParams = TcDesc<FI_TILES, FI_GROUPS, TC_SEGS>;
+// Small-parameter form for launches whose tile table is already in device
+// memory (a repeated plan): ~0.7 KB of parameters instead of ~6 KB.
+struct alignas(64) TcDev {
+    CUtensorMap xmap[2];
+    CUtensorMap ymap[2];
+    int64_t p_base[2];
+    FoldSeg segs[2];
+    const FoldTile* tiles;
+};
 // self: every tile's y window lies inside its x window at a 32-sample
 // boundary (x == y, d = lag_lo + 64 lb in [-64, 0], d % 32 == 0).
 // before_reduce: the reduce (not the fold) waits for this event (a gate scan on another stream).
+// dev_tiles: a device copy of D.tiles[0, L.n_tiles) (n_segs <= 2), or null.
+// fold_done: recorded after the fold kernel, before the reduce (a fused check's verdict).
 void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool self, cudaStream_t st,
-                    cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr, cudaEvent_t before_reduce = nullptr);
+                    cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr, cudaEvent_t before_reduce = nullptr,
+                    const FoldTile* dev_tiles = nullptr, cudaEvent_t fold_done = nullptr);
 // Fill D.xmap/ymap/p_base[si] for a linear segment (false: no TMA -- use the ring path).
 bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64_t rows, int Pf, int lag_lo,
                     int nlb);
+
+// Profiling events around kernel launches: plain records, or -- while a push
+// is being captured into a CUDA graph -- event-record nodes (so every replay
+// records them; the engine swaps in fresh events per replay).
+extern thread_local bool g_capture_events;
+inline cudaError_t record_event(cudaEvent_t e, cudaStream_t s) {
+    return cudaEventRecordWithFlags(e, s, g_capture_events ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
 
 void prepare_fold_kernels();      // set smem attributes (call outside stream capture)
 void prepare_finalize_kernels();

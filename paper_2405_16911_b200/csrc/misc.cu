@@ -4,6 +4,8 @@
 #include "kernels.cuh"
 
 namespace cyc {
+thread_local bool g_capture_events = false;
+
 namespace {
 
 __global__ void add_f64_kernel(double* dst, const double* src, int64_t n) {
