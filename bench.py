@@ -328,18 +328,25 @@ def run_ours(args, ws, rank, local):
     def timed(fn, k):
         barrier(ws)
         torch.cuda.synchronize(dev)
+        # events on the default stream: every push and device-out average is
+        # fenced against it (read after its earlier work, its later work waits
+        # for the engine's streams), so [e0, e1] brackets all of the K steps
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        e0.record()
         for _ in range(k):
             fn()
-        e1.record(stream)
+        e1.record()
         torch.cuda.synchronize(dev)
         barrier(ws)
         return e0.elapsed_time(e1) / k
 
     # warm-up (untimed)
     for _ in range(max(args.warmup, 0)):
+        # two device steps per round: reset alternates the accumulator buffer,
+        # and each (buffer, position) push is captured into a CUDA graph on
+        # its second occurrence -- the timed steps only replay
+        step_device()
         step_device()
         step_e2e()
     # device-resident (value)
@@ -353,7 +360,7 @@ def run_ours(args, ws, rank, local):
     # graph those events are extra graph nodes that add ~15 us per step, so
     # the value steps above run without them)
     est.profile(True)
-    for _ in range(2):  # capture the profiled push graph outside the pass
+    for _ in range(4):  # capture the profiled push graphs (both buffers) outside the pass
         step_device()
     prof0 = est.profile_read_ex()
     ms_prof = timed(step_device, args.steps)

@@ -508,8 +508,13 @@ Status Engine::init(const Cfg& cfg) {
         if (!c_.emit_frames) {
             if (use_fold_) {
                 const size_t b = (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double);
-                CK(cudaMalloc(&S_main_, b));
-                CK(cudaMemsetAsync(S_main_, 0, b, cs_));
+                for (int i = 0; i < 2; ++i) {
+                    CK(cudaMalloc(&S_buf_[i], b));
+                    CK(cudaMemsetAsync(S_buf_[i], 0, b, cs_));
+                    CK(cudaEventCreateWithFlags(&fin_ev_[i], cudaEventDisableTiming));
+                }
+                S_main_ = S_buf_[0];
+                CK(cudaStreamCreateWithFlags(&fs_, cudaStreamNonBlocking));
             } else {
                 CK(cudaMalloc(&dsum_main_, lay_all * sizeof(double2)));
                 CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
@@ -579,7 +584,14 @@ Engine::~Engine() {
     }
     cudaFree(ring_x_);
     cudaFree(ring_y_);
-    cudaFree(S_main_);
+    if (fs_) {
+        cudaStreamSynchronize(fs_);
+        cudaStreamDestroy(fs_);
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(S_buf_[i]);
+        if (fin_ev_[i]) cudaEventDestroy(fin_ev_[i]);
+    }
     cudaFree(dsum_main_);
     cudaFree(S_frames_);
     cudaFree(frames_dev_);
@@ -1152,7 +1164,8 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
 }
 
 Status Engine::finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
-                        double2* out) {
+                        double2* out, cudaStream_t st) {
+    if (!st) st = cs_;
     // The row table depends on nslots only: build and upload it once per size
     // (device memory kept for the estimator's lifetime), not per call.
     const FinalRow* drows = nullptr;
@@ -1188,7 +1201,7 @@ Status Engine::finalize(const double* S, int nslots, double scale, const std::ve
     L.stride_a = stride_a_;
     L.stride_t = stride_t_;
     L.use_fft = use_fft_ ? 1 : 0;
-    launch_finalize(L, cs_);
+    launch_finalize(L, st);
     launches_ += 1;
     return cuda_check(cudaGetLastError(), "finalize launch");
 }
@@ -1583,6 +1596,7 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     meta_mapped_now_ = false;
     CK(cudaSetDevice(c_.device));
     if (n == 0) return Status::ok();
+    TRY(wait_finalize_reads());  // a device-out average may still read S_main
     if (!xv) {
         Status s;
         s.code = CYC_ERR_USAGE;
@@ -2188,12 +2202,25 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
             }
         return Status::ok();
     }
-    if (is_device(out)) {  // finalize straight into the caller's table
-        TRY(legacy_fence(true));
-        tl("avg", cs_);
-        TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, (double2*)out));
-        tl("avg.end", cs_);
-        return legacy_fence(false);
+    if (is_device(out)) {
+        // finalize straight into the caller's table, on the finalize stream:
+        // after the folds (cs_) and the caller's default-stream work, before
+        // the caller's later default-stream work -- not before the next
+        // block's fold, which accumulates into the other S buffer
+        cudaEvent_t a = get_event(), b = get_event();
+        CK(cudaEventRecord(a, cs_));
+        CK(cudaEventRecord(b, cudaStreamLegacy));
+        CK(cudaStreamWaitEvent(fs_, a, 0));
+        CK(cudaStreamWaitEvent(fs_, b, 0));
+        ev_pool_.push_back(a);
+        ev_pool_.push_back(b);
+        tl("avg", fs_);
+        TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, (double2*)out, fs_));
+        tl("avg.end", fs_);
+        CK(cudaEventRecord(fin_ev_[S_cur_], fs_));
+        fin_live_[S_cur_] = true;
+        CK(cudaStreamWaitEvent(cudaStreamLegacy, fin_ev_[S_cur_], 0));
+        return Status::ok();
     }
     if (avg_all_len_ < (size_t)C * per) {
         CK(cudaStreamSynchronize(cs_));
@@ -2386,6 +2413,7 @@ Status Engine::fold_state(void** dev_ptr, size_t* count, uint64_t* frames) {
         return u;
     }
     CK(cudaStreamSynchronize(cs_));
+    if (fs_) CK(cudaStreamSynchronize(fs_));  // the caller may write the buffer a finalize reads
     if (dev_ptr) *dev_ptr = S_main_;
     if (count) *count = (size_t)c_.channels * t_pad_ * Pf_ * 4;
     if (frames) *frames = frames_;
@@ -2469,7 +2497,12 @@ Status Engine::reset() {
         ev_pool_.push_back(b);
     }
     const size_t lay_all = (size_t)c_.channels * nflags_ * layout_len_;
-    if (S_main_) CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
+    if (S_main_) {
+        S_cur_ ^= 1;
+        S_main_ = S_buf_[S_cur_];
+        TRY(wait_finalize_reads());
+        CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
+    }
     if (dsum_main_) CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
     if (coh_) CK(cudaMemsetAsync(coh_, 0, lay_all * sizeof(double2), cs_));
     if (mag_) CK(cudaMemsetAsync(mag_, 0, lay_all * sizeof(double), cs_));
@@ -2489,6 +2522,15 @@ Status Engine::synchronize() {
     CK(cudaSetDevice(c_.device));
     CK(cudaStreamSynchronize(xs_));
     CK(cudaStreamSynchronize(cs_));
+    if (fs_) CK(cudaStreamSynchronize(fs_));
+    return Status::ok();
+}
+
+Status Engine::wait_finalize_reads() {
+    if (fin_live_[S_cur_]) {
+        CK(cudaStreamWaitEvent(cs_, fin_ev_[S_cur_], 0));
+        fin_live_[S_cur_] = false;
+    }
     return Status::ok();
 }
 

@@ -121,7 +121,7 @@ private:
     bool tc_capable_ = false;  // sm_100 device (tcgen05)
     // Finalize slots [0, nslots) of S into out tables (out_block = slot) with per-slot scale.
     Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
-                    double2* out);
+                    double2* out, cudaStream_t st = nullptr);
     // Direct contraction of segs into out tables (out_block = seg.out_block).
     Status direct(const std::vector<DirectSeg>& segs, double scale, double2* out);
 
@@ -257,6 +257,14 @@ private:
     int64_t cap_ = 0, Q_ = 0;
     uint64_t mask_ = 0;
     double* S_main_ = nullptr;        // block fold accumulators [channels][t_pad][Pf][4]
+    // S_main_ alternates between two buffers at each reset, so a device-out
+    // average's finalize (on fs_) of one block overlaps the next block's fold
+    double* S_buf_[2] = {nullptr, nullptr};
+    int S_cur_ = 0;
+    cudaStream_t fs_ = nullptr;       // finalize stream of device-out averages
+    cudaEvent_t fin_ev_[2] = {};      // last finalize that read S_buf_[i]
+    bool fin_live_[2] = {};
+    Status wait_finalize_reads();     // cs_ after pending finalizes of the current buffer
     double2* dsum_main_ = nullptr;    // block direct sums [channels][nflags][layout]
     double* S_frames_ = nullptr;      // per-frame folds
     size_t S_frames_slots_ = 0;
