@@ -46,7 +46,16 @@ constexpr int YRAW = TKB * YF * 4;      // 16 KB
 constexpr int ATOM = TKB * 128;         // one MN atom column of a plane: 64 bf16 x 16 rows
 constexpr int XPLANE = TKB * XF * 2;    // 12 KB: 6 atoms
 constexpr int YPLANE = TKB * YF * 2;    // 8 KB: 4 atoms
-constexpr int TNC = 12;                 // converter / epilogue warps (warps 2 .. TNC+1), a multiple of 4
+#ifndef TC_TNC
+#define TC_TNC 12
+#endif
+#ifndef TC_NR_SELF
+#define TC_NR_SELF 5
+#endif
+#ifndef TC_NP_SELF
+#define TC_NP_SELF 4
+#endif
+constexpr int TNC = TC_TNC;             // converter / epilogue warps (warps 2 .. TNC+1), a multiple of 4
 constexpr int TNT = 64 + 32 * TNC;      // + warp 0 producer, warp 1 MMA issuer
 // Two rings: raw fp32 stages (producer -> converters, freed after conversion)
 // and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).
@@ -54,8 +63,8 @@ template <bool SELF>
 struct TcGeo {
     static constexpr int RAW = SELF ? XRAW : XRAW + YRAW;
     static constexpr int PLANE = SELF ? 2 * XPLANE : 2 * XPLANE + 2 * YPLANE;
-    static constexpr int NR = SELF ? 5 : 3;
-    static constexpr int NP = SELF ? 4 : 2;
+    static constexpr int NR = SELF ? TC_NR_SELF : 3;
+    static constexpr int NP = SELF ? TC_NP_SELF : 2;
     static constexpr int SMEM = NR * RAW + NP * PLANE + 1024;
     static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
 };
