@@ -181,7 +181,7 @@ def measured_peaks():
         return None
 
 
-def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int) -> dict:
+def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lags: int = 64) -> dict:
     """The dominant kernel (the fold) from CUDA-event profiles on its stream.
     achieved = ALGORITHMIC flops (8 per requested lag x folded sample: 4 FMAs
     give both flags) / launch duration.  Tensor-core folds also report the
@@ -203,6 +203,15 @@ def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int) -> 
         mp = measured_peaks()
         peak = mp["bf16_tflops"] if mp and mp.get("bf16_tflops") else 1590.0
         ex_rate = exe / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+        # the same launches against HBM: 8 algorithmic bytes per folded sample
+        # (the record read once); algorithmic intensity 8*T/8 = T flop/B
+        samples = alg / (8.0 * max(1, lags))
+        hbm = mp.get("hbm_gbs") if mp else None
+        gbs = 8.0 * samples / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        common["hbm_view"] = {"achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm if hbm else None,
+                              "algorithmic_bytes_per_launch": 8.0 * samples,
+                              "note": "algorithmic intensity = lags flop/B, below the bf16 ridge (~250 flop/B): "
+                                      "the record's HBM read bounds the ideal fold"}
         return {"bound": "tensor", "kernel": "fold_tc_kernel (tcgen05 bf16x3 banded Gram product)",
                 "achieved": rate, "peak": peak, "frac": rate / peak, **common,
                 "executed_tflops": ex_rate, "executed_frac": ex_rate / peak,
@@ -625,7 +634,8 @@ def run_config(args, ws, rank, local):
     if step_dev:
         ms_e2e = timed(step_e2e, args.steps)
     ms_val = ms_dev if ms_dev is not None else ms_e2e
-    roof = roofline_block(prof0, prof1, args.steps, ms_val, dev)
+    roof = roofline_block(prof0, prof1, args.steps, ms_val, dev,
+                          lags={"c1": 31, "c3": 32, "c4": 32, "c5": 256}[name])
     line = {"metric": METRIC, "value": spec["updates"] / (ms_val * 1e-3), "unit": UNIT, "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_val, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
