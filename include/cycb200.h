@@ -144,9 +144,10 @@ int cyc_push(cyc_est* est, const cyc_cf32* x, const cyc_cf32* y, size_t n,
 int cyc_push_f64(cyc_est* est, const cyc_cf64* x, const cyc_cf64* y, size_t n,
                  cyc_frame_sink sink, void* user);
 /* Same, from samples already resident in device memory (GPU pipelines).
- * Stream order: the chunk is read after work already queued on the legacy
- * default stream (e.g. the kernel that produced it), and work queued there
- * after the call (e.g. refilling d_x) waits for every read of it.  The call
+ * Stream order: the engine's streams are blocking CUDA streams, so the chunk
+ * is read after work already queued on the legacy default stream (e.g. the
+ * kernel that produced it), and work queued there after the call (e.g.
+ * refilling d_x) waits for every read of it.  The call
  * returns once the chunk's finite check is known -- a rejected chunk returns
  * CYC_ERR_DATA with the state unchanged, as for host chunks -- while the fold
  * itself may still be running on cyc_stream(est).  Callers writing d_x from a

@@ -487,15 +487,13 @@ Status Engine::init(const Cfg& cfg) {
         CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c_.device));
         tc_capable_ = major == 10;  // tcgen05 (the library is built for sm_100a only)
     }
-    CK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
-    if (std::getenv("CYC_SCAN_PRIO")) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        CK(cudaStreamCreateWithPriority(&vs_, cudaStreamNonBlocking, hi));
-    } else {
-        CK(cudaStreamCreateWithFlags(&vs_, cudaStreamNonBlocking));
-    }
+    // Blocking streams: they synchronize implicitly with the legacy default
+    // stream (torch's default stream), so device buffers are read after the
+    // caller's earlier default-stream work and the caller's later
+    // default-stream work waits for ours -- with no fence calls per step.
+    CK(cudaStreamCreate(&cs_));
+    CK(cudaStreamCreate(&xs_));
+    CK(cudaStreamCreate(&vs_));
     // ring: pieces of Q samples per channel, four pieces per ring
     int64_t qmin = std::max<int64_t>(next_pow2((int64_t)need_ + N_), 1 << 12);
     int64_t qdef = std::max<int64_t>((1 << 21) / next_pow2(c_.channels), 1 << 12);
@@ -514,7 +512,7 @@ Status Engine::init(const Cfg& cfg) {
                     CK(cudaEventCreateWithFlags(&fin_ev_[i], cudaEventDisableTiming));
                 }
                 S_main_ = S_buf_[0];
-                CK(cudaStreamCreateWithFlags(&fs_, cudaStreamNonBlocking));
+                CK(cudaStreamCreate(&fs_));
             } else {
                 CK(cudaMalloc(&dsum_main_, lay_all * sizeof(double2)));
                 CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
@@ -1604,9 +1602,6 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         return s;
     }
     const int C = c_.channels;
-    // device chunks are read in stream order after the caller's work on the
-    // legacy default stream (e.g. the torch kernel that produced them)
-    if (kind == IN_DEVICE_F32) TRY(legacy_fence(true, true));
     const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
     // Small chunks (< 1 MiB) are copied into our pinned staging even when the
     // caller's memory is pinned: a host memcpy is cheaper than the stream sync
@@ -1974,7 +1969,6 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
         // -- e.g. refilling d_x -- is ordered after it.
         const Status st = push_gated(xv, yv, n, hb, hc);
         tl("push.end", cs_);
-        TRY(legacy_fence(false));  // every reader of the caller's buffer is on cs_ now
         trace("fold enqueued");
         TRY(st);
         CK(cudaEventSynchronize(verdict_ev_));  // the verdict (the fold keeps running)
@@ -2203,23 +2197,19 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
         return Status::ok();
     }
     if (is_device(out)) {
-        // finalize straight into the caller's table, on the finalize stream:
-        // after the folds (cs_) and the caller's default-stream work, before
-        // the caller's later default-stream work -- not before the next
-        // block's fold, which accumulates into the other S buffer
-        cudaEvent_t a = get_event(), b = get_event();
+        // finalize straight into the caller's table, on the finalize stream
+        // (blocking: ordered with the caller's default-stream work both ways):
+        // after the folds on cs_, but not before the next block's fold, which
+        // accumulates into the other S buffer
+        cudaEvent_t a = get_event();
         CK(cudaEventRecord(a, cs_));
-        CK(cudaEventRecord(b, cudaStreamLegacy));
         CK(cudaStreamWaitEvent(fs_, a, 0));
-        CK(cudaStreamWaitEvent(fs_, b, 0));
         ev_pool_.push_back(a);
-        ev_pool_.push_back(b);
         tl("avg", fs_);
         TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, (double2*)out, fs_));
         tl("avg.end", fs_);
         CK(cudaEventRecord(fin_ev_[S_cur_], fs_));
         fin_live_[S_cur_] = true;
-        CK(cudaStreamWaitEvent(cudaStreamLegacy, fin_ev_[S_cur_], 0));
         return Status::ok();
     }
     if (avg_all_len_ < (size_t)C * per) {
@@ -2310,11 +2300,9 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
         }
         trace("avg finalize enqueued");
         if (dma_target(out)) {  // pinned host or device memory: one copy, no bounce
-            const bool dev = is_device(out);
-            if (dev) TRY(legacy_fence(true));
             CK(cudaMemcpyAsync(out, avg_dev_ + (size_t)fi * layout_len_, layout_len_ * sizeof(double2),
                                cudaMemcpyDefault, cs_));
-            if (dev) return legacy_fence(false);
+            if (is_device(out)) return Status::ok();  // stream-ordered (cs_ is a blocking stream)
             CK(cudaStreamSynchronize(cs_));
             return Status::ok();
         }
@@ -2452,27 +2440,10 @@ void Engine::tl_resolve(bool wait) {
     }
 }
 
-// Stream order with the caller's legacy default stream (torch's default
-// stream; every blocking stream syncs with it): before = our compute stream
-// (and, with copy, the copy stream) waits for the caller's work enqueued so
-// far; otherwise the caller's later work waits for ours on the compute stream.
-Status Engine::legacy_fence(bool before, bool copy) {
-    cudaEvent_t ev = get_event();
-    CK(cudaEventRecord(ev, before ? cudaStreamLegacy : cs_));
-    if (before) {
-        CK(cudaStreamWaitEvent(cs_, ev, 0));
-        if (copy) CK(cudaStreamWaitEvent(xs_, ev, 0));
-    } else {
-        CK(cudaStreamWaitEvent(cudaStreamLegacy, ev, 0));
-    }
-    ev_pool_.push_back(ev);
-    return Status::ok();
-}
-
 Status Engine::set_frames(uint64_t frames) {
-    // the caller's in-place reduction of the fold state (fold_state) was
-    // enqueued on the legacy default stream or a stream it waits for
-    TRY(legacy_fence(true));
+    // (the caller's in-place reduction of the fold state, e.g. an NCCL
+    // all-reduce the default stream waits for, precedes our later work on the
+    // blocking compute stream)
     frames_ = frames;
     avg_cache_frames_ = ~0ull;
     return Status::ok();

@@ -135,7 +135,6 @@ private:
     Status ensure_staging();
     Status ingest_piece(const void* xv, const void* yv, size_t n, size_t off, size_t len, int kind, bool pinned);
     Status history_copy(int64_t a, int64_t b, bool save);
-    Status legacy_fence(bool before, bool copy = false);
     // CYC_TIMELINE=1: timed events at named points of each step (reset to
     // reset), mean offsets printed at destruction (diagnostics)
     struct TlMark {
