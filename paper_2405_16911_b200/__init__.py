@@ -571,13 +571,20 @@ class CyclicCorrelator:
         table is written stream-ordered on `stream()`, and work later queued
         on the default stream (torch's) waits for it -- from other streams,
         call `synchronize()` first."""
+        last = getattr(self, "_avg_dev_out", None)
+        if last is not None and last[0] is out and (not hasattr(out, "data_ptr") or out.data_ptr() == last[1]):
+            # the device table validated last time (same object, same storage)
+            self._check(self._L.cyc_average_all(self._h, int(mode), last[1]))
+            return out
         nf = int(self._L.cyc_num_flags(self._h))
         shape = (self._cfg.channels, nf, layout_len(self._layout))
         cai = getattr(out, "__cuda_array_interface__", None)
         if cai is not None:
             if tuple(cai["shape"]) != shape or cai["typestr"] not in ("<c16",) or cai.get("strides") not in (None,):
                 raise UsageError(f"device out must be a contiguous complex128 array of shape {shape}")
-            self._check(self._L.cyc_average_all(self._h, int(mode), int(cai["data"][0])))
+            ptr = int(cai["data"][0])
+            self._avg_dev_out = (out, ptr)
+            self._check(self._L.cyc_average_all(self._h, int(mode), ptr))
             return out
         if out is None:
             out = np.empty(shape, dtype=np.complex128)

@@ -1594,7 +1594,10 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     meta_mapped_now_ = false;
     CK(cudaSetDevice(c_.device));
     if (n == 0) return Status::ok();
-    TRY(wait_finalize_reads());  // a device-out average may still read S_main
+    if (kind == IN_DEVICE_F32 && !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_)
+        TRY(wait_finalize_reads());  // a device-out average may still read S_main (cleared in enqueue_gated)
+    else
+        TRY(flush_clear());
     if (!xv) {
         Status s;
         s.code = CYC_ERR_USAGE;
@@ -1696,8 +1699,18 @@ Status Engine::ensure_staging() {
 
 // Copy samples [off, off+len) of every channel into the rings at absolute
 // consumed_ + [0, len), on the copy stream; the compute stream waits for it.
+void Engine::order_copy_after_compute() {
+    if (!xs_after_cs_) return;
+    cudaEvent_t e = get_event();
+    cudaEventRecord(e, cs_);
+    cudaStreamWaitEvent(xs_, e, 0);
+    ev_pool_.push_back(e);
+    xs_after_cs_ = false;
+}
+
 Status Engine::ingest_piece(const void* xv, const void* yv, size_t n, size_t off, size_t len, int kind, bool pinned) {
     const int C = c_.channels;
+    order_copy_after_compute();
     const int64_t abs0 = origin_ + (int64_t)consumed_;
     wait_ring_free(abs0 + (int64_t)len);
     if (kind == IN_DEVICE_F32) {
@@ -1799,6 +1812,8 @@ Status Engine::history_copy(int64_t a, int64_t b, bool save) {
 }
 
 Status Engine::enqueue_gated(const void* xv, const void* yv, size_t n, int64_t hb, int64_t hc) {
+    if (pending_clear_)  // the reset's clear (the caller drops the flag once this is enqueued)
+        CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
     TRY(history_copy(hb, hc, true));
     CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
     // fork the side (scan) and copy streams off the compute stream; the scan
@@ -1808,6 +1823,7 @@ Status Engine::enqueue_gated(const void* xv, const void* yv, size_t n, int64_t h
     CK(cudaEventRecord(ev_k, cs_));
     CK(cudaStreamWaitEvent(vs_, ev_k, 0));
     CK(cudaStreamWaitEvent(xs_, ev_k, 0));
+    xs_after_cs_ = false;
     ev_pool_.push_back(ev_k);
     fold_gate_ = key_dev_;
     const Status st = fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_main_);
@@ -1846,11 +1862,12 @@ Status Engine::push_gated(const void* xv, const void* yv, size_t n, int64_t hb, 
     k.partials = partials_;
     k.cross = cross_;
     k.prof = prof_;
+    k.clear = pending_clear_;
     PushGraph* e = nullptr;
     for (auto& g : push_graphs_)
         if (g.x == k.x && g.y == k.y && g.n == k.n && g.c0 == k.c0 && g.f0 == k.f0 && g.origin == k.origin &&
             g.cap == k.cap && g.rx == k.rx && g.ry == k.ry && g.S == k.S && g.partials == k.partials &&
-            g.cross == k.cross && g.prof == k.prof)
+            g.cross == k.cross && g.prof == k.prof && g.clear == k.clear)
             e = &g;
     if (!e) {  // first sighting: run directly (it also sizes every buffer the capture will bake in)
         if (push_graphs_.size() >= 4) {
@@ -1968,6 +1985,7 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
         // is made to wait for the fold, so work enqueued there after the call
         // -- e.g. refilling d_x -- is ordered after it.
         const Status st = push_gated(xv, yv, n, hb, hc);
+        pending_clear_ = false;  // enqueued (or replayed) with the push
         tl("push.end", cs_);
         trace("fold enqueued");
         TRY(st);
@@ -2185,6 +2203,7 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
 // launch and one D2H for multi-channel block mode.
 Status Engine::average_all(int avg_mode, cyc_cf64* out) {
     CK(cudaSetDevice(c_.device));
+    TRY(flush_clear());
     const int C = c_.channels;
     const size_t per = (size_t)nflags_ * layout_len_;
     const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
@@ -2227,6 +2246,7 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
 Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
     trace(nullptr);
     CK(cudaSetDevice(c_.device));
+    TRY(flush_clear());
     Status u;
     u.code = CYC_ERR_USAGE;
     if (frames_ == 0) {
@@ -2394,6 +2414,7 @@ Status Engine::profile_read(uint64_t* launches, double* ms, double* flops, doubl
 }
 
 Status Engine::fold_state(void** dev_ptr, size_t* count, uint64_t* frames) {
+    TRY(flush_clear());
     if (!S_main_) {
         Status u;
         u.code = CYC_ERR_USAGE;
@@ -2456,23 +2477,16 @@ Status Engine::reset() {
         tl_steps_.emplace_back();
         tl("reset", cs_);
     }
-    // Order both streams after everything already enqueued on either (ring
-    // readers / writers of the old stream) without blocking the host.
-    {
-        cudaEvent_t a = get_event(), b = get_event();
-        CK(cudaEventRecord(a, cs_));
-        CK(cudaEventRecord(b, xs_));
-        CK(cudaStreamWaitEvent(xs_, a, 0));
-        CK(cudaStreamWaitEvent(cs_, b, 0));
-        ev_pool_.push_back(a);
-        ev_pool_.push_back(b);
-    }
+    // The read marks are dropped below, so the copy stream's next ring write
+    // must first wait for every reader already queued on the compute stream
+    // (done lazily by order_copy_after_compute).  Every copy-stream write is
+    // already joined into the compute stream before its push returns.
+    xs_after_cs_ = true;
     const size_t lay_all = (size_t)c_.channels * nflags_ * layout_len_;
-    if (S_main_) {
+    if (S_main_) {  // cleared by the next call that touches it (a device push captures the clear)
         S_cur_ ^= 1;
         S_main_ = S_buf_[S_cur_];
-        TRY(wait_finalize_reads());
-        CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
+        pending_clear_ = true;
     }
     if (dsum_main_) CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
     if (coh_) CK(cudaMemsetAsync(coh_, 0, lay_all * sizeof(double2), cs_));
@@ -2494,6 +2508,14 @@ Status Engine::synchronize() {
     CK(cudaStreamSynchronize(xs_));
     CK(cudaStreamSynchronize(cs_));
     if (fs_) CK(cudaStreamSynchronize(fs_));
+    return Status::ok();
+}
+
+Status Engine::flush_clear() {
+    if (!pending_clear_) return Status::ok();
+    TRY(wait_finalize_reads());
+    CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
+    pending_clear_ = false;
     return Status::ok();
 }
 

@@ -164,7 +164,7 @@ private:
         const float2* ry = nullptr;
         const double* S = nullptr;
         const float* partials = nullptr;
-        bool cross = false, prof = false;
+        bool cross = false, prof = false, clear = false;
         // state
         int seen = 0;
         bool failed = false;
@@ -264,6 +264,8 @@ private:
     cudaEvent_t fin_ev_[2] = {};      // last finalize that read S_buf_[i]
     bool fin_live_[2] = {};
     Status wait_finalize_reads();     // cs_ after pending finalizes of the current buffer
+    bool pending_clear_ = false;      // reset's zeroing of S_main_, deferred to its next use
+    Status flush_clear();
     double2* dsum_main_ = nullptr;    // block direct sums [channels][nflags][layout]
     double* S_frames_ = nullptr;      // per-frame folds
     size_t S_frames_slots_ = 0;
@@ -318,6 +320,8 @@ private:
     cudaEvent_t get_event_timed();
     void mark_read(int64_t lo);
     void wait_ring_free(int64_t abs_end);
+    bool xs_after_cs_ = false;  // set by reset: the next copy-stream write waits for the compute stream
+    void order_copy_after_compute();
 
     // ---- profiling ----
     struct ProfRec {
