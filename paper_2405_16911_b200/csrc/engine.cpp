@@ -825,15 +825,16 @@ bool Engine::tc_interior(const FoldSeg& g, int64_t& pa, int64_t& pb) const {
     return g.n_end > g.n_start && g.vec && g.w_log2 == 0.f && pb - pa >= 192;
 }
 
-// A device chunk's folds qualify for the fused finite check when they are
-// exactly one tensor-core launch: every segment tensor-core eligible with the
-// same interior [pa, pb), one segment batch, one tile kind (self or not) for
-// every lag block, and the groups and minimum tiles within one launch.
+// A device chunk's folds qualify for the fused finite check when the first
+// tensor-core launch can hold every lb = 0 group: every segment tensor-core
+// eligible with the same interior [pa, pb), one segment batch, one tile kind
+// (x == y or not) for all segments, and the lb = 0 groups' minimum tiles
+// within one launch.  Later launches (other lag blocks) follow it.
 bool Engine::tc_check_plan(const std::vector<FoldSeg>& segs_in, int64_t& pa, int64_t& pb) const {
     static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;
     if (no_tc || t_pad_ < 32 || Pf_ % 128 != 0 || !tc_capable_ || segs_in.empty()) return false;
-    const int nrb = (int)(Pf_ / 128), nlb = (t_pad_ + 63) / 64;
-    if (segs_in.size() > (size_t)TC_SEGS || segs_in.size() * nrb * nlb > (size_t)FI_GROUPS) return false;
+    const int nrb = (int)(Pf_ / 128);
+    if (segs_in.size() > (size_t)TC_SEGS || segs_in.size() * nrb > (size_t)FI_GROUPS) return false;
     for (size_t i = 0; i < segs_in.size(); ++i) {
         FoldSeg g = segs_in[i];
         g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
@@ -842,17 +843,11 @@ bool Engine::tc_check_plan(const std::vector<FoldSeg>& segs_in, int64_t& pa, int
         if (i == 0) {
             pa = a;
             pb = b;
-        } else if (a != pa || b != pb) {
+        } else if (a != pa || b != pb || (g.x == g.y) != (segs_in[0].x == segs_in[0].y)) {
             return false;
         }
-        for (int lb = 0; lb < nlb; ++lb) {
-            const int64_t d = f_lo_ + 64 * (int64_t)lb;
-            const bool self = g.x == g.y && d <= 0 && -d <= 64 && (-d) % 32 == 0;
-            const bool self0 = segs_in[0].x == segs_in[0].y && f_lo_ <= 0 && -f_lo_ <= 64 && (-f_lo_) % 32 == 0;
-            if (self != self0) return false;
-        }
     }
-    return (int64_t)segs_in.size() * nrb * nlb * ceil_div(pb - pa, (int64_t)2048) <= FI_TILES;
+    return (int64_t)segs_in.size() * nrb * ceil_div(pb - pa, (int64_t)2048) <= FI_TILES;
 }
 
 Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<FoldSeg>& rest) {
@@ -963,7 +958,17 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         const int64_t d = f_lo_ + 64 * (int64_t)gr.lb;
         return tsegs[gr.seg].x == tsegs[gr.seg].y && d <= 0 && -d <= 64 && (-d) % 32 == 0;
     };
-    std::stable_partition(groups.begin(), groups.end(), is_self);
+    // fused check: the checking launch goes first and holds every lb = 0
+    // group (its tiles stage each covered sample once), so every reduce of
+    // the push runs after the check
+    size_t n_lb0 = 0;
+    if (chk_key_) {
+        n_lb0 = (size_t)(std::stable_partition(groups.begin(), groups.end(), [](const G& g) { return g.lb == 0; }) -
+                         groups.begin());
+        std::stable_partition(groups.begin() + n_lb0, groups.end(), is_self);
+    } else {
+        std::stable_partition(groups.begin(), groups.end(), is_self);
+    }
     size_t g0 = 0;
     while (g0 < groups.size()) {
         // one launch: up to FI_GROUPS groups of one kind, tiles ~ whole waves of 1 CTA/SM
@@ -1012,10 +1017,12 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         L.S = S;
         L.overwrite = 0;
         L.gate = fold_gate_;
-        L.chk_key = chk_key_;
+        const bool chk = chk_key_ && g0 == 0;
+        L.chk_key = chk ? chk_key_ : nullptr;
         L.chk_c0 = chk_c0_;
         L.chk_channels = c_.channels;
-        if (chk_key_) ++chk_launches_;
+        if (chk) chk_ok_ = ng >= n_lb0;
+        cudaEvent_t fold_done = chk ? fold_done_ev_ : nullptr;
         const FoldTile* dt = (tsegs.size() <= 2 && ng <= 16) ? cached_tiles(tcp_->tiles, nt) : nullptr;
         if (prof_) {
             // executed: 2 accumulators x 3 MMAs (M=128, N=256, K=16) per 16-period stage
@@ -1023,7 +1030,7 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
             for (int t = 0; t < nt; ++t)
                 exec += (double)ceil_div(tcp_->tiles[t].p1 - tcp_->tiles[t].p0, 16) * 6.0 * 2.0 * 128 * 256 * 16;
             ProfRec r{get_event_timed(), get_event_timed(), launch_flops, exec, true};
-            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b, reduce_wait_ev_, dt, fold_done_ev_);
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, r.a, r.b, reduce_wait_ev_, dt, fold_done);
             prof_pending_.push_back(r);
         } else {
             trace("tc maps encoded");
@@ -1034,7 +1041,7 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
                 cudaEventCreate(&b);
                 tl_steps_.back().push_back({"tc.fold.end", b});
             }
-            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, a, b, reduce_wait_ev_, dt, fold_done_ev_);
+            launch_fold_tc(L, *tcp_, (int)tsegs.size(), self, cs_, a, b, reduce_wait_ev_, dt, fold_done);
             tl("tc.reduce.end", cs_);
             trace("tc launched");
         }
@@ -2149,7 +2156,7 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
         chk_key_ = key_dev_;
         chk_c0_ = c0;
         fold_done_ev_ = ev_f;
-        chk_launches_ = 0;
+        chk_ok_ = false;
     } else {
         scan(c0, c1);
     }
@@ -2169,8 +2176,8 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
         }
         st = fold(ring_segs, S);
         if (st.code == CYC_OK) st = fold(user_segs, S);
-        if (st.code == CYC_OK && fused && chk_launches_ != 1)
-            st = Status{CYC_ERR_CUDA, "fused finite check: the fold was not one tensor-core launch", -1};
+        if (st.code == CYC_OK && fused && !chk_ok_)
+            st = Status{CYC_ERR_CUDA, "fused finite check: the first tensor-core launch missed lb = 0 groups", -1};
         mark_read(s + lag_lo_);
         frames_ = avail;
     }

@@ -184,7 +184,7 @@ private:
     // fused finite check of the current gated push (see fold_device_chunk)
     unsigned long long* chk_key_ = nullptr;
     int64_t chk_c0_ = 0;
-    int chk_launches_ = 0;
+    bool chk_ok_ = false;  // the checking launch held every lb = 0 group
     cudaEvent_t fold_done_ev_ = nullptr;
     bool tc_interior(const FoldSeg& g, int64_t& pa, int64_t& pb) const;
     bool tc_check_plan(const std::vector<FoldSeg>& segs, int64_t& pa, int64_t& pb) const;

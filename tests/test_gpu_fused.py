@@ -176,3 +176,32 @@ def test_chunked_device_pushes_match_one_push(cyc):
         if first is None:
             first = got
         assert np.array_equal(got, first), rep
+
+
+@pytest.mark.parametrize("pos", [0, 333_333, (1 << 21) - 1, (1 << 21) - 3000])
+def test_fused_check_multi_launch_plan(cyc, pos):
+    """Three 64-lag blocks (lb 0 self, lb 1-2 not): several tensor-core launches,
+    the first of which holds every lb = 0 group and checks the chunk.  Verdicts
+    are exact, and a clean chunk matches the pinned-host path's tables."""
+    from conftest import assert_parity, mean_power
+    n = 1 << 21
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=2048, lag_spec=cyc.LagSpec.Explicit(range(192)),
+                              flags=cyc.Flags.BOTH, emit_frames=False)
+    x = rand_c(n, 30)
+    est = cyc.CyclicCorrelator(cfg)
+    d = dev(x)
+    est.push_device(d.data_ptr(), n)
+    host = cyc.CyclicCorrelator(cfg)
+    p = cyc.host_alloc(x.shape)
+    p[:] = x
+    host.push(p)
+    got, want = est.average_all(), host.average_all()
+    for fl in range(2):
+        assert_parity(got[0, fl], want[0, fl], mean_power(x), rel_l2=1e-5, what=f"flag {fl}")
+    bad = x.copy()
+    bad[pos] = np.nan
+    est.reset()
+    db = dev(bad)
+    with pytest.raises(cyc.DataError) as ei:
+        est.push_device(db.data_ptr(), n)
+    assert ei.value.index == pos and est.consumed() == 0
