@@ -183,9 +183,15 @@ def measured_peaks():
 
 def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lags: int = 64) -> dict:
     """The dominant kernel (the fold) from CUDA-event profiles on its stream.
-    achieved = ALGORITHMIC flops (8 per requested lag x folded sample: 4 FMAs
-    give both flags) / launch duration.  Tensor-core folds also report the
-    executed MMA rate (bf16x3 split x banded 128x256 product = ~6x algorithmic)."""
+
+    Algorithmic work per launch: 8 flops per (requested lag, folded sample)
+    (4 FMAs give both flags) over 8 bytes per folded sample (the record read
+    once from HBM), i.e. an intensity of `lags` flop/B.  On the tensor cores
+    the ridge is bf16 peak / HBM peak (~250 flop/B), so a fold with fewer lags
+    is HBM-bound: `achieved` = algorithmic bytes / launch duration against the
+    measured HBM copy bandwidth; with more, tensor-bound: algorithmic flops /
+    duration against the bf16 peak.  Both views are reported.  Executed MMA
+    work is ~6x the algorithmic (bf16x3 split x the 128x256 band block)."""
     n = max(1, p1["launches"] - p0["launches"])
     ms = (p1["ms"] - p0["ms"]) / n
     alg = (p1["flops"] - p0["flops"]) / n
@@ -195,33 +201,40 @@ def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lag
     import paper_2405_16911_b200 as cyc
     fp32 = cyc.measure_fp32_peak(dev)
     traffic, tsrc = traffic_from_profiles(tc > 0)
-    common = {"unit": "TFLOP/s", "traffic": traffic, "traffic_source": tsrc, "algorithmic_flops_per_launch": alg,
+    common = {"traffic": traffic, "traffic_source": tsrc, "algorithmic_flops_per_launch": alg,
               "ms_per_launch": ms, "launches_per_step": (p1["launches"] - p0["launches"]) / steps,
               "fold_share_of_step": (p1["ms"] - p0["ms"]) / steps / ms_step,
-              "algorithmic_unit": "8 flops per (requested lag, folded sample): 4 FMAs give both flags"}
+              "algorithmic_unit": "8 flops per (requested lag, folded sample) -- 4 FMAs give both flags -- and "
+                                  "8 HBM bytes per folded sample (the record read once)"}
     if tc > 0:
-        mp = measured_peaks()
-        peak = mp["bf16_tflops"] if mp and mp.get("bf16_tflops") else 1590.0
+        mp = measured_peaks() or {}
+        tpeak = mp.get("bf16_tflops") or 1590.0
+        hpeak = mp.get("hbm_gbs") or 7700.0
         ex_rate = exe / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-        # the same launches against HBM: 8 algorithmic bytes per folded sample
-        # (the record read once); algorithmic intensity 8*T/8 = T flop/B
-        samples = alg / (8.0 * max(1, lags))
-        hbm = mp.get("hbm_gbs") if mp else None
-        gbs = 8.0 * samples / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-        common["hbm_view"] = {"achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm if hbm else None,
-                              "algorithmic_bytes_per_launch": 8.0 * samples,
-                              "note": "algorithmic intensity = lags flop/B, below the bf16 ridge (~250 flop/B): "
-                                      "the record's HBM read bounds the ideal fold"}
-        return {"bound": "tensor", "kernel": "fold_tc_kernel (tcgen05 bf16x3 banded Gram product)",
-                "achieved": rate, "peak": peak, "frac": rate / peak, **common,
-                "executed_tflops": ex_rate, "executed_frac": ex_rate / peak,
-                "executed_per_algorithmic": exe / alg if alg else None,
-                "fp32_ffma_peak_tflops": fp32, "algorithmic_vs_fp32_peak": rate / fp32 if fp32 else None,
-                "tensor_launches_share": tc / n,
-                "peak_source": ("MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 burst, this pool)" if mp
-                                else "fallback 1.59 PFLOP/s (B200_PROFILING.md)")}
+        abytes = alg / max(1, lags)  # 8 B per folded sample
+        gbs = abytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        ridge = tpeak * 1e12 / (hpeak * 1e9)
+        tensor_view = {"achieved_tflops": rate, "peak_tflops": tpeak, "frac": rate / tpeak,
+                       "executed_tflops": ex_rate, "executed_frac": ex_rate / tpeak,
+                       "executed_per_algorithmic": exe / alg if alg else None,
+                       "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 burst, this pool)"
+                       if mp.get("bf16_tflops") else "fallback 1.59 PFLOP/s (B200_PROFILING.md)"}
+        hbm_view = {"achieved_gbs": gbs, "peak_gbs": hpeak, "frac": gbs / hpeak,
+                    "algorithmic_bytes_per_launch": abytes,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, this pool)" if mp.get("hbm_gbs")
+                    else "fallback 7.7 TB/s (B200_PROFILING.md)"}
+        common.update({"kernel": "fold_tc_kernel (tcgen05 bf16x3 banded Gram product)",
+                       "intensity_flop_per_byte": float(lags), "ridge_flop_per_byte": ridge,
+                       "tensor_view": tensor_view, "hbm_view": hbm_view,
+                       "fp32_ffma_peak_tflops": fp32, "algorithmic_vs_fp32_peak": rate / fp32 if fp32 else None,
+                       "tensor_launches_share": tc / n})
+        if lags < ridge:
+            return {"bound": "hbm", "achieved": gbs, "peak": hpeak, "unit": "GB/s", "frac": gbs / hpeak,
+                    "peak_source": hbm_view["peak_source"], **common}
+        return {"bound": "tensor", "achieved": rate, "peak": tpeak, "unit": "TFLOP/s", "frac": rate / tpeak,
+                "peak_source": tensor_view["peak_source"], **common}
     return {"bound": "fp32", "kernel": "fold_kernel (FFMA2 residue fold)", "achieved": rate, "peak": fp32,
-            "frac": rate / fp32 if fp32 else None, **common,
+            "unit": "TFLOP/s", "frac": rate / fp32 if fp32 else None, **common,
             "peak_source": "measured live: FFMA microbenchmark in libcycb200 (MEASURED_PEAKS.json carries no "
                            "FP32 figure)"}
 
