@@ -70,7 +70,7 @@ def config_block(n_gpus: int):
 # ---------------------------------------------------------------------------
 class Clocks:
     """SM clock + throttle reasons sampled DURING the timed region (B200_PROFILING.md
-    clocks line).  NVML is polled every ~2 ms from a thread (nvidia-smi's 100 ms
+    clocks line).  NVML is polled every ~0.5 ms from a thread (nvidia-smi's 100 ms
     floor cannot resolve a region of a few ms)."""
 
     REASONS = {  # nvmlClocksEventReason* bits
@@ -105,7 +105,7 @@ class Clocks:
         except Exception:
             pass
         self._ready.set()
-        self._stop.wait(0.002)
+        self._stop.wait(0.0005)
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
@@ -115,16 +115,23 @@ class Clocks:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.002)
+            self._stop.wait(0.0005)
 
     def stop(self):
         if self.nv is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable"}
         self._stop.set()
         self.t.join()
+        if not self.samples:  # a region shorter than the poll period: sample as it ends
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons.update(name for bit, name in self.REASONS.items() if r & bit)
+            except Exception:
+                pass
         sm = self.samples
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
-                "reasons": sorted(self.reasons), "samples": len(sm), "source": "NVML poll ~2 ms"}
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": "NVML poll ~0.5 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -683,8 +690,8 @@ def run_config(args, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
