@@ -826,15 +826,20 @@ bool Engine::tc_interior(const FoldSeg& g, int64_t& pa, int64_t& pb) const {
 }
 
 // A device chunk's folds qualify for the fused finite check when the first
-// tensor-core launch can hold every lb = 0 group: every segment tensor-core
-// eligible with the same interior [pa, pb), one segment batch, one tile kind
-// (x == y or not) for all segments, and the lb = 0 groups' minimum tiles
-// within one launch.  Later launches (other lag blocks) follow it.
-bool Engine::tc_check_plan(const std::vector<FoldSeg>& segs_in, int64_t& pa, int64_t& pb) const {
+// tensor-core launch of each segment batch can hold the batch's lb = 0 groups:
+// every segment tensor-core eligible with the same interior [pa, pb), one tile
+// kind (x == y or not) for all segments, and a batch's lb = 0 groups' minimum
+// tiles within one launch.  Later launches (other lag blocks) follow it.  With
+// more than one segment batch the reduces of an early batch would commit
+// before a later batch is checked: `pending` then folds into the pending
+// accumulator, committed by a gated add.
+bool Engine::tc_check_plan(const std::vector<FoldSeg>& segs_in, int64_t& pa, int64_t& pb, bool& pending) const {
     static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;
     if (no_tc || t_pad_ < 32 || Pf_ % 128 != 0 || !tc_capable_ || segs_in.empty()) return false;
     const int nrb = (int)(Pf_ / 128);
-    if (segs_in.size() > (size_t)TC_SEGS || segs_in.size() * nrb > (size_t)FI_GROUPS) return false;
+    const size_t per_batch = std::min(segs_in.size(), (size_t)TC_SEGS);
+    pending = segs_in.size() > (size_t)TC_SEGS;
+    if (per_batch * nrb > (size_t)FI_GROUPS) return false;
     for (size_t i = 0; i < segs_in.size(); ++i) {
         FoldSeg g = segs_in[i];
         g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
@@ -847,7 +852,7 @@ bool Engine::tc_check_plan(const std::vector<FoldSeg>& segs_in, int64_t& pa, int
             return false;
         }
     }
-    return (int64_t)segs_in.size() * nrb * ceil_div(pb - pa, (int64_t)2048) <= FI_TILES;
+    return (int64_t)per_batch * nrb * ceil_div(pb - pa, (int64_t)2048) <= FI_TILES;
 }
 
 Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<FoldSeg>& rest) {
@@ -1021,7 +1026,10 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         L.chk_key = chk ? chk_key_ : nullptr;
         L.chk_c0 = chk_c0_;
         L.chk_channels = c_.channels;
-        if (chk) chk_ok_ = ng >= n_lb0;
+        if (chk) {
+            ++chk_launches_;
+            if (ng < n_lb0) chk_fail_ = true;
+        }
         cudaEvent_t fold_done = chk ? fold_done_ev_ : nullptr;
         const FoldTile* dt = (tsegs.size() <= 2 && ng <= 16) ? cached_tiles(tcp_->tiles, nt) : nullptr;
         if (prof_) {
@@ -2137,7 +2145,14 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     // the rest of the chunk: the record is read from HBM once, not twice.
     static const bool no_fuse = std::getenv("CYC_NO_FUSED_CHECK") != nullptr;
     int64_t pa = 0, pb = 0;
-    const bool fused = !no_fuse && ring_segs.empty() && !user_segs.empty() && tc_check_plan(user_segs, pa, pb);
+    bool pending = false;
+    const bool fused =
+        !no_fuse && ring_segs.empty() && !user_segs.empty() && tc_check_plan(user_segs, pa, pb, pending);
+    const size_t s_count = (size_t)C * t_pad_ * Pf_ * 4;
+    if (fused && pending) {  // fold into the pending accumulator; the gated add below commits it
+        if (!S_pend_) CK(cudaMalloc(&S_pend_, s_count * sizeof(double)));
+        CK(cudaMemsetAsync(S_pend_, 0, s_count * sizeof(double), cs_));
+    }
     cudaEvent_t ev_c = get_event(), ev_v = get_event(), ev_f = nullptr;
     auto scan = [&](int64_t a, int64_t b) {  // absolute [a, b) of every channel
         if (b <= a) return;
@@ -2156,7 +2171,8 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
         chk_key_ = key_dev_;
         chk_c0_ = c0;
         fold_done_ev_ = ev_f;
-        chk_ok_ = false;
+        chk_launches_ = 0;
+        chk_fail_ = false;
     } else {
         scan(c0, c1);
     }
@@ -2168,6 +2184,11 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     }
     trace("scan enqueued");
     reduce_wait_ev_ = ev_c;
+    const unsigned long long* gate = fold_gate_;
+    if (fused && pending) {  // scratch target: the reduces need neither the gate nor the scan
+        fold_gate_ = nullptr;
+        reduce_wait_ev_ = nullptr;
+    }
     Status st;
     if (avail > frames_) {
         if (!ring_segs.empty()) {  // frames straddling the previous chunk read the ring
@@ -2175,16 +2196,23 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
             joined = true;
         }
         st = fold(ring_segs, S);
-        if (st.code == CYC_OK) st = fold(user_segs, S);
-        if (st.code == CYC_OK && fused && !chk_ok_)
-            st = Status{CYC_ERR_CUDA, "fused finite check: the first tensor-core launch missed lb = 0 groups", -1};
+        if (st.code == CYC_OK) st = fold(user_segs, fused && pending ? S_pend_ : S);
+        const int batches = (int)((user_segs.size() + TC_SEGS - 1) / TC_SEGS);
+        if (st.code == CYC_OK && fused && (chk_fail_ || chk_launches_ != batches))
+            st = Status{CYC_ERR_CUDA, "fused finite check: a checking launch missed lb = 0 groups", -1};
         mark_read(s + lag_lo_);
         frames_ = avail;
     }
     chk_key_ = nullptr;
     fold_done_ev_ = nullptr;
     reduce_wait_ev_ = nullptr;
-    if (fused) {  // the verdict waits for the checking fold kernel (not its reduce)
+    fold_gate_ = gate;
+    if (fused && pending) {  // commit behind the complete verdict (checking kernels on cs_, rest scan on vs_)
+        CK(cudaStreamWaitEvent(cs_, ev_c, 0));
+        launch_add_f64(S, S_pend_, (int64_t)s_count, cs_, key_dev_);
+        launches_ += 1;
+    }
+    if (fused) {  // the verdict waits for the (last) checking fold kernel, not its reduce
         CK(cudaStreamWaitEvent(vs_, ev_f, 0));
         CK(cudaMemcpyAsync(key_host_, key_dev_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, vs_));
         CK(record_event(verdict_ev_, vs_));

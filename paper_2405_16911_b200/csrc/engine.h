@@ -184,10 +184,11 @@ private:
     // fused finite check of the current gated push (see fold_device_chunk)
     unsigned long long* chk_key_ = nullptr;
     int64_t chk_c0_ = 0;
-    bool chk_ok_ = false;  // the checking launch held every lb = 0 group
+    int chk_launches_ = 0;     // checking launches of the current push (one per segment batch)
+    bool chk_fail_ = false;   // a checking launch missed some lb = 0 group
     cudaEvent_t fold_done_ev_ = nullptr;
     bool tc_interior(const FoldSeg& g, int64_t& pa, int64_t& pb) const;
-    bool tc_check_plan(const std::vector<FoldSeg>& segs, int64_t& pa, int64_t& pb) const;
+    bool tc_check_plan(const std::vector<FoldSeg>& segs, int64_t& pa, int64_t& pb, bool& pending) const;
     bool capturing_ = false;
     std::vector<int64_t> cap_marks_;
     cudaEvent_t verdict_ev_ = nullptr;  // the verdict copy of the last gated push landed

@@ -208,7 +208,9 @@ struct DirectLaunch {
 void launch_direct(const DirectLaunch& L, cudaStream_t st);
 
 // Utilities.
-void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st);
+// gate non-null: adds only if *gate == ~0 (the chunk's finite check passed).
+void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st,
+                    const unsigned long long* gate = nullptr);
 void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len,
                          double2* coh, double* mag, cudaStream_t st);
 // First non-finite sample -> atomicMin(*key);

@@ -8,7 +8,8 @@ thread_local bool g_capture_events = false;
 
 namespace {
 
-__global__ void add_f64_kernel(double* dst, const double* src, int64_t n) {
+__global__ void add_f64_kernel(double* dst, const double* src, int64_t n, const unsigned long long* gate) {
+    if (gate && *gate != ~0ull) return;  // a rejected chunk commits nothing
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] += src[i];
 }
@@ -120,8 +121,8 @@ int grid_for(int64_t n, int threads) {
 
 }  // namespace
 
-void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st) {
-    if (n > 0) add_f64_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, src, n);
+void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st, const unsigned long long* gate) {
+    if (n > 0) add_f64_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, src, n, gate);
 }
 void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len, double2* coh, double* mag,
                          cudaStream_t st) {

@@ -205,3 +205,41 @@ def test_fused_check_multi_launch_plan(cyc, pos):
     with pytest.raises(cyc.DataError) as ei:
         est.push_device(db.data_ptr(), n)
     assert ei.value.index == pos and est.consumed() == 0
+
+
+def test_fused_check_many_channel_batches(cyc):
+    """C4-like (Full N=256, lags 0..31) with 20 channels: two segment batches,
+    so the folds land in the pending accumulator and a gated add commits them.
+    Clean chunks match the pinned-host path; a bad sample in the second batch
+    rejects the chunk (exact channel and index) and commits nothing."""
+    from conftest import assert_parity, mean_power
+    C, n = 20, 1 << 17
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=256, lag_spec=cyc.LagSpec.Explicit(range(32)),
+                              flags=cyc.Flags.BOTH, emit_frames=False, channels=C)
+    xs = np.stack([rand_c(n, 40 + c) for c in range(C)])
+    est, host = cyc.CyclicCorrelator(cfg), cyc.CyclicCorrelator(cfg)
+    d = dev(xs)
+    p = cyc.host_alloc(xs.shape)
+    p[:] = xs
+    for rep in range(3):  # direct, captured and replayed pushes
+        est.reset()
+        est.push_device(d.data_ptr(), n)
+        got = est.average_all()
+        if rep == 0:
+            host.push(p)
+            want = host.average_all()
+            first = got
+        assert np.array_equal(got, first)
+    for c in (0, 17, 19):
+        for fl in range(2):
+            assert_parity(got[c, fl], want[c, fl], mean_power(xs[c]), rel_l2=1e-5, what=f"ch {c} flag {fl}")
+    bad = xs.copy()
+    bad[18, 70_000] = np.nan
+    bad[3, 90_000] = np.inf
+    est.reset()
+    db = dev(bad)
+    with pytest.raises(cyc.DataError, match="index 70000 in x stream of channel 18"):
+        est.push_device(db.data_ptr(), n)
+    assert est.consumed() == 0
+    est.push_device(d.data_ptr(), n)  # the state was untouched: same tables as before
+    assert np.array_equal(est.average_all(), first)
