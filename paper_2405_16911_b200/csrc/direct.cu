@@ -9,6 +9,8 @@
 // (proj/src/estimator.cpp:70-73) or std::polar of a large argument
 // (proj/src/kernels.cpp:19-24).  The phasor is folded into y once per sample
 // and shared by every lag:  x conj(y e^{+j th}) and x (y e^{-j th}).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace cyc {
@@ -18,7 +20,10 @@ constexpr int DT = 256;     // threads
 constexpr int TILE = 512;   // samples per smem tile
 constexpr int MAXL = 4;     // lags per thread (T <= 1024)
 
-__global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span) {
+// Threads: SL sample lanes x (DT / SL) lag slots.  Short lag spans (T <= 32)
+// use 8 lanes, so every thread works; each lane sums the samples i = sub
+// (mod SL) of its lags, and the lanes combine in a fixed order in shared memory.
+__global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span, int SL) {
     extern __shared__ float2 sm[];
     float2* xs = sm;                  // TILE + span
     float2* yc = xs + TILE + span;    // y * e^{+j th}
@@ -34,6 +39,8 @@ __global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span) {
     const int64_t cnt = seg.n_end - seg.n_start;
     const int64_t b0 = seg.n_start + cnt * split / L.splits;
     const int64_t b1 = seg.n_start + cnt * (split + 1) / L.splits;
+    const int LT = DT / SL;              // lag slots
+    const int slot = threadIdx.x % LT, sub = threadIdx.x / LT;
 
     float2 accv[MAXL], accj[MAXL];
     int loff[MAXL];
@@ -41,7 +48,7 @@ __global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span) {
     for (int k = 0; k < MAXL; ++k) {
         accv[k] = make_float2(0.f, 0.f);
         accj[k] = make_float2(0.f, 0.f);
-        const int t = threadIdx.x + k * DT;
+        const int t = slot + k * LT;
         loff[k] = t < L.T ? L.lags[t] - L.lag_lo : -1;
     }
     for (int64_t n0 = b0; n0 < b1; n0 += TILE) {
@@ -72,7 +79,7 @@ __global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span) {
             if (loff[k] < 0) continue;
             float2 av = accv[k], aj = accj[k];
             const float2* xp = xs + loff[k];
-            for (int i = 0; i < len; ++i) {
+            for (int i = sub; i < len; i += SL) {
                 const float2 xv = xp[i], c = yc[i], j = yj[i];
                 av.x += xv.x * c.x + xv.y * c.y;   // x * conj(c)
                 av.y += xv.y * c.x - xv.x * c.y;
@@ -85,12 +92,42 @@ __global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span) {
     }
     float2* part = reinterpret_cast<float2*>(L.partials);
     const size_t base = (((size_t)si * L.A + a) * L.splits + split) * 2;
+    if (SL == 1) {
+#pragma unroll
+        for (int k = 0; k < MAXL; ++k) {
+            const int t = slot + k * LT;
+            if (t >= L.T) continue;
+            part[(base + 0) * L.T + t] = accv[k];
+            part[(base + 1) * L.T + t] = accj[k];
+        }
+        return;
+    }
+    // lanes 1.. hand their sums to lane 0 through shared memory (reusing the
+    // sample tiles), which adds them in lane order
+    __syncthreads();
+    float2* red = sm;  // [SL][MAXL][LT] x 2
 #pragma unroll
     for (int k = 0; k < MAXL; ++k) {
-        const int t = threadIdx.x + k * DT;
+        red[((sub * MAXL + k) * LT + slot) * 2 + 0] = accv[k];
+        red[((sub * MAXL + k) * LT + slot) * 2 + 1] = accj[k];
+    }
+    __syncthreads();
+    if (sub != 0) return;
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k) {
+        const int t = slot + k * LT;
         if (t >= L.T) continue;
-        part[(base + 0) * L.T + t] = accv[k];
-        part[(base + 1) * L.T + t] = accj[k];
+        float2 v = red[((0 * MAXL + k) * LT + slot) * 2 + 0], j = red[((0 * MAXL + k) * LT + slot) * 2 + 1];
+        for (int q = 1; q < SL; ++q) {
+            const float2 v2 = red[((q * MAXL + k) * LT + slot) * 2 + 0];
+            const float2 j2 = red[((q * MAXL + k) * LT + slot) * 2 + 1];
+            v.x += v2.x;
+            v.y += v2.y;
+            j.x += j2.x;
+            j.y += j2.y;
+        }
+        part[(base + 0) * L.T + t] = v;
+        part[(base + 1) * L.T + t] = j;
     }
 }
 
@@ -121,16 +158,25 @@ __global__ void direct_reduce_kernel(DirectLaunch L) {
 
 }  // namespace
 
+// sample lanes per lag: every thread busy for short lag spans (MAXL lags per thread at most)
+int direct_lanes(int T) {
+    int sl = 1;
+    while (sl < 8 && (DT / (2 * sl)) * MAXL >= T && DT / (2 * sl) >= 32) sl *= 2;
+    return sl;
+}
+
 void launch_direct(const DirectLaunch& L, cudaStream_t st) {
     if (L.n_segs == 0) return;
     const int span = L.lag_hi - L.lag_lo;
-    const size_t smem = (size_t)(TILE + span + 2 * TILE) * sizeof(float2);
+    const int SL = direct_lanes(L.T);
+    const size_t smem = std::max<size_t>((size_t)(TILE + span + 2 * TILE) * sizeof(float2),
+                                         (size_t)SL * MAXL * (DT / SL) * 2 * sizeof(float2));
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    direct_kernel<<<L.n_segs * L.A * L.splits, DT, smem, st>>>(L, span);
+    direct_kernel<<<L.n_segs * L.A * L.splits, DT, smem, st>>>(L, span, SL);
     direct_reduce_kernel<<<dim3((L.T + 127) / 128, L.A, L.n_segs), 128, 0, st>>>(L);
 }
 

@@ -460,6 +460,16 @@ Status Engine::plan(const Cfg& cfg) {
         int lg = 0;
         while ((int64_t(1) << lg) < Pf_) ++lg;
         use_fft_ = is_pow2(Pf_) && Pf_ <= 8192 && A_ > 2 * lg;
+        // short Set-mode frames: one direct kernel per frame batch beats the
+        // fold + reduce + DFT chain, whose small launches are latency-bound
+        // (C1: 4096-sample frames x 10 alphas x 31 lags)
+        static const char* fd = std::getenv("CYC_FRAMES_DIRECT");
+        frames_direct_ = c_.mode == CYC_MODE_SET && c_.emit_frames && N_ <= 16384 && (int64_t)A_ * T_ <= 1024;
+        if (fd) frames_direct_ = fd[0] == '1';
+        if (frames_direct_) {
+            afx_.resize(A_);
+            for (int a = 0; a < A_; ++a) afx_[a] = alpha_fixed(c_.alphas[a]);
+        }
     } else {
         if (T_ > 1024) {
             Status s;
@@ -540,7 +550,8 @@ Status Engine::init(const Cfg& cfg) {
         CK(cudaMemcpy(tw_, tw.data(), Pf_ * sizeof(double2), cudaMemcpyHostToDevice));
         CK(cudaMalloc(&bins_dev_, A_ * sizeof(int)));
         CK(cudaMemcpy(bins_dev_, bins_.data(), A_ * sizeof(int), cudaMemcpyHostToDevice));
-    } else {
+    }
+    if (!use_fold_ || frames_direct_) {
         CK(cudaMalloc(&afx_dev_, A_ * sizeof(uint64_t)));
         CK(cudaMemcpy(afx_dev_, afx_.data(), A_ * sizeof(uint64_t), cudaMemcpyHostToDevice));
     }
@@ -1223,7 +1234,9 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     if (segs.empty()) return Status::ok();
     int64_t maxcnt = 0;
     for (auto& s : segs) maxcnt = std::max(maxcnt, s.n_end - s.n_start);
-    int splits = (int)std::min<int64_t>(256, std::max<int64_t>(1, maxcnt / 8192));
+    // sample lanes (short lag spans) let a CTA take fewer samples: split finer
+    const int sl = direct_lanes(T_);
+    int splits = (int)std::min<int64_t>(256, std::max<int64_t>(1, maxcnt / (8192 / sl)));
     while (splits > 1 && (int64_t)segs.size() * A_ * splits > 64 * SMS) splits /= 2;
     const size_t pbytes = segs.size() * (size_t)A_ * splits * 2 * T_ * sizeof(float2);
     TRY(ensure_partials(pbytes));
@@ -1259,7 +1272,7 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
     const float lam_log2 = recursive ? (float)std::log2(c_.lambda) : 0.f;
     const float w_scale = recursive ? (float)(1.0 - c_.lambda) : 1.f;
     const double scale = recursive ? 1.0 : 1.0 / (double)N_;
-    if (use_fold_) {
+    if (use_fold_ && !frames_direct_) {
         std::vector<FoldSeg> segs(slots);
         for (size_t s = 0; s < slots; ++s) {
             const int ch = chans[s];
@@ -1303,7 +1316,7 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
 
 bool Engine::graph_eligible(size_t slots) const {
     static const bool off = std::getenv("CYC_NO_GRAPH") != nullptr;
-    return !off && use_fold_ && slots <= 16 && (N_ + Pf_ - 1) / Pf_ + 1 <= 4096;
+    return !off && use_fold_ && !frames_direct_ && slots <= 16 && (N_ + Pf_ - 1) / Pf_ + 1 <= 4096;
 }
 
 void Engine::fill_frame_segs(FoldSeg* segs, const std::vector<int64_t>& k0s, const std::vector<int>& chans,
@@ -2583,7 +2596,7 @@ void Engine::layout(cyc_layout_info* li) const {
 std::string Engine::algorithm() const {
     if (!use_fold_) return "direct";
     return std::string(use_fft_ ? "fold-fft" : "fold-dft") + " P=" + std::to_string(P_) + " Pf=" +
-           std::to_string(Pf_) + " lw=" + std::to_string(lw_);
+           std::to_string(Pf_) + " lw=" + std::to_string(lw_) + (frames_direct_ ? "; frames: direct" : "");
 }
 
 }  // namespace cyc

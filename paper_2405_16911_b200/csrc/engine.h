@@ -241,6 +241,7 @@ private:
     int64_t stride_a_ = 0, stride_t_ = 0;
 
     bool use_fold_ = true;
+    bool frames_direct_ = false;  // per-frame tables by the direct kernel (short Set-mode frames)
     int64_t P_ = 1, Pf_ = 1;
     std::vector<int> bins_;
     int lw_ = 8, TB_ = 64, RB_ = 128, n_rb_ = 1, n_lb_ = 1, t_pad_ = 64;

@@ -206,6 +206,7 @@ struct DirectLaunch {
 };
 
 void launch_direct(const DirectLaunch& L, cudaStream_t st);
+int direct_lanes(int T);  // sample lanes per lag of the direct kernel (1 for long lag spans)
 
 // Utilities.
 // gate non-null: adds only if *gate == ~0 (the chunk's finite check passed).
