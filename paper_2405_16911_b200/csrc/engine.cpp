@@ -121,6 +121,22 @@ inline bool screen(const cyc_cf64* p, size_t i0, size_t i1) {
     return acc != 0;
 }
 
+// Small host chunks: copy n samples of every channel into the pinned staging
+// (channel rows n apart) and screen them in the same pass (true: some
+// component may be non-finite) -- one read of the caller's memory, not two.
+inline bool copy_screen(float2* dst, const cyc_cf32* src, size_t n, int channels) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    const size_t m = 2 * n * (size_t)channels;
+    uint32_t acc = 0;
+    for (size_t i = 0; i < m; ++i) {
+        const uint32_t w = s[i];
+        d[i] = w;
+        acc |= (uint32_t)((w & 0x7f800000u) == 0x7f800000u);
+    }
+    return acc != 0;
+}
+
 template <typename T>
 Bad scan_bad(const T* x, const T* y, size_t n, int channels) {
     auto bad_val = [](double v) { return !std::isfinite(v) || std::fabs(v) > (double)FLT_MAX; };
@@ -1620,6 +1636,7 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     hprof(-1);
     ++hprof_calls_;
     meta_mapped_now_ = false;
+    prestaged_ = false;
     CK(cudaSetDevice(c_.device));
     if (n == 0) return Status::ok();
     if (kind == IN_DEVICE_F32 && !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_)
@@ -1647,8 +1664,17 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     if (!speculative) {
         // whole-chunk validation before any state change (estimator.cpp:43-52)
         Bad bad;
+        const bool one_piece = kind == IN_HOST_F32 && !pinned && n <= (size_t)Q_ && stage_len_ >= (size_t)Q_ &&
+                               ((!yv && !cross_) || (yv && cross_ && stage_y_[0]));
         if (kind == IN_HOST_F32 && prevalidated_) {
             prevalidated_ = false;  // the caller (push_file) scanned this chunk already
+        } else if (one_piece) {  // stage and screen in one pass; exact scan only if flagged
+            if (stage_ev_live_[stage_k_]) CK(cudaEventSynchronize(stage_ev_[stage_k_]));
+            stage_ev_live_[stage_k_] = false;
+            bool flag = copy_screen(stage_[stage_k_], (const cyc_cf32*)xv, n, C);
+            if (yv) flag = copy_screen(stage_y_[stage_k_], (const cyc_cf32*)yv, n, C) || flag;
+            if (flag) bad = scan_bad((const cyc_cf32*)xv, (const cyc_cf32*)yv, n, C);
+            prestaged_ = bad.key == ~0ull;
         } else if (kind == IN_HOST_F32) {
             bad = scan_bad((const cyc_cf32*)xv, (const cyc_cf32*)yv, n, C);
         } else if (kind == IN_HOST_F64) {
@@ -1762,7 +1788,9 @@ Status Engine::ingest_piece(const void* xv, const void* yv, size_t n, size_t off
             pitch = n;
         } else {
             if (stage_ev_live_[stage_k_]) CK(cudaEventSynchronize(stage_ev_[stage_k_]));
-            if (kind == IN_HOST_F32) {
+            if (prestaged_) {  // push() copied (and screened) this one-piece chunk already
+                prestaged_ = false;
+            } else if (kind == IN_HOST_F32) {
                 stage_copy(stage_[stage_k_], (const cyc_cf32*)xv, n, off, len, C);
                 if (cross_) stage_copy(stage_y_[stage_k_], (const cyc_cf32*)(yv ? yv : xv), n, off, len, C);
             } else {

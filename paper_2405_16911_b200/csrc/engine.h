@@ -298,6 +298,7 @@ private:
     char* meta_shadow_ = nullptr;  // device copy of the arena
     bool meta_mapped_now_ = false; // read descriptors mapped (inside pinned-host pushes)
     bool prevalidated_ = false;    // next host-f32 push was scanned by validate_host_f32
+    bool prestaged_ = false;       // the current one-piece push is already in stage_[stage_k_]
     size_t meta_slot_bytes_ = 0;
     size_t meta_used_ = 0;
     int meta_slot_ = 0;
