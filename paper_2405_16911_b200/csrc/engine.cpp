@@ -1868,8 +1868,6 @@ Status Engine::history_copy(int64_t a, int64_t b, bool save) {
 }
 
 Status Engine::enqueue_gated(const void* xv, const void* yv, size_t n, int64_t hb, int64_t hc) {
-    if (pending_clear_)  // the reset's clear (the caller drops the flag once this is enqueued)
-        CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), cs_));
     TRY(history_copy(hb, hc, true));
     CK(cudaMemsetAsync(key_dev_, 0xff, sizeof(unsigned long long), cs_));
     // fork the side (scan) and copy streams off the compute stream; the scan
@@ -1879,6 +1877,11 @@ Status Engine::enqueue_gated(const void* xv, const void* yv, size_t n, int64_t h
     CK(cudaEventRecord(ev_k, cs_));
     CK(cudaStreamWaitEvent(vs_, ev_k, 0));
     CK(cudaStreamWaitEvent(xs_, ev_k, 0));
+    // the reset's clear (the caller drops the flag once this is enqueued) runs
+    // on the side stream beside the fold kernel: every write of S_main below
+    // waits for the side stream's scan event
+    if (pending_clear_)
+        CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), vs_));
     xs_after_cs_ = false;
     ev_pool_.push_back(ev_k);
     fold_gate_ = key_dev_;
