@@ -209,6 +209,16 @@ __device__ __noinline__ void check_unit_slow(const FoldLaunch& L, uint32_t raw, 
     }
 }
 
+// -DTC_TRACE (diagnostics build): clock64 at the pipeline hand-offs of CTA 0,
+// read back with cyc_debug_tc_trace (tools/tc_trace.py)
+#ifdef TC_TRACE
+__device__ unsigned long long g_tc_trace[8][128];
+#define TC_MARK(kind, it) \
+    if (blockIdx.x == 0 && (it) < 128) g_tc_trace[kind][it] = clock64();
+#else
+#define TC_MARK(kind, it)
+#endif
+
 template <bool SELF, class DESC>
 __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
     using G = TcGeo<SELF>;
@@ -243,6 +253,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_s;
+    if (threadIdx.x == 0) TC_MARK(7, 0);
     const FoldTile& tile = s_tile;
     const FoldSeg& seg = s_seg;
     const int64_t Pf = L.Pf;
@@ -265,6 +276,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                 for (int it = 0; it < nst; ++it) {
                     const int s = it % G::NR;
                     if (it >= G::NR) mbar_wait(&rawfree[s], ((it / G::NR) - 1) & 1);
+                    TC_MARK(0, it);
                     const uint32_t st = su32(raw_ring + s * G::RAW);
                     mbar_expect_tx(&full[s], G::RAW);
 #pragma unroll
@@ -315,6 +327,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             for (int it = 0; it < nst; ++it) {
                 const int s = it % G::NP;
                 mbar_wait(&conv[s], (it / G::NP) & 1);
+                TC_MARK(1, it);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t xh = su32(plane_ring + s * G::PLANE), xl = xh + XPLANE;
                 const uint32_t yh0 = SELF ? xh + ya * ATOM : xl + XPLANE;
@@ -333,6 +346,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                     }
                 }
                 mma_commit(&planefree[s]);
+                TC_MARK(2, it);
             }
             mma_commit(&done);
         }
@@ -347,7 +361,9 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         for (int it = 0; it < nst; ++it) {
             const int rs = it % G::NR, ps = it % G::NP;
             mbar_wait(&full[rs], (it / G::NR) & 1);
+            if (warp == 2 && lane == 0) TC_MARK(3, it);
             if (it >= G::NP) mbar_wait(&planefree[ps], ((it / G::NP) - 1) & 1);
+            if (warp == 2 && lane == 0) TC_MARK(4, it);
             const uint32_t st = su32(raw_ring + rs * G::RAW);
             const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
             const uint32_t xh = su32(plane_ring + ps * G::PLANE);
@@ -372,11 +388,13 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[ps]);
+            if (warp == 2 && lane == 0) TC_MARK(5, it);
         }
         // epilogue: warps 2-5 read accumulator 0 (residues 0-63), warps 6-9
         // accumulator 1 (64-127).  Lane m = 2r + a of quarter q holds D[m][*];
         // the band is columns [2r, 2r + 128): float2 (c_{2a}, c_{2a+1}) per lag t
         mbar_wait(&done, 0);
+        if (warp == 2 && lane == 0) TC_MARK(6, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int q = warp & 3;  // TMEM lane quarter this warp may read
         const int m = 32 * q + lane;
@@ -410,6 +428,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if (threadIdx.x == 0) TC_MARK(7, 1);
 }
 
 template <int MG>
@@ -578,3 +597,9 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool sel
 }
 
 }  // namespace cyc
+
+#ifdef TC_TRACE
+extern "C" int cyc_debug_tc_trace(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, cyc::g_tc_trace, sizeof(cyc::g_tc_trace));
+}
+#endif
