@@ -353,23 +353,52 @@ int cyc_gmsk_mc_oracle(const cyc_cpm_params* p, const double* alphas, size_t n_a
     c.channels = TB;
     c.device = device;
     c.origin = (int64_t)(M - m_minus);
-    cyc::Engine* e = nullptr;
-    cyc::Status s = cyc::Engine::create_unchecked(c, &e);  // the oracle has no win_len > 2M rule
-    if (s.code) {
-        write_msg(err, errlen, s.msg);
-        return s.code;
+    // The estimator and the record buffer of the last geometry are kept per
+    // thread: repeated calls (more trials, other seeds) skip the set-up, which
+    // dominates small tables.  Never freed (process lifetime).
+    struct Cache {
+        cyc::Cfg cfg;
+        cyc::Engine* e = nullptr;
+        float2* x = nullptr;
+        size_t x_len = 0;
+        cudaStream_t st = nullptr;
+    };
+    static thread_local Cache* cache = nullptr;
+    if (!cache) cache = new Cache;
+    auto same = [](const cyc::Cfg& a, const cyc::Cfg& b) {
+        return a.mode == b.mode && a.flags == b.flags && a.win_len == b.win_len && a.alphas == b.alphas &&
+               a.lag_symmetric == b.lag_symmetric && a.max_lag == b.max_lag && a.emit_frames == b.emit_frames &&
+               a.channels == b.channels && a.device == b.device && a.origin == b.origin;
+    };
+    if (!cache->e || !same(cache->cfg, c)) {
+        delete cache->e;
+        cache->e = nullptr;
+        cyc::Engine* ne = nullptr;
+        cyc::Status cs = cyc::Engine::create_unchecked(c, &ne);  // the oracle has no win_len > 2M rule
+        if (cs.code) {
+            write_msg(err, errlen, cs.msg);
+            return cs.code;
+        }
+        cache->e = ne;
+        cache->cfg = c;
     }
+    cyc::Engine* e = cache->e;
+    cyc::Status s;
     const size_t total = total_len;
     const size_t n_syms = (total + (size_t)p->sps - 1) / (size_t)p->sps;
-    float2* x = nullptr;
-    cudaStream_t st;
-    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    if (cudaMalloc(&x, (size_t)TB * total * sizeof(float2)) != cudaSuccess) {
-        delete e;
-        cudaStreamDestroy(st);
-        write_msg(err, errlen, "device allocation failed");
-        return CYC_ERR_CUDA;
+    if (!cache->st) cudaStreamCreateWithFlags(&cache->st, cudaStreamNonBlocking);
+    cudaStream_t st = cache->st;
+    if (cache->x_len < (size_t)TB * total) {
+        cudaFree(cache->x);
+        cache->x = nullptr;
+        cache->x_len = 0;
+        if (cudaMalloc(&cache->x, (size_t)TB * total * sizeof(float2)) != cudaSuccess) {
+            write_msg(err, errlen, "device allocation failed");
+            return CYC_ERR_CUDA;
+        }
+        cache->x_len = (size_t)TB * total;
     }
+    float2* x = cache->x;
     const size_t lay = n_alphas * (2 * (size_t)M + 1);
     std::vector<cyc_cf64> avg(lay);
     std::vector<double> acc(n_alphas * n_lags, 0.0);
@@ -401,9 +430,6 @@ int cyc_gmsk_mc_oracle(const cyc_cpm_params* p, const double* alphas, size_t n_a
             m = s.msg;
         }
     }
-    cudaFree(x);
-    cudaStreamDestroy(st);
-    delete e;
     if (rc) {
         write_msg(err, errlen, m);
         return rc;
