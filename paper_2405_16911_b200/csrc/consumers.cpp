@@ -88,22 +88,39 @@ int cyc_estimate_cfo_ccf(const cyc_cf32* x, size_t n, double expected_beta, int 
         write_msg(err, errlen, "expected conjugate cycle frequency must lie in [-1/2, 1/2)");
         return CYC_ERR_USAGE;
     }
-    cyc_config c;
-    cyc_config_init(&c);
-    c.mode = CYC_MODE_FULL;
-    c.conj = 1;
-    c.win_len = N;
-    c.lag_symmetric = 0;
-    const int lag0 = 0;
-    c.lags = &lag0;
-    c.num_lags = 1;
-    c.device = device;
-    cyc_est* est = nullptr;
-    const int rc = cyc_create(&c, &est, err, errlen);  // validates N (impair.cpp:56)
-    if (rc) return rc;
+    // The scan's estimator is kept per (N, device) and thread across calls:
+    // its set-up (rings, pinned staging) costs far more than one scan.
+    struct Cache {
+        int N = 0, device = -1;
+        cyc_est* est = nullptr;
+    };
+    static thread_local Cache* cache = nullptr;
+    if (!cache) cache = new Cache;  // process lifetime
+    if (!cache->est || cache->N != N || cache->device != device) {
+        if (cache->est) cyc_destroy(cache->est);
+        cache->est = nullptr;
+        cyc_config c;
+        cyc_config_init(&c);
+        c.mode = CYC_MODE_FULL;
+        c.conj = 1;
+        c.win_len = N;
+        c.lag_symmetric = 0;
+        const int lag0 = 0;
+        c.lags = &lag0;
+        c.num_lags = 1;
+        c.device = device;
+        const int rc = cyc_create(&c, &cache->est, err, errlen);  // validates N (impair.cpp:56)
+        if (rc) return rc;
+        cache->N = N;
+        cache->device = device;
+    }
+    cyc_est* est = cache->est;
+    if (int rc = cyc_reset(est)) {
+        write_msg(err, errlen, cyc_last_error(est));
+        return rc;
+    }
     const size_t need = (size_t)N * (size_t)num_frames;
     if (!x || n < need) {
-        cyc_destroy(est);
         write_msg(err, errlen, "record too short for the requested number of frames");
         return CYC_ERR_USAGE;
     }
@@ -114,7 +131,6 @@ int cyc_estimate_cfo_ccf(const cyc_cf32* x, size_t n, double expected_beta, int 
     for (size_t i = need; !code && i < n; ++i) {
         if (!std::isfinite(x[i].re) || !std::isfinite(x[i].im)) {
             write_msg(err, errlen, "non-finite sample at absolute index " + std::to_string(i) + " in x stream");
-            cyc_destroy(est);
             return CYC_ERR_DATA;
         }
     }
@@ -122,10 +138,8 @@ int cyc_estimate_cfo_ccf(const cyc_cf32* x, size_t n, double expected_beta, int 
     if (!code) code = cyc_average(est, CYC_AVG_MAGNITUDE, CYC_FLAG_CONJ, 0, avg.data());
     if (code) {
         write_msg(err, errlen, cyc_last_error(est));
-        cyc_destroy(est);
         return code;
     }
-    cyc_destroy(est);
     std::vector<double> mag((size_t)N);
     for (int k = 0; k < N; ++k) mag[(size_t)k] = avg[(size_t)k].re;
 
