@@ -5,6 +5,7 @@
 
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "engine.h"
 
@@ -134,6 +135,45 @@ void cyc_host_free(void* p) {
     if (p) cudaFreeHost(p);
 }
 
+}  // extern "C"
+
+namespace {
+// One-shot windows (kernels.cpp:116-135) reuse the engines of the last few
+// geometries per thread: the set-up costs far more than one window.  The
+// engines live for the process.
+cyc::Status cached_window_engine(const cyc::Cfg& g, cyc::Engine** out) {
+    struct Entry {
+        cyc::Cfg cfg;
+        cyc::Engine* e;
+    };
+    static thread_local std::vector<Entry>* cache = nullptr;
+    if (!cache) cache = new std::vector<Entry>();
+    auto same = [](const cyc::Cfg& a, const cyc::Cfg& b) {
+        return a.mode == b.mode && a.flags == b.flags && a.win_len == b.win_len && a.alphas == b.alphas &&
+               a.lag_symmetric == b.lag_symmetric && a.max_lag == b.max_lag && a.lags == b.lags &&
+               a.lambda == b.lambda && a.emit_frames == b.emit_frames && a.channels == b.channels &&
+               a.device == b.device && a.origin == b.origin;
+    };
+    for (size_t i = 0; i < cache->size(); ++i)
+        if (same((*cache)[i].cfg, g)) {
+            *out = (*cache)[i].e;
+            return cyc::Status::ok();
+        }
+    cyc::Engine* e = nullptr;
+    cyc::Status s = cyc::Engine::create_unchecked(g, &e);
+    if (s.code) return s;
+    if (cache->size() >= 4) {
+        delete cache->front().e;
+        cache->erase(cache->begin());
+    }
+    cache->push_back({g, e});
+    *out = e;
+    return s;
+}
+}  // namespace
+
+extern "C" {
+
 int cyc_compute_set_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw, size_t yw_len,
                            const double* alphas, size_t num_alphas, int max_lag, int conj, uint64_t k0,
                            cyc_cf64* out, char* err, size_t errlen) {
@@ -166,13 +206,12 @@ int cyc_compute_set_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw
             return CYC_ERR_INTERNAL;
         }
     }
-    s = cyc::Engine::create_unchecked(g, &e);
+    s = cached_window_engine(g, &e);
     if (s.code) {
         write_err(err, errlen, s.msg);
         return s.code;
     }
     s = e->compute_window(xw, xw_len, yw, yw_len, k0, out);
-    delete e;
     write_err(err, errlen, s.msg);
     return s.code;
 }
@@ -202,13 +241,12 @@ int cyc_compute_full_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* y
     c.num_lags = num_lags;
     cyc::Cfg g = cyc::from_c(&c);
     cyc::Engine* e = nullptr;
-    cyc::Status s = cyc::Engine::create_unchecked(g, &e);
+    cyc::Status s = cached_window_engine(g, &e);
     if (s.code) {
         write_err(err, errlen, s.msg);
         return s.code;
     }
     s = e->compute_window(xw, xw_len, yw, yw_len, k0, out);
-    delete e;
     write_err(err, errlen, s.msg);
     return s.code;
 }

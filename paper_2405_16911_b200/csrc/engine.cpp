@@ -2432,8 +2432,6 @@ Status Engine::compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64*
     const size_t tot = xw_len + yw_len;
     if (dev_tmp_len_ < tot) {
         cudaFree(dev_tmp_);
-    cudaFree(S_pend_);
-    cudaFree(hist_bak_);
         CK(cudaMalloc(&dev_tmp_, tot * sizeof(float2)));
         dev_tmp_len_ = tot;
     }
