@@ -23,7 +23,7 @@ constexpr int MAXL = 4;     // lags per thread (T <= 1024)
 // Threads: SL sample lanes x (DT / SL) lag slots.  Short lag spans (T <= 32)
 // use 8 lanes, so every thread works; each lane sums the samples i = sub
 // (mod SL) of its lags, and the lanes combine in a fixed order in shared memory.
-__global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span, int SL) {
+__global__ void __launch_bounds__(DT) direct_kernel(const __grid_constant__ DirectLaunch L, int span, int SL) {
     extern __shared__ float2 sm[];
     float2* xs = sm;                  // TILE + span
     float2* yc = xs + TILE + span;    // y * e^{+j th}
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span, in
     const int a = (blockIdx.x / L.splits) % L.A;
     const int si = blockIdx.x / (L.splits * L.A);
     __shared__ DirectSeg s_seg;  // descriptors may be in mapped host memory: read once
-    if (threadIdx.x == 0) s_seg = L.segs[si];
+    if (threadIdx.x == 0) s_seg = L.segs ? L.segs[si] : L.inl[si];
     __syncthreads();
     const DirectSeg& seg = s_seg;
     const uint64_t afx = L.alpha_fx[a];
@@ -131,13 +131,13 @@ __global__ void __launch_bounds__(DT) direct_kernel(DirectLaunch L, int span, in
     }
 }
 
-__global__ void direct_reduce_kernel(DirectLaunch L) {
+__global__ void direct_reduce_kernel(const __grid_constant__ DirectLaunch L) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int a = blockIdx.y;
     const int si = blockIdx.z;
     const float2* part = reinterpret_cast<const float2*>(L.partials);
     __shared__ DirectSeg s_seg;  // descriptors may be in mapped host memory: read once
-    if (threadIdx.x == 0) s_seg = L.segs[si];
+    if (threadIdx.x == 0) s_seg = L.segs ? L.segs[si] : L.inl[si];
     __syncthreads();
     if (t >= L.T) return;
     const DirectSeg& seg = s_seg;
@@ -156,6 +156,45 @@ __global__ void direct_reduce_kernel(DirectLaunch L) {
     }
 }
 
+// direct_reduce_kernel fused with the running average_frames sums
+// (accum_frames_kernel): one thread per (channel, alpha, lag) walks the batch's
+// frames in order, so the sums are bit-identical to the separate kernels'.
+// Segments are [frame][channel]; out_block = segment index.
+__global__ void direct_reduce_accum_kernel(const __grid_constant__ DirectLaunch L, int n_frames, int C, double2* coh,
+                                           double* mag, int64_t per) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int a = blockIdx.y;
+    const int ch = blockIdx.z;
+    if (t >= L.T) return;
+    const float2* part = reinterpret_cast<const float2*>(L.partials);
+    int fi = 0;
+    for (int f = 0; f < 2; ++f) {
+        if (!(L.flags & (1 << f))) continue;
+        const int64_t e = (int64_t)ch * per + (int64_t)fi * L.out_flag_stride + (int64_t)a * L.stride_a +
+                          (int64_t)t * L.stride_t;
+        double2 c = coh[e];
+        double m = mag[e];
+        for (int fr = 0; fr < n_frames; ++fr) {
+            const int si = fr * C + ch;
+            double re = 0.0, im = 0.0;
+            for (int s = 0; s < L.splits; ++s) {
+                const float2 v = part[((((size_t)si * L.A + a) * L.splits + s) * 2 + f) * L.T + t];
+                re += v.x;
+                im += v.y;
+            }
+            const double2 v = make_double2(re * L.scale, im * L.scale);
+            L.out[(size_t)si * L.out_block_stride + (size_t)fi * L.out_flag_stride + (size_t)a * L.stride_a +
+                  (size_t)t * L.stride_t] = v;
+            c.x += v.x;
+            c.y += v.y;
+            m += hypot(v.x, v.y);
+        }
+        coh[e] = c;
+        mag[e] = m;
+        ++fi;
+    }
+}
+
 }  // namespace
 
 // sample lanes per lag: every thread busy for short lag spans (MAXL lags per thread at most)
@@ -165,7 +204,7 @@ int direct_lanes(int T) {
     return sl;
 }
 
-void launch_direct(const DirectLaunch& L, cudaStream_t st) {
+void launch_direct(const DirectLaunch& L, cudaStream_t st, double2* coh, double* mag, int channels, int64_t per) {
     if (L.n_segs == 0) return;
     const int span = L.lag_hi - L.lag_lo;
     const int SL = direct_lanes(L.T);
@@ -177,7 +216,11 @@ void launch_direct(const DirectLaunch& L, cudaStream_t st) {
         attr_set = true;
     }
     direct_kernel<<<L.n_segs * L.A * L.splits, DT, smem, st>>>(L, span, SL);
-    direct_reduce_kernel<<<dim3((L.T + 127) / 128, L.A, L.n_segs), 128, 0, st>>>(L);
+    if (coh)
+        direct_reduce_accum_kernel<<<dim3((L.T + 127) / 128, L.A, channels), 128, 0, st>>>(L, L.n_segs / channels,
+                                                                                          channels, coh, mag, per);
+    else
+        direct_reduce_kernel<<<dim3((L.T + 127) / 128, L.A, L.n_segs), 128, 0, st>>>(L);
 }
 
 }  // namespace cyc

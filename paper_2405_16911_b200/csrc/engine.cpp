@@ -1246,7 +1246,7 @@ Status Engine::finalize(const double* S, int nslots, double scale, const std::ve
     return cuda_check(cudaGetLastError(), "finalize launch");
 }
 
-Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2* out) {
+Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2* out, bool accum) {
     if (segs.empty()) return Status::ok();
     int64_t maxcnt = 0;
     for (auto& s : segs) maxcnt = std::max(maxcnt, s.n_end - s.n_start);
@@ -1256,8 +1256,12 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     while (splits > 1 && (int64_t)segs.size() * A_ * splits > 64 * SMS) splits /= 2;
     const size_t pbytes = segs.size() * (size_t)A_ * splits * 2 * T_ * sizeof(float2);
     TRY(ensure_partials(pbytes));
-    DirectLaunch L{};
-    L.segs = (const DirectSeg*)upload(segs.data(), segs.size() * sizeof(DirectSeg));
+    thread_local DirectLaunch L;  // ~0.7 KB of inline descriptors: host staging, copied by the launch
+    L = DirectLaunch{};
+    if (segs.size() <= (size_t)DIRECT_INL)
+        std::copy(segs.begin(), segs.end(), L.inl);
+    else
+        L.segs = (const DirectSeg*)upload(segs.data(), segs.size() * sizeof(DirectSeg));
     L.n_segs = (int)segs.size();
     L.alpha_fx = afx_dev_;
     L.A = A_;
@@ -1274,7 +1278,10 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     L.stride_a = stride_a_;
     L.stride_t = stride_t_;
     L.scale = scale;
-    launch_direct(L, cs_);
+    if (accum)  // per-frame batch: the reduce also adds the frames to the running sums
+        launch_direct(L, cs_, coh_, mag_, c_.channels, (int64_t)nflags_ * (int64_t)layout_len_);
+    else
+        launch_direct(L, cs_);
     launches_ += 2;
     return cuda_check(cudaGetLastError(), "direct launch");
 }
@@ -1325,7 +1332,7 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
             g.w_scale = w_scale;
             g.out_block = (int)s;
         }
-        TRY(direct(segs, scale, frames_dev_));
+        TRY(direct(segs, scale, frames_dev_, accum_in_direct_));
     }
     return Status::ok();
 }
@@ -1518,6 +1525,8 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
         const uint64_t batch = std::max<uint64_t>(1, FRAME_SLOT_BUDGET / (per_slot * C));
         bool stop = false;
         const size_t per = (size_t)nflags_ * layout_len_;
+        // direct per-frame tables fold the running sums into their reduce
+        const bool direct_frames = (!use_fold_ || frames_direct_) && c_.mode != CYC_MODE_RECURSIVE;
         for (uint64_t fb = f0; fb < f1; fb += batch) {
             const uint64_t fe = std::min(f1, fb + batch);
             std::vector<int64_t> k0s;
@@ -1534,9 +1543,14 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             if (!sink && c_.mode != CYC_MODE_RECURSIVE) {
                 // nobody receives the frames: keep only the running average_frames
                 // sums on the device (no frame D2H, no synchronisation)
-                TRY(compute_frames(k0s, chans, false));
-                launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
-                launches_ += 1;
+                accum_in_direct_ = direct_frames;
+                const Status cs = compute_frames(k0s, chans, false);
+                accum_in_direct_ = false;
+                TRY(cs);
+                if (!direct_frames) {
+                    launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
+                    launches_ += 1;
+                }
                 continue;
             }
             if (graph_eligible(slots)) {
@@ -1544,9 +1558,12 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                 // accumulate, D2H) instead of five launches and a memcpy
                 TRY(run_frame_graph(k0s, chans, c_.mode == CYC_MODE_RECURSIVE, &tables));
             } else {
-                TRY(compute_frames(k0s, chans, c_.mode == CYC_MODE_RECURSIVE));
+                accum_in_direct_ = direct_frames;
+                const Status cs = compute_frames(k0s, chans, c_.mode == CYC_MODE_RECURSIVE);
+                accum_in_direct_ = false;
+                TRY(cs);
                 tables = frames_host_;
-                if (c_.mode != CYC_MODE_RECURSIVE) {
+                if (c_.mode != CYC_MODE_RECURSIVE && !direct_frames) {
                     // running average_frames sums; slots are [frame][channel] blocks
                     launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
                     launches_ += 1;

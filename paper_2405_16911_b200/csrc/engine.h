@@ -123,7 +123,8 @@ private:
     Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
                     double2* out, cudaStream_t st = nullptr);
     // Direct contraction of segs into out tables (out_block = seg.out_block).
-    Status direct(const std::vector<DirectSeg>& segs, double scale, double2* out);
+    Status direct(const std::vector<DirectSeg>& segs, double scale, double2* out, bool accum = false);
+    bool accum_in_direct_ = false;  // compute_frames' direct reduce also updates coh_/mag_
 
     // Per-frame tables for the given (k0, channel) windows -> frames_dev_ (fp64).
     // Recursive weighting when `recursive`.

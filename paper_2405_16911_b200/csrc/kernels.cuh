@@ -189,8 +189,10 @@ struct DirectSeg {
     int pad;
 };
 
+constexpr int DIRECT_INL = 8;  // descriptors carried in the parameter block (small frame batches)
 struct DirectLaunch {
-    const DirectSeg* segs;
+    const DirectSeg* segs;      // device descriptors, or null: inl[0, n_segs)
+    DirectSeg inl[DIRECT_INL];
     int n_segs;
     const uint64_t* alpha_fx;   // [A] round(alpha * 2^64)
     int A;
@@ -205,7 +207,10 @@ struct DirectLaunch {
     double scale;
 };
 
-void launch_direct(const DirectLaunch& L, cudaStream_t st);
+// coh/mag non-null: the reduce also adds each frame to the running average_frames
+// sums (segments [frame][channel], `per` = values per channel block).
+void launch_direct(const DirectLaunch& L, cudaStream_t st, double2* coh = nullptr, double* mag = nullptr,
+                   int channels = 1, int64_t per = 0);
 int direct_lanes(int T);  // sample lanes per lag of the direct kernel (1 for long lag spans)
 
 // Utilities.
