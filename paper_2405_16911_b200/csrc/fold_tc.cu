@@ -49,6 +49,9 @@ constexpr int YPLANE = TKB * YF * 2;    // 8 KB: 4 atoms
 #ifndef TC_TNC
 #define TC_TNC 12
 #endif
+#ifndef TC_EXPERIMENT
+#define TC_EXPERIMENT 0
+#endif
 #ifndef TC_NR_SELF
 #define TC_NR_SELF 5
 #endif
@@ -127,38 +130,6 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 
-// 8 fp32 of row k (two 16-byte raw chunks at ra, rb) -> one 16-byte chunk of
-// the hi and lo planes for floats 8*n8 .. 8*n8+7 (MN-major SW128: atom n/64,
-// row k, chunk ((n%64)/8) ^ (k%8)).  Shared-window addresses (LDS/STS).
-// check: also flag a possibly non-finite input -- an inf or NaN makes its lo
-// part (x - hi) NaN, caught by one bf16x2 FMA with zero per pair (finite
-// values give +-0).  A flag is only a hint (so is the lo = -inf of a finite
-// value that rounds to a bf16 infinity): the caller re-checks the fp32 samples.
-__device__ __forceinline__ bool split8(uint32_t ra, uint32_t rb, int n8, int k, uint32_t hi, uint32_t lo, bool zero,
-                                      bool check) {
-    uint32_t h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
-    uint32_t acc = 0;
-    if (!zero) {
-        const float4 a = lds128(ra);
-        const float4 b = lds128(rb);
-        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            h[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
-            const float h0 = __uint_as_float(h[e] << 16), h1 = __uint_as_float(h[e] & 0xffff0000u);
-            l[e] = pack_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
-        }
-        if (check) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) asm("fma.rn.bf16x2 %0, %1, %2, %0;" : "+r"(acc) : "r"(l[e]), "r"(0u));
-        }
-    }
-    const uint32_t off = (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
-    sts128(hi + off, h[0], h[1], h[2], h[3]);
-    sts128(lo + off, l[0], l[1], l[2], l[3]);
-    return (acc & 0x7fff7fffu) != 0u;
-}
-
 // Unit u of a raw stage region (boxes of 32 floats x 16 rows): box a = u / 64;
 // within the box a warp takes one 8-row group and each quarter-warp the row
 // pair (k1, k1 ^ 5), 8-float groups m = 0..3 of both rows.  With the TMA 128B
@@ -186,19 +157,40 @@ __device__ __forceinline__ UnitPos unit_pos(uint32_t raw, int u, bool swz, uint3
     }
     return q;
 }
-// returns the check hint (see split8)
-__device__ __forceinline__ bool convert_unit(uint32_t raw, int u, bool swz, uint32_t pitch, uint32_t hi, uint32_t lo,
-                                             int rows, bool check) {
-    const UnitPos q = unit_pos(raw, u, swz, pitch);
-    return split8(q.ra, q.rb, 4 * q.a + q.m, q.k, hi, lo, q.k >= rows, check);
+// 8 fp32 of row k (a, b = floats 8 n8 .. +3, +4 .. +7, in registers) -> one
+// 16-byte chunk of the hi and lo planes (MN-major SW128: atom n/64, row k,
+// chunk ((n%64)/8) ^ (k%8)).  Shared-window addresses (STS).
+// check: also flag a possibly non-finite input -- an inf or NaN makes its lo
+// part (x - hi) NaN, caught by one bf16x2 FMA with zero per pair (finite
+// values give +-0).  A flag is only a hint (so is the lo = -inf of a finite
+// value that rounds to a bf16 infinity): the caller re-checks the fp32 samples.
+__device__ __forceinline__ bool split8_regs(const float4& a, const float4& b, int n8, int k, uint32_t hi, uint32_t lo,
+                                           bool zero, bool check) {
+    uint32_t h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
+    uint32_t acc = 0;
+    if (!zero) {
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            h[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+            const float h0 = __uint_as_float(h[e] << 16), h1 = __uint_as_float(h[e] & 0xffff0000u);
+            l[e] = pack_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
+        }
+        if (check) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) asm("fma.rn.bf16x2 %0, %1, %2, %0;" : "+r"(acc) : "r"(l[e]), "r"(0u));
+        }
+    }
+    const uint32_t off = (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
+    sts128(hi + off, h[0], h[1], h[2], h[3]);
+    sts128(lo + off, l[0], l[1], l[2], l[3]);
+    return (acc & 0x7fff7fffu) != 0u;
 }
 // Exact re-check of a flagged unit: samples 16a + 4m + j of the window of
 // period p + k, which starts at absolute sample (p + k) Pf + win0; atomicMin
 // of the scan's key.
-__device__ __noinline__ void check_unit_slow(const FoldLaunch& L, uint32_t raw, int u, bool swz, uint32_t pitch,
+__device__ __noinline__ void check_unit_slow(const FoldLaunch& L, const UnitPos q, const float4 A, const float4 B,
                                              int64_t p, int64_t win0, int is_y, int slot) {
-    const UnitPos q = unit_pos(raw, u, swz, pitch);
-    const float4 A = lds128(q.ra), B = lds128(q.rb);
     const float v[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
     for (int j = 3; j >= 0; --j) {
         if (isfinite(v[2 * j]) && isfinite(v[2 * j + 1])) continue;
@@ -213,6 +205,7 @@ __device__ __noinline__ void check_unit_slow(const FoldLaunch& L, uint32_t raw, 
 // read back with cyc_debug_tc_trace (tools/tc_trace.py)
 #ifdef TC_TRACE
 __device__ unsigned long long g_tc_trace[8][128];
+__device__ unsigned long long g_tc_warp[16][64][2];  // per converter warp: (full seen, conv arrive) per stage
 #define TC_MARK(kind, it) \
     if (blockIdx.x == 0 && (it) < 128) g_tc_trace[kind][it] = clock64();
 #else
@@ -340,9 +333,11 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                         const uint64_t dyh = sw128_desc(yh0 + 2 * h * ATOM, ATOM, 1024);
                         const uint64_t dyl = sw128_desc(yl0 + 2 * h * ATOM, ATOM, 1024);
                         const uint32_t dt = tmem + 256 * h;
+#if TC_EXPERIMENT != 1  // diagnostics: 1 = no MMAs (pipeline and conversion only)
                         mma_bf16(dt, dyh, dxh, TC_IDESC, it ? 1u : 0u);
                         mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
                         mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
+#endif
                     }
                 }
                 mma_commit(&planefree[s]);
@@ -362,33 +357,66 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             const int rs = it % G::NR, ps = it % G::NP;
             mbar_wait(&full[rs], (it / G::NR) & 1);
             if (warp == 2 && lane == 0) TC_MARK(3, it);
+#ifdef TC_TRACE
+            if (blockIdx.x == 0 && lane == 0 && it < 64) g_tc_warp[warp][it][0] = clock64();
+#endif
             if (it >= G::NP) mbar_wait(&planefree[ps], ((it / G::NP) - 1) & 1);
             if (warp == 2 && lane == 0) TC_MARK(4, it);
             const uint32_t st = su32(raw_ring + rs * G::RAW);
             const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
             const uint32_t xh = su32(plane_ring + ps * G::PLANE);
             const uint32_t xl = xh + XPLANE;
+            // A thread's units of this stage (2 of x; 0-2 of y when not self):
+            // all raw loads first, then the conversions and plane stores -- the
+            // shared loads are ordered asm, so this is what lets them overlap.
+            constexpr int XU = (XF / 32) * 64, YU = SELF ? 0 : (YF / 32) * 64;
+            constexpr int NU = (XU + 32 * TNC - 1) / (32 * TNC) + (YU + 32 * TNC - 1) / (32 * TNC);
+            UnitPos q[NU];
+            float4 va[NU], vb[NU];
+            bool yu[NU], on[NU];
 #pragma unroll
-            for (int u = ct; u < (XF / 32) * 64; u += 32 * TNC) {
-                const int a = u >> 6;  // warp-uniform
-                if (convert_unit(st, u, swz, XF * 4, xh, xl, rows, chk && a >= cb0 && a < cb0 + 8))
-                    check_unit_slow(L, st, u, swz, XF * 4, tile.p0 + (int64_t)it * TKB, r0 + d, 0, seg.slot);
+            for (int i = 0; i < NU; ++i) {
+                const int nx = (XU + 32 * TNC - 1) / (32 * TNC);
+                const bool isy = i >= nx;
+                const int u = ct + (isy ? i - nx : i) * 32 * TNC;
+                on[i] = u < (isy ? YU : XU);
+                yu[i] = isy;
+                q[i] = unit_pos(isy ? st + XRAW : st, on[i] ? u : 0, swz, isy ? YF * 4 : XF * 4);
             }
-            if (!SELF) {
-                const uint32_t yh = xl + XPLANE;
-                const uint32_t yl = yh + YPLANE;
 #pragma unroll
-                for (int u = ct; u < (YF / 32) * 64; u += 32 * TNC)
-                    if (convert_unit(st + XRAW, u, swz, YF * 4, yh, yl, rows, chk))
-                        check_unit_slow(L, st + XRAW, u, swz, YF * 4, tile.p0 + (int64_t)it * TKB, r0, chk_y,
-                                        seg.slot);
+            for (int i = 0; i < NU; ++i) {
+                va[i] = lds128(q[i].ra);
+                vb[i] = lds128(q[i].rb);
             }
+            // the raw slot is free as soon as its values are in registers: the
+            // producer's next TMA into it overlaps this stage's conversion
+            // (the arrive releases the warp's loads, ordered by __syncwarp)
             __syncwarp();
-            if (lane == 0) mbar_arrive(&rawfree[rs]);  // raw slot reusable (generic reads done)
+            if (lane == 0) mbar_arrive(&rawfree[rs]);
+            uint32_t flags = 0;
+#pragma unroll
+            for (int i = 0; i < NU; ++i) {
+                if (!on[i] || TC_EXPERIMENT == 2) continue;  // diagnostics: 2 = no conversion
+                const uint32_t h0 = yu[i] ? xl + XPLANE : xh, l0 = yu[i] ? xl + XPLANE + YPLANE : xl;
+                const bool ck = chk && (yu[i] || (q[i].a >= cb0 && q[i].a < cb0 + 8));
+                if (split8_regs(va[i], vb[i], 4 * q[i].a + q[i].m, q[i].k, h0, l0, q[i].k >= rows, ck))
+                    flags |= 1u << i;
+            }
+            if (flags) {  // a possibly non-finite sample: exact re-check (rare)
+#pragma unroll
+                for (int i = 0; i < NU; ++i) {
+                    if (!(flags & (1u << i))) continue;
+                    check_unit_slow(L, q[i], va[i], vb[i], tile.p0 + (int64_t)it * TKB, yu[i] ? r0 : r0 + d,
+                                    yu[i] ? chk_y : 0, seg.slot);
+                }
+            }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[ps]);
             if (warp == 2 && lane == 0) TC_MARK(5, it);
+#ifdef TC_TRACE
+            if (blockIdx.x == 0 && lane == 0 && it < 64) g_tc_warp[warp][it][1] = clock64();
+#endif
         }
         // epilogue: warps 2-5 read accumulator 0 (residues 0-63), warps 6-9
         // accumulator 1 (64-127).  Lane m = 2r + a of quarter q holds D[m][*];
@@ -601,5 +629,8 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool sel
 #ifdef TC_TRACE
 extern "C" int cyc_debug_tc_trace(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, cyc::g_tc_trace, sizeof(cyc::g_tc_trace));
+}
+extern "C" int cyc_debug_tc_warps(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, cyc::g_tc_warp, sizeof(cyc::g_tc_warp));
 }
 #endif

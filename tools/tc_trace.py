@@ -29,3 +29,11 @@ for i in range(n):
 d = np.diff(t[1, :n])
 print("mma_go interval mean", d[5:].mean(), "converter full->done mean", (t[5, :n] - t[4, :n])[5:].mean(),
       "pfree wait mean", (t[4, :n] - t[3, :n])[5:].mean())
+
+w = (C.c_ulonglong * (16 * 64 * 2))()
+assert cyc.lib().cyc_debug_tc_warps(w) == 0
+w = np.array(w, dtype=np.int64).reshape(16, 64, 2)
+print("per converter warp (stage 20..23): full-seen / conv-arrive, cycles from kernel start")
+for it in range(20, 24):
+    print(it, "full", [int(w[k, it, 0] - t0) for k in range(2, 14)])
+    print(it, "done", [int(w[k, it, 1] - t0) for k in range(2, 14)], "mma_go", int(t[1, it] - t0))
