@@ -550,9 +550,12 @@ Status Engine::init(const Cfg& cfg) {
             CK(cudaMemsetAsync(mag_, 0, lay_all * sizeof(double), cs_));
         }
     } else {
-        rec_R_.assign(lay_all * 2, 0.0);
-        host_coh_.assign(lay_all * 2, 0.0);
-        host_mag_.assign(lay_all, 0.0);
+        CK(cudaMalloc(&rec_R_, lay_all * sizeof(double2)));
+        CK(cudaMalloc(&coh_, lay_all * sizeof(double2)));
+        CK(cudaMalloc(&mag_, lay_all * sizeof(double)));
+        CK(cudaMemsetAsync(rec_R_, 0, lay_all * sizeof(double2), cs_));
+        CK(cudaMemsetAsync(coh_, 0, lay_all * sizeof(double2), cs_));
+        CK(cudaMemsetAsync(mag_, 0, lay_all * sizeof(double), cs_));
     }
     CK(cudaMalloc(&avg_dev_, (size_t)nflags_ * layout_len_ * sizeof(double2)));
     CK(cudaMallocHost(&avg_host_, layout_len_ * sizeof(double2)));
@@ -623,6 +626,7 @@ Engine::~Engine() {
     cudaFreeHost(frames_host_);
     cudaFree(coh_);
     cudaFree(mag_);
+    cudaFree(rec_R_);
     cudaFree(avg_dev_);
     cudaFree(avg_all_dev_);
     cudaFreeHost(avg_host_);
@@ -1312,8 +1316,15 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
             g.w_scale = w_scale;
             g.slot = (int)s;
         }
-        // every (slot, lag, residue) of S_frames_ is stored by exactly one group: no memset
-        TRY(fold(segs, S_frames_, true));
+        if (small_fold_ok(slots)) {
+            const FoldSeg* d = static_cast<const FoldSeg*>(upload(segs.data(), slots * sizeof(FoldSeg)));
+            launch_fold_small(d, (int)slots, (int)Pf_, f_lo_, lag_hi_ - f_lo_ + 1, t_pad_, S_frames_, cs_);
+            launches_ += 1;
+            TRY(cuda_check(cudaGetLastError(), "small fold launch"));
+        } else {
+            // every (slot, lag, residue) of S_frames_ is stored by exactly one group: no memset
+            TRY(fold(segs, S_frames_, true));
+        }
         TRY(finalize(S_frames_, (int)slots, scale, nullptr, frames_dev_));
     } else {
         std::vector<DirectSeg> segs(slots);
@@ -1335,6 +1346,16 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
         TRY(direct(segs, scale, frames_dev_, accum_in_direct_));
     }
     return Status::ok();
+}
+
+// Few periods per frame and little work in all: one thread per (slot, lag,
+// residue) beats the tiled fold + reduce (C3's emissions: 65 periods x 32 lags
+// x 1024 residues; measured 13 + 5.6 us -> see DESIGN §4).
+bool Engine::small_fold_ok(size_t slots) const {
+    static const bool off = std::getenv("CYC_NO_SMALL_FOLD") != nullptr;  // A/B knob
+    const int64_t maxper = (N_ + Pf_ - 1) / Pf_ + 1;
+    const double work = (double)slots * (double)(lag_hi_ - f_lo_ + 1) * (double)Pf_ * (double)maxper;
+    return !off && use_fold_ && !frames_direct_ && maxper <= 512 && work <= (double)(1 << 23);
 }
 
 bool Engine::graph_eligible(size_t slots) const {
@@ -1448,9 +1469,17 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal));
         cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_);
-        launch_fold(L, cs_);
+        n.small = small_fold_ok(slots);
+        if (n.small)
+            launch_fold_small(reinterpret_cast<const FoldSeg*>(md), (int)slots, (int)Pf_, f_lo_, lag_hi_ - f_lo_ + 1,
+                              t_pad_, n.S, cs_);
+        else
+            launch_fold(L, cs_);
         launch_finalize(Fz, cs_);
-        if (!recursive)
+        if (recursive)
+            launch_recursive_update(n.tables_dev, (int64_t)(slots / c_.channels), c_.channels, (int64_t)per, rec_R_,
+                                    std::pow(c_.lambda, (double)N_), coh_, mag_, cs_);
+        else
             launch_accum_frames(n.tables_dev, (int64_t)(slots / c_.channels), (int64_t)c_.channels * (int64_t)per,
                                 coh_, mag_, cs_);
         cudaMemcpyAsync(n.tables_host, n.tables_dev, slots * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_);
@@ -1486,7 +1515,7 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         hprof_us_[6] += ms * 1e3;
         hprof_us_[7] += 1;
     }
-    launches_ += recursive ? 3 : 4;
+    launches_ += g->small ? 3 : 4;
     *tables = g->tables_host;
     return Status::ok();
 }
@@ -1563,7 +1592,11 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                 accum_in_direct_ = false;
                 TRY(cs);
                 tables = frames_host_;
-                if (c_.mode != CYC_MODE_RECURSIVE && !direct_frames) {
+                if (c_.mode == CYC_MODE_RECURSIVE) {
+                    launch_recursive_update(frames_dev_, (int64_t)(fe - fb), C, (int64_t)per, rec_R_,
+                                            std::pow(c_.lambda, (double)N_), coh_, mag_, cs_);
+                    launches_ += 1;
+                } else if (!direct_frames) {
                     // running average_frames sums; slots are [frame][channel] blocks
                     launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
                     launches_ += 1;
@@ -1571,26 +1604,9 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                 CK(cudaMemcpyAsync(frames_host_, frames_dev_, slots * per * sizeof(double2), cudaMemcpyDeviceToHost,
                                    cs_));
             }
+            // recursive: R_f = lam^N R_{f-1} + (weighted window sum) ran on the
+            // device before the D2H
             CK(cudaStreamSynchronize(cs_));
-            if (c_.mode == CYC_MODE_RECURSIVE) {
-                // R_f = lam^N R_{f-1} + (weighted window sum)
-                const double decay = std::pow(c_.lambda, (double)N_);
-                for (size_t s = 0; s < slots; ++s) {
-                    const int ch = chans[s];
-                    double* R = rec_R_.data() + (size_t)ch * per * 2;
-                    double* hc = host_coh_.data() + (size_t)ch * per * 2;
-                    double* hm = host_mag_.data() + (size_t)ch * per;
-                    double2* v = tables + s * per;
-                    for (size_t i = 0; i < per; ++i) {
-                        R[2 * i] = decay * R[2 * i] + v[i].x;
-                        R[2 * i + 1] = decay * R[2 * i + 1] + v[i].y;
-                        v[i] = make_double2(R[2 * i], R[2 * i + 1]);
-                        hc[2 * i] += v[i].x;
-                        hc[2 * i + 1] += v[i].y;
-                        hm[i] += std::sqrt(v[i].x * v[i].x + v[i].y * v[i].y);  // |R|, no overflow risk here
-                    }
-                }
-            }
             if (c_.emit_frames && !stop) TRY(deliver(slots, fidx, chans, sink, user, stop, tables));
         }
     } else if (use_fold_) {
@@ -2366,22 +2382,8 @@ Status Engine::average(int avg_mode, int flag, int channel, cyc_cf64* out) {
     const int fi = (c_.flags == 3 && flag == CYC_FLAG_CONJ) ? 1 : 0;
     const size_t per = (size_t)nflags_ * layout_len_;
     const double invF = 1.0 / (double)frames_;
-    if (c_.mode == CYC_MODE_RECURSIVE) {
-        const double* hc = host_coh_.data() + ((size_t)channel * per + (size_t)fi * layout_len_) * 2;
-        const double* hm = host_mag_.data() + (size_t)channel * per + (size_t)fi * layout_len_;
-        for (size_t i = 0; i < layout_len_; ++i) {
-            if (avg_mode == CYC_AVG_MAGNITUDE) {
-                out[i].re = hm[i] * invF;
-                out[i].im = 0.0;
-            } else {
-                out[i].re = hc[2 * i] * invF;
-                out[i].im = hc[2 * i + 1] * invF;
-            }
-        }
-        return Status::ok();
-    }
     double2* tmp = avg_host_;  // pinned: the D2H of a table is a DMA, not a staged copy
-    if (c_.emit_frames) {
+    if (c_.emit_frames || c_.mode == CYC_MODE_RECURSIVE) {  // running sums of the emitted tables
         const size_t off = (size_t)channel * per + (size_t)fi * layout_len_;
         if (avg_mode == CYC_AVG_MAGNITUDE) {
             double* m = reinterpret_cast<double*>(avg_host_);
@@ -2585,9 +2587,7 @@ Status Engine::reset() {
     if (dsum_main_) CK(cudaMemsetAsync(dsum_main_, 0, lay_all * sizeof(double2), cs_));
     if (coh_) CK(cudaMemsetAsync(coh_, 0, lay_all * sizeof(double2), cs_));
     if (mag_) CK(cudaMemsetAsync(mag_, 0, lay_all * sizeof(double), cs_));
-    std::fill(rec_R_.begin(), rec_R_.end(), 0.0);
-    std::fill(host_coh_.begin(), host_coh_.end(), 0.0);
-    std::fill(host_mag_.begin(), host_mag_.end(), 0.0);
+    if (rec_R_) CK(cudaMemsetAsync(rec_R_, 0, lay_all * sizeof(double2), cs_));
     for (auto& m : reads_) ev_pool_.push_back(m.ev);
     reads_.clear();
     consumed_ = 0;

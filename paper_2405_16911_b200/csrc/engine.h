@@ -209,6 +209,7 @@ private:
         FoldTile* tiles = nullptr;
         int n_tiles = 0;
         int split = 1;  // tiles per (slot, residue block, lag block)
+        bool small = false;  // one fold_small launch instead of fold + reduce
         double* S = nullptr;
         float* partials = nullptr;
         double2* tables_dev = nullptr;
@@ -221,6 +222,7 @@ private:
     uint64_t hprof_calls_ = 0;
     cudaEvent_t gev_[2] = {};
     bool graph_eligible(size_t slots) const;
+    bool small_fold_ok(size_t slots) const;
     Status run_frame_graph(const std::vector<int64_t>& k0s, const std::vector<int>& chans, bool recursive,
                            double2** tables);
     void fill_frame_segs(FoldSeg* segs, const std::vector<int64_t>& k0s, const std::vector<int>& chans,
@@ -379,8 +381,7 @@ private:
     uint64_t frames_ = 0;
     uint64_t launches_ = 0;
     // recursive mode: running R per (channel, flag) on host, fp64
-    std::vector<double> rec_R_;
-    std::vector<double> host_coh_, host_mag_;  // recursive-mode averages
+    double2* rec_R_ = nullptr;  // recursive-mode state R per (channel, flag, layout) on the device
 };
 
 }  // namespace cyc

@@ -412,6 +412,58 @@ __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB,
     }
 }
 
+__device__ __forceinline__ int64_t floor_div_d(int64_t a, int64_t b) {
+    const int64_t q = a / b;
+    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+// Small per-frame folds (recursive emissions, short per-frame windows): one
+// thread per (slot, lag, residue) sums its few periods straight into S in
+// fp64 -- one launch, no partials and no reduce.  Same weights and the same
+// (c0, c1, c2, c3) = (xr yr, xi yr, xr yi, xi yi) as fold_kernel.
+__global__ void __launch_bounds__(128) fold_small_kernel(const FoldSeg* __restrict__ segs, int Pf, int lag_lo,
+                                                         int t_pad, double* __restrict__ S) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y, slot_i = blockIdx.z;
+    if (r >= Pf) return;
+    const FoldSeg g = segs[slot_i];
+    // periods p with n = p Pf + r in [n_start, n_end)
+    const int64_t pa = floor_div_d(g.n_start - r + Pf - 1, Pf);
+    const int64_t pb = floor_div_d(g.n_end - 1 - r, Pf) + 1;
+    const bool weighted = g.w_log2 != 0.f;
+    double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    int64_t n = pa * Pf + r;
+    const int64_t lag = (int64_t)lag_lo + t;
+    auto acc = [&](float2 yv, const float2 xv, int64_t nn) {
+        if (weighted) {
+            const float w = g.w_scale * exp2f((float)(g.w_ref - nn) * g.w_log2);
+            yv.x *= w;
+            yv.y *= w;
+        }
+        c0 = fma((double)xv.x, (double)yv.x, c0);
+        c1 = fma((double)xv.y, (double)yv.x, c1);
+        c2 = fma((double)xv.x, (double)yv.y, c2);
+        c3 = fma((double)xv.y, (double)yv.y, c3);
+    };
+    // 8 periods' loads in flight before their FMAs (the loop is latency-bound)
+    constexpr int U = 8;
+    int64_t p = pa;
+    for (; p + U <= pb; p += U, n += U * (int64_t)Pf) {
+        float2 yv[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            yv[u] = __ldg(g.y + ((uint64_t)(n + u * (int64_t)Pf) & g.mask));
+            xv[u] = __ldg(g.x + ((uint64_t)(n + u * (int64_t)Pf + lag) & g.mask));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc(yv[u], xv[u], n + u * (int64_t)Pf);
+    }
+    for (; p < pb; ++p, n += Pf) acc(__ldg(g.y + ((uint64_t)n & g.mask)), __ldg(g.x + ((uint64_t)(n + lag) & g.mask)), n);
+    double2* d = reinterpret_cast<double2*>(S + (((size_t)g.slot * t_pad + t) * (size_t)Pf + (size_t)r) * 4);
+    d[0] = make_double2(c0, c1);
+    d[1] = make_double2(c2, c3);
+}
+
 template <int LW>
 void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, const FoldInline* inl,
               cudaEvent_t before_reduce) {
@@ -432,6 +484,13 @@ void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t
 }
 
 }  // namespace
+
+void launch_fold_small(const FoldSeg* segs_dev, int n_slots, int Pf, int lag_lo, int t_span, int t_pad, double* S,
+                       cudaStream_t st) {
+    if (n_slots <= 0 || t_span <= 0) return;
+    fold_small_kernel<<<dim3((unsigned)((Pf + 127) / 128), (unsigned)t_span, (unsigned)n_slots), 128, 0, st>>>(
+        segs_dev, Pf, lag_lo, t_pad, S);
+}
 
 void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, const FoldInline* inl,
                  cudaEvent_t before_reduce) {

@@ -58,7 +58,16 @@ constexpr int YPLANE = TKB * YF * 2;    // 8 KB: 4 atoms
 #ifndef TC_NP_SELF
 #define TC_NP_SELF 4
 #endif
+#ifndef TC_GROUPS
+#define TC_GROUPS 1
+#endif
 constexpr int TNC = TC_TNC;             // converter / epilogue warps (warps 2 .. TNC+1), a multiple of 4
+// Converter stage groups: group g (warps 2 + g*TGW ..) converts stages it = g mod TG,
+// so one warp's per-stage latency chain (barrier waits, shared loads, fence,
+// arrive) is spread over TG stages of the pipeline.
+constexpr int TG = TC_GROUPS;
+constexpr int TGW = TNC / TG;
+static_assert(TNC % TG == 0, "converter groups");
 constexpr int TNT = 64 + 32 * TNC;      // + warp 0 producer, warp 1 MMA issuer
 // Two rings: raw fp32 stages (producer -> converters, freed after conversion)
 // and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).
@@ -229,10 +238,10 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         s_seg = D.segs[s_tile.seg];
         for (int s = 0; s < G::NR; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&rawfree[s], TNC);
+            mbar_init(&rawfree[s], TGW);
         }
         for (int s = 0; s < G::NP; ++s) {
-            mbar_init(&conv[s], TNC);
+            mbar_init(&conv[s], TGW);
             mbar_init(&planefree[s], 1);
         }
         mbar_init(&done, 1);
@@ -346,14 +355,15 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             mma_commit(&done);
         }
     } else {
-        const int ct = threadIdx.x - 64;  // 0 .. 32*TNC-1
+        const int grp = (warp - 2) / TGW;
+        const int ct = threadIdx.x - 64 - 32 * TGW * grp;  // 0 .. 32*TGW-1 within the group
         // fused check (lb = 0 tiles): the 128 samples of each period that this
         // tile's residues own -- x boxes [cb0, cb0 + 8) (self: the y part of
         // the x window; else x samples [0, 128)), and the y window
         const bool chk = L.chk_key != nullptr && tile.lb == 0;
         const int cb0 = SELF ? (int)(-d) / 16 : 0;
         const int chk_y = (seg.x != seg.y) ? 1 : 0;
-        for (int it = 0; it < nst; ++it) {
+        for (int it = grp; it < nst; it += TG) {
             const int rs = it % G::NR, ps = it % G::NP;
             mbar_wait(&full[rs], (it / G::NR) & 1);
             if (warp == 2 && lane == 0) TC_MARK(3, it);
@@ -370,15 +380,15 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             // all raw loads first, then the conversions and plane stores -- the
             // shared loads are ordered asm, so this is what lets them overlap.
             constexpr int XU = (XF / 32) * 64, YU = SELF ? 0 : (YF / 32) * 64;
-            constexpr int NU = (XU + 32 * TNC - 1) / (32 * TNC) + (YU + 32 * TNC - 1) / (32 * TNC);
+            constexpr int NU = (XU + 32 * TGW - 1) / (32 * TGW) + (YU + 32 * TGW - 1) / (32 * TGW);
             UnitPos q[NU];
             float4 va[NU], vb[NU];
             bool yu[NU], on[NU];
 #pragma unroll
             for (int i = 0; i < NU; ++i) {
-                const int nx = (XU + 32 * TNC - 1) / (32 * TNC);
+                const int nx = (XU + 32 * TGW - 1) / (32 * TGW);
                 const bool isy = i >= nx;
-                const int u = ct + (isy ? i - nx : i) * 32 * TNC;
+                const int u = ct + (isy ? i - nx : i) * 32 * TGW;
                 on[i] = u < (isy ? YU : XU);
                 yu[i] = isy;
                 q[i] = unit_pos(isy ? st + XRAW : st, on[i] ? u : 0, swz, isy ? YF * 4 : XF * 4);

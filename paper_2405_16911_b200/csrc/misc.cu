@@ -32,6 +32,31 @@ __global__ void accum_frames_kernel(const double2* frames, int64_t n_frames, int
     }
 }
 
+// Recursive emissions: the frames of a batch are slots
+// [frame][channel] of weighted window sums v; in frame order per channel,
+// R = decay * R + v (R_f = lam^N R_{f-1} + window sum), the emitted table is
+// R, and the running average_frames sums take R and |R|.
+__global__ void recursive_update_kernel(double2* frames, int64_t n_frames, int channels, int64_t per, double2* R,
+                                        double decay, double2* coh, double* mag) {
+    const int64_t len = (int64_t)channels * per;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        double2 r = R[i], c = coh[i];
+        double m = mag[i];
+        for (int64_t f = 0; f < n_frames; ++f) {
+            double2& v = frames[f * len + i];
+            r.x = decay * r.x + v.x;
+            r.y = decay * r.y + v.y;
+            v = r;
+            c.x += r.x;
+            c.y += r.y;
+            m += hypot(r.x, r.y);
+        }
+        R[i] = r;
+        coh[i] = c;
+        mag[i] = m;
+    }
+}
+
 // Whole-chunk finite scan (proj/src/estimator.cpp:43-52): the smallest key
 // 2*i (x) / 2*i+1 (y) names the first offending sample in the reference's
 // scan order (x before y at each index).
@@ -127,6 +152,12 @@ void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st, 
 void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len, double2* coh, double* mag,
                          cudaStream_t st) {
     if (n_frames > 0 && len > 0) accum_frames_kernel<<<grid_for(len, 256), 256, 0, st>>>(frames, n_frames, len, coh, mag);
+}
+void launch_recursive_update(double2* frames, int64_t n_frames, int channels, int64_t per, double2* R, double decay,
+                             double2* coh, double* mag, cudaStream_t st) {
+    if (n_frames > 0 && per > 0)
+        recursive_update_kernel<<<grid_for((int64_t)channels * per, 256), 256, 0, st>>>(frames, n_frames, channels, per,
+                                                                                     R, decay, coh, mag);
 }
 int launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
                         unsigned long long* key, cudaStream_t st, int nch, int64_t pitch) {
