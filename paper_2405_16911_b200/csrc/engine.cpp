@@ -11,6 +11,9 @@
 #include <cstring>
 #include <numeric>
 #include <thread>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 namespace cyc {
 
@@ -124,17 +127,47 @@ inline bool screen(const cyc_cf64* p, size_t i0, size_t i1) {
 // Small host chunks: copy n samples of every channel into the pinned staging
 // (channel rows n apart) and screen them in the same pass (true: some
 // component may be non-finite) -- one read of the caller's memory, not two.
-inline bool copy_screen(float2* dst, const cyc_cf32* src, size_t n, int channels) {
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
-    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
-    const size_t m = 2 * n * (size_t)channels;
+inline uint32_t copy_screen_scalar(uint32_t* d, const uint32_t* s, size_t m) {
     uint32_t acc = 0;
     for (size_t i = 0; i < m; ++i) {
         const uint32_t w = s[i];
         d[i] = w;
         acc |= (uint32_t)((w & 0x7f800000u) == 0x7f800000u);
     }
-    return acc != 0;
+    return acc;
+}
+#if defined(__x86_64__)
+// The staging is only read back by the DMA engine: non-temporal stores skip
+// the read-for-ownership of the destination lines (a third of the memory
+// traffic of a cached copy; the copy is host-memory-bound for cold input).
+__attribute__((target("avx2"))) uint32_t copy_screen_avx2(uint32_t* d, const uint32_t* s, size_t m) {
+    uint32_t acc = 0;
+    size_t i = 0;
+    const size_t head = ((32 - ((uintptr_t)d & 31)) & 31) / 4;
+    if (((uintptr_t)d & 3) != 0 || head > m) return copy_screen_scalar(d, s, m);
+    acc |= copy_screen_scalar(d, s, head);
+    i = head;
+    const __m256i em = _mm256_set1_epi32(0x7f800000);
+    __m256i va = _mm256_setzero_si256();
+    for (; i + 8 <= m; i += 8) {
+        const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+        va = _mm256_or_si256(va, _mm256_cmpeq_epi32(_mm256_and_si256(v, em), em));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), v);
+    }
+    _mm_sfence();  // the NT stores are visible before the DMA is queued
+    acc |= copy_screen_scalar(d + i, s + i, m - i);
+    return acc | (uint32_t)!_mm256_testz_si256(va, va);
+}
+#endif
+inline bool copy_screen(float2* dst, const cyc_cf32* src, size_t n, int channels) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    const size_t m = 2 * n * (size_t)channels;
+#if defined(__x86_64__)
+    static const bool avx2 = __builtin_cpu_supports("avx2") && std::getenv("CYC_NO_NT_COPY") == nullptr;
+    if (avx2 && m >= 1024) return copy_screen_avx2(d, s, m) != 0;
+#endif
+    return copy_screen_scalar(d, s, m) != 0;
 }
 
 template <typename T>

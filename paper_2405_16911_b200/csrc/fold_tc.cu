@@ -79,6 +79,9 @@ struct TcGeo {
     static constexpr int NP = SELF ? TC_NP_SELF : 2;
     static constexpr int SMEM = NR * RAW + NP * PLANE + 1024;
     static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
+    // a ring slot must always be converted by the same stage group, or a group
+    // running ahead could pass a barrier's phase parity one phase early
+    static_assert(TG == 1 || (NR % TG == 0 && NP % TG == 0), "converter groups need ring depths divisible by TG");
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
