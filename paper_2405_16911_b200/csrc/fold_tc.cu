@@ -194,9 +194,13 @@ __device__ __forceinline__ bool split8_regs(const float4& a, const float4& b, in
         }
     }
     const uint32_t off = (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
+#if TC_EXPERIMENT == 4  // diagnostics: conversion without the plane stores
+    return ((h[0] ^ h[1] ^ h[2] ^ h[3] ^ l[0] ^ l[1] ^ l[2] ^ l[3]) == 0x12345678u) | ((acc & 0x7fff7fffu) != 0u);
+#else
     sts128(hi + off, h[0], h[1], h[2], h[3]);
     sts128(lo + off, l[0], l[1], l[2], l[3]);
     return (acc & 0x7fff7fffu) != 0u;
+#endif
 }
 // Exact re-check of a flagged unit: samples 16a + 4m + j of the window of
 // period p + k, which starts at absolute sample (p + k) Pf + win0; atomicMin
@@ -398,8 +402,13 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             }
 #pragma unroll
             for (int i = 0; i < NU; ++i) {
+#if TC_EXPERIMENT == 5  // diagnostics: conversion and stores without the raw loads
+                va[i] = make_float4(__int_as_float(q[i].ra), 1.f, 2.f, 3.f);
+                vb[i] = make_float4(__int_as_float(q[i].rb), 1.f, 2.f, 3.f);
+#else
                 va[i] = lds128(q[i].ra);
                 vb[i] = lds128(q[i].rb);
+#endif
             }
             // the raw slot is free as soon as its values are in registers: the
             // producer's next TMA into it overlaps this stage's conversion
@@ -423,7 +432,9 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                                     yu[i] ? chk_y : 0, seg.slot);
                 }
             }
+#if TC_EXPERIMENT != 3  // diagnostics: 3 = no proxy fence before the hand-off
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[ps]);
             if (warp == 2 && lane == 0) TC_MARK(5, it);
