@@ -1500,22 +1500,34 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         prepare_fold_kernels();  // attributes are set outside the capture
         prepare_finalize_kernels();
         cudaGraph_t graph;
-        CK(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal));
-        cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_);
         n.small = small_fold_ok(slots);
+        // small recursive emissions: no copy nodes -- the fold reads the
+        // per-replay descriptors from mapped pinned memory, the finalize's rows
+        // (constant per shape) are copied once here, and the recursion writes
+        // the emitted tables straight into mapped pinned memory
+        static const bool no_zc = std::getenv("CYC_NO_ZERO_COPY") != nullptr;  // A/B knob
+        n.zero_copy = n.small && recursive && !no_zc;
+        if (n.zero_copy) {
+            CK(cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_));
+            CK(cudaStreamSynchronize(cs_));
+        }
+        CK(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal));
+        if (!n.zero_copy) cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_);
         if (n.small)
-            launch_fold_small(reinterpret_cast<const FoldSeg*>(md), (int)slots, (int)Pf_, f_lo_, lag_hi_ - f_lo_ + 1,
-                              t_pad_, n.S, cs_);
+            launch_fold_small(n.zero_copy ? n.segs : reinterpret_cast<const FoldSeg*>(md), (int)slots, (int)Pf_,
+                              f_lo_, lag_hi_ - f_lo_ + 1, t_pad_, n.S, cs_);
         else
             launch_fold(L, cs_);
         launch_finalize(Fz, cs_);
         if (recursive)
             launch_recursive_update(n.tables_dev, (int64_t)(slots / c_.channels), c_.channels, (int64_t)per, rec_R_,
-                                    std::pow(c_.lambda, (double)N_), coh_, mag_, cs_);
+                                    std::pow(c_.lambda, (double)N_), coh_, mag_, cs_,
+                                    n.zero_copy ? n.tables_host : nullptr);
         else
             launch_accum_frames(n.tables_dev, (int64_t)(slots / c_.channels), (int64_t)c_.channels * (int64_t)per,
                                 coh_, mag_, cs_);
-        cudaMemcpyAsync(n.tables_host, n.tables_dev, slots * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_);
+        if (!n.zero_copy)
+            cudaMemcpyAsync(n.tables_host, n.tables_dev, slots * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_);
         CK(cudaStreamEndCapture(cs_, &graph));
         CK(cudaGraphInstantiate(&n.exec, graph, 0));
         cudaGraphDestroy(graph);

@@ -209,7 +209,8 @@ private:
         FoldTile* tiles = nullptr;
         int n_tiles = 0;
         int split = 1;  // tiles per (slot, residue block, lag block)
-        bool small = false;  // one fold_small launch instead of fold + reduce
+        bool small = false;      // one fold_small launch instead of fold + reduce
+        bool zero_copy = false;  // no copy nodes: mapped descriptors in, mapped tables out
         double* S = nullptr;
         float* partials = nullptr;
         double2* tables_dev = nullptr;

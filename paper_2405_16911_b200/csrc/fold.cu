@@ -412,9 +412,13 @@ __global__ void fold_reduce_kernel(FoldLaunch L, int TB, int RB,
     }
 }
 
+// floor(a / b) for b > 0 without the 64-bit integer division routine: a double
+// estimate, corrected exactly with integer multiplies
 __device__ __forceinline__ int64_t floor_div_d(int64_t a, int64_t b) {
-    const int64_t q = a / b;
-    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+    int64_t q = (int64_t)floor((double)a / (double)b);
+    while (q * b > a) --q;
+    while ((q + 1) * b <= a) ++q;
+    return q;
 }
 
 // Small per-frame folds (recursive emissions, short per-frame windows): one
@@ -423,10 +427,17 @@ __device__ __forceinline__ int64_t floor_div_d(int64_t a, int64_t b) {
 // (c0, c1, c2, c3) = (xr yr, xi yr, xr yi, xi yi) as fold_kernel.
 __global__ void __launch_bounds__(128) fold_small_kernel(const FoldSeg* __restrict__ segs, int Pf, int lag_lo,
                                                          int t_pad, double* __restrict__ S) {
+    // segs may be mapped host memory (a replayed emission graph rewrites them
+    // in place instead of copying them): one read per CTA
+    __shared__ FoldSeg s_g;
+    static_assert(sizeof(FoldSeg) % 4 == 0 && sizeof(FoldSeg) / 4 <= 128, "FoldSeg words");
+    if (threadIdx.x < sizeof(FoldSeg) / 4)
+        reinterpret_cast<uint32_t*>(&s_g)[threadIdx.x] = reinterpret_cast<const uint32_t*>(segs + blockIdx.z)[threadIdx.x];
+    __syncthreads();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    const int t = blockIdx.y, slot_i = blockIdx.z;
+    const int t = blockIdx.y;
     if (r >= Pf) return;
-    const FoldSeg g = segs[slot_i];
+    const FoldSeg& g = s_g;
     // periods p with n = p Pf + r in [n_start, n_end)
     const int64_t pa = floor_div_d(g.n_start - r + Pf - 1, Pf);
     const int64_t pb = floor_div_d(g.n_end - 1 - r, Pf) + 1;

@@ -91,7 +91,7 @@ struct FoldInline {
 void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr,
                  const FoldInline* inl = nullptr, cudaEvent_t before_reduce = nullptr);
 
-// Small per-frame folds: slots segs_dev[0 .. n_slots) (device memory), lags
+// Small per-frame folds: slots segs_dev[0 .. n_slots) (device or mapped host memory), lags
 // lag_lo .. lag_lo + t_span - 1, stored (not accumulated) into S rows 0 .. t_span-1
 // of each seg's slot in fp64.  One thread per (slot, lag, residue).
 void launch_fold_small(const FoldSeg* segs_dev, int n_slots, int Pf, int lag_lo, int t_span, int t_pad, double* S,
@@ -227,8 +227,9 @@ void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len,
                          double2* coh, double* mag, cudaStream_t st);
 // Recursive emissions: per channel, in frame order, R = decay*R + frame; the
 // frame becomes R; coh += R, mag += |R|.  frames are [frame][channel][per].
+// host_out (mapped pinned, optional): the emitted tables are also written there.
 void launch_recursive_update(double2* frames, int64_t n_frames, int channels, int64_t per, double2* R, double decay,
-                             double2* coh, double* mag, cudaStream_t st);
+                             double2* coh, double* mag, cudaStream_t st, double2* host_out = nullptr);
 // First non-finite sample -> atomicMin(*key);
 // key = (2*(base+i) + is_y) * channels + ch  -- smallest = reference scan order.
 // returns the number of kernels launched; nch > 1 scans channels ch .. ch+nch-1

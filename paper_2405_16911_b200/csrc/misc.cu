@@ -37,7 +37,7 @@ __global__ void accum_frames_kernel(const double2* frames, int64_t n_frames, int
 // R = decay * R + v (R_f = lam^N R_{f-1} + window sum), the emitted table is
 // R, and the running average_frames sums take R and |R|.
 __global__ void recursive_update_kernel(double2* frames, int64_t n_frames, int channels, int64_t per, double2* R,
-                                        double decay, double2* coh, double* mag) {
+                                        double decay, double2* coh, double* mag, double2* host_out) {
     const int64_t len = (int64_t)channels * per;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
         double2 r = R[i], c = coh[i];
@@ -47,6 +47,7 @@ __global__ void recursive_update_kernel(double2* frames, int64_t n_frames, int c
             r.x = decay * r.x + v.x;
             r.y = decay * r.y + v.y;
             v = r;
+            if (host_out) host_out[f * len + i] = r;  // mapped pinned memory: no D2H copy node
             c.x += r.x;
             c.y += r.y;
             m += hypot(r.x, r.y);
@@ -154,10 +155,10 @@ void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len, d
     if (n_frames > 0 && len > 0) accum_frames_kernel<<<grid_for(len, 256), 256, 0, st>>>(frames, n_frames, len, coh, mag);
 }
 void launch_recursive_update(double2* frames, int64_t n_frames, int channels, int64_t per, double2* R, double decay,
-                             double2* coh, double* mag, cudaStream_t st) {
+                             double2* coh, double* mag, cudaStream_t st, double2* host_out) {
     if (n_frames > 0 && per > 0)
         recursive_update_kernel<<<grid_for((int64_t)channels * per, 256), 256, 0, st>>>(frames, n_frames, channels, per,
-                                                                                     R, decay, coh, mag);
+                                                                                     R, decay, coh, mag, host_out);
 }
 int launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
                         unsigned long long* key, cudaStream_t st, int nch, int64_t pitch) {
