@@ -183,8 +183,10 @@ __global__ void direct_reduce_accum_kernel(const __grid_constant__ DirectLaunch 
                 im += v.y;
             }
             const double2 v = make_double2(re * L.scale, im * L.scale);
-            L.out[(size_t)si * L.out_block_stride + (size_t)fi * L.out_flag_stride + (size_t)a * L.stride_a +
-                  (size_t)t * L.stride_t] = v;
+            const size_t o = (size_t)si * L.out_block_stride + (size_t)fi * L.out_flag_stride +
+                             (size_t)a * L.stride_a + (size_t)t * L.stride_t;
+            L.out[o] = v;
+            if (L.out_host) L.out_host[o] = v;
             c.x += v.x;
             c.y += v.y;
             m += hypot(v.x, v.y);

@@ -1315,8 +1315,11 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     L.stride_a = stride_a_;
     L.stride_t = stride_t_;
     L.scale = scale;
-    if (accum)  // per-frame batch: the reduce also adds the frames to the running sums
+    if (accum) {  // per-frame batch: the reduce also adds the frames to the running sums
+        // ... and writes the tables straight into the pinned host copy
+        L.out_host = (direct_host_out_ && out == frames_dev_) ? frames_host_ : nullptr;
         launch_direct(L, cs_, coh_, mag_, c_.channels, (int64_t)nflags_ * (int64_t)layout_len_);
+    }
     else
         launch_direct(L, cs_);
     launches_ += 2;
@@ -1632,9 +1635,13 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                 // accumulate, D2H) instead of five launches and a memcpy
                 TRY(run_frame_graph(k0s, chans, c_.mode == CYC_MODE_RECURSIVE, &tables));
             } else {
+                static const bool no_zc = std::getenv("CYC_NO_ZERO_COPY") != nullptr;  // A/B knob
                 accum_in_direct_ = direct_frames;
+                direct_host_out_ = direct_frames && !no_zc;
                 const Status cs = compute_frames(k0s, chans, c_.mode == CYC_MODE_RECURSIVE);
                 accum_in_direct_ = false;
+                const bool copied = direct_host_out_;
+                direct_host_out_ = false;
                 TRY(cs);
                 tables = frames_host_;
                 if (c_.mode == CYC_MODE_RECURSIVE) {
@@ -1646,8 +1653,9 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                     launch_accum_frames(frames_dev_, (int64_t)(fe - fb), (int64_t)C * (int64_t)per, coh_, mag_, cs_);
                     launches_ += 1;
                 }
-                CK(cudaMemcpyAsync(frames_host_, frames_dev_, slots * per * sizeof(double2), cudaMemcpyDeviceToHost,
-                                   cs_));
+                if (!copied)
+                    CK(cudaMemcpyAsync(frames_host_, frames_dev_, slots * per * sizeof(double2),
+                                       cudaMemcpyDeviceToHost, cs_));
             }
             // recursive: R_f = lam^N R_{f-1} + (weighted window sum) ran on the
             // device before the D2H

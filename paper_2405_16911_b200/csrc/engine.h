@@ -124,6 +124,7 @@ private:
                     double2* out, cudaStream_t st = nullptr);
     // Direct contraction of segs into out tables (out_block = seg.out_block).
     Status direct(const std::vector<DirectSeg>& segs, double scale, double2* out, bool accum = false);
+    bool direct_host_out_ = false;  // the next direct per-frame reduce also writes frames_host_ (mapped)
     bool accum_in_direct_ = false;  // compute_frames' direct reduce also updates coh_/mag_
 
     // Per-frame tables for the given (k0, channel) windows -> frames_dev_ (fp64).

@@ -209,6 +209,7 @@ struct DirectLaunch {
     int flags;
     float* partials;            // [n_segs][A][splits][2 flags][T] float2
     double2* out;               // [out_block][flag_index][...]
+    double2* out_host;          // optional mapped pinned mirror of `out` (per-frame tables: no D2H copy)
     int64_t out_block_stride, out_flag_stride, stride_a, stride_t;
     double scale;
 };
