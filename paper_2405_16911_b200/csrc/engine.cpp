@@ -509,6 +509,7 @@ Status Engine::plan(const Cfg& cfg) {
         int lg = 0;
         while ((int64_t(1) << lg) < Pf_) ++lg;
         use_fft_ = is_pow2(Pf_) && Pf_ <= 8192 && A_ > 2 * lg;
+        if (const char* f = std::getenv("CYC_FINALIZE")) use_fft_ = use_fft_ && std::strcmp(f, "dft") != 0;  // A/B knob
         // short Set-mode frames: one direct kernel per frame batch beats the
         // fold + reduce + DFT chain, whose small launches are latency-bound
         // (C1: 4096-sample frames x 10 alphas x 31 lags)
