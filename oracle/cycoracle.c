@@ -277,6 +277,9 @@ int orc_block_fold(const float* xf, const float* yf, size_t len, const int64_t* 
     /* four real correlations per (lag, residue): sum xr*yr, xi*yi, xi*yr, xr*yi */
     double* S = (double*)calloc(n_lags * Pz * 4, sizeof(double));
     if (!S) return -1;
+    /* lags are independent (each keeps the sequential sample-order sum), so
+       the production-size parity tests may fold them on all host cores */
+#pragma omp parallel for schedule(dynamic, 1)
     for (size_t t = 0; t < n_lags; ++t) {
         double* St = S + t * Pz * 4;
         const long long lag = lags[t];
@@ -297,6 +300,7 @@ int orc_block_fold(const float* xf, const float* yf, size_t len, const int64_t* 
     cd* tw = (cd*)malloc(sizeof(cd) * Pz);
     for (size_t r = 0; r < Pz; ++r) tw[r] = cpolar(-two_pi * (double)r / (double)P);
     const double inv = 1.0 / (double)count;
+#pragma omp parallel for schedule(dynamic, 1)
     for (size_t a = 0; a < n_alphas; ++a) {
         const int64_t kk = ((k[a] % P) + P) % P;
         for (size_t t = 0; t < n_lags; ++t) {
@@ -342,10 +346,12 @@ int orc_recursive(const double* x, const double* y, size_t len, const double* al
     const size_t cells = n_alphas * n_lags;
     cd* R = (cd*)calloc(cells, sizeof(cd));
     const size_t n_end = (size_t)m_minus + E * emit_every;
-    size_t e = 0;
-    for (size_t n = (size_t)m_minus; n < n_end; ++n) {
-        cd ys = cld(y, n);
-        for (size_t a = 0; a < n_alphas; ++a) {
+    /* alphas are independent recursions: one per thread, same per-sample order */
+#pragma omp parallel for schedule(dynamic, 1)
+    for (size_t a = 0; a < n_alphas; ++a) {
+        size_t e = 0;
+        for (size_t n = (size_t)m_minus; n < n_end; ++n) {
+            cd ys = cld(y, n);
             cd ph = cpolar(-two_pi * alphas[a] * (double)n);
             for (size_t t = 0; t < n_lags; ++t) {
                 cd xs = cld(x, (size_t)((long long)n + lags[t]));
@@ -355,10 +361,13 @@ int orc_recursive(const double* x, const double* y, size_t len, const double* al
                 r->re = lambda * r->re + (1.0 - lambda) * v.re;
                 r->im = lambda * r->im + (1.0 - lambda) * v.im;
             }
-        }
-        if (n + 1 == (size_t)m_minus + (e + 1) * emit_every) {
-            memcpy(out + 2 * e * cells, R, sizeof(cd) * cells);
-            ++e;
+            if (n + 1 == (size_t)m_minus + (e + 1) * emit_every) {
+                for (size_t t = 0; t < n_lags; ++t) {
+                    out[2 * (e * cells + a * n_lags + t)] = R[a * n_lags + t].re;
+                    out[2 * (e * cells + a * n_lags + t) + 1] = R[a * n_lags + t].im;
+                }
+                ++e;
+            }
         }
     }
     free(R);

@@ -21,8 +21,18 @@ LIB = os.path.join(HERE, "libcycb200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# CYC_NVCC_EXTRA (diagnostic builds: traces, ablations) never touches the
+# product library: its objects and library go to a directory keyed by a hash of
+# the extra flags, loaded with CYC_LIB=<that path>.
+EXTRA = os.environ.get("CYC_NVCC_EXTRA", "").split()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("CYC_NVCC_EXTRA", "").split()
+         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + EXTRA
+if EXTRA:
+    import hashlib
+    _tag = hashlib.sha1(" ".join(EXTRA).encode()).hexdigest()[:10]
+    BUILD = os.path.join(HERE, "_diag", _tag)
+    LIB = os.path.join(BUILD, "libcycb200.so")
+    FLAGS += ["-DTC_DIAG_BUILD"]
 
 
 def sources() -> list[str]:
@@ -37,7 +47,7 @@ def headers() -> list[str]:
 
 def _compile(src: str, force: bool) -> str:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    newest_dep = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in headers()])
+    newest_dep = max([os.path.getmtime(src), os.path.getmtime(__file__)] + [os.path.getmtime(h) for h in headers()])
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-x", "cu" if src.endswith(".cu") else "c++", "-c", src, "-o", obj]
@@ -80,4 +90,5 @@ def build_tools(force: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv))
-    print(build_tools())
+    if not EXTRA:
+        print(build_tools())

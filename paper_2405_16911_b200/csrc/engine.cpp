@@ -1044,7 +1044,10 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         // one launch: up to FI_GROUPS groups of one kind, tiles ~ whole waves of 1 CTA/SM
         // Each tile folds at most TC_MAX_PERIODS periods (fp32 TMEM accumulation
         // error grows with the count: ~1e-5 relative at 2048).
-        constexpr int64_t TC_MAX_PERIODS = 2048;
+        static const int64_t TC_MAX_PERIODS = [] {  // CYC_TC_MAXP: accuracy probe knob
+            const char* e = std::getenv("CYC_TC_MAXP");
+            return e ? std::max<int64_t>(64, std::atoll(e)) : (int64_t)2048;
+        }();
         auto min_tiles = [&](const G& gr) { return (int)ceil_div(gr.p1 - gr.p0, TC_MAX_PERIODS); };
         const bool self = is_self(groups[g0]);
         size_t ng = 0;

@@ -52,6 +52,9 @@ constexpr int YPLANE = TKB * YF * 2;    // 8 KB: 4 atoms
 #ifndef TC_EXPERIMENT
 #define TC_EXPERIMENT 0
 #endif
+#if TC_EXPERIMENT != 0 && !defined(TC_DIAG_BUILD)
+#error "TC_EXPERIMENT builds give wrong results: build them with CYC_NVCC_EXTRA (separate _diag/ library)"
+#endif
 #ifndef TC_NR_SELF
 #define TC_NR_SELF 5
 #endif

@@ -1,15 +1,18 @@
 """Pipeline trace of the tensor-core fold (CTA 0): run on a -DTC_TRACE build
-(CYC_NVCC_EXTRA=-DTC_TRACE, forced rebuild) -- diagnostics only."""
+(CYC_NVCC_EXTRA=-DTC_TRACE build under _diag/, loaded with CYC_LIB) -- diagnostics only."""
 import ctypes as C
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2405_16911_b200 as cyc
-L = 1 << 24
+# TRACE_CFG=c5: Pf = 8192, lags 0..255 (the trace keeps the last launch's CTA 0: a non-self lag block)
+c5 = os.environ.get("TRACE_CFG") == "c5"
+L = 1 << (26 if c5 else 24)
 rng = np.random.default_rng(0)
 x = (rng.standard_normal(L) + 1j * rng.standard_normal(L)).astype(np.complex64)
-cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=1024, lag_spec=cyc.LagSpec.Explicit(range(64)),
+cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=8192 if c5 else 1024,
+                          lag_spec=cyc.LagSpec.Explicit(range(256 if c5 else 64)),
                           flags=cyc.Flags.BOTH, emit_frames=False)
 est = cyc.CyclicCorrelator(cfg)
 dx = torch.from_numpy(x.view(np.float32)).cuda()
@@ -28,7 +31,8 @@ for i in range(n):
     print(f"{i:5d} " + " ".join(f"{(t[k, i] - t0 if t[k, i] else -1):9d}" for k in range(6)))
 d = np.diff(t[1, :n])
 print("mma_go interval mean", d[5:].mean(), "converter full->done mean", (t[5, :n] - t[4, :n])[5:].mean(),
-      "pfree wait mean", (t[4, :n] - t[3, :n])[5:].mean())
+      "pfree wait mean", (t[4, :n] - t[3, :n])[5:].mean(), "tma issue->full mean", (t[3, :n] - t[0, :n])[5:].mean(),
+      "issue interval mean", np.diff(t[0, :n])[5:].mean())
 
 w = (C.c_ulonglong * (16 * 64 * 2))()
 assert cyc.lib().cyc_debug_tc_warps(w) == 0
