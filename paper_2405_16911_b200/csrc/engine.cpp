@@ -49,6 +49,25 @@ int64_t next_pow2(int64_t v) {
 
 bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
+// TMEM accumulation chunk (stages of 16 periods) for tensor-core tiles of at
+// most `max_periods` periods: whole tiles up to 64 stages, else equal chunks
+// of about 32 stages.  The tensor core's truncating accumulation biases a cell
+// by ~7e-8 of its value per stage, and the dropped lo*lo term by ~2e-6: the
+// worst cell (the lag-0 power) measured 6.4e-6 of the mean power at C2's
+// 57-stage tiles and 4.3-4.6e-6 with 32-stage chunks (C5, C4), against the
+// 1e-5 cell tolerance (tools/acc_probe.py).
+int tc_drain_for(int64_t max_periods) {
+    static const int knob = [] {  // CYC_TC_DRAIN=<stages> (0: none): accuracy / speed probe
+        const char* e = std::getenv("CYC_TC_DRAIN");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (knob >= 0) return knob;
+    const int64_t ms = (max_periods + 15) / 16;
+    if (ms <= 64) return 0;
+    const int64_t nc = (ms + 31) / 32;
+    return (int)((ms + nc - 1) / nc);
+}
+
 // Smallest denominator q <= qmax with |alpha - p/q| <= 2^-50 (continued fractions).
 bool rational_of(double alpha, int64_t qmax, int64_t& p_out, int64_t& q_out) {
     long double x = alpha;
@@ -646,6 +665,8 @@ Engine::~Engine() {
     }
     cudaFree(ring_x_);
     cudaFree(ring_y_);
+    cudaFree(planes_);
+    for (auto& t : pl_tiles_) cudaFree(t.dev);
     if (fs_) {
         cudaStreamSynchronize(fs_);
         cudaStreamDestroy(fs_);
@@ -951,6 +972,19 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
     }
     if (groups.empty()) return Status::ok();
     (void)work;
+    if (planes_on_) {
+        // every lag block of a batch of segments in one launch (L2 reuse of the planes)
+        for (size_t b0 = 0; b0 < tsegs.size(); b0 += TC_SEGS) {
+            const size_t b1 = std::min(tsegs.size(), b0 + (size_t)TC_SEGS);
+            std::vector<FoldSeg> bsegs(tsegs.begin() + b0, tsegs.begin() + b1);
+            std::vector<TcGroupPlan> bgroups;
+            for (const G& gr : groups)
+                if (gr.seg >= (int)b0 && gr.seg < (int)b1)
+                    bgroups.push_back({gr.seg - (int)b0, gr.rb, gr.lb, gr.p0, gr.p1});
+            TRY(fold_tc_planes(bsegs, bgroups, S, nlb));
+        }
+        return Status::ok();
+    }
     // launches take at most TC_SEGS segments (tensor maps per segment): batch them
     for (size_t b0 = 0; b0 < tsegs.size(); b0 += TC_SEGS) {
         const size_t b1 = std::min(tsegs.size(), b0 + (size_t)TC_SEGS);
@@ -1079,7 +1113,10 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
             launch_flops += 8.0 * lags_in * 128.0 * (double)np;
         }
         TRY(ensure_partials((size_t)nt * 64 * 128 * sizeof(float4)));
+        int64_t max_np = 0;
+        for (int t = 0; t < nt; ++t) max_np = std::max<int64_t>(max_np, tcp_->tiles[t].p1 - tcp_->tiles[t].p0);
         FoldLaunch L{};
+        L.tc_drain = tc_drain_for(max_np);
         L.n_tiles = nt;
         L.n_groups = (int)ng;
         L.Pf = (int)Pf_;
@@ -1125,6 +1162,128 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         g0 += ng;
     }
     return cuda_check(cudaGetLastError(), "tensor-core fold launch");
+}
+
+// Device tile tables of the planes path, kept by content for the estimator's
+// lifetime: a captured push graph bakes the pointer in.
+const FoldTile* Engine::planes_tiles(const std::vector<FoldTile>& t) {
+    for (auto& c : pl_tiles_)
+        if (c.host.size() == t.size() && std::memcmp(c.host.data(), t.data(), t.size() * sizeof(FoldTile)) == 0)
+            return c.dev;
+    if (capturing_ || pl_tiles_.size() >= 16) return nullptr;
+    PlTiles c;
+    c.host = t;
+    if (cudaMalloc(&c.dev, t.size() * sizeof(FoldTile)) != cudaSuccess ||
+        cudaMemcpy(c.dev, t.data(), t.size() * sizeof(FoldTile), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(c.dev);
+        return nullptr;
+    }
+    pl_tiles_.push_back(std::move(c));
+    return pl_tiles_.back().dev;
+}
+
+// The chunk's folds take the planes path: tensor-core eligible self segments
+// with several lag blocks and non-negative lags (the maps index the planes
+// from the y sample of each window).
+bool Engine::planes_ok(const std::vector<FoldSeg>& segs) const {
+    static const bool off = std::getenv("CYC_NO_PLANES") != nullptr;  // A/B knob: fused converters only
+    static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;
+    if (off || no_tc || !tc_capable_ || cross_ || segs.empty() || Pf_ % 128 != 0 || f_lo_ < 0 ||
+        (t_pad_ + 63) / 64 < 2)
+        return false;
+    for (const FoldSeg& g0 : segs) {
+        FoldSeg g = g0;
+        g.vec = (Pf_ % 2 == 0) && ((uintptr_t)g.x % 16 == 0) && ((uintptr_t)g.y % 16 == 0) ? 1 : 0;
+        int64_t pa = 0, pb = 0;
+        if (g.x != g.y || g.mask != ~0ull || !tc_interior(g, pa, pb)) return false;
+    }
+    return true;
+}
+
+Status Engine::fold_tc_planes(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S,
+                              int nlb) {
+    using G = TcGroupPlan;
+    if (!tpd_) tpd_.reset(new TcPlDesc);
+    TcPlDesc& D = *tpd_;
+    std::memcpy(D.segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
+    for (size_t i = 0; i < tsegs.size(); ++i) {
+        int64_t pa = 0, pb = 0;
+        for (const G& gr : groups)
+            if (gr.seg == (int)i) {
+                pa = gr.p0;
+                pb = gr.p1;
+                break;
+            }
+        const int ch = tsegs[i].slot;
+        const int64_t off = pa * Pf_ - planes_c0_;  // planes word of the segment's first map sample
+        const uint32_t* hi = planes_ + (size_t)ch * planes_pitch_ + off;
+        const uint32_t* lo = planes_ + planes_words_ + (size_t)ch * planes_pitch_ + off;
+        // widest window: residues Pf-128.. at lag block nlb-1: samples up to Pf + lag_lo + 64 nlb
+        if (!encode_tcp_maps(D, (int)i, hi, lo, pa, pb - pa, (int)Pf_, Pf_ + f_lo_ + 64 * nlb))
+            return Status{CYC_ERR_CUDA, "cuTensorMapEncodeTiled failed for the planes fold", -1};
+    }
+    // tiles: every group split into `splits` period ranges (<= 2048 periods,
+    // at least one wave), launched range-major -- tile i * ng + g -- so the CTAs
+    // of a wave stream the neighbouring windows of one period range together
+    // and the lag blocks of a residue block reuse its planes from L2.  Group g's
+    // tiles are then g, g + ng, ...: the reduce walks them with stride ng (pad).
+    constexpr int64_t MAXP = 2048;
+    const int64_t ng = (int64_t)groups.size();
+    int64_t min_np = INT64_MAX;
+    int splits = 1;
+    for (const G& gr : groups) {
+        splits = (int)std::max<int64_t>(splits, ceil_div(gr.p1 - gr.p0, MAXP));
+        min_np = std::min<int64_t>(min_np, gr.p1 - gr.p0);
+    }
+    splits = (int)std::max<int64_t>(splits, std::min<int64_t>(ceil_div(SMS, ng), std::max<int64_t>(1, min_np / 16)));
+    std::vector<FoldTile> tiles;
+    std::vector<FoldGroup> fg(groups.size());
+    for (int i = 0; i < splits; ++i)
+        for (size_t g = 0; g < groups.size(); ++g) {
+            const G& gr = groups[g];
+            const int64_t np = gr.p1 - gr.p0;
+            // boundaries on whole stages: only a group's last tile has a partial
+            // stage, whose extra rows lie past the maps (TMA zero fill)
+            const int64_t a = gr.p0 + (np * i / splits) / 16 * 16;
+            const int64_t b = i + 1 == splits ? gr.p1 : gr.p0 + (np * (i + 1) / splits) / 16 * 16;
+            tiles.push_back(FoldTile{gr.seg, gr.rb, gr.lb, (int)g, a, b});
+        }
+    for (size_t g = 0; g < groups.size(); ++g)
+        fg[g] = FoldGroup{groups[g].seg, groups[g].rb, groups[g].lb, (int)g, (int)(g + (splits - 1) * ng) + 1,
+                          (int)ng};
+    int64_t max_np = 0;
+    for (const auto& t : tiles) max_np = std::max<int64_t>(max_np, t.p1 - t.p0);
+    TRY(ensure_partials(tiles.size() * 64 * 128 * sizeof(float4)));
+    const FoldTile* dt = planes_tiles(tiles);
+    if (!dt) return Status{CYC_ERR_CUDA, "planes fold: tile table upload", -1};
+    FoldLaunch L{};
+    L.tc_drain = tc_drain_for(max_np);
+    L.n_tiles = (int)tiles.size();
+    L.n_groups = (int)groups.size();
+    L.Pf = (int)Pf_;
+    L.lag_lo = f_lo_;
+    L.t_pad = t_pad_;
+    L.lw = lw_;
+    L.partials = partials_;
+    L.S = S;
+    L.gate = fold_gate_;
+    D.tiles = dt;
+    double launch_flops = 0.0, exec = 0.0;
+    for (const auto& gr : groups) {
+        const int lags_in = std::max(0, std::min(64, T_ - 64 * gr.lb));
+        launch_flops += 8.0 * lags_in * 128.0 * (double)(gr.p1 - gr.p0);
+    }
+    for (const auto& t : tiles) exec += (double)ceil_div(t.p1 - t.p0, 16) * 6.0 * 2.0 * 128 * 256 * 16;
+    if (prof_) {
+        ProfRec r{get_event_timed(), get_event_timed(), launch_flops, exec, true};
+        launch_fold_tcp(L, D, fg.data(), cs_, r.a, r.b);
+        prof_pending_.push_back(r);
+    } else {
+        launch_fold_tcp(L, D, fg.data(), cs_);
+    }
+    launches_ += 2;
+    return cuda_check(cudaGetLastError(), "planes fold launch");
 }
 
 Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwrite) {
@@ -2280,8 +2439,30 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     static const bool no_fuse = std::getenv("CYC_NO_FUSED_CHECK") != nullptr;
     int64_t pa = 0, pb = 0;
     bool pending = false;
-    const bool fused =
-        !no_fuse && ring_segs.empty() && !user_segs.empty() && tc_check_plan(user_segs, pa, pb, pending);
+    // Planes path (several lag blocks, e.g. C5): one pass splits the chunk
+    // into bf16 hi/lo planes and scans it; the tensor-core tiles of every lag
+    // block then stage planes without converting.
+    const bool planes = ring_segs.empty() && planes_ok(user_segs);
+    const bool fused = !planes && !no_fuse && ring_segs.empty() && !user_segs.empty() &&
+                       tc_check_plan(user_segs, pa, pb, pending);
+    if (planes) {
+        const int64_t pitch = ((int64_t)n + 4 + 3) & ~(int64_t)3;
+        const size_t words = (size_t)C * (size_t)pitch;
+        if (words > planes_words_) {
+            if (capturing_) return Status{CYC_ERR_CUDA, "planes buffer growth inside a captured push", -1};
+            // captured pushes bake the buffer in: drop them before it moves
+            for (auto& g : push_graphs_) drop_push_graph(g);
+            push_graphs_.clear();
+            CK(cudaStreamSynchronize(cs_));
+            cudaFree(planes_);
+            planes_ = nullptr;
+            planes_words_ = 0;
+            CK(cudaMalloc(&planes_, 2 * words * sizeof(uint32_t)));
+            planes_words_ = words;
+        }
+        planes_pitch_ = pitch;
+        planes_c0_ = c0 & ~(int64_t)3;
+    }
     const size_t s_count = (size_t)C * t_pad_ * Pf_ * 4;
     if (fused && pending) {  // fold into the pending accumulator; the gated add below commits it
         if (!S_pend_) CK(cudaMalloc(&S_pend_, s_count * sizeof(double)));
@@ -2294,7 +2475,14 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
                                          C, (int64_t)n);
     };
     tl("scan.start", vs_);
-    if (fused) {
+    cudaEvent_t ev_s = nullptr;
+    if (planes) {  // split + scan on the compute stream (the tiles read the planes); the side stream joins it
+        launches_ += launch_split_planes(x, (int64_t)n, C, (int64_t)n, planes_, planes_ + planes_words_, planes_pitch_,
+                                         c0 - planes_c0_, key_dev_, cs_);
+        ev_s = get_event();
+        CK(cudaEventRecord(ev_s, cs_));
+        CK(cudaStreamWaitEvent(vs_, ev_s, 0));
+    } else if (fused) {
         bool self = true;
         for (const auto& g : user_segs) self = self && g.x == g.y;
         const int64_t lo = pa * Pf_ + (self ? 0 : std::max(0, f_lo_));
@@ -2330,7 +2518,9 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
             joined = true;
         }
         st = fold(ring_segs, S);
+        planes_on_ = planes;
         if (st.code == CYC_OK) st = fold(user_segs, fused && pending ? S_pend_ : S);
+        planes_on_ = false;
         const int batches = (int)((user_segs.size() + TC_SEGS - 1) / TC_SEGS);
         if (st.code == CYC_OK && fused && (chk_fail_ || chk_launches_ != batches))
             st = Status{CYC_ERR_CUDA, "fused finite check: a checking launch missed lb = 0 groups", -1};
@@ -2360,6 +2550,7 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     ev_pool_.push_back(ev_c);
     ev_pool_.push_back(ev_v);
     if (ev_f) ev_pool_.push_back(ev_f);
+    if (ev_s) ev_pool_.push_back(ev_s);
     TRY(st);
     return cuda_check(cudaGetLastError(), "push_device");
 }

@@ -118,6 +118,23 @@ private:
         int64_t p0, p1;
     };
     Status fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S, int nlb);
+    // Planes path (fold_device_chunk, several lag blocks, x == y, lag_lo >= 0):
+    // the chunk's hi/lo bf16 planes, [channel][planes_pitch_] words from
+    // absolute sample planes_c0_ (4-aligned, so every period row of the TMA
+    // maps starts 16-byte aligned); planes_on_ while the chunk folds.
+    Status fold_tc_planes(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S, int nlb);
+    bool planes_ok(const std::vector<FoldSeg>& segs) const;
+    uint32_t* planes_ = nullptr;
+    size_t planes_words_ = 0;  // capacity of each of the hi / lo halves
+    bool planes_on_ = false;
+    int64_t planes_c0_ = 0, planes_pitch_ = 0;
+    std::unique_ptr<TcPlDesc> tpd_;
+    struct PlTiles {  // device tile tables of the planes path, by content (graph replays keep them)
+        std::vector<FoldTile> host;
+        FoldTile* dev = nullptr;
+    };
+    std::vector<PlTiles> pl_tiles_;
+    const FoldTile* planes_tiles(const std::vector<FoldTile>& t);
     bool tc_capable_ = false;  // sm_100 device (tcgen05)
     // Finalize slots [0, nslots) of S into out tables (out_block = slot) with per-slot scale.
     Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,

@@ -10,23 +10,24 @@
 // at lag d + t (c0 = xr*yr, c1 = xi*yr, c2 = xr*yi, c3 = xi*yi).
 // A CTA covers 128 residues with two such products (TMEM columns 0..255 and
 // 256..511) over one staged 192-sample window, so each x sample is read 1.5x
-// (not 2x) from L2 -- the staging bandwidth is this kernel's floor.
+// (not 2x) from L2.
 //
 // Precision: each fp32 sample is split into bf16 hi + lo (x = hi + lo + O(2^-17 x))
 // and D accumulates hi*hi + hi*lo + lo*hi with kind::f16 MMAs (fp32 TMEM
 // accumulator): relative error ~1e-5, inside the north-star 1e-4 (measured:
 // tools/exp/tc_probe2.cu).
 //
-// Pipeline per CTA (one tile = one residue block x lag block x period range):
-//   warp 0      producer: 1-D bulk copies (cp.async.bulk) of each period's
-//               1 KB x window (+ 512 B y window when y is not inside it) into
-//               a raw fp32 stage, completion on an mbarrier (transaction bytes);
-//   warps 2..5  converters: raw fp32 -> bf16 hi/lo planes in the UMMA
-//               MN-major 128B-swizzle layout; then the epilogue (tcgen05.ld of
-//               the band, fp32 partials like fold.cu's);
-//   warp 1      MMA issuer (one thread): 3 tcgen05.mma per 16 periods,
-//               tcgen05.commit frees the stage.
-// The tile's partials go through the same fixed-order fp64 reduce as fold.cu.
+// Two kernels (one tile = one residue block x lag block x period range):
+//   fold_tc_kernel (fused): warp 0 stages raw fp32 windows (2-D TMA boxes, or
+//     per-period bulk copies from a ring), warps 2..13 convert them to bf16
+//     hi/lo planes in the UMMA MN-major 128B-swizzle layout, warp 1 issues
+//     3 tcgen05.mma per 16 periods and tcgen05.commit frees the stage; the
+//     converters also drain the TMEM accumulators into the tile's partials.
+//   fold_tcp_kernel (planes): the split is done once per sample beforehand
+//     (split_planes_kernel); TMA stages the bf16 planes straight into the
+//     operand layout, so shared memory carries only TMA writes and MMA reads;
+//     dedicated epilogue warps keep the drained sums in registers.
+// The tile's partials go through a fixed-order fp64 reduce (fold_tc_reduce_kernel).
 #include <cuda_bf16.h>
 
 #include <cstring>
@@ -61,17 +62,23 @@ constexpr int YPLANE = TKB * YF * 2;    // 8 KB: 4 atoms
 #ifndef TC_NP_SELF
 #define TC_NP_SELF 4
 #endif
-#ifndef TC_GROUPS
-#define TC_GROUPS 1
-#endif
-constexpr int TNC = TC_TNC;             // converter / epilogue warps (warps 2 .. TNC+1), a multiple of 4
-// Converter stage groups: group g (warps 2 + g*TGW ..) converts stages it = g mod TG,
-// so one warp's per-stage latency chain (barrier waits, shared loads, fence,
-// arrive) is spread over TG stages of the pipeline.
-constexpr int TG = TC_GROUPS;
-constexpr int TGW = TNC / TG;
-static_assert(TNC % TG == 0, "converter groups");
-constexpr int TNT = 64 + 32 * TNC;      // + warp 0 producer, warp 1 MMA issuer
+// Warp roles: 0 producer (TMA / bulk copies), 1 MMA issuer, 2 .. TNC+1
+// converters (which also drain TMEM between chunks and at the end).  The stage
+// interval is bound by shared-memory bandwidth (TMA writes + converter
+// loads/stores + 72 KB of MMA operand reads per stage, ncu: l1tex data-pipe
+// wavefronts), and many thin converter warps hide the per-warp latency chain
+// best (round-2 sweep: 4 or 8 fat warps with precomputed offsets were 10-25%
+// slower).
+constexpr int TNC = TC_TNC;
+static_assert(TNC % 4 == 0, "converter warps cover every TMEM lane quarter");
+constexpr int TNT = 64 + 32 * TNC;
+// TMEM accumulation chunks (L.tc_drain stages): the tensor core adds each
+// MMA's products into the fp32 accumulator with a truncating alignment, a bias
+// of ~7e-8 of the accumulated value per stage (measured: 1.26e-5 relative on
+// the C5 lag-0 cell over 2048 periods, against the 1e-5 cell tolerance).
+// After each chunk the accumulator is added into the tile's sums (IEEE round
+// to nearest) and the next MMA restarts it, which bounds the bias by the chunk
+// length whatever the tile length.
 // Two rings: raw fp32 stages (producer -> converters, freed after conversion)
 // and bf16 plane stages (converters -> MMA, freed by tcgen05.commit).
 template <bool SELF>
@@ -82,9 +89,10 @@ struct TcGeo {
     static constexpr int NP = SELF ? TC_NP_SELF : 2;
     static constexpr int SMEM = NR * RAW + NP * PLANE + 1024;
     static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
-    // a ring slot must always be converted by the same stage group, or a group
-    // running ahead could pass a barrier's phase parity one phase early
-    static_assert(TG == 1 || (NR % TG == 0 && NP % TG == 0), "converter groups need ring depths divisible by TG");
+    // converter units (8 floats of one period row) per stage and per thread
+    static constexpr int XU = (XF / 32) * 64, YU = SELF ? 0 : (YF / 32) * 64;
+    static constexpr int NX = (XU + 32 * TNC - 1) / (32 * TNC), NYU = (YU + 32 * TNC - 1) / (32 * TNC);
+    static constexpr int NU = NX + NYU;
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -152,56 +160,63 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
 // and the plane writes, (4(a%2) + m) ^ k, of a quarter-warp then land on 8
 // distinct 16-byte bank groups: k1 ^ k2 = 5 has bits 0 and 2 set.
 // swz == false: rows are linear (1-D bulk copies, row pitch `pitch`).
+// Offsets are relative to the raw stage base (constant across stages).
 struct UnitPos {
-    uint32_t ra, rb;  // shared addresses of the unit's two 16-byte raw chunks
+    uint32_t ra, rb;  // offsets of the unit's two 16-byte raw chunks
     int a, m, k;      // box, 8-float group, row (period within the stage)
 };
-__device__ __forceinline__ UnitPos unit_pos(uint32_t raw, int u, bool swz, uint32_t pitch) {
+__device__ __forceinline__ UnitPos unit_pos(int u, bool swz, uint32_t pitch) {
     UnitPos q;
     const int w = u & 63, l = w & 31, qd = l >> 3, pos = l & 7;
     q.a = u >> 6;
     q.m = pos & 3;
     q.k = 8 * (w >> 5) + ((pos >> 2) ? (qd ^ 5) : qd);
     if (swz) {
-        const uint32_t row = raw + (uint32_t)(q.a * (TKB * 128) + q.k * 128);
+        const uint32_t row = (uint32_t)(q.a * (TKB * 128) + q.k * 128);
         q.ra = row + ((uint32_t)((2 * q.m) ^ (q.k & 7)) << 4);
         q.rb = row + ((uint32_t)((2 * q.m + 1) ^ (q.k & 7)) << 4);
     } else {
-        q.ra = raw + (uint32_t)q.k * pitch + (uint32_t)(q.a * 128 + q.m * 32);
+        q.ra = (uint32_t)q.k * pitch + (uint32_t)(q.a * 128 + q.m * 32);
         q.rb = q.ra + 16;
     }
     return q;
 }
-// 8 fp32 of row k (a, b = floats 8 n8 .. +3, +4 .. +7, in registers) -> one
-// 16-byte chunk of the hi and lo planes (MN-major SW128: atom n/64, row k,
-// chunk ((n%64)/8) ^ (k%8)).  Shared-window addresses (STS).
+// Plane offset of 8-float group n8 of row k (MN-major SW128: atom n8/8, row k,
+// 16-byte chunk (n8%8) ^ (k%8)).
+__device__ __forceinline__ uint32_t plane_off(int n8, int k) {
+    return (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
+}
+// 8 fp32 (a, b) -> one 16-byte chunk of the hi plane at `hi` and of the lo
+// plane at `lo`: hi = bf16_rn(x), lo = bf16_rn(x - hi) (x - hi exact in fp32;
+// packed fp32x2 subtractions).  zero: store zeros (rows past the stage's data).
 // check: also flag a possibly non-finite input -- an inf or NaN makes its lo
 // part (x - hi) NaN, caught by one bf16x2 FMA with zero per pair (finite
 // values give +-0).  A flag is only a hint (so is the lo = -inf of a finite
 // value that rounds to a bf16 infinity): the caller re-checks the fp32 samples.
-__device__ __forceinline__ bool split8_regs(const float4& a, const float4& b, int n8, int k, uint32_t hi, uint32_t lo,
-                                           bool zero, bool check) {
+__device__ __forceinline__ bool split8(const float4& a, const float4& b, uint32_t hi, uint32_t lo, bool zero,
+                                       bool check) {
     uint32_t h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
     uint32_t acc = 0;
     if (!zero) {
-        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const float2 v[4] = {make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y),
+                             make_float2(b.z, b.w)};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            h[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
-            const float h0 = __uint_as_float(h[e] << 16), h1 = __uint_as_float(h[e] & 0xffff0000u);
-            l[e] = pack_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
+            h[e] = pack_bf16(v[e].x, v[e].y);
+            const float2 nh = make_float2(-__uint_as_float(h[e] << 16), -__uint_as_float(h[e] & 0xffff0000u));
+            const float2 d = __fadd2_rn(v[e], nh);
+            l[e] = pack_bf16(d.x, d.y);
         }
         if (check) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) asm("fma.rn.bf16x2 %0, %1, %2, %0;" : "+r"(acc) : "r"(l[e]), "r"(0u));
         }
     }
-    const uint32_t off = (uint32_t)((n8 >> 3) * (TKB * 128) + k * 128 + (((n8 & 7) ^ (k & 7)) << 4));
 #if TC_EXPERIMENT == 4  // diagnostics: conversion without the plane stores
     return ((h[0] ^ h[1] ^ h[2] ^ h[3] ^ l[0] ^ l[1] ^ l[2] ^ l[3]) == 0x12345678u) | ((acc & 0x7fff7fffu) != 0u);
 #else
-    sts128(hi + off, h[0], h[1], h[2], h[3]);
-    sts128(lo + off, l[0], l[1], l[2], l[3]);
+    sts128(hi, h[0], h[1], h[2], h[3]);
+    sts128(lo, l[0], l[1], l[2], l[3]);
     return (acc & 0x7fff7fffu) != 0u;
 #endif
 }
@@ -231,6 +246,144 @@ __device__ unsigned long long g_tc_warp[16][64][2];  // per converter warp: (ful
 #define TC_MARK(kind, it)
 #endif
 
+// Drain of the fused kernel (NE converter warps, NE/4 per TMEM lane quarter):
+// add the 64-lag band of both accumulators into the tile's fp32 partials
+// (first chunk: store; later chunks: L2 reductions).  Lane m = 2r + a of
+// quarter q = warp % 4 holds D[m][*]; the band is columns [2r, 2r + 128):
+// float2 (c_{2a}, c_{2a+1}) per lag t, the residue's float4 written by the
+// even lane.  One thread's adds to a cell apply in program order, so the sums
+// are reproducible bit for bit.
+template <int NE>
+__device__ __forceinline__ void tc_drain_band(uint32_t tmem, const FoldLaunch& L, bool first, bool zero, int e,
+                                              int warp, int lane) {
+    const int q = warp & 3;
+    const int m = 32 * q + lane;
+    const int r = m >> 1, a = m & 1;
+    float4* part = reinterpret_cast<float4*>(L.partials) + (size_t)blockIdx.x * 64 * TRB;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // a quarter's work: 2 accumulators x 5 column chunks [32cc, 32cc + 32),
+    // cc = q .. q+4 (they cover the band), shared by the quarter's NE/4 warps
+    for (int item = e >> 2; item < 10; item += NE / 4) {
+        const int h = item / 5, cc = q + item % 5;
+        uint32_t v[32];
+        const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h + 32 * cc);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(addr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (zero) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int t = 16 * cc + j - r;  // lag offset of column pair 2(16cc + j)
+            const float o0 = __uint_as_float(v[2 * j]), o1 = __uint_as_float(v[2 * j + 1]);
+            const float p0 = __shfl_xor_sync(0xffffffffu, o0, 1), p1 = __shfl_xor_sync(0xffffffffu, o1, 1);
+            if (a != 0 || t < 0 || t >= 64) continue;
+            float4* dst = part + ((size_t)t * TRB + 64 * h + r);
+            if (first) {
+                *dst = make_float4(o0, o1, p0, p1);
+            } else {
+                // fire-and-forget fp32 adds in L2 (round to nearest)
+                asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(o0), "f"(o1),
+                             "f"(p0), "f"(p1)
+                             : "memory");
+            }
+        }
+    }
+    // the TMEM reads complete before the MMA warp restarts the accumulator
+    asm volatile("tcgen05.fence::before_thread_sync;");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
+    uint32_t u[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(u[k]);
+}
+
+// Dedicated epilogue warps of the planes kernel (NE = 16: four per TMEM lane
+// quarter; or 8): the chunks' sums stay in registers -- fp32 adds, round to
+// nearest -- and the band is stored once per tile.  Lane m = 2r + a of
+// quarter q (r = 16q + r') owns lags t = 0..63 of residue r, component pair
+// a, of both accumulators: 4 items of 16 column pairs per accumulator, item
+// k = 1..3 the column chunk cc = q + k (t = 16k + j - r'), item 0 the chunks
+// q (j >= r') and q + 4 (j < r') merged (t = (j - r') mod 64).  Warp w of the
+// quarter's NE/4 warps holds items w, w + NE/4, ... (h = item / 4).
+template <int NE>
+__device__ __forceinline__ void tc_epilogue(uint32_t tmem, const FoldLaunch& L, int nst, int nchunks, int e, int warp,
+                                            int lane, uint64_t* chunk_done, uint64_t* drain_free) {
+    static_assert(NE == 8 || NE == 16, "two or four epilogue warps per lane quarter");
+    constexpr int NI = 32 / NE, WQ = NE / 4;  // items per warp, warps per quarter
+    const int q = warp & 3, w = e >> 2;
+    const int m = 32 * q + lane;
+    const int r = m >> 1, a = m & 1, rp = r - 16 * q;
+    float acc[NI][32];
+#pragma unroll
+    for (int k = 0; k < NI; ++k)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[k][j] = 0.f;  // x + 0 is exact: chunk 0 adds like the rest
+    const int nc = nchunks > 0 ? nchunks : 1;
+    for (int c = 0; c < nc; ++c) {
+        mbar_wait(chunk_done, (uint32_t)c & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (nst > 0) {
+#pragma unroll
+            for (int k = 0; k < NI; ++k) {
+                const int item = w + WQ * k, h = item >> 2, kind = item & 3;
+                const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h);
+#pragma unroll
+                for (int jb = 0; jb < 16; jb += 8) {  // 8 column pairs per load
+#pragma unroll
+                    for (int part2 = 0; part2 < (kind ? 1 : 2); ++part2) {
+                        // merged item: chunk q for j >= r', chunk q + 4 for j < r'
+                        const int cc = kind ? q + kind : q + 4 * part2;
+                        float v[16];
+                        tmem_ld16(base + (uint32_t)(32 * cc + 2 * jb), v);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const bool use = kind || ((jb + j >= rp) == (part2 == 0));
+                            if (use) {
+                                acc[k][2 * (jb + j)] += v[2 * j];
+                                acc[k][2 * (jb + j) + 1] += v[2 * j + 1];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        // the TMEM reads complete before the MMA warp restarts the accumulator
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0 && c + 1 < nc) mbar_arrive(drain_free);
+    }
+    float4* part = reinterpret_cast<float4*>(L.partials) + (size_t)blockIdx.x * 64 * TRB;
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        const int item = w + WQ * k, h = item >> 2, kind = item & 3;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const float p0 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j], 1);
+            const float p1 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j + 1], 1);
+            if (a != 0) continue;
+            const int t = kind ? 16 * kind + j - rp : (j - rp) & 63;
+            part[(size_t)t * TRB + 64 * h + r] = make_float4(acc[k][2 * j], acc[k][2 * j + 1], p0, p1);
+        }
+    }
+}
+
 template <bool SELF, class DESC>
 __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
     using G = TcGeo<SELF>;
@@ -238,7 +391,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* raw_ring = smem;                       // NR x RAW
     uint8_t* plane_ring = smem + G::NR * G::RAW;    // NP x PLANE (1 KB aligned)
-    __shared__ uint64_t full[G::NR], rawfree[G::NR], conv[G::NP], planefree[G::NP], done;
+    __shared__ uint64_t full[G::NR], rawfree[G::NR], conv[G::NP], planefree[G::NP], chunk_done, drain_free;
     __shared__ uint32_t tmem_s;
     __shared__ FoldTile s_tile;
     __shared__ FoldSeg s_seg;
@@ -248,13 +401,14 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         s_seg = D.segs[s_tile.seg];
         for (int s = 0; s < G::NR; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&rawfree[s], TGW);
+            mbar_init(&rawfree[s], TNC);
         }
         for (int s = 0; s < G::NP; ++s) {
-            mbar_init(&conv[s], TGW);
+            mbar_init(&conv[s], TNC);
             mbar_init(&planefree[s], 1);
         }
-        mbar_init(&done, 1);
+        mbar_init(&chunk_done, 1);
+        mbar_init(&drain_free, TNC);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {  // two 128 x 256 fp32 accumulators
@@ -274,6 +428,11 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     const int ya = SELF ? (int)(-d) / 32 : 0;  // first x atom holding y (self tiles)
     const int nper = (int)(tile.p1 - tile.p0);
     const int nst = (nper + TKB - 1) / TKB;
+    const int DRAIN = L.tc_drain > 0 ? L.tc_drain : (1 << 30);
+    // chunk phases staggered over CTAs (stage it is in chunk (it + off) / DRAIN):
+    // the CTAs' drains, which all add into L2, do not coincide
+    const int off = L.tc_drain > 0 ? (int)(blockIdx.x % 4) * (DRAIN / 4) : 0;
+    const int nchunks = nst > 0 ? (nst - 1 + off) / DRAIN + 1 : 0;
     const bool swz = seg.mask == ~0ull;  // TMA-staged (128B-swizzled boxes) vs bulk-copied rows
 
     if (warp == 0) {
@@ -338,101 +497,121 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         if (lane == 0) {
             for (int it = 0; it < nst; ++it) {
                 const int s = it % G::NP;
+                const int j = (it + off) % DRAIN;  // stage within the accumulation chunk
                 mbar_wait(&conv[s], (it / G::NP) & 1);
+                // the chunk's first MMAs overwrite the accumulator: the
+                // converters must have drained the previous chunk (drain k -> phase k)
+                if (j == 0 && it > 0) mbar_wait(&drain_free, ((it + off) / DRAIN - 1) & 1);
+                const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
                 TC_MARK(1, it);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t xh = su32(plane_ring + s * G::PLANE), xl = xh + XPLANE;
                 const uint32_t yh0 = SELF ? xh + ya * ATOM : xl + XPLANE;
                 const uint32_t yl0 = SELF ? xl + ya * ATOM : yh0 + YPLANE;
-                {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {  // residues 64h..64h+63: y atoms 2h.., x atoms 2h..2h+3
-                        const uint64_t dxh = sw128_desc(xh + 2 * h * ATOM, ATOM, 1024);
-                        const uint64_t dxl = sw128_desc(xl + 2 * h * ATOM, ATOM, 1024);
-                        const uint64_t dyh = sw128_desc(yh0 + 2 * h * ATOM, ATOM, 1024);
-                        const uint64_t dyl = sw128_desc(yl0 + 2 * h * ATOM, ATOM, 1024);
-                        const uint32_t dt = tmem + 256 * h;
+                for (int h = 0; h < 2; ++h) {  // residues 64h..64h+63: y atoms 2h.., x atoms 2h..2h+3
+                    const uint64_t dxh = sw128_desc(xh + 2 * h * ATOM, ATOM, 1024);
+                    const uint64_t dxl = sw128_desc(xl + 2 * h * ATOM, ATOM, 1024);
+                    const uint64_t dyh = sw128_desc(yh0 + 2 * h * ATOM, ATOM, 1024);
+                    const uint64_t dyl = sw128_desc(yl0 + 2 * h * ATOM, ATOM, 1024);
+                    const uint32_t dt = tmem + 256 * h;
 #if TC_EXPERIMENT != 1  // diagnostics: 1 = no MMAs (pipeline and conversion only)
-                        mma_bf16(dt, dyh, dxh, TC_IDESC, it ? 1u : 0u);
-                        mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
-                        mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
+                    mma_bf16(dt, dyh, dxh, TC_IDESC, acc);
+                    mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
+                    mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
 #endif
-                    }
                 }
                 mma_commit(&planefree[s]);
+                if (it == nst - 1) mma_commit(&chunk_done);  // the final drain's signal
                 TC_MARK(2, it);
             }
-            mma_commit(&done);
+            if (nst == 0) mbar_arrive(&chunk_done);  // no MMAs: the drain stores zeros
         }
     } else {
-        const int grp = (warp - 2) / TGW;
-        const int ct = threadIdx.x - 64 - 32 * TGW * grp;  // 0 .. 32*TGW-1 within the group
-        // fused check (lb = 0 tiles): the 128 samples of each period that this
-        // tile's residues own -- x boxes [cb0, cb0 + 8) (self: the y part of
-        // the x window; else x samples [0, 128)), and the y window
+        // converters: a thread's units are ct + i * 32 TNC (x units, then y);
+        // their raw / plane offsets are the same every stage
+        const int ct = threadIdx.x - 64;
         const bool chk = L.chk_key != nullptr && tile.lb == 0;
         const int cb0 = SELF ? (int)(-d) / 16 : 0;
         const int chk_y = (seg.x != seg.y) ? 1 : 0;
-        for (int it = grp; it < nst; it += TG) {
-            const int rs = it % G::NR, ps = it % G::NP;
-            mbar_wait(&full[rs], (it / G::NR) & 1);
+        constexpr int NU = G::NU;
+        UnitPos q[NU];
+        uint32_t pho[NU], pdl[NU];
+        bool on[NU];
+        uint32_t ckm = 0;
+#pragma unroll
+        for (int i = 0; i < NU; ++i) {
+            const bool isy = i >= G::NX;
+            const int u = ct + (isy ? i - G::NX : i) * 32 * TNC;
+            on[i] = u < (isy ? G::YU : G::XU);
+            q[i] = unit_pos(on[i] ? u : 0, swz, isy ? YF * 4 : XF * 4);
+            if (isy) {
+                q[i].ra += XRAW;
+                q[i].rb += XRAW;
+            }
+            pho[i] = (isy ? 2 * XPLANE : 0) + plane_off(4 * q[i].a + q[i].m, q[i].k);
+            pdl[i] = isy ? YPLANE : XPLANE;
+            if (chk && (isy || (q[i].a >= cb0 && q[i].a < cb0 + 8))) ckm |= 1u << i;
+        }
+        const uint32_t rbase = su32(raw_ring), pbase = su32(plane_ring);
+        int rs = 0, ps = 0;
+        uint32_t rph = 0, pph = 0;  // ring phases
+        const int e = warp - 2;
+        // Drain of the chunk ending at stage b: MMA(b) is complete once the
+        // converters hold plane slot b % NP again (its tcgen05.commit), i.e.
+        // at iteration b + NP; the MMA warp waits on drain_free before the next
+        // chunk's first (overwriting) MMAs, while the converters have already
+        // filled the plane ring ahead.
+        auto drain_after = [&](int b) {
+            tc_drain_band<TNC>(tmem, L, b + off < DRAIN, false, e, warp, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&drain_free);
+        };
+        for (int it = 0; it < nst; ++it) {
+            mbar_wait(&full[rs], rph);
             if (warp == 2 && lane == 0) TC_MARK(3, it);
 #ifdef TC_TRACE
-            if (blockIdx.x == 0 && lane == 0 && it < 64) g_tc_warp[warp][it][0] = clock64();
+            if (blockIdx.x == 0 && lane == 0 && it < 64 && warp < 16) g_tc_warp[warp][it][0] = clock64();
 #endif
-            if (it >= G::NP) mbar_wait(&planefree[ps], ((it / G::NP) - 1) & 1);
-            if (warp == 2 && lane == 0) TC_MARK(4, it);
-            const uint32_t st = su32(raw_ring + rs * G::RAW);
-            const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
-            const uint32_t xh = su32(plane_ring + ps * G::PLANE);
-            const uint32_t xl = xh + XPLANE;
-            // A thread's units of this stage (2 of x; 0-2 of y when not self):
-            // all raw loads first, then the conversions and plane stores -- the
-            // shared loads are ordered asm, so this is what lets them overlap.
-            constexpr int XU = (XF / 32) * 64, YU = SELF ? 0 : (YF / 32) * 64;
-            constexpr int NU = (XU + 32 * TGW - 1) / (32 * TGW) + (YU + 32 * TGW - 1) / (32 * TGW);
-            UnitPos q[NU];
-            float4 va[NU], vb[NU];
-            bool yu[NU], on[NU];
-#pragma unroll
-            for (int i = 0; i < NU; ++i) {
-                const int nx = (XU + 32 * TGW - 1) / (32 * TGW);
-                const bool isy = i >= nx;
-                const int u = ct + (isy ? i - nx : i) * 32 * TGW;
-                on[i] = u < (isy ? YU : XU);
-                yu[i] = isy;
-                q[i] = unit_pos(isy ? st + XRAW : st, on[i] ? u : 0, swz, isy ? YF * 4 : XF * 4);
+            if (it >= G::NP) {
+                mbar_wait(&planefree[ps], pph ^ 1u);
+                const int b = it - G::NP;
+                if ((b + off) % DRAIN == DRAIN - 1 && b + 1 < nst) drain_after(b);
             }
+            if (warp == 2 && lane == 0) TC_MARK(4, it);
+            const uint32_t st = rbase + (uint32_t)(rs * G::RAW);
+            const uint32_t pl = pbase + (uint32_t)(ps * G::PLANE);
+            float4 va[NU], vb[NU];
 #pragma unroll
             for (int i = 0; i < NU; ++i) {
+                if (!on[i]) continue;
 #if TC_EXPERIMENT == 5  // diagnostics: conversion and stores without the raw loads
                 va[i] = make_float4(__int_as_float(q[i].ra), 1.f, 2.f, 3.f);
                 vb[i] = make_float4(__int_as_float(q[i].rb), 1.f, 2.f, 3.f);
 #else
-                va[i] = lds128(q[i].ra);
-                vb[i] = lds128(q[i].rb);
+                va[i] = lds128(st + q[i].ra);
+                vb[i] = lds128(st + q[i].rb);
 #endif
             }
             // the raw slot is free as soon as its values are in registers: the
             // producer's next TMA into it overlaps this stage's conversion
-            // (the arrive releases the warp's loads, ordered by __syncwarp)
             __syncwarp();
             if (lane == 0) mbar_arrive(&rawfree[rs]);
+            const int rows = min(TKB, nper - it * TKB);  // rows >= `rows` are zero-filled
             uint32_t flags = 0;
 #pragma unroll
             for (int i = 0; i < NU; ++i) {
                 if (!on[i] || TC_EXPERIMENT == 2) continue;  // diagnostics: 2 = no conversion
-                const uint32_t h0 = yu[i] ? xl + XPLANE : xh, l0 = yu[i] ? xl + XPLANE + YPLANE : xl;
-                const bool ck = chk && (yu[i] || (q[i].a >= cb0 && q[i].a < cb0 + 8));
-                if (split8_regs(va[i], vb[i], 4 * q[i].a + q[i].m, q[i].k, h0, l0, q[i].k >= rows, ck))
+                if (split8(va[i], vb[i], pl + pho[i], pl + pho[i] + pdl[i], q[i].k >= rows, (ckm >> i) & 1u))
                     flags |= 1u << i;
             }
             if (flags) {  // a possibly non-finite sample: exact re-check (rare)
 #pragma unroll
                 for (int i = 0; i < NU; ++i) {
                     if (!(flags & (1u << i))) continue;
-                    check_unit_slow(L, q[i], va[i], vb[i], tile.p0 + (int64_t)it * TKB, yu[i] ? r0 : r0 + d,
-                                    yu[i] ? chk_y : 0, seg.slot);
+                    const bool isy = i >= G::NX;
+                    check_unit_slow(L, q[i], va[i], vb[i], tile.p0 + (int64_t)it * TKB, isy ? r0 : r0 + d,
+                                    isy ? chk_y : 0, seg.slot);
                 }
             }
 #if TC_EXPERIMENT != 3  // diagnostics: 3 = no proxy fence before the hand-off
@@ -442,48 +621,199 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             if (lane == 0) mbar_arrive(&conv[ps]);
             if (warp == 2 && lane == 0) TC_MARK(5, it);
 #ifdef TC_TRACE
-            if (blockIdx.x == 0 && lane == 0 && it < 64) g_tc_warp[warp][it][1] = clock64();
+            if (blockIdx.x == 0 && lane == 0 && it < 64 && warp < 16) g_tc_warp[warp][it][1] = clock64();
 #endif
-        }
-        // epilogue: warps 2-5 read accumulator 0 (residues 0-63), warps 6-9
-        // accumulator 1 (64-127).  Lane m = 2r + a of quarter q holds D[m][*];
-        // the band is columns [2r, 2r + 128): float2 (c_{2a}, c_{2a+1}) per lag t
-        mbar_wait(&done, 0);
-        if (warp == 2 && lane == 0) TC_MARK(6, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const int q = warp & 3;  // TMEM lane quarter this warp may read
-        const int m = 32 * q + lane;
-        const int r = m >> 1, a = m & 1;
-        float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)blockIdx.x * 64 * TRB * 2;
-        // a quarter's work: 2 accumulators x 5 column chunks [32c, 32c + 32),
-        // c = q .. q+4 (they cover the band), shared by the quarter's TNC/4 warps
-        for (int item = (warp - 2) >> 2; item < 10; item += TNC / 4) {
-            const int h = item / 5, c = q + item % 5;
-            uint32_t v[32];
-            const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h + 32 * c);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(addr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int t = 16 * c + j - r;  // lag offset of column pair 2(16c + j)
-                if (t >= 0 && t < 64)
-                    part[((size_t)t * TRB + 64 * h + r) * 2 + a] =
-                        make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+            if (++rs == G::NR) {
+                rs = 0;
+                rph ^= 1u;
+            }
+            if (++ps == G::NP) {
+                ps = 0;
+                pph ^= 1u;
             }
         }
+        // chunk ends among the last NP stages (no converter iteration follows them)
+        for (int it = nst; it < nst + G::NP; ++it) {
+            const int b = it - G::NP;
+            if (b >= 0 && (b + off) % DRAIN == DRAIN - 1 && b + 1 < nst) {
+                mbar_wait(&planefree[ps], pph ^ 1u);
+                drain_after(b);
+            }
+            if (++ps == G::NP) {
+                ps = 0;
+                pph ^= 1u;
+            }
+        }
+        // final chunk
+        mbar_wait(&chunk_done, 0);
+        if (warp == 2 && lane == 0) TC_MARK(6, 0);
+        tc_drain_band<TNC>(tmem, L, nchunks <= 1, nst == 0, e, warp, lane);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     if (threadIdx.x == 0) TC_MARK(7, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Planes path: the split is done once per sample (split_planes_kernel) and
+// the fold stages bf16 planes with TMA straight into the operand layout.  One
+// stage slot holds x hi/lo (6 atoms each) and, for tiles whose y window is
+// not inside the x window, y hi/lo (4 atoms each); self and non-self tiles
+// share one launch, so the lag blocks of a residue block run together and
+// reuse the planes from L2.
+// ---------------------------------------------------------------------------
+#ifndef TC_NPL
+#define TC_NPL 5
+#endif
+#ifndef TC_TPE
+#define TC_TPE 16
+#endif
+constexpr int TPE = TC_TPE;                        // epilogue warps of the planes kernel
+constexpr int TPT = 64 + 32 * TPE;
+constexpr int NPL = TC_NPL;                        // plane stages in flight
+constexpr int PL_STAGE = 2 * XPLANE + 2 * YPLANE;  // 40 KB
+constexpr int PL_SMEM = NPL * PL_STAGE + 1024;
+static_assert(PL_SMEM <= 227 * 1024, "shared memory per CTA");
+
+template <class DESC>
+__global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t full[NPL], planefree[NPL], chunk_done, drain_free;
+    __shared__ uint32_t tmem_s;
+    __shared__ FoldTile s_tile;
+    __shared__ FoldSeg s_seg;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        s_tile = D.tiles[blockIdx.x];
+        s_seg = D.segs[s_tile.seg];
+        for (int s = 0; s < NPL; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&planefree[s], 1);
+        }
+        mbar_init(&chunk_done, 1);
+        mbar_init(&drain_free, TPE);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_s;
+    const FoldTile& tile = s_tile;
+    const int64_t r0 = (int64_t)tile.rb * TRB;
+    const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 64;
+    // y inside the x window at an atom boundary: skip the y planes
+    const bool self = s_seg.x == s_seg.y && d <= 0 && -d <= 64 && (-d) % 32 == 0;
+    const int ya = self ? (int)(-d) / 32 : 0;
+    const int nper = (int)(tile.p1 - tile.p0);
+    const int nst = (nper + TKB - 1) / TKB;
+    const int DRAIN = L.tc_drain > 0 ? L.tc_drain : (1 << 30);
+    const int off = L.tc_drain > 0 ? (int)(blockIdx.x % 4) * (DRAIN / 4) : 0;  // staggered drains
+    const int nchunks = nst > 0 ? (nst - 1 + off) / DRAIN + 1 : 0;
+    if (warp == 0) {
+        if (lane == 0) {
+            const CUtensorMap* hm = &D.hmap[tile.seg];
+            const CUtensorMap* lm = &D.lmap[tile.seg];
+            const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
+            const int xcol = 2 * (int)(r0 + d), ycol = 2 * (int)r0;
+            const uint32_t bytes = self ? 2 * XPLANE : PL_STAGE;
+            for (int it = 0; it < nst; ++it) {
+                const int s = it % NPL;
+                if (it >= NPL) mbar_wait(&planefree[s], ((it / NPL) - 1) & 1);
+                const uint32_t st = su32(ring + s * PL_STAGE);
+                const int row = row0 + it * TKB;
+                mbar_expect_tx(&full[s], bytes);
+                // one box = one plane atom column: 64 bf16 = 32 samples x 16 periods
+#pragma unroll
+                for (int a = 0; a < XF / 64; ++a) {
+                    tma_2d(st + a * ATOM, hm, xcol + 64 * a, row, &full[s]);
+                    tma_2d(st + XPLANE + a * ATOM, lm, xcol + 64 * a, row, &full[s]);
+                }
+                if (!self) {
+#pragma unroll
+                    for (int a = 0; a < YF / 64; ++a) {
+                        tma_2d(st + 2 * XPLANE + a * ATOM, hm, ycol + 64 * a, row, &full[s]);
+                        tma_2d(st + 2 * XPLANE + YPLANE + a * ATOM, lm, ycol + 64 * a, row, &full[s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            for (int it = 0; it < nst; ++it) {
+                const int s = it % NPL;
+                const int j = (it + off) % DRAIN;
+                mbar_wait(&full[s], (it / NPL) & 1);
+                if (j == 0 && it > 0) mbar_wait(&drain_free, ((it + off) / DRAIN - 1) & 1);
+                const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t xh = su32(ring + s * PL_STAGE), xl = xh + XPLANE;
+                const uint32_t yh0 = self ? xh + ya * ATOM : xl + XPLANE;
+                const uint32_t yl0 = self ? xl + ya * ATOM : yh0 + YPLANE;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint64_t dxh = sw128_desc(xh + 2 * h * ATOM, ATOM, 1024);
+                    const uint64_t dxl = sw128_desc(xl + 2 * h * ATOM, ATOM, 1024);
+                    const uint64_t dyh = sw128_desc(yh0 + 2 * h * ATOM, ATOM, 1024);
+                    const uint64_t dyl = sw128_desc(yl0 + 2 * h * ATOM, ATOM, 1024);
+                    const uint32_t dt = tmem + 256 * h;
+                    mma_bf16(dt, dyh, dxh, TC_IDESC, acc);
+                    mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
+                    mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
+                }
+                mma_commit(&planefree[s]);
+                if (j == DRAIN - 1 || it == nst - 1) mma_commit(&chunk_done);
+            }
+            if (nst == 0) mbar_arrive(&chunk_done);
+        }
+    } else {
+        tc_epilogue<TPE>(tmem, L, nst, nchunks, warp - 2, warp, lane, &chunk_done, &drain_free);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// hi = bf16_rn(x), lo = bf16_rn(x - hi) per component (the converters'
+// arithmetic, so planes and fused folds give the same products), packed
+// (re, im) per sample; and the chunk's finite scan.  Each thread takes 4
+// samples of one channel row (independent 8-byte loads in flight).
+__global__ void __launch_bounds__(256) split_planes_kernel(const float2* __restrict__ x, int64_t n, int C,
+                                                           int64_t pitch_in, uint32_t* __restrict__ hi,
+                                                           uint32_t* __restrict__ lo, int64_t pitch_out,
+                                                           int64_t out_off, unsigned long long* key) {
+    const int64_t per_row = (n + 4 * 256 - 1) / (4 * 256);  // blocks per channel row
+    const int ch = (int)(blockIdx.x / per_row);
+    const int64_t b = blockIdx.x % per_row;
+    if (ch >= C) return;
+    const float2* xr = x + (size_t)ch * pitch_in;
+    uint32_t* hr = hi + (size_t)ch * pitch_out + out_off;
+    uint32_t* lr = lo + (size_t)ch * pitch_out + out_off;
+    const int64_t i0 = b * 4 * 256 + threadIdx.x;
+    float2 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = i0 + 256 * k;
+        v[k] = i < n ? __ldcs(xr + i) : make_float2(0.f, 0.f);
+    }
+    int64_t bad = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = i0 + 256 * k;
+        if (i >= n) continue;
+        const uint32_t h = pack_bf16(v[k].x, v[k].y);
+        const float2 nh = make_float2(-__uint_as_float(h << 16), -__uint_as_float(h & 0xffff0000u));
+        const float2 dd = __fadd2_rn(v[k], nh);
+        hr[i] = h;
+        lr[i] = pack_bf16(dd.x, dd.y);
+        if (bad < 0 && !(isfinite(v[k].x) && isfinite(v[k].y))) bad = i;
+    }
+    if (bad >= 0) atomicMin(key, (2ull * (unsigned long long)bad) * (unsigned long long)C + (unsigned long long)ch);
 }
 
 template <int MG>
@@ -509,11 +839,15 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
     const int tg = g.lb * 64 + lag;
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-    int t = g.t0 + q;
-    for (; t + 12 < g.t1; t += 16) {  // 4 loads in flight, fixed summation order
+    // the group's tiles are t0, t0 + stride, ... < t1 (stride 1: contiguous;
+    // the planes path launches range-major, stride = its group count)
+    const int stride = g.pad > 0 ? g.pad : 1;
+    const int nt = (g.t1 - g.t0 + stride - 1) / stride;
+    int k = q;
+    for (; k + 12 < nt; k += 16) {  // 4 loads in flight, fixed summation order
         float4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(t + 4 * u) * 64 * TRB);
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(g.t0 + (k + 4 * u) * stride) * 64 * TRB);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             s0 += v[u].x;
@@ -522,8 +856,8 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
             s3 += v[u].w;
         }
     }
-    for (; t < g.t1; t += 4) {
-        const float4 v = __ldcs(part + (size_t)t * 64 * TRB);
+    for (; k < nt; k += 4) {
+        const float4 v = __ldcs(part + (size_t)(g.t0 + k * stride) * 64 * TRB);
         s0 += v.x;
         s1 += v.y;
         s2 += v.z;
@@ -561,15 +895,17 @@ EncodeTiledFn encode_fn() {
     }();
     return fn;
 }
-bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t row_bytes) {
+bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t row_bytes,
+               bool bf16 = false) {
     EncodeTiledFn enc = encode_fn();
-    if (!enc || ((uintptr_t)base & 15) || rows == 0) return false;
+    if (!enc || ((uintptr_t)base & 15) || rows == 0 || (row_bytes & 15)) return false;
     const cuuint64_t gdim[2] = {cols, rows};
     const cuuint64_t gstr[1] = {row_bytes};
-    const cuuint32_t box[2] = {32, (cuuint32_t)TKB}, es[2] = {1, 1};  // one 128-byte swizzle atom column
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstr, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    // one 128-byte swizzle atom column: 32 floats or 64 bf16 x 16 rows
+    const cuuint32_t box[2] = {bf16 ? 64u : 32u, (cuuint32_t)TKB}, es[2] = {1, 1};
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+               const_cast<void*>(base), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace
 
@@ -586,19 +922,25 @@ bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64
            encode_2d(&D.ymap[si], yb, 2ull * Pf, (uint64_t)rows, 8ull * Pf);
 }
 
+bool encode_tcp_maps(TcPlDesc& D, int si, const uint32_t* hi, const uint32_t* lo, int64_t p_base, int64_t rows,
+                     int Pf, int64_t cols_samples) {
+    D.p_base[si] = p_base;
+    return encode_2d(&D.hmap[si], hi, 2ull * (uint64_t)cols_samples, (uint64_t)rows, 4ull * Pf, true) &&
+           encode_2d(&D.lmap[si], lo, 2ull * (uint64_t)cols_samples, (uint64_t)rows, 4ull * Pf, true);
+}
+
 namespace {
 using TcSmall = TcDesc<160, 16, 2>;  // one or two segments, one wave of tiles
 
 template <class DESC, int MG>
 void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self, cudaStream_t st, cudaEvent_t ev0,
                cudaEvent_t ev1, cudaEvent_t before_reduce, cudaEvent_t fold_done) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(fold_tc_kernel<true, DESC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TcGeo<true>::SMEM);
         cudaFuncSetAttribute(fold_tc_kernel<false, DESC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TcGeo<false>::SMEM);
-        attr = true;
     }
     if (ev0) record_event(ev0, st);
     if (self)
@@ -649,6 +991,31 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool sel
         fill_red(R, D, L.n_groups);
         launch_tc(L, D, R, self, st, ev0, ev1, before_reduce, fold_done);
     }
+}
+
+void launch_fold_tcp(const FoldLaunch& L, const TcPlDesc& D, const FoldGroup* groups, cudaStream_t st,
+                     cudaEvent_t ev0, cudaEvent_t ev1) {
+    if (L.n_tiles == 0) return;
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr))
+        cudaFuncSetAttribute(fold_tcp_kernel<TcPlDesc>, cudaFuncAttributeMaxDynamicSharedMemorySize, PL_SMEM);
+    thread_local TcRed<FI_GROUPS> R;
+    for (int g = 0; g < L.n_groups; ++g) {
+        R.groups[g] = groups[g];
+        R.slot[g] = D.segs[groups[g].seg].slot;
+    }
+    if (ev0) record_event(ev0, st);
+    fold_tcp_kernel<TcPlDesc><<<L.n_tiles, TPT, PL_SMEM, st>>>(L, D);
+    if (ev1) record_event(ev1, st);
+    fold_tc_reduce_kernel<FI_GROUPS><<<dim3(4 * 64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+}
+
+int launch_split_planes(const float2* x, int64_t n, int C, int64_t pitch_in, uint32_t* hi, uint32_t* lo,
+                        int64_t pitch_out, int64_t out_off, unsigned long long* key, cudaStream_t st) {
+    if (n <= 0 || C <= 0) return 0;
+    const int64_t per_row = (n + 4 * 256 - 1) / (4 * 256);
+    split_planes_kernel<<<(unsigned)(per_row * C), 256, 0, st>>>(x, n, C, pitch_in, hi, lo, pitch_out, out_off, key);
+    return 1;
 }
 
 }  // namespace cyc

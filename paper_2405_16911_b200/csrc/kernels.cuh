@@ -15,11 +15,22 @@
 //             a 64-bit fixed-point phase (exact wrap) instead of the reference's
 //             drifting lead-phasor recurrence (proj/src/estimator.cpp:70-73).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace cyc {
+
+// Kernel attributes (the >48 KB dynamic shared memory opt-in) belong to the
+// current device's context: set them once per device, not once per process
+// (estimators may live on different devices of one process).
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    return (done.fetch_or(bit) & bit) == 0;
+}
 
 // One contiguous y-index range [n_start, n_end) of one stream whose fold goes
 // into accumulator slot `slot`.  Samples live in power-of-two device rings
@@ -74,6 +85,9 @@ struct FoldLaunch {
     unsigned long long* chk_key;
     long long chk_c0;
     int chk_channels;
+    // tensor-core folds: stages (16 periods) per TMEM accumulation chunk; the
+    // epilogue drains the accumulator into the fp32 partials after each chunk
+    int tc_drain;
 };
 
 // Launch descriptors carried in the kernel parameter block (<= 32 KB since
@@ -139,6 +153,32 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool sel
 // Fill D.xmap/ymap/p_base[si] for a linear segment (false: no TMA -- use the ring path).
 bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64_t rows, int Pf, int lag_lo,
                     int nlb);
+
+// Planes path (multi-lag-block self folds of device chunks, e.g. C5): the
+// bf16x3 split is done once per sample by launch_split_planes -- hi and lo
+// planes, one bf16x2 (re, im) word per sample, [channel][pitch] -- and the
+// fold kernel stages the planes with TMA straight into the UMMA operand layout
+// (no converter warps: shared memory carries only the TMA writes and the MMA
+// operand reads).  Tiles of every lag block run in one launch, ordered so that
+// the lag blocks of a residue block share the L2-resident planes.
+struct alignas(64) TcPlDesc {
+    CUtensorMap hmap[TC_SEGS];  // hi plane, bf16 box 64 x 16 periods, 128B swizzle (one atom column)
+    CUtensorMap lmap[TC_SEGS];  // lo plane
+    int64_t p_base[TC_SEGS];    // first period (row 0) of each segment's maps
+    FoldSeg segs[TC_SEGS];
+    const FoldTile* tiles;      // device tile table [n_tiles]
+};
+// Maps over planes whose element 0 is absolute sample p_base * Pf of the segment.
+bool encode_tcp_maps(TcPlDesc& D, int si, const uint32_t* hi, const uint32_t* lo, int64_t p_base, int64_t rows,
+                     int Pf, int64_t cols_samples);
+void launch_fold_tcp(const FoldLaunch& L, const TcPlDesc& D, const FoldGroup* groups, cudaStream_t st,
+                     cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+// hi/lo planes of n samples of every channel (rows pitch_in / pitch_out apart;
+// output index i + out_off) and the chunk's finite scan: the first non-finite
+// sample i (reference scan order, x only) -> atomicMin(*key, (2 i) * C + ch).
+// Returns the number of kernels launched.
+int launch_split_planes(const float2* x, int64_t n, int C, int64_t pitch_in, uint32_t* hi, uint32_t* lo,
+                        int64_t pitch_out, int64_t out_off, unsigned long long* key, cudaStream_t st);
 
 // Profiling events around kernel launches: plain records, or -- while a push
 // is being captured into a CUDA graph -- event-record nodes (so every replay
