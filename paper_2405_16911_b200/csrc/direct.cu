@@ -212,11 +212,9 @@ void launch_direct(const DirectLaunch& L, cudaStream_t st, double2* coh, double*
     const int SL = direct_lanes(L.T);
     const size_t smem = std::max<size_t>((size_t)(TILE + span + 2 * TILE) * sizeof(float2),
                                          (size_t)SL * MAXL * (DT / SL) * 2 * sizeof(float2));
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set))
         cudaFuncSetAttribute(direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
     direct_kernel<<<L.n_segs * L.A * L.splits, DT, smem, st>>>(L, span, SL);
     if (coh)
         direct_reduce_accum_kernel<<<dim3((L.T + 127) / 128, L.A, channels), 128, 0, st>>>(L, L.n_segs / channels,

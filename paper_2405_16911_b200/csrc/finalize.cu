@@ -165,12 +165,10 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
         int lg = 0;
         while ((1 << lg) < L.Pf) ++lg;
         const size_t smem = (size_t)L.Pf * 3 / 2 * sizeof(double2);
-        static bool attr_set = false;
-        if (!attr_set) {
+        static std::atomic<uint64_t> attr_set{0};
+        if (first_on_device(attr_set))
             cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  12288 * (int)sizeof(double2));
-            attr_set = true;
-        }
         finalize_fft_kernel<<<dim3(L.n_rows, nflag), std::min(512, std::max(32, L.Pf / 4)), smem, st>>>(L, lg);
     } else {
         finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
@@ -181,9 +179,8 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
 
 namespace cyc {
 void prepare_finalize_kernels() {
-    static bool done = false;
-    if (done) return;
+    static std::atomic<uint64_t> done{0};
+    if (!first_on_device(done)) return;
     cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12288 * (int)sizeof(double2));
-    done = true;
 }
 }  // namespace cyc

@@ -519,14 +519,14 @@ void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEven
 namespace cyc {
 // Set the dynamic-shared-memory attributes outside any stream capture.
 void prepare_fold_kernels() {
-    static bool done = false;
-    if (done) return;
+    static std::atomic<uint64_t> done{0};
+    if (!first_on_device(done)) return;
     cudaFuncSetAttribute(fold_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
     cudaFuncSetAttribute(fold_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<4>::SMEM);
     cudaFuncSetAttribute(fold_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<8>::SMEM);
     cudaFuncSetAttribute(fold_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
     cudaFuncSetAttribute(fold_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<4>::SMEM);
     cudaFuncSetAttribute(fold_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<8>::SMEM);
-    done = true;
+
 }
 }  // namespace cyc
