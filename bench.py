@@ -1,30 +1,36 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 cyclic-ACF hot path (BASELINE.json metric, configs[1]).
+"""Benchmark of the B200 cyclic-ACF hot path (BASELINE.json metric).
 
-Workload (config 2, "dense uniform grid"): 2^24 complex64 samples of QPSK,
-RRC rolloff 0.35, 4 samples/symbol, f_c = 0.1, SNR 5 dB (seeded synthetic);
-1024 cycle frequencies k/1024 in [-1/2, 1/2) x lags 0..63, conventional AND
-conjugate, one block average over the whole record.  The reference computes
-this as Full mode N = 1024, lags 0..63, pushes + average_frames(Coherent)
-(proj/tools/main.cpp:212-214, proj/src/estimator.cpp:86-105); F = 16383
-frames cover L_eff = 16,776,192 samples.
+Default workload: BASELINE.json configs[4] (C5, "large cyclic-domain profile"),
+the largest single-GPU configuration (BASELINE.json's metric names no config):
+2^26 complex64 samples of BPSK-RRC(0.35, 5 sps, f_c 0.07) + GMSK(BT 0.3,
+8 sps, f_c -0.11) at -6 dB, AWGN at 3 dB SNR (seeded synthetic; the paper's
+captures are not available); 8192 cycle frequencies k/8192 x lags 0..255,
+conventional AND conjugate, one block average.  The reference computes this
+as Full mode N = 8192, lags 0..255, N-sized pushes + average_frames(Coherent)
+(proj/src/estimator.cpp:39-105, proj/src/kernels.cpp:72-94, fft.cpp:44-87);
+F = 8191 frames cover L_eff = 67,100,672 samples.  `--config c1..c4` runs the
+other BASELINE configurations.
 
-One step = reset the estimator, push the record, read both (alpha, tau)
-tables.  Two measurements per run:
-  value  -- input already resident in HBM (cyc_push_device), both result
-            tables finalized into HBM (cyc_average_all to device memory),
-            CUDA events on the estimator's stream;
-  e2e    -- input in pinned HOST memory through the reference-facing C-ABI
-            call (cyc_push), H2D DMA and the D2H of both tables inside the
-            timed region.
-metric = direct-sum-equivalent (alpha, tau) updates/s = A*T*L_eff*flags / t
-(SURVEY §8d); the executed algorithm is the exact residue fold + fp64 FFT.
-The fold runs on the tensor cores (tcgen05, bf16x3 split of the fp32 samples,
-banded Gram product; FP32 FFMA2 kernel for partial periods), so the roofline
-line reports the fold's algorithmic rate (8 flops per lag x sample) against the
-measured bf16 tensor peak, with the executed MMA rate beside it.
+One step = reset the estimator, push the record, read every (alpha, tau)
+table.  Two measurements per run:
+  value  -- input already resident in HBM (cyc_push_device), the tables
+            finalized into HBM (cyc_average_all to device memory), CUDA events;
+  e2e    -- input in pinned HOST memory through the reference-facing C-ABI call
+            (cyc_push), H2D DMA and the D2H of the tables inside the timed region.
+metric = direct-sum-equivalent (alpha, tau) updates/s = A*T*L_eff*flags*channels / t
+(SURVEY §8d).  The executed algorithm is the exact residue fold (tcgen05 bf16x3
+banded Gram product; for several lag blocks from bf16 planes split once per
+sample) + fp64 FFT finalize.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Multi-GPU (`torchrun ... bench.py --gpus N`): C2/C5 are time-sharded
+(rank r folds frames [F r/N, F (r+1)/N) with `origin` anchoring the phases at
+absolute sample 0; an NCCL all-reduce sums the fp64 fold states before the
+finalize; the record is broadcast from rank 0 over NCCL at set-up); C4 is
+channel-sharded (64/N channels per rank, NCCL all-gather of the tables).
+Total work is fixed: `scaling` = "strong".  C1/C3 run replicas.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl reference]
 """
 from __future__ import annotations
 
@@ -44,27 +50,40 @@ sys.path.insert(0, ROOT)
 
 METRIC = "cyclic-ACF (alpha,tau) updates/s"
 UNIT = "updates/s"
-N_WIN, LAGS, A, FLAGS = 1024, 64, 1024, 2
-L_REC = 1 << 24
+DTYPE = "cf32 in; fold: bf16x3 split on tcgen05 (~fp32 products), fp32 TMEM accumulation drained every <=64 " \
+        "stages; fp64 reductions/FFT"
+
+# Block-average configurations (Full mode, conv + conj).  `bins`: the cycle
+# frequencies the config counts (C4: 128 of the 256 natural bins).
+BLOCK = {
+    "c2": dict(N=1024, T=64, A=1024, L=1 << 24, channels=1, shard="time",
+               workload="C2 dense grid: QPSK-RRC(0.35) 4 sps f_c=0.1 5 dB, 2^24 cf32 samples; 1024 alphas k/1024 x "
+                        "tau 0..63, conv+conj, one block average"),
+    "c4": dict(N=256, T=32, A=128, L=1 << 22, channels=64, shard="channel",
+               workload="C4 multi-channel: 64 x 2^22 (BPSK/QPSK-RRC, GMSK, noise; per-channel draws); 128 alphas "
+                        "k/256 in [-1/4,1/4) x tau 0..31, conv+conj, block average per channel"),
+    "c5": dict(N=8192, T=256, A=8192, L=1 << 26, channels=1, shard="time",
+               workload="C5 BPSK-RRC(0.35,5sps,0.07)+GMSK(BT0.3,8sps,-0.11)@-6dB, AWGN 3 dB, 2^26 cf32 samples; "
+                        "8192 alphas k/8192 x tau 0..255, conv+conj, one block average"),
+}
 
 
-def l_eff(L: int) -> int:
-    need = N_WIN + LAGS - 1
-    F = (L - need) // N_WIN + 1
-    return F * N_WIN
+def frames_of(c):
+    return (c["L"] - c["N"] - c["T"] + 1) // c["N"] + 1
 
 
-def updates(L: int) -> int:
-    return A * LAGS * l_eff(L) * FLAGS
+def updates_of(c):
+    return c["A"] * c["T"] * frames_of(c) * c["N"] * 2 * c["channels"]
 
 
-def config_block(n_gpus: int):
-    return {"workload": "C2 dense grid: QPSK-RRC(0.35) 4 sps f_c=0.1 5 dB, 2^24 cf32 samples/GPU; "
-                        "1024 alphas k/1024 x tau 0..63, conv+conj, one block average",
-            "samples_per_gpu": L_REC, "alphas": A, "lags": LAGS, "flags": ["conv", "conj"],
-            "win_len": N_WIN, "l_eff": l_eff(L_REC), "parallelism": f"independent records x{n_gpus}",
-            "l2": "input 134 MB > 126 MB L2 (no reuse across steps)",
-            "algorithm": "exact residue fold on tcgen05 (bf16x3 banded Gram product; FFMA2 for partial periods) + fp64 radix-2 FFT"}
+def gen_block(name, channels=None):
+    from paper_2405_16911_b200 import siggen
+    if name == "c2":
+        return siggen.c2_record(seed=2, n=1 << 24)[None]
+    if name == "c5":
+        return siggen.c5_record(n=1 << 26)[None]
+    chans = channels if channels is not None else range(64)
+    return np.stack([siggen.c4_channel(c, n=1 << 22) for c in chans])
 
 
 # ---------------------------------------------------------------------------
@@ -91,8 +110,6 @@ class Clocks:
             self.nv = None
             self.err = str(e)
             return
-        # the thread's start-up and first NVML call happen before the timed
-        # region begins (they cost ~0.1 ms of host time)
         self._ready = threading.Event()
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
@@ -144,6 +161,9 @@ def dist_init():
         import torch.distributed as dist
         backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
+            # communicator set-up lines (rank count, NVLS) on stderr for the scaling run
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return ws, rank, local
@@ -166,20 +186,6 @@ def barrier(ws: int):
         dist.barrier()
 
 
-DTYPE = "cf32 in; fold: bf16x3 split on tcgen05 (~fp32 products), fp32 TMEM accumulation; fp64 reductions/FFT"
-
-
-def traffic_from_profiles(tensor: bool):
-    name = "foldtc_ncu_summary.json" if tensor else "fold_ncu_summary.json"
-    p = os.path.join(ROOT, "profiles", name)
-    try:
-        with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("source")
-    except Exception:
-        return None, None
-
-
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -188,7 +194,19 @@ def measured_peaks():
         return None
 
 
-def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lags: int = 64) -> dict:
+def traffic_from_profiles(name: str, planes: bool):
+    """DRAM bytes per launch of the config's dominant fold kernel, from the
+    committed ncu summary of that config (profiles/<cfg>_fold_ncu_summary.json)."""
+    p = os.path.join(ROOT, "profiles", f"{name}_fold_ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    except Exception:
+        return None, None
+
+
+def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lags: int, name: str) -> dict:
     """The dominant kernel (the fold) from CUDA-event profiles on its stream.
 
     Algorithmic work per launch: 8 flops per (requested lag, folded sample)
@@ -207,7 +225,7 @@ def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lag
     rate = alg / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
     import paper_2405_16911_b200 as cyc
     fp32 = cyc.measure_fp32_peak(dev)
-    traffic, tsrc = traffic_from_profiles(tc > 0)
+    traffic, tsrc = traffic_from_profiles(name, lags > 64)
     common = {"traffic": traffic, "traffic_source": tsrc, "algorithmic_flops_per_launch": alg,
               "ms_per_launch": ms, "launches_per_step": (p1["launches"] - p0["launches"]) / steps,
               "fold_share_of_step": (p1["ms"] - p0["ms"]) / steps / ms_step,
@@ -216,11 +234,13 @@ def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lag
     if tc > 0:
         mp = measured_peaks() or {}
         tpeak = mp.get("bf16_tflops") or 1590.0
-        hpeak = mp.get("hbm_gbs") or 7700.0
+        hpeak = mp.get("hbm_gbs") or 6650.0
         ex_rate = exe / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
         abytes = alg / max(1, lags)  # 8 B per folded sample
         gbs = abytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
         ridge = tpeak * 1e12 / (hpeak * 1e9)
+        if traffic:
+            common["traffic_over_algorithmic_bytes"] = traffic / abytes
         tensor_view = {"achieved_tflops": rate, "peak_tflops": tpeak, "frac": rate / tpeak,
                        "executed_tflops": ex_rate, "executed_frac": ex_rate / tpeak,
                        "executed_per_algorithmic": exe / alg if alg else None,
@@ -229,9 +249,10 @@ def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lag
         hbm_view = {"achieved_gbs": gbs, "peak_gbs": hpeak, "frac": gbs / hpeak,
                     "algorithmic_bytes_per_launch": abytes,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, this pool)" if mp.get("hbm_gbs")
-                    else "fallback 7.7 TB/s (B200_PROFILING.md)"}
-        common.update({"kernel": "fold_tc_kernel (tcgen05 bf16x3 banded Gram product)",
-                       "intensity_flop_per_byte": float(lags), "ridge_flop_per_byte": ridge,
+                    else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+        kern = "fold_tcp_kernel (tcgen05 bf16x3 banded Gram product from split planes)" if lags > 64 else \
+            "fold_tc_kernel (tcgen05 bf16x3 banded Gram product, fused fp32->bf16 split)"
+        common.update({"kernel": kern, "intensity_flop_per_byte": float(lags), "ridge_flop_per_byte": ridge,
                        "tensor_view": tensor_view, "hbm_view": hbm_view,
                        "fp32_ffma_peak_tflops": fp32, "algorithmic_vs_fp32_peak": rate / fp32 if fp32 else None,
                        "tensor_launches_share": tc / n})
@@ -247,237 +268,17 @@ def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lag
 
 
 # ---------------------------------------------------------------------------
-def cpu_baseline(L_sample_frames: int, threads: int, x: np.ndarray):
-    """The reference library (oracle/_ref, else the C restatement) on the host cores."""
-    os.environ.setdefault("OMP_WAIT_POLICY", "passive")
-    os.environ["OMP_NUM_THREADS"] = str(threads)
-    from oracle.oracle import Oracle, RefLib, have_ref
-    lags = list(range(LAGS))
-    n = (L_sample_frames - 1) * N_WIN + N_WIN + LAGS - 1
-    xs = np.ascontiguousarray(x[:n])
-    if have_ref():
-        r = RefLib()
-        t0 = time.perf_counter()
-        F = 0
-        for conj in (0, 1):
-            _, F = r.block_average(1, conj, N_WIN, xs, xs, lags=lags)
-        dt = time.perf_counter() - t0
-        kind = "reference"
-    else:
-        o = Oracle()
-        t0 = time.perf_counter()
-        o.block_fold(xs, xs, np.arange(N_WIN), N_WIN, lags, 0, L_sample_frames * N_WIN)
-        dt = time.perf_counter() - t0
-        F = L_sample_frames
-        kind = "port"
-    ups = A * LAGS * F * N_WIN * FLAGS
-    return {"value": ups / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"Full N=1024 lags 0..63, conv+conj, {F} frames ({F * N_WIN} samples) of the C2 record, "
-                      f"N-sized pushes + running coherent sum, OMP_NUM_THREADS={threads}, "
-                      f"OMP_WAIT_POLICY={os.environ.get('OMP_WAIT_POLICY')}",
-            "seconds": dt, "msamples_per_s": F * N_WIN / dt / 1e6}
-
-
-def run_reference(args, ws, rank):
-    """--impl reference: the reference's own CPU path on this box's host cores."""
-    if rank != 0:
-        return
-    from paper_2405_16911_b200 import siggen
-    x = siggen.c2_record(seed=2, n=L_REC)
-    threads = os.cpu_count() or 1
-    frames = int(os.environ.get("CYC_REF_FRAMES", "4096"))  # ~1/4 of the record per step
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_baseline(64, threads, x)
-    vals = []
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(frames, threads, x))
-    v = statistics.median([c["value"] for c in vals])
-    cb = dict(vals[-1])
-    cb["value"] = v
-    ms = 1e3 * updates(L_REC) / v  # time the full record would take at this rate
-    cfgb = config_block(args.gpus)
-    cfgb["algorithm"] = ("reference cycstat (oracle/_ref, compiled from proj/src): full_window_values + radix-2 "
-                         "FFT per frame, fp64, OpenMP over lags")
-    cfgb["ms_per_step_basis"] = (f"the full C2 record at the measured rate; each timed step is a bounded "
-                                 f"{frames}-frame sample")
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": cfgb, "cpu_baseline": cb,
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-# ---------------------------------------------------------------------------
-def run_ours(args, ws, rank, local):
-    import torch
-    import paper_2405_16911_b200 as cyc
-    from paper_2405_16911_b200 import siggen
-
-    from paper_2405_16911_b200.shard import DeviceArray, time_shards
-
-    dev = local
-    torch.cuda.set_device(dev)
-    strong = args.scaling == "strong" and ws > 1
-    # weak: every GPU its own C2 record (independent receivers); strong: one
-    # record, time-sharded (SURVEY §8e), fold states summed with NCCL
-    x = siggen.c2_record(seed=2 if strong else 2 + rank, n=L_REC)
-    shard = time_shards(L_REC, N_WIN, LAGS - 1, 0, ws)[rank] if strong else None
-    if shard is not None:
-        x = np.ascontiguousarray(x[shard.sample0:shard.sample1])
-    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=N_WIN, lag_spec=cyc.LagSpec.Explicit(range(LAGS)),
-                              flags=cyc.Flags.BOTH, emit_frames=False, device=dev,
-                              origin=shard.origin if shard else 0)
-    est = cyc.CyclicCorrelator(cfg)
-    dx = torch.from_numpy(x.view(np.float32)).to(f"cuda:{dev}")
-    ptr = dx.data_ptr()
-    n_local = len(x)
-    F_total = l_eff(L_REC) // N_WIN
-
-    # the step's result: both flag tables, [1 channel][conv, conj][A * LAGS] --
-    # in HBM for `value`, DMA'd into pinned host memory for `e2e`
-    out_dev = torch.empty((1, 2, A * LAGS), dtype=torch.complex128, device=f"cuda:{dev}")
-    out_host = cyc.host_alloc((1, 2, A * LAGS), dtype=np.complex128)
-
-    def exchange():
-        """Time shards: NCCL all-reduce (sum) of the fp64 fold accumulators."""
-        if not strong:
-            return
-        import torch.distributed as dist
-        p, n, _ = est.fold_state()
-        dist.all_reduce(torch.as_tensor(DeviceArray(p, n), device=f"cuda:{dev}"))
-        est.fold_set_frames(F_total)
-
-    def step_device():
-        est.reset()
-        est.push_device(ptr, n_local)
-        exchange()
-        est.average_all(out=out_dev)
-
-    px = cyc.host_alloc(x.shape)
-    px[:] = x
-
-    def step_e2e():
-        est.reset()
-        est.push(px)
-        exchange()
-        est.average_all(out=out_host)
-
-    def timed(fn, k):
-        barrier(ws)
-        torch.cuda.synchronize(dev)
-        # events on the default stream: every push and device-out average is
-        # fenced against it (read after its earlier work, its later work waits
-        # for the engine's streams), so [e0, e1] brackets all of the K steps
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(k):
-            fn()
-        e1.record()
-        torch.cuda.synchronize(dev)
-        barrier(ws)
-        return e0.elapsed_time(e1) / k
-
-    # warm-up (untimed)
-    for _ in range(max(args.warmup, 0)):
-        # two device steps per round: reset alternates the accumulator buffer,
-        # and each (buffer, position) push is captured into a CUDA graph on
-        # its second occurrence -- the timed steps only replay
-        step_device()
-        step_device()
-        step_e2e()
-    # device-resident (value)
-    launches0 = est.kernel_launches()
-    clk = Clocks(dev)
-    ms_dev = timed(step_device, args.steps)
-    clocks = clk.stop()
-    launches = est.kernel_launches() - launches0
-    # the same K steps again with CUDA events around every fold launch on its
-    # stream: the kernel timing behind `roofline` (inside the replayed push
-    # graph those events are extra graph nodes that add ~15 us per step, so
-    # the value steps above run without them)
-    est.profile(True)
-    for _ in range(4):  # capture the profiled push graphs (both buffers) outside the pass
-        step_device()
-    prof0 = est.profile_read_ex()
-    ms_prof = timed(step_device, args.steps)
-    prof1 = est.profile_read_ex()
-    est.profile(False)
-    # e2e through the host C-ABI call
-    ms_e2e = timed(step_e2e, args.steps)
-
-    ms_dev_max = allreduce_max(ms_dev, ws)
-    ms_e2e_max = allreduce_max(ms_e2e, ws)
-    roof = roofline_block(prof0, prof1, args.steps, ms_dev_max, dev)
-    roof["timing"] = (f"CUDA events on the compute stream around each fold launch over a second pass of "
-                      f"{args.steps} device steps run right after the timed ones "
-                      f"({allreduce_max(ms_prof, ws):.4f} ms/step with the events)")
-    if rank != 0:
-        return
-    records = 1 if strong else ws
-    ups = updates(L_REC) * records
-    cfgb = config_block(ws)
-    if strong:
-        cfgb["parallelism"] = f"time-sharded record x{ws}: frame ranges per GPU + NCCL all-reduce of the fp64 folds"
-    line = {
-        "metric": METRIC, "value": ups / (ms_dev_max * 1e-3), "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev_max, "higher_is_better": True,
-        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": DTYPE,
-        "data": "synthetic",
-        "config": cfgb,
-        "msamples_per_s": L_REC * records / (ms_dev_max * 1e-3) / 1e6,
-        "e2e": {"value": ups / (ms_e2e_max * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e_max,
-                "h2d_bytes_per_step": n_local * 8, "d2h_bytes_per_step": 2 * A * LAGS * 16,
-                "msamples_per_s": L_REC * records / (ms_e2e_max * 1e-3) / 1e6,
-                "path": "cyc_push(pinned host cf32) + cyc_average_all (both tables, one D2H into pinned host)"},
-        "roofline": roof,
-        "gpu_launches": launches,
-        "clocks": clocks,
-    }
-    if ws == 1 and not args.no_cpu_baseline:
-        # the whole C2 record (16383 frames; ~10-15 s on 16 host cores)
-        line["cpu_baseline"] = cpu_baseline(int(os.environ.get("CYC_CPU_FRAMES", "16383")), os.cpu_count() or 1, x)
-    print(json.dumps(line), flush=True)
-
-
-# ---------------------------------------------------------------------------
-# The other BASELINE.json configurations (single GPU; `--config c1|c3|c4|c5`).
-# C2 above is the headline workload the driver runs.
+# CPU reference (oracle/_ref: the unmodified cycstat library) on the host cores
 # ---------------------------------------------------------------------------
 C1_CONV = [k / 8 for k in range(-2, 3)]
 C1_CONJ = [0.1 + k / 16 for k in range(-2, 3)]
 C3_ALPHAS = [m / 1024 for m in range(-128, 128)]
 
 
-def cfg_spec(name):
-    """(description, units of work, reference geometry) per config."""
-    if name == "c1":
-        F = (2 ** 20 - 4096 - 30) // 4096 + 1
-        return dict(workload="C1 GMSK BT0.3 8sps f_c=0.05 10 dB, 2^20 samples in 4096-sample pushes; Set N=4096 "
-                             "Symmetric(15); conv alpha=k/8, conj alpha=0.1+k/16 (k=-2..2); per-frame + coherent avg",
-                    updates=5 * 31 * F * 4096 * 2, samples=2 ** 20, F=F)
-    if name == "c3":
-        E = 65536
-        F = (2 ** 28 - E - 31) // E + 1
-        return dict(workload="C3 GMSK BT0.3 8sps f_c=0.02 0 dB, 2^28 samples in 8192-sample work() calls; recursive "
-                             "lambda=1-2^-12, 256 alpha=m/1024 x tau 0..31, conv, emit every 2^16",
-                    updates=256 * 32 * F * E, samples=2 ** 28, F=F)
-    if name == "c4":
-        F = (2 ** 22 - 256 - 31) // 256 + 1
-        return dict(workload="C4 64 channels x 2^22 (BPSK/QPSK-RRC, GMSK, noise; per-channel draws); Full N=256 "
-                             "lags 0..31, conv+conj, 128 alphas in [-1/4,1/4) counted, block average per channel",
-                    updates=64 * 2 * 128 * 32 * F * 256, samples=64 * 2 ** 22, F=F)
-    if name == "c5":
-        F = (2 ** 26 - 8192 - 255) // 8192 + 1
-        return dict(workload="C5 BPSK-RRC(0.35,5sps,0.07)+GMSK(BT0.3,8sps,-0.11)@-6dB, AWGN 3 dB, 2^26 samples; "
-                             "8192 alphas k/8192 x tau 0..255, conv+conj, block average",
-                    updates=8192 * 256 * F * 8192 * 2, samples=2 ** 26, F=F)
-    raise ValueError(name)
-
-
-def cfg_cpu_baseline(name, x, threads):
-    """Reference library on the host cores, bounded sample of the config's workload."""
+def ref_sample(name, x, threads):
+    """One bounded sample of the config's workload on the reference library:
+    (updates, seconds, description).  N-sized pushes + running coherent sum
+    (the reference's caller pattern), OpenMP over lags."""
     os.environ.setdefault("OMP_WAIT_POLICY", "passive")
     os.environ["OMP_NUM_THREADS"] = str(threads)
     from oracle.oracle import RefLib
@@ -503,221 +304,351 @@ def cfg_cpu_baseline(name, x, threads):
             for conj in (0, 1):
                 _, F = r.block_average(1, conj, 256, xs, xs, lags=list(range(32)))
         ups, smp = nch * 2 * 128 * 32 * F * 256, f"{nch} of 64 channels, whole channel ({F} frames), conv+conj"
+    elif name == "c2":
+        nf = 4096
+        xs = np.ascontiguousarray(x[0, :nf * 1024 + 63])
+        for conj in (0, 1):
+            _, F = r.block_average(1, conj, 1024, xs, xs, lags=list(range(64)))
+        ups, smp = 1024 * 64 * F * 1024 * 2, f"{F} of 16383 frames, conv+conj"
     else:
         nf = 48
-        xs = np.ascontiguousarray(x[:nf * 8192 + 255])
+        xs = np.ascontiguousarray(x[0, :nf * 8192 + 255])
         for conj in (0, 1):
             _, F = r.block_average(1, conj, 8192, xs, xs, lags=list(range(256)))
         ups, smp = 8192 * 256 * F * 8192 * 2, f"{F} of 8191 frames, conv+conj"
     dt = time.perf_counter() - t0
-    return {"value": ups / dt, "unit": UNIT, "cores": threads, "kind": "reference", "seconds": dt,
-            "sample": smp + f"; OMP_NUM_THREADS={threads}"}
+    return ups, dt, smp + f"; Full mode (Set for C1), N-sized pushes + coherent sum, OMP_NUM_THREADS={threads}, " \
+                          f"OMP_WAIT_POLICY={os.environ.get('OMP_WAIT_POLICY')}"
 
 
-def run_config(args, ws, rank, local):
+def cpu_baseline(name, x, threads):
+    ups, dt, smp = ref_sample(name, x, threads)
+    return {"value": ups / dt, "unit": UNIT, "cores": threads, "kind": "reference", "seconds": dt, "sample": smp}
+
+
+def parity_check(name, x, tables):
+    """The timed run's final tables against the fp64 oracle on the FULL record
+    (a subset of cycle frequencies, every lag, both flags) -- the checker, run
+    after timing in the CPU-baseline leg.  tables: [channels, 2, T * N]."""
+    from oracle.oracle import Oracle
+    c = BLOCK[name]
+    N, T = c["N"], c["T"]
+    F = frames_of(c)
+    o = Oracle()
+    rng = np.random.default_rng(7)
+    if name == "c4":
+        bins = np.array([k % N for k in range(-64, 64)])
+        chans = [0, 1, 2, 3, 21, 46, 63]
+    else:
+        bins = np.unique(np.concatenate([[0, 1, N - 1, N // 2], rng.choice(N, 60, replace=False)]))
+        chans = [0]
+    worst_rel, worst_cell = 0.0, 0.0
+    t0 = time.perf_counter()
+    for ch in chans:
+        xc = x[ch]
+        mp = float(np.mean(np.abs(xc.astype(np.complex128)) ** 2))
+        cv, cj = o.block_fold(xc, xc, bins, N, list(range(T)), 0, F * N)
+        for fi, want in ((0, cv), (1, cj)):
+            got = tables[ch, fi].reshape(T, N)[:, bins]
+            d = got - want.T
+            worst_rel = max(worst_rel, float(np.linalg.norm(d) / np.linalg.norm(want)))
+            worst_cell = max(worst_cell, float(np.abs(d).max() / mp))
+    return {"rel_l2": worst_rel, "max_abs_over_mean_power": worst_cell, "tolerance": {"rel_l2": 1e-4, "cell": 1e-5},
+            "pass": worst_rel <= 1e-4 and worst_cell <= 1e-5, "channels": chans, "bins": int(len(bins)),
+            "lags": T, "oracle": "oracle/cycoracle.c block_fold (fp64) on the full record",
+            "seconds": time.perf_counter() - t0}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU path (oracle/_ref) on this box's
+    host cores, each step a bounded sample of the config's workload."""
+    if rank != 0:
+        return
+    name = args.config
+    if name in BLOCK:
+        x = gen_block(name, channels=range(2) if name == "c4" else None)
+        wl = BLOCK[name]["workload"]
+    else:
+        from paper_2405_16911_b200 import siggen
+        x = siggen.c1_record(n=2 ** 20) if name == "c1" else siggen.c3_record(n=2 ** 22)
+        wl = SMALL[name]["workload"]
+    threads = os.cpu_count() or 1
+    for _ in range(min(1, args.warmup)):
+        ref_sample(name, x, threads)
+    samples = [ref_sample(name, x, threads) for _ in range(args.steps)]
+    ups, dt, smp = samples[-1]
+    value = statistics.median(u / t for u, t, _ in samples)
+    ms = statistics.median(t for _, t, _ in samples) * 1e3
+    cb = {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": smp,
+          "updates_per_step": ups}
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl, "algorithm": "reference cycstat (oracle/_ref, compiled from proj/src): "
+                                                    "full_window_values + radix-2 FFT per frame (Set: "
+                                                    "set_window_values), fp64, OpenMP over lags",
+                       "ms_per_step_basis": "measured: one bounded sample of the workload per step (see "
+                                            "cpu_baseline.sample); value = its updates / its time"},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Block-average configurations on the GPU (C2, C4, C5), sharded over ranks
+# ---------------------------------------------------------------------------
+def run_block(args, ws, rank, local):
     import torch
     import paper_2405_16911_b200 as cyc
-    from paper_2405_16911_b200 import siggen
+    from paper_2405_16911_b200.shard import DeviceArray, channel_shards, time_shards
 
     name = args.config
-    spec = cfg_spec(name)
+    c = BLOCK[name]
+    N, T, L, C_ = c["N"], c["T"], c["L"], c["channels"]
     dev = local
     torch.cuda.set_device(dev)
-    if name == "c1":
-        x = siggen.c1_record(n=2 ** 20)
-    elif name == "c3":
-        x = siggen.c3_record(n=2 ** 28)
-    elif name == "c4":
-        x = np.stack([siggen.c4_channel(c, n=2 ** 22) for c in range(64)])
-    else:
-        x = siggen.c5_record(n=2 ** 26)
-    if args.impl == "reference":
+    cuda = f"cuda:{dev}"
+    F_total = frames_of(c)
+    lay = T * N
+    # --- input: C2/C5 generated on rank 0 and broadcast over NCCL; C4 per rank (own channels)
+    if c["shard"] == "time":
         if rank == 0:
-            vals = [cfg_cpu_baseline(name, x, os.cpu_count() or 1) for _ in range(max(1, args.steps))]
-            cb = dict(vals[-1])
-            cb["value"] = statistics.median(v["value"] for v in vals)
-            print(json.dumps({"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
-                              "n_gpus": ws, "steps": args.steps, "warmup": 0, "higher_is_better": True,
-                              "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                              "config": {"workload": spec["workload"]}, "cpu_baseline": cb,
-                              "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                                      "d2h_bytes_per_step": 0}}), flush=True)
-        return
-
-    ests = []
-    if name == "c1":
-        # one pass over the stream: union alpha set, both functions (the reference needs two
-        # estimators; only the 5 conv + 5 conj tables the config asks for are counted)
-        ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
-            mode=cyc.Mode.Set, win_len=4096, alphas=C1_CONV + C1_CONJ, lag_spec=cyc.LagSpec.Symmetric(15),
-            flags=cyc.Flags.BOTH, device=dev)))
-    elif name == "c3":
-        ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
-            mode=cyc.Mode.Recursive, win_len=65536, alphas=C3_ALPHAS, lag_spec=cyc.LagSpec.Explicit(range(32)),
-            lam=1 - 2 ** -12, device=dev)))
-    elif name == "c4":
-        ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
-            mode=cyc.Mode.Full, win_len=256, lag_spec=cyc.LagSpec.Explicit(range(32)), flags=cyc.Flags.BOTH,
-            emit_frames=False, channels=64, device=dev)))
+            x = gen_block(name)
+            d_all = torch.from_numpy(x.view(np.float32)).to(cuda)
+        else:
+            x = None
+            d_all = torch.empty((1, 2 * L), dtype=torch.float32, device=cuda)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.broadcast(d_all, src=0)
+        sh = time_shards(L, N, T - 1, 0, ws)[rank]
+        n_local = sh.sample1 - sh.sample0
+        d_loc = d_all[:, 2 * sh.sample0:2 * sh.sample1]  # a view: the estimator folds it in place
+        ch0, ch1, origin = 0, 1, sh.origin
     else:
-        ests.append(cyc.CyclicCorrelator(cyc.EstimatorConfig(
-            mode=cyc.Mode.Full, win_len=8192, lag_spec=cyc.LagSpec.Explicit(range(256)), flags=cyc.Flags.BOTH,
-            emit_frames=False, device=dev)))
-    est = ests[0]
-    lay = cyc.layout_len(est.layout())
-    outs = [np.zeros(lay, dtype=np.complex128) for _ in range(2)]
-    n = x.shape[-1]
+        ch0, ch1 = channel_shards(C_, ws)[rank]
+        x = gen_block(name, channels=range(ch0, ch1))
+        d_loc = torch.from_numpy(x.view(np.float32)).to(cuda)
+        n_local, origin = L, 0
+    nch = ch1 - ch0
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=N, lag_spec=cyc.LagSpec.Explicit(range(T)),
+                              flags=cyc.Flags.BOTH, emit_frames=False, channels=nch, device=dev, origin=origin)
+    est = cyc.CyclicCorrelator(cfg)
+    ptr = d_loc.data_ptr()
+    host = cyc.host_alloc((nch, n_local))
+    host[:] = d_loc.cpu().numpy().view(np.complex64).reshape(nch, n_local)
+    out_dev = torch.empty((nch, 2, lay), dtype=torch.complex128, device=cuda)
+    full_dev = out_dev if (c["shard"] == "time" or ws == 1) else \
+        torch.empty((C_, 2, lay), dtype=torch.complex128, device=cuda)
+    out_host = cyc.host_alloc((C_ if c["shard"] == "channel" else 1, 2, lay), dtype=np.complex128)
+    engine_stream = torch.cuda.ExternalStream(est.stream(), device=cuda)
 
-    if name in ("c1", "c3"):
-        chunk = 4096 if name == "c1" else 8192
-        px = cyc.host_alloc(x.shape)
-        px[:] = x
+    def exchange():
+        """Time shards: NCCL all-reduce (sum) of the fp64 fold accumulators."""
+        if c["shard"] != "time" or ws == 1:
+            return
+        import torch.distributed as dist
+        torch.cuda.current_stream().wait_stream(engine_stream)
+        p, n, _ = est.fold_state()
+        dist.all_reduce(torch.as_tensor(DeviceArray(p, n), device=cuda))
+        est.fold_set_frames(F_total)
 
-        def step_e2e():
-            nfr = 0
-            for e in ests:
-                e.reset()
-            for off in range(0, n, chunk):
-                for e in ests:
-                    nfr += len(e.push(px[off:off + chunk]))
-            for e in ests:
-                e.average(out=outs[0])
-            return nfr
-        step_dev = None
-    else:
-        dx = torch.from_numpy(x.view(np.float32)).to(f"cuda:{dev}")
-        px = cyc.host_alloc(x.shape)
-        px[:] = x
+    def gather():
+        """Channel shards: NCCL all-gather of the (channel, flag) tables."""
+        if c["shard"] != "channel" or ws == 1:
+            return
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(full_dev, out_dev)
 
-        shape = (est.config().channels, 2, lay)
-        out_dev = torch.empty(shape, dtype=torch.complex128, device=f"cuda:{dev}")
-        out_host = cyc.host_alloc(shape, dtype=np.complex128)
+    def step_device():
+        est.reset()
+        est.push_device(ptr, n_local)
+        exchange()
+        est.average_all(out=out_dev)
+        gather()
 
-        def step_dev():  # result tables stay in HBM
-            est.reset()
-            est.push_device(dx.data_ptr(), n)
+    def step_e2e():
+        est.reset()
+        est.push(host)
+        exchange()
+        if c["shard"] == "channel" and ws > 1:
             est.average_all(out=out_dev)
-
-        def step_e2e():  # every (channel, flag) table: one finalize + one D2H into pinned host
-            est.reset()
-            est.push(px)
+            gather()
+            if rank == 0:
+                out_host[:] = full_dev.cpu().numpy()
+        elif rank == 0 or c["shard"] == "channel":
             est.average_all(out=out_host)
 
-    def timed(fn, k):  # default-stream events bracket all engine streams (see the C2 arm)
+    def timed(fn, k):
+        barrier(ws)
         torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # default-stream events bracket every engine stream: pushes read after
+        # earlier default-stream work and later default-stream work waits for them
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(k):
             fn()
         e1.record()
         torch.cuda.synchronize(dev)
+        barrier(ws)
         return e0.elapsed_time(e1) / k
 
-    cxx = None
-    if name in ("c1", "c3"):
-        # the streaming call pattern through the C-ABI from C++ (no Python per call)
-        from paper_2405_16911_b200.build import build_tools
-        exe = build_tools()
-        fd, path = tempfile.mkstemp(suffix=".cf32", dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
-        os.close(fd)
-        x.astype(np.complex64).tofile(path)
-        clk_c = Clocks(dev)
-        r = subprocess.run([exe, name, path, str(args.steps), str(max(args.warmup, 1))], capture_output=True,
-                           text=True)
-        clk_cxx = clk_c.stop()
-        os.unlink(path)
-        if r.returncode != 0:
-            raise RuntimeError(r.stderr)
-        cxx = json.loads(r.stdout.strip().splitlines()[-1])
-        cxx["clocks"] = clk_cxx
-    for _ in range(max(args.warmup, 1)):
-        if step_dev:  # both accumulator buffers' push graphs (see the C2 arm)
-            step_dev()
-            step_dev()
+    for _ in range(max(args.warmup, 3)):
+        # two device steps per round: reset alternates the accumulator buffer,
+        # and each (buffer, position) push is captured into a CUDA graph on its
+        # second occurrence -- the timed steps replay
+        step_device()
+        step_device()
         step_e2e()
-    l0 = sum(e.kernel_launches() for e in ests)
+    launches0 = est.kernel_launches()
     clk = Clocks(dev)
-    ms_dev = timed(step_dev, args.steps) if step_dev else None
-    ms_e2e = timed(step_e2e, args.steps) if not step_dev else None
+    ms_dev = timed(step_device, args.steps)
     clocks = clk.stop()
-    launches = sum(e.kernel_launches() for e in ests) - l0
-    # kernel timing: a second pass with CUDA events around every fold launch
-    fn_prof = step_dev or step_e2e
+    launches = est.kernel_launches() - launches0
+    final_tables = full_dev.cpu().numpy() if rank == 0 else None
+    # the same K steps again with CUDA events around every fold launch on its
+    # stream: the kernel timing behind `roofline` (inside the replayed push
+    # graph those events are extra graph nodes, so the value steps run without them)
     est.profile(True)
-    if step_dev:
-        for _ in range(4):
-            step_dev()
+    for _ in range(4):
+        step_device()
     prof0 = est.profile_read_ex()
-    timed(fn_prof, args.steps)
+    ms_prof = timed(step_device, args.steps)
     prof1 = est.profile_read_ex()
     est.profile(False)
-    if step_dev:
-        ms_e2e = timed(step_e2e, args.steps)
-    ms_val = ms_dev if ms_dev is not None else ms_e2e
-    roof = roofline_block(prof0, prof1, args.steps, ms_val, dev,
-                          lags={"c1": 31, "c3": 32, "c4": 32, "c5": 256}[name])
-    line = {"metric": METRIC, "value": spec["updates"] / (ms_val * 1e-3), "unit": UNIT, "n_gpus": 1,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_val, "higher_is_better": True,
+    ms_e2e = timed(step_e2e, args.steps)
+
+    ms_dev_max = allreduce_max(ms_dev, ws)
+    ms_e2e_max = allreduce_max(ms_e2e, ws)
+    roof = roofline_block(prof0, prof1, args.steps, ms_dev_max, dev, T, name)
+    roof["timing"] = (f"CUDA events on the compute stream around each fold launch over a second pass of "
+                      f"{args.steps} device steps run right after the timed ones "
+                      f"({allreduce_max(ms_prof, ws):.4f} ms/step with the events)")
+    if rank != 0:
+        return
+    ups = updates_of(c)
+    par = f"{'time' if c['shard'] == 'time' else 'channel'}-sharded x{ws}" + (
+        ": frame ranges per GPU + NCCL all-reduce of the fp64 fold states" if c["shard"] == "time" else
+        ": 64/N channels per GPU + NCCL all-gather of the tables") if ws > 1 else "single GPU"
+    cfgb = {"workload": c["workload"], "samples": L, "channels": C_, "alphas": c["A"], "lags": T,
+            "flags": ["conv", "conj"], "win_len": N, "l_eff": frames_of(c) * N, "parallelism": par,
+            "l2": f"input {L * C_ * 8 / 1e6:.0f} MB > 126 MB L2 (no reuse across steps)",
+            "algorithm": est.algorithm() + (" (planes path: split once per sample + conversion-free tcgen05 fold)"
+                                            if T > 64 else " (fused fp32->bf16 split in the tcgen05 fold)")}
+    h2d = n_local * nch * 8
+    d2h = int(out_host.nbytes)
+    line = {
+        "metric": METRIC, "value": ups / (ms_dev_max * 1e-3), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev_max, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic (seeded generators, "
+                                                                          "paper_2405_16911_b200/siggen.py)",
+        "config": cfgb,
+        "msamples_per_s": L * C_ / (ms_dev_max * 1e-3) / 1e6,
+        "e2e": {"value": ups / (ms_e2e_max * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e_max,
+                "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h,
+                "msamples_per_s": L * C_ / (ms_e2e_max * 1e-3) / 1e6,
+                "path": "cyc_push(pinned host cf32) + cyc_average_all (every table, one D2H into pinned host)"},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        if x is None:
+            x = gen_block(name)
+        line["cpu_baseline"] = cpu_baseline(name, x, os.cpu_count() or 1)
+        line["parity"] = parity_check(name, x, final_tables)
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Small-call configurations (C1, C3): the streaming call pattern through the
+# C-ABI from C++ (tools/stream_bench), replicas for N > 1
+# ---------------------------------------------------------------------------
+SMALL = {
+    "c1": dict(workload="C1 GMSK BT0.3 8sps f_c=0.05 10 dB, 2^20 samples in 4096-sample pushes; Set N=4096 "
+                        "Symmetric(15); conv alpha=k/8, conj alpha=0.1+k/16 (k=-2..2); per-frame + coherent avg",
+               samples=2 ** 20, chunk=4096),
+    "c3": dict(workload="C3 GMSK BT0.3 8sps f_c=0.02 0 dB, 2^28 samples in 8192-sample work() calls; recursive "
+                        "lambda=1-2^-12, 256 alpha=m/1024 x tau 0..31, conv, emit every 2^16",
+               samples=2 ** 28, chunk=8192),
+}
+
+
+def small_updates(name):
+    if name == "c1":
+        F = (2 ** 20 - 4096 - 30) // 4096 + 1
+        return 5 * 31 * F * 4096 * 2
+    E = 65536
+    F = (2 ** 28 - E - 31) // E + 1
+    return 256 * 32 * F * E
+
+
+def run_small(args, ws, rank, local):
+    from paper_2405_16911_b200 import siggen
+    from paper_2405_16911_b200.build import build_tools
+    name = args.config
+    s = SMALL[name]
+    x = siggen.c1_record(n=2 ** 20) if name == "c1" else siggen.c3_record(n=2 ** 28)
+    exe = build_tools()
+    fd, path = tempfile.mkstemp(suffix=".cf32", dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    os.close(fd)
+    x.astype(np.complex64).tofile(path)
+    barrier(ws)
+    clk = Clocks(local)
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=str(local))
+    r = subprocess.run([exe, name, path, str(args.steps), str(max(args.warmup, 1))], capture_output=True, text=True,
+                       env=env)
+    clocks = clk.stop()
+    os.unlink(path)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    cxx = json.loads(r.stdout.strip().splitlines()[-1])
+    ms = allreduce_max(cxx["ms_per_step"], ws)
+    if rank != 0:
+        return
+    ups = small_updates(name) * ws
+    gbs = s["samples"] * ws * 8 / (ms * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": ups / (ms * 1e-3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
-            "config": {"workload": spec["workload"], "algorithm": est.algorithm(),
-                       "value_path": "device-resident input" if step_dev else
-                       "host pushes of the stated chunk size (the workload is the streaming call pattern)"},
-            "msamples_per_s": spec["samples"] / (ms_val * 1e-3) / 1e6,
-            "e2e": {"value": spec["updates"] / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
-                    "h2d_bytes_per_step": int(x.size) * 8,
-                    "d2h_bytes_per_step": int(lay * 16 * (2 * est.config().channels if step_dev else len(ests)))},
-            "roofline": roof,
-            "gpu_launches": launches, "clocks": clocks}
-    if cxx is not None:
-        # headline for the small-call configs: the C++ caller through the C-ABI
-        line["python_ms_per_step"] = ms_val
-        line["ms_per_step"] = cxx["ms_per_step"]
-        line["value"] = spec["updates"] / (cxx["ms_per_step"] * 1e-3)
-        line["msamples_per_s"] = spec["samples"] / (cxx["ms_per_step"] * 1e-3) / 1e6
-        line["e2e"]["value"] = line["value"]
-        line["e2e"]["ms_per_step"] = cxx["ms_per_step"]
-        line["e2e"]["path"] = f"tools/stream_bench (C++): cyc_push of {4096 if name == 'c1' else 8192}-sample " \
-                              f"chunks from pinned host memory, frames delivered to a sink"
-        line["gpu_launches"] = int(cxx["launches_per_step"] * args.steps)
-        line["clocks"] = cxx["clocks"]
-        line["config"]["value_path"] = "host pushes through the C-ABI from C++ (tools/stream_bench)"
-        line["h2d_bound_ms"] = spec["samples"] * 8 / 53.6e9 * 1e3  # measured pinned H2D 53.6 GB/s
-        # small calls: the bound is the ingest of 8 B/sample over the host->device
-        # link (SURVEY §8 d), not a kernel -- the fold of a call is microseconds
-        gbs = spec["samples"] * 8 / (cxx["ms_per_step"] * 1e-3) / 1e9
-        roof["name"] = "kernel_view"
-        line["roofline"] = {"bound": "pcie", "achieved": gbs, "peak": 53.6, "unit": "GB/s", "frac": gbs / 53.6,
-                            "traffic": None,
-                            "peak_source": "measured pinned H2D copy bandwidth on this box type (tools/pcie_probe.py)",
-                            "algorithmic_unit": "8 B per input sample moved host -> device",
-                            "note": "streaming call pattern: the per-call host work (finite screen + staging copy "
-                                    "of the caller's chunk, DMA issue, synchronous frame delivery) binds",
-                            "kernel_view": roof}
-    if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cfg_cpu_baseline(name, x, os.cpu_count() or 1)
+            "config": {"workload": s["workload"], "parallelism": f"replicas x{ws} (the path does not shard)",
+                       "value_path": "tools/stream_bench (C++): cyc_push of "
+                                     f"{s['chunk']}-sample chunks from pinned host memory, frames to a sink"},
+            "msamples_per_s": s["samples"] * ws / (ms * 1e-3) / 1e6,
+            "e2e": {"value": ups / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+                    "h2d_bytes_per_step": s["samples"] * 8 * ws, "d2h_bytes_per_step": None,
+                    "path": "the streaming call pattern is end to end: host chunks in, frames out"},
+            "roofline": {"bound": "pcie", "achieved": gbs, "peak": 53.6 * ws, "unit": "GB/s", "frac": gbs / 53.6 / ws,
+                         "traffic": None,
+                         "peak_source": "measured pinned H2D copy bandwidth on this box type (tools/pcie_probe.py)",
+                         "algorithmic_unit": "8 B per input sample moved host -> device",
+                         "note": "streaming call pattern: per-call host work and per-emission kernel latency bind"},
+            "gpu_launches": int(cxx["launches_per_step"] * args.steps), "clocks": clocks,
+            "h2d_bound_ms": s["samples"] * 8 / 53.6e9 * 1e3}
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, x, os.cpu_count() or 1)
     print(json.dumps(line), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak = one C2 record per GPU; strong = one record time-sharded + NCCL fold reduce")
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
-                    help="BASELINE.json configuration (c2 = the headline workload)")
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE.json configuration (c5 = the largest single-GPU config, the default)")
     args = ap.parse_args()
     ws, rank, local = dist_init()
     try:
-        if args.config != "c2":
-            run_config(args, ws, rank, local)
-        elif args.impl == "reference":
+        if args.impl == "reference":
             run_reference(args, ws, rank)
+        elif args.config in BLOCK:
+            run_block(args, ws, rank, local)
         else:
-            run_ours(args, ws, rank, local)
+            run_small(args, ws, rank, local)
     finally:
         if ws > 1:
             import torch.distributed as dist
