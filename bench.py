@@ -400,7 +400,7 @@ def run_reference(args, ws, rank):
 def run_block(args, ws, rank, local):
     import torch
     import paper_2405_16911_b200 as cyc
-    from paper_2405_16911_b200.shard import DeviceArray, channel_shards, time_shards
+    from paper_2405_16911_b200.shard import channel_shards, exchange_time_shards, gather_channel_tables, time_shards
 
     name = args.config
     c = BLOCK[name]
@@ -441,24 +441,20 @@ def run_block(args, ws, rank, local):
     full_dev = out_dev if (c["shard"] == "time" or ws == 1) else \
         torch.empty((C_, 2, lay), dtype=torch.complex128, device=cuda)
     out_host = cyc.host_alloc((C_ if c["shard"] == "channel" else 1, 2, lay), dtype=np.complex128)
-    engine_stream = torch.cuda.ExternalStream(est.stream(), device=cuda)
 
     def exchange():
         """Time shards: NCCL all-reduce (sum) of the fp64 fold accumulators."""
         if c["shard"] != "time" or ws == 1:
             return
         import torch.distributed as dist
-        torch.cuda.current_stream().wait_stream(engine_stream)
-        p, n, _ = est.fold_state()
-        dist.all_reduce(torch.as_tensor(DeviceArray(p, n), device=cuda))
-        est.fold_set_frames(F_total)
+        exchange_time_shards(est, F_total, dist)
 
     def gather():
         """Channel shards: NCCL all-gather of the (channel, flag) tables."""
         if c["shard"] != "channel" or ws == 1:
             return
         import torch.distributed as dist
-        dist.all_gather_into_tensor(full_dev, out_dev)
+        full_dev.copy_(gather_channel_tables(out_dev, ws, dist))
 
     def step_device():
         est.reset()

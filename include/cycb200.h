@@ -45,7 +45,8 @@ typedef enum {
     CYC_ERR_DATA = 3,     /* DataError    (non-finite sample; absolute index)  */
     CYC_ERR_CUDA = 4,     /* device / driver failure (no CPU fallback exists)  */
     CYC_ERR_INTERNAL = 5, /* std::logic_error equivalent                       */
-    CYC_ERR_IO = 6        /* IoError / FormatError (errors.hpp:32-38)          */
+    CYC_ERR_IO = 6,       /* IoError      (unreadable file, errors.hpp:32-34)  */
+    CYC_ERR_FORMAT = 7    /* FormatError  (malformed file, errors.hpp:36-38)   */
 } cyc_status;
 
 /* Estimator mode (proj/include/cycstat/types.hpp:22-25) plus the

@@ -7,7 +7,8 @@
 //   SetLayout / FullLayout / FrameLayout / layout_len /
 //   flat_index / full_bin_to_alpha                          types.hpp:68-94
 //   CyclicFrame                                             types.hpp:97-104
-//   UsageError / ConfigError / DataError                    errors.hpp:13-42
+//   UsageError / ConfigError / IoError / FormatError /
+//   DataError / NoFeatureError                              errors.hpp:13-46
 //   CyclicCorrelator(cfg), push(x, y) -> vector<CyclicFrame>,
 //   buffer_need / consumed / frames_emitted                 estimator.hpp:97-137
 //   AverageMode / average_frames                            estimator.hpp:143-148
@@ -41,19 +42,29 @@ using cx = std::complex<double>;
 struct UsageError : std::runtime_error {
     explicit UsageError(const std::string& m) : std::runtime_error(m) {}
 };
-struct ConfigError : UsageError {
+struct ConfigError : UsageError {  // errors.hpp:17-30: the message joins every violation
     std::vector<std::string> violations;
-    ConfigError(std::vector<std::string> v, const std::string& msg) : UsageError(msg), violations(std::move(v)) {}
+    explicit ConfigError(std::vector<std::string> v) : UsageError(join(v)), violations(std::move(v)) {}
+
+private:
+    static std::string join(const std::vector<std::string>& v) {
+        std::string s = "invalid config:";
+        for (const auto& e : v) s += " [" + e + "]";
+        return s;
+    }
 };
-struct DataError : std::runtime_error {
+struct DataError : std::runtime_error {  // errors.hpp:40-42; `index` (extension): the absolute sample, or -1
     std::int64_t index = -1;
-    DataError(const std::string& m, std::int64_t i) : std::runtime_error(m), index(i) {}
+    explicit DataError(const std::string& m, std::int64_t i = -1) : std::runtime_error(m), index(i) {}
 };
 struct NoFeatureError : DataError {  // errors.hpp:44-46
     explicit NoFeatureError(const std::string& m) : DataError(m, -1) {}
 };
 struct IoError : std::runtime_error {  // errors.hpp:32-34
     explicit IoError(const std::string& m) : std::runtime_error(m) {}
+};
+struct FormatError : IoError {  // errors.hpp:36-38 (malformed input files; caught by proj/tools/main.cpp:157,355)
+    explicit FormatError(const std::string& m) : IoError(m) {}
 };
 struct DeviceError : std::runtime_error {  // no CPU fallback exists
     explicit DeviceError(const std::string& m) : std::runtime_error(m) {}
@@ -202,12 +213,13 @@ namespace detail {
             v.push_back(msg.substr(p + 1, q - p - 1));
             p = q;
         }
-        throw ConfigError(std::move(v), msg);
+        throw ConfigError(std::move(v));  // same message: "invalid config: [..] [..]"
     }
     if (code == CYC_ERR_USAGE) throw UsageError(msg);
     if (code == CYC_ERR_DATA) throw DataError(msg, index);
     if (code == CYC_ERR_CUDA) throw DeviceError(msg);
     if (code == CYC_ERR_IO) throw IoError(msg);
+    if (code == CYC_ERR_FORMAT) throw FormatError(msg);
     throw std::logic_error(msg);
 }
 }  // namespace detail

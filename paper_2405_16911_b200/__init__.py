@@ -35,7 +35,7 @@ __all__ = [
     "CyclicFrame", "CyclicCorrelator", "validate_config", "layout_len", "flat_index",
     "full_bin_to_alpha", "average_frames", "compute_set_window", "compute_full_window",
     "UsageError", "ConfigError", "DataError", "CudaError", "LogicError", "lib", "host_alloc",
-    "NoFeatureError", "IoError", "estimate_cfo_ccf", "write_cf32", "PulseKind", "CpmParams", "OracleTable",
+    "NoFeatureError", "IoError", "FormatError", "estimate_cfo_ccf", "write_cf32", "PulseKind", "CpmParams", "OracleTable",
     "random_symbols", "cpm_pulse", "cpm_modulate", "gmsk_mc_oracle",
 ]
 
@@ -68,7 +68,11 @@ class NoFeatureError(DataError):
 
 
 class IoError(RuntimeError):
-    """errors.hpp:32-34 (FormatError, errors.hpp:36-38, is reported the same way)."""
+    """errors.hpp:32-34: an unreadable input file."""
+
+
+class FormatError(IoError):
+    """errors.hpp:36-38: a malformed input file (e.g. a truncated cf32 record)."""
 
 
 class CudaError(RuntimeError):
@@ -389,6 +393,8 @@ def _raise(code: int, msg: str, index: int = -1):
         raise CudaError(msg)
     if code == 6:
         raise IoError(msg)
+    if code == 7:
+        raise FormatError(msg)
     raise LogicError(msg)
 
 
@@ -473,6 +479,15 @@ class CyclicCorrelator:
 
     def fold_set_frames(self, frames: int):
         self._check(self._L.cyc_fold_set_frames(self._h, int(frames)))
+
+    def fold_tensor(self):
+        """The block-mode fold state as a torch float64 CUDA tensor viewing the
+        estimator's accumulators in place ([channels][t_pad][Pf][4]: xr*yr,
+        xi*yr, xr*yi, xi*yi per absolute residue), for collectives."""
+        import torch
+        from .shard import DeviceArray
+        p, n, _ = self.fold_state()
+        return torch.as_tensor(DeviceArray(p, n), device=f"cuda:{self._cfg.device}")
 
     def reset(self):
         """Fresh stream state (same as constructing a new estimator with this config)."""

@@ -56,7 +56,7 @@ int cyc_push_cf32_file(cyc_est* est, const char* path, cyc_frame_sink sink, void
     const size_t bytes = (size_t)st.st_size;
     if (bytes % 8 != 0) {
         ::close(fd);
-        return fail(est, CYC_ERR_IO, std::string(path) + " is truncated: length is not a multiple of 8 bytes");
+        return fail(est, CYC_ERR_FORMAT, std::string(path) + " is truncated: length is not a multiple of 8 bytes");
     }
     const int C = 1;  // one stream per file (multi-channel callers push arrays)
     const size_t n = bytes / 8;

@@ -7,8 +7,14 @@
   per-GPU fold accumulators are then summed (NCCL all-reduce of
   channels x t_pad x Pf x 4 fp64 -- 2 MiB at C2, 64 MiB at C5) and the frame
   counts added.  Exact: the coherent average is linear in the frames.
-* channel shards (C4): independent streams, no data-path collective.
-* replicas (weak scaling): every GPU its own record.
+* channel shards (C4): independent streams; the (channel, flag) tables are
+  all-gathered at the end (no collective on the data path).
+* replicas (C1, C3: the small-call paths do not shard): every GPU its own record.
+
+The exchange steps below are what bench.py runs between the push and the
+finalize; they take any estimator-like object with fold_tensor(),
+fold_set_frames() (time shards) and any torch.distributed group (NCCL on the
+GPUs; gloo in the CPU tests, tests/test_shard.py).
 """
 from __future__ import annotations
 
@@ -61,3 +67,30 @@ class DeviceArray:
     def __init__(self, ptr: int, count: int, typestr: str = "<f8"):
         self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
                                          "version": 3, "strides": None}
+
+
+def exchange_time_shards(est, frames_total: int, dist, group=None):
+    """Time shards: sum every rank's fp64 fold state in place (all-reduce) and
+    set the record's frame count -- afterwards each rank's average() is the
+    whole record's (the states are indexed by absolute residue, so no phase
+    re-anchoring is needed).  Returns the summed state tensor."""
+    t = est.fold_tensor()  # synchronizes the estimator's fold before the collective reads it
+    dist.all_reduce(t, group=group)
+    est.fold_set_frames(frames_total)
+    return t
+
+
+def gather_channel_tables(local, world: int, dist, group=None):
+    """Channel shards: all-gather [channels/world, flags, layout] tables into
+    [channels, flags, layout] (rank order = channel order)."""
+    import torch
+    if world == 1:
+        return local
+    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    try:
+        dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    except (RuntimeError, AttributeError):  # backends without the fused form
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local.contiguous(), group=group)
+        out = torch.cat(parts)
+    return out

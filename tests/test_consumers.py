@@ -149,14 +149,14 @@ def test_push_file_streams_across_calls(cyc, tmp_path):
 @pytest.mark.gpu
 def test_push_file_errors(cyc, tmp_path):
     """io.cpp:92-100: unreadable -> IoError; length % 8 != 0 -> FormatError
-    (reported as IoError); non-finite -> DataError with the absolute index and
-    nothing consumed."""
+    (an IoError); non-finite -> DataError with the absolute index and nothing
+    consumed."""
     a = cyc.CyclicCorrelator(_set_cfg(cyc))
     with pytest.raises(cyc.IoError, match="cannot open"):
         a.push_file(str(tmp_path / "missing.cf32"))
     bad = tmp_path / "trunc.cf32"
     bad.write_bytes(b"\0" * 12)
-    with pytest.raises(cyc.IoError, match="truncated"):
+    with pytest.raises(cyc.FormatError, match="truncated"):
         a.push_file(str(bad))
     x = rand_c(1000, 33)
     x[417] = np.inf

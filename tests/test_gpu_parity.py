@@ -603,3 +603,40 @@ def test_multichannel_first_bad_sample(cyc, kind):
         call()
     assert ei.value.index == c0 + 2_000_123
     assert est.consumed() == c0
+
+
+# proj/src/fft.cpp:72-87: non-power-of-two N takes the direct DFT -- on the GPU
+# the exact-index DFT finalize over Pf = lcm(N, 128)
+@pytest.mark.parametrize("N", [1000, 768])
+def test_full_mode_non_pow2_window_vs_oracle(cyc, oracle, N):
+    x = rand_c(N * 9 + 17, 940 + N)
+    lags = [-2, 0, 3, 7]
+    mp = mean_power(x)
+    for conj in (False, True):
+        est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, conj))
+        frames = est.push(x)
+        want = oracle.stream(1, conj, N, x.astype(complex), x.astype(complex), lags=lags)
+        assert len(frames) == len(want) >= 8
+        assert_parity(frames_array(frames), want, mp, what=f"Full N={N} conj={conj} frames")
+        # block mode: the coherent average from one fold
+        blk = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, conj, emit_frames=False))
+        blk.push(x)
+        assert_parity(blk.average(), want.mean(axis=0), mp, what=f"Full N={N} conj={conj} block")
+
+
+def test_offgrid_direct_block_average_long_record(cyc, oracle):
+    """Alphas off any rational grid (direct kernel) averaged over 2^22 samples:
+    the long per-thread sums stay within the north-star tolerance of the fp64
+    literal sum (proj/src/reference.cpp:11-32 summed over the block)."""
+    L = 1 << 22
+    x = rand_c(L, 950)
+    alphas = [0.1234507, -0.3141592653]
+    est = cyc.CyclicCorrelator(set_cfg(cyc, 4096, 2, alphas, emit_frames=False))
+    assert est.algorithm() == "direct"
+    est.push(x)
+    F = est.frames_emitted()
+    got = est.average().reshape(len(alphas), 5)
+    want = oracle.block_direct(x.astype(complex), x.astype(complex), alphas, [-2, -1, 0, 1, 2], False, 2, F * 4096)
+    # the reference's frames carry e^{-j 2 pi alpha k0} with k0 = m_minus + f N (absolute anchor): the block
+    # sum over [m_minus, m_minus + F N) equals the mean of the frames
+    assert_parity(got, want, mean_power(x), what="off-grid direct block average")

@@ -34,35 +34,70 @@ def test_channel_shards():
     assert sh[0][0] == 0 and sh[-1][1] == 64 and sum(b - a for a, b in sh) == 64
 
 
+class FoldModel:
+    """CPU model of a block-mode estimator's fold state in the product's layout
+    ([channel][lag][residue][xr*yr, xi*yr, xr*yi, xi*yi], residues of ABSOLUTE
+    sample indices -- what cyc_fold_state exposes, include/cycb200.h), for a
+    time shard whose first sample is absolute index `origin`."""
+
+    def __init__(self, x_local, origin, N, lags, frames):
+        import torch
+        self.N, self.T = N, len(lags)
+        n = frames * N
+        y = x_local[:n].astype(np.complex128)
+        r = (origin + np.arange(n)) % N  # absolute residues: the shards sum without re-anchoring
+        S = np.zeros((self.T, N, 4))
+        for ti, lag in enumerate(lags):
+            xs = x_local[lag:lag + n].astype(np.complex128)
+            for comp, v in enumerate((xs.real * y.real, xs.imag * y.real, xs.real * y.imag, xs.imag * y.imag)):
+                S[ti, :, comp] = np.bincount(r, weights=v, minlength=N)
+        self.S = torch.from_numpy(S.reshape(-1).copy())
+        self.frames = frames
+
+    def fold_tensor(self):
+        return self.S
+
+    def fold_set_frames(self, frames):
+        self.frames = frames
+
+    def tables(self, bins):
+        """Coherent averages (conv, conj) [bins, lags] from the fold state."""
+        S = self.S.numpy().reshape(self.T, self.N, 4)
+        conv = (S[..., 0] + S[..., 3]) + 1j * (S[..., 1] - S[..., 2])  # x * conj(y)
+        conj = (S[..., 0] - S[..., 3]) + 1j * (S[..., 1] + S[..., 2])  # x * y
+        w = np.exp(-2j * np.pi * np.outer(bins, np.arange(self.N)) / self.N)
+        scale = 1.0 / (self.frames * self.N)
+        return (w @ conv.T) * scale, (w @ conj.T) * scale
+
+
 def _worker(rank, world, port, q):
     import sys
     sys.path.insert(0, ROOT)
     import torch
-    from oracle.oracle import Oracle
-    from paper_2405_16911_b200.shard import time_shards
+    from paper_2405_16911_b200.shard import exchange_time_shards, gather_channel_tables, time_shards
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    o = Oracle()
     x = rand_c(1 << 16, 5)
     N, lags = 512, list(range(16))
     sh = time_shards(len(x), N, 15, 0, world)[rank]
     # each rank sees ONLY its samples; absolute indices are carried by `origin`
-    xs = x[sh.sample0:sh.sample1]
-    cv, cj = o.block_fold(xs, xs, np.arange(N), N, lags, 0, sh.frames * N)
-    # re-anchor: block_fold anchors phases at the local index; the engine uses origin
-    k = np.arange(N)
-    ph = np.exp(-2j * np.pi * (k * sh.origin % N) / N)[:, None]
-    part = np.stack([cv * ph, cj * ph]) * (sh.frames * N)
-    t = torch.from_numpy(part.view(np.float64).copy())
-    dist.all_reduce(t)
-    fr = torch.tensor([sh.frames], dtype=torch.float64)
-    dist.all_reduce(fr)
+    m = FoldModel(x[sh.sample0:sh.sample1], sh.origin, N, lags, sh.frames)
+    F = sum(s.frames for s in time_shards(len(x), N, 15, 0, world))
+    exchange_time_shards(m, F, dist)  # the product's exchange step (bench.py)
+    bins = np.array([0, 1, 5, 100, 255, 256, 511])
+    cv, cj = m.tables(bins)
+    # channel shards: 6 channels, 3 per rank, tables gathered in channel order
+    chans = [rank * 3 + c for c in range(3)]
+    local = torch.from_numpy(np.stack([np.full((2, 4), float(c)) + 1j * c for c in chans]))
+    full = gather_channel_tables(local, world, dist)
     if rank == 0:
-        q.put((t.numpy().view(np.complex128) / (fr.item() * N), int(fr.item())))
+        q.put((cv, cj, m.frames, full.numpy()))
     dist.destroy_process_group()
 
 
-def test_gloo_time_shard_allreduce_equals_whole_record():
+def test_gloo_time_shard_exchange_equals_whole_record():
+    """world-2 gloo run of shard.exchange_time_shards (the bench's NCCL step)
+    over per-shard fold states: equals the whole record's oracle tables."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
@@ -70,16 +105,19 @@ def test_gloo_time_shard_allreduce_equals_whole_record():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got, F = q.get()
+    cv, cj, F, full = q.get()
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     from oracle.oracle import Oracle
     o = Oracle()
     x = rand_c(1 << 16, 5)
-    cv, cj = o.block_fold(x, x, np.arange(512), 512, list(range(16)), 0, F * 512)
-    assert np.max(np.abs(got[0] - cv)) <= 1e-12
-    assert np.max(np.abs(got[1] - cj)) <= 1e-12
+    bins = np.array([0, 1, 5, 100, 255, 256, 511])
+    wv, wj = o.block_fold(x, x, bins, 512, list(range(16)), 0, F * 512)
+    assert np.max(np.abs(cv - wv)) <= 1e-12
+    assert np.max(np.abs(cj - wj)) <= 1e-12
+    assert full.shape == (6, 2, 4)
+    assert np.array_equal(full.real[:, 0, 0], np.arange(6.0))
 
 
 @pytest.mark.gpu
