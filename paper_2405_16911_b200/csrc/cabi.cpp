@@ -140,14 +140,20 @@ void cyc_host_free(void* p) {
 namespace {
 // One-shot windows (kernels.cpp:116-135) reuse the engines of the last few
 // geometries per thread: the set-up costs far more than one window.  The
-// engines live for the process.
+// cache is a thread_local object: a worker thread's engines (device memory,
+// pinned staging) are freed when the thread exits.
 cyc::Status cached_window_engine(const cyc::Cfg& g, cyc::Engine** out) {
     struct Entry {
         cyc::Cfg cfg;
         cyc::Engine* e;
     };
-    static thread_local std::vector<Entry>* cache = nullptr;
-    if (!cache) cache = new std::vector<Entry>();
+    struct Cache : std::vector<Entry> {
+        ~Cache() {
+            for (auto& en : *this) delete en.e;
+        }
+    };
+    static thread_local Cache cache_obj;
+    Cache* cache = &cache_obj;
     auto same = [](const cyc::Cfg& a, const cyc::Cfg& b) {
         return a.mode == b.mode && a.flags == b.flags && a.win_len == b.win_len && a.alphas == b.alphas &&
                a.lag_symmetric == b.lag_symmetric && a.max_lag == b.max_lag && a.lags == b.lags &&

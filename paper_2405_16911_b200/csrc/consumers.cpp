@@ -93,9 +93,12 @@ int cyc_estimate_cfo_ccf(const cyc_cf32* x, size_t n, double expected_beta, int 
     struct Cache {
         int N = 0, device = -1;
         cyc_est* est = nullptr;
+        ~Cache() {  // a worker thread's estimator is freed when the thread exits
+            if (est) cyc_destroy(est);
+        }
     };
-    static thread_local Cache* cache = nullptr;
-    if (!cache) cache = new Cache;  // process lifetime
+    static thread_local Cache cache_obj;
+    Cache* cache = &cache_obj;
     if (!cache->est || cache->N != N || cache->device != device) {
         if (cache->est) cyc_destroy(cache->est);
         cache->est = nullptr;

@@ -1886,6 +1886,10 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     ++hprof_calls_;
     meta_mapped_now_ = false;
     prestaged_ = false;
+    // consumed here whatever happens next: only the very chunk validate_host_f32 scanned skips the scan
+    const bool pre = kind == IN_HOST_F32 && prevalidated_ptr_ != nullptr && prevalidated_ptr_ == xv &&
+                     prevalidated_n_ == n;
+    prevalidated_ptr_ = nullptr;
     CK(cudaSetDevice(c_.device));
     if (n == 0) return Status::ok();
     if (kind == IN_DEVICE_F32 && !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_)
@@ -1915,8 +1919,8 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         Bad bad;
         const bool one_piece = kind == IN_HOST_F32 && !pinned && n <= (size_t)Q_ && stage_len_ >= (size_t)Q_ &&
                                ((!yv && !cross_) || (yv && cross_ && stage_y_[0]));
-        if (kind == IN_HOST_F32 && prevalidated_) {
-            prevalidated_ = false;  // the caller (push_file) scanned this chunk already
+        if (pre) {
+            // the caller (push_file) scanned exactly this chunk already
         } else if (one_piece) {  // stage and screen in one pass; exact scan only if flagged
             if (stage_ev_live_[stage_k_]) CK(cudaEventSynchronize(stage_ev_[stage_k_]));
             stage_ev_live_[stage_k_] = false;
@@ -2815,6 +2819,7 @@ Status Engine::set_frames(uint64_t frames) {
 }
 
 Status Engine::reset() {
+    prevalidated_ptr_ = nullptr;
     CK(cudaSetDevice(c_.device));
     if (timeline_on()) {
         tl_resolve(false);
@@ -2872,9 +2877,11 @@ Status Engine::wait_finalize_reads() {
 // The whole-chunk finite scan on its own (push_file validates the mapped file
 // before pushing it, then marks the push prevalidated).
 Status Engine::validate_host_f32(const void* x, const void* y, size_t n) {
+    prevalidated_ptr_ = nullptr;
     const Bad bad = scan_bad((const cyc_cf32*)x, (const cyc_cf32*)y, n, c_.channels);
     if (bad.key != ~0ull) return data_error(bad.key, bad.channel, IN_HOST_F32, x, y, n);
-    prevalidated_ = true;
+    prevalidated_ptr_ = x;
+    prevalidated_n_ = n;
     return Status::ok();
 }
 

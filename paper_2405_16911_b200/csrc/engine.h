@@ -319,7 +319,10 @@ private:
     char* meta_dev_ = nullptr;
     char* meta_shadow_ = nullptr;  // device copy of the arena
     bool meta_mapped_now_ = false; // read descriptors mapped (inside pinned-host pushes)
-    bool prevalidated_ = false;    // next host-f32 push was scanned by validate_host_f32
+    // the host-f32 chunk validate_host_f32 scanned: a push of exactly this
+    // (pointer, length) skips its own scan; any other call clears it
+    const void* prevalidated_ptr_ = nullptr;
+    size_t prevalidated_n_ = 0;
     bool prestaged_ = false;       // the current one-piece push is already in stage_[stage_k_]
     size_t meta_slot_bytes_ = 0;
     size_t meta_used_ = 0;

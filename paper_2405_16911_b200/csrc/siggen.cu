@@ -355,16 +355,21 @@ int cyc_gmsk_mc_oracle(const cyc_cpm_params* p, const double* alphas, size_t n_a
     c.origin = (int64_t)(M - m_minus);
     // The estimator and the record buffer of the last geometry are kept per
     // thread: repeated calls (more trials, other seeds) skip the set-up, which
-    // dominates small tables.  Never freed (process lifetime).
+    // dominates small tables.  Freed when the thread exits.
     struct Cache {
         cyc::Cfg cfg;
         cyc::Engine* e = nullptr;
         float2* x = nullptr;
         size_t x_len = 0;
         cudaStream_t st = nullptr;
+        ~Cache() {
+            delete e;
+            cudaFree(x);
+            if (st) cudaStreamDestroy(st);
+        }
     };
-    static thread_local Cache* cache = nullptr;
-    if (!cache) cache = new Cache;
+    static thread_local Cache cache_obj;
+    Cache* cache = &cache_obj;
     auto same = [](const cyc::Cfg& a, const cyc::Cfg& b) {
         return a.mode == b.mode && a.flags == b.flags && a.win_len == b.win_len && a.alphas == b.alphas &&
                a.lag_symmetric == b.lag_symmetric && a.max_lag == b.max_lag && a.emit_frames == b.emit_frames &&

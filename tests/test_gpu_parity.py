@@ -640,3 +640,24 @@ def test_offgrid_direct_block_average_long_record(cyc, oracle):
     # the reference's frames carry e^{-j 2 pi alpha k0} with k0 = m_minus + f N (absolute anchor): the block
     # sum over [m_minus, m_minus + F N) equals the mean of the frames
     assert_parity(got, want, mean_power(x), what="off-grid direct block average")
+
+
+def test_estimators_on_two_devices(cyc, oracle):
+    """Handles on different devices of one process: each
+    device gets its kernels' shared-memory opt-in (kernels.cuh first_on_device)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    x = rand_c(1024 * 300 + 5, 960)
+    N, lags = 1024, list(range(64))
+    outs = []
+    for d in (0, 1):
+        est = cyc.CyclicCorrelator(full_cfg(cyc, N, lags, flags=cyc.Flags.BOTH, emit_frames=False, device=d))
+        dx = torch.from_numpy(x.view(np.float32)).to(f"cuda:{d}")
+        est.push_device(dx.data_ptr(), len(x))
+        outs.append(est.average_all())
+    F = (len(x) - N - 63) // N + 1
+    cv, cj = oracle.block_fold(x, x, np.arange(0, N, 37), N, lags, 0, F * N)
+    for o in outs:
+        assert_parity(o[0, 0].reshape(64, N)[:, ::37], cv.T, mean_power(x))
+        assert_parity(o[0, 1].reshape(64, N)[:, ::37], cj.T, mean_power(x))
