@@ -1189,7 +1189,7 @@ const FoldTile* Engine::planes_tiles(const std::vector<FoldTile>& t) {
 bool Engine::planes_ok(const std::vector<FoldSeg>& segs) const {
     static const bool off = std::getenv("CYC_NO_PLANES") != nullptr;  // A/B knob: fused converters only
     static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;
-    if (off || no_tc || !tc_capable_ || cross_ || segs.empty() || Pf_ % 128 != 0 || f_lo_ < 0 ||
+    if (off || no_tc || !tc_capable_ || cross_ || segs.empty() || Pf_ % 128 != 0 || f_lo_ < 0 || f_lo_ % 32 != 0 ||
         (t_pad_ + 63) / 64 < 2)
         return false;
     for (const FoldSeg& g0 : segs) {

@@ -115,6 +115,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
 }
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int c1, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+        "[%2];" ::"r"(dst), "l"((uint64_t)map), "r"(su32(bar)), "r"(0), "r"(c1), "r"(0), "r"(c3) : "memory");
+}
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
@@ -669,6 +674,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
 #ifndef TC_TPE
 #define TC_TPE 16
 #endif
+
 constexpr int TPE = TC_TPE;                        // epilogue warps of the planes kernel
 constexpr int TPT = 64 + 32 * TPE;
 constexpr int NPL = TC_NPL;                        // plane stages in flight
@@ -704,6 +710,7 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_s;
+    if (threadIdx.x == 0) TC_MARK(7, 0);
     const FoldTile& tile = s_tile;
     const int64_t r0 = (int64_t)tile.rb * TRB;
     const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 64;
@@ -717,30 +724,24 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
     const int nchunks = nst > 0 ? (nst - 1 + off) / DRAIN + 1 : 0;
     if (warp == 0) {
         if (lane == 0) {
-            const CUtensorMap* hm = &D.hmap[tile.seg];
-            const CUtensorMap* lm = &D.lmap[tile.seg];
+            // one 4-D TMA per window: {64 bf16, 16 periods, hi/lo, atoms} lands
+            // as [atom][hi, lo][16 rows][128 B] (one instruction instead of one
+            // per 2 KB atom column: a single issuing thread spends ~100 cycles
+            // per box, tools/exp/tma4d.cu: 844 -> 356 cycles per 24 KB stage)
+            const CUtensorMap* xm = &D.xmap[tile.seg];
+            const CUtensorMap* ym = &D.ymap[tile.seg];
             const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
-            const int xcol = 2 * (int)(r0 + d), ycol = 2 * (int)r0;
+            const int xatom = (int)(r0 + d) / 32, yatom = (int)r0 / 32;
             const uint32_t bytes = self ? 2 * XPLANE : PL_STAGE;
             for (int it = 0; it < nst; ++it) {
                 const int s = it % NPL;
                 if (it >= NPL) mbar_wait(&planefree[s], ((it / NPL) - 1) & 1);
+                TC_MARK(0, it);
                 const uint32_t st = su32(ring + s * PL_STAGE);
                 const int row = row0 + it * TKB;
                 mbar_expect_tx(&full[s], bytes);
-                // one box = one plane atom column: 64 bf16 = 32 samples x 16 periods
-#pragma unroll
-                for (int a = 0; a < XF / 64; ++a) {
-                    tma_2d(st + a * ATOM, hm, xcol + 64 * a, row, &full[s]);
-                    tma_2d(st + XPLANE + a * ATOM, lm, xcol + 64 * a, row, &full[s]);
-                }
-                if (!self) {
-#pragma unroll
-                    for (int a = 0; a < YF / 64; ++a) {
-                        tma_2d(st + 2 * XPLANE + a * ATOM, hm, ycol + 64 * a, row, &full[s]);
-                        tma_2d(st + 2 * XPLANE + YPLANE + a * ATOM, lm, ycol + 64 * a, row, &full[s]);
-                    }
-                }
+                tma_4d(st, xm, row, xatom, &full[s]);
+                if (!self) tma_4d(st + 2 * XPLANE, ym, row, yatom, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -749,18 +750,21 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                 const int s = it % NPL;
                 const int j = (it + off) % DRAIN;
                 mbar_wait(&full[s], (it / NPL) & 1);
+                TC_MARK(3, it);
                 if (j == 0 && it > 0) mbar_wait(&drain_free, ((it + off) / DRAIN - 1) & 1);
+                TC_MARK(1, it);
                 const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t xh = su32(ring + s * PL_STAGE), xl = xh + XPLANE;
-                const uint32_t yh0 = self ? xh + ya * ATOM : xl + XPLANE;
-                const uint32_t yl0 = self ? xl + ya * ATOM : yh0 + YPLANE;
+                // atom a of a window: hi at (2a) ATOM, lo at (2a + 1) ATOM -- the
+                // operands' MN-atom stride (LBO) is 2 ATOM
+                const uint32_t xb = su32(ring + s * PL_STAGE);
+                const uint32_t yb = self ? xb + 2 * ya * ATOM : xb + 2 * XPLANE;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const uint64_t dxh = sw128_desc(xh + 2 * h * ATOM, ATOM, 1024);
-                    const uint64_t dxl = sw128_desc(xl + 2 * h * ATOM, ATOM, 1024);
-                    const uint64_t dyh = sw128_desc(yh0 + 2 * h * ATOM, ATOM, 1024);
-                    const uint64_t dyl = sw128_desc(yl0 + 2 * h * ATOM, ATOM, 1024);
+                    const uint64_t dxh = sw128_desc(xb + 4 * h * ATOM, 2 * ATOM, 1024);
+                    const uint64_t dxl = sw128_desc(xb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
+                    const uint64_t dyh = sw128_desc(yb + 4 * h * ATOM, 2 * ATOM, 1024);
+                    const uint64_t dyl = sw128_desc(yb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
                     const uint32_t dt = tmem + 256 * h;
                     mma_bf16(dt, dyh, dxh, TC_IDESC, acc);
                     mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
@@ -768,6 +772,7 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                 }
                 mma_commit(&planefree[s]);
                 if (j == DRAIN - 1 || it == nst - 1) mma_commit(&chunk_done);
+                TC_MARK(2, it);
             }
             if (nst == 0) mbar_arrive(&chunk_done);
         }
@@ -922,11 +927,27 @@ bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64
            encode_2d(&D.ymap[si], yb, 2ull * Pf, (uint64_t)rows, 8ull * Pf);
 }
 
+// 4-D map over the planes: (64 bf16 of an atom, period rows, hi/lo plane,
+// atoms of 32 samples); box {64, 16, 2, natoms}.
+bool encode_planes_4d(CUtensorMap* m, const uint32_t* hi, uint64_t plane_bytes, int64_t rows, int Pf,
+                      int64_t cols_samples, int natoms) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc || ((uintptr_t)hi & 15) || rows <= 0 || (plane_bytes & 15)) return false;
+    const cuuint64_t gdim[4] = {64, (cuuint64_t)rows, 2, (cuuint64_t)((cols_samples + 31) / 32)};
+    const cuuint64_t gstr[3] = {4ull * (uint64_t)Pf, plane_bytes, 128};
+    const cuuint32_t box[4] = {64, (cuuint32_t)TKB, 2, (cuuint32_t)natoms}, es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint32_t*>(hi), gdim, gstr, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_tcp_maps(TcPlDesc& D, int si, const uint32_t* hi, const uint32_t* lo, int64_t p_base, int64_t rows,
                      int Pf, int64_t cols_samples) {
     D.p_base[si] = p_base;
-    return encode_2d(&D.hmap[si], hi, 2ull * (uint64_t)cols_samples, (uint64_t)rows, 4ull * Pf, true) &&
-           encode_2d(&D.lmap[si], lo, 2ull * (uint64_t)cols_samples, (uint64_t)rows, 4ull * Pf, true);
+    if (lo < hi) return false;
+    const uint64_t plane_bytes = (uint64_t)(lo - hi) * sizeof(uint32_t);
+    return encode_planes_4d(&D.xmap[si], hi, plane_bytes, rows, Pf, cols_samples, XF / 64) &&
+           encode_planes_4d(&D.ymap[si], hi, plane_bytes, rows, Pf, cols_samples, YF / 64);
 }
 
 namespace {

@@ -162,8 +162,10 @@ bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64
 // operand reads).  Tiles of every lag block run in one launch, ordered so that
 // the lag blocks of a residue block share the L2-resident planes.
 struct alignas(64) TcPlDesc {
-    CUtensorMap hmap[TC_SEGS];  // hi plane, bf16 box 64 x 16 periods, 128B swizzle (one atom column)
-    CUtensorMap lmap[TC_SEGS];  // lo plane
+    // 4-D maps (64 bf16, period rows, hi/lo, atoms of 32 samples), 128B swizzle:
+    // one TMA per window lands [atom][hi, lo][16 periods][128 B]
+    CUtensorMap xmap[TC_SEGS];  // box: the 6 atoms of an x window
+    CUtensorMap ymap[TC_SEGS];  // box: the 4 atoms of a y window
     int64_t p_base[TC_SEGS];    // first period (row 0) of each segment's maps
     FoldSeg segs[TC_SEGS];
     const FoldTile* tiles;      // device tile table [n_tiles]
