@@ -966,8 +966,13 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         if (tail.n_end > tail.n_start) rest.push_back(tail);
         const int si = (int)tsegs.size();
         tsegs.push_back(g);
-        for (int rb = 0; rb < nrb; ++rb)
-            for (int lb = 0; lb < nlb; ++lb) groups.push_back({si, rb, lb, pa, pb});
+        if (planes_on_) {  // planes tiles: 64 residues x a pair of lag blocks (rb = 64-residue block, lb = pair)
+            for (int rb = 0; rb < 2 * nrb; ++rb)
+                for (int lp = 0; lp < nlb / 2; ++lp) groups.push_back({si, rb, lp, pa, pb});
+        } else {
+            for (int rb = 0; rb < nrb; ++rb)
+                for (int lb = 0; lb < nlb; ++lb) groups.push_back({si, rb, lb, pa, pb});
+        }
         work += (pb - pa) * nrb * nlb;
     }
     if (groups.empty()) return Status::ok();
@@ -1189,8 +1194,9 @@ const FoldTile* Engine::planes_tiles(const std::vector<FoldTile>& t) {
 bool Engine::planes_ok(const std::vector<FoldSeg>& segs) const {
     static const bool off = std::getenv("CYC_NO_PLANES") != nullptr;  // A/B knob: fused converters only
     static const bool no_tc = std::getenv("CYC_NO_TC") != nullptr;
+    const int nlb = (t_pad_ + 63) / 64;  // tiles take lag blocks in pairs
     if (off || no_tc || !tc_capable_ || cross_ || segs.empty() || Pf_ % 128 != 0 || f_lo_ < 0 || f_lo_ % 32 != 0 ||
-        (t_pad_ + 63) / 64 < 2)
+        nlb < 2 || nlb % 2 != 0)
         return false;
     for (const FoldSeg& g0 : segs) {
         FoldSeg g = g0;
@@ -1268,11 +1274,12 @@ Status Engine::fold_tc_planes(const std::vector<FoldSeg>& tsegs, std::vector<TcG
     L.partials = partials_;
     L.S = S;
     L.gate = fold_gate_;
+    L.tc_pairs = 1;
     D.tiles = dt;
     double launch_flops = 0.0, exec = 0.0;
-    for (const auto& gr : groups) {
-        const int lags_in = std::max(0, std::min(64, T_ - 64 * gr.lb));
-        launch_flops += 8.0 * lags_in * 128.0 * (double)(gr.p1 - gr.p0);
+    for (const auto& gr : groups) {  // 64 residues x lag blocks 2 lb, 2 lb + 1
+        const int lags_in = std::max(0, std::min(128, T_ - 128 * gr.lb));
+        launch_flops += 8.0 * lags_in * 64.0 * (double)(gr.p1 - gr.p0);
     }
     for (const auto& t : tiles) exec += (double)ceil_div(t.p1 - t.p0, 16) * 6.0 * 2.0 * 128 * 256 * 16;
     if (prof_) {

@@ -668,25 +668,25 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
 // share one launch, so the lag blocks of a residue block run together and
 // reuse the planes from L2.
 // ---------------------------------------------------------------------------
-#ifndef TC_NPL
-#define TC_NPL 5
-#endif
 #ifndef TC_TPE
 #define TC_TPE 16
 #endif
 
 constexpr int TPE = TC_TPE;                        // epilogue warps of the planes kernel
 constexpr int TPT = 64 + 32 * TPE;
-constexpr int NPL = TC_NPL;                        // plane stages in flight
-constexpr int PL_STAGE = 2 * XPLANE + 2 * YPLANE;  // 40 KB
-constexpr int PL_SMEM = NPL * PL_STAGE + 1024;
+constexpr int PL_RING = 192 * 1024;               // stages: 24 KB (self) or 32 KB (x + 2 y atoms)
+constexpr int NPL_MAX = PL_RING / (2 * XPLANE);    // self tiles: 8 stages in flight (others 6)
+constexpr int PL_SMEM = PL_RING + 1024;
 static_assert(PL_SMEM <= 227 * 1024, "shared memory per CTA");
+// A stage's TMA lands ~3900 cycles after issue under load (tools/tcp_trace.py)
+// and its slot frees only when its MMAs complete, so the stages in flight set
+// the rate.
 
 template <class DESC>
 __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t full[NPL], planefree[NPL], chunk_done, drain_free;
+    __shared__ uint64_t full[NPL_MAX], planefree[NPL_MAX], chunk_done, drain_free;
     __shared__ uint32_t tmem_s;
     __shared__ FoldTile s_tile;
     __shared__ FoldSeg s_seg;
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
     if (threadIdx.x == 0) {
         s_tile = D.tiles[blockIdx.x];
         s_seg = D.segs[s_tile.seg];
-        for (int s = 0; s < NPL; ++s) {
+        for (int s = 0; s < NPL_MAX; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&planefree[s], 1);
         }
@@ -712,16 +712,21 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
     const uint32_t tmem = tmem_s;
     if (threadIdx.x == 0) TC_MARK(7, 0);
     const FoldTile& tile = s_tile;
-    const int64_t r0 = (int64_t)tile.rb * TRB;
-    const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 64;
+    // 64 residues [r0, r0 + 64) x lag blocks d .. d + 127: accumulator h takes
+    // the x atoms 2h .. 2h + 3 of the 192-sample window at r0 + d, both the
+    // same y (A) operand
+    const int64_t r0 = (int64_t)tile.rb * 64;
+    const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 128;
     // y inside the x window at an atom boundary: skip the y planes
-    const bool self = s_seg.x == s_seg.y && d <= 0 && -d <= 64 && (-d) % 32 == 0;
+    const bool self = s_seg.x == s_seg.y && d <= 0 && -d <= 128 && (-d) % 32 == 0;
     const int ya = self ? (int)(-d) / 32 : 0;
     const int nper = (int)(tile.p1 - tile.p0);
     const int nst = (nper + TKB - 1) / TKB;
     const int DRAIN = L.tc_drain > 0 ? L.tc_drain : (1 << 30);
     const int off = L.tc_drain > 0 ? (int)(blockIdx.x % 4) * (DRAIN / 4) : 0;  // staggered drains
     const int nchunks = nst > 0 ? (nst - 1 + off) / DRAIN + 1 : 0;
+    const uint32_t slot = self ? 2 * XPLANE : 2 * XPLANE + 2 * 2 * ATOM;  // stage bytes: x (+ 2 y atoms)
+    const int NPL = PL_RING / (int)slot;                  // stages in flight
     if (warp == 0) {
         if (lane == 0) {
             // one 4-D TMA per window: {64 bf16, 16 periods, hi/lo, atoms} lands
@@ -732,14 +737,13 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
             const CUtensorMap* ym = &D.ymap[tile.seg];
             const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
             const int xatom = (int)(r0 + d) / 32, yatom = (int)r0 / 32;
-            const uint32_t bytes = self ? 2 * XPLANE : PL_STAGE;
             for (int it = 0; it < nst; ++it) {
                 const int s = it % NPL;
                 if (it >= NPL) mbar_wait(&planefree[s], ((it / NPL) - 1) & 1);
                 TC_MARK(0, it);
-                const uint32_t st = su32(ring + s * PL_STAGE);
+                const uint32_t st = su32(ring + s * slot);
                 const int row = row0 + it * TKB;
-                mbar_expect_tx(&full[s], bytes);
+                mbar_expect_tx(&full[s], slot);
                 tma_4d(st, xm, row, xatom, &full[s]);
                 if (!self) tma_4d(st + 2 * XPLANE, ym, row, yatom, &full[s]);
             }
@@ -757,14 +761,14 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 // atom a of a window: hi at (2a) ATOM, lo at (2a + 1) ATOM -- the
                 // operands' MN-atom stride (LBO) is 2 ATOM
-                const uint32_t xb = su32(ring + s * PL_STAGE);
+                const uint32_t xb = su32(ring + s * slot);
                 const uint32_t yb = self ? xb + 2 * ya * ATOM : xb + 2 * XPLANE;
+                const uint64_t dyh = sw128_desc(yb, 2 * ATOM, 1024);
+                const uint64_t dyl = sw128_desc(yb + ATOM, 2 * ATOM, 1024);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint64_t dxh = sw128_desc(xb + 4 * h * ATOM, 2 * ATOM, 1024);
                     const uint64_t dxl = sw128_desc(xb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
-                    const uint64_t dyh = sw128_desc(yb + 4 * h * ATOM, 2 * ATOM, 1024);
-                    const uint64_t dyl = sw128_desc(yb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
                     const uint32_t dt = tmem + 256 * h;
                     mma_bf16(dt, dyh, dxh, TC_IDESC, acc);
                     mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
@@ -840,8 +844,9 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
     const int lane = threadIdx.x & 31, q = lane >> 3;
     const int e = (blockIdx.x * blockDim.x + threadIdx.x - lane) / 4 + (lane & 7);  // lag * TRB + residue
     const int lag = e / TRB, res = e % TRB;
-    const int64_t rg = (int64_t)g.rb * TRB + res;
-    const int tg = g.lb * 64 + lag;
+    // planes tiles: cell (t, 64 h + r) is residue 64 rb + r at lag block 2 lb + h
+    const int64_t rg = L.tc_pairs ? (int64_t)g.rb * 64 + (res & 63) : (int64_t)g.rb * TRB + res;
+    const int tg = L.tc_pairs ? (2 * g.lb + (res >> 6)) * 64 + lag : g.lb * 64 + lag;
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     // the group's tiles are t0, t0 + stride, ... < t1 (stride 1: contiguous;
@@ -947,7 +952,7 @@ bool encode_tcp_maps(TcPlDesc& D, int si, const uint32_t* hi, const uint32_t* lo
     if (lo < hi) return false;
     const uint64_t plane_bytes = (uint64_t)(lo - hi) * sizeof(uint32_t);
     return encode_planes_4d(&D.xmap[si], hi, plane_bytes, rows, Pf, cols_samples, XF / 64) &&
-           encode_planes_4d(&D.ymap[si], hi, plane_bytes, rows, Pf, cols_samples, YF / 64);
+           encode_planes_4d(&D.ymap[si], hi, plane_bytes, rows, Pf, cols_samples, 2);
 }
 
 namespace {

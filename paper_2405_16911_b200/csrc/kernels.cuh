@@ -88,6 +88,10 @@ struct FoldLaunch {
     // tensor-core folds: stages (16 periods) per TMEM accumulation chunk; the
     // epilogue drains the accumulator into the fp32 partials after each chunk
     int tc_drain;
+    // planes tiles (1): a tile is 64 residues (rb counts 64-residue blocks) x
+    // the lag blocks 2 lb and 2 lb + 1 -- partial cell (t, 64 h + r) is
+    // residue 64 rb + r at lag block 2 lb + h; else (0): 128 residues x lag block lb
+    int tc_pairs;
 };
 
 // Launch descriptors carried in the kernel parameter block (<= 32 KB since
@@ -154,7 +158,7 @@ void launch_fold_tc(const FoldLaunch& L, const TcParams& D, int n_segs, bool sel
 bool encode_tc_maps(TcParams& D, int si, const FoldSeg& g, int64_t p_base, int64_t rows, int Pf, int lag_lo,
                     int nlb);
 
-// Planes path (multi-lag-block self folds of device chunks, e.g. C5): the
+// Planes path (self folds of device chunks over an even number of lag blocks, e.g. C5): the
 // bf16x3 split is done once per sample by launch_split_planes -- hi and lo
 // planes, one bf16x2 (re, im) word per sample, [channel][pitch] -- and the
 // fold kernel stages the planes with TMA straight into the UMMA operand layout
@@ -165,7 +169,7 @@ struct alignas(64) TcPlDesc {
     // 4-D maps (64 bf16, period rows, hi/lo, atoms of 32 samples), 128B swizzle:
     // one TMA per window lands [atom][hi, lo][16 periods][128 B]
     CUtensorMap xmap[TC_SEGS];  // box: the 6 atoms of an x window
-    CUtensorMap ymap[TC_SEGS];  // box: the 4 atoms of a y window
+    CUtensorMap ymap[TC_SEGS];  // box: the 2 atoms of a y window (64 residues)
     int64_t p_base[TC_SEGS];    // first period (row 0) of each segment's maps
     FoldSeg segs[TC_SEGS];
     const FoldTile* tiles;      // device tile table [n_tiles]

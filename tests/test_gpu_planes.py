@@ -21,7 +21,7 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.float32)).cuda()
 
 
-@pytest.mark.parametrize("lags", [list(range(128)), list(range(5, 205)), list(range(256)), list(range(0, 300, 3))])
+@pytest.mark.parametrize("lags", [list(range(128)), list(range(5, 205)), list(range(256)), list(range(0, 384, 3)), list(range(32, 160))])
 def test_planes_fold_vs_oracle(cyc, oracle, lags):
     N = 1024
     x = rand_c(N * 700 + 333, 901)
