@@ -9,7 +9,7 @@
 //
 // Two paths, both fp64:
 //   * radix-2 DIT FFT in shared memory (Pf a power of two <= 8192; levels
-//     fused in pairs, twiddles in shared memory): replaces
+//     grouped four per pass in registers, twiddles in shared memory): replaces
 //     the reference's per-lag Fft::forward (proj/src/fft.cpp:44-87);
 //   * direct DFT with an exact (bin*r mod Pf) twiddle index, for small alpha
 //     sets or non-power-of-two periods (proj/src/fft.cpp:89-100 analogue).
@@ -28,15 +28,52 @@ __device__ __forceinline__ double2 combine(const double* s, int flag_bit) {  // 
                          : make_double2(s[0] - s[3], s[1] + s[2]);  // x * y
 }
 
-// grid: (n_rows, n_flag_tables); one CTA per (row, flag).  Radix-2 stages are
-// executed in pairs: each thread keeps the four points of two consecutive
-// butterfly levels in registers (exactly the radix-2 arithmetic, one barrier
-// per pair), with the Pf/2-entry twiddle table staged in shared memory.
+// Shared-memory index with one pad slot per 16 points: a thread's 16
+// consecutive points (first pass) then sit 272 B apart across a warp, off the
+// same banks.
+__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+
+// One pass of LOG2R radix-2 DIT levels (halves h, 2h, .., 2^(LOG2R-1) h): each
+// thread takes groups of R = 2^LOG2R points base + pos + k h (k < R) into
+// registers and runs the levels there -- exactly the radix-2 butterflies
+// (v = b w, a + v, a - v) with the level's twiddles, one barrier per pass.
+template <int LOG2R>
+__device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int Pf, int h) {
+    constexpr int R = 1 << LOG2R;
+    for (int g = threadIdx.x; g < Pf / R; g += blockDim.x) {
+        const int base = (g / h) * (R * h), pos = g - (g / h) * h;
+        double2 v[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) v[k] = buf[padi(base + pos + k * h)];
+#pragma unroll
+        for (int l = 0; l < LOG2R; ++l) {
+            const int hs = h << l;       // half size of this level
+            const int ts = Pf / (2 * hs);  // twiddle stride
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                if (k & (1 << l)) continue;
+                const int j = pos + (k & ((1 << l) - 1)) * h;  // position in the half block
+                const double2 w = tw[j * ts];
+                const double2 b = v[k + (1 << l)];
+                const double2 t = cmul(b, w);
+                v[k + (1 << l)] = make_double2(v[k].x - t.x, v[k].y - t.y);
+                v[k] = make_double2(v[k].x + t.x, v[k].y + t.y);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[padi(base + pos + k * h)] = v[k];
+    }
+    __syncthreads();
+}
+
+// grid: (n_rows, n_flag_tables); one CTA per (row, flag): the row's combined
+// correlations in bit-reversed order, then radix-16 passes (four radix-2
+// levels each, in registers) and a final pass of the remaining levels.
 __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
-    extern __shared__ double2 buf[];  // Pf points, then Pf/2 twiddles
+    extern __shared__ double2 buf[];  // Pf + Pf/16 points (padded), then Pf/2 twiddles
     __shared__ FinalRow s_row;        // descriptors may be in mapped host memory: read once
     const int Pf = L.Pf;
-    double2* tw = buf + Pf;
+    double2* tw = buf + Pf + (Pf >> 4);
     if (threadIdx.x == 0) s_row = L.rows[blockIdx.x];
     for (int k = threadIdx.x; k < (Pf >> 1); k += blockDim.x) tw[k] = __ldg(L.tw + k);
     __syncthreads();
@@ -44,54 +81,42 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
     const int fi = blockIdx.y;  // index among requested flags
     const int flag_bit = (L.flags == 2) ? 1 : fi;
     const double* Srow = L.S + ((size_t)row.slot * L.t_pad + row.t_span) * (size_t)Pf * 4;
-    for (int r = threadIdx.x; r < Pf; r += blockDim.x) {
-        const int rev = (int)(__brev((unsigned)r) >> (32 - log2Pf));
-        const double2 v0 = __ldg(reinterpret_cast<const double2*>(Srow) + 2 * r);
-        const double2 v1 = __ldg(reinterpret_cast<const double2*>(Srow) + 2 * r + 1);
-        const double c[4] = {v0.x, v0.y, v1.x, v1.y};
-        buf[rev] = combine(c, flag_bit);
+    // the row streams from HBM: 8 independent 16-byte loads in flight per thread
+    const double2* S2 = reinterpret_cast<const double2*>(Srow);
+    const int nb = blockDim.x;
+    for (int r0 = threadIdx.x; r0 < Pf; r0 += 4 * nb) {
+        double2 v[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u * nb;
+            if (r < Pf) {
+                v[u][0] = __ldcs(S2 + 2 * r);
+                v[u][1] = __ldcs(S2 + 2 * r + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u * nb;
+            if (r >= Pf) continue;
+            const int rev = (int)(__brev((unsigned)r) >> (32 - log2Pf));
+            const double c[4] = {v[u][0].x, v[u][0].y, v[u][1].x, v[u][1].y};
+            buf[padi(rev)] = combine(c, flag_bit);
+        }
     }
     __syncthreads();
-    int len = 2;
-    for (; 2 * len <= Pf; len <<= 2) {  // levels len (half h) and 2 len, fused
-        const int h = len >> 1;
-        const int ts1 = Pf / len, ts2 = ts1 >> 1;
-        for (int j = threadIdx.x; j < (Pf >> 2); j += blockDim.x) {
-            const int grp = j / h, pos = j - grp * h;
-            const int i0 = grp * 2 * len + pos;
-            double2 a = buf[i0], b = buf[i0 + h], c = buf[i0 + 2 * h], d = buf[i0 + 3 * h];
-            const double2 w1 = tw[pos * ts1];
-            double2 v = cmul(b, w1);
-            b = make_double2(a.x - v.x, a.y - v.y);
-            a = make_double2(a.x + v.x, a.y + v.y);
-            v = cmul(d, w1);
-            d = make_double2(c.x - v.x, c.y - v.y);
-            c = make_double2(c.x + v.x, c.y + v.y);
-            v = cmul(c, tw[pos * ts2]);
-            buf[i0] = make_double2(a.x + v.x, a.y + v.y);
-            buf[i0 + 2 * h] = make_double2(a.x - v.x, a.y - v.y);
-            v = cmul(d, tw[(pos + h) * ts2]);
-            buf[i0 + h] = make_double2(b.x + v.x, b.y + v.y);
-            buf[i0 + 3 * h] = make_double2(b.x - v.x, b.y - v.y);
-        }
-        __syncthreads();
-    }
-    if (len <= Pf) {  // odd log2 Pf: the last radix-2 level
-        const int half = len >> 1;
-        for (int j = threadIdx.x; j < (Pf >> 1); j += blockDim.x) {
-            const int i0 = j, i1 = j + half;  // a single group of size Pf
-            const double2 u = buf[i0];
-            const double2 v = cmul(buf[i1], tw[j]);
-            buf[i0] = make_double2(u.x + v.x, u.y + v.y);
-            buf[i1] = make_double2(u.x - v.x, u.y - v.y);
-        }
-        __syncthreads();
+    int h = 1, lv = 0;
+    for (; lv + 4 <= log2Pf; lv += 4, h <<= 4) fft_pass<4>(buf, tw, Pf, h);
+    switch (log2Pf - lv) {
+        case 3: fft_pass<3>(buf, tw, Pf, h); break;
+        case 2: fft_pass<2>(buf, tw, Pf, h); break;
+        case 1: fft_pass<1>(buf, tw, Pf, h); break;
+        default: break;
     }
     const double sc = L.row_scale ? L.row_scale[row.out_block] : L.scale_default;
     double2* out = L.out + (size_t)row.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride +
                    (size_t)row.t_out * L.stride_t;
     for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
-        const double2 v = buf[L.bins[a]];
+        const double2 v = buf[padi(L.bins[a])];
         out[(size_t)a * L.stride_a] = make_double2(v.x * sc, v.y * sc);
     }
 }
@@ -164,12 +189,12 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
     if (L.use_fft) {
         int lg = 0;
         while ((1 << lg) < L.Pf) ++lg;
-        const size_t smem = (size_t)L.Pf * 3 / 2 * sizeof(double2);
+        const size_t smem = ((size_t)L.Pf + L.Pf / 16 + L.Pf / 2) * sizeof(double2);
         static std::atomic<uint64_t> attr_set{0};
         if (first_on_device(attr_set))
             cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 12288 * (int)sizeof(double2));
-        finalize_fft_kernel<<<dim3(L.n_rows, nflag), std::min(512, std::max(32, L.Pf / 4)), smem, st>>>(L, lg);
+                                 (8192 + 512 + 4096) * (int)sizeof(double2));
+        finalize_fft_kernel<<<dim3(L.n_rows, nflag), std::min(512, std::max(32, L.Pf / 16)), smem, st>>>(L, lg);
     } else {
         finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
     }
@@ -181,6 +206,7 @@ namespace cyc {
 void prepare_finalize_kernels() {
     static std::atomic<uint64_t> done{0};
     if (!first_on_device(done)) return;
-    cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12288 * (int)sizeof(double2));
+    cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (8192 + 512 + 4096) * (int)sizeof(double2));
 }
 }  // namespace cyc
