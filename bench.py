@@ -422,8 +422,12 @@ def run_block(args, ws, rank, local):
             import torch.distributed as dist
             dist.broadcast(d_all, src=0)
         sh = time_shards(L, N, T - 1, 0, ws)[rank]
-        n_local = sh.sample1 - sh.sample0
-        d_loc = d_all[:, 2 * sh.sample0:2 * sh.sample1]  # a view: the estimator folds it in place
+        # one sample past the shard's last lag when the record has it: the
+        # tensor-core windows (192 samples for 128 residues x 64 lags) then
+        # cover the last fold period too (no FP32 tail launch); no extra frame
+        s1 = min(L, sh.sample1 + 1)
+        n_local = s1 - sh.sample0
+        d_loc = d_all[:, 2 * sh.sample0:2 * s1]  # a view: the estimator folds it in place
         ch0, ch1, origin = 0, 1, sh.origin
     else:
         ch0, ch1 = channel_shards(C_, ws)[rank]

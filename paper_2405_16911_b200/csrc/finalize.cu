@@ -105,7 +105,11 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
     }
     __syncthreads();
     int h = 1, lv = 0;
-    for (; lv + 4 <= log2Pf; lv += 4, h <<= 4) fft_pass<4>(buf, tw, Pf, h);
+    if (blockDim.x * 16 <= Pf) {  // enough groups of 16 for the block: radix-16 passes
+        for (; lv + 4 <= log2Pf; lv += 4, h <<= 4) fft_pass<4>(buf, tw, Pf, h);
+    } else {  // short rows: radix-4 passes keep every thread busy
+        for (; lv + 2 <= log2Pf; lv += 2, h <<= 2) fft_pass<2>(buf, tw, Pf, h);
+    }
     switch (log2Pf - lv) {
         case 3: fft_pass<3>(buf, tw, Pf, h); break;
         case 2: fft_pass<2>(buf, tw, Pf, h); break;
@@ -194,7 +198,9 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
         if (first_on_device(attr_set))
             cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (8192 + 512 + 4096) * (int)sizeof(double2));
-        finalize_fft_kernel<<<dim3(L.n_rows, nflag), std::min(512, std::max(32, L.Pf / 16)), smem, st>>>(L, lg);
+        // Pf = 8192: 512 threads x radix-16 groups; shorter rows: Pf / 4 threads x radix-4
+        const int nt = L.Pf >= 8192 ? 512 : std::min(512, std::max(32, L.Pf / 4));
+        finalize_fft_kernel<<<dim3(L.n_rows, nflag), nt, smem, st>>>(L, lg);
     } else {
         finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
     }

@@ -30,6 +30,7 @@
 // The tile's partials go through a fixed-order fp64 reduce (fold_tc_reduce_kernel).
 #include <cuda_bf16.h>
 
+#include <climits>
 #include <cstring>
 #include <type_traits>
 
@@ -500,13 +501,14 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            for (int it = 0; it < nst; ++it) {
+            int j = off, k = 0;  // stage within the accumulation chunk, drains so far
+            for (int it = 0; it < nst; ++it, ++j) {
                 const int s = it % G::NP;
-                const int j = (it + off) % DRAIN;  // stage within the accumulation chunk
+                if (j == DRAIN) j = 0;
                 mbar_wait(&conv[s], (it / G::NP) & 1);
                 // the chunk's first MMAs overwrite the accumulator: the
                 // converters must have drained the previous chunk (drain k -> phase k)
-                if (j == 0 && it > 0) mbar_wait(&drain_free, ((it + off) / DRAIN - 1) & 1);
+                if (j == 0 && it > 0) mbar_wait(&drain_free, (uint32_t)(k++) & 1u);
                 const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
                 TC_MARK(1, it);
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -572,6 +574,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             __syncwarp();
             if (lane == 0) mbar_arrive(&drain_free);
         };
+        int next_end = L.tc_drain > 0 ? DRAIN - 1 - off : INT_MAX;  // next chunk-end stage
         for (int it = 0; it < nst; ++it) {
             mbar_wait(&full[rs], rph);
             if (warp == 2 && lane == 0) TC_MARK(3, it);
@@ -581,7 +584,10 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
             if (it >= G::NP) {
                 mbar_wait(&planefree[ps], pph ^ 1u);
                 const int b = it - G::NP;
-                if ((b + off) % DRAIN == DRAIN - 1 && b + 1 < nst) drain_after(b);
+                if (b == next_end) {
+                    if (b + 1 < nst) drain_after(b);
+                    next_end += DRAIN;
+                }
             }
             if (warp == 2 && lane == 0) TC_MARK(4, it);
             const uint32_t st = rbase + (uint32_t)(rs * G::RAW);
@@ -640,9 +646,12 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         // chunk ends among the last NP stages (no converter iteration follows them)
         for (int it = nst; it < nst + G::NP; ++it) {
             const int b = it - G::NP;
-            if (b >= 0 && (b + off) % DRAIN == DRAIN - 1 && b + 1 < nst) {
-                mbar_wait(&planefree[ps], pph ^ 1u);
-                drain_after(b);
+            if (b >= 0 && b == next_end) {
+                next_end += DRAIN;
+                if (b + 1 < nst) {
+                    mbar_wait(&planefree[ps], pph ^ 1u);
+                    drain_after(b);
+                }
             }
             if (++ps == G::NP) {
                 ps = 0;
@@ -750,12 +759,13 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            for (int it = 0; it < nst; ++it) {
+            int j = off, k = 0;  // stage within the accumulation chunk, drains so far
+            for (int it = 0; it < nst; ++it, ++j) {
                 const int s = it % NPL;
-                const int j = (it + off) % DRAIN;
+                if (j == DRAIN) j = 0;
                 mbar_wait(&full[s], (it / NPL) & 1);
                 TC_MARK(3, it);
-                if (j == 0 && it > 0) mbar_wait(&drain_free, ((it + off) / DRAIN - 1) & 1);
+                if (j == 0 && it > 0) mbar_wait(&drain_free, (uint32_t)(k++) & 1u);
                 TC_MARK(1, it);
                 const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
                 asm volatile("tcgen05.fence::after_thread_sync;");
