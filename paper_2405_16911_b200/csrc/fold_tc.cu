@@ -261,16 +261,18 @@ __device__ unsigned long long g_tc_warp[16][64][2];  // per converter warp: (ful
 // are reproducible bit for bit.
 template <int NE>
 __device__ __forceinline__ void tc_drain_band(uint32_t tmem, const FoldLaunch& L, bool first, bool zero, int e,
-                                              int warp, int lane) {
+                                              int warp, int lane, int tmax) {
     const int q = warp & 3;
     const int m = 32 * q + lane;
     const int r = m >> 1, a = m & 1;
     float4* part = reinterpret_cast<float4*>(L.partials) + (size_t)blockIdx.x * 64 * TRB;
     asm volatile("tcgen05.fence::after_thread_sync;");
     // a quarter's work: 2 accumulators x 5 column chunks [32cc, 32cc + 32),
-    // cc = q .. q+4 (they cover the band), shared by the quarter's NE/4 warps
+    // cc = q .. q+4 (they cover the band), shared by the quarter's NE/4 warps;
+    // lags t >= tmax (past the requested span, e.g. C4's 32 of 64) are skipped
     for (int item = e >> 2; item < 10; item += NE / 4) {
         const int h = item / 5, cc = q + item % 5;
+        if (16 * (cc - q) - 15 >= tmax) continue;  // every lag of this column chunk is past the span
         uint32_t v[32];
         const uint32_t addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h + 32 * cc);
         asm volatile(
@@ -292,7 +294,7 @@ __device__ __forceinline__ void tc_drain_band(uint32_t tmem, const FoldLaunch& L
             const int t = 16 * cc + j - r;  // lag offset of column pair 2(16cc + j)
             const float o0 = __uint_as_float(v[2 * j]), o1 = __uint_as_float(v[2 * j + 1]);
             const float p0 = __shfl_xor_sync(0xffffffffu, o0, 1), p1 = __shfl_xor_sync(0xffffffffu, o1, 1);
-            if (a != 0 || t < 0 || t >= 64) continue;
+            if (a != 0 || t < 0 || t >= tmax) continue;
             float4* dst = part + ((size_t)t * TRB + 64 * h + r);
             if (first) {
                 *dst = make_float4(o0, o1, p0, p1);
@@ -569,8 +571,9 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         // at iteration b + NP; the MMA warp waits on drain_free before the next
         // chunk's first (overwriting) MMAs, while the converters have already
         // filled the plane ring ahead.
+        const int tmax = min(64, L.t_pad - 64 * tile.lb);  // lags of this lag block inside the span
         auto drain_after = [&](int b) {
-            tc_drain_band<TNC>(tmem, L, b + off < DRAIN, false, e, warp, lane);
+            tc_drain_band<TNC>(tmem, L, b + off < DRAIN, false, e, warp, lane, tmax);
             __syncwarp();
             if (lane == 0) mbar_arrive(&drain_free);
         };
@@ -661,7 +664,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
         // final chunk
         mbar_wait(&chunk_done, 0);
         if (warp == 2 && lane == 0) TC_MARK(6, 0);
-        tc_drain_band<TNC>(tmem, L, nchunks <= 1, nst == 0, e, warp, lane);
+        tc_drain_band<TNC>(tmem, L, nchunks <= 1, nst == 0, e, warp, lane, tmax);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
