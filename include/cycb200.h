@@ -236,6 +236,20 @@ int64_t cyc_data_error_index(const cyc_est* est);
 int cyc_fold_state(cyc_est* est, void** dev_ptr, size_t* count, uint64_t* frames);
 int cyc_fold_set_frames(cyc_est* est, uint64_t frames);
 
+/* CSV export of results (proj/src/io.cpp:161-208, the reference's
+ * export_frames_csv(path, frames, cfg) / export_average_csv(path, avg, cfg,
+ * mode)): same headers, rows in layout order, doubles as "%.17g", (alpha, lag)
+ * of each element from the config's layout (Full bins through
+ * full_bin_to_alpha).  frames: n_frames tables of layout_len values each, with
+ * their frame indices.  avg_mode selects the coherent (re, im, mag) or
+ * magnitude (mag) average format.  *rows = data rows written.  Host-only.
+ * CYC_ERR_CONFIG for an invalid config, CYC_ERR_USAGE for empty or mis-sized
+ * input, CYC_ERR_IO when the file cannot be written. */
+int cyc_export_frames_csv(const cyc_config* cfg, const char* path, const uint64_t* frame_index,
+                          const cyc_cf64* values, size_t n_frames, size_t* rows, char* err, size_t errlen);
+int cyc_export_average_csv(const cyc_config* cfg, const char* path, const cyc_cf64* avg, size_t len, int avg_mode,
+                           size_t* rows, char* err, size_t errlen);
+
 /* Block until all device work of this handle is complete. */
 int cyc_synchronize(cyc_est* est);
 /* Fresh stream state with the same config and allocations: equivalent to

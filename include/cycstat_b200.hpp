@@ -12,6 +12,7 @@
 //   CyclicCorrelator(cfg), push(x, y) -> vector<CyclicFrame>,
 //   buffer_need / consumed / frames_emitted                 estimator.hpp:97-137
 //   AverageMode / average_frames                            estimator.hpp:143-148
+//   export_frames_csv / export_average_csv                  io.hpp:68-75 (io.cpp:161-208)
 //   compute_set_window / compute_full_window                estimator.hpp:59-68
 // A caller switches by including this header instead of the reference's and
 // linking -lcycb200; `namespace cycstat = cycstat_b200;` is provided when
@@ -323,6 +324,40 @@ inline std::vector<cx> average_frames(const std::vector<CyclicFrame>& frames, Av
     }
     for (auto& v : out) v /= static_cast<double>(frames.size());
     return out;
+}
+
+// io.cpp:161-208: the CSV result writers (same headers and "%.17g" rows)
+inline std::size_t export_frames_csv(const std::string& path, const std::vector<CyclicFrame>& frames,
+                                     const EstimatorConfig& cfg) {
+    if (frames.empty()) throw UsageError("no frames to export");
+    const std::size_t len = frames.front().values.size();
+    std::vector<cx> vals;
+    std::vector<std::uint64_t> idx;
+    vals.reserve(frames.size() * len);
+    for (const auto& f : frames) {
+        if (f.layout.index() != frames.front().layout.index() || f.values.size() != len)
+            throw UsageError("cannot export frames with mixed layouts");
+        vals.insert(vals.end(), f.values.begin(), f.values.end());
+        idx.push_back(f.frame_index);
+    }
+    const cyc_config c = detail::to_c(cfg);
+    std::size_t rows = 0;
+    std::string err(1024, '\0');
+    const int rc = cyc_export_frames_csv(&c, path.c_str(), idx.data(), reinterpret_cast<const cyc_cf64*>(vals.data()),
+                                         frames.size(), &rows, err.data(), err.size());
+    if (rc) detail::raise(rc, err.c_str());
+    if (rows != vals.size()) throw UsageError("config does not match the frame layout");
+    return rows;
+}
+inline std::size_t export_average_csv(const std::string& path, const std::vector<cx>& avg, const EstimatorConfig& cfg,
+                                      AverageMode mode) {
+    const cyc_config c = detail::to_c(cfg);
+    std::size_t rows = 0;
+    std::string err(1024, '\0');
+    const int rc = cyc_export_average_csv(&c, path.c_str(), reinterpret_cast<const cyc_cf64*>(avg.data()), avg.size(),
+                                          (int)mode, &rows, err.data(), err.size());
+    if (rc) detail::raise(rc, err.c_str());
+    return rows;
 }
 
 // kernels.cpp:116-135 on the device

@@ -170,6 +170,12 @@ class RefLib:
         L.ref_gmsk_mc_oracle.argtypes = _cpm + [_dp, C.c_size_t, C.POINTER(C.c_int), C.c_size_t, C.c_int, C.c_int,
                                                 C.c_int, C.c_size_t, C.c_uint64, _dp]
         L.ref_estimate_cfo_ccf.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, _dp]
+        self.has_io = hasattr(L, "ref_export_frames_csv")  # io.cpp built (needs a json.hpp)
+        if self.has_io:
+            L.ref_export_frames_csv.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, C.c_size_t, C.c_int, _ip,
+                                                C.c_size_t, _dp, _u64p, C.c_size_t, _szp]
+            L.ref_export_average_csv.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, C.c_size_t, C.c_int, _ip,
+                                                 C.c_size_t, _dp, C.c_size_t, C.c_int, _szp]
         self.lib = L
 
     def cpm(self, n, h=0.5, bt=0.25, sps=8, seed=0):
@@ -224,6 +230,29 @@ class RefLib:
         if rc:
             raise ValueError(self.lib.ref_last_error().decode())
         return eps.value
+
+    def export_frames_csv(self, path, mode, win_len, frames, indices, alphas=(), max_lag=0, lags=()):
+        """io.cpp:161-186 (the reference's writer) on the given frame values."""
+        al = np.ascontiguousarray(alphas, dtype=np.float64)
+        lg = np.ascontiguousarray(lags, dtype=np.int32)
+        v = _cd(np.asarray(frames).reshape(-1))
+        ix = np.ascontiguousarray(indices, dtype=np.uint64)
+        rows = C.c_size_t()
+        self._err(self.lib.ref_export_frames_csv(os.fsencode(path), int(mode), int(win_len), _p(al, _dp), len(al),
+                                                 int(max_lag), _p(lg, _ip), len(lg), _p(v, _dp), _p(ix, _u64p),
+                                                 len(ix), C.byref(rows)))
+        return rows.value
+
+    def export_average_csv(self, path, mode, win_len, avg, magnitude, alphas=(), max_lag=0, lags=()):
+        """io.cpp:188-208 (the reference's writer)."""
+        al = np.ascontiguousarray(alphas, dtype=np.float64)
+        lg = np.ascontiguousarray(lags, dtype=np.int32)
+        v = _cd(np.asarray(avg).reshape(-1))
+        rows = C.c_size_t()
+        self._err(self.lib.ref_export_average_csv(os.fsencode(path), int(mode), int(win_len), _p(al, _dp), len(al),
+                                                  int(max_lag), _p(lg, _ip), len(lg), _p(v, _dp), len(v) // 2,
+                                                  int(magnitude), C.byref(rows)))
+        return rows.value
 
     def _err(self, rc):
         if rc:

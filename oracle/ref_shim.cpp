@@ -18,6 +18,9 @@
 #include "cycstat/impair.hpp"
 #include "cycstat/reference.hpp"
 #include "cycstat/siggen.hpp"
+#ifdef REF_HAVE_IO
+#include "cycstat/io.hpp"
+#endif
 
 using namespace cycstat;
 
@@ -296,5 +299,52 @@ int ref_add_noise_snr(double* x, std::size_t len, double snr_db, std::uint64_t s
         return 0;
     } catch (const std::exception& e) { return fail(e, 1); }
 }
+
+#ifdef REF_HAVE_IO
+// export_frames_csv / export_average_csv (io.cpp:161-208) on given values:
+// frames = n_frames x layout_len complex (interleaved doubles) with indices
+int ref_export_frames_csv(const char* path, int mode, int win_len, const double* alphas, std::size_t n_alphas,
+                          int max_lag, const int* lags, std::size_t n_lags, const double* values,
+                          const std::uint64_t* frame_index, std::size_t n_frames, std::size_t* rows) {
+    try {
+        const auto cfg = make_cfg(mode, 0, win_len, alphas, n_alphas, max_lag, lags, n_lags);
+        const std::size_t len = mode == 0 ? n_alphas * (2u * (std::size_t)max_lag + 1u) : n_lags * (std::size_t)win_len;
+        std::vector<CyclicFrame> frames(n_frames);
+        for (std::size_t f = 0; f < n_frames; ++f) {
+            frames[f].frame_index = frame_index[f];
+            if (mode == 0)
+                frames[f].layout = SetLayout{(int)n_alphas, max_lag};
+            else
+                frames[f].layout = FullLayout{(int)n_lags, win_len};
+            frames[f].values = load(values + 2 * f * len, len);
+        }
+        *rows = export_frames_csv(path, frames, cfg);
+        return 0;
+    } catch (const UsageError& e) {
+        return fail(e, 1);
+    } catch (const IoError& e) {
+        return fail(e, 6);
+    } catch (const std::exception& e) {
+        return fail(e, 5);
+    }
+}
+
+int ref_export_average_csv(const char* path, int mode, int win_len, const double* alphas, std::size_t n_alphas,
+                           int max_lag, const int* lags, std::size_t n_lags, const double* avg, std::size_t len,
+                           int magnitude, std::size_t* rows) {
+    try {
+        const auto cfg = make_cfg(mode, 0, win_len, alphas, n_alphas, max_lag, lags, n_lags);
+        *rows = export_average_csv(path, load(avg, len), cfg,
+                                   magnitude ? AverageMode::Magnitude : AverageMode::Coherent);
+        return 0;
+    } catch (const UsageError& e) {
+        return fail(e, 1);
+    } catch (const IoError& e) {
+        return fail(e, 6);
+    } catch (const std::exception& e) {
+        return fail(e, 5);
+    }
+}
+#endif
 
 } // extern "C"

@@ -35,7 +35,7 @@ __all__ = [
     "CyclicFrame", "CyclicCorrelator", "validate_config", "layout_len", "flat_index",
     "full_bin_to_alpha", "average_frames", "compute_set_window", "compute_full_window",
     "UsageError", "ConfigError", "DataError", "CudaError", "LogicError", "lib", "host_alloc",
-    "NoFeatureError", "IoError", "FormatError", "estimate_cfo_ccf", "write_cf32", "PulseKind", "CpmParams", "OracleTable",
+    "NoFeatureError", "IoError", "FormatError", "export_frames_csv", "export_average_csv", "estimate_cfo_ccf", "write_cf32", "PulseKind", "CpmParams", "OracleTable",
     "random_symbols", "cpm_pulse", "cpm_modulate", "gmsk_mc_oracle",
 ]
 
@@ -183,6 +183,9 @@ def lib() -> C.CDLL:
     L.cyc_measure_fp32_peak.argtypes = [C.c_int]
     L.cyc_measure_fp32_peak.restype = C.c_double
     L.cyc_compute_full_window.argtypes = [vp, sz, vp, sz, vp, sz, C.c_int, C.c_uint64, vp, C.c_char_p, sz]
+    L.cyc_export_frames_csv.argtypes = [C.POINTER(_Config), C.c_char_p, vp, vp, sz, C.POINTER(sz), C.c_char_p, sz]
+    L.cyc_export_average_csv.argtypes = [C.POINTER(_Config), C.c_char_p, vp, sz, C.c_int, C.POINTER(sz), C.c_char_p,
+                                         sz]
     _lib = L
     return L
 
@@ -733,6 +736,40 @@ def estimate_cfo_ccf(x, expected_beta: float, N: int, num_frames: int, device: i
     if rc:
         _raise(rc, msg)
     return eps.value
+
+
+def export_frames_csv(path: str, frames, cfg: EstimatorConfig) -> int:
+    """io.cpp:161-186: one row per (frame, element): frame_index,alpha,lag,re,im,mag
+    ("%.17g"), elements in the config's layout order.  Returns the data rows."""
+    frames = list(frames)
+    if not frames:
+        raise UsageError("no frames to export")
+    L = lib()
+    c, keep = cfg._c()
+    vals = np.ascontiguousarray(np.stack([np.asarray(f.values, dtype=np.complex128) for f in frames]))
+    idx = np.ascontiguousarray([f.frame_index for f in frames], dtype=np.uint64)
+    rows, err = C.c_size_t(), C.create_string_buffer(1024)
+    rc = L.cyc_export_frames_csv(C.byref(c), os.fsencode(path), idx.ctypes.data, vals.ctypes.data, len(frames),
+                                 C.byref(rows), err, 1024)
+    if rc == 0 and vals.shape[1] * len(frames) != rows.value:
+        raise UsageError("config does not match the frame layout")
+    if rc:
+        _raise(rc, err.value.decode())
+    return int(rows.value)
+
+
+def export_average_csv(path: str, avg, cfg: EstimatorConfig, mode: AverageMode = AverageMode.Coherent) -> int:
+    """io.cpp:188-208: alpha,lag,mean_re,mean_im,mean_mag (coherent) or
+    alpha,lag,mean_mag (magnitude) per element of an average_frames table."""
+    L = lib()
+    c, keep = cfg._c()
+    a = np.ascontiguousarray(np.asarray(avg, dtype=np.complex128).reshape(-1))
+    rows, err = C.c_size_t(), C.create_string_buffer(1024)
+    rc = L.cyc_export_average_csv(C.byref(c), os.fsencode(path), a.ctypes.data, a.size, int(mode), C.byref(rows),
+                                  err, 1024)
+    if rc:
+        _raise(rc, err.value.decode())
+    return int(rows.value)
 
 
 def write_cf32(path: str, samples) -> int:

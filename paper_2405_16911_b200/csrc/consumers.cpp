@@ -3,6 +3,8 @@
 //   * cyc_push_cf32_file: the cf32 interchange format (proj/src/io.cpp:74-103)
 //     streamed from the page cache into the device rings -- no fp64 copy of
 //     the record (the reference's read_cf32 materialises one);
+//   * cyc_export_frames_csv / cyc_export_average_csv: the CSV result formats
+//     (proj/src/io.cpp:161-208);
 //   * cyc_estimate_cfo_ccf: the CFO estimator (proj/src/impair.cpp:45-115) --
 //     a conjugate Full-mode lag-0 scan whose magnitude average is computed on
 //     the device, then the reference's peak search / median test / log-parabola
@@ -14,8 +16,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "engine.h"
@@ -38,9 +42,153 @@ int fail(cyc_est* est, int code, const std::string& msg, int64_t index = -1) {
     return code;
 }
 
+// "%.17g" (io.cpp:37-41): round-trips every double
+std::string fmt17(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    return buf;
+}
+
+// (alpha, lag) of flat element idx (io.cpp:43-53; the recursive mode's
+// alpha-major lag-list layout alike)
+std::pair<double, int> element_coords(const cyc::Cfg& c, size_t idx) {
+    if (c.mode == CYC_MODE_SET) {
+        const size_t row = 2u * (size_t)c.max_lag + 1u;
+        return {c.alphas[idx / row], (int)(idx % row) - c.max_lag};
+    }
+    if (c.mode == CYC_MODE_FULL) {
+        const size_t n = (size_t)c.win_len;
+        const int k = (int)(idx % n);
+        const double a = (2 * (int64_t)k >= (int64_t)n) ? (double)k / (double)n - 1.0 : (double)k / (double)n;
+        return {a, c.lags[idx / n]};
+    }
+    const size_t t = c.lags.size();
+    return {c.alphas[idx / t], c.lags[idx % t]};
+}
+
+// config_layout_len (io.cpp:55-59; the recursive mode: alphas x lags)
+size_t layout_len_of(const cyc::Cfg& c) {
+    if (c.mode == CYC_MODE_SET) return c.alphas.size() * (2u * (size_t)c.max_lag + 1u);
+    if (c.mode == CYC_MODE_FULL) return c.lags.size() * (size_t)c.win_len;
+    return c.alphas.size() * c.lags.size();
+}
+
+int config_of(const cyc_config* cc, cyc::Cfg& c, char* err, size_t errlen) {
+    if (!cc) {
+        write_msg(err, errlen, "null config");
+        return CYC_ERR_USAGE;
+    }
+    c = cyc::from_c(cc);
+    const auto v = cyc::validate(c);
+    if (!v.empty()) {
+        std::string m = "invalid config:";
+        for (const auto& e : v) m += " [" + e + "]";
+        write_msg(err, errlen, m);
+        return CYC_ERR_CONFIG;
+    }
+    return CYC_OK;
+}
+
+// open_out / finish_out (io.cpp:61-70)
+struct CsvOut {
+    FILE* f = nullptr;
+    std::string path;
+    std::string buf;
+    ~CsvOut() {
+        if (f) std::fclose(f);
+    }
+    void row(const std::string& s) {
+        buf += s;
+        if (buf.size() > (1u << 20)) flush();
+    }
+    bool flush() {
+        if (!buf.empty() && std::fwrite(buf.data(), 1, buf.size(), f) != buf.size()) return false;
+        buf.clear();
+        return true;
+    }
+};
+
+int open_csv(CsvOut& o, const char* path, char* err, size_t errlen) {
+    o.path = path ? path : "";
+    o.f = path ? std::fopen(path, "wb") : nullptr;
+    if (!o.f) {
+        write_msg(err, errlen, "cannot open " + o.path + " for writing");
+        return CYC_ERR_IO;
+    }
+    return CYC_OK;
+}
+
+int close_csv(CsvOut& o, char* err, size_t errlen) {
+    const bool ok = o.flush() && std::fflush(o.f) == 0 && std::fclose(o.f) == 0;
+    o.f = nullptr;
+    if (!ok) {
+        write_msg(err, errlen, "write to " + o.path + " failed");
+        return CYC_ERR_IO;
+    }
+    return CYC_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+// export_frames_csv (io.cpp:161-186)
+int cyc_export_frames_csv(const cyc_config* cfg, const char* path, const uint64_t* frame_index,
+                          const cyc_cf64* values, size_t n_frames, size_t* rows, char* err, size_t errlen) {
+    if (rows) *rows = 0;
+    cyc::Cfg c;
+    if (int rc = config_of(cfg, c, err, errlen)) return rc;
+    if (n_frames == 0 || !values || !frame_index) {
+        write_msg(err, errlen, "no frames to export");
+        return CYC_ERR_USAGE;
+    }
+    const size_t len = layout_len_of(c);
+    CsvOut o;
+    if (int rc = open_csv(o, path, err, errlen)) return rc;
+    o.row("frame_index,alpha,lag,re,im,mag\n");
+    for (size_t f = 0; f < n_frames; ++f)
+        for (size_t i = 0; i < len; ++i) {
+            const auto ac = element_coords(c, i);
+            const cyc_cf64 v = values[f * len + i];
+            o.row(std::to_string(frame_index[f]) + ',' + fmt17(ac.first) + ',' + std::to_string(ac.second) + ',' +
+                  fmt17(v.re) + ',' + fmt17(v.im) + ',' + fmt17(std::hypot(v.re, v.im)) + '\n');
+        }
+    if (int rc = close_csv(o, err, errlen)) return rc;
+    if (rows) *rows = n_frames * len;
+    return CYC_OK;
+}
+
+// export_average_csv (io.cpp:188-208)
+int cyc_export_average_csv(const cyc_config* cfg, const char* path, const cyc_cf64* avg, size_t len, int avg_mode,
+                           size_t* rows, char* err, size_t errlen) {
+    if (rows) *rows = 0;
+    cyc::Cfg c;
+    if (int rc = config_of(cfg, c, err, errlen)) return rc;
+    if (len == 0 || !avg) {
+        write_msg(err, errlen, "no averaged values to export");
+        return CYC_ERR_USAGE;
+    }
+    if (len != layout_len_of(c)) {
+        write_msg(err, errlen, "config does not match the averaged vector length");
+        return CYC_ERR_USAGE;
+    }
+    const bool coh = avg_mode == CYC_AVG_COHERENT;
+    CsvOut o;
+    if (int rc = open_csv(o, path, err, errlen)) return rc;
+    o.row(coh ? "alpha,lag,mean_re,mean_im,mean_mag\n" : "alpha,lag,mean_mag\n");
+    for (size_t i = 0; i < len; ++i) {
+        const auto ac = element_coords(c, i);
+        std::string r = fmt17(ac.first) + ',' + std::to_string(ac.second) + ',';
+        if (coh)
+            r += fmt17(avg[i].re) + ',' + fmt17(avg[i].im) + ',' + fmt17(std::hypot(avg[i].re, avg[i].im)) + '\n';
+        else
+            r += fmt17(avg[i].re) + '\n';
+        o.row(r);
+    }
+    if (int rc = close_csv(o, err, errlen)) return rc;
+    if (rows) *rows = len;
+    return CYC_OK;
+}
 
 // read_cf32 + push (proj/src/io.cpp:90-103, proj/tools/main.cpp:212-214): the
 // whole file is one chunk -- validated whole before any state change.
