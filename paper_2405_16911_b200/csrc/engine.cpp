@@ -966,7 +966,10 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
         if (tail.n_end > tail.n_start) rest.push_back(tail);
         const int si = (int)tsegs.size();
         tsegs.push_back(g);
-        if (planes_on_) {  // planes tiles: 64 residues x a pair of lag blocks (rb = 64-residue block, lb = pair)
+        if (planes_on_ && planes2_) {  // 2-CTA tiles: 128 residues x a pair of lag blocks
+            for (int rb = 0; rb < nrb; ++rb)
+                for (int lp = 0; lp < nlb / 2; ++lp) groups.push_back({si, rb, lp, pa, pb});
+        } else if (planes_on_) {  // planes tiles: 64 residues x a pair of lag blocks (rb = 64-residue block, lb = pair)
             for (int rb = 0; rb < 2 * nrb; ++rb)
                 for (int lp = 0; lp < nlb / 2; ++lp) groups.push_back({si, rb, lp, pa, pb});
         } else {
@@ -986,7 +989,7 @@ Status Engine::fold_tc(const std::vector<FoldSeg>& segs, double* S, std::vector<
             for (const G& gr : groups)
                 if (gr.seg >= (int)b0 && gr.seg < (int)b1)
                     bgroups.push_back({gr.seg - (int)b0, gr.rb, gr.lb, gr.p0, gr.p1});
-            TRY(fold_tc_planes(bsegs, bgroups, S, nlb));
+            TRY(planes2_ ? fold_tc_planes2(bsegs, bgroups, S, nlb) : fold_tc_planes(bsegs, bgroups, S, nlb));
         }
         return Status::ok();
     }
@@ -1291,6 +1294,94 @@ Status Engine::fold_tc_planes(const std::vector<FoldSeg>& tsegs, std::vector<TcG
     }
     launches_ += 2;
     return cuda_check(cudaGetLastError(), "planes fold launch");
+}
+
+Status Engine::fold_tc_planes2(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S,
+                              int nlb) {
+    using G = TcGroupPlan;
+    if (!tpd2_) tpd2_.reset(new TcPl2Desc);
+    TcPl2Desc& D = *tpd2_;
+    std::memcpy(D.segs, tsegs.data(), tsegs.size() * sizeof(FoldSeg));
+    for (size_t i = 0; i < tsegs.size(); ++i) {
+        int64_t pa = 0, pb = 0;
+        for (const G& gr : groups)
+            if (gr.seg == (int)i) {
+                pa = gr.p0;
+                pb = gr.p1;
+                break;
+            }
+        const int ch = tsegs[i].slot;
+        const int64_t off = pa * Pf_ - planes_c0_;  // planes element of the segment's first map sample
+        const uint16_t* p0 = reinterpret_cast<const uint16_t*>(planes_) + (size_t)ch * planes_pitch_ + off;
+        // widest window: residues Pf-128.. at lag pair nlb/2-1: samples up to Pf + lag_lo + 64 nlb
+        if (!encode_tcp2_maps(D, (int)i, p0, (int64_t)c_.channels * planes_pitch_, pa, pb - pa, (int)Pf_,
+                              Pf_ + f_lo_ + 64 * nlb))
+            return Status{CYC_ERR_CUDA, "cuTensorMapEncodeTiled failed for the 2-CTA planes fold", -1};
+    }
+    // tiles: every group split into `splits` period ranges (<= 2048 periods,
+    // at least one wave), launched range-major -- tile i * ng + g -- so the CTAs
+    // of a wave stream the neighbouring windows of one period range together
+    // and the lag blocks of a residue block reuse its planes from L2.  Group g's
+    // tiles are then g, g + ng, ...: the reduce walks them with stride ng (pad).
+    constexpr int64_t MAXP = 2048;
+    const int64_t ng = (int64_t)groups.size();
+    int64_t min_np = INT64_MAX;
+    int splits = 1;
+    for (const G& gr : groups) {
+        splits = (int)std::max<int64_t>(splits, ceil_div(gr.p1 - gr.p0, MAXP));
+        min_np = std::min<int64_t>(min_np, gr.p1 - gr.p0);
+    }
+    // pairs of SMs: SMS / 2 tiles per wave
+    splits = (int)std::max<int64_t>(splits, std::min<int64_t>(ceil_div(SMS / 2, ng), std::max<int64_t>(1, min_np / 16)));
+    std::vector<FoldTile> tiles;
+    std::vector<FoldGroup> fg(groups.size());
+    for (int i = 0; i < splits; ++i)
+        for (size_t g = 0; g < groups.size(); ++g) {
+            const G& gr = groups[g];
+            const int64_t np = gr.p1 - gr.p0;
+            // boundaries on whole stages: only a group's last tile has a partial
+            // stage, whose extra rows lie past the maps (TMA zero fill)
+            const int64_t a = gr.p0 + (np * i / splits) / 16 * 16;
+            const int64_t b = i + 1 == splits ? gr.p1 : gr.p0 + (np * (i + 1) / splits) / 16 * 16;
+            tiles.push_back(FoldTile{gr.seg, gr.rb, gr.lb, (int)g, a, b});
+        }
+    for (size_t g = 0; g < groups.size(); ++g)
+        fg[g] = FoldGroup{groups[g].seg, groups[g].rb, groups[g].lb, (int)g, (int)(g + (splits - 1) * ng) + 1,
+                          (int)ng};
+    int64_t max_np = 0;
+    for (const auto& t : tiles) max_np = std::max<int64_t>(max_np, t.p1 - t.p0);
+    TRY(ensure_partials(tiles.size() * 128 * 128 * sizeof(float4)));
+    const FoldTile* dt = planes_tiles(tiles);
+    if (!dt) return Status{CYC_ERR_CUDA, "planes fold: tile table upload", -1};
+    FoldLaunch L{};
+    L.tc_drain = tc_drain_for(max_np);
+    L.n_tiles = (int)tiles.size();
+    L.n_groups = (int)groups.size();
+    L.Pf = (int)Pf_;
+    L.lag_lo = f_lo_;
+    L.t_pad = t_pad_;
+    L.lw = lw_;
+    L.partials = partials_;
+    L.S = S;
+    L.gate = fold_gate_;
+    L.tc_pairs = 2;
+    D.tiles = dt;
+    double launch_flops = 0.0, exec = 0.0;
+    for (const auto& gr : groups) {  // 128 residues x lags 128 lb .. 128 lb + 127
+        const int lags_in = std::max(0, std::min(128, T_ - 128 * gr.lb));
+        launch_flops += 8.0 * lags_in * 128.0 * (double)(gr.p1 - gr.p0);
+    }
+    // per stage: 6 MMAs of 256 x 256 x 16 on the pair
+    for (const auto& t : tiles) exec += (double)ceil_div(t.p1 - t.p0, 16) * 6.0 * 2.0 * 256 * 256 * 16;
+    if (prof_) {
+        ProfRec r{get_event_timed(), get_event_timed(), launch_flops, exec, true};
+        launch_fold_tcp2(L, D, fg.data(), cs_, r.a, r.b);
+        prof_pending_.push_back(r);
+    } else {
+        launch_fold_tcp2(L, D, fg.data(), cs_);
+    }
+    launches_ += 2;
+    return cuda_check(cudaGetLastError(), "2-CTA planes fold launch");
 }
 
 Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwrite) {
@@ -2457,7 +2548,12 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     const bool fused = !planes && !no_fuse && ring_segs.empty() && !user_segs.empty() &&
                        tc_check_plan(user_segs, pa, pb, pending);
     if (planes) {
-        const int64_t pitch = ((int64_t)n + 4 + 3) & ~(int64_t)3;
+        // cta_group::2 fold (windows start at 64-sample atoms, lag_lo % 64 == 0):
+        // opt-in, it measures 622 vs 611 us on C5 against the 1-CTA pair tiles
+        //
+        static const bool two_cta = std::getenv("CYC_PLANES2") != nullptr;  // A/B knob
+        planes2_ = two_cta && f_lo_ % 64 == 0;
+        const int64_t pitch = ((int64_t)n + 8 + 7) & ~(int64_t)7;
         const size_t words = (size_t)C * (size_t)pitch;
         if (words > planes_words_) {
             if (capturing_) return Status{CYC_ERR_CUDA, "planes buffer growth inside a captured push", -1};
@@ -2472,7 +2568,7 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
             planes_words_ = words;
         }
         planes_pitch_ = pitch;
-        planes_c0_ = c0 & ~(int64_t)3;
+        planes_c0_ = c0 & ~(int64_t)7;
     }
     const size_t s_count = (size_t)C * t_pad_ * Pf_ * 4;
     if (fused && pending) {  // fold into the pending accumulator; the gated add below commits it
@@ -2488,6 +2584,10 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     tl("scan.start", vs_);
     cudaEvent_t ev_s = nullptr;
     if (planes) {  // split + scan on the compute stream (the tiles read the planes); the side stream joins it
+        if (planes2_)
+            launches_ += launch_split_planes4(x, (int64_t)n, C, (int64_t)n, reinterpret_cast<uint16_t*>(planes_),
+                                              (int64_t)C * planes_pitch_, planes_pitch_, c0 - planes_c0_, key_dev_, cs_);
+        else
         launches_ += launch_split_planes(x, (int64_t)n, C, (int64_t)n, planes_, planes_ + planes_words_, planes_pitch_,
                                          c0 - planes_c0_, key_dev_, cs_);
         ev_s = get_event();

@@ -127,6 +127,9 @@ private:
     uint32_t* planes_ = nullptr;
     size_t planes_words_ = 0;  // capacity of each of the hi / lo halves
     bool planes_on_ = false;
+    bool planes2_ = false;  // the chunk's planes are component planes for the 2-CTA fold (lag_lo % 64 == 0)
+    Status fold_tc_planes2(const std::vector<FoldSeg>& tsegs, std::vector<TcGroupPlan>& groups, double* S, int nlb);
+    std::unique_ptr<TcPl2Desc> tpd2_;
     int64_t planes_c0_ = 0, planes_pitch_ = 0;
     std::unique_ptr<TcPlDesc> tpd_;
     struct PlTiles {  // device tile tables of the planes path, by content (graph replays keep them)

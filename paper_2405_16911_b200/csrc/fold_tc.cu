@@ -838,6 +838,242 @@ __global__ void __launch_bounds__(256) split_planes_kernel(const float2* __restr
     if (bad >= 0) atomicMin(key, (2ull * (unsigned long long)bad) * (unsigned long long)C + (unsigned long long)ch);
 }
 
+
+// ---------------------------------------------------------------------------
+// 2-CTA planes fold (cta_group::2).  A CTA pair takes 128 residues x 128 lags:
+// M = 256 rows = the residues' real parts (CTA 0) and imaginary parts (CTA 1)
+// of y; B = 256 window samples of ONE x component (re for accumulator 0, im
+// for accumulator 1), CTA k holding window samples [128k, 128k + 128).  Per
+// SM and stage the tensor core then reads 8 KB per MMA (its A rows and half
+// of B) instead of 12 KB, which takes the SM's shared-memory port below the
+// MMA time.  Accumulator b of CTA k holds c_{2k+b} (c0 = xr yr,
+// c1 = xi yr, c2 = xr yi, c3 = xi yi) of residue r (TMEM lane) at window
+// sample i (column); the band is i - r in [0, 128).
+// ---------------------------------------------------------------------------
+constexpr int P2E = 16;                      // epilogue warps per CTA
+constexpr int P2T = 64 + 32 * P2E;           // + warp 0 producer, warp 1 MMA issuer (leader)
+constexpr int P2X = 4 * 2 * ATOM;            // x stage: 2 atoms x 4 planes = 16 KB
+constexpr int P2Y = 2 * 2 * ATOM;            // y stage: 2 atoms x (hi, lo) = 8 KB
+constexpr int P2S = P2X + P2Y;               // 24 KB per stage
+constexpr int P2N = 8;                       // stages in flight
+constexpr int P2_SMEM = P2N * P2S + 1024;
+static_assert(P2_SMEM <= 227 * 1024, "shared memory per CTA");
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of CTA 0's copy of a barrier
+// D f32, A/B bf16, both MN-major, M = 256 (CTA pair), N = 256
+constexpr uint32_t TC_IDESC2 =
+    (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_4d_pair(uint32_t dst, const CUtensorMap* map, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    // completes on CTA 0's barrier (the MMA issuer's) whichever CTA issues it
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"((uint64_t)map), "r"(su32(bar) & PEER_MASK), "r"(0),
+        "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(da), "l"(db), "r"(TC_IDESC2), "r"(acc));
+}
+__device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {  // arrive on this barrier in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(su32(bar)), "h"((uint16_t)3) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // arrive on CTA 0's copy
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(su32(bar) & PEER_MASK) : "memory");
+}
+
+template <class DESC>
+__global__ void __launch_bounds__(P2T, 1) fold_tcp2_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t full[P2N], planefree[P2N], chunk_done, drain_free;
+    __shared__ uint32_t tmem_s;
+    __shared__ FoldTile s_tile;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    if (threadIdx.x == 0) {
+        s_tile = D.tiles[blockIdx.x >> 1];
+        for (int s = 0; s < P2N; ++s) {
+            mbar_init(&full[s], 1);       // CTA 0: the issuer's expect_tx; both CTAs' TMA bytes
+            mbar_init(&planefree[s], 1);  // the MMA commit, multicast to both CTAs
+        }
+        mbar_init(&chunk_done, 1);
+        mbar_init(&drain_free, 2 * P2E);  // CTA 0: both CTAs' epilogue warps
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // both CTAs, same warp: two 128 x 256 fp32 accumulators per CTA
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive or TMA
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_s;
+    const FoldTile& tile = s_tile;
+    const int64_t r0 = (int64_t)tile.rb * TRB;
+    const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 128;
+    const int nper = (int)(tile.p1 - tile.p0);
+    const int nst = (nper + TKB - 1) / TKB;
+    const int DRAIN = L.tc_drain > 0 ? L.tc_drain : (1 << 30);
+    const int off = L.tc_drain > 0 ? (int)((blockIdx.x >> 1) % 4) * (DRAIN / 4) : 0;
+    const int nchunks = nst > 0 ? (nst - 1 + off) / DRAIN + 1 : 0;
+    if (warp == 0) {
+        if (lane == 0) {
+            // this CTA's half of the x window (all four planes) and its y
+            // component (re on CTA 0, im on CTA 1), hi and lo
+            const CUtensorMap* xm = &D.xmap[tile.seg];
+            const CUtensorMap* ym = &D.ymap[tile.seg];
+            const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
+            const int xatom = (int)((r0 + d) / 64) + 2 * (int)rank, yatom = (int)(r0 / 64);
+            for (int it = 0; it < nst; ++it) {
+                const int s = it % P2N;
+                if (it >= P2N) mbar_wait(&planefree[s], ((it / P2N) - 1) & 1);
+                const uint32_t st = su32(ring + s * P2S);
+                const int row = row0 + it * TKB;
+                if (rank == 0) mbar_expect_tx(&full[s], 2 * P2S);  // both CTAs' stages
+                tma_4d_pair(st, xm, row, 0, xatom, &full[s]);
+                tma_4d_pair(st + P2X, ym, row, 2 * (int)rank, yatom, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            int j = off, k = 0;
+            for (int it = 0; it < nst; ++it, ++j) {
+                const int s = it % P2N;
+                if (j == DRAIN) j = 0;
+                mbar_wait(&full[s], (it / P2N) & 1);
+                if (j == 0 && it > 0) mbar_wait(&drain_free, (uint32_t)(k++) & 1u);
+                const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                // x: [atom a][plane q][16 rows][128 B] at (4a + q) ATOM, q = re_hi, re_lo, im_hi, im_lo
+                // y: [atom a][hi, lo][16 rows][128 B] at P2X + (2a + h) ATOM
+                const uint32_t xb = su32(ring + s * P2S), yb = xb + P2X;
+                const uint64_t dyh = sw128_desc(yb, 2 * ATOM, 1024);
+                const uint64_t dyl = sw128_desc(yb + ATOM, 2 * ATOM, 1024);
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {  // x component: accumulator b
+                    const uint64_t dxh = sw128_desc(xb + (2 * b) * ATOM, 4 * ATOM, 1024);
+                    const uint64_t dxl = sw128_desc(xb + (2 * b + 1) * ATOM, 4 * ATOM, 1024);
+                    const uint32_t dt = tmem + 256 * b;
+                    mma2_bf16(dt, dyh, dxh, acc);
+                    mma2_bf16(dt, dyh, dxl, 1u);
+                    mma2_bf16(dt, dyl, dxh, 1u);
+                }
+                mma2_commit_both(&planefree[s]);
+                if (j == DRAIN - 1 || it == nst - 1) mma2_commit_both(&chunk_done);
+            }
+            if (nst == 0) {
+                // no MMAs: release both CTAs' epilogues (zeros)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&chunk_done)) : "memory");
+                asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, 1;\n\t"
+                             "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(su32(&chunk_done)) : "memory");
+            }
+        }
+    } else {
+        // epilogue: lane quarter q = warp % 4, residue r = 32 q + lane; items of
+        // 32 columns: kind 0 = chunks q (j >= r') and q + 4 (j < r') merged
+        // (t = (j - r') mod 128), kind k = 1..3 chunk q + k (t = 32 k + j - r');
+        // warp w of the quarter holds kind w of both accumulators (the pair of
+        // correlations one CTA owns at the same lag)
+        const int e = warp - 2;
+        const int q = warp & 3, w = e >> 2;
+        const int r = 32 * q + lane, rp = lane;
+        float acc[2][32];
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) acc[b][jj] = 0.f;
+        const int nc = nchunks > 0 ? nchunks : 1;
+        for (int c = 0; c < nc; ++c) {
+            mbar_wait(&chunk_done, (uint32_t)c & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (nst > 0) {
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * b);
+#pragma unroll
+                    for (int jb = 0; jb < 32; jb += 16) {
+#pragma unroll
+                        for (int part2 = 0; part2 < 2; ++part2) {
+                            if (w != 0 && part2 == 1) continue;
+                            const int cc = w != 0 ? q + w : q + 4 * part2;
+                            float v[16];
+                            tmem_ld16(base + (uint32_t)(32 * cc + jb), v);
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) {
+                                const bool use = w != 0 || ((jb + jj >= rp) == (part2 == 0));
+                                if (use) acc[b][jb + jj] += v[jj];
+                            }
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0 && c + 1 < nc) mbar_arrive_leader(&drain_free);
+        }
+        // cell (t, r) of the tile: float4 (c0, c1, c2, c3); this CTA writes its pair
+        float2* part = reinterpret_cast<float2*>(L.partials) + (size_t)(blockIdx.x >> 1) * 128 * TRB * 2;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+            const int t = w != 0 ? 32 * w + jj - rp : (jj - rp) & 127;
+            part[((size_t)t * TRB + r) * 2 + rank] = make_float2(acc[0][jj], acc[1][jj]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // the pair's MMAs, remote arrivals and TMEM reads are complete
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// component planes [re_hi, re_lo, im_hi, im_lo] (the converters' arithmetic)
+// and the chunk's finite scan; 4 samples per thread
+__global__ void __launch_bounds__(256) split_planes4_kernel(const float2* __restrict__ x, int64_t n, int C,
+                                                            int64_t pitch_in, uint16_t* __restrict__ planes,
+                                                            int64_t plane_elems, int64_t pitch_out, int64_t out_off,
+                                                            unsigned long long* key) {
+    const int64_t per_row = (n + 4 * 256 - 1) / (4 * 256);
+    const int ch = (int)(blockIdx.x / per_row);
+    const int64_t b = blockIdx.x % per_row;
+    if (ch >= C) return;
+    const float2* xr = x + (size_t)ch * pitch_in;
+    uint16_t* p0 = planes + (size_t)ch * pitch_out + out_off;
+    const int64_t i0 = b * 4 * 256 + threadIdx.x;
+    float2 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = i0 + 256 * k;
+        v[k] = i < n ? __ldcs(xr + i) : make_float2(0.f, 0.f);
+    }
+    int64_t bad = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = i0 + 256 * k;
+        if (i >= n) continue;
+        const uint32_t h = pack_bf16(v[k].x, v[k].y);
+        const float2 nh = make_float2(-__uint_as_float(h << 16), -__uint_as_float(h & 0xffff0000u));
+        const float2 dd = __fadd2_rn(v[k], nh);
+        const uint32_t l = pack_bf16(dd.x, dd.y);
+        p0[i] = (uint16_t)(h & 0xffffu);                            // re hi
+        p0[plane_elems + i] = (uint16_t)(l & 0xffffu);              // re lo
+        p0[2 * plane_elems + i] = (uint16_t)(h >> 16);              // im hi
+        p0[3 * plane_elems + i] = (uint16_t)(l >> 16);              // im lo
+        if (bad < 0 && !(isfinite(v[k].x) && isfinite(v[k].y))) bad = i;
+    }
+    if (bad >= 0) atomicMin(key, (2ull * (unsigned long long)bad) * (unsigned long long)C + (unsigned long long)ch);
+}
+
 template <int MG>
 struct TcRed {
     FoldGroup groups[MG];
@@ -857,9 +1093,11 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
     const int lane = threadIdx.x & 31, q = lane >> 3;
     const int e = (blockIdx.x * blockDim.x + threadIdx.x - lane) / 4 + (lane & 7);  // lag * TRB + residue
     const int lag = e / TRB, res = e % TRB;
-    // planes tiles: cell (t, 64 h + r) is residue 64 rb + r at lag block 2 lb + h
-    const int64_t rg = L.tc_pairs ? (int64_t)g.rb * 64 + (res & 63) : (int64_t)g.rb * TRB + res;
-    const int tg = L.tc_pairs ? (2 * g.lb + (res >> 6)) * 64 + lag : g.lb * 64 + lag;
+    // planes tiles: cell (t, 64 h + r) is residue 64 rb + r at lag block 2 lb + h;
+    // 2-CTA tiles: cell (t, r) is residue 128 rb + r at lag 128 lb + t
+    const int64_t rg = L.tc_pairs == 1 ? (int64_t)g.rb * 64 + (res & 63) : (int64_t)g.rb * TRB + res;
+    const int tg = L.tc_pairs == 1 ? (2 * g.lb + (res >> 6)) * 64 + lag : g.lb * (L.tc_pairs == 2 ? 128 : 64) + lag;
+    const int cells = L.tc_pairs == 2 ? 128 * TRB : 64 * TRB;  // partial cells per tile
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     // the group's tiles are t0, t0 + stride, ... < t1 (stride 1: contiguous;
@@ -870,7 +1108,7 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
     for (; k + 12 < nt; k += 16) {  // 4 loads in flight, fixed summation order
         float4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(g.t0 + (k + 4 * u) * stride) * 64 * TRB);
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(g.t0 + (k + 4 * u) * stride) * cells);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             s0 += v[u].x;
@@ -880,7 +1118,7 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
         }
     }
     for (; k < nt; k += 4) {
-        const float4 v = __ldcs(part + (size_t)(g.t0 + k * stride) * 64 * TRB);
+        const float4 v = __ldcs(part + (size_t)(g.t0 + k * stride) * cells);
         s0 += v.x;
         s1 += v.y;
         s2 += v.z;
@@ -893,7 +1131,7 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
         s2 += __shfl_down_sync(0xffffffffu, s2, o);
         s3 += __shfl_down_sync(0xffffffffu, s3, o);
     }
-    if (q != 0 || e >= 64 * TRB || rg >= L.Pf || tg >= L.t_pad) return;
+    if (q != 0 || e >= cells || rg >= L.Pf || tg >= L.t_pad) return;
     double* dst = L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4;
     dst[0] += s0;
     dst[1] += s1;
@@ -1047,6 +1285,61 @@ void launch_fold_tcp(const FoldLaunch& L, const TcPlDesc& D, const FoldGroup* gr
     fold_tcp_kernel<TcPlDesc><<<L.n_tiles, TPT, PL_SMEM, st>>>(L, D);
     if (ev1) record_event(ev1, st);
     fold_tc_reduce_kernel<FI_GROUPS><<<dim3(4 * 64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+}
+
+bool encode_tcp2_maps(TcPl2Desc& D, int si, const uint16_t* plane0, int64_t plane_elems, int64_t p_base, int64_t rows,
+                      int Pf, int64_t cols_samples) {
+    D.p_base[si] = p_base;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc || ((uintptr_t)plane0 & 15) || rows <= 0 || ((plane_elems * 2) & 15)) return false;
+    // (64 samples of an atom, period rows, planes, atoms of 64 samples)
+    const cuuint64_t gdim[4] = {64, (cuuint64_t)rows, 4, (cuuint64_t)((cols_samples + 63) / 64)};
+    const cuuint64_t gstr[3] = {2ull * (uint64_t)Pf, 2ull * (uint64_t)plane_elems, 128};
+    const cuuint32_t xbox[4] = {64, (cuuint32_t)TKB, 4, 2}, ybox[4] = {64, (cuuint32_t)TKB, 2, 2}, es[4] = {1, 1, 1, 1};
+    return enc(&D.xmap[si], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(plane0), gdim, gstr, xbox, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+           enc(&D.ymap[si], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(plane0), gdim, gstr, ybox, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_fold_tcp2(const FoldLaunch& L, const TcPl2Desc& D, const FoldGroup* groups, cudaStream_t st,
+                      cudaEvent_t ev0, cudaEvent_t ev1) {
+    if (L.n_tiles == 0) return;
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr))
+        cudaFuncSetAttribute(fold_tcp2_kernel<TcPl2Desc>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM);
+    thread_local TcRed<FI_GROUPS> R;
+    for (int g = 0; g < L.n_groups; ++g) {
+        R.groups[g] = groups[g];
+        R.slot[g] = D.segs[groups[g].seg].slot;
+    }
+    if (ev0) record_event(ev0, st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * L.n_tiles);
+    cfg.blockDim = dim3(P2T);
+    cfg.dynamicSmemBytes = P2_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, fold_tcp2_kernel<TcPl2Desc>, L, D);
+    if (ev1) record_event(ev1, st);
+    fold_tc_reduce_kernel<FI_GROUPS><<<dim3(4 * 128 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+}
+
+int launch_split_planes4(const float2* x, int64_t n, int C, int64_t pitch_in, uint16_t* planes, int64_t plane_elems,
+                         int64_t pitch_out, int64_t out_off, unsigned long long* key, cudaStream_t st) {
+    if (n <= 0 || C <= 0) return 0;
+    const int64_t per_row = (n + 4 * 256 - 1) / (4 * 256);
+    split_planes4_kernel<<<(unsigned)(per_row * C), 256, 0, st>>>(x, n, C, pitch_in, planes, plane_elems, pitch_out,
+                                                                  out_off, key);
+    return 1;
 }
 
 int launch_split_planes(const float2* x, int64_t n, int C, int64_t pitch_in, uint32_t* hi, uint32_t* lo,

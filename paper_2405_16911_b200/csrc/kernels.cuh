@@ -90,7 +90,9 @@ struct FoldLaunch {
     int tc_drain;
     // planes tiles (1): a tile is 64 residues (rb counts 64-residue blocks) x
     // the lag blocks 2 lb and 2 lb + 1 -- partial cell (t, 64 h + r) is
-    // residue 64 rb + r at lag block 2 lb + h; else (0): 128 residues x lag block lb
+    // residue 64 rb + r at lag block 2 lb + h; (2): 2-CTA tiles of 128 residues
+    // x lags 128 lb .. 128 lb + 127, partials [tile][128 lags][128 residues];
+    // else (0): 128 residues x lag block lb
     int tc_pairs;
 };
 
@@ -174,6 +176,27 @@ struct alignas(64) TcPlDesc {
     FoldSeg segs[TC_SEGS];
     const FoldTile* tiles;      // device tile table [n_tiles]
 };
+// 2-CTA planes path (fold_tcp2_kernel): component planes [re_hi, re_lo,
+// im_hi, im_lo] of bf16 per sample, plane stride `plane_elems`; tiles of 128
+// residues x 2 lag blocks on a CTA pair (cta_group::2, M = 256 rows = the
+// residues' real parts on CTA 0 and imaginary parts on CTA 1; each CTA stages
+// half of the 256-sample x window).  xmap2: box {64, 16, 4 planes, 2 atoms};
+// ymap2: box {64, 16, 2 planes, 2 atoms}.
+struct alignas(64) TcPl2Desc {
+    CUtensorMap xmap[TC_SEGS];
+    CUtensorMap ymap[TC_SEGS];
+    int64_t p_base[TC_SEGS];
+    FoldSeg segs[TC_SEGS];
+    const FoldTile* tiles;
+};
+bool encode_tcp2_maps(TcPl2Desc& D, int si, const uint16_t* plane0, int64_t plane_elems, int64_t p_base, int64_t rows,
+                      int Pf, int64_t cols_samples);
+void launch_fold_tcp2(const FoldLaunch& L, const TcPl2Desc& D, const FoldGroup* groups, cudaStream_t st,
+                      cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+// component planes of n samples of every channel: plane q of channel ch at
+// planes + q * plane_elems + ch * pitch_out + out_off + i; and the finite scan
+int launch_split_planes4(const float2* x, int64_t n, int C, int64_t pitch_in, uint16_t* planes, int64_t plane_elems,
+                         int64_t pitch_out, int64_t out_off, unsigned long long* key, cudaStream_t st);
 // Maps over planes whose element 0 is absolute sample p_base * Pf of the segment.
 bool encode_tcp_maps(TcPlDesc& D, int si, const uint32_t* hi, const uint32_t* lo, int64_t p_base, int64_t rows,
                      int Pf, int64_t cols_samples);

@@ -102,3 +102,17 @@ def test_planes_matches_fused_converters(cyc):
     mp = mean_power(x)
     for fl in (cyc.Flags.CONV, cyc.Flags.CONJ):
         assert np.max(np.abs(a.average(flag=fl) - b.average(flag=fl))) <= 2e-6 * mp
+
+
+def test_planes_two_cta_variant():
+    """The cta_group::2 planes fold (opt-in, CYC_PLANES2=1) passes the same
+    oracle checks; run in a child process because the knob is read once."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, CYC_PLANES2="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_planes.py"), "-k", "not two_cta"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <vector>
+#include <cstdlib>
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 template <int MODE>
 __global__ void __launch_bounds__(32, 1) k(const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m4,
@@ -31,7 +32,9 @@ __global__ void __launch_bounds__(32, 1) k(const __grid_constant__ CUtensorMap m
         if (it < stages) {
             const int s = it % NS;
             const uint32_t st = su32(ring + s * STAGE);
-            const int row = (int)(((long long)it * 16 + blockIdx.x * 64) % (rows_total - 16));
+            // each CTA streams its own band of rows (like a fold tile over its period range)
+            const long long band = (rows_total - 16) / gridDim.x;
+            const int row = (int)(blockIdx.x * band + ((long long)it * 16) % (band > 16 ? band - 16 : 1));
             const int atom0 = (blockIdx.x * 6) % 120;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(STAGE) : "memory");
             if (MODE == 0) {
@@ -51,14 +54,14 @@ __global__ void __launch_bounds__(32, 1) k(const __grid_constant__ CUtensorMap m
 typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                         const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                         CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-int main() {
+int main(int argc, char** argv) {
     void* fp = nullptr;
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
     Enc enc = (Enc)fp;
     // planes: row pitch 32 KB (8192 samples x 4 B), hi plane then lo plane 16 MB apart... keep the
     // whole buffer L2-resident: 512 rows x 32 KB = 16 MB per plane
-    const uint64_t pitch = 32768, rows = 256, plane = pitch * rows;
+    const uint64_t pitch = 32768, rows = argc > 1 ? (uint64_t)atoi(argv[1]) * 16 : 256, plane = pitch * rows;
     void* buf;
     cudaMalloc(&buf, 2 * plane);
     cudaMemset(buf, 0, 2 * plane);
