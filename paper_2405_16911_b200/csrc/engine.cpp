@@ -1,5 +1,6 @@
 // engine.cpp -- streaming cyclic-ACF engine (host side).  See engine.h.
 #include "engine.h"
+#include "hostpool.h"
 
 #include <algorithm>
 #include <atomic>
@@ -11,9 +12,6 @@
 #include <cstring>
 #include <numeric>
 #include <thread>
-#if defined(__x86_64__)
-#include <immintrin.h>
-#endif
 
 namespace cyc {
 
@@ -145,48 +143,11 @@ inline bool screen(const cyc_cf64* p, size_t i0, size_t i1) {
 
 // Small host chunks: copy n samples of every channel into the pinned staging
 // (channel rows n apart) and screen them in the same pass (true: some
-// component may be non-finite) -- one read of the caller's memory, not two.
-inline uint32_t copy_screen_scalar(uint32_t* d, const uint32_t* s, size_t m) {
-    uint32_t acc = 0;
-    for (size_t i = 0; i < m; ++i) {
-        const uint32_t w = s[i];
-        d[i] = w;
-        acc |= (uint32_t)((w & 0x7f800000u) == 0x7f800000u);
-    }
-    return acc;
-}
-#if defined(__x86_64__)
-// The staging is only read back by the DMA engine: non-temporal stores skip
-// the read-for-ownership of the destination lines (a third of the memory
-// traffic of a cached copy; the copy is host-memory-bound for cold input).
-__attribute__((target("avx2"))) uint32_t copy_screen_avx2(uint32_t* d, const uint32_t* s, size_t m) {
-    uint32_t acc = 0;
-    size_t i = 0;
-    const size_t head = ((32 - ((uintptr_t)d & 31)) & 31) / 4;
-    if (((uintptr_t)d & 3) != 0 || head > m) return copy_screen_scalar(d, s, m);
-    acc |= copy_screen_scalar(d, s, head);
-    i = head;
-    const __m256i em = _mm256_set1_epi32(0x7f800000);
-    __m256i va = _mm256_setzero_si256();
-    for (; i + 8 <= m; i += 8) {
-        const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
-        va = _mm256_or_si256(va, _mm256_cmpeq_epi32(_mm256_and_si256(v, em), em));
-        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), v);
-    }
-    _mm_sfence();  // the NT stores are visible before the DMA is queued
-    acc |= copy_screen_scalar(d + i, s + i, m - i);
-    return acc | (uint32_t)!_mm256_testz_si256(va, va);
-}
-#endif
+// component may be non-finite) -- one read of the caller's memory, not two;
+// split over the host pool's helper threads (hostpool.h).
 inline bool copy_screen(float2* dst, const cyc_cf32* src, size_t n, int channels) {
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
-    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
-    const size_t m = 2 * n * (size_t)channels;
-#if defined(__x86_64__)
-    static const bool avx2 = __builtin_cpu_supports("avx2") && std::getenv("CYC_NO_NT_COPY") == nullptr;
-    if (avx2 && m >= 1024) return copy_screen_avx2(d, s, m) != 0;
-#endif
-    return copy_screen_scalar(d, s, m) != 0;
+    return copy_screen_words(reinterpret_cast<uint32_t*>(dst), reinterpret_cast<const uint32_t*>(src),
+                             2 * n * (size_t)channels) != 0;
 }
 
 template <typename T>
@@ -661,6 +622,8 @@ Engine::~Engine() {
         cudaFree(g.S);
         cudaFree(g.partials);
         cudaFree(g.tables_dev);
+        cudaFree(g.shift_dev);
+        cudaFreeHost(g.shift_pin);
         cudaFreeHost(g.tables_host);
     }
     cudaFree(ring_x_);
@@ -712,6 +675,9 @@ Engine::~Engine() {
         cudaFreeHost(stage_y_[i]);
         if (stage_ev_[i]) cudaEventDestroy(stage_ev_[i]);
     }
+    cudaFreeHost(dstage_);
+    cudaFreeHost(dstage_y_);
+    for (auto& d : dma_ev_) ev_pool_.push_back(d.second);
     for (auto& m : reads_) ev_pool_.push_back(m.ev);
     for (auto e : ev_pool_) cudaEventDestroy(e);
     for (auto e : timed_pool_) cudaEventDestroy(e);
@@ -1769,21 +1735,40 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         // per-replay descriptors from mapped pinned memory, the finalize's rows
         // (constant per shape) are copied once here, and the recursion writes
         // the emitted tables straight into mapped pinned memory
-        static const bool no_zc = std::getenv("CYC_NO_ZERO_COPY") != nullptr;  // A/B knob
-        n.zero_copy = n.small && recursive && !no_zc;
-        if (n.zero_copy) {
+        // tables out through a D2H node: a kernel's stores into mapped host
+        // memory cost more than the copy on these hosts (C3 FFT 22 vs 9 us)
+        static const bool zc_out = std::getenv("CYC_ZERO_COPY_OUT") != nullptr;  // A/B knob
+        n.zero_copy = n.small && recursive && zc_out;
+        // small graphs read no host descriptors: the rows are uploaded here, the
+        // segment template when it changes and the frame offset lives on the
+        // device (a kernel's read of mapped host memory costs ~13 us on these hosts)
+        if (n.small) {
+            CK(cudaMalloc(&n.shift_dev, sizeof(int64_t)));
+            CK(cudaMallocHost(&n.shift_pin, sizeof(int64_t)));
             CK(cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_));
             CK(cudaStreamSynchronize(cs_));
+            Fz.shift_ctr = n.shift_dev;
+            Fz.shift_inc = (int64_t)(slots / c_.channels) * N_;
         }
         CK(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal));
-        if (!n.zero_copy) cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_);
+        if (!n.small) cudaMemcpyAsync(n.meta_dev, n.meta_host, n.meta_bytes, cudaMemcpyHostToDevice, cs_);
         if (n.small)
-            launch_fold_small(n.zero_copy ? n.segs : reinterpret_cast<const FoldSeg*>(md), (int)slots, (int)Pf_,
-                              f_lo_, lag_hi_ - f_lo_ + 1, t_pad_, n.S, cs_);
+            launch_fold_small(reinterpret_cast<const FoldSeg*>(md), (int)slots, (int)Pf_, f_lo_, lag_hi_ - f_lo_ + 1,
+                              t_pad_, n.S, cs_, n.shift_dev);
         else
             launch_fold(L, cs_);
+        // one frame per replay: the recursion rides in the FFT's output loop
+        n.fused_rec = recursive && slots == (size_t)c_.channels && use_fft_;
+        if (n.fused_rec) {
+            Fz.rec_R = rec_R_;
+            Fz.rec_decay = std::pow(c_.lambda, (double)N_);
+            Fz.rec_coh = coh_;
+            Fz.rec_mag = mag_;
+            Fz.rec_host = n.zero_copy ? n.tables_host : nullptr;
+        }
         launch_finalize(Fz, cs_);
-        if (recursive)
+        if (n.fused_rec) {
+        } else if (recursive)
             launch_recursive_update(n.tables_dev, (int64_t)(slots / c_.channels), c_.channels, (int64_t)per, rec_R_,
                                     std::pow(c_.lambda, (double)N_), coh_, mag_, cs_,
                                     n.zero_copy ? n.tables_host : nullptr);
@@ -1798,8 +1783,28 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         graphs_.push_back(n);
         g = &graphs_.back();
     }
-    fill_frame_segs(g->segs, k0s, chans, recursive);
-    for (int t = 0; t < g->n_tiles; t += g->split) {
+    if (g->small) {
+        // batch offset against the static template (frames f0.. -> 0..)
+        const int64_t delta = k0s[0] - (origin_ + (int64_t)m_minus_);
+        std::vector<int64_t> k0t(k0s);
+        for (auto& k : k0t) k -= delta;
+        std::vector<FoldSeg> tmpl(slots);
+        fill_frame_segs(tmpl.data(), k0t, chans, recursive);
+        const bool tmpl_changed = g->tmpl.size() != slots ||
+                                  std::memcmp(g->tmpl.data(), tmpl.data(), slots * sizeof(FoldSeg)) != 0;
+        if (tmpl_changed || delta != g->shift_expect) {  // first replay, reset, ring growth, other emission paths
+            std::memcpy(g->segs, tmpl.data(), slots * sizeof(FoldSeg));
+            *g->shift_pin = delta;
+            CK(cudaMemcpyAsync(g->meta_dev, g->segs, slots * sizeof(FoldSeg), cudaMemcpyHostToDevice, cs_));
+            CK(cudaMemcpyAsync(g->shift_dev, g->shift_pin, sizeof(int64_t), cudaMemcpyHostToDevice, cs_));
+            CK(cudaStreamSynchronize(cs_));
+            g->tmpl = std::move(tmpl);
+        }
+        g->shift_expect = delta + (int64_t)(slots / c_.channels) * N_;
+    } else {
+        fill_frame_segs(g->segs, k0s, chans, recursive);
+    }
+    for (int t = 0; t < g->n_tiles && !g->small; t += g->split) {
         const FoldSeg& s = g->segs[g->tiles[t].seg];
         const int64_t p0 = floor_div(s.n_start, Pf_), np = floor_div(s.n_end - 1, Pf_) + 1 - p0;
         for (int k = 0; k < g->split; ++k) {  // an empty range (p0 == p1) folds nothing
@@ -1824,7 +1829,7 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         hprof_us_[6] += ms * 1e3;
         hprof_us_[7] += 1;
     }
-    launches_ += g->small ? 3 : 4;
+    launches_ += (g->small ? 3 : 4) - (g->fused_rec ? 1 : 0);
     *tables = g->tables_host;
     return Status::ok();
 }
@@ -2000,6 +2005,8 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         s.msg = "x and y chunks must have equal length";
         return s;
     }
+    if (!pre && deferred_ok(kind, n, yv)) return push_deferred(xv, yv, n, sink, user);
+    TRY(flush_deferred());  // the other paths read and write the rings directly
     const int C = c_.channels;
     const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
     // Small chunks (< 1 MiB) are copied into our pinned staging even when the
@@ -2068,6 +2075,107 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
     // caller memory may not be retained after return
     if (pinned || kind == IN_DEVICE_F32) CK(cudaStreamSynchronize(xs_));
     return cuda_check(cudaGetLastError(), "push");
+}
+
+bool Engine::deferred_ok(int kind, size_t n, const void* yv) const {
+    static const bool off = std::getenv("CYC_NO_DEFER") != nullptr;  // A/B knob
+    return !off && kind == IN_HOST_F32 && (c_.emit_frames || c_.mode == CYC_MODE_RECURSIVE) && n <= (size_t)Q_ &&
+           ((!yv && !cross_) || (yv && cross_));
+}
+
+// Staging positions below abs_lo + dcap_ are about to be rewritten: wait for
+// the flushes that still read the samples they held.
+Status Engine::wait_dstage(int64_t abs_lo) {
+    while (dfree_to_ < abs_lo && !dma_ev_.empty()) {
+        CK(cudaEventSynchronize(dma_ev_.front().second));
+        dfree_to_ = dma_ev_.front().first;
+        ev_pool_.push_back(dma_ev_.front().second);
+        dma_ev_.pop_front();
+    }
+    if (dfree_to_ < abs_lo) dfree_to_ = abs_lo;  // nothing in flight reads it
+    return Status::ok();
+}
+
+Status Engine::push_deferred(const void* xv, const void* yv, size_t n, cyc_frame_sink sink, void* user) {
+    const int C = c_.channels;
+    if (!dstage_) {
+        int64_t want = next_pow2(std::max<int64_t>(4 * (int64_t)Q_, 4 * (N_ + (lag_hi_ - lag_lo_) + 1)));
+        while (want > cap_ || (want > 4 * (int64_t)Q_ && (size_t)want * C * sizeof(float2) > (64u << 20))) want >>= 1;
+        dcap_ = want;
+        CK(cudaMallocHost(&dstage_, (size_t)C * dcap_ * sizeof(float2)));
+        if (cross_) CK(cudaMallocHost(&dstage_y_, (size_t)C * dcap_ * sizeof(float2)));
+        int64_t fl = (256 << 10) / (int64_t)(C * sizeof(float2) * (cross_ ? 2 : 1));
+        if (const char* e = std::getenv("CYC_DEFER_FLUSH")) fl = std::atoll(e);  // tuning knob (samples)
+        dflush_ = std::max<int64_t>(1, std::min<int64_t>(fl, dcap_ / 4));
+        dma_to_ = dfree_to_ = origin_ + (int64_t)consumed_;
+    }
+    if (cross_ && !dstage_y_) CK(cudaMallocHost(&dstage_y_, (size_t)C * dcap_ * sizeof(float2)));
+    const int64_t a = origin_ + (int64_t)consumed_, b = a + (int64_t)n;
+    if (b - dma_to_ > dcap_ / 2) TRY(flush_deferred());  // keeps staged-not-flushed data < dcap_
+    TRY(wait_dstage(b - dcap_));
+    // copy + screen into the staging ring, split at its wrap; staged samples
+    // past consumed_ are ignored if the chunk is rejected
+    bool flag = false;
+    for (int64_t p = a; p < b;) {
+        const int64_t pos = p & (dcap_ - 1), len = std::min(b - p, dcap_ - pos);
+        for (int ch = 0; ch < C; ++ch) {
+            flag = copy_screen(dstage_ + (size_t)ch * dcap_ + pos, (const cyc_cf32*)xv + (size_t)ch * n + (p - a),
+                               (size_t)len, 1) || flag;
+            if (yv)
+                flag = copy_screen(dstage_y_ + (size_t)ch * dcap_ + pos, (const cyc_cf32*)yv + (size_t)ch * n + (p - a),
+                                   (size_t)len, 1) || flag;
+        }
+        p += len;
+    }
+    if (flag) {
+        const Bad bad = scan_bad((const cyc_cf32*)xv, (const cyc_cf32*)yv, n, C);
+        if (bad.key != ~0ull) return data_error(bad.key, bad.channel, IN_HOST_F32, xv, yv, n);
+    }
+    hprof(1);
+    consumed_ += n;
+    const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
+    if (avail > frames_) {
+        TRY(flush_deferred());
+        hprof(2);
+        TRY(emit_new_frames(sink, user, S_main_));
+        hprof(3);
+    } else if (origin_ + (int64_t)consumed_ - dma_to_ >= dflush_) {
+        TRY(flush_deferred());
+        hprof(2);
+    }
+    return cuda_check(cudaGetLastError(), "push");
+}
+
+// DMA the staged samples [dma_to_, consumed) into the rings (one copy per
+// staging wrap; dcap_ divides cap_, so the ring wraps at a subset of those
+// points) and order the compute stream after it.
+Status Engine::flush_deferred() {
+    const int64_t a = dma_to_, b = origin_ + (int64_t)consumed_;
+    if (!dstage_ || b <= a) return Status::ok();
+    const int C = c_.channels;
+    order_copy_after_compute();
+    wait_ring_free(b);
+    for (int64_t p = a; p < b;) {
+        const int64_t ps = p & (dcap_ - 1), len = std::min(b - p, dcap_ - ps);
+        const size_t pr = (size_t)((uint64_t)p & mask_);
+        auto dma = [&](float2* ring, const float2* st) -> Status {
+            if (C == 1)
+                CK(cudaMemcpyAsync(ring + pr, st + ps, (size_t)len * sizeof(float2), cudaMemcpyHostToDevice, xs_));
+            else
+                CK(cudaMemcpy2DAsync(ring + pr, cap_ * sizeof(float2), st + ps, dcap_ * sizeof(float2),
+                                     (size_t)len * sizeof(float2), C, cudaMemcpyHostToDevice, xs_));
+            return Status::ok();
+        };
+        TRY(dma(ring_x_, dstage_));
+        if (cross_) TRY(dma(ring_y_, dstage_y_));
+        p += len;
+    }
+    cudaEvent_t e = get_event();
+    CK(cudaEventRecord(e, xs_));
+    CK(cudaStreamWaitEvent(cs_, e, 0));
+    dma_ev_.push_back({b, e});
+    dma_to_ = b;
+    return Status::ok();
 }
 
 Status Engine::data_error(uint64_t key, int channel, int kind, const void* xv, const void* yv, size_t n) {
@@ -2950,6 +3058,12 @@ Status Engine::reset() {
     if (rec_R_) CK(cudaMemsetAsync(rec_R_, 0, lay_all * sizeof(double2), cs_));
     for (auto& m : reads_) ev_pool_.push_back(m.ev);
     reads_.clear();
+    for (auto& d : dma_ev_) {  // staging is rewritten from the new stream position
+        CK(cudaEventSynchronize(d.second));
+        ev_pool_.push_back(d.second);
+    }
+    dma_ev_.clear();
+    dma_to_ = dfree_to_ = origin_;
     consumed_ = 0;
     frames_ = 0;
     avg_cache_frames_ = ~0ull;

@@ -232,6 +232,13 @@ private:
         int split = 1;  // tiles per (slot, residue block, lag block)
         bool small = false;      // one fold_small launch instead of fold + reduce
         bool zero_copy = false;  // no copy nodes: mapped descriptors in, mapped tables out
+        bool fused_rec = false;  // recursive update inside the FFT (one frame per replay)
+        // small graphs: static segment template in device memory (frame 0 of the
+        // batch at f = 0) + a device frame offset the finalize advances per replay
+        int64_t* shift_dev = nullptr;
+        int64_t* shift_pin = nullptr;
+        int64_t shift_expect = INT64_MIN;
+        std::vector<FoldSeg> tmpl;
         double* S = nullptr;
         float* partials = nullptr;
         double2* tables_dev = nullptr;
@@ -339,6 +346,24 @@ private:
     cudaEvent_t stage_ev_[2] = {};
     bool stage_ev_live_[2] = {};
     size_t stage_len_ = 0;
+
+    // Deferred ingest (small host pushes of per-frame / recursive streams):
+    // each push is copied and screened into a pinned staging ring indexed by
+    // absolute sample (dstage_[channel][dcap_]); the rings receive it in one
+    // DMA per flush -- when frames are due, or every dflush_ samples -- instead
+    // of one DMA + event edges per push (~5 us of copy-engine time and ~4 us of
+    // host driver calls per 64 KB push on these hosts).
+    float2* dstage_ = nullptr;
+    float2* dstage_y_ = nullptr;
+    int64_t dcap_ = 0;       // power of two, <= cap_
+    int64_t dflush_ = 0;     // samples staged before an unforced flush
+    int64_t dma_to_ = 0;     // absolute: staged samples below this have their DMA enqueued
+    int64_t dfree_to_ = 0;   // absolute: staging below this is no longer read by a DMA
+    std::deque<std::pair<int64_t, cudaEvent_t>> dma_ev_;  // (absolute end, event on xs_) per flush
+    bool deferred_ok(int kind, size_t n, const void* yv) const;
+    Status push_deferred(const void* xv, const void* yv, size_t n, cyc_frame_sink sink, void* user);
+    Status flush_deferred();
+    Status wait_dstage(int64_t abs_lo);
 
     // ring overwrite protection: (event, lowest absolute x index read)
     struct ReadMark {

@@ -75,12 +75,25 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
     const int Pf = L.Pf;
     double2* tw = buf + Pf + (Pf >> 4);
     if (threadIdx.x == 0) s_row = L.rows[blockIdx.x];
+    if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) *L.shift_ctr += L.shift_inc;
     for (int k = threadIdx.x; k < (Pf >> 1); k += blockDim.x) tw[k] = __ldg(L.tw + k);
     __syncthreads();
     const FinalRow row = s_row;
     const int fi = blockIdx.y;  // index among requested flags
     const int flag_bit = (L.flags == 2) ? 1 : fi;
     const double* Srow = L.S + ((size_t)row.slot * L.t_pad + row.t_span) * (size_t)Pf * 4;
+    double2* out = L.out + (size_t)row.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride +
+                   (size_t)row.t_out * L.stride_t;
+    // recursive emission: this thread's recursion state loads overlap the FFT
+    const bool rec_pre = L.rec_R && L.A <= (int)blockDim.x;
+    double2 rR = make_double2(0.0, 0.0), rC = rR;
+    double rM = 0.0;
+    if (rec_pre && (int)threadIdx.x < L.A) {
+        const size_t o = (size_t)(out - L.out) + (size_t)threadIdx.x * L.stride_a;
+        rR = L.rec_R[o];
+        rC = L.rec_coh[o];
+        rM = L.rec_mag[o];
+    }
     // the row streams from HBM: 8 independent 16-byte loads in flight per thread
     const double2* S2 = reinterpret_cast<const double2*>(Srow);
     const int nb = blockDim.x;
@@ -117,8 +130,42 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
         default: break;
     }
     const double sc = L.row_scale ? L.row_scale[row.out_block] : L.scale_default;
-    double2* out = L.out + (size_t)row.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride +
-                   (size_t)row.t_out * L.stride_t;
+    if (rec_pre) {
+        const int a = threadIdx.x;
+        if (a >= L.A) return;
+        const double2 v0 = buf[padi(L.bins[a])];
+        const double2 v = make_double2(v0.x * sc, v0.y * sc);
+        const size_t o = (size_t)(out - L.out) + (size_t)a * L.stride_a;
+        rR.x = L.rec_decay * rR.x + v.x;
+        rR.y = L.rec_decay * rR.y + v.y;
+        L.rec_R[o] = rR;
+        L.out[o] = rR;
+        if (L.rec_host) L.rec_host[o] = rR;
+        rC.x += rR.x;
+        rC.y += rR.y;
+        L.rec_coh[o] = rC;
+        L.rec_mag[o] = rM + hypot(rR.x, rR.y);
+        return;
+    }
+    if (L.rec_R) {
+        const size_t o0 = (size_t)(out - L.out);
+        for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
+            const double2 v0 = buf[padi(L.bins[a])];
+            const double2 v = make_double2(v0.x * sc, v0.y * sc);
+            const size_t o = o0 + (size_t)a * L.stride_a;
+            double2 r = L.rec_R[o], c = L.rec_coh[o];
+            r.x = L.rec_decay * r.x + v.x;
+            r.y = L.rec_decay * r.y + v.y;
+            L.rec_R[o] = r;
+            L.out[o] = r;
+            if (L.rec_host) L.rec_host[o] = r;
+            c.x += r.x;
+            c.y += r.y;
+            L.rec_coh[o] = c;
+            L.rec_mag[o] += hypot(r.x, r.y);
+        }
+        return;
+    }
     for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
         const double2 v = buf[padi(L.bins[a])];
         out[(size_t)a * L.stride_a] = make_double2(v.x * sc, v.y * sc);
@@ -134,6 +181,8 @@ __global__ void __launch_bounds__(DFT_T) finalize_dft_kernel(FinalizeLaunch L) {
     __shared__ double2 red[DFT_T / 32][DFT_AB];
     __shared__ FinalRow s_row;  // descriptors may be in mapped host memory: read once
     if (threadIdx.x == 0) s_row = L.rows[blockIdx.x];
+    if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        *L.shift_ctr += L.shift_inc;
     __syncthreads();
     const FinalRow row = s_row;
     const int fi = blockIdx.y;

@@ -23,6 +23,7 @@
 // 64 FFMA2 (128 FMAs); the next period's registers are loaded while the
 // current one is multiplied.  Partial sums leave the CTA in fp32 and are
 // reduced in fp64 in a fixed order (deterministic).
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -421,12 +422,21 @@ __device__ __forceinline__ int64_t floor_div_d(int64_t a, int64_t b) {
     return q;
 }
 
+__device__ __forceinline__ void shift_seg(FoldSeg& g, int64_t d) {
+    g.n_start += d;
+    g.n_end += d;
+    g.x_lo += d;
+    g.x_hi += d;
+    g.w_ref += d;
+}
+
 // Small per-frame folds (recursive emissions, short per-frame windows): one
 // thread per (slot, lag, residue) sums its few periods straight into S in
 // fp64 -- one launch, no partials and no reduce.  Same weights and the same
 // (c0, c1, c2, c3) = (xr yr, xi yr, xr yi, xi yi) as fold_kernel.
 __global__ void __launch_bounds__(128) fold_small_kernel(const FoldSeg* __restrict__ segs, int Pf, int lag_lo,
-                                                         int t_pad, double* __restrict__ S) {
+                                                         int t_pad, double* __restrict__ S,
+                                                         const int64_t* __restrict__ shift) {
     // segs may be mapped host memory (a replayed emission graph rewrites them
     // in place instead of copying them): one read per CTA
     __shared__ FoldSeg s_g;
@@ -434,6 +444,10 @@ __global__ void __launch_bounds__(128) fold_small_kernel(const FoldSeg* __restri
     if (threadIdx.x < sizeof(FoldSeg) / 4)
         reinterpret_cast<uint32_t*>(&s_g)[threadIdx.x] = reinterpret_cast<const uint32_t*>(segs + blockIdx.z)[threadIdx.x];
     __syncthreads();
+    if (shift) {
+        if (threadIdx.x == 0) shift_seg(s_g, *shift);
+        __syncthreads();
+    }
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int t = blockIdx.y;
     if (r >= Pf) return;
@@ -475,6 +489,132 @@ __global__ void __launch_bounds__(128) fold_small_kernel(const FoldSeg* __restri
     d[1] = make_double2(c2, c3);
 }
 
+// Whole-frame folds with few lags (recursive emissions, per-frame windows): a
+// CTA owns FR_RB residues of one slot; it stages FR_PCH periods of y (weighted
+// once per sample, the same fp32 weights as fold_small_kernel) and of the x
+// window in shared memory as fp64, then each thread accumulates LPT lags of
+// one residue over the periods with exact fp32 x fp32 products in fp64, in
+// four interleaved partial sums per component (period p mod 4) so the
+// dependent-FMA chains are a quarter as long: the fp64 pipe is latency-bound
+// with a handful of warps per SM (C3 emissions: 64 periods x 32 lags).
+constexpr int FR_RB = 8, FR_LG = 32, FR_PCH = 64;
+template <int LPT>
+constexpr int fr_smem() { return FR_PCH * (FR_RB + FR_RB + FR_LG * LPT - 1) * (int)sizeof(double2); }
+
+template <int LPT>
+__global__ void __launch_bounds__(256) fold_frame_kernel(const FoldSeg* __restrict__ segs, int Pf, int lag_lo,
+                                                         int t_span, int t_pad, double* __restrict__ S,
+                                                         const int64_t* __restrict__ shift) {
+    constexpr int XW = FR_RB + FR_LG * LPT - 1;
+    extern __shared__ double2 fr_smem_buf[];
+    double2* ys = fr_smem_buf;                // [FR_PCH][FR_RB]
+    double2* xs = fr_smem_buf + FR_PCH * FR_RB;  // [FR_PCH][XW]
+    __shared__ FoldSeg s_g;
+    static_assert(sizeof(FoldSeg) % 4 == 0 && sizeof(FoldSeg) / 4 <= 256, "FoldSeg words");
+    if (threadIdx.x < sizeof(FoldSeg) / 4)
+        reinterpret_cast<uint32_t*>(&s_g)[threadIdx.x] = reinterpret_cast<const uint32_t*>(segs + blockIdx.y)[threadIdx.x];
+    __syncthreads();
+    if (shift) {
+        if (threadIdx.x == 0) shift_seg(s_g, *shift);
+        __syncthreads();
+    }
+    const FoldSeg& g = s_g;
+    const int r0 = blockIdx.x * FR_RB;
+    const int ri = threadIdx.x % FR_RB, lg = threadIdx.x / FR_RB;
+    const int r = r0 + ri;
+    const bool weighted = g.w_log2 != 0.f;
+    // this residue's periods (fold_small_kernel's range) and the block's union
+    const int64_t pa = floor_div_d(g.n_start - r + Pf - 1, Pf), pb = floor_div_d(g.n_end - 1 - r, Pf) + 1;
+    const int64_t Pa = floor_div_d(g.n_start - (r0 + FR_RB - 1) + Pf - 1, Pf), Pb = floor_div_d(g.n_end - 1 - r0, Pf) + 1;
+    double c[LPT][4][4];  // [lag][component][period mod 4]
+#pragma unroll
+    for (int k = 0; k < LPT; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[k][j][0] = c[k][j][1] = c[k][j][2] = c[k][j][3] = 0.0;
+    for (int64_t c0 = Pa; c0 < Pb; c0 += FR_PCH) {
+        const int np = (int)min((int64_t)FR_PCH, Pb - c0);
+        // U loads in flight per thread before their conversions and stores
+        constexpr int U = 8;
+        for (int i0 = threadIdx.x; i0 < np * FR_RB; i0 += U * blockDim.x) {
+            float2 yv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * blockDim.x, pp = i / FR_RB, q = i - pp * FR_RB;
+                const int64_t n = (c0 + pp) * Pf + r0 + q;
+                yv[u] = (i < np * FR_RB && n >= g.n_start && n < g.n_end) ? __ldg(g.y + ((uint64_t)n & g.mask))
+                                                                          : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * blockDim.x, pp = i / FR_RB, q = i - pp * FR_RB;
+                if (i >= np * FR_RB) break;
+                const int64_t n = (c0 + pp) * Pf + r0 + q;
+                if (weighted) {
+                    const float w = g.w_scale * exp2f((float)(g.w_ref - n) * g.w_log2);
+                    yv[u].x *= w;
+                    yv[u].y *= w;
+                }
+                ys[i] = make_double2((double)yv[u].x, (double)yv[u].y);
+            }
+        }
+        for (int i0 = threadIdx.x; i0 < np * XW; i0 += U * blockDim.x) {
+            float2 xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * blockDim.x, pp = i / XW, j = i - pp * XW;
+                const int64_t xi = (c0 + pp) * Pf + r0 + lag_lo + j;
+                xv[u] = (i < np * XW && xi >= g.x_lo && xi < g.x_hi) ? __ldg(g.x + ((uint64_t)xi & g.mask))
+                                                                     : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i >= np * XW) break;
+                xs[i] = make_double2((double)xv[u].x, (double)xv[u].y);
+            }
+        }
+        __syncthreads();
+        const int p_lo = (int)(max(pa, c0) - c0), p_hi = (int)(min(pb, c0 + np) - c0);
+        auto step = [&](int pp, int u) {
+            const double2 yd = ys[pp * FR_RB + ri];
+#pragma unroll
+            for (int k = 0; k < LPT; ++k) {
+                const int t = lg + FR_LG * k;
+                if (t < t_span) {
+                    const double2 xd = xs[pp * XW + ri + t];
+                    c[k][0][u] = fma(xd.x, yd.x, c[k][0][u]);
+                    c[k][1][u] = fma(xd.y, yd.x, c[k][1][u]);
+                    c[k][2][u] = fma(xd.x, yd.y, c[k][2][u]);
+                    c[k][3][u] = fma(xd.y, yd.y, c[k][3][u]);
+                }
+            }
+        };
+        int pp = p_lo;
+        for (; pp + 4 <= p_hi; pp += 4) {
+            step(pp, 0);
+            step(pp + 1, 1);
+            step(pp + 2, 2);
+            step(pp + 3, 3);
+        }
+        if (pp < p_hi) step(pp, 0);
+        if (pp + 1 < p_hi) step(pp + 1, 1);
+        if (pp + 2 < p_hi) step(pp + 2, 2);
+        __syncthreads();
+    }
+    if (r >= Pf) return;
+#pragma unroll
+    for (int k = 0; k < LPT; ++k) {
+        const int t = lg + FR_LG * k;
+        if (t >= t_span) continue;
+        double2* d = reinterpret_cast<double2*>(S + (((size_t)g.slot * t_pad + t) * (size_t)Pf + (size_t)r) * 4);
+        double v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (c[k][j][0] + c[k][j][1]) + (c[k][j][2] + c[k][j][3]);
+        d[0] = make_double2(v[0], v[1]);
+        d[1] = make_double2(v[2], v[3]);
+    }
+}
+
 template <int LW>
 void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, const FoldInline* inl,
               cudaEvent_t before_reduce) {
@@ -497,10 +637,22 @@ void run_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t
 }  // namespace
 
 void launch_fold_small(const FoldSeg* segs_dev, int n_slots, int Pf, int lag_lo, int t_span, int t_pad, double* S,
-                       cudaStream_t st) {
+                       cudaStream_t st, const int64_t* shift) {
     if (n_slots <= 0 || t_span <= 0) return;
+    prepare_fold_kernels();
+    static const bool no_frame = std::getenv("CYC_NO_FRAME_FOLD") != nullptr;  // A/B knob
+    if (!no_frame && Pf % FR_RB == 0 && t_span <= 4 * FR_LG) {
+        const dim3 grid((unsigned)(Pf / FR_RB), (unsigned)n_slots);
+        if (t_span <= FR_LG)
+            fold_frame_kernel<1><<<grid, 256, fr_smem<1>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
+        else if (t_span <= 2 * FR_LG)
+            fold_frame_kernel<2><<<grid, 256, fr_smem<2>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
+        else
+            fold_frame_kernel<4><<<grid, 256, fr_smem<4>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
+        return;
+    }
     fold_small_kernel<<<dim3((unsigned)((Pf + 127) / 128), (unsigned)t_span, (unsigned)n_slots), 128, 0, st>>>(
-        segs_dev, Pf, lag_lo, t_pad, S);
+        segs_dev, Pf, lag_lo, t_pad, S, shift);
 }
 
 void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, const FoldInline* inl,
@@ -527,6 +679,9 @@ void prepare_fold_kernels() {
     cudaFuncSetAttribute(fold_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
     cudaFuncSetAttribute(fold_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<4>::SMEM);
     cudaFuncSetAttribute(fold_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<8>::SMEM);
+    cudaFuncSetAttribute(fold_frame_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fr_smem<1>());
+    cudaFuncSetAttribute(fold_frame_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fr_smem<2>());
+    cudaFuncSetAttribute(fold_frame_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, fr_smem<4>());
 
 }
 }  // namespace cyc

@@ -114,8 +114,11 @@ void launch_fold(const FoldLaunch& L, cudaStream_t st, cudaEvent_t ev0 = nullptr
 // Small per-frame folds: slots segs_dev[0 .. n_slots) (device or mapped host memory), lags
 // lag_lo .. lag_lo + t_span - 1, stored (not accumulated) into S rows 0 .. t_span-1
 // of each seg's slot in fp64.  One thread per (slot, lag, residue).
+// shift (nullable, device memory): added to every segment's absolute indices
+// (n_start, n_end, x_lo, x_hi, w_ref) -- replayed frame graphs keep a static
+// segment template and a device-side frame offset instead of host descriptors.
 void launch_fold_small(const FoldSeg* segs_dev, int n_slots, int Pf, int lag_lo, int t_span, int t_pad, double* S,
-                       cudaStream_t st);
+                       cudaStream_t st, const int64_t* shift = nullptr);
 
 // Tensor-core fold (fold_tc.cu): tiles of 128 residues x 64 lags, descriptors
 // by value; partials [n_tiles][64 lags][128 residues] float4, reduced into S
@@ -247,6 +250,18 @@ struct FinalizeLaunch {
     int64_t out_flag_stride;  // elements per flag table
     int64_t stride_a, stride_t;
     int use_fft;              // 1: radix-2 FFT (Pf pow2 <= 8192); 0: direct DFT
+    // recursive emission of one frame fused into the FFT's output (the same
+    // arithmetic as recursive_update_kernel): R = decay R + value, the running
+    // sums, and an optional copy into mapped host memory; rec_R == nullptr: off
+    double2* rec_R;
+    double rec_decay;
+    double2* rec_coh;
+    double* rec_mag;
+    double2* rec_host;
+    // replayed frame graphs: block (0, 0) adds shift_inc to *shift_ctr (the
+    // fold that read it has completed); nullptr: off
+    int64_t* shift_ctr;
+    int64_t shift_inc;
 };
 
 void launch_finalize(const FinalizeLaunch& L, cudaStream_t st);
