@@ -13,6 +13,8 @@
 //     the reference's per-lag Fft::forward (proj/src/fft.cpp:44-87);
 //   * direct DFT with an exact (bin*r mod Pf) twiddle index, for small alpha
 //     sets or non-power-of-two periods (proj/src/fft.cpp:89-100 analogue).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace cyc {
@@ -28,23 +30,25 @@ __device__ __forceinline__ double2 combine(const double* s, int flag_bit) {  // 
                          : make_double2(s[0] - s[3], s[1] + s[2]);  // x * y
 }
 
-// Shared-memory index with one pad slot per 16 points: a thread's 16
-// consecutive points (first pass) then sit 272 B apart across a warp, off the
-// same banks.
-__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+// Shared-memory index with one pad slot per 16 points (a thread's 16
+// consecutive points in the first pass sit 272 B apart across a warp, off the
+// same banks) and one per Pf/8 (the bit-reversed stores of 8 consecutive
+// residues land Pf/8-multiples apart: without it they share a bank group).
+// sh = log2(Pf) - 3; the buffer holds Pf + Pf/16 + 8 points.
+__device__ __forceinline__ int padi(int i, int sh) { return i + (i >> 4) + (i >> sh); }
 
 // One pass of LOG2R radix-2 DIT levels (halves h, 2h, .., 2^(LOG2R-1) h): each
 // thread takes groups of R = 2^LOG2R points base + pos + k h (k < R) into
 // registers and runs the levels there -- exactly the radix-2 butterflies
 // (v = b w, a + v, a - v) with the level's twiddles, one barrier per pass.
 template <int LOG2R>
-__device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int Pf, int h) {
+__device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int Pf, int h, int sh) {
     constexpr int R = 1 << LOG2R;
     for (int g = threadIdx.x; g < Pf / R; g += blockDim.x) {
         const int base = (g / h) * (R * h), pos = g - (g / h) * h;
         double2 v[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) v[k] = buf[padi(base + pos + k * h)];
+        for (int k = 0; k < R; ++k) v[k] = buf[padi(base + pos + k * h, sh)];
 #pragma unroll
         for (int l = 0; l < LOG2R; ++l) {
             const int hs = h << l;       // half size of this level
@@ -61,25 +65,29 @@ __device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int Pf
             }
         }
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[padi(base + pos + k * h)] = v[k];
+        for (int k = 0; k < R; ++k) buf[padi(base + pos + k * h, sh)] = v[k];
     }
     __syncthreads();
 }
 
-// grid: (n_rows, n_flag_tables); one CTA per (row, flag): the row's combined
+// One CTA per (row, flag): the row's combined
 // correlations in bit-reversed order, then radix-16 passes (four radix-2
 // levels each, in registers) and a final pass of the remaining levels.
 __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
-    extern __shared__ double2 buf[];  // Pf + Pf/16 points (padded), then Pf/2 twiddles
+    extern __shared__ double2 buf[];  // Pf + Pf/16 + 8 points (padded), then Pf/2 twiddles
     __shared__ FinalRow s_row;        // descriptors may be in mapped host memory: read once
     const int Pf = L.Pf;
-    double2* tw = buf + Pf + (Pf >> 4);
-    if (threadIdx.x == 0) s_row = L.rows[blockIdx.x];
-    if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) *L.shift_ctr += L.shift_inc;
+    const int sh = max(log2Pf - 3, 1);
+    double2* tw = buf + Pf + (Pf >> 4) + 8;
+    // grid (n_rows * n_flag_tables): the flag tables of a row are adjacent CTAs,
+    // so the second read of the row's S comes from L2
+    const int nflag = (L.flags == 3) ? 2 : 1;
+    const int row_i = blockIdx.x / nflag, fi = blockIdx.x % nflag;  // fi: index among requested flags
+    if (threadIdx.x == 0) s_row = L.rows[row_i];
+    if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0) *L.shift_ctr += L.shift_inc;
     for (int k = threadIdx.x; k < (Pf >> 1); k += blockDim.x) tw[k] = __ldg(L.tw + k);
     __syncthreads();
     const FinalRow row = s_row;
-    const int fi = blockIdx.y;  // index among requested flags
     const int flag_bit = (L.flags == 2) ? 1 : fi;
     const double* Srow = L.S + ((size_t)row.slot * L.t_pad + row.t_span) * (size_t)Pf * 4;
     double2* out = L.out + (size_t)row.out_block * L.out_block_stride + (size_t)fi * L.out_flag_stride +
@@ -113,27 +121,27 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
             if (r >= Pf) continue;
             const int rev = (int)(__brev((unsigned)r) >> (32 - log2Pf));
             const double c[4] = {v[u][0].x, v[u][0].y, v[u][1].x, v[u][1].y};
-            buf[padi(rev)] = combine(c, flag_bit);
+            buf[padi(rev, sh)] = combine(c, flag_bit);
         }
     }
     __syncthreads();
     int h = 1, lv = 0;
     if (blockDim.x * 16 <= Pf) {  // enough groups of 16 for the block: radix-16 passes
-        for (; lv + 4 <= log2Pf; lv += 4, h <<= 4) fft_pass<4>(buf, tw, Pf, h);
+        for (; lv + 4 <= log2Pf; lv += 4, h <<= 4) fft_pass<4>(buf, tw, Pf, h, sh);
     } else {  // short rows: radix-4 passes keep every thread busy
-        for (; lv + 2 <= log2Pf; lv += 2, h <<= 2) fft_pass<2>(buf, tw, Pf, h);
+        for (; lv + 2 <= log2Pf; lv += 2, h <<= 2) fft_pass<2>(buf, tw, Pf, h, sh);
     }
     switch (log2Pf - lv) {
-        case 3: fft_pass<3>(buf, tw, Pf, h); break;
-        case 2: fft_pass<2>(buf, tw, Pf, h); break;
-        case 1: fft_pass<1>(buf, tw, Pf, h); break;
+        case 3: fft_pass<3>(buf, tw, Pf, h, sh); break;
+        case 2: fft_pass<2>(buf, tw, Pf, h, sh); break;
+        case 1: fft_pass<1>(buf, tw, Pf, h, sh); break;
         default: break;
     }
     const double sc = L.row_scale ? L.row_scale[row.out_block] : L.scale_default;
     if (rec_pre) {
         const int a = threadIdx.x;
         if (a >= L.A) return;
-        const double2 v0 = buf[padi(L.bins[a])];
+        const double2 v0 = buf[padi(L.bins[a], sh)];
         const double2 v = make_double2(v0.x * sc, v0.y * sc);
         const size_t o = (size_t)(out - L.out) + (size_t)a * L.stride_a;
         rR.x = L.rec_decay * rR.x + v.x;
@@ -150,7 +158,7 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
     if (L.rec_R) {
         const size_t o0 = (size_t)(out - L.out);
         for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
-            const double2 v0 = buf[padi(L.bins[a])];
+            const double2 v0 = buf[padi(L.bins[a], sh)];
             const double2 v = make_double2(v0.x * sc, v0.y * sc);
             const size_t o = o0 + (size_t)a * L.stride_a;
             double2 r = L.rec_R[o], c = L.rec_coh[o];
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
         return;
     }
     for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
-        const double2 v = buf[padi(L.bins[a])];
+        const double2 v = buf[padi(L.bins[a], sh)];
         out[(size_t)a * L.stride_a] = make_double2(v.x * sc, v.y * sc);
     }
 }
@@ -242,14 +250,14 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
     if (L.use_fft) {
         int lg = 0;
         while ((1 << lg) < L.Pf) ++lg;
-        const size_t smem = ((size_t)L.Pf + L.Pf / 16 + L.Pf / 2) * sizeof(double2);
+        const size_t smem = ((size_t)L.Pf + L.Pf / 16 + 8 + L.Pf / 2) * sizeof(double2);
         static std::atomic<uint64_t> attr_set{0};
         if (first_on_device(attr_set))
             cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (8192 + 512 + 4096) * (int)sizeof(double2));
+                                 (8192 + 512 + 8 + 4096) * (int)sizeof(double2));
         // Pf = 8192: 512 threads x radix-16 groups; shorter rows: Pf / 4 threads x radix-4
         const int nt = L.Pf >= 8192 ? 512 : std::min(512, std::max(32, L.Pf / 4));
-        finalize_fft_kernel<<<dim3(L.n_rows, nflag), nt, smem, st>>>(L, lg);
+        finalize_fft_kernel<<<(unsigned)(L.n_rows * nflag), nt, smem, st>>>(L, lg);
     } else {
         finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
     }
@@ -262,6 +270,6 @@ void prepare_finalize_kernels() {
     static std::atomic<uint64_t> done{0};
     if (!first_on_device(done)) return;
     cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (8192 + 512 + 4096) * (int)sizeof(double2));
+                         (8192 + 512 + 8 + 4096) * (int)sizeof(double2));
 }
 }  // namespace cyc

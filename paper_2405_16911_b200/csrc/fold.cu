@@ -492,25 +492,38 @@ __global__ void __launch_bounds__(128) fold_small_kernel(const FoldSeg* __restri
 // Whole-frame folds with few lags (recursive emissions, per-frame windows): a
 // CTA owns FR_RB residues of one slot; it stages FR_PCH periods of y (weighted
 // once per sample, the same fp32 weights as fold_small_kernel) and of the x
-// window in shared memory as fp64, then each thread accumulates LPT lags of
-// one residue over the periods with exact fp32 x fp32 products in fp64, in
-// four interleaved partial sums per component (period p mod 4) so the
-// dependent-FMA chains are a quarter as long: the fp64 pipe is latency-bound
-// with a handful of warps per SM (C3 emissions: 64 periods x 32 lags).
+// window in shared memory as fp64.  Its 1024 threads are (residue, lag group,
+// period group): each accumulates LPT lags of one residue over every FR_PG-th
+// period with exact fp32 x fp32 products in fp64, and the FR_PG partial sums
+// meet in shared memory in a fixed order.  The fp64 pipe is latency-bound at a
+// few warps per SM, so the period split buys the parallelism (C3 emissions:
+// 64 periods x 32 lags x 1024 residues).
 constexpr int FR_RB = 8, FR_LG = 32, FR_PCH = 64;
+// period groups: 4 at one lag per thread (1024 threads), fewer when a thread
+// carries more lags (register budget)
 template <int LPT>
-constexpr int fr_smem() { return FR_PCH * (FR_RB + FR_RB + FR_LG * LPT - 1) * (int)sizeof(double2); }
+constexpr int fr_pg() { return LPT == 1 ? 4 : LPT == 2 ? 2 : 1; }
+template <int LPT>
+constexpr int fr_nt() { return FR_RB * FR_LG * fr_pg<LPT>(); }
+template <int LPT>
+constexpr int fr_smem() {
+    return (FR_PCH * (FR_RB + FR_RB + FR_LG * LPT - 1) > (fr_pg<LPT>() - 1) * FR_RB * FR_LG * LPT * 2
+                ? FR_PCH * (FR_RB + FR_RB + FR_LG * LPT - 1)
+                : (fr_pg<LPT>() - 1) * FR_RB * FR_LG * LPT * 2) *
+           (int)sizeof(double2);
+}
 
 template <int LPT>
-__global__ void __launch_bounds__(256) fold_frame_kernel(const FoldSeg* __restrict__ segs, int Pf, int lag_lo,
-                                                         int t_span, int t_pad, double* __restrict__ S,
-                                                         const int64_t* __restrict__ shift) {
+__global__ void __launch_bounds__(fr_nt<LPT>()) fold_frame_kernel(const FoldSeg* __restrict__ segs, int Pf, int lag_lo,
+                                                           int t_span, int t_pad, double* __restrict__ S,
+                                                           const int64_t* __restrict__ shift) {
     constexpr int XW = FR_RB + FR_LG * LPT - 1;
+    constexpr int FR_PG = fr_pg<LPT>(), FR_NT = fr_nt<LPT>();
     extern __shared__ double2 fr_smem_buf[];
-    double2* ys = fr_smem_buf;                // [FR_PCH][FR_RB]
+    double2* ys = fr_smem_buf;                   // [FR_PCH][FR_RB]
     double2* xs = fr_smem_buf + FR_PCH * FR_RB;  // [FR_PCH][XW]
     __shared__ FoldSeg s_g;
-    static_assert(sizeof(FoldSeg) % 4 == 0 && sizeof(FoldSeg) / 4 <= 256, "FoldSeg words");
+    static_assert(sizeof(FoldSeg) % 4 == 0 && sizeof(FoldSeg) / 4 <= FR_NT, "FoldSeg words");
     if (threadIdx.x < sizeof(FoldSeg) / 4)
         reinterpret_cast<uint32_t*>(&s_g)[threadIdx.x] = reinterpret_cast<const uint32_t*>(segs + blockIdx.y)[threadIdx.x];
     __syncthreads();
@@ -520,36 +533,35 @@ __global__ void __launch_bounds__(256) fold_frame_kernel(const FoldSeg* __restri
     }
     const FoldSeg& g = s_g;
     const int r0 = blockIdx.x * FR_RB;
-    const int ri = threadIdx.x % FR_RB, lg = threadIdx.x / FR_RB;
+    const int ri = threadIdx.x % FR_RB, lg = (threadIdx.x / FR_RB) % FR_LG, pg = threadIdx.x / (FR_RB * FR_LG);
     const int r = r0 + ri;
     const bool weighted = g.w_log2 != 0.f;
     // this residue's periods (fold_small_kernel's range) and the block's union
     const int64_t pa = floor_div_d(g.n_start - r + Pf - 1, Pf), pb = floor_div_d(g.n_end - 1 - r, Pf) + 1;
     const int64_t Pa = floor_div_d(g.n_start - (r0 + FR_RB - 1) + Pf - 1, Pf), Pb = floor_div_d(g.n_end - 1 - r0, Pf) + 1;
-    double c[LPT][4][4];  // [lag][component][period mod 4]
+    double c[LPT][4];
 #pragma unroll
-    for (int k = 0; k < LPT; ++k)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) c[k][j][0] = c[k][j][1] = c[k][j][2] = c[k][j][3] = 0.0;
+    for (int k = 0; k < LPT; ++k) c[k][0] = c[k][1] = c[k][2] = c[k][3] = 0.0;
     for (int64_t c0 = Pa; c0 < Pb; c0 += FR_PCH) {
         const int np = (int)min((int64_t)FR_PCH, Pb - c0);
         // U loads in flight per thread before their conversions and stores
-        constexpr int U = 8;
-        for (int i0 = threadIdx.x; i0 < np * FR_RB; i0 += U * blockDim.x) {
+        constexpr int U = 4;
+        const int64_t ybase = c0 * Pf + r0, xbase = ybase + lag_lo;
+        for (int i0 = threadIdx.x; i0 < np * FR_RB; i0 += U * FR_NT) {
             float2 yv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * blockDim.x, pp = i / FR_RB, q = i - pp * FR_RB;
-                const int64_t n = (c0 + pp) * Pf + r0 + q;
+                const int i = i0 + u * FR_NT, pp = i / FR_RB;
+                const int64_t n = ybase + (pp * Pf + (i - pp * FR_RB));
                 yv[u] = (i < np * FR_RB && n >= g.n_start && n < g.n_end) ? __ldg(g.y + ((uint64_t)n & g.mask))
                                                                           : make_float2(0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * blockDim.x, pp = i / FR_RB, q = i - pp * FR_RB;
+                const int i = i0 + u * FR_NT, pp = i / FR_RB;
                 if (i >= np * FR_RB) break;
-                const int64_t n = (c0 + pp) * Pf + r0 + q;
                 if (weighted) {
+                    const int64_t n = ybase + (pp * Pf + (i - pp * FR_RB));
                     const float w = g.w_scale * exp2f((float)(g.w_ref - n) * g.w_log2);
                     yv[u].x *= w;
                     yv[u].y *= w;
@@ -557,61 +569,75 @@ __global__ void __launch_bounds__(256) fold_frame_kernel(const FoldSeg* __restri
                 ys[i] = make_double2((double)yv[u].x, (double)yv[u].y);
             }
         }
-        for (int i0 = threadIdx.x; i0 < np * XW; i0 += U * blockDim.x) {
+        for (int i0 = threadIdx.x; i0 < np * XW; i0 += U * FR_NT) {
             float2 xv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * blockDim.x, pp = i / XW, j = i - pp * XW;
-                const int64_t xi = (c0 + pp) * Pf + r0 + lag_lo + j;
+                const int i = i0 + u * FR_NT, pp = i / XW;
+                const int64_t xi = xbase + (pp * Pf + (i - pp * XW));
                 xv[u] = (i < np * XW && xi >= g.x_lo && xi < g.x_hi) ? __ldg(g.x + ((uint64_t)xi & g.mask))
                                                                      : make_float2(0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * blockDim.x;
+                const int i = i0 + u * FR_NT;
                 if (i >= np * XW) break;
                 xs[i] = make_double2((double)xv[u].x, (double)xv[u].y);
             }
         }
         __syncthreads();
         const int p_lo = (int)(max(pa, c0) - c0), p_hi = (int)(min(pb, c0 + np) - c0);
-        auto step = [&](int pp, int u) {
+        for (int pp = p_lo + pg; pp < p_hi; pp += FR_PG) {
             const double2 yd = ys[pp * FR_RB + ri];
 #pragma unroll
             for (int k = 0; k < LPT; ++k) {
                 const int t = lg + FR_LG * k;
                 if (t < t_span) {
                     const double2 xd = xs[pp * XW + ri + t];
-                    c[k][0][u] = fma(xd.x, yd.x, c[k][0][u]);
-                    c[k][1][u] = fma(xd.y, yd.x, c[k][1][u]);
-                    c[k][2][u] = fma(xd.x, yd.y, c[k][2][u]);
-                    c[k][3][u] = fma(xd.y, yd.y, c[k][3][u]);
+                    c[k][0] = fma(xd.x, yd.x, c[k][0]);
+                    c[k][1] = fma(xd.y, yd.x, c[k][1]);
+                    c[k][2] = fma(xd.x, yd.y, c[k][2]);
+                    c[k][3] = fma(xd.y, yd.y, c[k][3]);
                 }
             }
-        };
-        int pp = p_lo;
-        for (; pp + 4 <= p_hi; pp += 4) {
-            step(pp, 0);
-            step(pp + 1, 1);
-            step(pp + 2, 2);
-            step(pp + 3, 3);
         }
-        if (pp < p_hi) step(pp, 0);
-        if (pp + 1 < p_hi) step(pp + 1, 1);
-        if (pp + 2 < p_hi) step(pp + 2, 2);
         __syncthreads();
     }
-    if (r >= Pf) return;
+    // period groups 1.. hand their partials to group 0 (staging reused)
+    double2* red = fr_smem_buf;  // [FR_PG - 1][LPT][2][FR_RB * FR_LG]
+    const int cell = threadIdx.x % (FR_RB * FR_LG);
+    if (pg > 0) {
+#pragma unroll
+        for (int k = 0; k < LPT; ++k) {
+            red[(((pg - 1) * LPT + k) * 2 + 0) * (FR_RB * FR_LG) + cell] = make_double2(c[k][0], c[k][1]);
+            red[(((pg - 1) * LPT + k) * 2 + 1) * (FR_RB * FR_LG) + cell] = make_double2(c[k][2], c[k][3]);
+        }
+    }
+    __syncthreads();
+    if (pg > 0 || r >= Pf) return;
 #pragma unroll
     for (int k = 0; k < LPT; ++k) {
         const int t = lg + FR_LG * k;
         if (t >= t_span) continue;
-        double2* d = reinterpret_cast<double2*>(S + (((size_t)g.slot * t_pad + t) * (size_t)Pf + (size_t)r) * 4);
-        double v[4];
+        double2 v[2] = {make_double2(c[k][0], c[k][1]), make_double2(c[k][2], c[k][3])};
+        if constexpr (FR_PG > 1) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = (c[k][j][0] + c[k][j][1]) + (c[k][j][2] + c[k][j][3]);
-        d[0] = make_double2(v[0], v[1]);
-        d[1] = make_double2(v[2], v[3]);
+            for (int h = 0; h < 2; ++h) {
+                double2 q[FR_PG - 1];
+#pragma unroll
+                for (int u = 0; u < FR_PG - 1; ++u) q[u] = red[((u * LPT + k) * 2 + h) * (FR_RB * FR_LG) + cell];
+                if constexpr (FR_PG == 4) {  // fixed order: (g0 + g1) + (g2 + g3)
+                    v[h].x = (v[h].x + q[0].x) + (q[1].x + q[2].x);
+                    v[h].y = (v[h].y + q[0].y) + (q[1].y + q[2].y);
+                } else {
+                    v[h].x += q[0].x;
+                    v[h].y += q[0].y;
+                }
+            }
+        }
+        double2* d = reinterpret_cast<double2*>(S + (((size_t)g.slot * t_pad + t) * (size_t)Pf + (size_t)r) * 4);
+        d[0] = v[0];
+        d[1] = v[1];
     }
 }
 
@@ -644,11 +670,11 @@ void launch_fold_small(const FoldSeg* segs_dev, int n_slots, int Pf, int lag_lo,
     if (!no_frame && Pf % FR_RB == 0 && t_span <= 4 * FR_LG) {
         const dim3 grid((unsigned)(Pf / FR_RB), (unsigned)n_slots);
         if (t_span <= FR_LG)
-            fold_frame_kernel<1><<<grid, 256, fr_smem<1>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
+            fold_frame_kernel<1><<<grid, fr_nt<1>(), fr_smem<1>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
         else if (t_span <= 2 * FR_LG)
-            fold_frame_kernel<2><<<grid, 256, fr_smem<2>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
+            fold_frame_kernel<2><<<grid, fr_nt<2>(), fr_smem<2>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
         else
-            fold_frame_kernel<4><<<grid, 256, fr_smem<4>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
+            fold_frame_kernel<4><<<grid, fr_nt<4>(), fr_smem<4>(), st>>>(segs_dev, Pf, lag_lo, t_span, t_pad, S, shift);
         return;
     }
     fold_small_kernel<<<dim3((unsigned)((Pf + 127) / 128), (unsigned)t_span, (unsigned)n_slots), 128, 0, st>>>(

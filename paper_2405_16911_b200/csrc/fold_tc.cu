@@ -1080,63 +1080,50 @@ struct TcRed {
     int slot[MG];  // accumulator slot of each group's segment
 };
 
-// The fp64 reduce of fold.cu for the tensor-core tile geometry (64 lags x 128
-// residues).  Four lanes share an output: lane quarter q sums the group's tiles
-// t0+q, t0+q+4, ... in order, then the quarters combine as (q0+q1)+(q2+q3) --
-// a fixed order, so results are reproducible bit for bit.  A warp covers 8
-// outputs x 4 tiles per load (4 full 128-byte lines).
+// The fp64 reduce of fold.cu for the tensor-core tile geometry.  One thread
+// per partial cell sums the group's tiles t0, t0 + stride, ... in tile order
+// (a fixed order: results are reproducible bit for bit), eight float4 loads in
+// flight, and adds the sums into S with 16-byte accesses issued before the
+// partial loads complete.
 template <int MG>
 __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcRed<MG> R) {
     if (L.gate && *L.gate != ~0ull) return;
     const FoldGroup g = R.groups[blockIdx.y];
     const int slot = R.slot[blockIdx.y];
-    const int lane = threadIdx.x & 31, q = lane >> 3;
-    const int e = (blockIdx.x * blockDim.x + threadIdx.x - lane) / 4 + (lane & 7);  // lag * TRB + residue
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // lag * TRB + residue (pairs: 2 x 64 residues)
+    const int cells = L.tc_pairs == 2 ? 128 * TRB : 64 * TRB;  // partial cells per tile
+    if (e >= cells) return;
     const int lag = e / TRB, res = e % TRB;
     // planes tiles: cell (t, 64 h + r) is residue 64 rb + r at lag block 2 lb + h;
     // 2-CTA tiles: cell (t, r) is residue 128 rb + r at lag 128 lb + t
     const int64_t rg = L.tc_pairs == 1 ? (int64_t)g.rb * 64 + (res & 63) : (int64_t)g.rb * TRB + res;
     const int tg = L.tc_pairs == 1 ? (2 * g.lb + (res >> 6)) * 64 + lag : g.lb * (L.tc_pairs == 2 ? 128 : 64) + lag;
-    const int cells = L.tc_pairs == 2 ? 128 * TRB : 64 * TRB;  // partial cells per tile
+    if (rg >= L.Pf || tg >= L.t_pad) return;
+    double2* dst = reinterpret_cast<double2*>(L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4);
+    const double2 d0 = dst[0], d1 = dst[1];
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
-    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     // the group's tiles are t0, t0 + stride, ... < t1 (stride 1: contiguous;
     // the planes path launches range-major, stride = its group count)
     const int stride = g.pad > 0 ? g.pad : 1;
     const int nt = (g.t1 - g.t0 + stride - 1) / stride;
-    int k = q;
-    for (; k + 12 < nt; k += 16) {  // 4 loads in flight, fixed summation order
-        float4 v[4];
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    constexpr int U = 8;
+    for (int k0 = 0; k0 < nt; k0 += U) {
+        float4 v[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(part + (size_t)(g.t0 + (k + 4 * u) * stride) * cells);
+        for (int u = 0; u < U; ++u)
+            if (k0 + u < nt) v[u] = __ldcs(part + (size_t)(g.t0 + (k0 + u) * stride) * cells);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
+            if (k0 + u >= nt) break;
             s0 += v[u].x;
             s1 += v[u].y;
             s2 += v[u].z;
             s3 += v[u].w;
         }
     }
-    for (; k < nt; k += 4) {
-        const float4 v = __ldcs(part + (size_t)(g.t0 + k * stride) * cells);
-        s0 += v.x;
-        s1 += v.y;
-        s2 += v.z;
-        s3 += v.w;
-    }
-#pragma unroll
-    for (int o = 8; o <= 16; o <<= 1) {
-        s0 += __shfl_down_sync(0xffffffffu, s0, o);
-        s1 += __shfl_down_sync(0xffffffffu, s1, o);
-        s2 += __shfl_down_sync(0xffffffffu, s2, o);
-        s3 += __shfl_down_sync(0xffffffffu, s3, o);
-    }
-    if (q != 0 || e >= cells || rg >= L.Pf || tg >= L.t_pad) return;
-    double* dst = L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4;
-    dst[0] += s0;
-    dst[1] += s1;
-    dst[2] += s2;
-    dst[3] += s3;
+    dst[0] = make_double2(d0.x + s0, d0.y + s1);
+    dst[1] = make_double2(d1.x + s2, d1.y + s3);
 }
 
 }  // namespace
@@ -1227,7 +1214,7 @@ void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self
     if (ev1) record_event(ev1, st);
     if (fold_done) cudaEventRecord(fold_done, st);
     if (before_reduce) cudaStreamWaitEvent(st, before_reduce, 0);
-    fold_tc_reduce_kernel<MG><<<dim3(4 * 64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+    fold_tc_reduce_kernel<MG><<<dim3((L.tc_pairs == 2 ? 128 : 64) * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
 }
 
 template <int MG>
@@ -1284,7 +1271,7 @@ void launch_fold_tcp(const FoldLaunch& L, const TcPlDesc& D, const FoldGroup* gr
     if (ev0) record_event(ev0, st);
     fold_tcp_kernel<TcPlDesc><<<L.n_tiles, TPT, PL_SMEM, st>>>(L, D);
     if (ev1) record_event(ev1, st);
-    fold_tc_reduce_kernel<FI_GROUPS><<<dim3(4 * 64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+    fold_tc_reduce_kernel<FI_GROUPS><<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
 }
 
 bool encode_tcp2_maps(TcPl2Desc& D, int si, const uint16_t* plane0, int64_t plane_elems, int64_t p_base, int64_t rows,
@@ -1330,7 +1317,7 @@ void launch_fold_tcp2(const FoldLaunch& L, const TcPl2Desc& D, const FoldGroup* 
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, fold_tcp2_kernel<TcPl2Desc>, L, D);
     if (ev1) record_event(ev1, st);
-    fold_tc_reduce_kernel<FI_GROUPS><<<dim3(4 * 128 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+    fold_tc_reduce_kernel<FI_GROUPS><<<dim3(128 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
 }
 
 int launch_split_planes4(const float2* x, int64_t n, int C, int64_t pitch_in, uint16_t* planes, int64_t plane_elems,
