@@ -461,6 +461,9 @@ def run_block(args, ws, rank, local):
         full_dev.copy_(gather_channel_tables(out_dev, ws, dist))
 
     def step_device():
+        if ws == 1:  # one call, one host synchronisation (cyc_block_average_device)
+            est.block_average_device(ptr, n_local, out_dev)
+            return
         est.reset()
         est.push_device(ptr, n_local)
         exchange()

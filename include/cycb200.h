@@ -156,6 +156,17 @@ int cyc_push_f64(cyc_est* est, const cyc_cf64* x, const cyc_cf64* y, size_t n,
 int cyc_push_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size_t n,
                     cyc_frame_sink sink, void* user);
 
+/* One device-resident block step (extension; no reference counterpart):
+ * cyc_reset + cyc_push_device(d_x, d_y, n) + cyc_average_all(avg_mode, out)
+ * with ONE host synchronisation -- on the chunk's finite check -- after the
+ * fold, its reduce and the finalize are all enqueued, instead of one per call
+ * (the push's verdict round trip otherwise sits between the fold and the
+ * finalize).  `out` as for cyc_average_all (device memory: written
+ * stream-ordered).  A rejected chunk returns CYC_ERR_DATA (index, message as
+ * cyc_push_device) and leaves the reset state; `out` is then undefined. */
+int cyc_block_average_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size_t n, int avg_mode,
+                             cyc_cf64* out);
+
 /* read_cf32 + push (proj/src/io.cpp:90-103, proj/tools/main.cpp:212-214):
  * the cf32 file (interleaved little-endian float32 I/Q) is pushed as ONE
  * chunk -- validated whole, then streamed from the page cache into the device

@@ -163,6 +163,7 @@ def lib() -> C.CDLL:
     L.cyc_fold_state.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), C.POINTER(C.c_uint64)]
     L.cyc_fold_set_frames.argtypes = [vp, C.c_uint64]
     L.cyc_average_all.argtypes = [vp, C.c_int, vp]
+    L.cyc_block_average_device.argtypes = [vp, vp, vp, C.c_size_t, C.c_int, vp]
     L.cyc_push_cf32_file.argtypes = [vp, C.c_char_p, _SINK, vp]
     L.cyc_estimate_cfo_ccf.argtypes = [vp, sz, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
                                        C.c_char_p, sz]
@@ -609,6 +610,26 @@ class CyclicCorrelator:
         elif out.shape != shape or out.dtype != np.complex128 or not out.flags.c_contiguous:
             raise UsageError(f"out must be a contiguous complex128 array of shape {shape}")
         self._check(self._L.cyc_average_all(self._h, int(mode), out.ctypes.data))
+        return out
+
+    def block_average_device(self, x_ptr: int, n: int, out, mode: AverageMode = AverageMode.Coherent,
+                             y_ptr: Optional[int] = None):
+        """reset + push_device(x_ptr, n) + average_all(out) with one host
+        synchronisation (cyc_block_average_device): the block average of exactly
+        this device chunk.  `out` as for average_all (a device array is written
+        stream-ordered).  DataError leaves the reset state; `out` is then undefined."""
+        nf = int(self._L.cyc_num_flags(self._h))
+        shape = (self._cfg.channels, nf, layout_len(self._layout))
+        cai = getattr(out, "__cuda_array_interface__", None)
+        if cai is not None:
+            if tuple(cai["shape"]) != shape or cai["typestr"] not in ("<c16",) or cai.get("strides") not in (None,):
+                raise UsageError(f"device out must be a contiguous complex128 array of shape {shape}")
+            ptr = int(cai["data"][0])
+        else:
+            if out.shape != shape or out.dtype != np.complex128 or not out.flags.c_contiguous:
+                raise UsageError(f"out must be a contiguous complex128 array of shape {shape}")
+            ptr = out.ctypes.data
+        self._check(self._L.cyc_block_average_device(self._h, x_ptr, y_ptr, n, int(mode), ptr))
         return out
 
     def close(self):

@@ -92,6 +92,12 @@ int cyc_push_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size
     return finish(est, est->e->push(d_x, d_y, n, cyc::Engine::IN_DEVICE_F32, sink, user));
 }
 
+int cyc_block_average_device(cyc_est* est, const cyc_cf32* d_x, const cyc_cf32* d_y, size_t n, int avg_mode,
+                             cyc_cf64* out) {
+    if (!est || !out) return CYC_ERR_USAGE;
+    return finish(est, est->e->block_average_device(d_x, d_y, n, avg_mode, out));
+}
+
 int cyc_average(cyc_est* est, int avg_mode, int flag, int channel, cyc_cf64* out) {
     if (!est || !out) return CYC_ERR_USAGE;
     return finish(est, est->e->average(avg_mode, flag, channel, out));

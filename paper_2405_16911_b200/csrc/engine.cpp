@@ -2507,6 +2507,10 @@ Status Engine::push_speculative(const void* xv, const void* yv, size_t n, int ki
         tl("push.end", cs_);
         trace("fold enqueued");
         TRY(st);
+        if (defer_verdict_) {  // block_average_device checks it after enqueuing the average
+            pv_ = PendingVerdict{true, c0, f0, hb, hc, xv, yv, n};
+            return Status::ok();
+        }
         CK(cudaEventSynchronize(verdict_ev_));  // the verdict (the fold keeps running)
         trace("verdict");
         const uint64_t key = *key_host_;
@@ -2780,6 +2784,28 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
 
 // Every (channel, flag) table at once, [channel][flag][layout] -- one finalize
 // launch and one D2H for multi-channel block mode.
+Status Engine::block_average_device(const void* x, const void* y, size_t n, int avg_mode, cyc_cf64* out) {
+    TRY(reset());
+    pv_.live = false;
+    defer_verdict_ = true;
+    const Status st = push(x, y, n, IN_DEVICE_F32, nullptr, nullptr);
+    defer_verdict_ = false;
+    TRY(st);
+    if (!pv_.live) return average_all(avg_mode, out);  // a path that already knew its verdict
+    const PendingVerdict v = pv_;
+    pv_.live = false;
+    const Status sa = average_all(avg_mode, out);
+    CK(cudaEventSynchronize(verdict_ev_));
+    const uint64_t key = *key_host_;
+    if (key == ~0ull) return sa;
+    const int C = c_.channels;
+    consumed_ = v.c0;  // roll back; the gated reduces skipped themselves
+    frames_ = v.f0;
+    TRY(history_copy(v.hb, v.hc, false));
+    CK(cudaStreamSynchronize(cs_));
+    return data_error(key / C, (int)(key % C), IN_DEVICE_F32, v.x, v.y, v.n);
+}
+
 Status Engine::average_all(int avg_mode, cyc_cf64* out) {
     CK(cudaSetDevice(c_.device));
     TRY(flush_clear());

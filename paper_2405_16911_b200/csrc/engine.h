@@ -68,6 +68,11 @@ public:
     Status push(const void* x, const void* y, size_t n, int kind, cyc_frame_sink sink, void* user);
     Status average(int avg_mode, int flag, int channel, cyc_cf64* out);
     Status average_all(int avg_mode, cyc_cf64* out);
+    // reset + push(device chunk) + average_all(avg_mode, out) with one host
+    // synchronisation (the chunk's verdict) after everything is enqueued: the
+    // block average of exactly this chunk.  On CYC_ERR_DATA the state is the
+    // reset state and `out` is undefined.
+    Status block_average_device(const void* x, const void* y, size_t n, int avg_mode, cyc_cf64* out);
     Status compute_window(const cyc_cf64* xw, size_t xw_len, const cyc_cf64* yw, size_t yw_len,
                           uint64_t k0, cyc_cf64* out);
     Status synchronize();
@@ -168,6 +173,17 @@ private:
     void tl(const char* name, cudaStream_t s);
     void tl_resolve(bool wait);
     Status push_speculative(const void* xv, const void* yv, size_t n, int kind);
+    // block_average_device: the gated device push returns without waiting for
+    // its verdict; the caller checks it once after enqueuing the average
+    bool defer_verdict_ = false;
+    struct PendingVerdict {
+        bool live = false;
+        uint64_t c0 = 0, f0 = 0;
+        int64_t hb = 0, hc = 0;
+        const void* x = nullptr;
+        const void* y = nullptr;
+        size_t n = 0;
+    } pv_;
     // Device-resident block push: history save, key reset, the finite scan +
     // verdict copy on vs_, the fold (reduces gated on the verdict) -- enqueued
     // directly, or replayed as one CUDA graph when the same (buffer, length,

@@ -661,3 +661,36 @@ def test_estimators_on_two_devices(cyc, oracle):
     for o in outs:
         assert_parity(o[0, 0].reshape(64, N)[:, ::37], cv.T, mean_power(x))
         assert_parity(o[0, 1].reshape(64, N)[:, ::37], cj.T, mean_power(x))
+
+
+def test_block_average_device_matches_separate_calls(cyc, oracle):
+    """cyc_block_average_device = reset + push_device + average_all (one host
+    synchronisation), against the oracle; a rejected chunk raises DataError with
+    the chunk's index and leaves the reset state."""
+    import torch
+    N, lags = 1024, list(range(64))
+    x = rand_c(N * 300 + 17, 77)
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=N, lag_spec=cyc.LagSpec.Explicit(lags),
+                              flags=cyc.Flags.BOTH, emit_frames=False)
+    est = cyc.CyclicCorrelator(cfg)
+    d = torch.from_numpy(x.view(np.float32)).cuda()
+    out = torch.empty((1, 2, len(lags) * N), dtype=torch.complex128, device="cuda")
+    for _ in range(2):  # the second call replays the captured push
+        est.block_average_device(d.data_ptr(), len(x), out)
+    got = out.cpu().numpy()
+    ref = cyc.CyclicCorrelator(cfg)
+    ref.push_device(d.data_ptr(), len(x))
+    want = ref.average_all()
+    assert np.array_equal(got, want)
+    F = est.frames_emitted()
+    bins = np.array([0, 5, 511, 1023])
+    cv, cj = oracle.block_fold(x, x, bins, N, lags, 0, F * N)
+    for fi, w in ((0, cv), (1, cj)):
+        assert_parity(got[0, fi].reshape(len(lags), N)[:, bins], w.T, mean_power(x), what=f"flag {fi}")
+    bad = x.copy()
+    bad[4321] = np.nan
+    db = torch.from_numpy(bad.view(np.float32)).cuda()
+    with pytest.raises(cyc.DataError) as ei:
+        est.block_average_device(db.data_ptr(), len(bad), out)
+    assert ei.value.index == 4321
+    assert est.consumed() == 0 and est.frames_emitted() == 0
