@@ -248,8 +248,18 @@ __device__ unsigned long long g_tc_trace[8][128];
 __device__ unsigned long long g_tc_warp[16][64][2];  // per converter warp: (full seen, conv arrive) per stage
 #define TC_MARK(kind, it) \
     if (blockIdx.x == 0 && (it) < 128) g_tc_trace[kind][it] = clock64();
+// (clock64, globaltimer) of CTA 0 and of the last CTA at kernel start (s=0) and end (s=1): the SM clock under load
+#define TC_TIME(s)                                                                          \
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) {             \
+        unsigned long long gt;                                                              \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));                              \
+        const int b = blockIdx.x == 0 ? 100 : 110;                                          \
+        g_tc_trace[6][b + 2 * (s)] = clock64();                                             \
+        g_tc_trace[6][b + 2 * (s) + 1] = gt;                                                \
+    }
 #else
 #define TC_MARK(kind, it)
+#define TC_TIME(s)
 #endif
 
 // Drain of the fused kernel (NE converter warps, NE/4 per TMEM lane quarter):
@@ -686,7 +696,10 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
 
 constexpr int TPE = TC_TPE;                        // epilogue warps of the planes kernel
 constexpr int TPT = 64 + 32 * TPE;
-constexpr int PL_RING = 192 * 1024;               // stages: 24 KB (self) or 32 KB (x + 2 y atoms)
+#ifndef PL_RING_KB
+#define PL_RING_KB 192
+#endif
+constexpr int PL_RING = PL_RING_KB * 1024;        // stages: 24 KB (self) or 32 KB (x + 2 y atoms)
 constexpr int NPL_MAX = PL_RING / (2 * XPLANE);    // self tiles: 8 stages in flight (others 6)
 constexpr int PL_SMEM = PL_RING + 1024;
 static_assert(PL_SMEM <= 227 * 1024, "shared memory per CTA");
@@ -722,6 +735,7 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_s;
+    TC_TIME(0);
     if (threadIdx.x == 0) TC_MARK(7, 0);
     const FoldTile& tile = s_tile;
     // 64 residues [r0, r0 + 64) x lag blocks d .. d + 127: accumulator h takes
@@ -755,6 +769,12 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                 TC_MARK(0, it);
                 const uint32_t st = su32(ring + s * slot);
                 const int row = row0 + it * TKB;
+#ifdef TC_ABL_NO_TMA  // ablation (diagnostic builds): stages after the first ring reuse stale data
+                if (it >= NPL) {
+                    mbar_arrive(&full[s]);
+                    continue;
+                }
+#endif
                 mbar_expect_tx(&full[s], slot);
                 tma_4d(st, xm, row, xatom, &full[s]);
                 if (!self) tma_4d(st + 2 * XPLANE, ym, row, yatom, &full[s]);
@@ -772,6 +792,11 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                 TC_MARK(1, it);
                 const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
                 asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef TC_ABL_NO_MMA  // ablation (diagnostic builds): stages are released without MMAs
+                mbar_arrive(&planefree[s]);
+                if (j == DRAIN - 1 || it == nst - 1) mbar_arrive(&chunk_done);
+                continue;
+#endif
                 // atom a of a window: hi at (2a) ATOM, lo at (2a + 1) ATOM -- the
                 // operands' MN-atom stride (LBO) is 2 ATOM
                 const uint32_t xb = su32(ring + s * slot);
@@ -798,6 +823,7 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    TC_TIME(1);
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 

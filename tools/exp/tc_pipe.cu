@@ -1,0 +1,142 @@
+// Producer/MMA pipeline overhead (diagnostics): warp 0 lane 0 arrives full[s]
+// after planefree[s] (8-slot ring, no TMA), warp 1 lane 0 waits full[s],
+// issues MPS MMAs (M=128 N=256 K=16, two accumulators), commits planefree[s];
+// optional idle warps polling an mbarrier like the epilogue.  Cycles per MMA.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc),
+        "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+
+template <int MPS>
+__global__ void __launch_bounds__(576, 1) k(int nst, int idle_warps, unsigned long long* out, int fill) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t full[8], pfree[8], never;
+    __shared__ uint32_t tmem_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 8 * 24576 / 4; i += blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u + 12345u;
+        h ^= h >> 13;
+        h *= 0x5bd1e995u;
+        h ^= h >> 15;
+        // two bf16 with exponent 120..135 (|v| ~ 2^-7 .. 2^8), random sign/mantissa: like split samples
+        const uint32_t lo = (h & 0x807f) | ((120u + ((h >> 8) & 15)) << 7), hi = ((h >> 16) & 0x807f) | ((120u + ((h >> 24) & 15)) << 7);
+        reinterpret_cast<uint32_t*>(sm)[i] = fill ? (lo | (hi << 16)) : 0u;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 8; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&pfree[s], 1);
+        }
+        mbar_init(&never, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_s;
+    const uint32_t slot = 24576;
+    if (warp == 0 && lane == 0) {
+        for (int it = 0; it < nst; ++it) {
+            const int s = it & 7;
+            if (it >= 8) mbar_wait(&pfree[s], ((it >> 3) - 1) & 1);
+            mbar_arrive(&full[s]);
+        }
+    } else if (warp == 1 && lane == 0) {
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((256u >> 3) << 17) |
+                               ((128u >> 4) << 24);
+        const long long t0 = clock64();
+        for (int it = 0; it < nst; ++it) {
+            const int s = it & 7;
+            mbar_wait(&full[s], (it >> 3) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t xb = su32(sm) + (uint32_t)s * slot;
+#pragma unroll
+            for (int m = 0; m < MPS / 6; ++m) {
+                const uint64_t dyh = desc_sw128(xb + 2048 * m, 4096, 1024), dyl = desc_sw128(xb + 2048 * m + 1024, 4096, 1024);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint64_t dxh = desc_sw128(xb + 8192 * h + 2048 * m, 4096, 1024);
+                    const uint64_t dxl = desc_sw128(xb + 8192 * h + 2048 * m + 1024, 4096, 1024);
+                    mma_bf16(tmem + 256 * h, dyh, dxh, idesc, 1u);
+                    mma_bf16(tmem + 256 * h, dyh, dxl, idesc, 1u);
+                    mma_bf16(tmem + 256 * h, dyl, dxh, idesc, 1u);
+                }
+            }
+            mma_commit(&pfree[s]);
+        }
+        mbar_wait(&pfree[(nst - 1) & 7], ((nst - 1) >> 3) & 1);
+        if (blockIdx.x == 0) out[0] = clock64() - t0;
+    } else if (warp >= 2 && warp < 2 + idle_warps) {
+        // idle epilogue stand-ins: poll a barrier that completes at the end (warp 1 arrives after its loop)
+        if (lane == 0) {
+            unsigned n = 0;
+            while (true) {
+                uint32_t ok;
+                asm volatile(
+                    "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+                    : "=r"(ok) : "r"(su32(&never)), "r"(0u) : "memory");
+                if (ok || ++n > 4000000) break;
+            }
+        }
+    }
+    if (warp == 1 && lane == 0) mbar_arrive(&never);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+int main() {
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    const int smem = 8 * 24576 + 1024;
+    cudaFuncSetAttribute(k<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int fill = 0; fill < 2; ++fill)
+    for (int idle : {16})
+        for (int mps : {6, 12}) {
+            const int nmma = 6144, nst = nmma / mps;
+            unsigned long long h = 0;
+            for (int rep = 0; rep < 2; ++rep) {
+                if (mps == 6) k<6><<<148, 576, smem>>>(nst, idle, d, fill);
+                else k<12><<<148, 576, smem>>>(nst, idle, d, fill);
+                cudaDeviceSynchronize();
+            }
+            cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+            printf("%s data, idle warps %2d, %2d MMAs per stage: %.1f cycles per MMA %s\n", fill ? "random" : "zero  ", idle, mps, (double)h / nmma,
+                   cudaGetErrorString(cudaGetLastError()));
+        }
+    return 0;
+}

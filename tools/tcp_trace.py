@@ -33,3 +33,8 @@ print("issue->fullseen mean", (t[3, :n] - t[0, :n])[5:].mean())
 print("fullseen->mma_go (drain waits) mean", (t[1, :n] - t[3, :n])[5:].mean())
 print("mma issue time mean", (t[2, :n] - t[1, :n])[5:].mean())
 print("issue interval mean", np.diff(t[0, :n])[5:].mean())
+for name, b in (("CTA 0", 100), ("last CTA", 110)):
+    c0, g0, c1, g1 = (int(t[6, b + k]) for k in range(4))
+    if g1 > g0:
+        print(f"{name}: {c1 - c0} cycles in {(g1 - g0) / 1e3:.1f} us -> SM clock {(c1 - c0) / (g1 - g0):.3f} GHz")
+print("kernel span (CTA 0 start -> last CTA end) us", (int(t[6, 113]) - int(t[6, 101])) / 1e3)
