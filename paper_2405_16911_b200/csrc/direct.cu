@@ -20,6 +20,51 @@ constexpr int DT = 256;     // threads
 constexpr int TILE = 512;   // samples per smem tile
 constexpr int MAXL = 4;     // lags per thread (T <= 1024)
 
+// The last CTA of (segment si, alpha a) to finish sums the splits' partials
+// (split order, fp64) into the frame's table and the running sums -- the
+// arithmetic of direct_reduce_accum_kernel for one frame per channel.  Every
+// thread of every CTA calls this after writing its partials.
+__device__ void fused_reduce(const DirectLaunch& L, int si, int a) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int* ctr = L.fuse_counters + (size_t)si * L.A + a;
+        s_last = atomicAdd(ctr, 1) == L.splits - 1;
+        if (s_last) *ctr = 0;  // ready for the next launch (stream-ordered)
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const float2* part = reinterpret_cast<const float2*>(L.partials);
+    const int ch = si;  // one frame per channel: segment = channel
+    for (int t = threadIdx.x; t < L.T; t += blockDim.x) {
+        int fi = 0;
+        for (int f = 0; f < 2; ++f) {
+            if (!(L.flags & (1 << f))) continue;
+            const int64_t e = (int64_t)ch * L.per + (int64_t)fi * L.out_flag_stride + (int64_t)a * L.stride_a +
+                              (int64_t)t * L.stride_t;
+            double re = 0.0, im = 0.0;
+            for (int s = 0; s < L.splits; ++s) {
+                const float2 v = __ldcg(part + ((((size_t)si * L.A + a) * L.splits + s) * 2 + f) * L.T + t);
+                re += v.x;
+                im += v.y;
+            }
+            const double2 v = make_double2(re * L.scale, im * L.scale);
+            const size_t o = (size_t)si * L.out_block_stride + (size_t)fi * L.out_flag_stride +
+                             (size_t)a * L.stride_a + (size_t)t * L.stride_t;
+            L.out[o] = v;
+            if (L.out_host) L.out_host[o] = v;
+            double2 c = L.coh[e];
+            c.x += v.x;
+            c.y += v.y;
+            L.coh[e] = c;
+            L.mag[e] += hypot(v.x, v.y);
+            ++fi;
+        }
+    }
+}
+
 // Threads: SL sample lanes x (DT / SL) lag slots.  Short lag spans (T <= 32)
 // use 8 lanes, so every thread works; each lane sums the samples i = sub
 // (mod SL) of its lags, and the lanes combine in a fixed order in shared memory.
@@ -100,6 +145,7 @@ __global__ void __launch_bounds__(DT) direct_kernel(const __grid_constant__ Dire
             part[(base + 0) * L.T + t] = accv[k];
             part[(base + 1) * L.T + t] = accj[k];
         }
+        if (L.fuse_counters) fused_reduce(L, si, a);
         return;
     }
     // lanes 1.. hand their sums to lane 0 through shared memory (reusing the
@@ -112,11 +158,10 @@ __global__ void __launch_bounds__(DT) direct_kernel(const __grid_constant__ Dire
         red[((sub * MAXL + k) * LT + slot) * 2 + 1] = accj[k];
     }
     __syncthreads();
-    if (sub != 0) return;
 #pragma unroll
     for (int k = 0; k < MAXL; ++k) {
         const int t = slot + k * LT;
-        if (t >= L.T) continue;
+        if (sub != 0 || t >= L.T) continue;  // lane 0 writes (no early return: the fused reduce syncs the CTA)
         float2 v = red[((0 * MAXL + k) * LT + slot) * 2 + 0], j = red[((0 * MAXL + k) * LT + slot) * 2 + 1];
         for (int q = 1; q < SL; ++q) {
             const float2 v2 = red[((q * MAXL + k) * LT + slot) * 2 + 0];
@@ -129,6 +174,7 @@ __global__ void __launch_bounds__(DT) direct_kernel(const __grid_constant__ Dire
         part[(base + 0) * L.T + t] = v;
         part[(base + 1) * L.T + t] = j;
     }
+    if (L.fuse_counters) fused_reduce(L, si, a);
 }
 
 __global__ void direct_reduce_kernel(const __grid_constant__ DirectLaunch L) {
@@ -216,6 +262,7 @@ void launch_direct(const DirectLaunch& L, cudaStream_t st, double2* coh, double*
     if (first_on_device(attr_set))
         cudaFuncSetAttribute(direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     direct_kernel<<<L.n_segs * L.A * L.splits, DT, smem, st>>>(L, span, SL);
+    if (L.fuse_counters) return;  // reduced by the last CTA of each (segment, alpha)
     if (coh)
         direct_reduce_accum_kernel<<<dim3((L.T + 127) / 128, L.A, channels), 128, 0, st>>>(L, L.n_segs / channels,
                                                                                           channels, coh, mag, per);

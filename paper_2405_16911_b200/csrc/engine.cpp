@@ -677,6 +677,7 @@ Engine::~Engine() {
     }
     cudaFreeHost(dstage_);
     cudaFreeHost(dstage_y_);
+    cudaFree(direct_ctr_);
     for (auto& d : dma_ev_) ev_pool_.push_back(d.second);
     for (auto& m : reads_) ev_pool_.push_back(m.ev);
     for (auto e : ev_pool_) cudaEventDestroy(e);
@@ -1517,6 +1518,10 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     // sample lanes (short lag spans) let a CTA take fewer samples: split finer
     const int sl = direct_lanes(T_);
     int splits = (int)std::min<int64_t>(256, std::max<int64_t>(1, maxcnt / (8192 / sl)));
+    // small calls (C1: one 4096-sample frame x 10 alphas): at least ~two CTAs per
+    // SM, down to 256 samples per split -- the launch is latency-bound
+    const int64_t want = (2 * SMS + (int64_t)segs.size() * A_ - 1) / ((int64_t)segs.size() * A_);
+    splits = (int)std::max<int64_t>(splits, std::min<int64_t>(want, maxcnt / 256));
     while (splits > 1 && (int64_t)segs.size() * A_ * splits > 64 * SMS) splits /= 2;
     const size_t pbytes = segs.size() * (size_t)A_ * splits * 2 * T_ * sizeof(float2);
     TRY(ensure_partials(pbytes));
@@ -1545,6 +1550,23 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     if (accum) {  // per-frame batch: the reduce also adds the frames to the running sums
         // ... and writes the tables straight into the pinned host copy
         L.out_host = (direct_host_out_ && out == frames_dev_) ? frames_host_ : nullptr;
+        static const bool no_fuse = std::getenv("CYC_NO_DIRECT_FUSE") != nullptr;  // A/B knob
+        if (!no_fuse && segs.size() == (size_t)c_.channels) {  // one frame: the last CTA reduces
+            const size_t need = segs.size() * (size_t)A_;
+            if (direct_ctr_n_ < need) {
+                cudaFree(direct_ctr_);
+                CK(cudaMalloc(&direct_ctr_, need * sizeof(int)));
+                CK(cudaMemsetAsync(direct_ctr_, 0, need * sizeof(int), cs_));
+                direct_ctr_n_ = need;
+            }
+            L.fuse_counters = direct_ctr_;
+            L.coh = coh_;
+            L.mag = mag_;
+            L.per = (int64_t)nflags_ * (int64_t)layout_len_;
+            launch_direct(L, cs_);
+            launches_ += 1;
+            return cuda_check(cudaGetLastError(), "direct launch");
+        }
         launch_direct(L, cs_, coh_, mag_, c_.channels, (int64_t)nflags_ * (int64_t)layout_len_);
     }
     else

@@ -369,6 +369,8 @@ private:
     // DMA per flush -- when frames are due, or every dflush_ samples -- instead
     // of one DMA + event edges per push (~5 us of copy-engine time and ~4 us of
     // host driver calls per 64 KB push on these hosts).
+    int* direct_ctr_ = nullptr;  // fused direct reduce: per-(segment, alpha) CTA counters
+    size_t direct_ctr_n_ = 0;
     float2* dstage_ = nullptr;
     float2* dstage_y_ = nullptr;
     int64_t dcap_ = 0;       // power of two, <= cap_

@@ -296,6 +296,13 @@ struct DirectLaunch {
     double2* out_host;          // optional mapped pinned mirror of `out` (per-frame tables: no D2H copy)
     int64_t out_block_stride, out_flag_stride, stride_a, stride_t;
     double scale;
+    // one frame per channel (n_segs == channels) with running sums: the last
+    // CTA of each (segment, alpha) to finish reduces its splits in the direct
+    // kernel itself (counters: [n_segs][A] zeros, left zeroed), no second launch
+    int* fuse_counters;
+    double2* coh;
+    double* mag;
+    int64_t per;
 };
 
 // coh/mag non-null: the reduce also adds each frame to the running average_frames
