@@ -49,11 +49,13 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
 // TMEM accumulation chunk (stages of 16 periods) for tensor-core tiles of at
 // most `max_periods` periods: whole tiles up to 64 stages, else equal chunks
-// of about 32 stages.  The tensor core's truncating accumulation biases a cell
-// by ~7e-8 of its value per stage, and the dropped lo*lo term by ~2e-6: the
-// worst cell (the lag-0 power) measured 6.4e-6 of the mean power at C2's
-// 57-stage tiles and 4.3-4.6e-6 with 32-stage chunks (C5, C4), against the
-// 1e-5 cell tolerance (tools/acc_probe.py).
+// of at most 48 stages.  The tensor core's truncating accumulation biases a
+// cell by ~7e-8 of its value per stage, and the dropped lo*lo term by ~2e-6:
+// the worst cell (the lag-0 power, whose value is the mean power) measured
+// 6.4e-6 of the mean power at 57- and 64-stage chunks (C2, C5), 5.1e-6 at 43
+// and 4.3-4.7e-6 at 32 (C5, C4), against the 1e-5 cell tolerance
+// (tools/acc_probe.py).  Each drain stalls the MMAs for the TMEM read of the
+// band (C5 fold: 575 us at 32-stage chunks, 564 at 43, 553 at 64).
 int tc_drain_for(int64_t max_periods) {
     static const int knob = [] {  // CYC_TC_DRAIN=<stages> (0: none): accuracy / speed probe
         const char* e = std::getenv("CYC_TC_DRAIN");
@@ -62,7 +64,7 @@ int tc_drain_for(int64_t max_periods) {
     if (knob >= 0) return knob;
     const int64_t ms = (max_periods + 15) / 16;
     if (ms <= 64) return 0;
-    const int64_t nc = (ms + 31) / 32;
+    const int64_t nc = (ms + 47) / 48;
     return (int)((ms + nc - 1) / nc);
 }
 

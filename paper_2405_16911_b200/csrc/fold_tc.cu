@@ -763,38 +763,56 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
             const CUtensorMap* ym = &D.ymap[tile.seg];
             const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
             const int xatom = (int)(r0 + d) / 32, yatom = (int)r0 / 32;
+            // ring slot and phase by counters: an integer division by the
+            // run-time ring depth in these loops costs the MMA issue enough to
+            // starve the tensor pipe (tools/exp/tc_pipe.cu: 128 -> 174 cycles per MMA)
+            int s = 0;
+            uint32_t ph = 0;
             for (int it = 0; it < nst; ++it) {
-                const int s = it % NPL;
-                if (it >= NPL) mbar_wait(&planefree[s], ((it / NPL) - 1) & 1);
+                if (it >= NPL) mbar_wait(&planefree[s], ph ^ 1u);
                 TC_MARK(0, it);
                 const uint32_t st = su32(ring + s * slot);
                 const int row = row0 + it * TKB;
 #ifdef TC_ABL_NO_TMA  // ablation (diagnostic builds): stages after the first ring reuse stale data
                 if (it >= NPL) {
                     mbar_arrive(&full[s]);
+                    if (++s == NPL) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
                     continue;
                 }
 #endif
                 mbar_expect_tx(&full[s], slot);
                 tma_4d(st, xm, row, xatom, &full[s]);
                 if (!self) tma_4d(st + 2 * XPLANE, ym, row, yatom, &full[s]);
+                if (++s == NPL) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             int j = off, k = 0;  // stage within the accumulation chunk, drains so far
+            int s = 0;
+            uint32_t ph = 0;
+            if (nst > 0) mbar_wait(&full[0], 0u);
             for (int it = 0; it < nst; ++it, ++j) {
-                const int s = it % NPL;
                 if (j == DRAIN) j = 0;
-                mbar_wait(&full[s], (it / NPL) & 1);
                 TC_MARK(3, it);
                 if (j == 0 && it > 0) mbar_wait(&drain_free, (uint32_t)(k++) & 1u);
                 TC_MARK(1, it);
                 const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                const int sn = s + 1 == NPL ? 0 : s + 1;
+                const uint32_t phn = s + 1 == NPL ? ph ^ 1u : ph;
 #ifdef TC_ABL_NO_MMA  // ablation (diagnostic builds): stages are released without MMAs
+                if (it + 1 < nst) mbar_wait(&full[sn], phn);
                 mbar_arrive(&planefree[s]);
                 if (j == DRAIN - 1 || it == nst - 1) mbar_arrive(&chunk_done);
+                s = sn;
+                ph = phn;
                 continue;
 #endif
                 // atom a of a window: hi at (2a) ATOM, lo at (2a + 1) ATOM -- the
@@ -812,9 +830,16 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                     mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
                     mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
                 }
+                // the next stage's barrier is checked while this stage's last
+                // MMAs are still queued (the tensor pipe's queue is shallow: any
+                // gap between stages longer than its work is a bubble); the
+                // commits go after it
+                if (it + 1 < nst) mbar_wait(&full[sn], phn);
                 mma_commit(&planefree[s]);
                 if (j == DRAIN - 1 || it == nst - 1) mma_commit(&chunk_done);
                 TC_MARK(2, it);
+                s = sn;
+                ph = phn;
             }
             if (nst == 0) mbar_arrive(&chunk_done);
         }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -35,7 +36,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 
 template <int MPS>
-__global__ void __launch_bounds__(576, 1) k(int nst, int idle_warps, unsigned long long* out, int fill) {
+__global__ void __launch_bounds__(576, 1) k(int nst, int idle_warps, unsigned long long* out, int fill, int exact,
+                                            int npl) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t full[8], pfree[8], never;
@@ -70,8 +72,8 @@ __global__ void __launch_bounds__(576, 1) k(int nst, int idle_warps, unsigned lo
     const uint32_t slot = 24576;
     if (warp == 0 && lane == 0) {
         for (int it = 0; it < nst; ++it) {
-            const int s = it & 7;
-            if (it >= 8) mbar_wait(&pfree[s], ((it >> 3) - 1) & 1);
+            const int s = exact >= 3 ? it % npl : it & 7;
+            if (it >= npl) mbar_wait(&pfree[s], exact >= 3 ? ((it / npl) - 1) & 1 : ((it >> 3) - 1) & 1);
             mbar_arrive(&full[s]);
         }
     } else if (warp == 1 && lane == 0) {
@@ -79,10 +81,25 @@ __global__ void __launch_bounds__(576, 1) k(int nst, int idle_warps, unsigned lo
                                ((128u >> 4) << 24);
         const long long t0 = clock64();
         for (int it = 0; it < nst; ++it) {
-            const int s = it & 7;
-            mbar_wait(&full[s], (it >> 3) & 1);
+            const int s = exact >= 3 ? it % npl : it & 7;
+            mbar_wait(&full[s], exact >= 3 ? (it / npl) & 1 : (it >> 3) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t xb = su32(sm) + (uint32_t)s * slot;
+            if (exact) {  // fold_tcp_kernel self tile (3: + runtime ring depth): atom a hi at 2a ATOM, lo at (2a+1) ATOM, y = atoms 0..1
+                constexpr uint32_t ATOM = 2048;
+                const uint32_t yb = exact != 2 ? xb : xb + 16384;  // 2: y in a separate region
+                const uint64_t dyh = desc_sw128(yb, 2 * ATOM, 1024), dyl = desc_sw128(yb + ATOM, 2 * ATOM, 1024);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint64_t dxh = desc_sw128(xb + 4 * h * ATOM, 2 * ATOM, 1024);
+                    const uint64_t dxl = desc_sw128(xb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
+                    mma_bf16(tmem + 256 * h, dyh, dxh, idesc, 1u);
+                    mma_bf16(tmem + 256 * h, dyh, dxl, idesc, 1u);
+                    mma_bf16(tmem + 256 * h, dyl, dxh, idesc, 1u);
+                }
+                mma_commit(&pfree[s]);
+                continue;
+            }
 #pragma unroll
             for (int m = 0; m < MPS / 6; ++m) {
                 const uint64_t dyh = desc_sw128(xb + 2048 * m, 4096, 1024), dyl = desc_sw128(xb + 2048 * m + 1024, 4096, 1024);
@@ -97,7 +114,7 @@ __global__ void __launch_bounds__(576, 1) k(int nst, int idle_warps, unsigned lo
             }
             mma_commit(&pfree[s]);
         }
-        mbar_wait(&pfree[(nst - 1) & 7], ((nst - 1) >> 3) & 1);
+        mbar_wait(&pfree[(nst - 1) % npl], ((nst - 1) / npl) & 1);
         if (blockIdx.x == 0) out[0] = clock64() - t0;
     } else if (warp >= 2 && warp < 2 + idle_warps) {
         // idle epilogue stand-ins: poll a barrier that completes at the end (warp 1 arrives after its loop)
@@ -118,24 +135,25 @@ __global__ void __launch_bounds__(576, 1) k(int nst, int idle_warps, unsigned lo
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-int main() {
+int main(int argc, char** argv) {
     unsigned long long* d;
     cudaMalloc(&d, 8);
     const int smem = 8 * 24576 + 1024;
     cudaFuncSetAttribute(k<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int fill = 0; fill < 2; ++fill)
+    for (int exact = 0; exact < 4; ++exact)
+    for (int fill = 1; fill < 2; ++fill)
     for (int idle : {16})
-        for (int mps : {6, 12}) {
-            const int nmma = 6144, nst = nmma / mps;
+        for (int mps : {6}) {
+            const int nmma = 6144 * (argc > 1 ? atoi(argv[1]) : 1), nst = nmma / mps;
             unsigned long long h = 0;
             for (int rep = 0; rep < 2; ++rep) {
-                if (mps == 6) k<6><<<148, 576, smem>>>(nst, idle, d, fill);
-                else k<12><<<148, 576, smem>>>(nst, idle, d, fill);
+                if (mps == 6) k<6><<<148, 576, smem>>>(nst, idle, d, fill, exact, 8);
+                else k<12><<<148, 576, smem>>>(nst, idle, d, fill, exact, 8);
                 cudaDeviceSynchronize();
             }
             cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-            printf("%s data, idle warps %2d, %2d MMAs per stage: %.1f cycles per MMA %s\n", fill ? "random" : "zero  ", idle, mps, (double)h / nmma,
+            printf("exact %d %s data, idle warps %2d, %2d MMAs per stage: %.1f cycles per MMA %s\n", exact, fill ? "random" : "zero  ", idle, mps, (double)h / nmma,
                    cudaGetErrorString(cudaGetLastError()));
         }
     return 0;
