@@ -514,10 +514,10 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
     } else if (warp == 1) {
         if (lane == 0) {
             int j = off, k = 0;  // stage within the accumulation chunk, drains so far
+            if (nst > 0) mbar_wait(&conv[0], 0u);
             for (int it = 0; it < nst; ++it, ++j) {
                 const int s = it % G::NP;
                 if (j == DRAIN) j = 0;
-                mbar_wait(&conv[s], (it / G::NP) & 1);
                 // the chunk's first MMAs overwrite the accumulator: the
                 // converters must have drained the previous chunk (drain k -> phase k)
                 if (j == 0 && it > 0) mbar_wait(&drain_free, (uint32_t)(k++) & 1u);
@@ -540,6 +540,9 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
                     mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
 #endif
                 }
+                // the next stage's planes are checked while this stage's MMAs are
+                // still queued; the commits follow (as in the planes kernel)
+                if (it + 1 < nst) mbar_wait(&conv[(it + 1) % G::NP], ((it + 1) / G::NP) & 1);
                 mma_commit(&planefree[s]);
                 if (it == nst - 1) mma_commit(&chunk_done);  // the final drain's signal
                 TC_MARK(2, it);
