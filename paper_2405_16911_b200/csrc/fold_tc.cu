@@ -402,6 +402,68 @@ __device__ __forceinline__ void tc_epilogue(uint32_t tmem, const FoldLaunch& L, 
     }
 }
 
+template <int NE>
+__device__ __forceinline__ void tc_epilogue_tile(uint32_t tmem, const FoldLaunch& L, int nst, int nchunks, int e,
+                                                 int warp, int lane, uint64_t* chunk_done, uint64_t* drain_free,
+                                                 int& gc, bool release_last, float4* part) {
+    static_assert(NE == 8 || NE == 16, "two or four epilogue warps per lane quarter");
+    constexpr int NI = 32 / NE, WQ = NE / 4;  // items per warp, warps per quarter
+    const int q = warp & 3, w = e >> 2;
+    const int m = 32 * q + lane;
+    const int r = m >> 1, a = m & 1, rp = r - 16 * q;
+    float acc[NI][32];
+#pragma unroll
+    for (int k = 0; k < NI; ++k)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[k][j] = 0.f;  // x + 0 is exact: chunk 0 adds like the rest
+    const int nc = nchunks;  // 0: an empty tile (zeros), no MMAs to wait for
+    for (int c = 0; c < nc; ++c) {
+        mbar_wait(chunk_done, (uint32_t)(gc++) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (nst > 0) {
+#pragma unroll
+            for (int k = 0; k < NI; ++k) {
+                const int item = w + WQ * k, h = item >> 2, kind = item & 3;
+                const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h);
+#pragma unroll
+                for (int jb = 0; jb < 16; jb += 8) {  // 8 column pairs per load
+#pragma unroll
+                    for (int part2 = 0; part2 < (kind ? 1 : 2); ++part2) {
+                        // merged item: chunk q for j >= r', chunk q + 4 for j < r'
+                        const int cc = kind ? q + kind : q + 4 * part2;
+                        float v[16];
+                        tmem_ld16(base + (uint32_t)(32 * cc + 2 * jb), v);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const bool use = kind || ((jb + j >= rp) == (part2 == 0));
+                            if (use) {
+                                acc[k][2 * (jb + j)] += v[2 * j];
+                                acc[k][2 * (jb + j) + 1] += v[2 * j + 1];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        // the TMEM reads complete before the MMA warp restarts the accumulator
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0 && (c + 1 < nc || release_last)) mbar_arrive(drain_free);
+    }
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        const int item = w + WQ * k, h = item >> 2, kind = item & 3;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const float p0 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j], 1);
+            const float p1 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j + 1], 1);
+            if (a != 0) continue;
+            const int t = kind ? 16 * kind + j - rp : (j - rp) & 63;
+            part[(size_t)t * TRB + 64 * h + r] = make_float4(acc[k][2 * j], acc[k][2 * j + 1], p0, p1);
+        }
+    }
+}
+
 template <bool SELF, class DESC>
 __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
     using G = TcGeo<SELF>;
@@ -710,19 +772,56 @@ static_assert(PL_SMEM <= 227 * 1024, "shared memory per CTA");
 // and its slot frees only when its MMAs complete, so the stages in flight set
 // the rate.
 
+// Per-tile geometry of the planes fold (every role derives it from the tile
+// table): 64 residues [r0, r0 + 64) x lag blocks d .. d + 127; accumulator h
+// takes the x atoms 2h .. 2h + 3 of the 192-sample window at r0 + d, both the
+// same y (A) operand.
+struct TcpTile {
+    int seg, nst, nchunks, off, ya, row0, xatom, yatom;
+    bool self;
+};
+__device__ __forceinline__ TcpTile tcp_tile(const FoldLaunch& L, const TcPlDesc& D, int t, int DRAIN) {
+    const FoldTile ft = D.tiles[t];
+    const FoldSeg& sg = D.segs[ft.seg];
+    TcpTile g;
+    g.seg = ft.seg;
+    const int64_t r0 = (int64_t)ft.rb * 64;
+    const int64_t d = (int64_t)L.lag_lo + (int64_t)ft.lb * 128;
+    // y inside the x window at an atom boundary: skip the y planes
+    g.self = sg.x == sg.y && d <= 0 && -d <= 128 && (-d) % 32 == 0;
+    g.ya = g.self ? (int)(-d) / 32 : 0;
+    g.nst = (int)((ft.p1 - ft.p0) + TKB - 1) / TKB;
+    g.off = L.tc_drain > 0 ? (t % 4) * (DRAIN / 4) : 0;  // staggered drains
+    g.nchunks = g.nst > 0 ? (g.nst - 1 + g.off) / DRAIN + 1 : 0;
+    g.row0 = (int)(ft.p0 - D.p_base[ft.seg]);
+    g.xatom = (int)(r0 + d) / 32;
+    g.yatom = (int)r0 / 32;
+    return g;
+}
+
+// Persistent planes fold: one CTA per SM walks the tiles t = blockIdx.x,
+// + gridDim.x, ... (range-major order, so the SMs work on one period range at
+// a time and share the planes through L2).  The stage ring, the chunk barriers
+// and the TMEM accumulator carry over from tile to tile: the producer loads the
+// next tile's first stages while the last ones are multiplied, and the MMA
+// warp starts the next tile as soon as the epilogue warps have read the
+// accumulator out of TMEM -- the tile's partial stores, its final drain wait
+// and the prologue (TMEM allocation, barrier set-up, first loads) no longer
+// idle the tensor pipe between tiles (they cost ~12 % of a 128-stage C5 tile).
+// Stage slots are uniform (x hi/lo + 2 y atoms, 32 KB); self tiles leave the
+// y part unused.
 template <class DESC>
 __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t full[NPL_MAX], planefree[NPL_MAX], chunk_done, drain_free;
+    constexpr uint32_t SLOT = 2 * XPLANE + 2 * 2 * ATOM;  // 32 KB
+    constexpr int NPL = PL_RING / (int)SLOT;               // stages in flight
+    static_assert(NPL >= 2, "ring depth");
+    __shared__ uint64_t full[NPL], planefree[NPL], chunk_done, drain_free;
     __shared__ uint32_t tmem_s;
-    __shared__ FoldTile s_tile;
-    __shared__ FoldSeg s_seg;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        s_tile = D.tiles[blockIdx.x];
-        s_seg = D.segs[s_tile.seg];
-        for (int s = 0; s < NPL_MAX; ++s) {
+        for (int s = 0; s < NPL; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&planefree[s], 1);
         }
@@ -740,114 +839,124 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
     const uint32_t tmem = tmem_s;
     TC_TIME(0);
     if (threadIdx.x == 0) TC_MARK(7, 0);
-    const FoldTile& tile = s_tile;
-    // 64 residues [r0, r0 + 64) x lag blocks d .. d + 127: accumulator h takes
-    // the x atoms 2h .. 2h + 3 of the 192-sample window at r0 + d, both the
-    // same y (A) operand
-    const int64_t r0 = (int64_t)tile.rb * 64;
-    const int64_t d = (int64_t)L.lag_lo + (int64_t)tile.lb * 128;
-    // y inside the x window at an atom boundary: skip the y planes
-    const bool self = s_seg.x == s_seg.y && d <= 0 && -d <= 128 && (-d) % 32 == 0;
-    const int ya = self ? (int)(-d) / 32 : 0;
-    const int nper = (int)(tile.p1 - tile.p0);
-    const int nst = (nper + TKB - 1) / TKB;
     const int DRAIN = L.tc_drain > 0 ? L.tc_drain : (1 << 30);
-    const int off = L.tc_drain > 0 ? (int)(blockIdx.x % 4) * (DRAIN / 4) : 0;  // staggered drains
-    const int nchunks = nst > 0 ? (nst - 1 + off) / DRAIN + 1 : 0;
-    const uint32_t slot = self ? 2 * XPLANE : 2 * XPLANE + 2 * 2 * ATOM;  // stage bytes: x (+ 2 y atoms)
-    const int NPL = PL_RING / (int)slot;                  // stages in flight
+    const int nt = L.n_tiles;
     if (warp == 0) {
         if (lane == 0) {
             // one 4-D TMA per window: {64 bf16, 16 periods, hi/lo, atoms} lands
             // as [atom][hi, lo][16 rows][128 B] (one instruction instead of one
             // per 2 KB atom column: a single issuing thread spends ~100 cycles
             // per box, tools/exp/tma4d.cu: 844 -> 356 cycles per 24 KB stage)
-            const CUtensorMap* xm = &D.xmap[tile.seg];
-            const CUtensorMap* ym = &D.ymap[tile.seg];
-            const int row0 = (int)(tile.p0 - D.p_base[tile.seg]);
-            const int xatom = (int)(r0 + d) / 32, yatom = (int)r0 / 32;
-            // ring slot and phase by counters: an integer division by the
-            // run-time ring depth in these loops costs the MMA issue enough to
-            // starve the tensor pipe (tools/exp/tc_pipe.cu: 128 -> 174 cycles per MMA)
-            int s = 0;
-            uint32_t ph = 0;
-            for (int it = 0; it < nst; ++it) {
-                if (it >= NPL) mbar_wait(&planefree[s], ph ^ 1u);
-                TC_MARK(0, it);
-                const uint32_t st = su32(ring + s * slot);
-                const int row = row0 + it * TKB;
+            int s = 0, filled = 0;  // ring slot by counters (no run-time division in these loops:
+            uint32_t ph = 0;        // tools/exp/tc_pipe.cu, 128 -> 174 cycles per MMA with one)
+            for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+                const TcpTile g = tcp_tile(L, D, t, DRAIN);
+                const CUtensorMap* xm = &D.xmap[g.seg];
+                const CUtensorMap* ym = &D.ymap[g.seg];
+                const bool first = t == (int)blockIdx.x;
+                for (int it = 0; it < g.nst; ++it) {
+                    if (filled >= NPL) mbar_wait(&planefree[s], ph ^ 1u);
+                    if (first) TC_MARK(0, it);
+                    const uint32_t st = su32(ring + s * SLOT);
+                    const int row = g.row0 + it * TKB;
 #ifdef TC_ABL_NO_TMA  // ablation (diagnostic builds): stages after the first ring reuse stale data
-                if (it >= NPL) {
-                    mbar_arrive(&full[s]);
+                    if (filled >= NPL) {
+                        mbar_arrive(&full[s]);
+                    } else
+#endif
+                    {
+                        mbar_expect_tx(&full[s], g.self ? 2 * XPLANE : SLOT);
+                        tma_4d(st, xm, row, g.xatom, &full[s]);
+                        if (!g.self) tma_4d(st + 2 * XPLANE, ym, row, g.yatom, &full[s]);
+                    }
+                    ++filled;
                     if (++s == NPL) {
                         s = 0;
                         ph ^= 1u;
                     }
-                    continue;
-                }
-#endif
-                mbar_expect_tx(&full[s], slot);
-                tma_4d(st, xm, row, xatom, &full[s]);
-                if (!self) tma_4d(st + 2 * XPLANE, ym, row, yatom, &full[s]);
-                if (++s == NPL) {
-                    s = 0;
-                    ph ^= 1u;
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            int j = off, k = 0;  // stage within the accumulation chunk, drains so far
-            int s = 0;
+            int s = 0, k = 0;  // ring slot; drains so far (every chunk but the CTA's first waits for one)
             uint32_t ph = 0;
-            if (nst > 0) mbar_wait(&full[0], 0u);
-            for (int it = 0; it < nst; ++it, ++j) {
-                if (j == DRAIN) j = 0;
-                TC_MARK(3, it);
-                if (j == 0 && it > 0) mbar_wait(&drain_free, (uint32_t)(k++) & 1u);
-                TC_MARK(1, it);
-                const uint32_t acc = (it > 0 && j != 0) ? 1u : 0u;
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const int sn = s + 1 == NPL ? 0 : s + 1;
-                const uint32_t phn = s + 1 == NPL ? ph ^ 1u : ph;
-#ifdef TC_ABL_NO_MMA  // ablation (diagnostic builds): stages are released without MMAs
-                if (it + 1 < nst) mbar_wait(&full[sn], phn);
-                mbar_arrive(&planefree[s]);
-                if (j == DRAIN - 1 || it == nst - 1) mbar_arrive(&chunk_done);
-                s = sn;
-                ph = phn;
-                continue;
-#endif
-                // atom a of a window: hi at (2a) ATOM, lo at (2a + 1) ATOM -- the
-                // operands' MN-atom stride (LBO) is 2 ATOM
-                const uint32_t xb = su32(ring + s * slot);
-                const uint32_t yb = self ? xb + 2 * ya * ATOM : xb + 2 * XPLANE;
-                const uint64_t dyh = sw128_desc(yb, 2 * ATOM, 1024);
-                const uint64_t dyl = sw128_desc(yb + ATOM, 2 * ATOM, 1024);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint64_t dxh = sw128_desc(xb + 4 * h * ATOM, 2 * ATOM, 1024);
-                    const uint64_t dxl = sw128_desc(xb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
-                    const uint32_t dt = tmem + 256 * h;
-                    mma_bf16(dt, dyh, dxh, TC_IDESC, acc);
-                    mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
-                    mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
+            bool started = false, waited_first = false;
+            for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+                const TcpTile g = tcp_tile(L, D, t, DRAIN);
+                const bool first = t == (int)blockIdx.x;
+                if (g.nst == 0) continue;
+                bool last_tile = true;  // no later tile of this CTA has stages
+                for (int t2 = t + (int)gridDim.x; t2 < nt && last_tile; t2 += gridDim.x)
+                    last_tile = tcp_tile(L, D, t2, DRAIN).nst == 0;
+                if (!waited_first) {
+                    mbar_wait(&full[0], 0u);
+                    waited_first = true;
                 }
-                // the next stage's barrier is checked while this stage's last
-                // MMAs are still queued (the tensor pipe's queue is shallow: any
-                // gap between stages longer than its work is a bubble); the
-                // commits go after it
-                if (it + 1 < nst) mbar_wait(&full[sn], phn);
-                mma_commit(&planefree[s]);
-                if (j == DRAIN - 1 || it == nst - 1) mma_commit(&chunk_done);
-                TC_MARK(2, it);
-                s = sn;
-                ph = phn;
+                int j = g.off;
+                for (int it = 0; it < g.nst; ++it, ++j) {
+                    if (j == DRAIN) j = 0;
+                    if (first) TC_MARK(3, it);
+                    // a chunk's first MMAs overwrite the accumulator: the epilogue
+                    // warps must have read the previous chunk out of TMEM
+                    const bool chunk_start = it == 0 || j == 0;
+                    if (chunk_start && started) mbar_wait(&drain_free, (uint32_t)(k++) & 1u);
+                    started = true;
+                    if (first) TC_MARK(1, it);
+                    const uint32_t acc = chunk_start ? 0u : 1u;
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const int sn = s + 1 == NPL ? 0 : s + 1;
+                    const uint32_t phn = s + 1 == NPL ? ph ^ 1u : ph;
+                    const bool more = it + 1 < g.nst || !last_tile;  // another stage follows in this CTA
+                    const bool chunk_end = j == DRAIN - 1 || it == g.nst - 1;
+#ifdef TC_ABL_NO_MMA  // ablation (diagnostic builds): stages are released without MMAs
+                    if (more) mbar_wait(&full[sn], phn);
+                    mbar_arrive(&planefree[s]);
+                    if (chunk_end) mbar_arrive(&chunk_done);
+                    s = sn;
+                    ph = phn;
+                    continue;
+#endif
+                    // atom a of a window: hi at (2a) ATOM, lo at (2a + 1) ATOM -- the
+                    // operands' MN-atom stride (LBO) is 2 ATOM
+                    const uint32_t xb = su32(ring + s * SLOT);
+                    const uint32_t yb = g.self ? xb + 2 * g.ya * ATOM : xb + 2 * XPLANE;
+                    const uint64_t dyh = sw128_desc(yb, 2 * ATOM, 1024);
+                    const uint64_t dyl = sw128_desc(yb + ATOM, 2 * ATOM, 1024);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint64_t dxh = sw128_desc(xb + 4 * h * ATOM, 2 * ATOM, 1024);
+                        const uint64_t dxl = sw128_desc(xb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
+                        const uint32_t dt = tmem + 256 * h;
+                        mma_bf16(dt, dyh, dxh, TC_IDESC, acc);
+                        mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
+                        mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
+                    }
+                    // the next stage's barrier is checked while this stage's last
+                    // MMAs are still queued (the tensor pipe's queue is shallow: any
+                    // gap between stages longer than its work is a bubble); the
+                    // commits go after it
+                    if (more) mbar_wait(&full[sn], phn);
+                    mma_commit(&planefree[s]);
+                    if (chunk_end) mma_commit(&chunk_done);
+                    if (first) TC_MARK(2, it);
+                    s = sn;
+                    ph = phn;
+                }
             }
-            if (nst == 0) mbar_arrive(&chunk_done);
         }
     } else {
-        tc_epilogue<TPE>(tmem, L, nst, nchunks, warp - 2, warp, lane, &chunk_done, &drain_free);
+        // epilogue warps: per tile, every chunk's accumulator is added into
+        // registers (IEEE fp32) as soon as its MMAs completed; the MMA warp is
+        // released (drain_free) before the tile's partials are stored
+        const int e = warp - 2;
+        int gc = 0;  // chunks drained so far (chunk_done phase)
+        for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+            const TcpTile g = tcp_tile(L, D, t, DRAIN);
+            const bool last_tile = t + (int)gridDim.x >= nt;
+            tc_epilogue_tile<TPE>(tmem, L, g.nst, g.nchunks, e, warp, lane, &chunk_done, &drain_free, gc, !last_tile,
+                                  reinterpret_cast<float4*>(L.partials) + (size_t)t * 64 * TRB);
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -1323,7 +1432,10 @@ void launch_fold_tcp(const FoldLaunch& L, const TcPlDesc& D, const FoldGroup* gr
         R.slot[g] = D.segs[groups[g].seg].slot;
     }
     if (ev0) record_event(ev0, st);
-    fold_tcp_kernel<TcPlDesc><<<L.n_tiles, TPT, PL_SMEM, st>>>(L, D);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    fold_tcp_kernel<TcPlDesc><<<std::min(L.n_tiles, sms), TPT, PL_SMEM, st>>>(L, D);
     if (ev1) record_event(ev1, st);
     fold_tc_reduce_kernel<FI_GROUPS><<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
 }
