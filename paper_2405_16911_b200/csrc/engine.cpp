@@ -1253,7 +1253,8 @@ Status Engine::fold_tc_planes(const std::vector<FoldSeg>& tsegs, std::vector<TcG
         const int lags_in = std::max(0, std::min(128, T_ - 128 * gr.lb));
         launch_flops += 8.0 * lags_in * 64.0 * (double)(gr.p1 - gr.p0);
     }
-    for (const auto& t : tiles) exec += (double)ceil_div(t.p1 - t.p0, 16) * 6.0 * 2.0 * 128 * 256 * 16;
+    // executed per stage: 3 split products x (N = 256 + N = 128) columns of M = 128 rows, K = 16
+    for (const auto& t : tiles) exec += (double)ceil_div(t.p1 - t.p0, 16) * 3.0 * 2.0 * 128 * 384 * 16;
     if (prof_) {
         ProfRec r{get_event_timed(), get_event_timed(), launch_flops, exec, true};
         launch_fold_tcp(L, D, fg.data(), cs_, r.a, r.b);

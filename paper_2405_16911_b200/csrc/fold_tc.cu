@@ -144,6 +144,8 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 // instruction descriptor: D f32, A/B bf16, both MN-major, M = 128, N = 256
 constexpr uint32_t TC_IDESC =
     (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t TC_IDESC_N128 =
+    (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -334,74 +336,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
 
 // Dedicated epilogue warps of the planes kernel (NE = 16: four per TMEM lane
 // quarter; or 8): the chunks' sums stay in registers -- fp32 adds, round to
-// nearest -- and the band is stored once per tile.  Lane m = 2r + a of
-// quarter q (r = 16q + r') owns lags t = 0..63 of residue r, component pair
-// a, of both accumulators: 4 items of 16 column pairs per accumulator, item
-// k = 1..3 the column chunk cc = q + k (t = 16k + j - r'), item 0 the chunks
-// q (j >= r') and q + 4 (j < r') merged (t = (j - r') mod 64).  Warp w of the
-// quarter's NE/4 warps holds items w, w + NE/4, ... (h = item / 4).
-template <int NE>
-__device__ __forceinline__ void tc_epilogue(uint32_t tmem, const FoldLaunch& L, int nst, int nchunks, int e, int warp,
-                                            int lane, uint64_t* chunk_done, uint64_t* drain_free) {
-    static_assert(NE == 8 || NE == 16, "two or four epilogue warps per lane quarter");
-    constexpr int NI = 32 / NE, WQ = NE / 4;  // items per warp, warps per quarter
-    const int q = warp & 3, w = e >> 2;
-    const int m = 32 * q + lane;
-    const int r = m >> 1, a = m & 1, rp = r - 16 * q;
-    float acc[NI][32];
-#pragma unroll
-    for (int k = 0; k < NI; ++k)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[k][j] = 0.f;  // x + 0 is exact: chunk 0 adds like the rest
-    const int nc = nchunks > 0 ? nchunks : 1;
-    for (int c = 0; c < nc; ++c) {
-        mbar_wait(chunk_done, (uint32_t)c & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (nst > 0) {
-#pragma unroll
-            for (int k = 0; k < NI; ++k) {
-                const int item = w + WQ * k, h = item >> 2, kind = item & 3;
-                const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h);
-#pragma unroll
-                for (int jb = 0; jb < 16; jb += 8) {  // 8 column pairs per load
-#pragma unroll
-                    for (int part2 = 0; part2 < (kind ? 1 : 2); ++part2) {
-                        // merged item: chunk q for j >= r', chunk q + 4 for j < r'
-                        const int cc = kind ? q + kind : q + 4 * part2;
-                        float v[16];
-                        tmem_ld16(base + (uint32_t)(32 * cc + 2 * jb), v);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const bool use = kind || ((jb + j >= rp) == (part2 == 0));
-                            if (use) {
-                                acc[k][2 * (jb + j)] += v[2 * j];
-                                acc[k][2 * (jb + j) + 1] += v[2 * j + 1];
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        // the TMEM reads complete before the MMA warp restarts the accumulator
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0 && c + 1 < nc) mbar_arrive(drain_free);
-    }
-    float4* part = reinterpret_cast<float4*>(L.partials) + (size_t)blockIdx.x * 64 * TRB;
-#pragma unroll
-    for (int k = 0; k < NI; ++k) {
-        const int item = w + WQ * k, h = item >> 2, kind = item & 3;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const float p0 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j], 1);
-            const float p1 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j + 1], 1);
-            if (a != 0) continue;
-            const int t = kind ? 16 * kind + j - rp : (j - rp) & 63;
-            part[(size_t)t * TRB + 64 * h + r] = make_float4(acc[k][2 * j], acc[k][2 * j + 1], p0, p1);
-        }
-    }
-}
-
+// nearest -- and the band is stored once per tile.  The accumulator is the
+// 384-column union of the tile's two lag blocks (columns 2i + b, window sample
+// i in [0, 192)); lane m = 2r + a of quarter q (r = 16q + r') owns lags
+// t' = i - r = 0..127 of residue r, component pair a: 8 items of 16 column
+// pairs, item k = 1..7 the column chunk cc = q + k (t' = 16k + j - r'), item 0
+// the chunks q (j >= r') and q + 8 (j < r') merged (t' = (j - r') mod 128).
+// Warp w of the quarter's NE/4 warps holds items w, w + NE/4, ...; lag t' is
+// stored as lag block t' / 64, offset t' % 64 (the reduce's layout).
 template <int NE>
 __device__ __forceinline__ void tc_epilogue_tile(uint32_t tmem, const FoldLaunch& L, int nst, int nchunks, int e,
                                                  int warp, int lane, uint64_t* chunk_done, uint64_t* drain_free,
@@ -423,14 +365,14 @@ __device__ __forceinline__ void tc_epilogue_tile(uint32_t tmem, const FoldLaunch
         if (nst > 0) {
 #pragma unroll
             for (int k = 0; k < NI; ++k) {
-                const int item = w + WQ * k, h = item >> 2, kind = item & 3;
-                const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(256 * h);
+                const int kind = w + WQ * k;
+                const uint32_t base = tmem + ((uint32_t)(32 * q) << 16);
 #pragma unroll
                 for (int jb = 0; jb < 16; jb += 8) {  // 8 column pairs per load
 #pragma unroll
                     for (int part2 = 0; part2 < (kind ? 1 : 2); ++part2) {
-                        // merged item: chunk q for j >= r', chunk q + 4 for j < r'
-                        const int cc = kind ? q + kind : q + 4 * part2;
+                        // merged item: chunk q for j >= r', chunk q + 8 for j < r'
+                        const int cc = kind ? q + kind : q + 8 * part2;
                         float v[16];
                         tmem_ld16(base + (uint32_t)(32 * cc + 2 * jb), v);
 #pragma unroll
@@ -452,14 +394,14 @@ __device__ __forceinline__ void tc_epilogue_tile(uint32_t tmem, const FoldLaunch
     }
 #pragma unroll
     for (int k = 0; k < NI; ++k) {
-        const int item = w + WQ * k, h = item >> 2, kind = item & 3;
+        const int kind = w + WQ * k;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const float p0 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j], 1);
             const float p1 = __shfl_xor_sync(0xffffffffu, acc[k][2 * j + 1], 1);
             if (a != 0) continue;
-            const int t = kind ? 16 * kind + j - rp : (j - rp) & 63;
-            part[(size_t)t * TRB + 64 * h + r] = make_float4(acc[k][2 * j], acc[k][2 * j + 1], p0, p1);
+            const int t = kind ? 16 * kind + j - rp : (j - rp) & 127;
+            part[(size_t)(t & 63) * TRB + 64 * (t >> 6) + r] = make_float4(acc[k][2 * j], acc[k][2 * j + 1], p0, p1);
         }
     }
 }
@@ -773,9 +715,8 @@ static_assert(PL_SMEM <= 227 * 1024, "shared memory per CTA");
 // the rate.
 
 // Per-tile geometry of the planes fold (every role derives it from the tile
-// table): 64 residues [r0, r0 + 64) x lag blocks d .. d + 127; accumulator h
-// takes the x atoms 2h .. 2h + 3 of the 192-sample window at r0 + d, both the
-// same y (A) operand.
+// table): 64 residues [r0, r0 + 64) x lags d .. d + 127; the accumulator
+// takes the 192-sample x window at r0 + d (6 atoms) against the y (A) operand.
 struct TcpTile {
     int seg, nst, nchunks, off, ya, row0, xatom, yatom;
     bool self;
@@ -923,14 +864,19 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                     const uint32_t yb = g.self ? xb + 2 * g.ya * ATOM : xb + 2 * XPLANE;
                     const uint64_t dyh = sw128_desc(yb, 2 * ATOM, 1024);
                     const uint64_t dyl = sw128_desc(yb + ATOM, 2 * ATOM, 1024);
+                    // the 192-sample window once: atoms 0..3 (N = 256) into TMEM
+                    // columns 0..255, atoms 4..5 (N = 128) into 256..383 -- the
+                    // union of the two lag blocks' 128-sample windows (3/4 of the
+                    // MMA work of two N = 256 products)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const uint64_t dxh = sw128_desc(xb + 4 * h * ATOM, 2 * ATOM, 1024);
-                        const uint64_t dxl = sw128_desc(xb + (4 * h + 1) * ATOM, 2 * ATOM, 1024);
+                        const uint64_t dxh = sw128_desc(xb + 8 * h * ATOM, 2 * ATOM, 1024);
+                        const uint64_t dxl = sw128_desc(xb + (8 * h + 1) * ATOM, 2 * ATOM, 1024);
                         const uint32_t dt = tmem + 256 * h;
-                        mma_bf16(dt, dyh, dxh, TC_IDESC, acc);
-                        mma_bf16(dt, dyh, dxl, TC_IDESC, 1u);
-                        mma_bf16(dt, dyl, dxh, TC_IDESC, 1u);
+                        const uint32_t id = h ? TC_IDESC_N128 : TC_IDESC;
+                        mma_bf16(dt, dyh, dxh, id, acc);
+                        mma_bf16(dt, dyh, dxl, id, 1u);
+                        mma_bf16(dt, dyl, dxh, id, 1u);
                     }
                     // the next stage's barrier is checked while this stage's last
                     // MMAs are still queued (the tensor pipe's queue is shallow: any
