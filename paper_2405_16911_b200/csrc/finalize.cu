@@ -23,6 +23,19 @@ namespace {
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// FFT element types: fp64 (double2) or fp32 (float2, inputs combined in fp64
+// and rounded once)
+template <class V>
+__device__ __forceinline__ V to_v(double2 a);
+template <>
+__device__ __forceinline__ double2 to_v<double2>(double2 a) { return a; }
+template <>
+__device__ __forceinline__ float2 to_v<float2>(double2 a) { return make_float2((float)a.x, (float)a.y); }
+__device__ __forceinline__ double2 to_d(double2 a) { return a; }
+__device__ __forceinline__ double2 to_d(float2 a) { return make_double2(a.x, a.y); }
 
 __device__ __forceinline__ double2 combine(const double* s, int flag_bit) {  // s: 4 values
     // s = (c0, c1, c2, c3) = (sum xr*yr, sum xi*yr, sum xr*yi, sum xi*yi)
@@ -37,31 +50,55 @@ __device__ __forceinline__ double2 combine(const double* s, int flag_bit) {  // 
 // sh = log2(Pf) - 3; the buffer holds Pf + Pf/16 + 8 points.
 __device__ __forceinline__ int padi(int i, int sh) { return i + (i >> 4) + (i >> sh); }
 
+// b * e^{-j pi e / 8}, e = 1..7 (e = 4: -j, exact)
+template <class V>
+__device__ __forceinline__ V rot16(V b, int e) {
+    if (e == 4) {
+        V r;
+        r.x = b.y;
+        r.y = -b.x;
+        return r;
+    }
+    constexpr double C[8] = {1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508977, 0.0,
+                             -0.38268343236508977, -0.70710678118654752, -0.92387953251128674};
+    constexpr double S[8] = {0.0, 0.38268343236508977, 0.70710678118654752, 0.92387953251128674, 1.0,
+                             0.92387953251128674, 0.70710678118654752, 0.38268343236508977};
+    V w;
+    w.x = (decltype(b.x))C[e];
+    w.y = -(decltype(b.x))S[e];
+    return cmul(b, w);
+}
+
 // One pass of LOG2R radix-2 DIT levels (halves h, 2h, .., 2^(LOG2R-1) h): each
 // thread takes groups of R = 2^LOG2R points base + pos + k h (k < R) into
 // registers and runs the levels there -- exactly the radix-2 butterflies
 // (v = b w, a + v, a - v) with the level's twiddles, one barrier per pass.
-template <int LOG2R>
-__device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int Pf, int h, int sh) {
+// Level l's twiddle W^{(pos + m h) Pf / (2^{l+1} h)} = b_l * e^{-j pi m / 2^l}
+// with b_l = tp[l h + pos] from the pass's own table (consecutive threads read
+// consecutive entries: no bank conflicts -- one shared table indexed at
+// stride Pf / (2^{l+1} h) was 6-way conflicted, ncu) and a 16th root of unity.
+template <int LOG2R, class V>
+__device__ __forceinline__ void fft_pass(V* buf, const V* tp, int Pf, int h, int sh) {
     constexpr int R = 1 << LOG2R;
     for (int g = threadIdx.x; g < Pf / R; g += blockDim.x) {
         const int base = (g / h) * (R * h), pos = g - (g / h) * h;
-        double2 v[R];
+        V v[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) v[k] = buf[padi(base + pos + k * h, sh)];
 #pragma unroll
         for (int l = 0; l < LOG2R; ++l) {
-            const int hs = h << l;       // half size of this level
-            const int ts = Pf / (2 * hs);  // twiddle stride
+            const V b0 = tp[l * h + pos];
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 if (k & (1 << l)) continue;
-                const int j = pos + (k & ((1 << l) - 1)) * h;  // position in the half block
-                const double2 w = tw[j * ts];
-                const double2 b = v[k + (1 << l)];
-                const double2 t = cmul(b, w);
-                v[k + (1 << l)] = make_double2(v[k].x - t.x, v[k].y - t.y);
-                v[k] = make_double2(v[k].x + t.x, v[k].y + t.y);
+                const int m = k & ((1 << l) - 1);
+                const V w = m == 0 ? b0 : rot16(b0, m << (3 - l));
+                const V b = v[k + (1 << l)];
+                const V t = cmul(b, w);
+                v[k + (1 << l)].x = v[k].x - t.x;
+                v[k + (1 << l)].y = v[k].y - t.y;
+                v[k].x += t.x;
+                v[k].y += t.y;
             }
         }
 #pragma unroll
@@ -70,22 +107,50 @@ __device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int Pf
     __syncthreads();
 }
 
+// The pass sequence of a row (shared by the kernel and the host's shared-memory
+// size): radix-16 passes when the block has enough groups of 16 (else radix-4),
+// then one pass of the remaining levels; fn(log2r, h) per pass.
+template <class F>
+__host__ __device__ inline void fft_passes(int log2Pf, int nthreads, F fn) {
+    int h = 1, lv = 0;
+    const int r = nthreads * 16 <= (1 << log2Pf) ? 4 : 2;
+    for (; lv + r <= log2Pf; lv += r, h <<= r) fn(r, h);
+    if (log2Pf > lv) fn(log2Pf - lv, h);
+}
+// entries of the per-pass twiddle tables: sum over passes of log2r * h
+__host__ __device__ inline int fft_tw_entries(int log2Pf, int nthreads) {
+    int n = 0;
+    fft_passes(log2Pf, nthreads, [&](int r, int h) { n += r * h; });
+    return n;
+}
+
 // One CTA per (row, flag): the row's combined
 // correlations in bit-reversed order, then radix-16 passes (four radix-2
 // levels each, in registers) and a final pass of the remaining levels.
-__global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
-    extern __shared__ double2 buf[];  // Pf + Pf/16 + 8 points (padded), then Pf/2 twiddles
-    __shared__ FinalRow s_row;        // descriptors may be in mapped host memory: read once
+template <class V>
+__global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
+    extern __shared__ __align__(16) uint8_t fft_smem[];
+    V* buf = reinterpret_cast<V*>(fft_smem);  // Pf + Pf/16 + 8 points (padded), then Pf/2 twiddles
+    __shared__ FinalRow s_row;                // descriptors may be in mapped host memory: read once
     const int Pf = L.Pf;
     const int sh = max(log2Pf - 3, 1);
-    double2* tw = buf + Pf + (Pf >> 4) + 8;
+    V* tw = buf + Pf + (Pf >> 4) + 8;  // per-pass twiddle tables, pass after pass
     // grid (n_rows * n_flag_tables): the flag tables of a row are adjacent CTAs,
     // so the second read of the row's S comes from L2
     const int nflag = (L.flags == 3) ? 2 : 1;
     const int row_i = blockIdx.x / nflag, fi = blockIdx.x % nflag;  // fi: index among requested flags
     if (threadIdx.x == 0) s_row = L.rows[row_i];
     if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0) *L.shift_ctr += L.shift_inc;
-    for (int k = threadIdx.x; k < (Pf >> 1); k += blockDim.x) tw[k] = __ldg(L.tw + k);
+    {
+        int off = 0;
+        fft_passes(log2Pf, blockDim.x, [&](int r, int h) {
+            for (int i = threadIdx.x; i < r * h; i += blockDim.x) {
+                const int l = i / h, pos = i - l * h;
+                tw[off + i] = to_v<V>(__ldg(L.tw + (size_t)pos * (Pf / (2 * (h << l)))));
+            }
+            off += r * h;
+        });
+    }
     __syncthreads();
     const FinalRow row = s_row;
     const int flag_bit = (L.flags == 2) ? 1 : fi;
@@ -121,27 +186,28 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
             if (r >= Pf) continue;
             const int rev = (int)(__brev((unsigned)r) >> (32 - log2Pf));
             const double c[4] = {v[u][0].x, v[u][0].y, v[u][1].x, v[u][1].y};
-            buf[padi(rev, sh)] = combine(c, flag_bit);
+            buf[padi(rev, sh)] = to_v<V>(combine(c, flag_bit));
         }
     }
     __syncthreads();
-    int h = 1, lv = 0;
-    if (blockDim.x * 16 <= Pf) {  // enough groups of 16 for the block: radix-16 passes
-        for (; lv + 4 <= log2Pf; lv += 4, h <<= 4) fft_pass<4>(buf, tw, Pf, h, sh);
-    } else {  // short rows: radix-4 passes keep every thread busy
-        for (; lv + 2 <= log2Pf; lv += 2, h <<= 2) fft_pass<2>(buf, tw, Pf, h, sh);
-    }
-    switch (log2Pf - lv) {
-        case 3: fft_pass<3>(buf, tw, Pf, h, sh); break;
-        case 2: fft_pass<2>(buf, tw, Pf, h, sh); break;
-        case 1: fft_pass<1>(buf, tw, Pf, h, sh); break;
-        default: break;
+    {
+        int off = 0;
+        fft_passes(log2Pf, blockDim.x, [&](int r, int h) {
+            const V* tp = tw + off;
+            switch (r) {
+                case 4: fft_pass<4>(buf, tp, Pf, h, sh); break;
+                case 3: fft_pass<3>(buf, tp, Pf, h, sh); break;
+                case 2: fft_pass<2>(buf, tp, Pf, h, sh); break;
+                default: fft_pass<1>(buf, tp, Pf, h, sh); break;
+            }
+            off += r * h;
+        });
     }
     const double sc = L.row_scale ? L.row_scale[row.out_block] : L.scale_default;
     if (rec_pre) {
         const int a = threadIdx.x;
         if (a >= L.A) return;
-        const double2 v0 = buf[padi(L.bins[a], sh)];
+        const double2 v0 = to_d(buf[padi(L.bins[a], sh)]);
         const double2 v = make_double2(v0.x * sc, v0.y * sc);
         const size_t o = (size_t)(out - L.out) + (size_t)a * L.stride_a;
         rR.x = L.rec_decay * rR.x + v.x;
@@ -158,7 +224,7 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
     if (L.rec_R) {
         const size_t o0 = (size_t)(out - L.out);
         for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
-            const double2 v0 = buf[padi(L.bins[a], sh)];
+            const double2 v0 = to_d(buf[padi(L.bins[a], sh)]);
             const double2 v = make_double2(v0.x * sc, v0.y * sc);
             const size_t o = o0 + (size_t)a * L.stride_a;
             double2 r = L.rec_R[o], c = L.rec_coh[o];
@@ -175,7 +241,7 @@ __global__ void __launch_bounds__(512) finalize_fft_kernel(FinalizeLaunch L, int
         return;
     }
     for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
-        const double2 v = buf[padi(L.bins[a], sh)];
+        const double2 v = to_d(buf[padi(L.bins[a], sh)]);
         out[(size_t)a * L.stride_a] = make_double2(v.x * sc, v.y * sc);
     }
 }
@@ -244,20 +310,44 @@ __global__ void __launch_bounds__(DFT_T) finalize_dft_kernel(FinalizeLaunch L) {
 
 }  // namespace
 
+// FFT arithmetic: fp32 by default -- S is combined per flag in fp64 and
+// rounded once, the transform's error (~1e-7 of the row's norm) sits two
+// orders below the fold's and the 8192-point buffers fit two CTAs per SM
+// (one streams its row while the other transforms); CYC_FFT64=1: fp64.
+static bool fft64() {
+    static const bool on = [] {
+        const char* e = std::getenv("CYC_FFT64");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+
+template <class V>
+static int fft_smem_max() {  // Pf = 8192 at 512 threads: the largest row
+    return (8192 + 512 + 8 + fft_tw_entries(13, 512)) * (int)sizeof(V);
+}
+
+template <class V>
+static void launch_fft(const FinalizeLaunch& L, cudaStream_t st, int nflag) {
+    int lg = 0;
+    while ((1 << lg) < L.Pf) ++lg;
+    // Pf = 8192: 512 threads x radix-16 groups; shorter rows: Pf / 4 threads x radix-4
+    const int nt = L.Pf >= 8192 ? 512 : std::min(512, std::max(32, L.Pf / 4));
+    const size_t smem = ((size_t)L.Pf + L.Pf / 16 + 8 + fft_tw_entries(lg, nt)) * sizeof(V);
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set))
+        cudaFuncSetAttribute(finalize_fft_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, fft_smem_max<V>());
+    finalize_fft_kernel<V><<<(unsigned)(L.n_rows * nflag), nt, smem, st>>>(L, lg);
+}
+
 void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
     if (L.n_rows == 0) return;
     const int nflag = L.flags == 3 ? 2 : 1;
     if (L.use_fft) {
-        int lg = 0;
-        while ((1 << lg) < L.Pf) ++lg;
-        const size_t smem = ((size_t)L.Pf + L.Pf / 16 + 8 + L.Pf / 2) * sizeof(double2);
-        static std::atomic<uint64_t> attr_set{0};
-        if (first_on_device(attr_set))
-            cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (8192 + 512 + 8 + 4096) * (int)sizeof(double2));
-        // Pf = 8192: 512 threads x radix-16 groups; shorter rows: Pf / 4 threads x radix-4
-        const int nt = L.Pf >= 8192 ? 512 : std::min(512, std::max(32, L.Pf / 4));
-        finalize_fft_kernel<<<(unsigned)(L.n_rows * nflag), nt, smem, st>>>(L, lg);
+        if (fft64())
+            launch_fft<double2>(L, st, nflag);
+        else
+            launch_fft<float2>(L, st, nflag);
     } else {
         finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
     }
@@ -269,7 +359,9 @@ namespace cyc {
 void prepare_finalize_kernels() {
     static std::atomic<uint64_t> done{0};
     if (!first_on_device(done)) return;
-    cudaFuncSetAttribute(finalize_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (8192 + 512 + 8 + 4096) * (int)sizeof(double2));
+    cudaFuncSetAttribute(finalize_fft_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fft_smem_max<double2>());
+    cudaFuncSetAttribute(finalize_fft_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fft_smem_max<float2>());
 }
 }  // namespace cyc
