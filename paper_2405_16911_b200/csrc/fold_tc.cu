@@ -322,6 +322,22 @@ __device__ __forceinline__ void tc_drain_band(uint32_t tmem, const FoldLaunch& L
     asm volatile("tcgen05.fence::before_thread_sync;");
 }
 
+// 32 consecutive TMEM columns of this warp's lanes, one load and one wait
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
+    uint32_t u[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15]),
+          "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]),
+          "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(u[k]);
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
     uint32_t u[16];
     asm volatile(
@@ -368,20 +384,17 @@ __device__ __forceinline__ void tc_epilogue_tile(uint32_t tmem, const FoldLaunch
                 const int kind = w + WQ * k;
                 const uint32_t base = tmem + ((uint32_t)(32 * q) << 16);
 #pragma unroll
-                for (int jb = 0; jb < 16; jb += 8) {  // 8 column pairs per load
+                for (int part2 = 0; part2 < (kind ? 1 : 2); ++part2) {
+                    // merged item: chunk q for j >= r', chunk q + 8 for j < r'
+                    const int cc = kind ? q + kind : q + 8 * part2;
+                    float v[32];  // the chunk's 16 column pairs in one load
+                    tmem_ld32(base + (uint32_t)(32 * cc), v);
 #pragma unroll
-                    for (int part2 = 0; part2 < (kind ? 1 : 2); ++part2) {
-                        // merged item: chunk q for j >= r', chunk q + 8 for j < r'
-                        const int cc = kind ? q + kind : q + 8 * part2;
-                        float v[16];
-                        tmem_ld16(base + (uint32_t)(32 * cc + 2 * jb), v);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const bool use = kind || ((jb + j >= rp) == (part2 == 0));
-                            if (use) {
-                                acc[k][2 * (jb + j)] += v[2 * j];
-                                acc[k][2 * (jb + j) + 1] += v[2 * j + 1];
-                            }
+                    for (int j = 0; j < 16; ++j) {
+                        const bool use = kind || ((j >= rp) == (part2 == 0));
+                        if (use) {
+                            acc[k][2 * j] += v[2 * j];
+                            acc[k][2 * j + 1] += v[2 * j + 1];
                         }
                     }
                 }
