@@ -21,7 +21,7 @@ table.  Two measurements per run:
 metric = direct-sum-equivalent (alpha, tau) updates/s = A*T*L_eff*flags*channels / t
 (SURVEY §8d).  The executed algorithm is the exact residue fold (tcgen05 bf16x3
 banded Gram product; for several lag blocks from bf16 planes split once per
-sample) + fp64 FFT finalize.
+sample) + FFT finalize (fp64 combine, fp32 transform).
 
 Multi-GPU (`torchrun ... bench.py --gpus N`): C2/C5 are time-sharded
 (rank r folds frames [F r/N, F (r+1)/N) with `origin` anchoring the phases at
@@ -51,7 +51,7 @@ sys.path.insert(0, ROOT)
 METRIC = "cyclic-ACF (alpha,tau) updates/s"
 UNIT = "updates/s"
 DTYPE = "cf32 in; fold: bf16x3 split on tcgen05 (~fp32 products), fp32 TMEM accumulation drained every <=64 " \
-        "stages; fp64 reductions/FFT"
+        "stages; fp64 reductions; FFT: fp64 combine, fp32 transform"
 
 # Block-average configurations (Full mode, conv + conj).  `bins`: the cycle
 # frequencies the config counts (C4: 128 of the 256 natural bins).

@@ -576,13 +576,15 @@ Status Engine::init(const Cfg& cfg) {
     CK(cudaMalloc(&avg_dev_, (size_t)nflags_ * layout_len_ * sizeof(double2)));
     CK(cudaMallocHost(&avg_host_, layout_len_ * sizeof(double2)));
     if (use_fold_) {
-        std::vector<double2> tw(Pf_);
+        const int npass = Pf_ <= 8192 ? fft_pass_twiddles((int)Pf_, nullptr) : 0;
+        std::vector<double2> tw(Pf_ + npass);
         for (int64_t j = 0; j < Pf_; ++j) {
             const long double th = -2.0L * 3.14159265358979323846264338327950288L * (long double)j / (long double)Pf_;
             tw[j] = make_double2((double)cosl(th), (double)sinl(th));
         }
-        CK(cudaMalloc(&tw_, Pf_ * sizeof(double2)));
-        CK(cudaMemcpy(tw_, tw.data(), Pf_ * sizeof(double2), cudaMemcpyHostToDevice));
+        if (npass) fft_pass_twiddles((int)Pf_, tw.data() + Pf_);
+        CK(cudaMalloc(&tw_, tw.size() * sizeof(double2)));
+        CK(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
         CK(cudaMalloc(&bins_dev_, A_ * sizeof(int)));
         CK(cudaMemcpy(bins_dev_, bins_.data(), A_ * sizeof(int), cudaMemcpyHostToDevice));
     }

@@ -13,6 +13,7 @@
 //     the reference's per-lag Fft::forward (proj/src/fft.cpp:44-87);
 //   * direct DFT with an exact (bin*r mod Pf) twiddle index, for small alpha
 //     sets or non-power-of-two periods (proj/src/fft.cpp:89-100 analogue).
+#include <cmath>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -142,14 +143,10 @@ __global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kern
     if (threadIdx.x == 0) s_row = L.rows[row_i];
     if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0) *L.shift_ctr += L.shift_inc;
     {
-        int off = 0;
-        fft_passes(log2Pf, blockDim.x, [&](int r, int h) {
-            for (int i = threadIdx.x; i < r * h; i += blockDim.x) {
-                const int l = i / h, pos = i - l * h;
-                tw[off + i] = to_v<V>(__ldg(L.tw + (size_t)pos * (Pf / (2 * (h << l)))));
-            }
-            off += r * h;
-        });
+        // the per-pass tables follow the Pf plain twiddles (fft_pass_twiddles, built on the host)
+        const double2* twp = L.tw + Pf;
+        const int ntw = fft_tw_entries(log2Pf, blockDim.x);
+        for (int i = threadIdx.x; i < ntw; i += blockDim.x) tw[i] = to_v<V>(__ldg(twp + i));
     }
     __syncthreads();
     const FinalRow row = s_row;
@@ -240,9 +237,23 @@ __global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kern
         }
         return;
     }
-    for (int a = threadIdx.x; a < L.A; a += blockDim.x) {
-        const double2 v = to_d(buf[padi(L.bins[a], sh)]);
-        out[(size_t)a * L.stride_a] = make_double2(v.x * sc, v.y * sc);
+    // 8 bins loaded at once: the dependent index -> shared read -> store chain of
+    // one bin at a time stalled on each bins[] load (13 % of the samples, ncu)
+    const int nb8 = 8 * (int)blockDim.x;
+    for (int a0 = threadIdx.x; a0 < L.A; a0 += nb8) {
+        int bi[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int a = a0 + u * (int)blockDim.x;
+            bi[u] = a < L.A ? __ldg(L.bins + a) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int a = a0 + u * (int)blockDim.x;
+            if (a >= L.A) break;
+            const double2 v = to_d(buf[padi(bi[u], sh)]);
+            out[(size_t)a * L.stride_a] = make_double2(v.x * sc, v.y * sc);
+        }
     }
 }
 
@@ -320,6 +331,27 @@ static bool fft64() {
         return e && *e && *e != '0';
     }();
     return on;
+}
+
+// Per-pass twiddle tables of a Pf-point row in the kernel's pass order:
+// pass (log2r, h), level l < log2r, position pos < h: W^{pos Pf / (2^{l+1} h)}.
+// out == nullptr: the count only.  Stored after the Pf plain twiddles.
+int fft_pass_twiddles(int Pf, double2* out) {
+    int lg = 0;
+    while ((1 << lg) < Pf) ++lg;
+    if ((1 << lg) != Pf || Pf > 8192) return 0;
+    const int nt = Pf >= 8192 ? 512 : std::min(512, std::max(32, Pf / 4));
+    int n = 0;
+    fft_passes(lg, nt, [&](int r, int h) {
+        for (int l = 0; l < r; ++l)
+            for (int pos = 0; pos < h; ++pos, ++n) {
+                if (!out) continue;
+                const long long j = (long long)pos * (Pf / (2 * (h << l)));
+                const long double th = -2.0L * 3.14159265358979323846264338327950288L * (long double)j / (long double)Pf;
+                out[n] = make_double2((double)cosl(th), (double)sinl(th));
+            }
+    });
+    return n;
 }
 
 template <class V>

@@ -242,7 +242,7 @@ struct FinalizeLaunch {
     int flags;                // bit0 conv, bit1 conj
     const int* bins;          // [A] DFT bin (mod Pf) per output alpha
     int A;
-    const double2* tw;        // e^{-j2pi j / Pf}, j < Pf
+    const double2* tw;        // e^{-j2pi j / Pf}, j < Pf; then fft_pass_twiddles(Pf) entries
     double scale_default;     // multiply (1/count)
     const double* row_scale;  // optional per-out_block scale (nullptr => scale_default)
     double2* out;             // [out_block][flag_index][...] with strides below
@@ -265,6 +265,10 @@ struct FinalizeLaunch {
 };
 
 void launch_finalize(const FinalizeLaunch& L, cudaStream_t st);
+// FFT rows (Pf a power of two <= 8192) read per-pass twiddle tables stored right
+// after the Pf plain twiddles of FinalizeLaunch::tw; fills `out` (nullable) and
+// returns their count (0 for other Pf).
+int fft_pass_twiddles(int Pf, double2* out);
 
 // Direct contraction for arbitrary alphas.
 struct DirectSeg {
