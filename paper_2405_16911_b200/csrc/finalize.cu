@@ -141,13 +141,16 @@ __global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kern
     const int nflag = (L.flags == 3) ? 2 : 1;
     const int row_i = blockIdx.x / nflag, fi = blockIdx.x % nflag;  // fi: index among requested flags
     if (threadIdx.x == 0) s_row = L.rows[row_i];
-    if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0) *L.shift_ctr += L.shift_inc;
     {
         // the per-pass tables follow the Pf plain twiddles (fft_pass_twiddles, built on the host)
         const double2* twp = L.tw + Pf;
         const int ntw = fft_tw_entries(log2Pf, blockDim.x);
         for (int i = threadIdx.x; i < ntw; i += blockDim.x) tw[i] = to_v<V>(__ldg(twp + i));
     }
+    // everything above is independent of the predecessor (PDL launch: it overlaps
+    // the reduce's tail); S and the frame counter below are not
+    pdl_wait();
+    if (L.shift_ctr && threadIdx.x == 0 && blockIdx.x == 0) *L.shift_ctr += L.shift_inc;
     __syncthreads();
     const FinalRow row = s_row;
     const int flag_bit = (L.flags == 2) ? 1 : fi;
@@ -369,7 +372,7 @@ static void launch_fft(const FinalizeLaunch& L, cudaStream_t st, int nflag) {
     static std::atomic<uint64_t> attr_set{0};
     if (first_on_device(attr_set))
         cudaFuncSetAttribute(finalize_fft_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, fft_smem_max<V>());
-    finalize_fft_kernel<V><<<(unsigned)(L.n_rows * nflag), nt, smem, st>>>(L, lg);
+    launch_pdl(finalize_fft_kernel<V>, dim3((unsigned)(L.n_rows * nflag)), dim3(nt), smem, st, L, lg);
 }
 
 void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {

@@ -1209,6 +1209,7 @@ struct TcRed {
 // partial loads complete.
 template <int MG>
 __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcRed<MG> R) {
+    pdl_wait();  // the fold's partials (PDL launch: scheduled during the fold's tail)
     if (L.gate && *L.gate != ~0ull) return;
     const FoldGroup g = R.groups[blockIdx.y];
     const int slot = R.slot[blockIdx.y];
@@ -1336,7 +1337,8 @@ void launch_tc(const FoldLaunch& L, const DESC& D, const TcRed<MG>& R, bool self
     if (ev1) record_event(ev1, st);
     if (fold_done) cudaEventRecord(fold_done, st);
     if (before_reduce) cudaStreamWaitEvent(st, before_reduce, 0);
-    fold_tc_reduce_kernel<MG><<<dim3((L.tc_pairs == 2 ? 128 : 64) * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+    launch_pdl(fold_tc_reduce_kernel<MG>, dim3((L.tc_pairs == 2 ? 128 : 64) * TRB / 256, L.n_groups), dim3(256), 0, st,
+               L, R);
 }
 
 template <int MG>
@@ -1396,7 +1398,7 @@ void launch_fold_tcp(const FoldLaunch& L, const TcPlDesc& D, const FoldGroup* gr
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     fold_tcp_kernel<TcPlDesc><<<std::min(L.n_tiles, sms), TPT, PL_SMEM, st>>>(L, D);
     if (ev1) record_event(ev1, st);
-    fold_tc_reduce_kernel<FI_GROUPS><<<dim3(64 * TRB / 256, L.n_groups), 256, 0, st>>>(L, R);
+    launch_pdl(fold_tc_reduce_kernel<FI_GROUPS>, dim3(64 * TRB / 256, L.n_groups), dim3(256), 0, st, L, R);
 }
 
 bool encode_tcp2_maps(TcPl2Desc& D, int si, const uint16_t* plane0, int64_t plane_elems, int64_t p_base, int64_t rows,

@@ -15,6 +15,7 @@
 //             a 64-bit fixed-point phase (exact wrap) instead of the reference's
 //             drifting lead-phasor recurrence (proj/src/estimator.cpp:70-73).
 #pragma once
+#include <utility>
 #include <atomic>
 #include <cstdint>
 #include <cuda.h>
@@ -263,6 +264,29 @@ struct FinalizeLaunch {
     int64_t* shift_ctr;
     int64_t shift_inc;
 };
+
+// Programmatic dependent launch: the kernel may be scheduled while its stream
+// predecessor finishes (launch latency and prologue overlap the predecessor's
+// tail); it executes pdl_wait() before touching the predecessor's output.
+// Outside a PDL launch pdl_wait() is a no-op.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 void launch_finalize(const FinalizeLaunch& L, cudaStream_t st);
 // FFT rows (Pf a power of two <= 8192) read per-pass twiddle tables stored right
