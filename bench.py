@@ -25,7 +25,7 @@ sample) + FFT finalize (fp64 combine, fp32 transform).
 
 Multi-GPU (`torchrun ... bench.py --gpus N`): C2/C5 are time-sharded
 (rank r folds frames [F r/N, F (r+1)/N) with `origin` anchoring the phases at
-absolute sample 0; an NCCL all-reduce sums the fp64 fold states before the
+absolute sample 0; an NCCL reduce-scatter sums the fp64 fold states by lag rows before the
 finalize; the record is broadcast from rank 0 over NCCL at set-up); C4 is
 channel-sharded (64/N channels per rank, NCCL all-gather of the tables).
 Total work is fixed: `scaling` = "strong".  C1/C3 run replicas.
@@ -400,7 +400,8 @@ def run_reference(args, ws, rank):
 def run_block(args, ws, rank, local):
     import torch
     import paper_2405_16911_b200 as cyc
-    from paper_2405_16911_b200.shard import channel_shards, exchange_time_shards, gather_channel_tables, time_shards
+    from paper_2405_16911_b200.shard import (channel_shards, exchange_lag_slices, gather_channel_tables,
+                                             gather_lag_tables, time_shards)
 
     name = args.config
     c = BLOCK[name]
@@ -446,19 +447,27 @@ def run_block(args, ws, rank, local):
         torch.empty((C_, 2, lay), dtype=torch.complex128, device=cuda)
     out_host = cyc.host_alloc((C_ if c["shard"] == "channel" else 1, 2, lay), dtype=np.complex128)
 
+    t_pad = est.fold_state()[1] // (4 * N * nch) if c["shard"] == "time" else T  # Full mode: Pf = N
+    lags_mine = [0, T]
+
     def exchange():
-        """Time shards: NCCL all-reduce (sum) of the fp64 fold accumulators."""
+        """Time shards: NCCL reduce-scatter of the fp64 fold accumulators by lag
+        rows; each rank then finalizes its T/N lags (set_lag_slice)."""
         if c["shard"] != "time" or ws == 1:
             return
         import torch.distributed as dist
-        exchange_time_shards(est, F_total, dist)
+        lags_mine[:] = exchange_lag_slices(est, F_total, T, t_pad, ws, rank, dist)
 
     def gather():
-        """Channel shards: NCCL all-gather of the (channel, flag) tables."""
-        if c["shard"] != "channel" or ws == 1:
+        """NCCL all-gather of the tables: time shards the lag slices, channel
+        shards the (channel, flag) tables."""
+        if ws == 1:
             return
         import torch.distributed as dist
-        full_dev.copy_(gather_channel_tables(out_dev, ws, dist))
+        if c["shard"] == "channel":
+            full_dev.copy_(gather_channel_tables(out_dev, ws, dist))
+        elif tuple(lags_mine) != (0, T):
+            gather_lag_tables(out_dev, lags_mine[0], lags_mine[1], T, ws, dist)
 
     def step_device():
         if ws == 1:  # one call, one host synchronisation (cyc_block_average_device)
@@ -474,12 +483,12 @@ def run_block(args, ws, rank, local):
         est.reset()
         est.push(host)
         exchange()
-        if c["shard"] == "channel" and ws > 1:
+        if ws > 1:
             est.average_all(out=out_dev)
             gather()
             if rank == 0:
                 out_host[:] = full_dev.cpu().numpy()
-        elif rank == 0 or c["shard"] == "channel":
+        else:
             est.average_all(out=out_host)
 
     def timed(fn, k):
@@ -532,7 +541,8 @@ def run_block(args, ws, rank, local):
         return
     ups = updates_of(c)
     par = f"{'time' if c['shard'] == 'time' else 'channel'}-sharded x{ws}" + (
-        ": frame ranges per GPU + NCCL all-reduce of the fp64 fold states" if c["shard"] == "time" else
+        ": frame ranges per GPU + NCCL reduce-scatter of the fp64 fold states by lag rows, T/N lags finalized per "
+        "GPU, NCCL all-gather of the tables" if c["shard"] == "time" else
         ": 64/N channels per GPU + NCCL all-gather of the tables") if ws > 1 else "single GPU"
     cfgb = {"workload": c["workload"], "samples": L, "channels": C_, "alphas": c["A"], "lags": T,
             "flags": ["conv", "conj"], "win_len": N, "l_eff": frames_of(c) * N, "parallelism": par,

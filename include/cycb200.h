@@ -246,6 +246,14 @@ int64_t cyc_data_error_index(const cyc_est* est);
  * coherent average is then exactly the whole record's. */
 int cyc_fold_state(cyc_est* est, void** dev_ptr, size_t* count, uint64_t* frames);
 int cyc_fold_set_frames(cyc_est* est, uint64_t frames);
+/* Lag slice of the block-mode coherent averages (multi-GPU lag slices): later
+ * cyc_average_all / cyc_block_average_device calls finalize only the requested
+ * lags with index in [lag_begin, lag_end) (indices into the lag list; the
+ * rows of the other lags in `out` are left untouched), so time shards can
+ * reduce-scatter their fold states by lag rows -- each rank then holds the
+ * whole record's state for its slice only -- and finalize 1/G of the tables.
+ * (0, 0) restores every lag.  No reference counterpart. */
+int cyc_set_lag_slice(cyc_est* est, uint32_t lag_begin, uint32_t lag_end);
 
 /* CSV export of results (proj/src/io.cpp:161-208, the reference's
  * export_frames_csv(path, frames, cfg) / export_average_csv(path, avg, cfg,

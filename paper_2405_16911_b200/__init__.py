@@ -162,6 +162,7 @@ def lib() -> C.CDLL:
     L.cyc_plan.argtypes = [C.POINTER(_Config), C.c_char_p, sz]
     L.cyc_fold_state.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), C.POINTER(C.c_uint64)]
     L.cyc_fold_set_frames.argtypes = [vp, C.c_uint64]
+    L.cyc_set_lag_slice.argtypes = [vp, C.c_uint32, C.c_uint32]
     L.cyc_average_all.argtypes = [vp, C.c_int, vp]
     L.cyc_block_average_device.argtypes = [vp, vp, vp, C.c_size_t, C.c_int, vp]
     L.cyc_push_cf32_file.argtypes = [vp, C.c_char_p, _SINK, vp]
@@ -483,6 +484,13 @@ class CyclicCorrelator:
 
     def fold_set_frames(self, frames: int):
         self._check(self._L.cyc_fold_set_frames(self._h, int(frames)))
+
+    def set_lag_slice(self, begin: int = 0, end: int = 0):
+        """Block-mode coherent averages (average_all / block_average_device)
+        finalize only the lags with index in [begin, end) of the lag list, the
+        other rows of `out` untouched; (0, 0) restores every lag
+        (cyc_set_lag_slice: multi-GPU lag slices, shard.exchange_lag_slices)."""
+        self._check(self._L.cyc_set_lag_slice(self._h, int(begin), int(end)))
 
     def fold_tensor(self):
         """The block-mode fold state as a torch float64 CUDA tensor viewing the

@@ -321,6 +321,11 @@ extern "C" int cyc_fold_set_frames(cyc_est* est, uint64_t frames) {
     return finish(est, est->e->set_frames(frames));
 }
 
+extern "C" int cyc_set_lag_slice(cyc_est* est, uint32_t lag_begin, uint32_t lag_end) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->set_lag_slice(lag_begin, lag_end));
+}
+
 extern "C" int cyc_average_all(cyc_est* est, int avg_mode, cyc_cf64* out) {
     if (!est || !out) return CYC_ERR_USAGE;
     return finish(est, est->e->average_all(avg_mode, out));

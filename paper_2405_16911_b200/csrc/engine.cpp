@@ -1474,23 +1474,26 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
 }
 
 Status Engine::finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
-                        double2* out, cudaStream_t st) {
+                        double2* out, cudaStream_t st, bool use_slice) {
     if (!st) st = cs_;
     // The row table depends on nslots only: build and upload it once per size
     // (device memory kept for the estimator's lifetime), not per call.
+    // block finalizes honour the lag slice (cyc_set_lag_slice); per-frame ones take every lag
+    const bool sliced = use_slice && lag_e_ > lag_b_;
+    const int tb = sliced ? lag_b_ : 0, te = sliced ? lag_e_ : T_;
     const FinalRow* drows = nullptr;
     for (const auto& rc : rows_cache_)
-        if (rc.first == nslots) drows = rc.second;
+        if (rc.first.nslots == nslots && rc.first.b == tb && rc.first.e == te) drows = rc.second;
     if (!drows) {
         std::vector<FinalRow> rows;
-        rows.reserve((size_t)nslots * T_);
+        rows.reserve((size_t)nslots * (te - tb));
         for (int s = 0; s < nslots; ++s)
-            for (int t = 0; t < T_; ++t) rows.push_back({s, lags_req_[t] - f_lo_, t, s});
+            for (int t = tb; t < te; ++t) rows.push_back({s, lags_req_[t] - f_lo_, t, s});
         FinalRow* d = nullptr;
         CK(cudaMalloc(&d, rows.size() * sizeof(FinalRow)));
         CK(cudaMemcpyAsync(d, rows.data(), rows.size() * sizeof(FinalRow), cudaMemcpyHostToDevice, cs_));
         CK(cudaStreamSynchronize(cs_));  // `rows` is pageable and goes out of scope
-        rows_cache_.push_back({nslots, d});
+        rows_cache_.push_back({RowsKey{nslots, tb, te}, d});
         drows = d;
     }
     FinalizeLaunch L{};
@@ -1498,7 +1501,7 @@ Status Engine::finalize(const double* S, int nslots, double scale, const std::ve
     L.t_pad = t_pad_;
     L.Pf = (int)Pf_;
     L.rows = drows;
-    L.n_rows = nslots * T_;
+    L.n_rows = nslots * (te - tb);
     L.flags = c_.flags;
     L.bins = bins_dev_;
     L.A = A_;
@@ -2857,7 +2860,7 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
         CK(cudaStreamWaitEvent(fs_, a, 0));
         ev_pool_.push_back(a);
         tl("avg", fs_);
-        TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, (double2*)out, fs_));
+        TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, (double2*)out, fs_, true));
         tl("avg.end", fs_);
         CK(cudaEventRecord(fin_ev_[S_cur_], fs_));
         fin_live_[S_cur_] = true;
@@ -2869,8 +2872,23 @@ Status Engine::average_all(int avg_mode, cyc_cf64* out) {
         CK(cudaMalloc(&avg_all_dev_, (size_t)C * per * sizeof(double2)));
         avg_all_len_ = (size_t)C * per;
     }
-    TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, avg_all_dev_));
-    CK(cudaMemcpyAsync(out, avg_all_dev_, (size_t)C * per * sizeof(double2), cudaMemcpyDefault, cs_));
+    TRY(finalize(S_main_, C, 1.0 / ((double)frames_ * (double)N_), nullptr, avg_all_dev_, nullptr, true));
+    if (lag_e_ > lag_b_) {
+        // only the slice's rows: every other row of `out` stays as the caller left it
+        const size_t nb = (size_t)(lag_e_ - lag_b_);
+        for (size_t blk = 0; blk < (size_t)C * nflags_; ++blk) {
+            const size_t base = blk * layout_len_;
+            if (stride_t_ == 1)  // alpha-major [alpha][lag]: a strided column band
+                CK(cudaMemcpy2DAsync(out + base + lag_b_, (size_t)stride_a_ * sizeof(double2),
+                                     avg_all_dev_ + base + lag_b_, (size_t)stride_a_ * sizeof(double2),
+                                     nb * sizeof(double2), (size_t)A_, cudaMemcpyDefault, cs_));
+            else  // lag-major [lag][alpha]: contiguous rows
+                CK(cudaMemcpyAsync(out + base + (size_t)lag_b_ * stride_t_, avg_all_dev_ + base + (size_t)lag_b_ * stride_t_,
+                                   nb * (size_t)stride_t_ * sizeof(double2), cudaMemcpyDefault, cs_));
+        }
+    } else {
+        CK(cudaMemcpyAsync(out, avg_all_dev_, (size_t)C * per * sizeof(double2), cudaMemcpyDefault, cs_));
+    }
     CK(cudaStreamSynchronize(cs_));
     return Status::ok();
 }
@@ -3075,6 +3093,18 @@ void Engine::tl_resolve(bool wait) {
         for (auto& k : m) cudaEventDestroy(k.ev);
         tl_steps_.pop_front();
     }
+}
+
+Status Engine::set_lag_slice(uint32_t b, uint32_t e) {
+    if (b == 0 && e == 0) {
+        lag_b_ = lag_e_ = 0;
+        return Status::ok();
+    }
+    if (b >= e || e > (uint32_t)T_) return Status{CYC_ERR_USAGE, "lag slice out of range", -1};
+    lag_b_ = (int)b;
+    lag_e_ = (int)e;
+    avg_cache_frames_ = ~0ull;  // cached averages hold other rows
+    return Status::ok();
 }
 
 Status Engine::set_frames(uint64_t frames) {

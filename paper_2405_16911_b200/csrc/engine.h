@@ -83,6 +83,7 @@ public:
     // Block-mode fold state (time-sharded multi-GPU, checkpoint/resume).
     Status fold_state(void** dev_ptr, size_t* count, uint64_t* frames);
     Status set_frames(uint64_t frames);
+    Status set_lag_slice(uint32_t b, uint32_t e);
     // Fold-kernel timing with CUDA events on the compute stream.
     void set_profiling(bool on) { prof_ = on; }
     Status profile_read(uint64_t* launches, double* ms, double* flops, double* exec_flops = nullptr,
@@ -146,7 +147,7 @@ private:
     bool tc_capable_ = false;  // sm_100 device (tcgen05)
     // Finalize slots [0, nslots) of S into out tables (out_block = slot) with per-slot scale.
     Status finalize(const double* S, int nslots, double scale, const std::vector<double>* slot_scale,
-                    double2* out, cudaStream_t st = nullptr);
+                    double2* out, cudaStream_t st = nullptr, bool use_slice = false);
     // Direct contraction of segs into out tables (out_block = seg.out_block).
     Status direct(const std::vector<DirectSeg>& segs, double scale, double2* out, bool accum = false);
     bool direct_host_out_ = false;  // the next direct per-frame reduce also writes frames_host_ (mapped)
@@ -413,7 +414,12 @@ private:
     // speculative block pushes: pending fold + history backup for roll-back
     double* S_pend_ = nullptr;
     std::vector<char> blob_;              // host staging of one launch's descriptors
-    std::vector<std::pair<int, FinalRow*>> rows_cache_;  // finalize row tables by slot count (device)
+    // finalize row tables by (slot count, lag slice) (device)
+    struct RowsKey {
+        int nslots, b, e;
+    };
+    std::vector<std::pair<RowsKey, FinalRow*>> rows_cache_;
+    int lag_b_ = 0, lag_e_ = 0;  // block finalize lag slice [lag_b_, lag_e_) (cyc_set_lag_slice)
     std::unique_ptr<FoldInline> inline_;  // by-value descriptors of the next fold launch
     std::unique_ptr<TcParams> tcp_;       // by-value descriptors of the next tensor-core fold launch
     struct MapCache {                     // last tensor maps encoded per segment index

@@ -11,6 +11,10 @@
   all-gathered at the end (no collective on the data path).
 * replicas (C1, C3: the small-call paths do not shard): every GPU its own record.
 
+With one channel and the lag list 0..T-1, the bench reduce-scatters the states
+by lag rows instead (exchange_lag_slices: each GPU then finalizes only its
+T/G lags) and all-gathers the tables (gather_lag_tables).
+
 The exchange steps below are what bench.py runs between the push and the
 finalize; they take any estimator-like object with fold_tensor(),
 fold_set_frames() (time shards) and any torch.distributed group (NCCL on the
@@ -78,6 +82,61 @@ def exchange_time_shards(est, frames_total: int, dist, group=None):
     dist.all_reduce(t, group=group)
     est.fold_set_frames(frames_total)
     return t
+
+
+def lag_slice(T: int, world: int, rank: int):
+    """Contiguous lag range [t0, t1) of the lag list owned by `rank`."""
+    return T * rank // world, T * (rank + 1) // world
+
+
+def exchange_lag_slices(est, frames_total: int, T: int, t_pad: int, world: int, rank: int, dist, group=None):
+    """Time shards, lag-sliced: reduce-scatter the fp64 fold states by lag rows
+    (rank r ends up with the whole record's state for its lags T r/G .. T (r+1)/G
+    only -- each rank sends and receives (G-1)/G of one slice instead of an
+    all-reduce's two passes over the whole state) and point the estimator's
+    finalize at that slice (set_lag_slice), so each rank transforms 1/G of the
+    tables.  Needs one channel, the lag list 0..T-1 with T == t_pad (state rows =
+    lags) and T % G == 0; otherwise the states are all-reduced and every lag is
+    finalized.  Backends without a reduce-scatter (gloo) all-reduce instead --
+    the same sums.  Returns the rank's lag range [t0, t1)."""
+    if world == 1 or T != t_pad or T % world or est_channels(est) != 1:
+        exchange_time_shards(est, frames_total, dist, group)
+        return 0, T
+    t0, t1 = lag_slice(T, world, rank)
+    t = est.fold_tensor()  # [t_pad][Pf][4] for one channel
+    mine = t.view(t_pad, -1)[t0:t1].reshape(-1)
+    try:
+        dist.reduce_scatter_tensor(mine, t, group=group)
+    except (RuntimeError, AttributeError, NotImplementedError, ValueError):
+        dist.all_reduce(t, group=group)
+    est.fold_set_frames(frames_total)
+    est.set_lag_slice(t0, t1)
+    return t0, t1
+
+
+def est_channels(est) -> int:
+    cfg = getattr(est, "_cfg", None)
+    return getattr(cfg, "channels", 1) if cfg is not None else getattr(est, "channels", 1)
+
+
+def gather_lag_tables(out, t0: int, t1: int, T: int, world: int, dist, group=None):
+    """All-gather the lag slices of a Full-mode table [1, flags, T * N]
+    (lag-major) in place: rank r contributes rows [T r/G, T (r+1)/G)."""
+    if world == 1:
+        return out
+    import torch
+    flags = out.shape[1]
+    n = out.shape[2] // T
+    for f in range(flags):
+        full = out[0, f].view(T, n)
+        local = full[t0:t1].contiguous()
+        try:
+            dist.all_gather_into_tensor(full.view(-1), local.view(-1), group=group)
+        except (RuntimeError, AttributeError, ValueError):
+            parts = [torch.empty_like(local) for _ in range(world)]
+            dist.all_gather(parts, local, group=group)
+            full.copy_(torch.cat(parts))
+    return out
 
 
 def gather_channel_tables(local, world: int, dist, group=None):

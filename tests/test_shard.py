@@ -60,6 +60,9 @@ class FoldModel:
     def fold_set_frames(self, frames):
         self.frames = frames
 
+    def set_lag_slice(self, begin=0, end=0):
+        self.lag_slice = (begin, end)
+
     def tables(self, bins):
         """Coherent averages (conv, conj) [bins, lags] from the fold state."""
         S = self.S.numpy().reshape(self.T, self.N, 4)
@@ -118,6 +121,95 @@ def test_gloo_time_shard_exchange_equals_whole_record():
     assert np.max(np.abs(cj - wj)) <= 1e-12
     assert full.shape == (6, 2, 4)
     assert np.array_equal(full.real[:, 0, 0], np.arange(6.0))
+
+
+def _worker_lags(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    from paper_2405_16911_b200.shard import exchange_lag_slices, gather_lag_tables, time_shards
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x = rand_c(1 << 16, 7)
+    N, T = 256, 16
+    sh = time_shards(len(x), N, T - 1, 0, world)[rank]
+    m = FoldModel(x[sh.sample0:sh.sample1], sh.origin, N, list(range(T)), sh.frames)
+    F = sum(s.frames for s in time_shards(len(x), N, T - 1, 0, world))
+    t0, t1 = exchange_lag_slices(m, F, T, T, world, rank, dist)  # the bench's exchange step
+    assert (t0, t1) == (T * rank // world, T * (rank + 1) // world) and m.lag_slice == (t0, t1)
+    cv, cj = m.tables(np.arange(N))  # [bins, lags]
+    # Full-mode tables [1, flags, T * N] (lag-major): this rank fills only its
+    # finalized slice (the rest NaN), then the lag slices are all-gathered
+    out = torch.full((1, 2, T * N), float("nan"), dtype=torch.complex128)
+    for f, tab in enumerate((cv, cj)):
+        rows = out[0, f].view(T, N)
+        rows[t0:t1] = torch.from_numpy(np.ascontiguousarray(tab.T[t0:t1]))
+    gather_lag_tables(out, t0, t1, T, world, dist)
+    if rank == 0:
+        q.put((out.numpy(), m.frames))
+    dist.destroy_process_group()
+
+
+def test_gloo_lag_slice_exchange_and_gather_equal_whole_record():
+    """world-2 gloo run of shard.exchange_lag_slices (reduce-scatter by lag rows;
+    gloo takes the all-reduce branch) + gather_lag_tables: the assembled
+    tables equal the whole record's oracle tables for every lag."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker_lags, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out, F = q.get()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    from oracle.oracle import Oracle
+    x = rand_c(1 << 16, 7)
+    N, T = 256, 16
+    wv, wj = Oracle().block_fold(x, x, np.arange(N), N, list(range(T)), 0, F * N)
+    for f, want in ((0, wv), (1, wj)):
+        got = out[0, f].reshape(T, N)
+        assert not np.isnan(got).any()
+        assert np.max(np.abs(got - want.T)) <= 1e-12
+
+
+def test_lag_slice_plan():
+    from paper_2405_16911_b200.shard import lag_slice
+    for T, W in [(256, 8), (64, 4), (30, 4)]:
+        sl = [lag_slice(T, W, r) for r in range(W)]
+        assert sl[0][0] == 0 and sl[-1][1] == T and all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+
+
+@pytest.mark.gpu
+def test_lag_slice_finalize_matches_full_average(cyc):
+    """cyc_set_lag_slice: average_all finalizes only the slice's lags (device and
+    host outputs), the other rows untouched, the slice's rows equal to the full
+    average; (0, 0) restores every lag."""
+    import torch
+    x = rand_c(1 << 20, 8)
+    N, T = 1024, 64
+    est = cyc.CyclicCorrelator(cyc.EstimatorConfig(mode=cyc.Mode.Full, win_len=N, lag_spec=cyc.LagSpec.Explicit(range(T)),
+                                                   flags=cyc.Flags.BOTH, emit_frames=False))
+    est.push(x)
+    full = est.average_all()  # [1, 2, T * N]
+    for t0, t1 in [(16, 32), (0, 8), (48, 64)]:
+        est.set_lag_slice(t0, t1)
+        host = np.full_like(full, np.nan)
+        est.average_all(out=host)
+        dev = torch.full(full.shape, float("nan"), dtype=torch.complex128, device="cuda")
+        est.average_all(out=dev)
+        torch.cuda.synchronize()
+        for got in (host, dev.cpu().numpy()):
+            g = got.reshape(2, T, N)
+            f = full.reshape(2, T, N)
+            assert np.array_equal(g[:, t0:t1], f[:, t0:t1])
+            assert np.isnan(np.delete(g, np.s_[t0:t1], axis=1)).all()
+    est.set_lag_slice(0, 0)
+    assert np.array_equal(est.average_all(), full)
+    with pytest.raises(Exception):
+        est.set_lag_slice(10, 70)
 
 
 @pytest.mark.gpu
