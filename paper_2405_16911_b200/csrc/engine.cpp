@@ -1531,6 +1531,11 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     const int64_t want = (2 * SMS + (int64_t)segs.size() * A_ - 1) / ((int64_t)segs.size() * A_);
     splits = (int)std::max<int64_t>(splits, std::min<int64_t>(want, maxcnt / 256));
     while (splits > 1 && (int64_t)segs.size() * A_ * splits > 64 * SMS) splits /= 2;
+    static const int split_knob = [] {  // CYC_DIRECT_SPLITS=<n>: tuning knob (diagnostics)
+        const char* e = std::getenv("CYC_DIRECT_SPLITS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (split_knob > 0) splits = (int)std::min<int64_t>(split_knob, std::max<int64_t>(1, maxcnt / 64));
     const size_t pbytes = segs.size() * (size_t)A_ * splits * 2 * T_ * sizeof(float2);
     TRY(ensure_partials(pbytes));
     thread_local DirectLaunch L;  // ~0.7 KB of inline descriptors: host staging, copied by the launch
