@@ -1,4 +1,4 @@
-# C1 direct-kernel split count and table path (diagnostics): kernel time (warm) and the driver's ms/step
+# C1 direct-kernel split count (diagnostics): kernel time (warm) and the driver's ms/step
 python - <<'PY'
 import numpy as np, sys
 sys.path.insert(0, '.')
@@ -8,11 +8,8 @@ build_tools()
 siggen.c1_record().astype(np.complex64).tofile('/dev/shm/c1.cf32')
 siggen.c1_record()[: 1 << 18].astype(np.complex64).tofile('/dev/shm/c1s.cf32')
 PY
-for s in 0 1 2 4 8 32; do
-  for zc in 0 1; do
-    if [ $zc = 1 ]; then export CYC_NO_ZERO_COPY=1; else unset CYC_NO_ZERO_COPY; fi
-    k=$(CYC_DIRECT_SPLITS=$s ncu --cache-control none --metrics gpu__time_duration.sum --clock-control none -k regex:direct -s 20 -c 10 --csv ./tools/stream_bench c1 /dev/shm/c1s.cf32 1 1 2>/dev/null | grep direct | awk -F'","' '{gsub(/"/,"",$NF); s+=$NF; n++} END {print s/n}')
-    r=$(CYC_DIRECT_SPLITS=$s ./tools/stream_bench c1 /dev/shm/c1.cf32 5 2)
-    echo "splits $s nozc $zc kernel_ns $k $r"
-  done
+for s in ${SPLITS:-0 2 4 8 16 32}; do
+  k=$(CYC_DIRECT_SPLITS=$s ncu --cache-control none --metrics gpu__time_duration.sum --clock-control none -k regex:direct -s 20 -c 10 --csv ./tools/stream_bench c1 /dev/shm/c1s.cf32 1 1 2>/dev/null | grep direct | awk -F'","' '{gsub(/"/,"",$NF); s+=$NF; n++} END {print s/n}')
+  r=$(CYC_DIRECT_SPLITS=$s ./tools/stream_bench c1 /dev/shm/c1.cf32 5 2)
+  echo "splits $s kernel_ns $k $r"
 done
