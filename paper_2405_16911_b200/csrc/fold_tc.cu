@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(TNT, 1) fold_tc_kernel(FoldLaunch L, const __g
 constexpr int TPE = TC_TPE;                        // epilogue warps of the planes kernel
 constexpr int TPT = 64 + 32 * TPE;
 #ifndef PL_RING_KB
-#define PL_RING_KB 192
+#define PL_RING_KB 128
 #endif
 constexpr int PL_RING = PL_RING_KB * 1024;        // stages: 24 KB (self) or 32 KB (x + 2 y atoms)
 constexpr int NPL_MAX = PL_RING / (2 * XPLANE);    // self tiles: 8 stages in flight (others 6)
@@ -768,7 +768,11 @@ template <class DESC>
 __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __grid_constant__ DESC D) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+#ifdef TC_ABL_SLOT24  // ablation (diagnostic builds): 24 KB slots -- non-self stages overrun the next slot
+    constexpr uint32_t SLOT = 2 * XPLANE;
+#else
     constexpr uint32_t SLOT = 2 * XPLANE + 2 * 2 * ATOM;  // 32 KB
+#endif
     constexpr int NPL = PL_RING / (int)SLOT;               // stages in flight
     static_assert(NPL >= 2, "ring depth");
     __shared__ uint64_t full[NPL], planefree[NPL], chunk_done, drain_free;
@@ -819,7 +823,7 @@ __global__ void __launch_bounds__(TPT, 1) fold_tcp_kernel(FoldLaunch L, const __
                     } else
 #endif
                     {
-                        mbar_expect_tx(&full[s], g.self ? 2 * XPLANE : SLOT);
+                        mbar_expect_tx(&full[s], g.self ? 2 * XPLANE : 2 * XPLANE + 2 * 2 * ATOM);
                         tma_4d(st, xm, row, g.xatom, &full[s]);
                         if (!g.self) tma_4d(st + 2 * XPLANE, ym, row, g.yatom, &full[s]);
                     }
