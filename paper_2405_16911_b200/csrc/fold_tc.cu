@@ -719,13 +719,14 @@ constexpr int TPT = 64 + 32 * TPE;
 #ifndef PL_RING_KB
 #define PL_RING_KB 128
 #endif
-constexpr int PL_RING = PL_RING_KB * 1024;        // stages: 24 KB (self) or 32 KB (x + 2 y atoms)
-constexpr int NPL_MAX = PL_RING / (2 * XPLANE);    // self tiles: 8 stages in flight (others 6)
+constexpr int PL_RING = PL_RING_KB * 1024;        // 32 KB stage slots (x hi/lo + 2 y atoms): 4 in flight
 constexpr int PL_SMEM = PL_RING + 1024;
 static_assert(PL_SMEM <= 227 * 1024, "shared memory per CTA");
-// A stage's TMA lands ~3900 cycles after issue under load (tools/tcp_trace.py)
-// and its slot frees only when its MMAs complete, so the stages in flight set
-// the rate.
+// A stage's TMA lands ~3500 cycles after issue under load (tools/tcp_trace.py)
+// and its slot frees only when its MMAs complete.  More windows in flight do
+// not help: with 148 SMs streaming, the fold ran 909 / 543 / 487 / 497 / 505 /
+// 523 us at 2 / 3 / 4 / 5 / 6 / 7 slots (C5) -- the memory system congests
+// before the latency is covered, so 4 slots (128 KB) is the default.
 
 // Per-tile geometry of the planes fold (every role derives it from the tile
 // table): 64 residues [r0, r0 + 64) x lags d .. d + 127; the accumulator
