@@ -167,13 +167,17 @@ __global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kern
         rC = L.rec_coh[o];
         rM = L.rec_mag[o];
     }
-    // the row streams from HBM: 8 independent 16-byte loads in flight per thread
+    // the row streams from HBM: independent 16-byte loads in flight per thread
     const double2* S2 = reinterpret_cast<const double2*>(Srow);
     const int nb = blockDim.x;
-    for (int r0 = threadIdx.x; r0 < Pf; r0 += 4 * nb) {
-        double2 v[4][2];
+// two residues (4 x 16-byte loads) in flight per thread: with 2 CTAs of 512
+// threads per SM more outstanding loads only congest (4: 57.9 us, 6: 59.6,
+// 2: 56.1 at C5, warm ncu)
+constexpr int FFT_U = 2;
+    for (int r0 = threadIdx.x; r0 < Pf; r0 += FFT_U * nb) {
+        double2 v[FFT_U][2];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < FFT_U; ++u) {
             const int r = r0 + u * nb;
             if (r < Pf) {
                 v[u][0] = __ldcs(S2 + 2 * r);
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kern
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < FFT_U; ++u) {
             const int r = r0 + u * nb;
             if (r >= Pf) continue;
             const int rev = (int)(__brev((unsigned)r) >> (32 - log2Pf));
