@@ -2631,15 +2631,14 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     const int64_t c0 = origin_ + (int64_t)consumed_, c1 = c0 + (int64_t)n;  // absolute
     const int64_t keep = std::min<int64_t>((int64_t)n, (int64_t)need_ + N_);
     wait_ring_free(c1);
-    for (int ch = 0; ch < C; ++ch) {
-        const float2* xs = x + (size_t)ch * n;
-        const float2* ys = (y ? y : x) + (size_t)ch * n;
-        launch_ring_write(ring_x_ + (size_t)ch * cap_, mask_, c0, xs, keep, xs_);
-        launch_ring_write(ring_x_ + (size_t)ch * cap_, mask_, c1 - keep, xs + (n - keep), keep, xs_);
+    {  // every channel's head and tail in one launch each
+        const float2* ys = y ? y : x;
+        launch_ring_write(ring_x_, mask_, c0, x, keep, xs_, C, cap_, (int64_t)n);
+        launch_ring_write(ring_x_, mask_, c1 - keep, x + (n - keep), keep, xs_, C, cap_, (int64_t)n);
         launches_ += 2;
         if (cross_) {
-            launch_ring_write(ring_y_ + (size_t)ch * cap_, mask_, c0, ys, keep, xs_);
-            launch_ring_write(ring_y_ + (size_t)ch * cap_, mask_, c1 - keep, ys + (n - keep), keep, xs_);
+            launch_ring_write(ring_y_, mask_, c0, ys, keep, xs_, C, cap_, (int64_t)n);
+            launch_ring_write(ring_y_, mask_, c1 - keep, ys + (n - keep), keep, xs_, C, cap_, (int64_t)n);
             launches_ += 2;
         }
     }

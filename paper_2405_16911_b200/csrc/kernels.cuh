@@ -357,7 +357,9 @@ void launch_recursive_update(double2* frames, int64_t n_frames, int channels, in
 int launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t base, int channels, int ch,
                         unsigned long long* key, cudaStream_t st, int nch = 1, int64_t pitch = 0);
 // Ring write from a device source with wrap: ring[(abs0 + i) & mask] = src[i].
-void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src,
-                       int64_t n, cudaStream_t st);
+// Copy n samples of `channels` rows (src row c at src + c * src_pitch) into the
+// rings (row c at ring + c * ring_pitch) at absolute index abs0 (masked).
+void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n, cudaStream_t st,
+                       int channels = 1, int64_t ring_pitch = 0, int64_t src_pitch = 0);
 
 }  // namespace cyc

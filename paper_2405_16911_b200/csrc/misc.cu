@@ -134,7 +134,11 @@ __global__ void __launch_bounds__(256) finite_check_v4_kernel(const float4* x, c
     }
 }
 
-__global__ void ring_write_kernel(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n) {
+// channel blockIdx.y: ring row ring + y * ring_pitch, source row src + y * src_pitch
+__global__ void ring_write_kernel(float2* ring, int64_t ring_pitch, uint64_t mask, int64_t abs0, const float2* src,
+                                  int64_t src_pitch, int64_t n) {
+    ring += (size_t)blockIdx.y * ring_pitch;
+    src += (size_t)blockIdx.y * src_pitch;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         ring[(uint64_t)(abs0 + i) & mask] = src[i];
 }
@@ -180,8 +184,11 @@ int launch_finite_check(const float2* x, const float2* y, int64_t n, int64_t bas
     finite_check_kernel<<<dim3((unsigned)g, (unsigned)nch), 256, 0, st>>>(x, y, n, base, channels, ch, key, pitch);
     return 1;
 }
-void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n, cudaStream_t st) {
-    if (n > 0) ring_write_kernel<<<grid_for(n, 256), 256, 0, st>>>(ring, mask, abs0, src, n);
+void launch_ring_write(float2* ring, uint64_t mask, int64_t abs0, const float2* src, int64_t n, cudaStream_t st,
+                       int channels, int64_t ring_pitch, int64_t src_pitch) {
+    if (n <= 0 || channels <= 0) return;
+    const int gx = std::max(1, grid_for(n, 256) / channels);
+    ring_write_kernel<<<dim3(gx, channels), 256, 0, st>>>(ring, ring_pitch, mask, abs0, src, src_pitch, n);
 }
 
 }  // namespace cyc
