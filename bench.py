@@ -241,7 +241,11 @@ def roofline_block(p0: dict, p1: dict, steps: int, ms_step: float, dev: int, lag
         ridge = tpeak * 1e12 / (hpeak * 1e9)
         if traffic:
             common["traffic_over_algorithmic_bytes"] = traffic / abytes
+        tsus = mp.get("bf16_tflops_sustained")
         tensor_view = {"achieved_tflops": rate, "peak_tflops": tpeak, "frac": rate / tpeak,
+                       # the fold runs under sustained tcgen05 load (SM clock ~1.6 GHz inside it):
+                       # the sustained cuBLAS figure beside the burst one the line's `frac` uses
+                       "sustained_peak_tflops": tsus, "frac_vs_sustained": rate / tsus if tsus else None,
                        "executed_tflops": ex_rate, "executed_frac": ex_rate / tpeak,
                        "executed_per_algorithmic": exe / alg if alg else None,
                        "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 burst, this pool)"
