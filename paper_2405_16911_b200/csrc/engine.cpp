@@ -1249,6 +1249,7 @@ Status Engine::fold_tc_planes(const std::vector<FoldSeg>& tsegs, std::vector<TcG
     L.S = S;
     L.gate = fold_gate_;
     L.tc_pairs = 1;
+    L.overwrite = planes_fresh_ ? 1 : 0;  // first writer of a freshly reset state
     D.tiles = dt;
     double launch_flops = 0.0, exec = 0.0;
     for (const auto& gr : groups) {  // 64 residues x lag blocks 2 lb, 2 lb + 1
@@ -2371,16 +2372,16 @@ Status Engine::enqueue_gated(const void* xv, const void* yv, size_t n, int64_t h
     CK(cudaEventRecord(ev_k, cs_));
     CK(cudaStreamWaitEvent(vs_, ev_k, 0));
     CK(cudaStreamWaitEvent(xs_, ev_k, 0));
-    // the reset's clear (the caller drops the flag once this is enqueued) runs
-    // on the side stream beside the fold kernel: every write of S_main below
-    // waits for the side stream's scan event
-    if (pending_clear_)
-        CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), vs_));
+    // the reset's clear (the caller drops the flag once this is enqueued):
+    // fold_device_chunk runs it on the side stream beside the fold kernel, or
+    // lets the first reduce overwrite the state (planes path)
+    clear_req_ = pending_clear_;
     xs_after_cs_ = false;
     ev_pool_.push_back(ev_k);
     fold_gate_ = key_dev_;
     const Status st = fold_device_chunk((const float2*)xv, (const float2*)yv, n, S_main_);
     fold_gate_ = nullptr;
+    clear_req_ = false;
     return st;
 }
 
@@ -2716,6 +2717,14 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
         planes_pitch_ = pitch;
         planes_c0_ = c0 & ~(int64_t)7;
     }
+    // The reset's clear: on the side stream (every write of S below waits for
+    // its scan event), or -- a fresh state folded by the planes path alone --
+    // no clear at all: the planes reduce is the first writer of every cell and
+    // overwrites (no 64 MiB memset, no read of the zeros at C5), and a rejected
+    // chunk (its reduces skip themselves) clears the state behind the verdict.
+    const bool fresh = clear_req_ && planes && !planes2_ && ring_segs.empty() && S == S_main_;
+    if (clear_req_ && !fresh)
+        CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), vs_));
     const size_t s_count = (size_t)C * t_pad_ * Pf_ * 4;
     if (fused && pending) {  // fold into the pending accumulator; the gated add below commits it
         if (!S_pend_) CK(cudaMalloc(&S_pend_, s_count * sizeof(double)));
@@ -2776,8 +2785,14 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
         }
         st = fold(ring_segs, S);
         planes_on_ = planes;
+        planes_fresh_ = fresh;
         if (st.code == CYC_OK) st = fold(user_segs, fused && pending ? S_pend_ : S);
         planes_on_ = false;
+        planes_fresh_ = false;
+        if (st.code == CYC_OK && fresh) {
+            launch_clear_if_rejected(S, (int64_t)c_.channels * t_pad_ * Pf_ * 4, key_dev_, cs_);
+            launches_ += 1;
+        }
         const int batches = (int)((user_segs.size() + TC_SEGS - 1) / TC_SEGS);
         if (st.code == CYC_OK && fused && (chk_fail_ || chk_launches_ != batches))
             st = Status{CYC_ERR_CUDA, "fused finite check: a checking launch missed lb = 0 groups", -1};

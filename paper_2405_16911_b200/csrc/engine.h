@@ -419,6 +419,8 @@ private:
         int nslots, b, e;
     };
     std::vector<std::pair<RowsKey, FinalRow*>> rows_cache_;
+    bool clear_req_ = false;     // enqueue_gated -> fold_device_chunk: the reset's clear is due
+    bool planes_fresh_ = false;  // the planes reduce overwrites (first writer of a fresh state)
     int lag_b_ = 0, lag_e_ = 0;  // block finalize lag slice [lag_b_, lag_e_) (cyc_set_lag_slice)
     std::unique_ptr<FoldInline> inline_;  // by-value descriptors of the next fold launch
     std::unique_ptr<TcParams> tcp_;       // by-value descriptors of the next tensor-core fold launch

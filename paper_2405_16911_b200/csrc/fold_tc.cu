@@ -1228,7 +1228,9 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
     const int tg = L.tc_pairs == 1 ? (2 * g.lb + (res >> 6)) * 64 + lag : g.lb * (L.tc_pairs == 2 ? 128 : 64) + lag;
     if (rg >= L.Pf || tg >= L.t_pad) return;
     double2* dst = reinterpret_cast<double2*>(L.S + (((size_t)slot * L.t_pad + tg) * (size_t)L.Pf + (size_t)rg) * 4);
-    const double2 d0 = dst[0], d1 = dst[1];
+    // overwrite: the first writer of a freshly reset state (planes path) -- no
+    // clear pass and no read of the old zeros
+    const double2 d0 = L.overwrite ? make_double2(0.0, 0.0) : dst[0], d1 = L.overwrite ? make_double2(0.0, 0.0) : dst[1];
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
     // the group's tiles are t0, t0 + stride, ... < t1 (stride 1: contiguous;
     // the planes path launches range-major, stride = its group count)

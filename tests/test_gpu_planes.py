@@ -85,6 +85,38 @@ def test_planes_split_rejects_chunk(cyc, where):
         assert np.max(np.abs(est.average(flag=fl) - ref_est.average(flag=fl))) <= 1e-12
 
 
+def test_planes_fresh_state_rejection_leaves_zeros(cyc):
+    """After reset the planes reduce overwrites the state instead of clearing
+    it first; a rejected first chunk must still leave the reset (zero) state:
+    the next chunk then gives the tables of an estimator that only saw it.
+    (Two 64-lag blocks: the planes path; three would take the fused kernel.)"""
+    N, lags = 1024, list(range(128))
+    good = rand_c(N * 300, 930)
+    more = rand_c(N * 400, 931)
+    bad = rand_c(N * 700, 932)
+    bad[4321] = np.nan
+    ref_est, est = cyc.CyclicCorrelator(cfg(cyc, N, lags)), cyc.CyclicCorrelator(cfg(cyc, N, lags))
+    g, m, b = dev(good), dev(more), dev(bad)
+    # both accumulator buffers (reset alternates them) hold sums, and the
+    # reset's clear is due
+    est.push_device(g.data_ptr(), len(good))
+    est.reset()
+    est.push_device(g.data_ptr(), len(good))
+    est.reset()
+    with pytest.raises(cyc.DataError) as ei:
+        est.push_device(b.data_ptr(), len(bad))
+    assert ei.value.index == 4321 and est.consumed() == 0
+    est.push_device(m.data_ptr(), len(more))
+    ref_est.push_device(m.data_ptr(), len(more))
+    for fl in (cyc.Flags.CONV, cyc.Flags.CONJ):
+        assert np.max(np.abs(est.average(flag=fl) - ref_est.average(flag=fl))) <= 1e-12
+    # and the accepted fresh path (reset + one chunk) equals a new estimator's
+    est.reset()
+    est.push_device(m.data_ptr(), len(more))
+    for fl in (cyc.Flags.CONV, cyc.Flags.CONJ):
+        assert np.max(np.abs(est.average(flag=fl) - ref_est.average(flag=fl))) <= 1e-12
+
+
 def test_planes_matches_fused_converters(cyc):
     """The planes path and the fused-converter path compute the same products
     (same split arithmetic); tile boundaries differ, so they agree to fp32
