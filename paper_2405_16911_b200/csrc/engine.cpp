@@ -2720,8 +2720,8 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
     // The reset's clear: on the side stream (every write of S below waits for
     // its scan event), or -- a fresh state folded by the planes path alone --
     // no clear at all: the planes reduce is the first writer of every cell and
-    // overwrites (no 64 MiB memset, no read of the zeros at C5), and a rejected
-    // chunk (its reduces skip themselves) clears the state behind the verdict.
+    // overwrites (no 64 MiB memset, no read of the zeros at C5); behind a
+    // rejecting verdict it writes the zeros instead.
     const bool fresh = clear_req_ && planes && !planes2_ && ring_segs.empty() && S == S_main_;
     if (clear_req_ && !fresh)
         CK(cudaMemsetAsync(S_main_, 0, (size_t)c_.channels * t_pad_ * Pf_ * 4 * sizeof(double), vs_));
@@ -2789,10 +2789,7 @@ Status Engine::fold_device_chunk(const float2* x, const float2* y, size_t n, dou
         if (st.code == CYC_OK) st = fold(user_segs, fused && pending ? S_pend_ : S);
         planes_on_ = false;
         planes_fresh_ = false;
-        if (st.code == CYC_OK && fresh) {
-            launch_clear_if_rejected(S, (int64_t)c_.channels * t_pad_ * Pf_ * 4, key_dev_, cs_);
-            launches_ += 1;
-        }
+
         const int batches = (int)((user_segs.size() + TC_SEGS - 1) / TC_SEGS);
         if (st.code == CYC_OK && fused && (chk_fail_ || chk_launches_ != batches))
             st = Status{CYC_ERR_CUDA, "fused finite check: a checking launch missed lb = 0 groups", -1};

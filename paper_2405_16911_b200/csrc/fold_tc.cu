@@ -1215,7 +1215,10 @@ struct TcRed {
 template <int MG>
 __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const __grid_constant__ TcRed<MG> R) {
     pdl_wait();  // the fold's partials (PDL launch: scheduled during the fold's tail)
-    if (L.gate && *L.gate != ~0ull) return;
+    // a rejected chunk: the state is left as it was -- or, for an overwriting
+    // reduce (the first writer of a freshly reset state), as the reset's zeros
+    const bool rejected = L.gate && *L.gate != ~0ull;
+    if (rejected && !L.overwrite) return;
     const FoldGroup g = R.groups[blockIdx.y];
     const int slot = R.slot[blockIdx.y];
     const int e = blockIdx.x * blockDim.x + threadIdx.x;  // lag * TRB + residue (pairs: 2 x 64 residues)
@@ -1231,6 +1234,11 @@ __global__ void __launch_bounds__(256) fold_tc_reduce_kernel(FoldLaunch L, const
     // overwrite: the first writer of a freshly reset state (planes path) -- no
     // clear pass and no read of the old zeros
     const double2 d0 = L.overwrite ? make_double2(0.0, 0.0) : dst[0], d1 = L.overwrite ? make_double2(0.0, 0.0) : dst[1];
+    if (rejected) {
+        dst[0] = d0;
+        dst[1] = d1;
+        return;
+    }
     const float4* part = reinterpret_cast<const float4*>(L.partials) + e;
     // the group's tiles are t0, t0 + stride, ... < t1 (stride 1: contiguous;
     // the planes path launches range-major, stride = its group count)

@@ -341,8 +341,6 @@ int direct_lanes(int T);  // sample lanes per lag of the direct kernel (1 for lo
 
 // Utilities.
 // gate non-null: adds only if *gate == ~0 (the chunk's finite check passed).
-// dst[0, n) = 0 unless *gate == ~0 (the chunk's finite scan found nothing)
-void launch_clear_if_rejected(double* dst, int64_t n, const unsigned long long* gate, cudaStream_t st);
 void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st,
                     const unsigned long long* gate = nullptr);
 void launch_accum_frames(const double2* frames, int64_t n_frames, int64_t len,

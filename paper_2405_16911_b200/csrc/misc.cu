@@ -149,19 +149,8 @@ int grid_for(int64_t n, int threads) {
     return g < 1 ? 1 : (int)g;
 }
 
-__global__ void clear_if_rejected_kernel(double* dst, int64_t n, const unsigned long long* gate) {
-    if (*gate == ~0ull) return;  // accepted: the overwriting reduce wrote every cell
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = 0.0;
-}
-
 }  // namespace
 
-// A rejected chunk's overwriting reduce skipped itself: the reset state must
-// still read as zeros.  Accepted chunks exit at once.
-void launch_clear_if_rejected(double* dst, int64_t n, const unsigned long long* gate, cudaStream_t st) {
-    if (n > 0) clear_if_rejected_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, n, gate);
-}
 
 void launch_add_f64(double* dst, const double* src, int64_t n, cudaStream_t st, const unsigned long long* gate) {
     if (n > 0) add_f64_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, src, n, gate);
