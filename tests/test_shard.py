@@ -213,6 +213,26 @@ def test_lag_slice_finalize_matches_full_average(cyc):
 
 
 @pytest.mark.gpu
+def test_lag_slice_finalize_set_mode_alpha_major(cyc):
+    """The lag slice in the alpha-major Set layout ([alpha][lag]): the host copy
+    is a strided column band; rows of other lags untouched."""
+    x = rand_c(1 << 18, 9)
+    alphas = [k / 64 for k in range(-8, 8)]
+    est = cyc.CyclicCorrelator(cyc.EstimatorConfig(mode=cyc.Mode.Set, win_len=256, alphas=alphas,
+                                                   lag_spec=cyc.LagSpec.Symmetric(7), flags=cyc.Flags.BOTH,
+                                                   emit_frames=False))
+    est.push(x)
+    full = est.average_all()  # [1, 2, A * (2M + 1)] alpha-major
+    A, T = len(alphas), 15
+    est.set_lag_slice(3, 9)
+    host = np.full_like(full, np.nan)
+    est.average_all(out=host)
+    g, f = host.reshape(2, A, T), full.reshape(2, A, T)
+    assert np.array_equal(g[:, :, 3:9], f[:, :, 3:9])
+    assert np.isnan(g[:, :, :3]).all() and np.isnan(g[:, :, 9:]).all()
+
+
+@pytest.mark.gpu
 def test_time_shards_on_device_sum_to_whole_record(cyc):
     """Single-GPU emulation of the NCCL exchange: per-shard estimators with
     origin, fold states summed with torch, frames added."""
