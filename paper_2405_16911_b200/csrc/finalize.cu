@@ -108,6 +108,40 @@ __device__ __forceinline__ void fft_pass(V* buf, const V* tp, int Pf, int h, int
     __syncthreads();
 }
 
+// The same pass with each level's base twiddle computed as W^k = T1[k >> 6] *
+// T2[k & 63] (T1[a] = W^{64a}, T2[b] = W^b: 1 KB at Pf = 8192 instead of the
+// 41 KB of per-pass tables), so three 8192-point fp32 rows fit an SM.
+template <int LOG2R, class V>
+__device__ __forceinline__ void fft_pass_f(V* buf, const V* t2, const V* t1, int Pf, int h, int sh) {
+    constexpr int R = 1 << LOG2R;
+    for (int g = threadIdx.x; g < Pf / R; g += blockDim.x) {
+        const int base = (g / h) * (R * h), pos = g - (g / h) * h;
+        V v[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) v[k] = buf[padi(base + pos + k * h, sh)];
+#pragma unroll
+        for (int l = 0; l < LOG2R; ++l) {
+            const int kk = pos * (Pf / (2 * (h << l)));
+            const V b0 = cmul(t1[kk >> 6], t2[kk & 63]);
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                if (k & (1 << l)) continue;
+                const int m = k & ((1 << l) - 1);
+                const V w = m == 0 ? b0 : rot16(b0, m << (3 - l));
+                const V b = v[k + (1 << l)];
+                const V t = cmul(b, w);
+                v[k + (1 << l)].x = v[k].x - t.x;
+                v[k + (1 << l)].y = v[k].y - t.y;
+                v[k].x += t.x;
+                v[k].y += t.y;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[padi(base + pos + k * h, sh)] = v[k];
+    }
+    __syncthreads();
+}
+
 // The pass sequence of a row (shared by the kernel and the host's shared-memory
 // size): radix-16 passes when the block has enough groups of 16 (else radix-4),
 // then one pass of the remaining levels; fn(log2r, h) per pass.
@@ -128,10 +162,11 @@ __host__ __device__ inline int fft_tw_entries(int log2Pf, int nthreads) {
 // One CTA per (row, flag): the row's combined
 // correlations in bit-reversed order, then radix-16 passes (four radix-2
 // levels each, in registers) and a final pass of the remaining levels.
-template <class V>
-__global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
+template <class V, bool FACT>
+__global__ void __launch_bounds__(FACT ? 256 : 512, FACT ? 3 : (sizeof(V) == 8 ? 2 : 1))
+    finalize_fft_kernel(FinalizeLaunch L, int log2Pf) {
     extern __shared__ __align__(16) uint8_t fft_smem[];
-    V* buf = reinterpret_cast<V*>(fft_smem);  // Pf + Pf/16 + 8 points (padded), then Pf/2 twiddles
+    V* buf = reinterpret_cast<V*>(fft_smem);  // Pf + Pf/16 + 8 points (padded), then the twiddle tables
     __shared__ FinalRow s_row;                // descriptors may be in mapped host memory: read once
     const int Pf = L.Pf;
     const int sh = max(log2Pf - 3, 1);
@@ -141,7 +176,10 @@ __global__ void __launch_bounds__(512, sizeof(V) == 8 ? 2 : 1) finalize_fft_kern
     const int nflag = (L.flags == 3) ? 2 : 1;
     const int row_i = blockIdx.x / nflag, fi = blockIdx.x % nflag;  // fi: index among requested flags
     if (threadIdx.x == 0) s_row = L.rows[row_i];
-    {
+    if (FACT) {  // T2[b] = W^b (b < 64), then T1[a] = W^{64 a} (a < Pf / 128)
+        for (int i = threadIdx.x; i < 64 + (Pf >> 7); i += blockDim.x)
+            tw[i] = to_v<V>(__ldg(L.tw + (i < 64 ? i : 64 * (i - 64))));
+    } else {
         // the per-pass tables follow the Pf plain twiddles (fft_pass_twiddles, built on the host)
         const double2* twp = L.tw + Pf;
         const int ntw = fft_tw_entries(log2Pf, blockDim.x);
@@ -198,11 +236,20 @@ constexpr int FFT_U = 2;
         int off = 0;
         fft_passes(log2Pf, blockDim.x, [&](int r, int h) {
             const V* tp = tw + off;
-            switch (r) {
-                case 4: fft_pass<4>(buf, tp, Pf, h, sh); break;
-                case 3: fft_pass<3>(buf, tp, Pf, h, sh); break;
-                case 2: fft_pass<2>(buf, tp, Pf, h, sh); break;
-                default: fft_pass<1>(buf, tp, Pf, h, sh); break;
+            if (FACT) {
+                switch (r) {
+                    case 4: fft_pass_f<4>(buf, tw, tw + 64, Pf, h, sh); break;
+                    case 3: fft_pass_f<3>(buf, tw, tw + 64, Pf, h, sh); break;
+                    case 2: fft_pass_f<2>(buf, tw, tw + 64, Pf, h, sh); break;
+                    default: fft_pass_f<1>(buf, tw, tw + 64, Pf, h, sh); break;
+                }
+            } else {
+                switch (r) {
+                    case 4: fft_pass<4>(buf, tp, Pf, h, sh); break;
+                    case 3: fft_pass<3>(buf, tp, Pf, h, sh); break;
+                    case 2: fft_pass<2>(buf, tp, Pf, h, sh); break;
+                    default: fft_pass<1>(buf, tp, Pf, h, sh); break;
+                }
             }
             off += r * h;
         });
@@ -370,18 +417,26 @@ template <class V>
 static int fft_smem_max() {  // Pf = 8192 at 512 threads: the largest row
     return (8192 + 512 + 8 + fft_tw_entries(13, 512)) * (int)sizeof(V);
 }
+// factored twiddles (fft_pass_f): fp32 8192-point rows at 256 threads, three CTAs
+// per SM (FFT_FACT=0: the per-pass tables, 512 threads, two CTAs per SM)
+#ifndef FFT_FACT
+#define FFT_FACT 1
+#endif
+static bool fft_fact(int Pf, bool fp32) { return FFT_FACT && fp32 && Pf == 8192; }
 
-template <class V>
-static void launch_fft(const FinalizeLaunch& L, cudaStream_t st, int nflag) {
+template <class V, bool FACT>
+static void launch_fft_t(const FinalizeLaunch& L, cudaStream_t st, int nflag) {
     int lg = 0;
     while ((1 << lg) < L.Pf) ++lg;
-    // Pf = 8192: 512 threads x radix-16 groups; shorter rows: Pf / 4 threads x radix-4
-    const int nt = fft_threads(L.Pf);
-    const size_t smem = ((size_t)L.Pf + L.Pf / 16 + 8 + fft_tw_entries(lg, nt)) * sizeof(V);
+    // Pf = 8192: 512 threads x radix-16 groups (factored: 256); shorter rows: Pf / 4 threads x radix-4
+    const int nt = FACT ? 256 : fft_threads(L.Pf);
+    const size_t tw_n = FACT ? (size_t)(64 + (L.Pf >> 7)) : (size_t)fft_tw_entries(lg, nt);
+    const size_t smem = ((size_t)L.Pf + L.Pf / 16 + 8 + tw_n) * sizeof(V);
     static std::atomic<uint64_t> attr_set{0};
     if (first_on_device(attr_set))
-        cudaFuncSetAttribute(finalize_fft_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, fft_smem_max<V>());
-    launch_pdl(finalize_fft_kernel<V>, dim3((unsigned)(L.n_rows * nflag)), dim3(nt), smem, st, L, lg);
+        cudaFuncSetAttribute(finalize_fft_kernel<V, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             fft_smem_max<V>());
+    launch_pdl(finalize_fft_kernel<V, FACT>, dim3((unsigned)(L.n_rows * nflag)), dim3(nt), smem, st, L, lg);
 }
 
 void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
@@ -389,9 +444,11 @@ void launch_finalize(const FinalizeLaunch& L, cudaStream_t st) {
     const int nflag = L.flags == 3 ? 2 : 1;
     if (L.use_fft) {
         if (fft64())
-            launch_fft<double2>(L, st, nflag);
+            launch_fft_t<double2, false>(L, st, nflag);
+        else if (fft_fact(L.Pf, true))
+            launch_fft_t<float2, true>(L, st, nflag);
         else
-            launch_fft<float2>(L, st, nflag);
+            launch_fft_t<float2, false>(L, st, nflag);
     } else {
         finalize_dft_kernel<<<dim3(L.n_rows, nflag, (L.A + DFT_AB - 1) / DFT_AB), DFT_T, 0, st>>>(L);
     }
@@ -403,9 +460,11 @@ namespace cyc {
 void prepare_finalize_kernels() {
     static std::atomic<uint64_t> done{0};
     if (!first_on_device(done)) return;
-    cudaFuncSetAttribute(finalize_fft_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(finalize_fft_kernel<double2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fft_smem_max<double2>());
-    cudaFuncSetAttribute(finalize_fft_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(finalize_fft_kernel<float2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fft_smem_max<float2>());
+    cudaFuncSetAttribute(finalize_fft_kernel<float2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fft_smem_max<float2>());
 }
 }  // namespace cyc
