@@ -211,7 +211,8 @@ __global__ void __launch_bounds__(FACT ? 256 : 512, FACT ? 3 : (sizeof(V) == 8 ?
 // two residues (4 x 16-byte loads) in flight per thread: with 2 CTAs of 512
 // threads per SM more outstanding loads only congest (4: 57.9 us, 6: 59.6,
 // 2: 56.1 at C5, warm ncu)
-constexpr int FFT_U = 2;
+    // (factored rows, 3 CTAs of 256 threads: 4 residues -- 2: 52.6 us, 4: 50.0, 8: 56.8)
+    constexpr int FFT_U = FACT ? 4 : 2;
     for (int r0 = threadIdx.x; r0 < Pf; r0 += FFT_U * nb) {
         double2 v[FFT_U][2];
 #pragma unroll
