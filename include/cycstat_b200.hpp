@@ -267,6 +267,17 @@ public:
         return run([&](cyc_frame_sink s, void* u) { return cyc_push_cf32_file(h_, path.c_str(), s, u); });
     }
 
+    // Pipelined emission (cyc_set_emit_pipeline; no reference counterpart): with
+    // depth 1 a push that completes frames only enqueues them and a later push
+    // (or flush_frames) returns them, same order and values.
+    void set_emit_pipeline(int depth) {
+        const int rc = cyc_set_emit_pipeline(h_, depth);
+        if (rc) detail::raise(rc, cyc_last_error(h_), cyc_data_error_index(h_));
+    }
+    std::vector<CyclicFrame> flush_frames() {
+        return run([&](cyc_frame_sink s, void* u) { return cyc_flush_frames(h_, s, u); });
+    }
+
     // average_frames over every frame emitted so far, without materialising them
     std::vector<cx> average(AverageMode mode = AverageMode::Coherent, int flag = 0, int channel = 0) {
         std::vector<cx> out(layout_len(layout_));

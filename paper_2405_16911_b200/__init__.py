@@ -163,6 +163,8 @@ def lib() -> C.CDLL:
     L.cyc_fold_state.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), C.POINTER(C.c_uint64)]
     L.cyc_fold_set_frames.argtypes = [vp, C.c_uint64]
     L.cyc_set_lag_slice.argtypes = [vp, C.c_uint32, C.c_uint32]
+    L.cyc_set_emit_pipeline.argtypes = [vp, C.c_int]
+    L.cyc_flush_frames.argtypes = [vp, _SINK, vp]
     L.cyc_average_all.argtypes = [vp, C.c_int, vp]
     L.cyc_block_average_device.argtypes = [vp, vp, vp, C.c_size_t, C.c_int, vp]
     L.cyc_push_cf32_file.argtypes = [vp, C.c_char_p, _SINK, vp]
@@ -554,6 +556,20 @@ class CyclicCorrelator:
         self._frames = []
         rc = fn(self._h, xa.ctypes.data, ya.ctypes.data if ya is not None else None, n, self._sink, None)
         self._check(rc)
+        out, self._frames = self._frames, []
+        return out
+
+    def set_emit_pipeline(self, depth: int = 1):
+        """Pipelined emission (cyc_set_emit_pipeline): with depth 1 a push that
+        completes frames only enqueues them; a later push (or flush_frames)
+        returns them, same order and values.  depth 0 restores the reference's
+        synchronous push()."""
+        self._check(self._L.cyc_set_emit_pipeline(self._h, int(depth)))
+
+    def flush_frames(self) -> list:
+        """The frame batch still in flight under pipelined emission, if any."""
+        self._frames = []
+        self._check(self._L.cyc_flush_frames(self._h, self._sink, None))
         out, self._frames = self._frames, []
         return out
 

@@ -326,6 +326,16 @@ extern "C" int cyc_set_lag_slice(cyc_est* est, uint32_t lag_begin, uint32_t lag_
     return finish(est, est->e->set_lag_slice(lag_begin, lag_end));
 }
 
+extern "C" int cyc_set_emit_pipeline(cyc_est* est, int depth) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->set_emit_pipeline(depth));
+}
+
+extern "C" int cyc_flush_frames(cyc_est* est, cyc_frame_sink sink, void* user) {
+    if (!est) return CYC_ERR_USAGE;
+    return finish(est, est->e->flush_frames(sink, user));
+}
+
 extern "C" int cyc_average_all(cyc_est* est, int avg_mode, cyc_cf64* out) {
     if (!est || !out) return CYC_ERR_USAGE;
     return finish(est, est->e->average_all(avg_mode, out));

@@ -645,6 +645,7 @@ Engine::~Engine() {
     cudaFree(dsum_main_);
     cudaFree(S_frames_);
     cudaFree(frames_dev_);
+    if (pend_.ev) cudaEventDestroy(pend_.ev);
     cudaFreeHost(frames_host_);
     cudaFree(coh_);
     cudaFree(mag_);
@@ -754,6 +755,7 @@ Status Engine::ensure_partials(size_t bytes) {
 Status Engine::ensure_frames(size_t slots) {
     const size_t per = (size_t)nflags_ * layout_len_;
     if (frames_slots_ < slots) {
+        TRY(stash_pending());
         if (frames_dev_) {
             CK(cudaStreamSynchronize(cs_));
             cudaFree(frames_dev_);
@@ -1891,6 +1893,58 @@ Status Engine::deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const 
     return Status::ok();
 }
 
+// Pipelined emission: deliver the batch in flight if its tables have landed
+// (force: wait for them).  Without a sink a forced drain keeps the frames in
+// `stash` for the next call that brings one.
+Status Engine::drain_pending(cyc_frame_sink sink, void* user, bool force) {
+    if (!pend_.live) return Status::ok();
+    if (!force) {
+        if (!sink) return Status::ok();
+        const cudaError_t q = cudaEventQuery(pend_.ev);
+        if (q == cudaErrorNotReady) return Status::ok();
+        CK(q);
+    } else {
+        CK(cudaEventSynchronize(pend_.ev));
+    }
+    if (!sink) return stash_pending();
+    pend_.live = false;
+    bool stop = false;
+    return deliver(pend_.slots, pend_.fidx, pend_.chans, sink, user, stop, pend_.tables);
+}
+
+Status Engine::stash_pending() {
+    if (!pend_.live || pend_.tables == pend_.stash.data()) return Status::ok();
+    CK(cudaEventSynchronize(pend_.ev));
+    const size_t per = (size_t)nflags_ * layout_len_;
+    pend_.stash.assign(pend_.tables, pend_.tables + pend_.slots * per);
+    pend_.tables = pend_.stash.data();
+    return Status::ok();
+}
+
+Status Engine::set_emit_pipeline(int depth) {
+    if (depth < 0 || depth > 1) {
+        Status s;
+        s.code = CYC_ERR_USAGE;
+        s.msg = "emit pipeline depth must be 0 (frames delivered by the push that completes them) or 1";
+        return s;
+    }
+    CK(cudaSetDevice(c_.device));
+    if (depth == 0) TRY(stash_pending());  // still delivered by cyc_flush_frames or the next push
+    pipeline_emit_ = depth == 1;
+    return Status::ok();
+}
+
+Status Engine::flush_frames(cyc_frame_sink sink, void* user) {
+    CK(cudaSetDevice(c_.device));
+    if (!sink) {
+        Status s;
+        s.code = CYC_ERR_USAGE;
+        s.msg = "cyc_flush_frames needs a sink";
+        return s;
+    }
+    return drain_pending(sink, user, true);
+}
+
 // Emit every frame that became computable (estimator.cpp:59-82).
 Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target) {
     const uint64_t avail = consumed_ >= need_ ? (consumed_ - need_) / (uint64_t)N_ + 1 : 0;
@@ -1918,6 +1972,8 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                     fidx.push_back(f);
                 }
             const size_t slots = k0s.size();
+            // the batch in flight owns the pinned tables this one will overwrite
+            if (pend_.live) TRY(drain_pending(sink, user, true));
             double2* tables = frames_host_;
             if (!sink && c_.mode != CYC_MODE_RECURSIVE) {
                 // nobody receives the frames: keep only the running average_frames
@@ -1961,6 +2017,18 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             }
             // recursive: R_f = lam^N R_{f-1} + (weighted window sum) ran on the
             // device before the D2H
+            if (pipeline_emit_ && c_.emit_frames && sink && !stop) {
+                // pipelined emission: the tables land behind this event; a later
+                // call delivers them (drain_pending)
+                if (!pend_.ev) CK(cudaEventCreateWithFlags(&pend_.ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(pend_.ev, cs_));
+                pend_.live = true;
+                pend_.slots = slots;
+                pend_.fidx = std::move(fidx);
+                pend_.chans = std::move(chans);
+                pend_.tables = tables;
+                continue;
+            }
             CK(cudaStreamSynchronize(cs_));
             if (c_.emit_frames && !stop) TRY(deliver(slots, fidx, chans, sink, user, stop, tables));
         }
@@ -2042,6 +2110,7 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         return s;
     }
     if (!pre && deferred_ok(kind, n, yv)) return push_deferred(xv, yv, n, sink, user);
+    if (pend_.live) TRY(drain_pending(sink, user, false));
     TRY(flush_deferred());  // the other paths read and write the rings directly
     const int C = c_.channels;
     const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
@@ -2175,9 +2244,12 @@ Status Engine::push_deferred(const void* xv, const void* yv, size_t n, cyc_frame
         hprof(2);
         TRY(emit_new_frames(sink, user, S_main_));
         hprof(3);
-    } else if (origin_ + (int64_t)consumed_ - dma_to_ >= dflush_) {
-        TRY(flush_deferred());
-        hprof(2);
+    } else {
+        if (origin_ + (int64_t)consumed_ - dma_to_ >= dflush_) {
+            TRY(flush_deferred());
+            hprof(2);
+        }
+        if (pend_.live) TRY(drain_pending(sink, user, false));
     }
     return cuda_check(cudaGetLastError(), "push");
 }
@@ -3135,6 +3207,10 @@ Status Engine::set_frames(uint64_t frames) {
 Status Engine::reset() {
     prevalidated_ptr_ = nullptr;
     CK(cudaSetDevice(c_.device));
+    if (pend_.live) {  // frames of the old stream nobody flushed are dropped
+        CK(cudaEventSynchronize(pend_.ev));
+        pend_.live = false;
+    }
     if (timeline_on()) {
         tl_resolve(false);
         tl_steps_.emplace_back();

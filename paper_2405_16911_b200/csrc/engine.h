@@ -84,6 +84,12 @@ public:
     Status fold_state(void** dev_ptr, size_t* count, uint64_t* frames);
     Status set_frames(uint64_t frames);
     Status set_lag_slice(uint32_t b, uint32_t e);
+    // Pipelined emission (cyc_set_emit_pipeline / cyc_flush_frames): one frame
+    // batch stays in flight on the GPU while the caller's next pushes are
+    // copied and screened; its frames reach the sink of the first later call
+    // that finds them complete.
+    Status set_emit_pipeline(int depth);
+    Status flush_frames(cyc_frame_sink sink, void* user);
     // Fold-kernel timing with CUDA events on the compute stream.
     void set_profiling(bool on) { prof_ = on; }
     Status profile_read(uint64_t* launches, double* ms, double* flops, double* exec_flops = nullptr,
@@ -323,6 +329,21 @@ private:
     double2* frames_dev_ = nullptr;   // per-frame tables [slot][nflags][layout]
     size_t frames_slots_ = 0;
     double2* frames_host_ = nullptr;  // pinned
+    // the frame batch in flight under pipelined emission: its tables land in
+    // pinned host memory behind `ev`; `stash` holds them if that memory has to
+    // be reallocated before delivery
+    struct PendingEmit {
+        bool live = false;
+        cudaEvent_t ev = nullptr;
+        size_t slots = 0;
+        std::vector<uint64_t> fidx;
+        std::vector<int> chans;
+        const double2* tables = nullptr;
+        std::vector<double2> stash;
+    } pend_;
+    bool pipeline_emit_ = false;
+    Status drain_pending(cyc_frame_sink sink, void* user, bool force);
+    Status stash_pending();
     double2* coh_ = nullptr;          // running coherent sums [channels][nflags][layout]
     double* mag_ = nullptr;           // running magnitude sums
     double2* avg_dev_ = nullptr;      // average scratch

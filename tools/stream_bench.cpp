@@ -98,6 +98,11 @@ int main(int argc, char** argv) {
         ests.push_back(make(CYC_MODE_RECURSIVE, 0, 65536, al, 0, 0, lags, 1.0 - 1.0 / 4096.0));
         chunk = 8192;
     }
+    // CYC_EMIT_PIPELINE=0: the reference's synchronous push() (frames delivered
+    // by the push that completes them); default: one emission in flight
+    const char* pe = std::getenv("CYC_EMIT_PIPELINE");
+    const int depth = pe ? std::atoi(pe) : 1;
+    for (auto* e : ests) cyc_set_emit_pipeline(e, depth);
     Sink sink;
     auto step = [&]() {
         for (auto* e : ests) cyc_reset(e);
@@ -111,7 +116,10 @@ int main(int argc, char** argv) {
                 }
             }
         }
-        for (auto* e : ests) cyc_synchronize(e);
+        for (auto* e : ests) {
+            cyc_flush_frames(e, sink_fn, &sink);
+            cyc_synchronize(e);
+        }
     };
     for (int i = 0; i < warmup; ++i) step();
     cudaStream_t st = static_cast<cudaStream_t>(cyc_stream(ests[0]));
