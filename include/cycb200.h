@@ -256,15 +256,17 @@ int cyc_fold_set_frames(cyc_est* est, uint64_t frames);
 int cyc_set_lag_slice(cyc_est* est, uint32_t lag_begin, uint32_t lag_end);
 /* Pipelined emission for small-call streams (per-frame and recursive modes).
  * depth 0 (default): a push delivers the frames it completes before it returns
- * (CyclicCorrelator::push, estimator.cpp:59-82).  depth 1: the push that
- * completes a frame batch only enqueues its GPU work; the frames go to the sink
- * of the first later cyc_push that finds them finished (at the latest the push
- * that completes the next batch), or to cyc_flush_frames, so the GPU round trip
- * of an emission overlaps the caller's next chunks.  Frame order, indices and
- * values are those of depth 0.  cyc_reset drops a batch nobody flushed.
- * No reference counterpart (the reference computes frames inside push()). */
+ * (CyclicCorrelator::push, estimator.cpp:59-82).  depth 1 or 2: the push that
+ * completes a frame batch only enqueues its GPU work, and up to `depth` batches
+ * stay in flight (CUDA-graph replayed batches: one); their frames go, oldest
+ * first, to the sink of the first later cyc_push that finds them finished (at
+ * the latest the push that would exceed the depth) or to cyc_flush_frames, so
+ * the GPU round trip of an emission overlaps the caller's next chunks.  Frame
+ * order, indices and values are those of depth 0.  cyc_reset drops batches
+ * nobody flushed.  No reference counterpart (the reference computes frames
+ * inside push()). */
 int cyc_set_emit_pipeline(cyc_est* est, int depth);
-/* Wait for the frame batch in flight (if any) and deliver it to `sink`. */
+/* Wait for the frame batches in flight (if any) and deliver them to `sink`. */
 int cyc_flush_frames(cyc_est* est, cyc_frame_sink sink, void* user);
 
 /* CSV export of results (proj/src/io.cpp:161-208, the reference's

@@ -268,7 +268,7 @@ public:
     }
 
     // Pipelined emission (cyc_set_emit_pipeline; no reference counterpart): with
-    // depth 1 a push that completes frames only enqueues them and a later push
+    // depth 1 or 2 a push that completes frames only enqueues them and a later push
     // (or flush_frames) returns them, same order and values.
     void set_emit_pipeline(int depth) {
         const int rc = cyc_set_emit_pipeline(h_, depth);

@@ -560,7 +560,7 @@ class CyclicCorrelator:
         return out
 
     def set_emit_pipeline(self, depth: int = 1):
-        """Pipelined emission (cyc_set_emit_pipeline): with depth 1 a push that
+        """Pipelined emission (cyc_set_emit_pipeline): with depth 1 or 2 a push that
         completes frames only enqueues them; a later push (or flush_frames)
         returns them, same order and values.  depth 0 restores the reference's
         synchronous push()."""

@@ -645,7 +645,8 @@ Engine::~Engine() {
     cudaFree(dsum_main_);
     cudaFree(S_frames_);
     cudaFree(frames_dev_);
-    if (pend_.ev) cudaEventDestroy(pend_.ev);
+    for (auto& p : pendq_) cudaEventDestroy(p.ev);
+    cudaFreeHost(frames_host_alt_);
     cudaFreeHost(frames_host_);
     cudaFree(coh_);
     cudaFree(mag_);
@@ -764,6 +765,9 @@ Status Engine::ensure_frames(size_t slots) {
         frames_slots_ = slots;
         CK(cudaMalloc(&frames_dev_, frames_slots_ * per * sizeof(double2)));
         CK(cudaMallocHost(&frames_host_, frames_slots_ * per * sizeof(double2)));
+        if (frames_host_alt_) cudaFreeHost(frames_host_alt_);
+        frames_host_alt_ = nullptr;
+        if (emit_depth_ > 1) CK(cudaMallocHost(&frames_host_alt_, frames_slots_ * per * sizeof(double2)));
     }
     if (use_fold_ && S_frames_slots_ < slots) {
         if (S_frames_) {
@@ -1893,44 +1897,59 @@ Status Engine::deliver(size_t n_slots, const std::vector<uint64_t>& fidx, const 
     return Status::ok();
 }
 
-// Pipelined emission: deliver the batch in flight if its tables have landed
-// (force: wait for them).  Without a sink a forced drain keeps the frames in
-// `stash` for the next call that brings one.
-Status Engine::drain_pending(cyc_frame_sink sink, void* user, bool force) {
-    if (!pend_.live) return Status::ok();
-    if (!force) {
-        if (!sink) return Status::ok();
-        const cudaError_t q = cudaEventQuery(pend_.ev);
-        if (q == cudaErrorNotReady) return Status::ok();
-        CK(q);
-    } else {
-        CK(cudaEventSynchronize(pend_.ev));
+// Pipelined emission: deliver, oldest first, the batches whose tables have
+// landed, waiting for those beyond the `keep` newest that still hold pinned
+// tables.  Without a sink those are kept in their own `stash` for the next call
+// that brings one.
+Status Engine::drain_pending(cyc_frame_sink sink, void* user, size_t keep) {
+    size_t holders = 0;
+    for (const auto& p : pendq_) holders += !p.stashed;
+    if (!sink) return holders > keep ? stash_pending() : Status::ok();
+    while (!pendq_.empty()) {
+        PendingEmit& p = pendq_.front();
+        if (!p.stashed) {
+            if (holders > keep) {
+                CK(cudaEventSynchronize(p.ev));
+            } else {
+                const cudaError_t q = cudaEventQuery(p.ev);
+                if (q == cudaErrorNotReady) break;
+                CK(q);
+            }
+            --holders;
+        }
+        PendingEmit done = std::move(p);
+        pendq_.pop_front();
+        ev_pool_.push_back(done.ev);
+        bool stop = false;
+        TRY(deliver(done.slots, done.fidx, done.chans, sink, user, stop,
+                    done.stashed ? done.stash.data() : done.tables));
     }
-    if (!sink) return stash_pending();
-    pend_.live = false;
-    bool stop = false;
-    return deliver(pend_.slots, pend_.fidx, pend_.chans, sink, user, stop, pend_.tables);
+    return Status::ok();
 }
 
 Status Engine::stash_pending() {
-    if (!pend_.live || pend_.tables == pend_.stash.data()) return Status::ok();
-    CK(cudaEventSynchronize(pend_.ev));
     const size_t per = (size_t)nflags_ * layout_len_;
-    pend_.stash.assign(pend_.tables, pend_.tables + pend_.slots * per);
-    pend_.tables = pend_.stash.data();
+    for (auto& p : pendq_) {
+        if (p.stashed) continue;
+        CK(cudaEventSynchronize(p.ev));
+        p.stash.assign(p.tables, p.tables + p.slots * per);
+        p.stashed = true;
+    }
     return Status::ok();
 }
 
 Status Engine::set_emit_pipeline(int depth) {
-    if (depth < 0 || depth > 1) {
+    if (depth < 0 || depth > 2) {
         Status s;
         s.code = CYC_ERR_USAGE;
-        s.msg = "emit pipeline depth must be 0 (frames delivered by the push that completes them) or 1";
+        s.msg = "emit pipeline depth must be 0 (frames delivered by the push that completes them), 1 or 2";
         return s;
     }
     CK(cudaSetDevice(c_.device));
-    if (depth == 0) TRY(stash_pending());  // still delivered by cyc_flush_frames or the next push
-    pipeline_emit_ = depth == 1;
+    if (depth < emit_depth_) TRY(stash_pending());  // still delivered by cyc_flush_frames or the next push
+    emit_depth_ = depth;
+    if (depth > 1 && frames_host_ && !frames_host_alt_)
+        CK(cudaMallocHost(&frames_host_alt_, frames_slots_ * (size_t)nflags_ * layout_len_ * sizeof(double2)));
     return Status::ok();
 }
 
@@ -1942,7 +1961,7 @@ Status Engine::flush_frames(cyc_frame_sink sink, void* user) {
         s.msg = "cyc_flush_frames needs a sink";
         return s;
     }
-    return drain_pending(sink, user, true);
+    return drain_pending(sink, user, 0);
 }
 
 // Emit every frame that became computable (estimator.cpp:59-82).
@@ -1972,8 +1991,13 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                     fidx.push_back(f);
                 }
             const size_t slots = k0s.size();
-            // the batch in flight owns the pinned tables this one will overwrite
-            if (pend_.live) TRY(drain_pending(sink, user, true));
+            // batches in flight own the pinned tables: a graph replay rewrites its
+            // own, the other paths alternate between two at depth 2
+            if (!pendq_.empty() || emit_depth_ > 1) {
+                const size_t depth = graph_eligible(slots) ? 1 : (size_t)std::max(emit_depth_, 1);
+                TRY(drain_pending(sink, user, depth - 1));
+                if (depth > 1 && frames_host_alt_) std::swap(frames_host_, frames_host_alt_);
+            }
             double2* tables = frames_host_;
             if (!sink && c_.mode != CYC_MODE_RECURSIVE) {
                 // nobody receives the frames: keep only the running average_frames
@@ -2017,16 +2041,17 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             }
             // recursive: R_f = lam^N R_{f-1} + (weighted window sum) ran on the
             // device before the D2H
-            if (pipeline_emit_ && c_.emit_frames && sink && !stop) {
+            if (emit_depth_ > 0 && c_.emit_frames && sink && !stop) {
                 // pipelined emission: the tables land behind this event; a later
                 // call delivers them (drain_pending)
-                if (!pend_.ev) CK(cudaEventCreateWithFlags(&pend_.ev, cudaEventDisableTiming));
-                CK(cudaEventRecord(pend_.ev, cs_));
-                pend_.live = true;
-                pend_.slots = slots;
-                pend_.fidx = std::move(fidx);
-                pend_.chans = std::move(chans);
-                pend_.tables = tables;
+                PendingEmit pe;
+                pe.ev = get_event();
+                CK(cudaEventRecord(pe.ev, cs_));
+                pe.slots = slots;
+                pe.fidx = std::move(fidx);
+                pe.chans = std::move(chans);
+                pe.tables = tables;
+                pendq_.push_back(std::move(pe));
                 continue;
             }
             CK(cudaStreamSynchronize(cs_));
@@ -2110,7 +2135,7 @@ Status Engine::push(const void* xv, const void* yv, size_t n, int kind, cyc_fram
         return s;
     }
     if (!pre && deferred_ok(kind, n, yv)) return push_deferred(xv, yv, n, sink, user);
-    if (pend_.live) TRY(drain_pending(sink, user, false));
+    if (!pendq_.empty()) TRY(drain_pending(sink, user, ~(size_t)0));
     TRY(flush_deferred());  // the other paths read and write the rings directly
     const int C = c_.channels;
     const bool block_fold = !c_.emit_frames && c_.mode != CYC_MODE_RECURSIVE && use_fold_;
@@ -2249,7 +2274,7 @@ Status Engine::push_deferred(const void* xv, const void* yv, size_t n, cyc_frame
             TRY(flush_deferred());
             hprof(2);
         }
-        if (pend_.live) TRY(drain_pending(sink, user, false));
+        if (!pendq_.empty()) TRY(drain_pending(sink, user, ~(size_t)0));
     }
     return cuda_check(cudaGetLastError(), "push");
 }
@@ -3207,10 +3232,11 @@ Status Engine::set_frames(uint64_t frames) {
 Status Engine::reset() {
     prevalidated_ptr_ = nullptr;
     CK(cudaSetDevice(c_.device));
-    if (pend_.live) {  // frames of the old stream nobody flushed are dropped
-        CK(cudaEventSynchronize(pend_.ev));
-        pend_.live = false;
+    for (auto& p : pendq_) {  // frames of the old stream nobody flushed are dropped
+        if (!p.stashed) CK(cudaEventSynchronize(p.ev));
+        ev_pool_.push_back(p.ev);
     }
+    pendq_.clear();
     if (timeline_on()) {
         tl_resolve(false);
         tl_steps_.emplace_back();

@@ -329,20 +329,22 @@ private:
     double2* frames_dev_ = nullptr;   // per-frame tables [slot][nflags][layout]
     size_t frames_slots_ = 0;
     double2* frames_host_ = nullptr;  // pinned
-    // the frame batch in flight under pipelined emission: its tables land in
-    // pinned host memory behind `ev`; `stash` holds them if that memory has to
-    // be reallocated before delivery
+    // frame batches in flight under pipelined emission (oldest first): the
+    // tables land in pinned host memory behind `ev`; `stash` holds them once
+    // that memory had to be handed on before a sink came by
     struct PendingEmit {
-        bool live = false;
         cudaEvent_t ev = nullptr;
         size_t slots = 0;
         std::vector<uint64_t> fidx;
         std::vector<int> chans;
         const double2* tables = nullptr;
+        bool stashed = false;
         std::vector<double2> stash;
-    } pend_;
-    bool pipeline_emit_ = false;
-    Status drain_pending(cyc_frame_sink sink, void* user, bool force);
+    };
+    std::deque<PendingEmit> pendq_;
+    int emit_depth_ = 0;                 // cyc_set_emit_pipeline
+    double2* frames_host_alt_ = nullptr; // depth 2: the batches alternate between two pinned tables
+    Status drain_pending(cyc_frame_sink sink, void* user, size_t keep);
     Status stash_pending();
     double2* coh_ = nullptr;          // running coherent sums [channels][nflags][layout]
     double* mag_ = nullptr;           // running magnitude sums

@@ -42,6 +42,7 @@ def test_recursive_small_calls_pipelined(cyc, oracle):
     pipe, pp1, tail1, _ = run_stream(cyc, cfg, x, 512, 1)
     assert tail0 == 0
     same_frames(pipe, sync)
+    same_frames(run_stream(cyc, cfg, x, 512, 2)[0], sync)
     # no pipelined push returns a frame earlier than the push that completes it
     assert all(sum(pp1[:i + 1]) <= sum(pp0[:i + 1]) for i in range(len(pp0)))
     want = oracle.recursive(x.astype(complex), x.astype(complex), alphas, lags, False, lam, E)
@@ -49,8 +50,9 @@ def test_recursive_small_calls_pipelined(cyc, oracle):
     assert_parity(got, want, mean_power(x), what="recursive pipelined")
 
 
+@pytest.mark.parametrize("depth", [1, 2])
 @pytest.mark.parametrize("chunk", [64, 100, 1000])
-def test_set_frames_pipelined(cyc, oracle, chunk):
+def test_set_frames_pipelined(cyc, oracle, chunk, depth):
     # the C1 call pattern: one Set frame per push (chunk == N), ragged and multi-frame pushes
     x = rand_c(3000, 11)
     y = rand_c(3000, 12)
@@ -58,7 +60,7 @@ def test_set_frames_pipelined(cyc, oracle, chunk):
     cfg = cyc.EstimatorConfig(mode=cyc.Mode.Set, win_len=64, alphas=alphas, lag_spec=cyc.LagSpec.Symmetric(3),
                               flags=cyc.Flags.BOTH)
     sync, _, _, e0 = run_stream(cyc, cfg, x, chunk, 0, y)
-    pipe, _, _, e1 = run_stream(cyc, cfg, x, chunk, 1, y)
+    pipe, _, _, e1 = run_stream(cyc, cfg, x, chunk, depth, y)
     same_frames(pipe, sync)
     for conj, flag in ((False, cyc.Flags.CONV), (True, cyc.Flags.CONJ)):
         want = oracle.stream(0, conj, 64, x.astype(complex), y.astype(complex), alphas=alphas, max_lag=3)
@@ -79,6 +81,8 @@ def test_full_frames_pipelined_and_depth_switch(cyc):
         if i == 10:
             est.set_emit_pipeline(0)  # the batch in flight is kept and delivered by the next push
         if i == 20:
+            est.set_emit_pipeline(2)
+        if i == 26:
             est.set_emit_pipeline(1)
         frames += est.push(x[o:o + 256])
     frames += est.flush_frames()
@@ -98,4 +102,18 @@ def test_reset_drops_the_batch_in_flight(cyc):
     ref, _, _, _ = run_stream(cyc, cfg, x[:300], 300, 0)
     same_frames(again, ref)
     with pytest.raises(cyc.UsageError):
-        est.set_emit_pipeline(2)
+        est.set_emit_pipeline(3)
+
+
+def test_c1_geometry_depth_two(cyc):
+    # BASELINE C1's call pattern (4096-sample pushes, union alpha set, both flags): direct per-frame kernel
+    x = rand_c(40 * 4096, 31)
+    alphas = [k / 8 for k in range(-2, 3)] + [0.1 + k / 16 for k in range(-2, 3)]
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Set, win_len=4096, alphas=alphas, lag_spec=cyc.LagSpec.Symmetric(15),
+                              flags=cyc.Flags.BOTH)
+    sync, _, _, e0 = run_stream(cyc, cfg, x, 4096, 0)
+    pipe, pp, tail, e2 = run_stream(cyc, cfg, x, 4096, 2)
+    same_frames(pipe, sync)
+    assert tail >= 2  # frames were still in flight at the end (both flags of at least one batch)
+    assert np.array_equal(e0.average(cyc.AverageMode.Coherent, cyc.Flags.CONV),
+                          e2.average(cyc.AverageMode.Coherent, cyc.Flags.CONV))

@@ -99,9 +99,9 @@ int main(int argc, char** argv) {
         chunk = 8192;
     }
     // CYC_EMIT_PIPELINE=0: the reference's synchronous push() (frames delivered
-    // by the push that completes them); default: one emission in flight
+    // by the push that completes them); default: up to two emissions in flight
     const char* pe = std::getenv("CYC_EMIT_PIPELINE");
-    const int depth = pe ? std::atoi(pe) : 1;
+    const int depth = pe ? std::atoi(pe) : 2;
     for (auto* e : ests) cyc_set_emit_pipeline(e, depth);
     Sink sink;
     auto step = [&]() {
