@@ -24,7 +24,7 @@ constexpr int MAXL = 4;     // lags per thread (T <= 1024)
 // (split order, fp64) into the frame's table and the running sums -- the
 // arithmetic of direct_reduce_accum_kernel for one frame per channel.  Every
 // thread of every CTA calls this after writing its partials.
-__device__ void fused_reduce(const DirectLaunch& L, int si, int a) {
+__device__ void fused_reduce(const DirectLaunch& L, int si, int a, float2* stage, int stage_cap) {
     __shared__ int s_last;
     __threadfence();
     __syncthreads();
@@ -36,32 +36,58 @@ __device__ void fused_reduce(const DirectLaunch& L, int si, int a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const float2* part = reinterpret_cast<const float2*>(L.partials);
+    // partials of (si, a): [split][flag][lag]
+    const float2* part = reinterpret_cast<const float2*>(L.partials) + ((size_t)si * L.A + a) * L.splits * 2 * L.T;
     const int ch = si;  // one frame per channel: segment = channel
-    for (int t = threadIdx.x; t < L.T; t += blockDim.x) {
-        int fi = 0;
-        for (int f = 0; f < 2; ++f) {
-            if (!(L.flags & (1 << f))) continue;
-            const int64_t e = (int64_t)ch * L.per + (int64_t)fi * L.out_flag_stride + (int64_t)a * L.stride_a +
-                              (int64_t)t * L.stride_t;
-            double re = 0.0, im = 0.0;
-            for (int s = 0; s < L.splits; ++s) {
-                const float2 v = __ldcg(part + ((((size_t)si * L.A + a) * L.splits + s) * 2 + f) * L.T + t);
-                re += v.x;
-                im += v.y;
-            }
-            const double2 v = make_double2(re * L.scale, im * L.scale);
-            const size_t o = (size_t)si * L.out_block_stride + (size_t)fi * L.out_flag_stride +
-                             (size_t)a * L.stride_a + (size_t)t * L.stride_t;
-            L.out[o] = v;
-            if (L.out_host) L.out_host[o] = v;
-            double2 c = L.coh[e];
-            c.x += v.x;
-            c.y += v.y;
-            L.coh[e] = c;
-            L.mag[e] += hypot(v.x, v.y);
-            ++fi;
+    const int nv = L.splits * 2 * L.T;
+    // Short tables (C1: 16 splits x 2 x 31 lags): the whole CTA fetches every
+    // partial at once into shared memory -- one L2 round trip instead of one
+    // per group of splits -- and the sums below keep the split order.
+    const bool staged = nv <= stage_cap;
+    if (staged)
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) stage[i] = __ldcg(part + i);
+    auto cell = [&](int idx, int& f, int& t, int& fi, int64_t& e) -> bool {
+        f = idx / L.T;
+        t = idx - f * L.T;
+        if (idx >= 2 * L.T || !(L.flags & (1 << f))) return false;
+        fi = f == 1 && (L.flags & 1) ? 1 : 0;
+        e = (int64_t)ch * L.per + (int64_t)fi * L.out_flag_stride + (int64_t)a * L.stride_a + (int64_t)t * L.stride_t;
+        return true;
+    };
+    // only this CTA touches the running sums of (si, a): the first pass fetches
+    // them beside the partials
+    int f, t, fi;
+    int64_t e;
+    double2 c0 = make_double2(0.0, 0.0);
+    double m0 = 0.0;
+    if (cell(threadIdx.x, f, t, fi, e)) {
+        c0 = L.coh[e];
+        m0 = L.mag[e];
+    }
+    __syncthreads();  // s_last is uniform: every thread of the last CTA is here
+    for (int idx = threadIdx.x; idx < 2 * L.T; idx += blockDim.x) {
+        if (!cell(idx, f, t, fi, e)) continue;
+        double2 c = c0;
+        double m = m0;
+        if (idx != (int)threadIdx.x) {
+            c = L.coh[e];
+            m = L.mag[e];
         }
+        double re = 0.0, im = 0.0;
+        for (int s = 0; s < L.splits; ++s) {
+            const float2 v = staged ? stage[(s * 2 + f) * L.T + t] : __ldcg(part + (s * 2 + f) * L.T + t);
+            re += v.x;
+            im += v.y;
+        }
+        const double2 v = make_double2(re * L.scale, im * L.scale);
+        const size_t o = (size_t)si * L.out_block_stride + (size_t)fi * L.out_flag_stride +
+                         (size_t)a * L.stride_a + (size_t)t * L.stride_t;
+        L.out[o] = v;
+        if (L.out_host) L.out_host[o] = v;
+        c.x += v.x;
+        c.y += v.y;
+        L.coh[e] = c;
+        L.mag[e] = m + hypot(v.x, v.y);
     }
 }
 
@@ -99,13 +125,23 @@ __global__ void __launch_bounds__(DT) direct_kernel(const __grid_constant__ Dire
     for (int64_t n0 = b0; n0 < b1; n0 += TILE) {
         const int len = (int)min((int64_t)TILE, b1 - n0);
         __syncthreads();
+        // y loads first, so they are in flight beside the x loads
+        float2 yr[TILE / DT];
+#pragma unroll
+        for (int k = 0; k < TILE / DT; ++k) {
+            const int i = threadIdx.x + k * DT;
+            if (i < len) yr[k] = seg.y[(uint64_t)(n0 + i) & seg.mask];
+        }
         for (int i = threadIdx.x; i < len + span; i += DT) {
             const int64_t n = n0 + L.lag_lo + i;
             xs[i] = (n >= seg.x_lo && n < seg.x_hi) ? seg.x[(uint64_t)n & seg.mask] : make_float2(0.f, 0.f);
         }
-        for (int i = threadIdx.x; i < len; i += DT) {
+#pragma unroll
+        for (int k = 0; k < TILE / DT; ++k) {
+            const int i = threadIdx.x + k * DT;
+            if (i >= len) continue;
             const int64_t n = n0 + i;
-            float2 y = seg.y[(uint64_t)n & seg.mask];
+            float2 y = yr[k];
             if (seg.w_log2 != 0.f) {
                 const float w = seg.w_scale * exp2f((float)(seg.w_ref - n) * seg.w_log2);
                 y.x *= w;
@@ -145,7 +181,7 @@ __global__ void __launch_bounds__(DT) direct_kernel(const __grid_constant__ Dire
             part[(base + 0) * L.T + t] = accv[k];
             part[(base + 1) * L.T + t] = accj[k];
         }
-        if (L.fuse_counters) fused_reduce(L, si, a);
+        if (L.fuse_counters) fused_reduce(L, si, a, sm, 3 * TILE + span);
         return;
     }
     // lanes 1.. hand their sums to lane 0 through shared memory (reusing the
@@ -174,7 +210,7 @@ __global__ void __launch_bounds__(DT) direct_kernel(const __grid_constant__ Dire
         part[(base + 0) * L.T + t] = v;
         part[(base + 1) * L.T + t] = j;
     }
-    if (L.fuse_counters) fused_reduce(L, si, a);
+    if (L.fuse_counters) fused_reduce(L, si, a, sm, 3 * TILE + span);
 }
 
 __global__ void direct_reduce_kernel(const __grid_constant__ DirectLaunch L) {
