@@ -644,7 +644,15 @@ Engine::~Engine() {
     }
     cudaFree(dsum_main_);
     cudaFree(S_frames_);
+    if (ds_) {
+        cudaStreamSynchronize(ds_);
+        cudaStreamDestroy(ds_);
+    }
+    if (d2h_ready_) cudaEventDestroy(d2h_ready_);
+    for (int i = 0; i < 2; ++i)
+        if (d2h_done_[i]) cudaEventDestroy(d2h_done_[i]);
     cudaFree(frames_dev_);
+    cudaFree(frames_dev_alt_);
     for (auto& p : pendq_) cudaEventDestroy(p.ev);
     cudaFreeHost(frames_host_alt_);
     cudaFreeHost(frames_host_);
@@ -759,6 +767,8 @@ Status Engine::ensure_frames(size_t slots) {
         TRY(stash_pending());
         if (frames_dev_) {
             CK(cudaStreamSynchronize(cs_));
+            if (ds_) CK(cudaStreamSynchronize(ds_));
+            d2h_busy_[0] = d2h_busy_[1] = false;
             cudaFree(frames_dev_);
             cudaFreeHost(frames_host_);
         }
@@ -767,7 +777,12 @@ Status Engine::ensure_frames(size_t slots) {
         CK(cudaMallocHost(&frames_host_, frames_slots_ * per * sizeof(double2)));
         if (frames_host_alt_) cudaFreeHost(frames_host_alt_);
         frames_host_alt_ = nullptr;
-        if (emit_depth_ > 1) CK(cudaMallocHost(&frames_host_alt_, frames_slots_ * per * sizeof(double2)));
+        cudaFree(frames_dev_alt_);
+        frames_dev_alt_ = nullptr;
+        if (emit_depth_ > 1) {
+            CK(cudaMallocHost(&frames_host_alt_, frames_slots_ * per * sizeof(double2)));
+            CK(cudaMalloc(&frames_dev_alt_, frames_slots_ * per * sizeof(double2)));
+        }
     }
     if (use_fold_ && S_frames_slots_ < slots) {
         if (S_frames_) {
@@ -1600,6 +1615,7 @@ Status Engine::compute_frames(const std::vector<int64_t>& k0s, const std::vector
                               const float2* xbo, const float2* ybo, uint64_t mask_o) {
     const size_t slots = k0s.size();
     TRY(ensure_frames(slots));
+    TRY(wait_side_copies(false));
     const uint64_t mask = xbo ? mask_o : mask_;
     const float lam_log2 = recursive ? (float)std::log2(c_.lambda) : 0.f;
     const float w_scale = recursive ? (float)(1.0 - c_.lambda) : 1.f;
@@ -1950,6 +1966,25 @@ Status Engine::set_emit_pipeline(int depth) {
     emit_depth_ = depth;
     if (depth > 1 && frames_host_ && !frames_host_alt_)
         CK(cudaMallocHost(&frames_host_alt_, frames_slots_ * (size_t)nflags_ * layout_len_ * sizeof(double2)));
+    if (depth > 1 && frames_dev_ && !frames_dev_alt_)
+        CK(cudaMalloc(&frames_dev_alt_, frames_slots_ * (size_t)nflags_ * layout_len_ * sizeof(double2)));
+    return Status::ok();
+}
+
+Status Engine::side_copy_setup() {
+    if (ds_) return Status::ok();
+    CK(cudaStreamCreateWithFlags(&ds_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&d2h_ready_, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&d2h_done_[i], cudaEventDisableTiming));
+    return Status::ok();
+}
+
+Status Engine::wait_side_copies(bool both) {
+    for (int i = 0; i < (both ? 2 : 1); ++i)
+        if (d2h_busy_[i]) {
+            CK(cudaStreamWaitEvent(cs_, d2h_done_[i], 0));
+            d2h_busy_[i] = false;
+        }
     return Status::ok();
 }
 
@@ -1996,9 +2031,17 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             if (!pendq_.empty() || emit_depth_ > 1) {
                 const size_t depth = graph_eligible(slots) ? 1 : (size_t)std::max(emit_depth_, 1);
                 TRY(drain_pending(sink, user, depth - 1));
-                if (depth > 1 && frames_host_alt_) std::swap(frames_host_, frames_host_alt_);
+                if (depth > 1 && frames_host_alt_) {
+                    std::swap(frames_host_, frames_host_alt_);
+                    if (frames_dev_alt_) {
+                        std::swap(frames_dev_, frames_dev_alt_);
+                        std::swap(d2h_done_[0], d2h_done_[1]);
+                        std::swap(d2h_busy_[0], d2h_busy_[1]);
+                    }
+                }
             }
             double2* tables = frames_host_;
+            bool side_copy = false;
             if (!sink && c_.mode != CYC_MODE_RECURSIVE) {
                 // nobody receives the frames: keep only the running average_frames
                 // sums on the device (no frame D2H, no synchronisation)
@@ -2015,17 +2058,33 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             if (graph_eligible(slots)) {
                 // small frame batches: one CUDA-graph replay (fold, reduce, finalize,
                 // accumulate, D2H) instead of five launches and a memcpy
+                TRY(wait_side_copies(true));  // a graph bakes whichever device table it was captured with
                 TRY(run_frame_graph(k0s, chans, c_.mode == CYC_MODE_RECURSIVE, &tables));
             } else {
                 static const bool no_zc = std::getenv("CYC_NO_ZERO_COPY") != nullptr;  // A/B knob
+                static const bool no_side = std::getenv("CYC_NO_SIDE_COPY") != nullptr;  // A/B knob
+                // depth 2: the direct kernel writes its device table and a side-stream
+                // copy delivers it, so the next push's kernel starts behind this one
+                // instead of behind its mapped stores' PCIe flush
+                side_copy = direct_frames && emit_depth_ > 1 && frames_dev_alt_ && c_.emit_frames && sink && !stop &&
+                            !no_side;
                 accum_in_direct_ = direct_frames;
-                direct_host_out_ = direct_frames && !no_zc;
+                direct_host_out_ = direct_frames && !no_zc && !side_copy;
                 const Status cs = compute_frames(k0s, chans, c_.mode == CYC_MODE_RECURSIVE);
                 accum_in_direct_ = false;
-                const bool copied = direct_host_out_;
+                const bool copied = direct_host_out_ || side_copy;
                 direct_host_out_ = false;
                 TRY(cs);
                 tables = frames_host_;
+                if (side_copy) {
+                    TRY(side_copy_setup());
+                    CK(cudaEventRecord(d2h_ready_, cs_));
+                    CK(cudaStreamWaitEvent(ds_, d2h_ready_, 0));
+                    CK(cudaMemcpyAsync(frames_host_, frames_dev_, slots * per * sizeof(double2),
+                                       cudaMemcpyDeviceToHost, ds_));
+                    CK(cudaEventRecord(d2h_done_[0], ds_));
+                    d2h_busy_[0] = true;
+                }
                 if (c_.mode == CYC_MODE_RECURSIVE) {
                     launch_recursive_update(frames_dev_, (int64_t)(fe - fb), C, (int64_t)per, rec_R_,
                                             std::pow(c_.lambda, (double)N_), coh_, mag_, cs_);
@@ -2046,7 +2105,7 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
                 // call delivers them (drain_pending)
                 PendingEmit pe;
                 pe.ev = get_event();
-                CK(cudaEventRecord(pe.ev, cs_));
+                CK(cudaEventRecord(pe.ev, side_copy ? ds_ : cs_));
                 pe.slots = slots;
                 pe.fidx = std::move(fidx);
                 pe.chans = std::move(chans);
@@ -2090,6 +2149,7 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
         }
         // unnormalised block sums into scratch frames_dev_, then accumulate
         TRY(ensure_frames(C));
+        TRY(wait_side_copies(false));
         TRY(direct(segs, 1.0, frames_dev_));
         launch_add_f64((double*)dsum_main_, (const double*)frames_dev_, (int64_t)C * nflags_ * layout_len_ * 2, cs_);
         launches_ += 1;

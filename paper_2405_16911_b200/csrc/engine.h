@@ -344,6 +344,16 @@ private:
     std::deque<PendingEmit> pendq_;
     int emit_depth_ = 0;                 // cyc_set_emit_pipeline
     double2* frames_host_alt_ = nullptr; // depth 2: the batches alternate between two pinned tables
+    // depth 2, direct per-frame tables: the kernel writes a device table and a
+    // copy on the side stream brings it to the host while the next push's
+    // kernel runs (mapped stores would keep the kernel alive for a PCIe flush)
+    double2* frames_dev_alt_ = nullptr;  // swapped with frames_dev_ beside the pinned tables
+    cudaStream_t ds_ = nullptr;          // D2H side stream
+    cudaEvent_t d2h_ready_ = nullptr;    // the tables are written (compute stream)
+    cudaEvent_t d2h_done_[2] = {nullptr, nullptr};  // [0]: last side copy out of frames_dev_, [1]: of frames_dev_alt_
+    bool d2h_busy_[2] = {false, false};
+    Status side_copy_setup();
+    Status wait_side_copies(bool both);  // compute stream waits before frames_dev_ (or either table) is rewritten
     Status drain_pending(cyc_frame_sink sink, void* user, size_t keep);
     Status stash_pending();
     double2* coh_ = nullptr;          // running coherent sums [channels][nflags][layout]
