@@ -117,3 +117,35 @@ def test_c1_geometry_depth_two(cyc):
     assert tail >= 2  # frames were still in flight at the end (both flags of at least one batch)
     assert np.array_equal(e0.average(cyc.AverageMode.Coherent, cyc.Flags.CONV),
                           e2.average(cyc.AverageMode.Coherent, cyc.Flags.CONV))
+
+
+def test_direct_side_copy_growth_and_depth_switch(cyc):
+    # depth-2 direct frames leave through a side-stream copy of alternating device tables:
+    # growing batches reallocate those tables with copies in flight, depth switches move
+    # between the side copy and the mapped stores, and a reset drops what is in flight
+    x = rand_c(60 * 256, 41)
+    alphas = [0.1234507, -0.3141, 1 / 7]
+    cfg = cyc.EstimatorConfig(mode=cyc.Mode.Set, win_len=256, alphas=alphas, lag_spec=cyc.LagSpec.Symmetric(5),
+                              flags=cyc.Flags.BOTH)
+    sync = run_stream(cyc, cfg, x, 256, 0)[0]
+    est = cyc.CyclicCorrelator(cfg)
+    est.set_emit_pipeline(2)
+    est.push(x[:700])
+    est.reset()  # frames in flight belong to the old stream
+    frames, o = [], 0
+    sizes = [256, 256, 256, 512, 256, 1024, 256, 256, 2048, 300, 212, 256, 256]
+    for i, n in enumerate(sizes * 2):
+        if o + n > len(x):
+            break
+        if i == 5:
+            est.set_emit_pipeline(1)
+        if i == 8:
+            est.set_emit_pipeline(2)
+        if i == 14:
+            est.set_emit_pipeline(0)
+        if i == 16:
+            est.set_emit_pipeline(2)
+        frames += est.push(x[o:o + n])
+        o += n
+    frames += est.flush_frames()
+    same_frames(frames, [f for f in sync if f.start_abs + 256 + 5 <= o])
