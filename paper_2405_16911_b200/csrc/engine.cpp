@@ -621,6 +621,8 @@ Engine::~Engine() {
     if (xs_) cudaStreamSynchronize(xs_);
     for (auto& g : graphs_) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.exec_alt) cudaGraphExecDestroy(g.exec_alt);
+        cudaFreeHost(g.tables_host_alt);
         cudaFreeHost(g.meta_host);
         cudaFree(g.meta_dev);
         cudaFree(g.S);
@@ -1679,6 +1681,14 @@ bool Engine::small_fold_ok(size_t slots) const {
     return !off && use_fold_ && !frames_direct_ && maxper <= 512 && work <= (double)(1 << 23);
 }
 
+// Small recursive/per-frame graphs keep two instances with their own pinned
+// tables (run_frame_graph): two replays may be in flight at depth 2.
+bool Engine::graph_two_deep(size_t slots) const {
+    static const bool zc_out = std::getenv("CYC_ZERO_COPY_OUT") != nullptr;
+    static const bool off = std::getenv("CYC_GRAPH_DEPTH1") != nullptr;  // A/B knob
+    return !off && !zc_out && graph_eligible(slots) && small_fold_ok(slots);
+}
+
 bool Engine::graph_eligible(size_t slots) const {
     static const bool off = std::getenv("CYC_NO_GRAPH") != nullptr;
     return !off && use_fold_ && !frames_direct_ && slots <= 16 && (N_ + Pf_ - 1) / Pf_ + 1 <= 4096;
@@ -1837,6 +1847,23 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
             cudaMemcpyAsync(n.tables_host, n.tables_dev, slots * per * sizeof(double2), cudaMemcpyDeviceToHost, cs_);
         CK(cudaStreamEndCapture(cs_, &graph));
         CK(cudaGraphInstantiate(&n.exec, graph, 0));
+        if (n.small && !n.zero_copy) {
+            // the same graph with its one copy node (the tables' D2H) retargeted
+            size_t nn = 0;
+            CK(cudaGraphGetNodes(graph, nullptr, &nn));
+            std::vector<cudaGraphNode_t> nodes(nn);
+            CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType ty;
+                CK(cudaGraphNodeGetType(nd, &ty));
+                if (ty != cudaGraphNodeTypeMemcpy) continue;
+                CK(cudaMallocHost(&n.tables_host_alt, slots * per * sizeof(double2)));
+                CK(cudaGraphMemcpyNodeSetParams1D(nd, n.tables_host_alt, n.tables_dev, slots * per * sizeof(double2),
+                                                  cudaMemcpyDeviceToHost));
+                CK(cudaGraphInstantiate(&n.exec_alt, graph, 0));
+                break;
+            }
+        }
         cudaGraphDestroy(graph);
         graphs_.push_back(n);
         g = &graphs_.back();
@@ -1878,7 +1905,10 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         }
         cudaEventRecord(gev_[0], cs_);
     }
-    CK(cudaGraphLaunch(g->exec, cs_));
+    // depth 2: consecutive replays alternate between the two instances (pinned tables)
+    const bool alt = emit_depth_ > 1 && g->exec_alt && !g->flip;
+    g->flip = alt;
+    CK(cudaGraphLaunch(alt ? g->exec_alt : g->exec, cs_));
     if (prof) {
         cudaEventRecord(gev_[1], cs_);
         cudaEventSynchronize(gev_[1]);
@@ -1888,7 +1918,7 @@ Status Engine::run_frame_graph(const std::vector<int64_t>& k0s, const std::vecto
         hprof_us_[7] += 1;
     }
     launches_ += (g->small ? 3 : 4) - (g->fused_rec ? 1 : 0);
-    *tables = g->tables_host;
+    *tables = alt ? g->tables_host_alt : g->tables_host;
     return Status::ok();
 }
 
@@ -2029,7 +2059,7 @@ Status Engine::emit_new_frames(cyc_frame_sink sink, void* user, double* S_target
             // batches in flight own the pinned tables: a graph replay rewrites its
             // own, the other paths alternate between two at depth 2
             if (!pendq_.empty() || emit_depth_ > 1) {
-                const size_t depth = graph_eligible(slots) ? 1 : (size_t)std::max(emit_depth_, 1);
+                const size_t depth = graph_eligible(slots) && !graph_two_deep(slots) ? 1 : (size_t)std::max(emit_depth_, 1);
                 TRY(drain_pending(sink, user, depth - 1));
                 if (depth > 1 && frames_host_alt_) {
                     std::swap(frames_host_, frames_host_alt_);

@@ -266,8 +266,14 @@ private:
         float* partials = nullptr;
         double2* tables_dev = nullptr;
         double2* tables_host = nullptr;  // pinned
+        // small graphs: a second instance whose D2H node lands in its own pinned
+        // table, so two replays can be in flight under pipelined emission
+        cudaGraphExec_t exec_alt = nullptr;
+        double2* tables_host_alt = nullptr;
+        bool flip = false;  // the last replay used exec_alt
     };
     std::vector<FrameGraph> graphs_;
+    bool graph_two_deep(size_t slots) const;
     void hprof(int phase);
     double hprof_us_[8] = {};
     double hprof_t_ = 0.0;
