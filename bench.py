@@ -633,7 +633,7 @@ def run_small(args, ws, rank, local):
                        "value_path": "tools/stream_bench (C++): cyc_push of "
                                      f"{s['chunk']}-sample chunks from pinned host memory, frames to a sink",
                        "emission": "pipelined (cyc_set_emit_pipeline depth 2: up to two frame batches in flight "
-                                   "(graph-replayed batches: one), delivered by a later push; same frames bit for bit, tests/test_gpu_pipeline.py); "
+                                   "(graph-replayed batches: two instances with their own pinned tables for the small fold graphs, else one), delivered by a later push; same frames bit for bit, tests/test_gpu_pipeline.py); "
                                    "CYC_EMIT_PIPELINE=0 times the reference's synchronous push()"},
             "msamples_per_s": s["samples"] * ws / (ms * 1e-3) / 1e6,
             "e2e": {"value": ups / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,

@@ -258,7 +258,7 @@ int cyc_set_lag_slice(cyc_est* est, uint32_t lag_begin, uint32_t lag_end);
  * depth 0 (default): a push delivers the frames it completes before it returns
  * (CyclicCorrelator::push, estimator.cpp:59-82).  depth 1 or 2: the push that
  * completes a frame batch only enqueues its GPU work, and up to `depth` batches
- * stay in flight (CUDA-graph replayed batches: one); their frames go, oldest
+ * stay in flight (CUDA-graph replayed batches: two for the small one-launch fold graphs, else one); their frames go, oldest
  * first, to the sink of the first later cyc_push that finds them finished (at
  * the latest the push that would exceed the depth) or to cyc_flush_frames, so
  * the GPU round trip of an emission overlaps the caller's next chunks.  Frame
