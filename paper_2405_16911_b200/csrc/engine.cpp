@@ -20,7 +20,6 @@ namespace {
 constexpr int64_t PMAX = 1 << 16;          // largest rational alpha grid folded
 constexpr size_t MAX_TILES = 2048;          // fold tiles per launch (partials: 128 KiB each)
 constexpr size_t FRAME_SLOT_BUDGET = 256ull << 20;  // bytes of per-frame scratch per batch
-constexpr int SMS = 148;
 
 int64_t floor_div(int64_t a, int64_t b) {
     int64_t q = a / b;
@@ -528,6 +527,9 @@ Status Engine::init(const Cfg& cfg) {
         int major = 0;
         CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c_.device));
         tc_capable_ = major == 10;  // tcgen05 (the library is built for sm_100a only)
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c_.device));
+        if (sms > 0) sms_ = sms;  // tile splits and grid sizes follow the device
     }
     // Blocking streams: they synchronize implicitly with the legacy default
     // stream (torch's default stream), so device buffers are read after the
@@ -1094,8 +1096,8 @@ Status Engine::fold_tc_batch(const std::vector<FoldSeg>& tsegs, std::vector<TcGr
         int64_t lwork = 0;
         for (size_t g = g0; g < g0 + ng; ++g) lwork += groups[g].p1 - groups[g].p0;
         // extra tiles (beyond the minimum) fill whole waves of 1 CTA/SM
-        const int64_t waves = std::max<int64_t>(1, ceil_div(base_tiles, SMS));
-        const int64_t extra = std::max<int64_t>(0, std::min<int64_t>(waves * SMS, FI_TILES) - base_tiles);
+        const int64_t waves = std::max<int64_t>(1, ceil_div(base_tiles, sms_));
+        const int64_t extra = std::max<int64_t>(0, std::min<int64_t>(waves * sms_, FI_TILES) - base_tiles);
         int nt = 0;
         double launch_flops = 0.0;
         for (size_t g = g0; g < g0 + ng; ++g) {
@@ -1239,7 +1241,7 @@ Status Engine::fold_tc_planes(const std::vector<FoldSeg>& tsegs, std::vector<TcG
         splits = (int)std::max<int64_t>(splits, ceil_div(gr.p1 - gr.p0, MAXP));
         min_np = std::min<int64_t>(min_np, gr.p1 - gr.p0);
     }
-    splits = (int)std::max<int64_t>(splits, std::min<int64_t>(ceil_div(SMS, ng), std::max<int64_t>(1, min_np / 16)));
+    splits = (int)std::max<int64_t>(splits, std::min<int64_t>(ceil_div(sms_, ng), std::max<int64_t>(1, min_np / 16)));
     std::vector<FoldTile> tiles;
     std::vector<FoldGroup> fg(groups.size());
     for (int i = 0; i < splits; ++i)
@@ -1327,8 +1329,8 @@ Status Engine::fold_tc_planes2(const std::vector<FoldSeg>& tsegs, std::vector<Tc
         splits = (int)std::max<int64_t>(splits, ceil_div(gr.p1 - gr.p0, MAXP));
         min_np = std::min<int64_t>(min_np, gr.p1 - gr.p0);
     }
-    // pairs of SMs: SMS / 2 tiles per wave
-    splits = (int)std::max<int64_t>(splits, std::min<int64_t>(ceil_div(SMS / 2, ng), std::max<int64_t>(1, min_np / 16)));
+    // pairs of SMs: sms_ / 2 tiles per wave
+    splits = (int)std::max<int64_t>(splits, std::min<int64_t>(ceil_div(sms_ / 2, ng), std::max<int64_t>(1, min_np / 16)));
     std::vector<FoldTile> tiles;
     std::vector<FoldGroup> fg(groups.size());
     for (int i = 0; i < splits; ++i)
@@ -1422,7 +1424,7 @@ Status Engine::fold(const std::vector<FoldSeg>& segs_in, double* S, bool overwri
     };
     // split long groups into whole waves of 1 CTA/SM: each group gets a share of
     // `target` tiles proportional to its periods (floor), so no partial wave
-    const int64_t target = std::max<int64_t>(SMS, (int64_t)groups.size());
+    const int64_t target = std::max<int64_t>(sms_, (int64_t)groups.size());
     size_t g0 = 0;
     while (g0 < groups.size()) {
         std::vector<FoldTile> tiles;
@@ -1552,9 +1554,9 @@ Status Engine::direct(const std::vector<DirectSeg>& segs, double scale, double2*
     int splits = (int)std::min<int64_t>(256, std::max<int64_t>(1, maxcnt / (8192 / sl)));
     // small calls (C1: one 4096-sample frame x 10 alphas): at least ~two CTAs per
     // SM, down to 256 samples per split -- the launch is latency-bound
-    const int64_t want = (2 * SMS + (int64_t)segs.size() * A_ - 1) / ((int64_t)segs.size() * A_);
+    const int64_t want = (2 * sms_ + (int64_t)segs.size() * A_ - 1) / ((int64_t)segs.size() * A_);
     splits = (int)std::max<int64_t>(splits, std::min<int64_t>(want, maxcnt / 256));
-    while (splits > 1 && (int64_t)segs.size() * A_ * splits > 64 * SMS) splits /= 2;
+    while (splits > 1 && (int64_t)segs.size() * A_ * splits > 64 * sms_) splits /= 2;
     static const int split_knob = [] {  // CYC_DIRECT_SPLITS=<n>: tuning knob (diagnostics)
         const char* e = std::getenv("CYC_DIRECT_SPLITS");
         return e ? std::atoi(e) : 0;

@@ -348,6 +348,7 @@ private:
         std::vector<double2> stash;
     };
     std::deque<PendingEmit> pendq_;
+    int sms_ = 148;                      // SM count of c_.device (B200: 148)
     int emit_depth_ = 0;                 // cyc_set_emit_pipeline
     double2* frames_host_alt_ = nullptr; // depth 2: the batches alternate between two pinned tables
     // depth 2, direct per-frame tables: the kernel writes a device table and a
